@@ -1,0 +1,24 @@
+# Builds the sm_100a kernel library behind the C ABI (include/dicm_b200.h).
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH ?= -gencode arch=compute_100a,code=sm_100a
+NVFLAGS ?= -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+SRC_DIR := paper_1711_06505_b200/csrc
+OBJ_DIR := build/obj
+SRCS := $(wildcard $(SRC_DIR)/*.cu)
+OBJS := $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(SRCS))
+HDRS := $(wildcard $(SRC_DIR)/*.cuh) include/dicm_b200.h
+LIB := paper_1711_06505_b200/libdicm_b200.so
+
+all: $(LIB)
+
+$(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p $(OBJ_DIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJ_DIR)/$*.ptxas.log || (cat $(OBJ_DIR)/$*.ptxas.log; false)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS)
+
+clean:
+	rm -rf build $(LIB)
+
+.PHONY: all clean

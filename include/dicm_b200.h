@@ -1,0 +1,274 @@
+/*
+ * dicm_b200.h -- C ABI of the B200 (sm_100a) DICM / AMS training hot path.
+ *
+ * The reference (arxiv 1711.06505 re-implementation, package `dicm`) is pure
+ * Python/numpy and has no FFI; its "operator API" is the Python call chain
+ * LocalTrainer.train_batch -> encode_batch -> logits_graph -> backward -> Adam
+ * (reference training.py:66-91).  Each entry point below replaces one link of
+ * that chain and cites the reference code it stands in for.  The Python host
+ * package (paper_1711_06505_b200) binds these with ctypes; INTEGRATION.md
+ * shows the binding a maintainer of the reference would add.
+ *
+ * Conventions
+ *  - every pointer is caller-owned DEVICE memory unless noted; sizes are
+ *    explicit; nothing is allocated inside a call;
+ *  - calls are asynchronous on `stream` (a cudaStream_t) and thread-safe across
+ *    distinct streams;
+ *  - data-dependent counts (unique keys, unique rows) stay on the device
+ *    (`*_dev` int32 pointers) so a whole step runs without host round trips;
+ *  - the return value is a status code; dicm_last_error() describes the last
+ *    failure of the calling thread;
+ *  - device-side faults (out-of-vocabulary ids, non-finite loss/gradients) are
+ *    latched into the caller's int32 `status[DICM_STATUS_WORDS]` buffer and
+ *    surface when the host reads it (the reference raises KeyError at
+ *    model.py:127-129 / images.py:89-94 and FloatingPointError at
+ *    training.py:75-76 / optim.py:53-54).
+ */
+#ifndef DICM_B200_H
+#define DICM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* dicm_stream_t; /* cudaStream_t */
+
+/* status codes (python side maps them to the reference's exception types) */
+#define DICM_OK 0
+#define DICM_ERR_CUDA 1        /* RuntimeError */
+#define DICM_ERR_SHAPE 2       /* ShapeError (ValueError), autograd.py:18-19 */
+#define DICM_ERR_KEY 3         /* KeyError, model.py:127-129 */
+#define DICM_ERR_VALUE 4       /* ValueError */
+#define DICM_ERR_FLOAT 5       /* FloatingPointError, optim.py:53-54 */
+#define DICM_ERR_UNSUPPORTED 6 /* NotImplementedError */
+
+/* device status words */
+#define DICM_STATUS_WORDS 8
+#define DICM_ST_KEY_FLAG 0     /* != 0: an id was outside its vocabulary */
+#define DICM_ST_KEY_VALUE 1    /* the offending id */
+#define DICM_ST_KEY_SEG 2      /* which key segment it came from */
+#define DICM_ST_NONFINITE 3    /* bit 1: loss, bit 2: dense grad, bit 4: row grad */
+
+/* pool element types */
+#define DICM_POOL_F32 0
+#define DICM_POOL_BF16 1
+
+/* image-MLP layer-0 arithmetic */
+#define DICM_PREC_FP32 0   /* CUDA-core fp32 (strict parity mode) */
+#define DICM_PREC_TF32 1   /* tcgen05 kind::tf32 on an fp32 pool */
+#define DICM_PREC_BF16 2   /* tcgen05 kind::f16 (bf16) on a bf16 pool */
+
+const char* dicm_last_error(void);
+int dicm_version(void);
+/* returns the device's SM major*10+minor, or <0 if no usable device */
+int dicm_device_arch(void);
+
+/* ------------------------------------------------------------------------
+ * a2: per-batch key dedup with inverse index.
+ * Replaces np.unique(np.concatenate(needed)) (reference model.py:187),
+ * np.searchsorted(unique, ids) (model.py:374, 378) and Batch.unique_field_ids
+ * (model.py:152-155).  Keys of several segments share one key space: segment
+ * s maps id -> base_s + id, ids must lie in [0, vocab_s) (else status KEY).
+ * Output: sorted distinct global keys uniq[0..*count_dev) and, for every input
+ * id, inv[inv_off_s + j] = position of its key in uniq.  Bit-exact with numpy.
+ * An id outside its vocabulary latches status[KEY_FLAG], the id and
+ * KEY_SEG = tag * 16 + s; its inverse entry is set to 0 (a safe index) and
+ * every later update kernel of the step refuses to run.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  const int32_t* ids;
+  int64_t n;
+  int64_t base;
+  int64_t vocab;
+  int64_t inv_off;
+} dicm_keyseg_t;
+
+size_t dicm_dedup_workspace(int64_t key_space);
+int dicm_dedup(const dicm_keyseg_t* segs, int nseg, int64_t key_space, void* workspace,
+               size_t workspace_bytes, int32_t* uniq_out, int32_t* inv_out, int32_t* count_dev,
+               int32_t tag, int32_t* status, dicm_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * a3: the image pool -- 4096-d feature rows resident in HBM.
+ * materialize: rows[p] = round(tanh(latent[p] . proj^T)) computed in fp64, the
+ *   frozen extractor of reference images.py:48-71 (FixedExtractor.extract).
+ * gather: out[i] = rows[row_ids[i]] as fp32 for i < *count_dev (bit-exact);
+ *   reference images.py:96-101 (ImageFeatureStore.raw_features).
+ * ---------------------------------------------------------------------- */
+int dicm_pool_materialize(const float* latents, const double* proj, int64_t rows, int d_raw,
+                          int latent_dim, void* pool, int pool_dtype, dicm_stream_t stream);
+int dicm_pool_gather(const void* pool, int pool_dtype, int d_raw, const int32_t* row_ids,
+                     const int32_t* count_dev, int64_t n_max, float* out, dicm_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * a4/a5: the image MLP d_raw -> 256 -> 64 -> 12 (reference model.py:108-120,
+ * image_net_apply) and its reverse path (autograd.py:201-204, 222-225;
+ * distributed: ServerNode.local_model_gradient runtime.py:169-201).
+ * Rows are pool rows rows[0..*count_dev); weights are [out, in] row-major.
+ * fwd writes the pre-activations act0 [n,256], act1 [n,64] and the
+ * embeddings emb [n,12].  bwd consumes demb [n,12] and writes the gradients
+ * of all img/ parameters (overwriting).  The input gradient of layer 0 is not
+ * formed (the features are frozen; the reference computes and drops it).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  const float *w0, *b0, *a0, *w1, *b1, *a1, *w2, *b2;
+} dicm_imgmlp_params_t;
+typedef struct {
+  float *w0, *b0, *a0, *w1, *b1, *a1, *w2, *b2;
+} dicm_imgmlp_grads_t;
+
+size_t dicm_imgmlp_workspace(int64_t rows_max, int d_raw, int precision);
+int dicm_imgmlp_fwd(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
+                    const int32_t* count_dev, int64_t rows_max, const dicm_imgmlp_params_t* p,
+                    float* act0, float* act1, float* emb, int precision, void* workspace,
+                    size_t workspace_bytes, dicm_stream_t stream);
+int dicm_imgmlp_bwd(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
+                    const int32_t* count_dev, int64_t rows_max, const dicm_imgmlp_params_t* p,
+                    const float* act0, const float* act1, const float* demb,
+                    const dicm_imgmlp_grads_t* g, int precision, void* workspace,
+                    size_t workspace_bytes, dicm_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * a6-a10: per-sample gather / pooling, forward and backward, fused.
+ * Forward (reference model.py:358-396): writes every part of the head input
+ *   x = hstack(field vectors, ad-image embedding, pooled behaviors):
+ *   one-hot field rows (rows(table, ids), autograd.py:262-272), multi-hot
+ *   sums (segment_sum, autograd.py:275-287), the ad-image embedding
+ *   (rows(E, inverse), model.py:373-376) and the aggregator: sum pooling
+ *   (model.py:219-220) or attentive pooling with the ad-image query
+ *   (model.py:206-215, 225-226) and the complementary ID query
+ *   (multi-query, model.py:227-229, 381-383).
+ * Backward: the same graph reversed (segment_softmax bwd autograd.py:334-337,
+ *   col_scale bwd 348-350); embedding and ID-row gradients are scatter-added
+ *   into the deduplicated row buffers (np.add.at, autograd.py:267-271);
+ *   attention-parameter gradients are written as per-block partial sums.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int32_t kind;                 /* 0 sum, 1 attn, 2 multiquery-attn */
+  int32_t normalize;            /* softmax over scores (model.py:211-214) */
+  int32_t use_ad_image;
+  int32_t use_behavior_images;
+  int32_t n_fields;
+  int32_t field_multi[8];
+  int32_t field_col[8];         /* column of each field vector in the head input */
+  int32_t ad_col;               /* column of the ad-image embedding (or -1) */
+  int32_t pool_col;             /* column of the aggregator output (or -1) */
+  int32_t width;                /* head input width */
+  int32_t n_query;              /* multiquery: number of ID query fields (1 or 2) */
+  int32_t query_col[2];         /* their columns in the head input */
+  int32_t query_field[2];       /* their field indices */
+} dicm_layout_t;
+
+typedef struct {
+  int32_t batch;
+  int64_t refs;                 /* R = behavior rows */
+  const int32_t* field_ids[8];  /* one-hot: [B]; multi-hot: flat [R_f] */
+  const int32_t* field_off[8];  /* multi-hot CSR offsets [B+1]; NULL for one-hot */
+  const float* tables[8];       /* id_emb/<field> [V_f, 12] */
+  const int32_t* field_inv[8];  /* per reference: row in the deduplicated ID-row list */
+  const int32_t* ad_local;      /* [B] inverse of the ad images into emb */
+  const int32_t* beh_local;     /* [R] inverse of the behavior images into emb */
+  const int32_t* beh_off;       /* [B+1] */
+  const float* emb;             /* [U,12] image embeddings */
+} dicm_batch_view_t;
+
+typedef struct {
+  const float *w0, *b0, *a0, *w1, *b1; /* attn/<ch>/0/{w,b,a}, attn/<ch>/1/{w,b} */
+} dicm_attn_params_t;
+
+/* number of float partial slots one block writes (attention grads, both channels) */
+int64_t dicm_attn_partial_size(const dicm_layout_t* layout);
+int dicm_sample_blocks(int batch);
+int dicm_sample_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv,
+                    const dicm_attn_params_t* attn /* [2]: img, id */, float* head_in,
+                    float* scores /* [2, R] */, float* stats /* [2, B, 2] */,
+                    dicm_stream_t stream);
+int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv,
+                    const dicm_attn_params_t* attn, const float* head_in, const float* d_head_in,
+                    const float* scores, const float* stats, float* d_emb /* [U,12], zeroed */,
+                    float* d_rows /* [K,12], zeroed */, float* attn_partials,
+                    dicm_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * a11-a12: head MLP width -> 128 -> 64 -> 1 and BCE (reference model.py:397-401,
+ * autograd.py:230-246, training.py:39-42), forward and backward fused per
+ * sample tile.  d_head_in = dLoss/dx; weight gradients of the mlp/ group are
+ * written as per-block partials in sorted-name layout (mlp/0/a, mlp/0/b,
+ * mlp/0/w, mlp/1/a, mlp/1/b, mlp/1/w, mlp/2/b, mlp/2/w).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  const float *w0, *b0, *a0, *w1, *b1, *a1, *w2, *b2;
+} dicm_head_params_t;
+
+int64_t dicm_head_partial_size(int width);
+int dicm_head_blocks(int batch);
+int dicm_head_fwd_bwd(const float* head_in, int batch, int width, const float* labels,
+                      float inv_denominator, const dicm_head_params_t* p, float* logits,
+                      float* d_head_in, float* partials, float* loss_partials,
+                      dicm_stream_t stream);
+
+/* partials [nblk, n] -> out[n] (deterministic, fixed order; += if accumulate) */
+int dicm_reduce_partials(const float* partials, int nblk, int64_t n, float* out, int accumulate,
+                         dicm_stream_t stream);
+/* loss = sum(loss_partials) * scale; latches a non-finite loss into status */
+int dicm_loss_finalize(const float* loss_partials, int nblk, float scale, float* loss_out,
+                       int32_t* status, dicm_stream_t stream);
+/* latches non-finite values of x[0..n) into status[DICM_ST_NONFINITE] |= bit */
+int dicm_check_finite(const float* x, int64_t n, const int32_t* count_dev, int row_width,
+                      int bit, int32_t* status, dicm_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * a14: optimizer (reference optim.py).
+ * dense: bias-corrected Adam per parameter span (optim.py:44-63); an all-zero
+ *   gradient leaves the span and its state untouched, each span keeps its own
+ *   step count t[span]; nothing moves if status flags a non-finite value.
+ * rows: per-row Adam on the deduplicated rows (optim.py:83-104); keys are
+ *   global keys of dicm_dedup over tables laid out at `base`.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int64_t offset;
+  int64_t size;
+} dicm_span_t;
+
+size_t dicm_adam_dense_workspace(int nspans);
+int dicm_adam_dense(float* param, const float* grad, float* m, float* v, int32_t* t,
+                    const dicm_span_t* spans, int nspans, float lr, float beta1, float beta2,
+                    float eps, void* workspace, size_t workspace_bytes, int32_t* status,
+                    dicm_stream_t stream);
+
+typedef struct {
+  float* table;
+  float* m;
+  float* v;
+  int32_t* t;
+  int64_t base;
+  int64_t vocab;
+} dicm_table_state_t;
+
+int dicm_adam_rows(const dicm_table_state_t* tabs, int ntab, const int32_t* uniq_keys,
+                   const int32_t* count_dev, int64_t max_rows, const float* grads, float lr,
+                   float beta1, float beta2, float eps, int32_t* status, dicm_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * a16: AMS exchange helpers for the multi-GPU step (reference
+ * Cluster.run_iteration runtime.py:370-470, shard_of runtime.py:60-68).
+ * Keys are owned by rank = key % world; the owner's local row is key / world.
+ * bucket: stable partition of sorted keys[0..*count_dev) by owner ->
+ *   send_keys (owner-local ids), send_counts[world], perm[i] = slot of key i.
+ * permute rows: out[perm[i]] = in[i] (scatter) or out[i] = in[perm[i]] (gather)
+ *   for 12-float rows.
+ * ---------------------------------------------------------------------- */
+int dicm_bucket_by_owner(const int32_t* keys, const int32_t* count_dev, int64_t n_max, int world,
+                         int32_t* send_keys, int32_t* send_counts, int32_t* perm,
+                         void* workspace, size_t workspace_bytes, dicm_stream_t stream);
+size_t dicm_bucket_workspace(int64_t n_max, int world);
+int dicm_permute_rows12(const float* in, const int32_t* perm, const int32_t* count_dev,
+                        int64_t n_max, int scatter, float* out, dicm_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DICM_B200_H */

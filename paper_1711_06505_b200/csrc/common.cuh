@@ -1,0 +1,84 @@
+// Shared definitions for the DICM B200 kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/dicm_b200.h"
+
+// The paper's configuration is compiled in: 12-d ID and image embeddings
+// (reference model.py:51-52 at the benchmark settings), a 32-unit attention
+// net (model.py:73) and the 128/64 head (model.py:275).
+#define DICM_D 12
+#define DICM_ATT 32
+#define DICM_HEAD0 128
+#define DICM_HEAD1 64
+#define DICM_MAX_SEGS 8
+#define DICM_MAX_FIELDS 8
+
+namespace dicm {
+
+// ---- host-side error plumbing (capi.cu) ---------------------------------
+int fail(int code, const char* fmt, ...);
+int check_cuda(cudaError_t e, const char* where);
+int last_launch(const char* where);
+
+// ---- device helpers -------------------------------------------------------
+__device__ __forceinline__ float prelu(float x, float a) { return x > 0.f ? x : a * x; }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// 12-float embedding row <-> 3 x float4 (rows are 48 B, 16 B aligned)
+struct Row12 {
+  float v[DICM_D];
+};
+
+__device__ __forceinline__ Row12 load_row12(const float* __restrict__ p) {
+  Row12 r;
+  const float4* q = reinterpret_cast<const float4*>(p);
+  float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+  r.v[0] = a.x; r.v[1] = a.y; r.v[2] = a.z; r.v[3] = a.w;
+  r.v[4] = b.x; r.v[5] = b.y; r.v[6] = b.z; r.v[7] = b.w;
+  r.v[8] = c.x; r.v[9] = c.y; r.v[10] = c.z; r.v[11] = c.w;
+  return r;
+}
+
+// rows of tensors updated inside the same step must bypass the read-only path
+__device__ __forceinline__ Row12 load_row12_cg(const float* p) {
+  Row12 r;
+  const float4* q = reinterpret_cast<const float4*>(p);
+  float4 a = __ldcg(q), b = __ldcg(q + 1), c = __ldcg(q + 2);
+  r.v[0] = a.x; r.v[1] = a.y; r.v[2] = a.z; r.v[3] = a.w;
+  r.v[4] = b.x; r.v[5] = b.y; r.v[6] = b.z; r.v[7] = b.w;
+  r.v[8] = c.x; r.v[9] = c.y; r.v[10] = c.z; r.v[11] = c.w;
+  return r;
+}
+
+__device__ __forceinline__ void atomic_add_row12(float* p, const float* v) {
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) atomicAdd(p + c, v[c]);
+}
+
+__device__ __forceinline__ int num_sms() {
+  return 148;
+}
+
+}  // namespace dicm
+
+// launch helpers ------------------------------------------------------------
+static inline int dicm_grid(int64_t n, int tpb, int cap = 148 * 16) {
+  int64_t g = (n + tpb - 1) / tpb;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}

@@ -1,0 +1,221 @@
+// a2: deduplication of keys with an inverse index, by dense-key-space bitmap.
+//
+// Reference semantics: unique = np.unique(keys) (model.py:187),
+// inverse = np.searchsorted(unique, keys) (model.py:374, 378).  Keys are
+// bounded ids (pool rows, vocabulary rows), so instead of sorting we mark a
+// bitmap over the key space, prefix-scan the popcounts of its words, and read
+// both results off the scan:
+//   unique[r]  = the r-th set bit (ascending by construction),
+//   inverse[i] = prefix(word(k)) + popc(word(k) & below(k)).
+// Work is O(refs + key_space/32) with coalesced passes and no sort; results
+// are bit-exact with numpy.
+#include "common.cuh"
+
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kWordsPerThread = 16;
+constexpr int kTile = kScanThreads * kWordsPerThread;  // 4096 words = 131072 keys
+
+struct Segs {
+  const int32_t* ids[DICM_MAX_SEGS];
+  int64_t base[DICM_MAX_SEGS];
+  int64_t vocab[DICM_MAX_SEGS];
+  int64_t inv_off[DICM_MAX_SEGS];
+  int64_t start[DICM_MAX_SEGS + 1];
+  int nseg;
+};
+
+__device__ __forceinline__ int find_seg(const Segs& s, int64_t i) {
+  int k = 0;
+  while (k + 1 < s.nseg && i >= s.start[k + 1]) ++k;
+  return k;
+}
+
+__global__ void k_mark(const __grid_constant__ Segs segs, uint32_t* __restrict__ bitmap, int tag,
+                       int32_t* __restrict__ status) {
+  const int64_t total = segs.start[segs.nseg];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int s = find_seg(segs, i);
+    const int64_t id = segs.ids[s][i - segs.start[s]];
+    if (id < 0 || id >= segs.vocab[s]) {
+      if (atomicCAS(&status[DICM_ST_KEY_FLAG], 0, 1) == 0) {
+        status[DICM_ST_KEY_VALUE] = (int32_t)id;
+        status[DICM_ST_KEY_SEG] = tag * 16 + s;
+      }
+      continue;
+    }
+    const uint32_t key = (uint32_t)(segs.base[s] + id);
+    const uint32_t bit = 1u << (key & 31);
+    uint32_t* w = bitmap + (key >> 5);
+    // test before set: hot keys (Zipf) would otherwise serialize on one word
+    if ((__ldcg(w) & bit) == 0) atomicOr(w, bit);
+  }
+}
+
+__device__ __forceinline__ int block_excl_scan(int v, int* total) {
+  __shared__ int warp_tot[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int t = lane < kScanThreads / 32 ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < kScanThreads / 32) warp_tot[lane] = t;
+  }
+  __syncthreads();
+  const int warp_off = wid ? warp_tot[wid - 1] : 0;
+  *total = warp_tot[kScanThreads / 32 - 1];
+  __syncthreads();
+  return warp_off + x - v;
+}
+
+// per-tile popcount sums (coalesced: consecutive threads read consecutive uint4)
+__global__ void k_tile_sums(const uint32_t* __restrict__ bitmap, int32_t* __restrict__ tile_sums) {
+  const uint4* p = reinterpret_cast<const uint4*>(bitmap + (int64_t)blockIdx.x * kTile);
+  int c = 0;
+#pragma unroll
+  for (int q = 0; q < kWordsPerThread / 4; ++q) {
+    uint4 v = __ldcg(p + q * kScanThreads + threadIdx.x);
+    c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+  }
+  int tot;
+  block_excl_scan(c, &tot);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+}
+
+// exclusive scan of the tile sums in one block; total -> count
+__global__ void k_scan_tiles(int32_t* __restrict__ tile_sums, int ntiles, int32_t* count) {
+  int carry = 0;
+  for (int base = 0; base < ntiles; base += kScanThreads) {
+    const int i = base + threadIdx.x;
+    const int v = i < ntiles ? tile_sums[i] : 0;
+    int tot;
+    const int ex = block_excl_scan(v, &tot);
+    if (i < ntiles) tile_sums[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *count = carry;
+}
+
+// word prefixes + emission of the unique keys
+__global__ void k_emit(const uint32_t* __restrict__ bitmap, const int32_t* __restrict__ tile_off,
+                       int32_t* __restrict__ word_prefix, int32_t* __restrict__ uniq) {
+  __shared__ uint32_t sw[kTile];
+  const int64_t tile_base = (int64_t)blockIdx.x * kTile;
+  const uint4* p = reinterpret_cast<const uint4*>(bitmap + tile_base);
+  uint4* s4 = reinterpret_cast<uint4*>(sw);
+#pragma unroll
+  for (int q = 0; q < kWordsPerThread / 4; ++q)
+    s4[q * kScanThreads + threadIdx.x] = __ldcg(p + q * kScanThreads + threadIdx.x);
+  __syncthreads();
+  const uint32_t* mine = sw + threadIdx.x * kWordsPerThread;
+  int c = 0;
+#pragma unroll
+  for (int q = 0; q < kWordsPerThread; ++q) c += __popc(mine[q]);
+  int tot;
+  int run = tile_off[blockIdx.x] + block_excl_scan(c, &tot);
+  // stage the word prefixes through shared memory for coalesced stores
+  __shared__ int32_t sp[kTile];
+#pragma unroll
+  for (int q = 0; q < kWordsPerThread; ++q) {
+    sp[threadIdx.x * kWordsPerThread + q] = run;
+    uint32_t bits = mine[q];
+    const uint32_t wkey = (uint32_t)((tile_base + threadIdx.x * kWordsPerThread + q) << 5);
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      uniq[run++] = (int32_t)(wkey + b);
+      bits &= bits - 1;
+    }
+  }
+  __syncthreads();
+  int4* dst = reinterpret_cast<int4*>(word_prefix + tile_base);
+  const int4* src = reinterpret_cast<const int4*>(sp);
+#pragma unroll
+  for (int q = 0; q < kWordsPerThread / 4; ++q)
+    dst[q * kScanThreads + threadIdx.x] = src[q * kScanThreads + threadIdx.x];
+}
+
+__global__ void k_inverse(const __grid_constant__ Segs segs, const uint32_t* __restrict__ bitmap,
+                          const int32_t* __restrict__ word_prefix, int32_t* __restrict__ inv) {
+  const int64_t total = segs.start[segs.nseg];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int s = find_seg(segs, i);
+    const int64_t j = i - segs.start[s];
+    const int64_t id = segs.ids[s][j];
+    int32_t r = 0;  // out-of-vocabulary: flagged by k_mark, index kept in bounds
+    if (id >= 0 && id < segs.vocab[s]) {
+      const uint32_t key = (uint32_t)(segs.base[s] + id);
+      const uint32_t w = key >> 5;
+      r = word_prefix[w] + __popc(__ldg(bitmap + w) & ((1u << (key & 31)) - 1u));
+    }
+    inv[segs.inv_off[s] + j] = r;
+  }
+}
+
+int64_t padded_words(int64_t key_space) {
+  const int64_t w = (key_space + 31) / 32;
+  return ((w + kTile - 1) / kTile) * kTile;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t dicm_dedup_workspace(int64_t key_space) {
+  const int64_t W = padded_words(key_space < 1 ? 1 : key_space);
+  return (size_t)(W * 4 * 2 + (W / kTile) * 4 + 256);
+}
+
+int dicm_dedup(const dicm_keyseg_t* segs, int nseg, int64_t key_space, void* workspace,
+               size_t workspace_bytes, int32_t* uniq_out, int32_t* inv_out, int32_t* count_dev,
+               int32_t tag, int32_t* status, dicm_stream_t stream) {
+  using namespace dicm;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (nseg < 1 || nseg > DICM_MAX_SEGS) return fail(DICM_ERR_VALUE, "dedup: nseg %d not in [1, %d]", nseg, DICM_MAX_SEGS);
+  if (key_space < 1 || key_space > (int64_t)1 << 31)
+    return fail(DICM_ERR_VALUE, "dedup: key space %lld outside [1, 2^31]", (long long)key_space);
+  if (workspace_bytes < dicm_dedup_workspace(key_space)) return fail(DICM_ERR_VALUE, "dedup: workspace too small");
+  Segs s{};
+  s.nseg = nseg;
+  s.start[0] = 0;
+  for (int i = 0; i < nseg; ++i) {
+    s.ids[i] = segs[i].ids;
+    s.base[i] = segs[i].base;
+    s.vocab[i] = segs[i].vocab;
+    s.inv_off[i] = segs[i].inv_off;
+    s.start[i + 1] = s.start[i] + segs[i].n;
+    if (segs[i].n < 0 || segs[i].base < 0 || segs[i].base + segs[i].vocab > key_space)
+      return fail(DICM_ERR_VALUE, "dedup: segment %d [%lld, +%lld) exceeds key space %lld", i,
+                  (long long)segs[i].base, (long long)segs[i].vocab, (long long)key_space);
+  }
+  const int64_t W = padded_words(key_space);
+  const int ntiles = (int)(W / kTile);
+  uint32_t* bitmap = (uint32_t*)workspace;
+  int32_t* word_prefix = (int32_t*)(bitmap + W);
+  int32_t* tile_sums = word_prefix + W;
+  int rc = check_cuda(cudaMemsetAsync(bitmap, 0, W * 4, st), "dedup memset");
+  if (rc) return rc;
+  const int64_t total = s.start[nseg];
+  if (total > 0) k_mark<<<dicm_grid(total, 256, 148 * 32), 256, 0, st>>>(s, bitmap, tag, status);
+  k_tile_sums<<<ntiles, kScanThreads, 0, st>>>(bitmap, tile_sums);
+  k_scan_tiles<<<1, kScanThreads, 0, st>>>(tile_sums, ntiles, count_dev);
+  k_emit<<<ntiles, kScanThreads, 0, st>>>(bitmap, tile_sums, word_prefix, uniq_out);
+  if (total > 0)
+    k_inverse<<<dicm_grid(total, 256, 148 * 32), 256, 0, st>>>(s, bitmap, word_prefix, inv_out);
+  return last_launch("dicm_dedup");
+}
+
+}  // extern "C"

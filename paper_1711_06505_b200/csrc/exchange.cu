@@ -1,0 +1,119 @@
+// a16: AMS exchange helpers (reference Cluster._embed_plan / _key_plan,
+// runtime.py:353-368, shard_of runtime.py:60-68).
+//
+// Keys are owned by rank = key % world and stored there at row key / world.
+// Requests go out sorted within each destination (the reference sorts ids
+// within a shard, runtime.py:353-358), so the stable partition below keeps
+// the ascending order of the (already sorted) unique keys per owner.
+#include "common.cuh"
+
+namespace {
+using namespace dicm;
+
+constexpr int BLK = 1024;  // keys per block
+constexpr int MAXW = 64;
+
+__global__ void k_block_counts(const int32_t* __restrict__ keys, const int32_t* __restrict__ count, int64_t n_max,
+                               int world, int32_t* __restrict__ blkcnt) {
+  __shared__ int c[MAXW];
+  if (threadIdx.x < world) c[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t n = min((int64_t)*count, n_max);
+  const int64_t i = (int64_t)blockIdx.x * BLK + threadIdx.x;
+  if (i < n) atomicAdd(&c[keys[i] % world], 1);
+  __syncthreads();
+  if (threadIdx.x < world) blkcnt[(int64_t)blockIdx.x * world + threadIdx.x] = c[threadIdx.x];
+}
+
+// owner-major exclusive scan over (owner, block); send_counts[o] = totals
+__global__ void k_scan_counts(int32_t* __restrict__ blkcnt, int nblk, int world, int32_t* __restrict__ send_counts) {
+  if (threadIdx.x != 0) return;
+  int run = 0;
+  for (int o = 0; o < world; ++o) {
+    int tot = 0;
+    for (int b = 0; b < nblk; ++b) {
+      const int v = blkcnt[(int64_t)b * world + o];
+      blkcnt[(int64_t)b * world + o] = run;
+      run += v;
+      tot += v;
+    }
+    send_counts[o] = tot;
+  }
+}
+
+__global__ void k_place(const int32_t* __restrict__ keys, const int32_t* __restrict__ count, int64_t n_max, int world,
+                        const int32_t* __restrict__ base, int32_t* __restrict__ send_keys, int32_t* __restrict__ perm) {
+  __shared__ int warp_cnt[BLK / 32][MAXW];
+  const int64_t n = min((int64_t)*count, n_max);
+  const int64_t i = (int64_t)blockIdx.x * BLK + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool valid = i < n;
+  const int32_t key = valid ? keys[i] : 0;
+  const int own = valid ? key % world : -1;
+  int rank = 0;
+  for (int o = 0; o < world; ++o) {
+    const unsigned mask = __ballot_sync(0xffffffffu, own == o);
+    if (own == o) rank = __popc(mask & ((1u << lane) - 1u));
+    if (lane == 0) warp_cnt[warp][o] = __popc(mask);
+  }
+  __syncthreads();
+  if (valid) {
+    int before = 0;
+    for (int w = 0; w < warp; ++w) before += warp_cnt[w][own];
+    const int pos = base[(int64_t)blockIdx.x * world + own] + before + rank;
+    send_keys[pos] = key / world;
+    perm[i] = pos;
+  }
+}
+
+__global__ void k_permute12(const float* __restrict__ in, const int32_t* __restrict__ perm,
+                            const int32_t* __restrict__ count, int64_t n_max, int scatter, float* __restrict__ out) {
+  const int64_t n = min((int64_t)*count, n_max);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t src = scatter ? i : perm[i];
+    const int64_t dst = scatter ? perm[i] : i;
+    const float4* s = reinterpret_cast<const float4*>(in + src * DICM_D);
+    float4* d = reinterpret_cast<float4*>(out + dst * DICM_D);
+    d[0] = s[0];
+    d[1] = s[1];
+    d[2] = s[2];
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t dicm_bucket_workspace(int64_t n_max, int world) {
+  const int64_t nblk = (n_max + BLK - 1) / BLK + 1;
+  return (size_t)(nblk * world * 4 + 256);
+}
+
+int dicm_bucket_by_owner(const int32_t* keys, const int32_t* count_dev, int64_t n_max, int world, int32_t* send_keys,
+                         int32_t* send_counts, int32_t* perm, void* workspace, size_t workspace_bytes,
+                         dicm_stream_t stream) {
+  using namespace dicm;
+  if (world < 1 || world > MAXW) return fail(DICM_ERR_VALUE, "bucket: world %d not in [1, %d]", world, MAXW);
+  if (workspace_bytes < dicm_bucket_workspace(n_max, world)) return fail(DICM_ERR_VALUE, "bucket: workspace");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nblk = (int)((n_max + BLK - 1) / BLK);
+  if (nblk == 0) {
+    cudaMemsetAsync(send_counts, 0, world * 4, st);
+    return last_launch("dicm_bucket_by_owner");
+  }
+  int32_t* blkcnt = (int32_t*)workspace;
+  k_block_counts<<<nblk, BLK, 0, st>>>(keys, count_dev, n_max, world, blkcnt);
+  k_scan_counts<<<1, 32, 0, st>>>(blkcnt, nblk, world, send_counts);
+  k_place<<<nblk, BLK, 0, st>>>(keys, count_dev, n_max, world, blkcnt, send_keys, perm);
+  return last_launch("dicm_bucket_by_owner");
+}
+
+int dicm_permute_rows12(const float* in, const int32_t* perm, const int32_t* count_dev, int64_t n_max, int scatter,
+                        float* out, dicm_stream_t stream) {
+  if (n_max <= 0) return DICM_OK;
+  k_permute12<<<dicm_grid(n_max, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(in, perm, count_dev, n_max, scatter,
+                                                                                out);
+  return dicm::last_launch("dicm_permute_rows12");
+}
+
+}  // extern "C"

@@ -1,0 +1,298 @@
+// a11-a12: the MLP head width -> 128 -> 64 -> 1 and the BCE loss, forward and
+// backward fused per tile of 32 samples.
+//
+// Reference: logits_graph tail (model.py:397-401) = _layer x2 + linear,
+// sigmoid_cross_entropy (autograd.py:230-246) summed and scaled by
+// 1/denominator (training.py:39-42).  dLoss/dz = (sigmoid(z) - y)/denominator
+// depends only on the sample itself, so the whole head -- forward, loss and
+// backward down to dLoss/dx -- runs in one pass per tile without a grid-wide
+// barrier.  Weight gradients are reduced over the tile in shared memory and
+// written as one partial row per block (deterministic, fixed order).
+#include <math.h>
+
+#include "common.cuh"
+
+namespace {
+using namespace dicm;
+
+constexpr int BT = 32;  // samples per block
+constexpr int H0 = DICM_HEAD0, H1 = DICM_HEAD1;
+constexpr int THREADS = 128;
+constexpr int MAXW = 128;
+
+__host__ __device__ inline int64_t part_size(int W) {
+  return (int64_t)H0 + H0 + (int64_t)H0 * W + H1 + H1 + (int64_t)H1 * H0 + 1 + H1;
+}
+
+struct Smem {
+  float w0[H0 * MAXW];  // mlp/0/w [128][W]
+  float w1[H1 * H0];    // mlp/1/w [64][128]
+  float xs[MAXW][BT];   // x^T
+  float a0[H0][BT];     // layer-0 pre-activation^T
+  float a1[H1][BT];     // layer-1 pre-activation^T
+  float da1[H1][BT];
+  float da0[H0][BT];
+  float dz[BT];
+  float loss[BT];
+};
+
+__device__ __forceinline__ void load32(const float* p, float (&v)[BT]) {
+#pragma unroll
+  for (int q = 0; q < BT / 4; ++q) {
+    const float4 t = *reinterpret_cast<const float4*>(p + 4 * q);
+    v[4 * q] = t.x;
+    v[4 * q + 1] = t.y;
+    v[4 * q + 2] = t.z;
+    v[4 * q + 3] = t.w;
+  }
+}
+
+__global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, int B, int W,
+                                                  const float* __restrict__ labels, float inv_denom,
+                                                  dicm_head_params_t p, float* __restrict__ logits,
+                                                  float* __restrict__ dx, float* __restrict__ part,
+                                                  float* __restrict__ loss_part) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+  const int t = threadIdx.x;
+  const int b0 = blockIdx.x * BT;
+  const int nb = min(BT, B - b0);
+  for (int i = t; i < H0 * W; i += THREADS) s.w0[i] = p.w0[i];
+  for (int i = t; i < H1 * H0; i += THREADS) s.w1[i] = p.w1[i];
+  for (int i = t; i < BT * W; i += THREADS) {
+    const int r = i / W, c = i % W;
+    s.xs[c][r] = r < nb ? x[(int64_t)(b0 + r) * W + c] : 0.f;
+  }
+  __syncthreads();
+
+  // layer 0: thread = unit j
+  {
+    const int j = t;
+    float acc[BT];
+    const float bj = p.b0[j];
+#pragma unroll
+    for (int r = 0; r < BT; ++r) acc[r] = bj;
+    for (int k = 0; k < W; ++k) {
+      const float w = s.w0[j * W + k];
+      float xv[BT];
+      load32(s.xs[k], xv);
+#pragma unroll
+      for (int r = 0; r < BT; ++r) acc[r] = fmaf(w, xv[r], acc[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < BT; ++r) s.a0[j][r] = acc[r];
+  }
+  __syncthreads();
+  // layer 1: thread = (unit j, half of the tile)
+  {
+    const int j = t & (H1 - 1), half = t >> 6;
+    float acc[BT / 2];
+    const float bj = p.b1[j];
+#pragma unroll
+    for (int r = 0; r < BT / 2; ++r) acc[r] = bj;
+    for (int k = 0; k < H0; ++k) {
+      const float w = s.w1[j * H0 + k];
+      const float al = __ldg(p.a0 + k);
+#pragma unroll
+      for (int r = 0; r < BT / 2; ++r) acc[r] = fmaf(w, prelu(s.a0[k][half * (BT / 2) + r], al), acc[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < BT / 2; ++r) s.a1[j][half * (BT / 2) + r] = acc[r];
+  }
+  __syncthreads();
+  // layer 2 + loss: thread = sample
+  if (t < BT) {
+    float z = p.b2[0];
+    for (int j = 0; j < H1; ++j) z = fmaf(__ldg(p.w2 + j), prelu(s.a1[j][t], __ldg(p.a1 + j)), z);
+    float l = 0.f, dz = 0.f;
+    if (t < nb) {
+      const float y = labels[b0 + t];
+      l = fmaxf(z, 0.f) - z * y + log1pf(expf(-fabsf(z)));
+      const float sig = 1.f / (1.f + expf(-z));
+      dz = (sig - y) * inv_denom;
+      logits[b0 + t] = z;
+    }
+    s.dz[t] = dz;
+    s.loss[t] = l;
+  }
+  __syncthreads();
+  float* out = part + (int64_t)blockIdx.x * part_size(W);
+  const int64_t o_a0 = 0, o_b0 = H0, o_w0 = 2 * H0, o_a1 = o_w0 + (int64_t)H0 * W, o_b1 = o_a1 + H1,
+                o_w1 = o_b1 + H1, o_b2 = o_w1 + (int64_t)H1 * H0, o_w2 = o_b2 + 1;
+  if (t == 0) {
+    float l = 0.f, d = 0.f;
+    for (int r = 0; r < BT; ++r) {
+      l += s.loss[r];
+      d += s.dz[r];
+    }
+    loss_part[blockIdx.x] = l;
+    out[o_b2] = d;
+  }
+  // layer 2 / prelu 1 backward: thread = unit j of layer 1 (two halves)
+  {
+    const int j = t & (H1 - 1), half = t >> 6;
+    const float al = __ldg(p.a1 + j), w2j = __ldg(p.w2 + j);
+    float sw = 0.f, sa = 0.f, sb = 0.f;
+    for (int rr = 0; rr < BT / 2; ++rr) {
+      const int r = half * (BT / 2) + rr;
+      const float a = s.a1[j][r], dz = s.dz[r];
+      sw = fmaf(dz, prelu(a, al), sw);
+      const float dh = dz * w2j;
+      const float d = a > 0.f ? dh : al * dh;
+      if (!(a > 0.f)) sa = fmaf(a, dh, sa);
+      sb += d;
+      s.da1[j][r] = d;
+    }
+    // combine the two halves through shared memory (reuse loss[] is too small)
+    __shared__ float tmp[3][H1];
+    if (half == 1) {
+      tmp[0][j] = sw;
+      tmp[1][j] = sa;
+      tmp[2][j] = sb;
+    }
+    __syncthreads();
+    if (half == 0) {
+      out[o_w2 + j] = sw + tmp[0][j];
+      out[o_a1 + j] = sa + tmp[1][j];
+      out[o_b1 + j] = sb + tmp[2][j];
+    }
+  }
+  __syncthreads();
+  // dW1[j][k] = sum_r da1[r][j] h0[r][k]: thread = k
+  {
+    const int k = t;
+    const float al = __ldg(p.a0 + k);
+    float h[BT];
+#pragma unroll
+    for (int r = 0; r < BT; ++r) h[r] = prelu(s.a0[k][r], al);
+    for (int j = 0; j < H1; ++j) {
+      float d[BT];
+      load32(s.da1[j], d);
+      float acc = 0.f;
+#pragma unroll
+      for (int r = 0; r < BT; ++r) acc = fmaf(d[r], h[r], acc);
+      out[o_w1 + (int64_t)j * H0 + k] = acc;
+    }
+    // dh0[r][k] = sum_j da1[r][j] W1[j][k]; da0 = prelu'(a0) dh0
+    float dh[BT];
+#pragma unroll
+    for (int r = 0; r < BT; ++r) dh[r] = 0.f;
+    for (int j = 0; j < H1; ++j) {
+      const float w = s.w1[j * H0 + k];
+      float d[BT];
+      load32(s.da1[j], d);
+#pragma unroll
+      for (int r = 0; r < BT; ++r) dh[r] = fmaf(d[r], w, dh[r]);
+    }
+    float sa = 0.f, sb = 0.f;
+#pragma unroll
+    for (int r = 0; r < BT; ++r) {
+      const float a = s.a0[k][r];
+      const float d = a > 0.f ? dh[r] : al * dh[r];
+      if (!(a > 0.f)) sa = fmaf(a, dh[r], sa);
+      sb += d;
+      s.da0[k][r] = d;
+    }
+    out[o_a0 + k] = sa;
+    out[o_b0 + k] = sb;
+  }
+  __syncthreads();
+  // dW0[k][c] = sum_r da0[r][k] x[r][c]: thread = k
+  {
+    const int k = t;
+    float d[BT];
+    load32(s.da0[k], d);
+    for (int c = 0; c < W; ++c) {
+      float xv[BT];
+      load32(s.xs[c], xv);
+      float acc = 0.f;
+#pragma unroll
+      for (int r = 0; r < BT; ++r) acc = fmaf(d[r], xv[r], acc);
+      out[o_w0 + (int64_t)k * W + c] = acc;
+    }
+  }
+  // dx[r][c] = sum_k da0[r][k] W0[k][c]: thread = c
+  for (int c = t; c < W; c += THREADS) {
+    float acc[BT];
+#pragma unroll
+    for (int r = 0; r < BT; ++r) acc[r] = 0.f;
+    for (int k = 0; k < H0; ++k) {
+      const float w = s.w0[k * W + c];
+      float d[BT];
+      load32(s.da0[k], d);
+#pragma unroll
+      for (int r = 0; r < BT; ++r) acc[r] = fmaf(d[r], w, acc[r]);
+    }
+    for (int r = 0; r < nb; ++r) dx[(int64_t)(b0 + r) * W + c] = acc[r];
+  }
+}
+
+__global__ void k_loss_finalize(const float* __restrict__ part, int n, float scale, float* __restrict__ out,
+                                int32_t* __restrict__ status) {
+  __shared__ float red[256];
+  float s = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const float l = red[0] * scale;
+    *out = l;
+    if (!isfinite(l)) atomicOr(&status[DICM_ST_NONFINITE], 1);
+  }
+}
+
+__global__ void k_check_finite(const float* __restrict__ x, int64_t n, const int32_t* __restrict__ count,
+                               int row_width, int bit, int32_t* __restrict__ status) {
+  if (count) n = min(n, (int64_t)*count * row_width);
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&status[DICM_ST_NONFINITE], bit);
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t dicm_head_partial_size(int width) { return part_size(width); }
+
+int dicm_head_blocks(int batch) { return (batch + BT - 1) / BT; }
+
+int dicm_head_fwd_bwd(const float* head_in, int batch, int width, const float* labels, float inv_denominator,
+                      const dicm_head_params_t* p, float* logits, float* d_head_in, float* partials,
+                      float* loss_partials, dicm_stream_t stream) {
+  using namespace dicm;
+  if (width < 1 || width > MAXW) return fail(DICM_ERR_UNSUPPORTED, "head: input width %d not in [1, %d]", width, MAXW);
+  if (batch <= 0) return DICM_OK;
+  const size_t smem = sizeof(Smem);
+  static bool attr = false;
+  if (!attr) {
+    int rc = check_cuda(cudaFuncSetAttribute(k_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                        "head smem attribute");
+    if (rc) return rc;
+    attr = true;
+  }
+  k_head<<<dicm_head_blocks(batch), THREADS, smem, (cudaStream_t)stream>>>(
+      head_in, batch, width, labels, inv_denominator, *p, logits, d_head_in, partials, loss_partials);
+  return last_launch("dicm_head_fwd_bwd");
+}
+
+int dicm_loss_finalize(const float* loss_partials, int nblk, float scale, float* loss_out, int32_t* status,
+                       dicm_stream_t stream) {
+  k_loss_finalize<<<1, 256, 0, (cudaStream_t)stream>>>(loss_partials, nblk, scale, loss_out, status);
+  return dicm::last_launch("dicm_loss_finalize");
+}
+
+int dicm_check_finite(const float* x, int64_t n, const int32_t* count_dev, int row_width, int bit,
+                      int32_t* status, dicm_stream_t stream) {
+  if (n <= 0) return DICM_OK;
+  k_check_finite<<<dicm_grid(n, 256, 148 * 4), 256, 0, (cudaStream_t)stream>>>(x, n, count_dev, row_width, bit,
+                                                                               status);
+  return dicm::last_launch("dicm_check_finite");
+}
+
+}  // extern "C"

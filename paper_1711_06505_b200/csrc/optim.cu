@@ -1,0 +1,169 @@
+// a14: Adam with the reference's semantics (reference optim.py).
+//   dense (optim.py:44-63): per parameter span; an all-zero gradient skips the
+//     span entirely (value, moments and step count untouched, optim.py:55-56);
+//   rows  (optim.py:83-104): per-row step counter, zero rows skipped.
+// Non-finite values anywhere in the step (loss or gradients, latched in the
+// status words by earlier kernels) freeze every update, mirroring the
+// reference raising before it touches a parameter (optim.py:53-54, 90-91).
+#include <math.h>
+
+#include "common.cuh"
+
+namespace {
+using namespace dicm;
+
+constexpr int MAXSPANS = 64;
+
+struct Spans {
+  int64_t off[MAXSPANS + 1];
+  int n;
+};
+
+__device__ __forceinline__ int span_of(const Spans& s, int64_t i) {
+  int lo = 0, hi = s.n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s.off[mid] <= i)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void k_dense_flags(const float* __restrict__ g, const __grid_constant__ Spans s, int32_t* __restrict__ nz,
+                              int32_t* __restrict__ status) {
+  const int64_t total = s.off[s.n];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = g[i];
+    if (!isfinite(v)) atomicOr(&status[DICM_ST_NONFINITE], 2);
+    if (v != 0.f) {
+      const int k = span_of(s, i);
+      if (!nz[k]) atomicOr(&nz[k], 1);
+    }
+  }
+}
+
+__global__ void k_dense_update(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                               float* __restrict__ v, const int32_t* __restrict__ t, const __grid_constant__ Spans s,
+                               const int32_t* __restrict__ nz, const int32_t* __restrict__ status, float lr, float b1,
+                               float b2, float eps) {
+  if (status[DICM_ST_NONFINITE] || status[DICM_ST_KEY_FLAG]) return;
+  const int64_t total = s.off[s.n];
+  int cur = -1;
+  float c1 = 0.f, c2 = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = span_of(s, i);
+    if (!nz[k]) continue;
+    if (k != cur) {
+      cur = k;
+      const int tt = t[k] + 1;
+      c1 = (float)(1.0 / (1.0 - pow((double)b1, (double)tt)));
+      c2 = (float)(1.0 / (1.0 - pow((double)b2, (double)tt)));
+    }
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    p[i] -= lr * (mi * c1) / (sqrtf(vi * c2) + eps);
+  }
+}
+
+__global__ void k_dense_steps(int32_t* __restrict__ t, const int32_t* __restrict__ nz, int n,
+                              const int32_t* __restrict__ status) {
+  if (status[DICM_ST_NONFINITE] || status[DICM_ST_KEY_FLAG]) return;
+  const int k = threadIdx.x;
+  if (k < n && nz[k]) t[k] += 1;
+}
+
+struct Tables {
+  dicm_table_state_t t[DICM_MAX_FIELDS];
+  int n;
+};
+
+__global__ void k_rows(const __grid_constant__ Tables tb, const int32_t* __restrict__ keys,
+                       const int32_t* __restrict__ count, int64_t max_rows, const float* __restrict__ grads, float lr,
+                       float b1, float b2, float eps, const int32_t* __restrict__ status) {
+  if (status[DICM_ST_NONFINITE] || status[DICM_ST_KEY_FLAG]) return;
+  const int64_t n = min((int64_t)*count, max_rows);
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+    const Row12 g = load_row12_cg(grads + u * DICM_D);
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) any |= g.v[c] != 0.f;
+    if (!any) continue;  // optim.py:93-94
+    const int64_t key = keys[u];
+    int k = 0;
+    while (k + 1 < tb.n && key >= tb.t[k + 1].base) ++k;
+    const dicm_table_state_t& T = tb.t[k];
+    const int64_t row = key - T.base;
+    const int tt = T.t[row] + 1;
+    T.t[row] = tt;
+    const float c1 = (float)(1.0 / (1.0 - pow((double)b1, (double)tt)));
+    const float c2 = (float)(1.0 / (1.0 - pow((double)b2, (double)tt)));
+    float* pm = T.m + row * DICM_D;
+    float* pv = T.v + row * DICM_D;
+    float* pp = T.table + row * DICM_D;
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) {
+      const float mi = b1 * pm[c] + (1.f - b1) * g.v[c];
+      const float vi = b2 * pv[c] + (1.f - b2) * g.v[c] * g.v[c];
+      pm[c] = mi;
+      pv[c] = vi;
+      pp[c] -= lr * (mi * c1) / (sqrtf(vi * c2) + eps);
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t dicm_adam_dense_workspace(int nspans) { return (size_t)(nspans + 1) * 4 + 256; }
+
+int dicm_adam_dense(float* param, const float* grad, float* m, float* v, int32_t* t, const dicm_span_t* spans,
+                    int nspans, float lr, float beta1, float beta2, float eps, void* workspace,
+                    size_t workspace_bytes, int32_t* status, dicm_stream_t stream) {
+  using namespace dicm;
+  if (nspans < 1 || nspans > MAXSPANS) return fail(DICM_ERR_VALUE, "adam_dense: %d spans (max %d)", nspans, MAXSPANS);
+  if (workspace_bytes < dicm_adam_dense_workspace(nspans)) return fail(DICM_ERR_VALUE, "adam_dense: workspace");
+  Spans s{};
+  s.n = nspans;
+  int64_t off = 0;
+  for (int i = 0; i < nspans; ++i) {
+    if (spans[i].offset != off) return fail(DICM_ERR_VALUE, "adam_dense: spans must tile the buffer contiguously");
+    s.off[i] = off;
+    off += spans[i].size;
+  }
+  s.off[nspans] = off;
+  cudaStream_t st = (cudaStream_t)stream;
+  int32_t* nz = (int32_t*)workspace;
+  int rc = check_cuda(cudaMemsetAsync(nz, 0, nspans * 4, st), "adam_dense memset");
+  if (rc) return rc;
+  const int grid = dicm_grid(off, 256, 148 * 8);
+  k_dense_flags<<<grid, 256, 0, st>>>(grad, s, nz, status);
+  k_dense_update<<<grid, 256, 0, st>>>(param, grad, m, v, t, s, nz, status, lr, beta1, beta2, eps);
+  k_dense_steps<<<1, MAXSPANS, 0, st>>>(t, nz, nspans, status);
+  return last_launch("dicm_adam_dense");
+}
+
+int dicm_adam_rows(const dicm_table_state_t* tabs, int ntab, const int32_t* uniq_keys, const int32_t* count_dev,
+                   int64_t max_rows, const float* grads, float lr, float beta1, float beta2, float eps,
+                   int32_t* status, dicm_stream_t stream) {
+  using namespace dicm;
+  if (ntab < 1 || ntab > DICM_MAX_FIELDS) return fail(DICM_ERR_VALUE, "adam_rows: %d tables", ntab);
+  if (max_rows <= 0) return DICM_OK;
+  Tables tb{};
+  tb.n = ntab;
+  for (int i = 0; i < ntab; ++i) {
+    tb.t[i] = tabs[i];
+    if (i && tabs[i].base < tabs[i - 1].base + tabs[i - 1].vocab)
+      return fail(DICM_ERR_VALUE, "adam_rows: table key ranges must be ascending and disjoint");
+  }
+  k_rows<<<dicm_grid(max_rows, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(tb, uniq_keys, count_dev, max_rows,
+                                                                              grads, lr, beta1, beta2, eps, status);
+  return last_launch("dicm_adam_rows");
+}
+
+}  // extern "C"

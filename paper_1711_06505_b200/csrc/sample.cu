@@ -1,0 +1,564 @@
+// a6-a10: per-sample gather and behavior aggregation, forward and backward.
+//
+// One warp owns one sample.  Forward builds the head input row
+//   x[b] = [field vectors (schema order) | ad-image emb | pooled behaviors]
+// (reference model.py:358-397) straight from the embedding tables and the
+// deduplicated image embeddings E (gathered through the dedup inverse).
+// Attentive pooling (model.py:206-215) is restructured so the per-reference
+// cost is a 12->32 projection:  W0 [q || k] = Wq q + Wk k, with P = Wq q + b0
+// formed once per sample; the segment softmax is computed online (running
+// max / sum per lane, merged across the warp), and (max, sum) are kept for
+// the backward pass together with the raw scores.
+//
+// Backward reverses the graph (segment_softmax bwd autograd.py:334-337,
+// col_scale bwd 348-350, linear/prelu bwd 201-204/222-225) and scatter-adds
+// embedding and ID-row gradients into the deduplicated row buffers
+// (np.add.at, autograd.py:267-271).  Attention-parameter gradients are
+// accumulated lane-per-hidden-unit and written as deterministic block partials.
+#include <math.h>
+
+#include "common.cuh"
+
+namespace {
+using namespace dicm;
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int FWD_WARPS = 8;
+constexpr int BWD_WARPS = 8;
+constexpr int MAXQ = 2 * DICM_D;
+
+struct AttnSmem {
+  float wq[DICM_ATT][MAXQ];
+  float wk[DICM_ATT][DICM_D];
+  float b0[DICM_ATT], a0[DICM_ATT], w1[DICM_ATT];
+  float b1;
+};
+
+struct Args {
+  dicm_layout_t L;
+  dicm_batch_view_t V;
+  dicm_attn_params_t A[2];
+  float* head_in;
+  float* scores;
+  float* stats;
+  const float* d_head_in;
+  float* d_emb;
+  float* d_rows;
+  float* attn_part;
+};
+
+__device__ __forceinline__ int dq_of(const Args& a, int ch) { return ch == 0 ? DICM_D : DICM_D * a.L.n_query; }
+
+__device__ void load_attn(AttnSmem& s, const dicm_attn_params_t& p, int dq) {
+  const int in = dq + DICM_D;
+  for (int i = threadIdx.x; i < DICM_ATT * in; i += blockDim.x) {
+    const int j = i / in, t = i % in;
+    const float v = p.w0[i];
+    if (t < dq)
+      s.wq[j][t] = v;
+    else
+      s.wk[j][t - dq] = v;
+  }
+  for (int j = threadIdx.x; j < DICM_ATT; j += blockDim.x) {
+    s.b0[j] = p.b0[j];
+    s.a0[j] = p.a0[j];
+    s.w1[j] = p.w1[j];
+  }
+  if (threadIdx.x == 0) s.b1 = p.b1[0];
+}
+
+// the query of a channel, in every lane: ch 0 = ad-image embedding,
+// ch 1 = hstack of the ID query fields (one-hot rows)
+template <int DQ>
+__device__ __forceinline__ void load_query(const Args& a, int ch, int b, float (&q)[DQ]) {
+  if (ch == 0) {
+    const Row12 r = load_row12(a.V.emb + (int64_t)a.V.ad_local[b] * DICM_D);
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) q[c] = r.v[c];
+  } else {
+#pragma unroll
+    for (int f = 0; f < DQ / DICM_D; ++f) {
+      const int fi = a.L.query_field[f];
+      const Row12 r = load_row12(a.V.tables[fi] + (int64_t)a.V.field_ids[fi][b] * DICM_D);
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) q[f * DICM_D + c] = r.v[c];
+    }
+  }
+}
+
+template <int DQ>
+__device__ __forceinline__ float query_proj(const AttnSmem& s, const float (&q)[DQ], int j) {
+  float p = s.b0[j];
+#pragma unroll
+  for (int t = 0; t < DQ; ++t) p = fmaf(s.wq[j][t], q[t], p);
+  return p;
+}
+
+__device__ __forceinline__ float attn_score(const AttnSmem& s, const float (&P)[DICM_ATT], const Row12& k) {
+  float sc = s.b1;
+#pragma unroll 8
+  for (int j = 0; j < DICM_ATT; ++j) {
+    float pre = P[j];
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) pre = fmaf(s.wk[j][c], k.v[c], pre);
+    sc = fmaf(s.w1[j], prelu(pre, s.a0[j]), sc);
+  }
+  return sc;
+}
+
+// ---------------------------------------------------------------------------
+// forward
+// ---------------------------------------------------------------------------
+
+template <int DQ>
+__device__ void attn_fwd(const Args& a, const AttnSmem& s, int ch, int b, int lane) {
+  float q[DQ];
+  load_query<DQ>(a, ch, b, q);
+  const float pj = query_proj<DQ>(s, q, lane);
+  float P[DICM_ATT];
+#pragma unroll
+  for (int j = 0; j < DICM_ATT; ++j) P[j] = __shfl_sync(FULL, pj, j);
+  const int64_t i0 = a.V.beh_off[b], i1 = a.V.beh_off[b + 1];
+  float m = -INFINITY, ssum = 0.f, acc[DICM_D];
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) acc[c] = 0.f;
+  const bool norm = a.L.normalize != 0;
+  for (int64_t i = i0 + lane; i < i1; i += 32) {
+    const Row12 k = load_row12(a.V.emb + (int64_t)a.V.beh_local[i] * DICM_D);
+    const float sc = attn_score(s, P, k);
+    a.scores[(int64_t)ch * a.V.refs + i] = sc;
+    if (norm) {
+      const float mn = fmaxf(m, sc);
+      const float scale = expf(m - mn);  // exp(-inf) = 0 on the first element
+      const float e = expf(sc - mn);
+      ssum = ssum * scale + e;
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) acc[c] = fmaf(e, k.v[c], acc[c] * scale);
+      m = mn;
+    } else {
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) acc[c] = fmaf(sc, k.v[c], acc[c]);
+    }
+  }
+  float out[DICM_D];
+  if (norm) {
+    const float M = warp_max(m);
+    const float f = (m == -INFINITY) ? 0.f : expf(m - M);
+    const float S = warp_sum(ssum * f);
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) out[c] = warp_sum(acc[c] * f);
+    const float inv = S > 0.f ? 1.f / S : 0.f;
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) out[c] *= inv;
+    if (lane == 0) {
+      a.stats[((int64_t)ch * a.V.batch + b) * 2] = M;
+      a.stats[((int64_t)ch * a.V.batch + b) * 2 + 1] = S;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) out[c] = warp_sum(acc[c]);
+  }
+  float* dst = a.head_in + (int64_t)b * a.L.width + a.L.pool_col + ch * DICM_D;
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c)
+    if (lane == c) dst[c] = out[c];
+}
+
+__global__ void __launch_bounds__(FWD_WARPS * 32) k_sample_fwd(const __grid_constant__ Args a) {
+  __shared__ AttnSmem sa[2];
+  const bool att = a.L.use_behavior_images && a.L.kind != 0;
+  if (att) {
+    load_attn(sa[0], a.A[0], DICM_D);
+    if (a.L.kind == 2) load_attn(sa[1], a.A[1], DICM_D * a.L.n_query);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int b = blockIdx.x * FWD_WARPS + warp; b < a.V.batch; b += gridDim.x * FWD_WARPS) {
+    float* row = a.head_in + (int64_t)b * a.L.width;
+    // ID fields: one-hot rows and multi-hot sums
+    for (int f = 0; f < a.L.n_fields; ++f) {
+      const float* T = a.V.tables[f];
+      if (!a.L.field_multi[f]) {
+        if (lane < DICM_D) row[a.L.field_col[f] + lane] = __ldg(T + (int64_t)a.V.field_ids[f][b] * DICM_D + lane);
+      } else {
+        const int32_t* off = a.V.field_off[f];
+        const int32_t* ids = a.V.field_ids[f];
+        float acc[DICM_D];
+#pragma unroll
+        for (int c = 0; c < DICM_D; ++c) acc[c] = 0.f;
+        for (int64_t i = off[b] + lane; i < off[b + 1]; i += 32) {
+          const Row12 r = load_row12(T + (int64_t)ids[i] * DICM_D);
+#pragma unroll
+          for (int c = 0; c < DICM_D; ++c) acc[c] += r.v[c];
+        }
+#pragma unroll
+        for (int c = 0; c < DICM_D; ++c) acc[c] = warp_sum(acc[c]);
+#pragma unroll
+        for (int c = 0; c < DICM_D; ++c)
+          if (lane == c) row[a.L.field_col[f] + c] = acc[c];
+      }
+    }
+    if (a.L.use_ad_image && lane < DICM_D)
+      row[a.L.ad_col + lane] = __ldg(a.V.emb + (int64_t)a.V.ad_local[b] * DICM_D + lane);
+    if (!a.L.use_behavior_images) continue;
+    if (a.L.kind == 0) {
+      float acc[DICM_D];
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) acc[c] = 0.f;
+      for (int64_t i = a.V.beh_off[b] + lane; i < a.V.beh_off[b + 1]; i += 32) {
+        const Row12 r = load_row12(a.V.emb + (int64_t)a.V.beh_local[i] * DICM_D);
+#pragma unroll
+        for (int c = 0; c < DICM_D; ++c) acc[c] += r.v[c];
+      }
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) acc[c] = warp_sum(acc[c]);
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c)
+        if (lane == c) row[a.L.pool_col + c] = acc[c];
+    } else {
+      attn_fwd<DICM_D>(a, sa[0], 0, b, lane);
+      if (a.L.kind == 2) {
+        if (a.L.n_query == 2)
+          attn_fwd<2 * DICM_D>(a, sa[1], 1, b, lane);
+        else
+          attn_fwd<DICM_D>(a, sa[1], 1, b, lane);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward
+// ---------------------------------------------------------------------------
+
+struct WarpScratch {
+  float ds[32];
+  float ks[32][DICM_D];
+  float dp[32][DICM_ATT + 1];
+};
+
+__host__ __device__ constexpr int chan_part(int dq) { return 3 * DICM_ATT + 1 + DICM_ATT * (dq + DICM_D); }
+
+// per-lane (= hidden unit j) accumulators of one channel
+template <int DQ>
+struct AttnAcc {
+  float wq[DQ];
+  float wk[DICM_D];
+  float a0, b0, w1;
+  float b1;  // lane-partial, warp-summed at the end
+};
+
+template <int DQ>
+__device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int ch, int b, int lane,
+                         AttnAcc<DQ>& acc) {
+  const int64_t i0 = a.V.beh_off[b], i1 = a.V.beh_off[b + 1];
+  if (i1 <= i0) return;
+  float q[DQ];
+  load_query<DQ>(a, ch, b, q);
+  const float Pj = query_proj<DQ>(s, q, lane);
+  float wkj[DICM_D];
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) wkj[c] = s.wk[lane][c];
+  const float w1j = s.w1[lane], a0j = s.a0[lane];
+  float dout[DICM_D];
+  const float* dsrc = a.d_head_in + (int64_t)b * a.L.width + a.L.pool_col + ch * DICM_D;
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) dout[c] = __ldg(dsrc + c);
+  const bool norm = a.L.normalize != 0;
+  float M = 0.f, invS = 0.f;
+  if (norm) {
+    M = a.stats[((int64_t)ch * a.V.batch + b) * 2];
+    const float S = a.stats[((int64_t)ch * a.V.batch + b) * 2 + 1];
+    invS = S > 0.f ? 1.f / S : 0.f;
+  }
+  const float* sc = a.scores + (int64_t)ch * a.V.refs;
+  // pass 1: dot = sum_i w_i (dout . k_i)   (softmax backward, autograd.py:335-337)
+  float dot = 0.f;
+  if (norm) {
+    for (int64_t i = i0 + lane; i < i1; i += 32) {
+      const Row12 k = load_row12(a.V.emb + (int64_t)a.V.beh_local[i] * DICM_D);
+      float dw = 0.f;
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) dw = fmaf(dout[c], k.v[c], dw);
+      dot = fmaf(expf(sc[i] - M) * invS, dw, dot);
+    }
+    dot = warp_sum(dot);
+  }
+  float dP = 0.f;
+  // pass 2: chunks of 32 references, lane r owns reference r of the chunk
+  for (int64_t c0 = i0; c0 < i1; c0 += 32) {
+    const int64_t i = c0 + lane;
+    const bool valid = i < i1;
+    Row12 k;
+    float w = 0.f, ds = 0.f;
+    int32_t row = 0;
+    if (valid) {
+      row = a.V.beh_local[i];
+      k = load_row12(a.V.emb + (int64_t)row * DICM_D);
+      float dw = 0.f;
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) dw = fmaf(dout[c], k.v[c], dw);
+      w = norm ? expf(sc[i] - M) * invS : sc[i];
+      ds = norm ? w * (dw - dot) : dw;
+    } else {
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) k.v[c] = 0.f;
+    }
+    ws.ds[lane] = ds;
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) ws.ks[lane][c] = k.v[c];
+    acc.b1 += ds;
+    __syncwarp();
+    // lane j: hidden unit j across the chunk's references
+    const int nr = (int)min((int64_t)32, i1 - c0);
+    for (int r = 0; r < nr; ++r) {
+      float pre = Pj;
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) pre = fmaf(wkj[c], ws.ks[r][c], pre);
+      const float dsr = ws.ds[r];
+      const float dh = dsr * w1j;
+      const bool pos = pre > 0.f;
+      const float dpre = pos ? dh : a0j * dh;
+      acc.w1 = fmaf(dsr, pos ? pre : a0j * pre, acc.w1);
+      if (!pos) acc.a0 = fmaf(pre, dh, acc.a0);
+      acc.b0 += dpre;
+      dP += dpre;
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) acc.wk[c] = fmaf(dpre, ws.ks[r][c], acc.wk[c]);
+      ws.dp[r][lane] = dpre;
+    }
+    __syncwarp();
+    if (valid) {
+      float dk[DICM_D];
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) dk[c] = w * dout[c];
+#pragma unroll 4
+      for (int j = 0; j < DICM_ATT; ++j) {
+        const float d = ws.dp[lane][j];
+#pragma unroll
+        for (int c = 0; c < DICM_D; ++c) dk[c] = fmaf(s.wk[j][c], d, dk[c]);
+      }
+      atomic_add_row12(a.d_emb + (int64_t)row * DICM_D, dk);
+    }
+    __syncwarp();
+  }
+  // query side: dWq[j] += dP_j q ; dq = Wq^T dP
+#pragma unroll
+  for (int t = 0; t < DQ; ++t) acc.wq[t] = fmaf(dP, q[t], acc.wq[t]);
+  float dq[DQ];
+#pragma unroll
+  for (int t = 0; t < DQ; ++t) dq[t] = warp_sum(s.wq[lane][t] * dP);
+  if (ch == 0) {
+    if (lane < DICM_D) {
+      float v = 0.f;
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c)
+        if (c == lane) v = dq[c];
+      atomicAdd(a.d_emb + (int64_t)a.V.ad_local[b] * DICM_D + lane, v);
+    }
+  } else {
+#pragma unroll
+    for (int f = 0; f < DQ / DICM_D; ++f) {
+      const int fi = a.L.query_field[f];
+      if (lane < DICM_D) {
+        float v = 0.f;
+#pragma unroll
+        for (int c = 0; c < DICM_D; ++c)
+          if (c == lane) v = dq[f * DICM_D + c];
+        atomicAdd(a.d_rows + (int64_t)a.V.field_inv[fi][b] * DICM_D + lane, v);
+      }
+    }
+  }
+}
+
+// writes a channel's accumulators into red[warp][...] in sorted-name order:
+// 0/a [32], 0/b [32], 0/w [32 x (dq+12)], 1/b [1], 1/w [32]
+template <int DQ>
+__device__ void dump_acc(const AttnAcc<DQ>& acc, float* dst, int lane) {
+  const int in = DQ + DICM_D;
+  dst[lane] = acc.a0;
+  dst[DICM_ATT + lane] = acc.b0;
+  float* w = dst + 2 * DICM_ATT + lane * in;
+#pragma unroll
+  for (int t = 0; t < DQ; ++t) w[t] = acc.wq[t];
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) w[DQ + c] = acc.wk[c];
+  const float b1 = warp_sum(acc.b1);
+  if (lane == 0) dst[2 * DICM_ATT + DICM_ATT * in] = b1;
+  dst[2 * DICM_ATT + DICM_ATT * in + 1 + lane] = acc.w1;
+}
+
+template <int DQ>
+__device__ void zero_acc(AttnAcc<DQ>& acc) {
+#pragma unroll
+  for (int t = 0; t < DQ; ++t) acc.wq[t] = 0.f;
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) acc.wk[c] = 0.f;
+  acc.a0 = acc.b0 = acc.w1 = acc.b1 = 0.f;
+}
+
+template <int DQ>
+__device__ void attn_channel_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int ch, int lane, int warp,
+                                 float* red, float* part_base) {
+  AttnAcc<DQ> acc;
+  zero_acc(acc);
+  for (int b = blockIdx.x * BWD_WARPS + warp; b < a.V.batch; b += gridDim.x * BWD_WARPS)
+    attn_bwd<DQ>(a, s, ws, ch, b, lane, acc);
+  __syncthreads();  // scratch -> reduction buffer
+  const int n = chan_part(DQ);
+  dump_acc<DQ>(acc, red + warp * n, lane);
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    float t = 0.f;
+    for (int w = 0; w < BWD_WARPS; ++w) t += red[w * n + i];
+    part_base[i] = t;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(BWD_WARPS * 32) k_sample_bwd(const __grid_constant__ Args a, int64_t part_stride) {
+  __shared__ AttnSmem sa[2];
+  extern __shared__ float dyn[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool att = a.L.use_behavior_images && a.L.kind != 0;
+  if (att) {
+    load_attn(sa[0], a.A[0], DICM_D);
+    if (a.L.kind == 2) load_attn(sa[1], a.A[1], DICM_D * a.L.n_query);
+    __syncthreads();
+    WarpScratch& ws = reinterpret_cast<WarpScratch*>(dyn)[warp];
+    float* base = a.attn_part + (int64_t)blockIdx.x * part_stride;
+    // sorted names: attn/id/* before attn/img/*
+    if (a.L.kind == 2) {
+      const int id_size = chan_part(DICM_D * a.L.n_query);
+      if (a.L.n_query == 2)
+        attn_channel_bwd<2 * DICM_D>(a, sa[1], ws, 1, lane, warp, dyn, base);
+      else
+        attn_channel_bwd<DICM_D>(a, sa[1], ws, 1, lane, warp, dyn, base);
+      attn_channel_bwd<DICM_D>(a, sa[0], ws, 0, lane, warp, dyn, base + id_size);
+    } else {
+      attn_channel_bwd<DICM_D>(a, sa[0], ws, 0, lane, warp, dyn, base);
+    }
+  }
+  // field / embedding scatters
+  for (int b = blockIdx.x * BWD_WARPS + warp; b < a.V.batch; b += gridDim.x * BWD_WARPS) {
+    const float* drow = a.d_head_in + (int64_t)b * a.L.width;
+    for (int f = 0; f < a.L.n_fields; ++f) {
+      const float* dsrc = drow + a.L.field_col[f];
+      if (!a.L.field_multi[f]) {
+        if (lane < DICM_D)
+          atomicAdd(a.d_rows + (int64_t)a.V.field_inv[f][b] * DICM_D + lane, __ldg(dsrc + lane));
+      } else {
+        float dv[DICM_D];
+#pragma unroll
+        for (int c = 0; c < DICM_D; ++c) dv[c] = __ldg(dsrc + c);
+        const int32_t* off = a.V.field_off[f];
+        const int32_t* inv = a.V.field_inv[f];
+        for (int64_t i = off[b] + lane; i < off[b + 1]; i += 32)
+          atomic_add_row12(a.d_rows + (int64_t)inv[i] * DICM_D, dv);
+      }
+    }
+    if (a.L.use_ad_image && lane < DICM_D)
+      atomicAdd(a.d_emb + (int64_t)a.V.ad_local[b] * DICM_D + lane, __ldg(drow + a.L.ad_col + lane));
+    if (a.L.use_behavior_images && a.L.kind == 0) {
+      float dv[DICM_D];
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) dv[c] = __ldg(drow + a.L.pool_col + c);
+      for (int64_t i = a.V.beh_off[b] + lane; i < a.V.beh_off[b + 1]; i += 32)
+        atomic_add_row12(a.d_emb + (int64_t)a.V.beh_local[i] * DICM_D, dv);
+    }
+  }
+}
+
+int bwd_grid(int batch) {
+  const int g = (batch + BWD_WARPS - 1) / BWD_WARPS;
+  return g < 1 ? 1 : (g > 148 * 8 ? 148 * 8 : g);
+}
+
+size_t bwd_smem() {
+  const size_t scratch = sizeof(WarpScratch) * BWD_WARPS;
+  const size_t red = sizeof(float) * BWD_WARPS * chan_part(MAXQ);
+  return scratch > red ? scratch : red;
+}
+
+int64_t part_size(const dicm_layout_t* L) {
+  if (!L->use_behavior_images || L->kind == 0) return 0;
+  int64_t n = chan_part(DICM_D);
+  if (L->kind == 2) n += chan_part(DICM_D * L->n_query);
+  return n;
+}
+
+int validate(const dicm_layout_t* L, const dicm_batch_view_t* V) {
+  if (L->n_fields < 0 || L->n_fields > DICM_MAX_FIELDS) return fail(DICM_ERR_VALUE, "sample: %d fields (max 8)", L->n_fields);
+  if (L->kind < 0 || L->kind > 2) return fail(DICM_ERR_UNSUPPORTED, "sample: aggregator kind %d", L->kind);
+  if (L->kind != 0 && L->use_behavior_images && !L->use_ad_image)
+    return fail(DICM_ERR_VALUE, "attentive aggregator needs the ad image as query");
+  if (L->kind == 2 && (L->n_query < 1 || L->n_query > 2))
+    return fail(DICM_ERR_VALUE, "multiquery-attn needs 1 or 2 one-hot query fields");
+  if (L->kind == 2)
+    for (int f = 0; f < L->n_query; ++f)
+      if (L->query_field[f] < 0 || L->query_field[f] >= L->n_fields || L->field_multi[L->query_field[f]])
+        return fail(DICM_ERR_UNSUPPORTED, "multiquery-attn: query fields must be one-hot fields");
+  if (V->batch < 0) return fail(DICM_ERR_VALUE, "sample: negative batch");
+  return DICM_OK;
+}
+
+Args make_args(const dicm_layout_t* L, const dicm_batch_view_t* V, const dicm_attn_params_t* A) {
+  Args a{};
+  a.L = *L;
+  a.V = *V;
+  if (A) {
+    a.A[0] = A[0];
+    a.A[1] = A[1];
+  }
+  return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t dicm_attn_partial_size(const dicm_layout_t* layout) { return part_size(layout); }
+
+int dicm_sample_blocks(int batch) { return bwd_grid(batch); }
+
+int dicm_sample_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const dicm_attn_params_t* attn,
+                    float* head_in, float* scores, float* stats, dicm_stream_t stream) {
+  int rc = validate(layout, bv);
+  if (rc) return rc;
+  if (bv->batch == 0) return DICM_OK;
+  Args a = make_args(layout, bv, attn);
+  a.head_in = head_in;
+  a.scores = scores;
+  a.stats = stats;
+  const int grid = (bv->batch + FWD_WARPS - 1) / FWD_WARPS;
+  k_sample_fwd<<<grid, FWD_WARPS * 32, 0, (cudaStream_t)stream>>>(a);
+  return last_launch("dicm_sample_fwd");
+}
+
+int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const dicm_attn_params_t* attn,
+                    const float* head_in, const float* d_head_in, const float* scores, const float* stats,
+                    float* d_emb, float* d_rows, float* attn_partials, dicm_stream_t stream) {
+  int rc = validate(layout, bv);
+  if (rc) return rc;
+  if (bv->batch == 0) return DICM_OK;
+  Args a = make_args(layout, bv, attn);
+  a.head_in = const_cast<float*>(head_in);
+  a.d_head_in = d_head_in;
+  a.scores = const_cast<float*>(scores);
+  a.stats = const_cast<float*>(stats);
+  a.d_emb = d_emb;
+  a.d_rows = d_rows;
+  a.attn_part = attn_partials;
+  const size_t smem = bwd_smem();
+  static bool attr_set = false;
+  if (!attr_set) {
+    rc = check_cuda(cudaFuncSetAttribute(k_sample_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                    "sample_bwd smem attribute");
+    if (rc) return rc;
+    attr_set = true;
+  }
+  k_sample_bwd<<<bwd_grid(bv->batch), BWD_WARPS * 32, smem, (cudaStream_t)stream>>>(a, part_size(layout));
+  return last_launch("dicm_sample_bwd");
+}
+
+}  // extern "C"

@@ -1,0 +1,157 @@
+"""The DICM model with its parameters resident on the GPU.
+
+API mirror of the reference ``DicmModel`` (model.py:266-408): same
+constructor arguments and validation errors, same parameter names and --
+through ``schema.init_params`` -- bit-identical initial values (cast to fp32
+on the device).  Storage is laid out for the kernels:
+
+* every dense parameter (attn/*, mlp/*, img/*) lives in ONE fused fp32 buffer
+  in ``dense_param_names`` order (sorted worker names, then sorted image
+  names, reference training.py:53), with matching gradient / Adam-moment
+  buffers -- one Adam launch and one NCCL all-reduce cover all of them;
+* each ID table ``id_emb/<field>`` is a [V, 12] fp32 tensor with per-row Adam
+  moments and step counts (reference optim.py:66-80).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import schema as S
+from .schema import AggregatorSpec, FeatureSchema, FieldSpec, ModelLayout  # noqa: F401
+
+KIND_CODE = {"sum": 0, "attn": 1, "multiquery-attn": 2}
+
+
+class Parameter:
+    """A named device tensor; ``.data`` returns a float64 host copy like the
+    reference's ``Parameter.data`` (autograd.py:49-53)."""
+
+    __slots__ = ("name", "tensor")
+
+    def __init__(self, name, tensor):
+        self.name = name
+        self.tensor = tensor
+
+    @property
+    def shape(self):
+        return tuple(self.tensor.shape)
+
+    @property
+    def data(self):
+        return self.tensor.detach().double().cpu().numpy()
+
+    def copy_(self, value):
+        self.tensor.copy_(torch.as_tensor(np.asarray(value), dtype=torch.float32))
+
+    def __repr__(self):
+        return f"Parameter({self.name!r}, shape={self.shape})"
+
+
+def check_hot_path(layout):
+    """The kernels are compiled for the paper's configuration."""
+    s = layout.schema
+    if layout.aggregator.kind not in S.HOT_PATH_AGGREGATORS:
+        raise NotImplementedError(
+            f"aggregator {layout.aggregator.kind!r} is outside this build's hot path "
+            f"(supported: {S.HOT_PATH_AGGREGATORS})")
+    if s.d_id != 12 or s.d_img != 12:
+        raise NotImplementedError("kernels are built for d_id = d_img = 12")
+    if layout.h1 != 256 or layout.h2 != 64 or s.d_raw % 64:
+        raise NotImplementedError("kernels are built for the 4096 -> 256 -> 64 -> 12 image net")
+    if tuple(layout.mlp_widths) != (128, 64):
+        raise NotImplementedError("kernels are built for the (128, 64) head")
+    if layout.attentive and layout.aggregator.attention_hidden != 32:
+        raise NotImplementedError("kernels are built for a 32-unit attention net")
+    if layout.mlp_input_width() > 128:
+        raise NotImplementedError(f"head input width {layout.mlp_input_width()} > 128")
+    if len(s.fields) > 8:
+        raise NotImplementedError("at most 8 ID fields")
+    if layout.multiquery:
+        for q in layout.query_fields_present():
+            if s.field(q).multi:
+                raise NotImplementedError("multiquery-attn query fields must be one-hot")
+
+
+class DicmModel:
+    """Embedding&MLP CTR net with ad-image and behavior-image paths."""
+
+    def __init__(self, schema, aggregator, extractor=None, seed=0, mlp_widths=(128, 64),
+                 use_ad_image=True, use_behavior_images=True, device="cuda", params=None,
+                 table_rows=None):
+        layout = ModelLayout(schema, aggregator, tuple(mlp_widths), use_ad_image, use_behavior_images)
+        S.validate_layout(layout, None if extractor is None else extractor.out_dim)
+        check_hot_path(layout)
+        self.schema = schema
+        self.aggregator = aggregator
+        self.extractor = extractor
+        self.seed = seed
+        self.mlp_widths = tuple(mlp_widths)
+        self.use_ad_image = use_ad_image
+        self.use_behavior_images = use_behavior_images
+        self.layout = layout
+        self.device = torch.device(device)
+        self.specs = S.param_specs(layout)
+        self.dense_names = S.dense_param_names(layout)
+        shapes = {n: shp for n, shp, _ in self.specs}
+        # fused dense buffer
+        self.dense_offsets, off = {}, 0
+        for n in self.dense_names:
+            size = int(np.prod(shapes[n]))
+            self.dense_offsets[n] = (off, size, shapes[n])
+            off += size
+        self.dense_size = off
+        self.dense = torch.zeros(off, dtype=torch.float32, device=self.device)
+        self.params = {}
+        host = params if params is not None else {}
+        kinds = {nm: k for nm, _, k in self.specs}
+        for n in self.dense_names:
+            o, size, shp = self.dense_offsets[n]
+            view = self.dense[o:o + size].view(shp)
+            val = host[n] if n in host else S.init_param(seed, n, shp, kinds[n])
+            view.copy_(torch.as_tensor(np.asarray(val, dtype=np.float64), dtype=torch.float32))
+            self.params[n] = Parameter(n, view)
+        # ID tables (``table_rows`` lets a sharded model hold only its rows)
+        self.tables = {}
+        for f in schema.fields:
+            n = f"id_emb/{f.name}"
+            if table_rows is not None:
+                t = table_rows(f, n)
+            elif n in host:
+                t = torch.as_tensor(np.asarray(host[n], dtype=np.float64), dtype=torch.float32).to(self.device)
+            else:
+                t = torch.as_tensor(S.init_param(seed, n, (f.vocab, schema.d_id), "table"),
+                                    dtype=torch.float32).to(self.device)
+            self.tables[f.name] = t.contiguous()
+            self.params[n] = Parameter(n, self.tables[f.name])
+        self.head_offsets = layout.head_offsets()
+
+    # -- reference bookkeeping (model.py:339-347)
+    def worker_param_names(self):
+        return S.worker_param_names(self.layout)
+
+    def image_param_names(self):
+        return S.image_param_names(self.layout)
+
+    def table_fields(self):
+        return [f.name for f in self.schema.fields]
+
+    def mlp_input_width(self):
+        return self.layout.mlp_input_width()
+
+    def dense_view(self, buf, name):
+        o, size, shp = self.dense_offsets[name]
+        return buf[o:o + size].view(shp)
+
+    def group_range(self, prefix):
+        """[start, end) of the contiguous fused-buffer range of a name group."""
+        names = [n for n in self.dense_names if n.startswith(prefix)]
+        if not names:
+            return None
+        start = self.dense_offsets[names[0]][0]
+        o, size, _ = self.dense_offsets[names[-1]]
+        return start, o + size
+
+    def snapshot(self):
+        return {n: p.data for n, p in self.params.items()}

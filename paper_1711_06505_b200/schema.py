@@ -1,0 +1,262 @@
+"""Feature schema, aggregator spec and reference-compatible parameter init.
+
+Host-side mirror of the reference's model description so that a user of
+``dicm.model`` finds the same names, defaults, validation errors and -- bit
+for bit -- the same initial parameter values:
+
+* ``FieldSpec`` / ``FeatureSchema``      -- reference ``model.py:38-67``
+* ``AggregatorSpec``                     -- reference ``model.py:70-85``
+* ``image_net_widths``                   -- reference ``model.py:88-91``
+* ``param_specs`` / ``init_params``      -- reference ``model.py:94-105`` and
+  ``DicmModel._build_params`` ``model.py:314-335``
+* ``default_schema``                     -- reference ``experiments.py:17-32``
+
+Nothing here touches the GPU; the device model lives in ``model.py``.
+"""
+
+from __future__ import annotations
+
+import zlib
+from dataclasses import dataclass
+
+import numpy as np
+
+AGGREGATOR_KINDS = ("concat", "max", "sum", "attn", "multiquery-attn")
+# aggregators built on the B200 hot path
+HOT_PATH_AGGREGATORS = ("sum", "attn", "multiquery-attn")
+
+GROUP_ID = "id-embeddings"
+GROUP_IMAGE = "image-embedding-model"
+GROUP_MLP = "mlp"
+GROUP_ATTN = "aggregator-attention"
+
+
+def group_of(name):
+    """Checkpoint group / owner side of a parameter (reference model.py:28-35)."""
+    if name.startswith("id_emb/"):
+        return GROUP_ID
+    if name.startswith("img/"):
+        return GROUP_IMAGE
+    if name.startswith("attn/"):
+        return GROUP_ATTN
+    return GROUP_MLP
+
+
+@dataclass(frozen=True)
+class FieldSpec:
+    name: str
+    vocab: int
+    multi: bool = False
+
+
+@dataclass
+class FeatureSchema:
+    """ID fields plus dimension settings (reference model.py:45-67)."""
+
+    fields: list
+    d_id: int = 12
+    d_raw: int = 64
+    d_img: int = 12
+    b_max: int = 32
+    query_fields: tuple = ("ad", "ad_category")
+
+    def __post_init__(self):
+        if min(self.d_id, self.d_raw, self.d_img, self.b_max) < 1:
+            raise ValueError("schema dimensions must be >= 1")
+        for f in self.fields:
+            if f.vocab < 1:
+                raise ValueError(f"field {f.name}: vocabulary must be >= 1")
+
+    def field(self, name):
+        for f in self.fields:
+            if f.name == name:
+                return f
+        raise KeyError(f"schema has no field {name!r}")
+
+
+@dataclass
+class AggregatorSpec:
+    kind: str = "sum"
+    attention_hidden: int = 32
+    normalize: bool = True
+
+    def __post_init__(self):
+        if self.kind not in AGGREGATOR_KINDS:
+            raise ValueError(f"unknown aggregator {self.kind!r}; use one of {AGGREGATOR_KINDS}")
+
+    def output_width(self, d_img, b_max):
+        if self.kind == "concat":
+            return d_img * b_max
+        if self.kind == "multiquery-attn":
+            return 2 * d_img
+        return d_img
+
+
+def image_net_widths(d_raw, d_img):
+    """Hidden widths of the image net (reference model.py:88-91)."""
+    return max(d_raw // 16, d_img), max(d_raw // 64, d_img)
+
+
+def default_schema(users, scenarios, ad_vocab, categories, image_count, d_id=12,
+                   d_raw=4096, d_img=12, b_max=32, image_id_fields=True):
+    """The benchmark field layout of reference experiments.py:17-32, with the
+    vocabularies given directly instead of through a SyntheticConfig."""
+    fields = [
+        FieldSpec("user", users),
+        FieldSpec("scenario", scenarios),
+        FieldSpec("ad", ad_vocab),
+        FieldSpec("ad_category", categories),
+        FieldSpec("behavior_items", ad_vocab, multi=True),
+    ]
+    if image_id_fields:
+        fields.append(FieldSpec("ad_image", image_count))
+        fields.append(FieldSpec("behavior_images", image_count, multi=True))
+    return FeatureSchema(fields=fields, d_id=d_id, d_raw=d_raw, d_img=d_img, b_max=b_max)
+
+
+def rng_for(seed, name):
+    """Per-parameter generator (reference model.py:94-95)."""
+    return np.random.default_rng([int(seed) & 0xFFFFFFFF, zlib.crc32(name.encode())])
+
+
+@dataclass(frozen=True)
+class ModelLayout:
+    """Everything the kernels need to know about one DICM configuration."""
+
+    schema: FeatureSchema
+    aggregator: AggregatorSpec
+    mlp_widths: tuple
+    use_ad_image: bool
+    use_behavior_images: bool
+
+    @property
+    def h1(self):
+        return image_net_widths(self.schema.d_raw, self.schema.d_img)[0]
+
+    @property
+    def h2(self):
+        return image_net_widths(self.schema.d_raw, self.schema.d_img)[1]
+
+    @property
+    def attentive(self):
+        return self.use_behavior_images and self.aggregator.kind in ("attn", "multiquery-attn")
+
+    @property
+    def multiquery(self):
+        return self.use_behavior_images and self.aggregator.kind == "multiquery-attn"
+
+    def query_fields_present(self):
+        names = [f.name for f in self.schema.fields]
+        return [q for q in self.schema.query_fields if q in names]
+
+    def id_query_width(self):
+        return self.schema.d_id * len(self.query_fields_present())
+
+    def mlp_input_width(self):
+        s = self.schema
+        w = len(s.fields) * s.d_id
+        if self.use_ad_image:
+            w += s.d_img
+        if self.use_behavior_images:
+            w += self.aggregator.output_width(s.d_img, s.b_max)
+        return w
+
+    def head_offsets(self):
+        """Column offsets of every part of the head input (the hstack order of
+        reference model.py:364-397): fields in schema order, then the ad-image
+        embedding, then the aggregator output."""
+        s = self.schema
+        off, out = 0, {}
+        for f in s.fields:
+            out["field/" + f.name] = off
+            off += s.d_id
+        if self.use_ad_image:
+            out["ad_image_emb"] = off
+            off += s.d_img
+        if self.use_behavior_images:
+            out["pool"] = off
+            off += self.aggregator.output_width(s.d_img, s.b_max)
+        out["width"] = off
+        return out
+
+
+def validate_layout(layout, extractor_out_dim=None):
+    """The constructor checks of reference model.py:279-288."""
+    agg = layout.aggregator
+    if layout.use_behavior_images and agg.kind in ("attn", "multiquery-attn") and not layout.use_ad_image:
+        raise ValueError(f"aggregator {agg.kind!r} needs the ad image as query")
+    if agg.kind == "multiquery-attn" and not layout.query_fields_present():
+        raise ValueError("multiquery-attn needs at least one ad-side query field")
+    if extractor_out_dim is not None and extractor_out_dim != layout.schema.d_raw:
+        raise ValueError(
+            f"extractor emits {extractor_out_dim}-D features, schema expects {layout.schema.d_raw}"
+        )
+
+
+def param_specs(layout):
+    """Ordered (name, shape, kind) of every parameter, in the reference's
+    construction order (model.py:314-335). kind: table|w|b|a."""
+    s = layout.schema
+    out = []
+
+    def lin(prefix, n_in, n_out, alpha=True):
+        out.append((prefix + "w", (n_out, n_in), "w"))
+        out.append((prefix + "b", (n_out,), "b"))
+        if alpha:
+            out.append((prefix + "a", (n_out,), "a"))
+
+    for f in s.fields:
+        out.append((f"id_emb/{f.name}", (f.vocab, s.d_id), "table"))
+    h1, h2 = layout.h1, layout.h2
+    lin("img/0/", s.d_raw, h1)
+    lin("img/1/", h1, h2)
+    lin("img/2/", h2, s.d_img, alpha=False)
+    if layout.attentive:
+        hidden = layout.aggregator.attention_hidden
+        lin("attn/img/0/", 2 * s.d_img, hidden)
+        lin("attn/img/1/", hidden, 1, alpha=False)
+        if layout.multiquery:
+            lin("attn/id/0/", layout.id_query_width() + s.d_img, hidden)
+            lin("attn/id/1/", hidden, 1, alpha=False)
+    widths = [layout.mlp_input_width(), *layout.mlp_widths]
+    for i in range(len(widths) - 1):
+        lin(f"mlp/{i}/", widths[i], widths[i + 1])
+    lin(f"mlp/{len(widths) - 1}/", widths[-1], 1, alpha=False)
+    return out
+
+
+def init_param(seed, name, shape, kind):
+    """Initial value of one parameter, float64, identical to the reference
+    (model.py:98-105 for linear layers, model.py:316-319 for tables)."""
+    if kind == "table":
+        return 0.05 * rng_for(seed, name).standard_normal(shape)
+    if kind == "w":
+        n_out, n_in = shape
+        return rng_for(seed, name).normal(0.0, np.sqrt(2.0 / n_in), (n_out, n_in))
+    if kind == "b":
+        return np.zeros(shape)
+    if kind == "a":
+        return np.full(shape, 0.25)
+    raise ValueError(kind)
+
+
+def init_params(layout, seed, include_tables=True):
+    return {
+        name: init_param(seed, name, shape, kind)
+        for name, shape, kind in param_specs(layout)
+        if include_tables or kind != "table"
+    }
+
+
+def worker_param_names(layout):
+    """Dense replicated parameters (reference model.py:339-341)."""
+    return sorted(n for n, _, _ in param_specs(layout) if group_of(n) in (GROUP_MLP, GROUP_ATTN))
+
+
+def image_param_names(layout):
+    return sorted(n for n, _, _ in param_specs(layout) if group_of(n) == GROUP_IMAGE)
+
+
+def dense_param_names(layout):
+    """Dense parameters in the order LocalTrainer steps them (training.py:53)."""
+    return worker_param_names(layout) + image_param_names(layout)

@@ -1,0 +1,177 @@
+"""Training-step parity on the B200: the device step against the golden vectors
+of the reference (tests/golden) and against the CPU oracle at benchmark-like
+shapes.  Tolerances (metric |a-b| / max(1,|a|,|b|), reference
+tests/test_autograd.py:10-11):
+  * fp32 paths (precision "fp32"): 1e-4 on loss, logits, embeddings, every
+    gradient, and parameters after Adam;
+  * tensor-core layer 0 ("tf32", "bf16"): 2e-2 on logits (BASELINE.json);
+  * attn/*/1/b after Adam: absolute 2*lr per step -- their exact gradient is 0
+    (softmax shift invariance), so the sign of rounding noise decides a full
+    Adam step in the reference too (hard part 6).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import golden_io as G
+import gpu_helpers as H
+from oracle import dicm_oracle as O
+
+pytestmark = pytest.mark.gpu
+FP32_TOL = 1e-4
+
+
+def _noise(n):
+    return n.startswith("attn/") and n.endswith("/1/b")
+
+
+def _engine(name, precision="fp32", pool_dtype="fp32"):
+    from paper_1711_06505_b200.training import LocalTrainer, TrainConfig
+    fx = G.load(name)
+    m = G.meta(fx)
+    model, pool = H.device_model(m, G.pool(fx), pool_dtype)
+    tr = LocalTrainer(model, pool, TrainConfig(batch_size=24), precision=precision)
+    return fx, m, model, tr
+
+
+@pytest.mark.parametrize("name", G.FULL)
+def test_step0_forward_backward_matches_reference(name):
+    from paper_1711_06505_b200.batch import encode_batch
+    fx, m, model, tr = _engine(name)
+    e = tr.engine
+    batch = encode_batch(G.samples(fx, 0), model)
+    pk = e.upload(batch)
+    loss = e.forward_backward(pk)
+    torch.cuda.synchronize()
+    e.raise_status()
+    assert np.array_equal(e.unique_images(), fx["s0/unique_images"])
+    U = len(fx["s0/unique_images"])
+    assert O.rel_err(loss.item(), fx["s0/loss"]) < FP32_TOL
+    assert O.rel_err(e.logits[:batch.size].cpu().numpy(), fx["s0/logits"]) < FP32_TOL
+    assert O.rel_err(e.emb[:U].cpu().numpy(), fx["s0/E"]) < FP32_TOL
+    assert O.rel_err(e.d_emb[:U].cpu().numpy(), fx["s0/dE"]) < FP32_TOL
+    for n, g in H.dense_grads(e).items():
+        for exp, got in G.golden_view(fx, f"s0/grad/{n}", g):
+            assert O.rel_err(got, exp) < FP32_TOL, n
+    for f, (ids, rows) in H.table_grads(e).items():
+        assert np.array_equal(ids, fx[f"s0/tgrad/{f}/ids"]), f
+        assert O.rel_err(rows, fx[f"s0/tgrad/{f}/rows"]) < FP32_TOL, f
+
+
+@pytest.mark.parametrize("name", G.FULL)
+def test_two_train_steps_match_reference(name):
+    fx, m, model, tr = _engine(name)
+    losses = [tr.train_batch(G.samples(fx, b)) for b in (0, 1)]
+    for got, exp in zip(losses, fx["train/losses"]):
+        assert O.rel_err(got, exp) < FP32_TOL
+    snap = model.snapshot()
+    for n, a in snap.items():
+        for exp, got in G.golden_view(fx, f"train/after/{n}", a):
+            if _noise(n):
+                assert np.max(np.abs(got - exp)) <= 2 * 2 * 0.001 + 1e-6, n
+            else:
+                assert O.rel_err(got, exp) < FP32_TOL, n
+    st = tr.dense_state
+    for n in model.dense_names:
+        if not _noise(n):
+            assert st[n].t == int(fx[f"train/t/{n}"]), n
+    for f, s in tr.table_state.items():
+        assert np.array_equal(s.t, fx[f"train/tt/{f}"]), f
+
+
+def _bench_like(kind, B=256, L=50, P=3000, vocab=20_000, seed=0, lengths=None, zipf=None):
+    from paper_1711_06505_b200.batch import synthetic_batch
+    from paper_1711_06505_b200.model import DicmModel
+    from paper_1711_06505_b200.pool import ImagePool
+    from paper_1711_06505_b200.schema import AggregatorSpec, default_schema
+    schema = default_schema(vocab, 4, vocab, 8, P, b_max=max(L, 1) if lengths is None else 500)
+    model = DicmModel(schema, AggregatorSpec(kind), None, seed=seed)
+    pool = ImagePool.synthetic(P, seed=seed)
+    rng = np.random.default_rng(seed)
+    batch = synthetic_batch(rng, schema, B, L if lengths is None else lengths, P, zipf=zipf)
+    return model, pool, batch
+
+
+@pytest.mark.parametrize("kind", ["sum", "attn", "multiquery-attn"])
+def test_bench_shape_step_matches_oracle(kind):
+    """cfg-1-like shapes (B=256, L=50, 4096-d pool) against the oracle."""
+    from paper_1711_06505_b200.engine import StepEngine
+    model, pool, batch = _bench_like(kind)
+    params = H.host_params(model)
+    e = StepEngine(model, pool, "fp32")
+    pk = e.upload(batch)
+    loss = e.forward_backward(pk)
+    torch.cuda.synchronize()
+    e.raise_status()
+    cfg = H.oracle_cfg_of(model)
+    rows = pool.rows.double().cpu().numpy()
+    ob = H.oracle_batch(batch)
+    out = O.forward_backward(params, cfg, ob, rows)
+    assert np.array_equal(e.unique_images(), out["uniq"])
+    assert O.rel_err(loss.item(), out["loss"]) < FP32_TOL
+    assert O.rel_err(e.logits[:batch.size].cpu().numpy(), out["logits"]) < FP32_TOL
+    for n, g in H.dense_grads(e).items():
+        assert O.rel_err(g, out["grads"][n]) < FP32_TOL, n
+    for f, (ids, rows_) in H.table_grads(e).items():
+        u, r = out["tgrads"][f]
+        assert np.array_equal(ids, u), f
+        assert O.rel_err(rows_, r) < FP32_TOL, f
+
+
+def test_long_tail_lengths_match_oracle():
+    """cfg-5-like variable lengths 1..500 (incl. empty) with attentive pooling."""
+    from paper_1711_06505_b200.engine import StepEngine
+    rng = np.random.default_rng(9)
+    lengths = np.clip(np.round(rng.lognormal(np.log(40), 1.0, 64)), 1, 500).astype(int)
+    lengths[5] = 0
+    lengths[7] = 500
+    model, pool, batch = _bench_like("attn", B=64, P=4000, lengths=lengths)
+    params = H.host_params(model)
+    e = StepEngine(model, pool, "fp32")
+    loss = e.forward_backward(e.upload(batch))
+    torch.cuda.synchronize()
+    out = O.forward_backward(params, H.oracle_cfg_of(model), H.oracle_batch(batch), pool.rows.double().cpu().numpy())
+    assert O.rel_err(loss.item(), out["loss"]) < FP32_TOL
+    for n, g in H.dense_grads(e).items():
+        assert O.rel_err(g, out["grads"][n]) < FP32_TOL, n
+
+
+def test_out_of_vocabulary_raises_keyerror_and_leaves_params():
+    from paper_1711_06505_b200.training import LocalTrainer
+    model, pool, batch = _bench_like("sum", B=32, L=8, P=500)
+    tr = LocalTrainer(model, pool)
+    before = model.snapshot()
+    batch.onehot["user"][3] = 10**6
+    with pytest.raises(KeyError, match="vocabulary"):
+        tr.train_batch(batch)
+    after = model.snapshot()
+    assert all(np.array_equal(before[n], after[n]) for n in before)
+    assert tr.iteration == 0
+    batch.onehot["user"][3] = 1
+    batch.beh_image_ids[0] = 500
+    with pytest.raises(KeyError, match="image"):
+        tr.train_batch(batch)
+
+
+def test_nonfinite_loss_raises_and_leaves_params():
+    from paper_1711_06505_b200.training import LocalTrainer
+    model, pool, batch = _bench_like("sum", B=32, L=8, P=500)
+    tr = LocalTrainer(model, pool)
+    model.params["mlp/2/b"].copy_([np.inf])
+    before = model.snapshot()
+    with pytest.raises(FloatingPointError):
+        tr.train_batch(batch)
+    after = model.snapshot()
+    for n in before:
+        assert np.array_equal(before[n], after[n], equal_nan=True), n
+
+
+@pytest.mark.parametrize("kind", ["sum", "attn"])
+def test_training_loss_decreases(kind):
+    from paper_1711_06505_b200.batch import synthetic_batch
+    from paper_1711_06505_b200.training import LocalTrainer, TrainConfig
+    model, pool, batch = _bench_like(kind, B=128, L=20, P=800)
+    tr = LocalTrainer(model, pool, TrainConfig(lr0=0.003))
+    losses = [tr.train_batch(batch) for _ in range(30)]
+    assert np.mean(losses[-5:]) < np.mean(losses[:5]) - 0.05

@@ -1,0 +1,144 @@
+"""CPU-only tests: the C ABI library loads and exports every declared entry
+point; host-side encoding / layout logic matches the oracle."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import golden_io as G
+from oracle import dicm_oracle as O
+from paper_1711_06505_b200 import schema as S
+from paper_1711_06505_b200.batch import Batch, encode_batch, synthetic_batch, zipf_keys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "dicm_b200.h")
+LIB = os.path.join(ROOT, "paper_1711_06505_b200", "libdicm_b200.so")
+
+
+def _ensure_lib():
+    if not os.path.exists(LIB):
+        import subprocess
+        subprocess.run(["make", "-j8"], cwd=ROOT, check=True, capture_output=True)
+    return LIB
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(dicm_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(_ensure_lib())
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert lib.dicm_version() == 1
+
+
+def test_python_binding_covers_header():
+    _ensure_lib()
+    from paper_1711_06505_b200 import _lib
+    assert sorted(_lib.EXPORTED) == declared_symbols()
+
+
+def test_library_reports_no_device_here_without_crashing():
+    lib = ctypes.CDLL(_ensure_lib())
+    arch = lib.dicm_device_arch()
+    assert isinstance(arch, int)
+
+
+def test_workspace_queries_are_pure_host():
+    _ensure_lib()
+    from paper_1711_06505_b200 import _lib as L
+    assert L.lib.dicm_dedup_workspace(1_000_000) >= 1_000_000 // 8
+    assert L.lib.dicm_head_partial_size(120) == 128 + 128 + 128 * 120 + 64 + 64 + 64 * 128 + 1 + 64
+    lay = L.Layout()
+    lay.kind, lay.use_behavior_images, lay.n_query = 2, 1, 2
+    assert L.lib.dicm_attn_partial_size(ctypes.byref(lay)) == (97 + 32 * 24) + (97 + 32 * 36)
+
+
+@pytest.mark.parametrize("name", G.FULL + G.TINY)
+def test_encode_batch_matches_oracle_encode(name):
+    fx = G.load(name)
+    m = G.meta(fx)
+    lay = G.layout_of(m)
+
+    class M:
+        schema = lay.schema
+
+    samples = G.samples(fx, 0)
+    b = encode_batch(samples, M)
+    ob = O.encode(samples, G.oracle_cfg(m))
+    for f, v in b.onehot.items():
+        assert np.array_equal(v, ob["onehot"][f])
+    for f, (fl, of) in b.multihot.items():
+        assert np.array_equal(fl, ob["multihot"][f][0]) and np.array_equal(of, ob["multihot"][f][1])
+    assert np.array_equal(b.beh_image_ids, ob["beh_image_ids"])
+    assert np.array_equal(b.beh_off, ob["beh_off"])
+    assert np.array_equal(b.labels, ob["labels"])
+    assert np.array_equal(b.unique_images(lay.use_ad_image, lay.use_behavior_images),
+                          np.unique(O.needed_image_keys(G.oracle_cfg(m), ob)))
+
+
+def test_head_offsets_follow_reference_hstack_order():
+    lay = S.ModelLayout(S.default_schema(10, 4, 10, 8, 10), S.AggregatorSpec("multiquery-attn"), (128, 64),
+                        True, True)
+    ho = lay.head_offsets()
+    names = [f.name for f in lay.schema.fields]
+    assert [ho["field/" + n] for n in names] == [12 * i for i in range(7)]
+    assert ho["ad_image_emb"] == 84 and ho["pool"] == 96 and ho["width"] == 120 == lay.mlp_input_width()
+
+
+def test_dense_groups_are_contiguous_in_sorted_order():
+    for kind in ("sum", "attn", "multiquery-attn"):
+        lay = S.ModelLayout(S.default_schema(10, 4, 10, 8, 10), S.AggregatorSpec(kind), (128, 64), True, True)
+        names = S.dense_param_names(lay)
+        groups = [n.split("/")[0] for n in names]
+        # attn/*, mlp/*, img/* each contiguous
+        seen = []
+        for g in groups:
+            if not seen or seen[-1] != g:
+                assert g not in seen
+                seen.append(g)
+
+
+def test_batch_slice_is_contiguous_worker_split():
+    schema = S.default_schema(100, 4, 100, 8, 50, b_max=16)
+    b = synthetic_batch(np.random.default_rng(0), schema, 40, 10, 50)
+    parts = [b.slice(i * 10, (i + 1) * 10) for i in range(4)]
+    assert np.array_equal(np.concatenate([p.beh_image_ids for p in parts]), b.beh_image_ids)
+    assert all(p.size == 10 and p.beh_off[0] == 0 for p in parts)
+
+
+def test_synthetic_batch_shapes_and_zipf():
+    schema = S.default_schema(1000, 4, 1000, 8, 5000, b_max=50)
+    rng = np.random.default_rng(1)
+    b = synthetic_batch(rng, schema, 256, 50, 5000)
+    assert b.refs == 256 * 50 and b.beh_off[-1] == b.refs
+    assert np.array_equal(b.multihot["behavior_images"][0], b.beh_image_ids)
+    assert np.array_equal(b.onehot["ad_image"], b.ad_image_ids)
+    z = zipf_keys(rng, 100_000, 1_000_000, 1.1)
+    top = np.bincount(z).max() / len(z)
+    assert 0.05 < top < 0.2  # the hottest key takes ~11% of the references
+
+
+def test_lr_schedule_paper_values():
+    from paper_1711_06505_b200.engine import lr_schedule
+    assert lr_schedule(0) == 0.001
+    assert abs(lr_schedule(24000) - 0.0009) < 1e-15
+    assert abs(lr_schedule(48000) - 0.00081) < 1e-15
+    with pytest.raises(ValueError):
+        lr_schedule(-1)
+
+
+def test_model_validation_errors_mirror_reference():
+    lay = S.ModelLayout(S.default_schema(10, 4, 10, 8, 10), S.AggregatorSpec("attn"), (128, 64), False, True)
+    with pytest.raises(ValueError, match="needs the ad image"):
+        S.validate_layout(lay)
+    with pytest.raises(ValueError, match="unknown aggregator"):
+        S.AggregatorSpec("bogus")
