@@ -27,7 +27,7 @@ constexpr int FWD_WARPS = 8;
 constexpr int BWD_WARPS = 8;
 constexpr int MAXQ = 2 * DICM_D;
 
-struct AttnSmem {
+struct __align__(16) AttnSmem {
   float wq[DICM_ATT][MAXQ];
   float wk[DICM_ATT][DICM_D];
   float b0[DICM_ATT], a0[DICM_ATT], w1[DICM_ATT];
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_sample_fwd(const __grid_cons
 // backward
 // ---------------------------------------------------------------------------
 
-struct WarpScratch {
+struct __align__(16) WarpScratch {
   float ds[32];
   float ks[32][DICM_D];
   float dp[32][DICM_ATT + 1];
