@@ -181,6 +181,12 @@ size_t carve(int64_t rows_max, int d_raw, Ws* w, char* base) {
   return off + sm100::workspace_bytes(rows_max, d_raw);
 }
 
+int check_aligned(const void* a, const void* b, const void* c, const void* d) {
+  if (((uintptr_t)a | (uintptr_t)b | (uintptr_t)c | (uintptr_t)d) & 15)
+    return fail(DICM_ERR_VALUE, "image MLP: pool, act buffers and img/*/w must be 16-byte aligned");
+  return DICM_OK;
+}
+
 int check_shapes(int d_raw, int64_t rows_max) {
   if (d_raw % 64 != 0 || d_raw / 16 != H1)
     return fail(DICM_ERR_UNSUPPORTED,
@@ -203,6 +209,7 @@ int dicm_imgmlp_fwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
                     size_t workspace_bytes, dicm_stream_t stream) {
   using namespace dicm::simt;
   int rc = check_shapes(d_raw, rows_max);
+  if (!rc) rc = check_aligned(pool, p->w0, p->w1, act0);
   if (rc) return rc;
   if (rows_max == 0) return DICM_OK;
   if (workspace_bytes < dicm_imgmlp_workspace(rows_max, d_raw, precision))
@@ -241,6 +248,7 @@ int dicm_imgmlp_bwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
                     size_t workspace_bytes, dicm_stream_t stream) {
   using namespace dicm::simt;
   int rc = check_shapes(d_raw, rows_max);
+  if (!rc) rc = check_aligned(pool, p->w1, g->w0, act0);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   if (rows_max == 0) {

@@ -119,12 +119,14 @@ class StepEngine:
         self.grad = torch.zeros_like(model.dense)
         self.m = torch.zeros_like(model.dense)
         self.v = torch.zeros_like(model.dense)
-        self.spans = (L.Span * len(model.dense_names))()
-        for i, n in enumerate(model.dense_names):
-            o, size, _ = model.dense_offsets[n]
+        self.spans = (L.Span * len(model.dense_spans))()
+        self.span_index = {}
+        for i, (o, size, n) in enumerate(model.dense_spans):
             self.spans[i].offset, self.spans[i].size = o, size
-        self.t = torch.zeros(len(model.dense_names), dtype=torch.int32, device=dev)
-        self.adam_ws = _u8(L.lib.dicm_adam_dense_workspace(len(model.dense_names)), dev)
+            if n is not None:
+                self.span_index[n] = i
+        self.t = torch.zeros(len(model.dense_spans), dtype=torch.int32, device=dev)
+        self.adam_ws = _u8(L.lib.dicm_adam_dense_workspace(len(model.dense_spans)), dev)
         self.tm = {f.name: torch.zeros_like(model.tables[f.name]) for f in self.fields}
         self.tv = {f.name: torch.zeros_like(model.tables[f.name]) for f in self.fields}
         self.tt = {f.name: torch.zeros(model.tables[f.name].shape[0], dtype=torch.int32, device=dev)

@@ -96,10 +96,18 @@ class DicmModel:
         self.dense_names = S.dense_param_names(layout)
         shapes = {n: shp for n, shp, _ in self.specs}
         # fused dense buffer
+        # the image group starts on a 256-B boundary so the kernels can use
+        # 16-B vector loads on img/*/w; the gap is its own (always-zero) span
         self.dense_offsets, off = {}, 0
+        self.dense_spans = []  # (offset, size, name or None) tiling the buffer
         for n in self.dense_names:
+            if n.startswith("img/") and off % 64:
+                pad = 64 - off % 64
+                self.dense_spans.append((off, pad, None))
+                off += pad
             size = int(np.prod(shapes[n]))
             self.dense_offsets[n] = (off, size, shapes[n])
+            self.dense_spans.append((off, size, n))
             off += size
         self.dense_size = off
         self.dense = torch.zeros(off, dtype=torch.float32, device=self.device)

@@ -104,9 +104,9 @@ class LocalTrainer:
         e, m = self.engine, self.model
         t = e.t.cpu().numpy()
         out = {}
-        for i, n in enumerate(m.dense_names):
+        for n in m.dense_names:
             out[n] = AdamStateView(m.dense_view(e.m, n).double().cpu().numpy(),
-                                   m.dense_view(e.v, n).double().cpu().numpy(), int(t[i]))
+                                   m.dense_view(e.v, n).double().cpu().numpy(), int(t[e.span_index[n]]))
         return out
 
     @property
