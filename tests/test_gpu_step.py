@@ -70,6 +70,13 @@ def test_two_train_steps_match_reference(name):
         for exp, got in G.golden_view(fx, f"train/after/{n}", a):
             if _noise(n):
                 assert np.max(np.abs(got - exp)) <= 2 * 2 * 0.001 + 1e-6, n
+            elif n == "img/0/w":
+                # 1M entries seen through random projections: an entry whose
+                # exact gradient nearly cancels (|g| below fp32 accumulation
+                # error) can take Adam's +-lr step with the opposite sign;
+                # one such entry moves a projection by ~lr * |probe| ~ 1e-3.
+                # Adam itself is pinned entry-wise in test_adam_* below.
+                assert O.rel_err(got, exp) < 5e-3, n
             else:
                 assert O.rel_err(got, exp) < FP32_TOL, n
     st = tr.dense_state
@@ -78,6 +85,39 @@ def test_two_train_steps_match_reference(name):
             assert st[n].t == int(fx[f"train/t/{n}"]), n
     for f, s in tr.table_state.items():
         assert np.array_equal(s.t, fx[f"train/tt/{f}"]), f
+
+
+@pytest.mark.parametrize("name", ["full_sum", "full_mq"])
+def test_adam_matches_oracle_on_device_gradients(name):
+    """Adam pinned entry-wise: the oracle's optim.py restatement applied to
+    the device's own gradients reproduces the device update (fp32 vs f64)."""
+    from paper_1711_06505_b200.batch import encode_batch
+    fx, m, model, tr = _engine(name)
+    e = tr.engine
+    before = model.snapshot()
+    loss = e.forward_backward(e.upload(encode_batch(G.samples(fx, 0), model)))
+    grads = H.dense_grads(e)
+    tgr = H.table_grads(e)
+    # zero-gradient skip: blank one span and check it is left alone
+    model.dense_view(e.grad, "mlp/1/a").zero_()
+    grads["mlp/1/a"][:] = 0.0
+    e.optimizer_step(0.001)
+    torch.cuda.synchronize()
+    e.raise_status()
+    after = model.snapshot()
+    st = tr.dense_state
+    for n in model.dense_names:
+        v = before[n].copy()
+        state = {"m": np.zeros_like(v), "v": np.zeros_like(v), "t": 0}
+        O.adam_step(v, grads[n], state, 0.001)
+        assert np.max(np.abs(after[n] - v)) < 2e-6, n
+        assert st[n].t == state["t"], n
+    for f, (ids, rows) in tgr.items():
+        T = before[f"id_emb/{f}"].copy()
+        ts = {"m": np.zeros_like(T), "v": np.zeros_like(T), "t": np.zeros(len(T), dtype=np.int64)}
+        O.adam_rows(T, ids, rows, ts, 0.001)
+        assert np.max(np.abs(after[f"id_emb/{f}"] - T)) < 2e-6, f
+        assert np.array_equal(tr.table_state[f].t, ts["t"]), f
 
 
 def _bench_like(kind, B=256, L=50, P=3000, vocab=20_000, seed=0, lengths=None, zipf=None):
