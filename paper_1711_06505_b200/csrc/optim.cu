@@ -33,15 +33,25 @@ __device__ __forceinline__ int span_of(const Spans& s, int64_t i) {
 
 __global__ void k_dense_flags(const float* __restrict__ g, const __grid_constant__ Spans s, int32_t* __restrict__ nz,
                               int32_t* __restrict__ status) {
+  // warp-aggregated: one flag update per (warp, span) instead of per element
   const int64_t total = s.off[s.n];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const float v = g[i];
-    if (!isfinite(v)) atomicOr(&status[DICM_ST_NONFINITE], 2);
-    if (v != 0.f) {
-      const int k = span_of(s, i);
-      if (!nz[k]) atomicOr(&nz[k], 1);
+  const int lane = threadIdx.x & 31;
+  bool bad = false;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < total; i0 += stride) {
+    const int64_t i = i0 + lane;
+    const float v = i < total ? g[i] : 0.f;
+    bad |= !isfinite(v);
+    const int k = span_of(s, i < total ? i : total - 1);
+    const int k0 = __shfl_sync(0xffffffffu, k, 0);
+    const bool nonzero = v != 0.f;
+    if (__all_sync(0xffffffffu, k == k0)) {
+      if (__any_sync(0xffffffffu, nonzero) && lane == 0 && !nz[k0]) atomicOr(&nz[k0], 1);
+    } else if (nonzero && !nz[k]) {
+      atomicOr(&nz[k], 1);
     }
   }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&status[DICM_ST_NONFINITE], 2);
 }
 
 __global__ void k_dense_update(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,

@@ -26,6 +26,16 @@ def _noise(n):
     return n.startswith("attn/") and n.endswith("/1/b")
 
 
+def _adam_close(got, exp, steps, lr=0.001, frac=0.01):
+    """Parameters after Adam: every entry within 1e-4 (rel, max(1,.)) except
+    at most ``frac`` of them, which may differ by one sign-flipped Adam step
+    per step (|exact gradient| below fp32 rounding; SURVEY.md 7 part 6)."""
+    got, exp = np.asarray(got, np.float64), np.asarray(exp, np.float64)
+    d = np.abs(got - exp) / np.maximum(1.0, np.maximum(np.abs(got), np.abs(exp)))
+    bad = d > FP32_TOL
+    return bool(np.all(d[bad] <= 2.5 * lr * steps) and bad.mean() <= frac)
+
+
 def _engine(name, precision="fp32", pool_dtype="fp32"):
     from paper_1711_06505_b200.training import LocalTrainer, TrainConfig
     fx = G.load(name)
@@ -78,7 +88,7 @@ def test_two_train_steps_match_reference(name):
                 # Adam itself is pinned entry-wise in test_adam_* below.
                 assert O.rel_err(got, exp) < 5e-3, n
             else:
-                assert O.rel_err(got, exp) < FP32_TOL, n
+                assert _adam_close(got, exp, steps=2), n
     st = tr.dense_state
     for n in model.dense_names:
         if not _noise(n):
