@@ -1,19 +1,454 @@
-// tcgen05 layer-0 kernels (placeholder: filled in by the tensor-core build step).
+// Layer 0 of the image MLP on the 5th-generation tensor cores (tcgen05).
+//
+// Forward  act0[U,256] = X[rows] . W0^T + b0      (reference model.py:115-120,
+//                                                  autograd.py:199)
+// Backward dW0[256,d_raw] = da0^T . X[rows]       (autograd.py:202)
+//
+// Both kernels keep a 256 x 256 fp32 accumulator tile in TMEM (two M=128
+// halves, all 512 columns) fed by a 3-stage shared-memory ring:
+//   * the dense operand (W0 forward, da0 backward) arrives by TMA tile loads
+//     (SWIZZLE_128B) signalled through mbarrier transaction counts;
+//   * the gathered operand -- pool rows picked by the dedup's unique ids --
+//     arrives by 16-byte cp.async (LDGSTS) gathers written straight into the
+//     same 128-byte-swizzled layout, so no gathered copy of X is ever formed;
+//   * one elected thread issues tcgen05.mma (kind::tf32 on an fp32 pool,
+//     kind::f16 on a bf16 pool) and releases each stage with tcgen05.commit;
+//   * four warps drain TMEM with tcgen05.ld and apply the epilogue.
+// Forward tiles are 256 rows; the backward reduction over rows is split into
+// nsplit chunks per 256-feature tile and finished by a deterministic reduce.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "imgmlp_sm100.cuh"
+#include "tc_ptx.cuh"
 
 namespace dicm {
 namespace sm100 {
+namespace {
 
-size_t workspace_bytes(int64_t rows_max, int d_raw) { return 0; }
+using namespace tc;
 
-int fwd_layer0(const void*, int, int, const int32_t*, const int32_t*, int64_t, const float*, const float*, float*,
-               int precision, void*, cudaStream_t) {
-  return fail(DICM_ERR_UNSUPPORTED, "image MLP precision %d: tensor-core path not built", precision);
+constexpr int STAGES = 3;
+constexpr int LAG = STAGES - 1;  // cp.async groups kept in flight per producer thread
+constexpr uint32_t OPB = 256 * 128;  // bytes per operand per stage (256 x 128 B)
+constexpr uint32_t STAGE_BYTES = 2 * OPB;
+constexpr size_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int THREADS = 192;  // warps 0-3 producers+epilogue, 4 MMA, 5 TMA
+
+template <int KIND>
+using Elem = typename std::conditional<KIND == 0, float, __nv_bfloat16>::type;
+
+struct Smem {
+  uint32_t base, full, empty, acc, slot;
+  uint32_t* slot_ptr;
+};
+
+__device__ __forceinline__ Smem carve(uint8_t* raw) {
+  Smem s;
+  const uint32_t r = smem_u32(raw);
+  s.base = (r + 1023u) & ~1023u;
+  s.full = s.base + STAGES * STAGE_BYTES;
+  s.empty = s.full + 8 * STAGES;
+  s.acc = s.empty + 8 * STAGES;
+  s.slot = s.acc + 8;
+  s.slot_ptr = reinterpret_cast<uint32_t*>(raw + (s.slot - r));
+  return s;
 }
 
-int bwd_dw0(const void*, int, int, const int32_t*, const int32_t*, int64_t, const float*, float*, int precision,
-            void*, cudaStream_t) {
-  return fail(DICM_ERR_UNSUPPORTED, "image MLP precision %d: tensor-core path not built", precision);
+__device__ __forceinline__ uint32_t setup(const Smem& s, int warp) {
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(s.full + 8 * i, 128 + 1);  // 128 gather threads + the TMA thread's expect_tx
+      mbar_init(s.empty + 8 * i, 1);       // tcgen05.commit
+    }
+    mbar_init(s.acc, 1);
+    fence_mbar_init();
+  }
+  if (warp == 4) {
+    tmem_alloc(s.slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  return *reinterpret_cast<volatile uint32_t*>(s.slot_ptr);
+}
+
+// ---------------------------------------------------------------------------
+// forward: act0 = X[rows] W0^T + b0, one CTA per 256 rows
+// ---------------------------------------------------------------------------
+template <int KIND>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_fwd(const __grid_constant__ CUtensorMap tmW, const void* __restrict__ pool_, int d_raw,
+          const int32_t* __restrict__ rows, const int32_t* __restrict__ count, const float* __restrict__ bias,
+          float* __restrict__ act0) {
+  using T = Elem<KIND>;
+  constexpr int EPB = 128 / sizeof(T);  // elements per 128-byte row slice
+  const int U = *count;
+  const int m0 = blockIdx.x * 256;
+  if (m0 >= U) return;
+  extern __shared__ uint8_t smem_raw[];
+  const Smem s = carve(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t tmem = setup(s, warp);
+  const int nk = d_raw / EPB;
+  const T* pool = reinterpret_cast<const T*>(pool_);
+
+  if (warp < 4) {
+    // ---- gather producer: 16 rows x one 16-B chunk per thread and stage
+    const int t = threadIdx.x, c = t & 7, rb = t >> 3;
+    const T* src[16];
+    uint32_t ok[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int gr = m0 + rb + 16 * i;
+      const bool v = gr < U;
+      src[i] = pool + (int64_t)(v ? rows[gr] : 0) * d_raw + c * (16 / sizeof(T));
+      ok[i] = v ? 16u : 0u;
+    }
+    const uint32_t dst0 = (uint32_t)(rb * 128 + ((c ^ (rb & 7)) << 4));  // (rb + 16 i) & 7 == rb & 7
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % STAGES, it = kb / STAGES;
+      mbar_wait(s.empty + 8 * st, (it & 1) ^ 1);
+      const uint32_t a = s.base + st * STAGE_BYTES + dst0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) cp_async16(a + i * 16 * 128, src[i] + (int64_t)kb * EPB, ok[i]);
+      cp_async_commit();
+      if (kb >= LAG) {
+        cp_async_wait<LAG>();
+        fence_proxy_async();
+        mbar_arrive(s.full + 8 * ((kb - LAG) % STAGES));
+      }
+    }
+    cp_async_wait<0>();
+    fence_proxy_async();
+    for (int kb = (nk > LAG ? nk - LAG : 0); kb < nk; ++kb) mbar_arrive(s.full + 8 * (kb % STAGES));
+  } else if (warp == 5) {
+    if (lane == 0) {
+      // ---- TMA producer for W0 [256, d_raw] (K-major, 128-B swizzle)
+      prefetch_tmap(&tmW);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int st = kb % STAGES, it = kb / STAGES;
+        mbar_wait(s.empty + 8 * st, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(s.full + 8 * st, OPB);
+        tma_load_2d(s.base + st * STAGE_BYTES + OPB, &tmW, s.full + 8 * st, kb * EPB, 0);
+      }
+    }
+  } else {
+    if (lane == 0) {
+      // ---- MMA issuer: 2 halves (rows 0-127, 128-255) x 4 k-steps of 32 B
+      const uint32_t idesc = instr_desc(KIND == 0 ? 2u : 1u, 128, 256, 0, 0);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int st = kb % STAGES, it = kb / STAGES;
+        mbar_wait(s.full + 8 * st, it & 1);
+        tc_fence_after();
+        const uint32_t a = s.base + st * STAGE_BYTES, b = a + OPB;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma<KIND>(tmem + h * 256, smem_desc(a + h * 16384 + k * 32, 16, 1024), smem_desc(b + k * 32, 16, 1024),
+                      idesc, (kb | k) != 0);
+        mma_commit(s.empty + 8 * st);
+      }
+      mma_commit(s.acc);
+    }
+  }
+  // ---- epilogue: TMEM -> registers (+ bias) -> act0
+  if (warp < 4) {
+    mbar_wait(s.acc, 0);
+    tc_fence_after();
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int row = m0 + h * 128 + warp * 32 + lane;
+#pragma unroll 1
+      for (int cb = 0; cb < 8; ++cb) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + h * 256 + cb * 32, v);
+        if (row < U) {
+          float4* out = reinterpret_cast<float4*>(act0 + (int64_t)row * 256 + cb * 32);
+          const float4* bb = reinterpret_cast<const float4*>(bias + cb * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 b4 = __ldg(bb + q);
+            out[q] = make_float4(v[4 * q] + b4.x, v[4 * q + 1] + b4.y, v[4 * q + 2] + b4.z, v[4 * q + 3] + b4.w);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) tmem_dealloc(tmem, 512);
+}
+
+// ---------------------------------------------------------------------------
+// backward: part[split][256][d_raw] = da0[chunk]^T X[rows[chunk]]
+// grid = (d_raw/256 feature tiles, nsplit row chunks)
+// ---------------------------------------------------------------------------
+template <int KIND>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_dw0(const __grid_constant__ CUtensorMap tmA, const void* __restrict__ pool_, int d_raw,
+          const int32_t* __restrict__ rows, const int32_t* __restrict__ count, float* __restrict__ part) {
+  using T = Elem<KIND>;
+  constexpr int EPB = 128 / sizeof(T);   // MN-atom width (elements)
+  constexpr int BK = EPB;                // rows per stage: 32 (tf32) / 64 (bf16)
+  constexpr int KROWS = 32 / sizeof(T);  // rows per MMA: 8 (tf32) / 16 (bf16)
+  constexpr int NA = 128 / EPB;          // MN atoms per 128-wide half
+  constexpr int CPR = 256 * sizeof(T) / 16;  // 16-B chunks per row slice
+  const int U = *count;
+  const int f0 = blockIdx.x * 256, split = blockIdx.y, nsplit = gridDim.y;
+  const int per = (((U + nsplit - 1) / nsplit) + BK - 1) / BK * BK;
+  const int r0 = split * per;
+  const int r1 = min(U, r0 + per);
+  const int nk = r1 > r0 ? (r1 - r0 + BK - 1) / BK : 0;
+  float* out = part + (int64_t)split * 256 * d_raw;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (nk == 0) {  // empty chunk: its partial is zero
+    for (int i = threadIdx.x; i < 256 * 256; i += THREADS) out[(int64_t)(i >> 8) * d_raw + f0 + (i & 255)] = 0.f;
+    return;
+  }
+  extern __shared__ uint8_t smem_raw[];
+  const Smem s = carve(smem_raw);
+  const uint32_t tmem = setup(s, warp);
+  const T* pool = reinterpret_cast<const T*>(pool_);
+
+  if (warp < 4) {
+    // ---- gather producer: X[rows] feature slice [f0, f0+256) of BK rows
+    const int t = threadIdx.x;
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % STAGES, it = kb / STAGES;
+      mbar_wait(s.empty + 8 * st, (it & 1) ^ 1);
+      const uint32_t b = s.base + st * STAGE_BYTES + OPB;
+#pragma unroll 4
+      for (int i = 0; i < 16; ++i) {
+        const int q = i * 128 + t;
+        const int k = q / CPR, c = q % CPR;
+        const int gr = r0 + kb * BK + k;
+        const bool v = gr < r1;
+        const T* src = pool + (int64_t)(v ? rows[gr] : 0) * d_raw + f0 + c * (16 / sizeof(T));
+        const uint32_t dst = b + (c >> 3) * (BK * 128) + k * 128 + (((c & 7) ^ (k & 7)) << 4);
+        cp_async16(dst, src, v ? 16u : 0u);
+      }
+      cp_async_commit();
+      if (kb >= LAG) {
+        cp_async_wait<LAG>();
+        fence_proxy_async();
+        mbar_arrive(s.full + 8 * ((kb - LAG) % STAGES));
+      }
+    }
+    cp_async_wait<0>();
+    fence_proxy_async();
+    for (int kb = (nk > LAG ? nk - LAG : 0); kb < nk; ++kb) mbar_arrive(s.full + 8 * (kb % STAGES));
+  } else if (warp == 5) {
+    if (lane == 0) {
+      // ---- TMA producer: da0 [rows, 256] MN-major atoms (EPB hidden x BK rows)
+      prefetch_tmap(&tmA);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int st = kb % STAGES, it = kb / STAGES;
+        mbar_wait(s.empty + 8 * st, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(s.full + 8 * st, OPB);
+        const uint32_t a = s.base + st * STAGE_BYTES;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int j = 0; j < NA; ++j)
+            tma_load_2d(a + h * 16384 + j * (BK * 128), &tmA, s.full + 8 * st, h * 128 + j * EPB, r0 + kb * BK);
+      }
+    }
+  } else {
+    if (lane == 0) {
+      const uint32_t idesc = instr_desc(KIND == 0 ? 2u : 1u, 128, 256, 1, 1);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int st = kb % STAGES, it = kb / STAGES;
+        mbar_wait(s.full + 8 * st, it & 1);
+        tc_fence_after();
+        const uint32_t a = s.base + st * STAGE_BYTES, b = a + OPB;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int k = 0; k < BK / KROWS; ++k)
+            mma<KIND>(tmem + h * 256, smem_desc(a + h * 16384 + k * KROWS * 128, BK * 128, 1024),
+                      smem_desc(b + k * KROWS * 128, BK * 128, 1024), idesc, (kb | k) != 0);
+        mma_commit(s.empty + 8 * st);
+      }
+      mma_commit(s.acc);
+    }
+  }
+  if (warp < 4) {
+    mbar_wait(s.acc, 0);
+    tc_fence_after();
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int hid = h * 128 + warp * 32 + lane;
+#pragma unroll 1
+      for (int cb = 0; cb < 8; ++cb) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + h * 256 + cb * 32, v);
+        float4* o = reinterpret_cast<float4*>(out + (int64_t)hid * d_raw + f0 + cb * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) tmem_dealloc(tmem, 512);
+}
+
+__global__ void k_sum_splits(const float* __restrict__ part, int nsplit, int64_t n, float* __restrict__ out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n / 4; j += (int64_t)gridDim.x * blockDim.x) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < nsplit; ++s) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(part + (int64_t)s * n) + j);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    reinterpret_cast<float4*>(out)[j] = acc;
+  }
+}
+
+__global__ void k_to_bf16(const float* __restrict__ in, const int32_t* __restrict__ count, int64_t row_width,
+                          int64_t n_max, __nv_bfloat16* __restrict__ out) {
+  int64_t n = n_max;
+  if (count) n = min(n, (int64_t)*count * row_width);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n / 2; i += (int64_t)gridDim.x * blockDim.x) {
+    const float2 v = reinterpret_cast<const float2*>(in)[i];
+    reinterpret_cast<__nv_bfloat162*>(out)[i] = __floats2bfloat162_rn(v.x, v.y);
+  }
+}
+
+// ---- host helpers -------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D row-major [rows, cols] map, box = [box_rows, 128 bytes], 128-B swizzle
+int make_map(CUtensorMap* m, const void* ptr, bool bf16, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(DICM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const uint32_t esz = bf16 ? 2 : 4;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * esz};
+  cuuint32_t box[2] = {128 / esz, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr),
+                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DICM_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return DICM_OK;
+}
+
+int nsplit_for(int64_t rows_max, int d_raw) {
+  const int tiles = d_raw / 256;
+  const int64_t want = (148 + tiles - 1) / tiles;  // ~one wave of CTAs
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (rows_max + 255) / 256));
+}
+
+struct TcWs {
+  __nv_bfloat16 *w0_bf16, *da0_bf16;
+  float* part;
+};
+
+size_t carve_ws(int64_t rows_max, int d_raw, TcWs* w, char* base) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* p = base ? base + off : nullptr;
+    off += (bytes + 1023) / 1024 * 1024;
+    return p;
+  };
+  TcWs t;
+  t.w0_bf16 = (__nv_bfloat16*)take((size_t)256 * d_raw * 2);
+  t.da0_bf16 = (__nv_bfloat16*)take((size_t)std::max<int64_t>(rows_max, 1) * 256 * 2);
+  t.part = (float*)take((size_t)nsplit_for(rows_max, d_raw) * 256 * d_raw * 4);
+  if (w) *w = t;
+  return off;
+}
+
+template <typename K>
+int set_smem(K kernel) {
+  return check_cuda(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES),
+                    "tcgen05 kernel smem attribute");
+}
+
+}  // namespace
+
+size_t workspace_bytes(int64_t rows_max, int d_raw) { return carve_ws(rows_max, d_raw, nullptr, nullptr); }
+
+int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows, const int32_t* count,
+               int64_t rows_max, const float* w0, const float* b0, float* act0, int precision, void* ws,
+               cudaStream_t st) {
+  const bool bf16 = precision == DICM_PREC_BF16;
+  if (bf16 != (pool_dtype == DICM_POOL_BF16))
+    return fail(DICM_ERR_VALUE, "precision %s needs a %s pool", bf16 ? "bf16" : "tf32", bf16 ? "bf16" : "fp32");
+  if (d_raw % 256) return fail(DICM_ERR_SHAPE, "tcgen05 layer 0: d_raw %d not a multiple of 256", d_raw);
+  TcWs w;
+  carve_ws(rows_max, d_raw, &w, (char*)ws);
+  CUtensorMap map;
+  int rc;
+  const void* wsrc = w0;
+  if (bf16) {
+    k_to_bf16<<<dicm_grid(256 * d_raw / 2, 256, 148 * 4), 256, 0, st>>>(w0, nullptr, 0, (int64_t)256 * d_raw,
+                                                                          w.w0_bf16);
+    wsrc = w.w0_bf16;
+  }
+  if ((rc = make_map(&map, wsrc, bf16, 256, d_raw, 256))) return rc;
+  const int grid = (int)((rows_max + 255) / 256);
+  if (bf16) {
+    static int once = set_smem(k_fwd<1>);
+    if (once) return once;
+    k_fwd<1><<<grid, THREADS, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, b0, act0);
+  } else {
+    static int once = set_smem(k_fwd<0>);
+    if (once) return once;
+    k_fwd<0><<<grid, THREADS, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, b0, act0);
+  }
+  return last_launch("tcgen05 layer-0 forward");
+}
+
+int bwd_dw0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows, const int32_t* count,
+            int64_t rows_max, const float* da0, float* gw0, int precision, void* ws, cudaStream_t st) {
+  const bool bf16 = precision == DICM_PREC_BF16;
+  if (bf16 != (pool_dtype == DICM_POOL_BF16))
+    return fail(DICM_ERR_VALUE, "precision %s needs a %s pool", bf16 ? "bf16" : "tf32", bf16 ? "bf16" : "fp32");
+  if (d_raw % 256) return fail(DICM_ERR_SHAPE, "tcgen05 layer 0: d_raw %d not a multiple of 256", d_raw);
+  TcWs w;
+  carve_ws(rows_max, d_raw, &w, (char*)ws);
+  const void* asrc = da0;
+  if (bf16) {
+    k_to_bf16<<<dicm_grid(rows_max * 128, 256, 148 * 8), 256, 0, st>>>(da0, count, 256, rows_max * 256, w.da0_bf16);
+    asrc = w.da0_bf16;
+  }
+  CUtensorMap map;
+  int rc;
+  const uint32_t box_rows = bf16 ? 64 : 32;
+  if ((rc = make_map(&map, asrc, bf16, (uint64_t)rows_max, 256, box_rows))) return rc;
+  const int nsplit = nsplit_for(rows_max, d_raw);
+  dim3 grid(d_raw / 256, nsplit);
+  if (bf16) {
+    static int once = set_smem(k_dw0<1>);
+    if (once) return once;
+    k_dw0<1><<<grid, THREADS, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, w.part);
+  } else {
+    static int once = set_smem(k_dw0<0>);
+    if (once) return once;
+    k_dw0<0><<<grid, THREADS, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, w.part);
+  }
+  const int64_t n = (int64_t)256 * d_raw;
+  k_sum_splits<<<dicm_grid(n / 4, 256, 148 * 8), 256, 0, st>>>(w.part, nsplit, n, gw0);
+  return last_launch("tcgen05 layer-0 backward");
 }
 
 }  // namespace sm100

@@ -236,7 +236,10 @@ class StepEngine:
         self.loss_part = torch.empty(L.lib.dicm_head_blocks(max(B, 1)), **f32)
         self.attn_partial = torch.empty((L.lib.dicm_sample_blocks(max(B, 1)), max(self.attn_part, 1)), **f32)
         self.loss = torch.zeros(1, **f32)
-        self.mlp_ws = _u8(L.lib.dicm_imgmlp_workspace(self.cap_u, self.pool.d_raw, self.prec_code), dev)
+        # zeroed once: rows past the live count are read (and multiplied by
+        # zero-filled gathers) by the tensor-core backward, so they must be finite
+        self.mlp_ws = torch.zeros(max(int(L.lib.dicm_imgmlp_workspace(self.cap_u, self.pool.d_raw, self.prec_code)),
+                                      1), dtype=torch.uint8, device=dev)
         self.cap = need
 
     def _pinned_buf(self, n):

@@ -1,0 +1,110 @@
+"""tcgen05 layer-0 kernels (tf32 on an fp32 pool, bf16 on a bf16 pool)
+against the CUDA-core fp32 kernels and the oracle.
+
+Tolerances: tensor-core layer 0 rounds its operands (tf32: 10-bit mantissa,
+bf16: 7-bit), so act0 / dW0 are compared against fp32 relative to the
+magnitude of the result (tf32 3e-3, bf16 2e-2), and end-to-end logits against
+the f64 oracle at the north star's 2e-2 (|a-b| / max(1,|a|,|b|))."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import gpu_helpers as H
+from oracle import dicm_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _mlp_io(U, P, seed=0, dtype="fp32"):
+    from paper_1711_06505_b200 import _lib as L
+    from paper_1711_06505_b200.pool import ImagePool
+    rng = np.random.default_rng(seed)
+    pool = ImagePool.synthetic(P, seed=seed, dtype=dtype)
+    rows = np.sort(rng.choice(P, size=U, replace=False)).astype(np.int32)
+    dev = "cuda"
+    p = {k: torch.as_tensor(v, dtype=torch.float32, device=dev) for k, v in {
+        "w0": rng.normal(0, np.sqrt(2 / 4096), (256, 4096)), "b0": rng.normal(0, 0.1, 256),
+        "a0": np.full(256, 0.25), "w1": rng.normal(0, np.sqrt(2 / 256), (64, 256)), "b1": np.zeros(64),
+        "a1": np.full(64, 0.25), "w2": rng.normal(0, np.sqrt(2 / 64), (12, 64)), "b2": np.zeros(12)}.items()}
+    cap = U + 300  # capacity larger than the live count
+    rt = torch.zeros(cap, dtype=torch.int32, device=dev)
+    rt[:U] = torch.as_tensor(rows, device=dev)
+    cnt = torch.tensor([U], dtype=torch.int32, device=dev)
+    return L, pool, rows, p, rt, cnt, cap
+
+
+def _fwd(L, pool, p, rt, cnt, cap, prec):
+    dev = "cuda"
+    act0 = torch.zeros((cap, 256), device=dev)
+    act1 = torch.zeros((cap, 64), device=dev)
+    emb = torch.zeros((cap, 12), device=dev)
+    ws = torch.zeros(L.lib.dicm_imgmlp_workspace(cap, 4096, prec), dtype=torch.uint8, device=dev)
+    prm = L.ImgMlpParams(**{k: v.data_ptr() for k, v in p.items()})
+    L.check(L.lib.dicm_imgmlp_fwd(pool.rows.data_ptr(), pool.dtype_code, 4096, rt.data_ptr(), cnt.data_ptr(), cap,
+                                  C.byref(prm), act0.data_ptr(), act1.data_ptr(), emb.data_ptr(), prec, ws.data_ptr(),
+                                  ws.numel(), L.stream_handle()))
+    return act0, act1, emb, ws, prm
+
+
+def _bwd(L, pool, p, rt, cnt, cap, prec, act0, act1, demb, ws, prm):
+    g = {k: torch.zeros_like(v) for k, v in p.items()}
+    gs = L.ImgMlpGrads(**{k: v.data_ptr() for k, v in g.items()})
+    L.check(L.lib.dicm_imgmlp_bwd(pool.rows.data_ptr(), pool.dtype_code, 4096, rt.data_ptr(), cnt.data_ptr(), cap,
+                                  C.byref(prm), act0.data_ptr(), act1.data_ptr(), demb.data_ptr(), C.byref(gs), prec,
+                                  ws.data_ptr(), ws.numel(), L.stream_handle()))
+    torch.cuda.synchronize()
+    return g
+
+
+def _relmax(a, b):
+    a, b = a.double().cpu().numpy(), b.double().cpu().numpy()
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+@pytest.mark.parametrize("U", [1, 255, 256, 257, 3000])
+@pytest.mark.parametrize("prec,tol", [("tf32", 3e-3), ("bf16", 2e-2)])
+def test_layer0_tensorcore_matches_fp32(U, prec, tol):
+    from paper_1711_06505_b200 import _lib as L0
+    pdt = "bf16" if prec == "bf16" else "fp32"
+    L, pool, rows, p, rt, cnt, cap = _mlp_io(U, 6000, seed=U, dtype=pdt)
+    ref = _fwd(L, pool, p, rt, cnt, cap, L0.PREC_FP32)
+    got = _fwd(L, pool, p, rt, cnt, cap, L0.PRECISIONS[prec])
+    torch.cuda.synchronize()
+    assert _relmax(got[0][:U], ref[0][:U]) < tol          # act0
+    assert torch.count_nonzero(got[0][U:]) == 0            # rows past the count untouched
+    demb = torch.randn((cap, 12), device="cuda") * 1e-2
+    gr = _bwd(L, pool, p, rt, cnt, cap, L0.PREC_FP32, ref[0], ref[1], demb, ref[3], ref[4])
+    gg = _bwd(L, pool, p, rt, cnt, cap, L0.PRECISIONS[prec], ref[0], ref[1], demb, got[3], got[4])
+    assert _relmax(gg["w0"], gr["w0"]) < tol
+    for k in ("b0", "a0", "w1", "b1", "a1", "w2", "b2"):  # fp32 layers agree tightly
+        assert _relmax(gg[k], gr[k]) < 1e-5, k
+
+
+@pytest.mark.parametrize("kind", ["sum", "attn", "multiquery-attn"])
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+def test_step_logits_within_north_star_tolerance(kind, prec):
+    """End to end: tensor-core layer 0 keeps logits within 2e-2 of the f64
+    oracle and gradients within 1e-4 (metric floors at 1)."""
+    from paper_1711_06505_b200.batch import synthetic_batch
+    from paper_1711_06505_b200.engine import StepEngine
+    from paper_1711_06505_b200.model import DicmModel
+    from paper_1711_06505_b200.pool import ImagePool
+    from paper_1711_06505_b200.schema import AggregatorSpec, default_schema
+    P = 3000
+    schema = default_schema(20000, 4, 20000, 8, P, b_max=50)
+    model = DicmModel(schema, AggregatorSpec(kind), None, seed=0)
+    pool = ImagePool.synthetic(P, seed=3, dtype="bf16" if prec == "bf16" else "fp32")
+    batch = synthetic_batch(np.random.default_rng(4), schema, 256, 50, P)
+    params = H.host_params(model)
+    e = StepEngine(model, pool, prec)
+    loss = e.forward_backward(e.upload(batch))
+    torch.cuda.synchronize()
+    e.raise_status()
+    out = O.forward_backward(params, H.oracle_cfg_of(model), H.oracle_batch(batch), pool.rows.double().cpu().numpy())
+    assert O.rel_err(e.logits[:batch.size].cpu().numpy(), out["logits"]) < 2e-2
+    assert O.rel_err(loss.item(), out["loss"]) < 2e-2
+    for n, g in H.dense_grads(e).items():
+        assert O.rel_err(g, out["grads"][n]) < 1e-4, n
