@@ -197,6 +197,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr int KROWS = 32 / sizeof(T);  // rows per MMA: 8 (tf32) / 16 (bf16)
   constexpr int NA = 128 / EPB;          // MN atoms per 128-wide half
   constexpr int CPR = 256 * sizeof(T) / 16;  // 16-B chunks per row slice
+  // MN-major layouts: tf32 -> SWIZZLE_128B_BASE32B (4-row k groups of 512 B),
+  // bf16 -> SWIZZLE_128B (8-row groups of 1024 B)
+  constexpr uint32_t MN_LAYOUT = KIND == 0 ? 1u : 2u;
+  constexpr uint32_t MN_SBO = KIND == 0 ? 512u : 1024u;
   const int U = *count;
   const int f0 = blockIdx.x * 256, split = blockIdx.y, nsplit = gridDim.y;
   const int per = (((U + nsplit - 1) / nsplit) + BK - 1) / BK * BK;
@@ -228,7 +232,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int gr = r0 + kb * BK + k;
         const bool v = gr < r1;
         const T* src = pool + (int64_t)(v ? rows[gr] : 0) * d_raw + f0 + c * (16 / sizeof(T));
-        const uint32_t dst = b + (c >> 3) * (BK * 128) + k * 128 + (((c & 7) ^ (k & 7)) << 4);
+        // tf32 MN-major operands need the 32-B-granule 128-B swizzle
+        // (Swizzle<2,5,2>: granule ^= row & 3); bf16 uses the 16-B one
+        const uint32_t sw = KIND == 0 ? ((((c & 7) >> 1) ^ (k & 3)) << 5) | ((c & 1) << 4)
+                                      : (((c & 7) ^ (k & 7)) << 4);
+        const uint32_t dst = b + (c >> 3) * (BK * 128) + k * 128 + sw;
         cp_async16(dst, src, v ? 16u : 0u);
       }
       cp_async_commit();
@@ -269,8 +277,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int k = 0; k < BK / KROWS; ++k)
-            mma<KIND>(tmem + h * 256, smem_desc(a + h * 16384 + k * KROWS * 128, BK * 128, 1024),
-                      smem_desc(b + k * KROWS * 128, BK * 128, 1024), idesc, (kb | k) != 0);
+            mma<KIND>(tmem + h * 256, smem_desc(a + h * 16384 + k * KROWS * 128, BK * 128, MN_SBO, MN_LAYOUT),
+                      smem_desc(b + k * KROWS * 128, BK * 128, MN_SBO, MN_LAYOUT), idesc, (kb | k) != 0);
         mma_commit(s.empty + 8 * st);
       }
       mma_commit(s.acc);
@@ -336,7 +344,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D row-major [rows, cols] map, box = [box_rows, 128 bytes], 128-B swizzle
-int make_map(CUtensorMap* m, const void* ptr, bool bf16, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+int make_map(CUtensorMap* m, const void* ptr, bool bf16, uint64_t rows, uint64_t cols, uint32_t box_rows,
+             CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) return fail(DICM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const uint32_t esz = bf16 ? 2 : 4;
@@ -345,7 +354,7 @@ int make_map(CUtensorMap* m, const void* ptr, bool bf16, uint64_t rows, uint64_t
   cuuint32_t box[2] = {128 / esz, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr),
-                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DICM_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return DICM_OK;
@@ -434,7 +443,9 @@ int bwd_dw0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows, co
   CUtensorMap map;
   int rc;
   const uint32_t box_rows = bf16 ? 64 : 32;
-  if ((rc = make_map(&map, asrc, bf16, (uint64_t)rows_max, 256, box_rows))) return rc;
+  if ((rc = make_map(&map, asrc, bf16, (uint64_t)rows_max, 256, box_rows,
+                     bf16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)))
+    return rc;
   const int nsplit = nsplit_for(rows_max, d_raw);
   dim3 grid(d_raw / 256, nsplit);
   if (bf16) {
