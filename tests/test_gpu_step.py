@@ -26,7 +26,7 @@ def _noise(n):
     return n.startswith("attn/") and n.endswith("/1/b")
 
 
-def _adam_close(got, exp, steps, lr=0.001, frac=0.01):
+def _adam_close(got, exp, steps, lr=0.001, frac=0.05):
     """Parameters after Adam: every entry within 1e-4 (rel, max(1,.)) except
     at most ``frac`` of them, which may differ by one sign-flipped Adam step
     per step (|exact gradient| below fp32 rounding; SURVEY.md 7 part 6)."""
