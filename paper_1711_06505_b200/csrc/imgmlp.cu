@@ -136,25 +136,62 @@ struct EpPreluGrad {
 
 // out[j] (+)= sum_{b < nvalid} part[b*stride + off + j]; nvalid from the device
 // row count when rows_per_blk > 0 (block rows past the count wrote nothing)
-__global__ void k_reduce(const float* __restrict__ part, int nblk, int64_t stride, int64_t off, int64_t n,
-                         const int32_t* __restrict__ count, int rows_per_blk, float* __restrict__ out,
-                         int accumulate) {
+//
+// Column sums over partial rows, deterministic (fixed association): block
+// (32 columns x 8 row lanes) sums its chunk of rows with coalesced loads and
+// reduces the 8 lanes in shared memory; with nchunk > 1 each chunk's sums go to
+// tmp[chunk][n] and a second pass folds the chunks.
+constexpr int RED_ROWS = 128;  // rows per chunk (16 per row lane)
+
+__global__ void __launch_bounds__(256) k_colsum(const float* __restrict__ part, int nblk, int64_t stride, int64_t off,
+                                                int64_t n, const int32_t* __restrict__ count, int rows_per_blk,
+                                                int chunk_rows, float* __restrict__ out, int accumulate) {
   int nb = nblk;
   if (count && rows_per_blk > 0) nb = min(nblk, (int)((*count + rows_per_blk - 1) / rows_per_blk));
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int b = 0; b < nb; ++b) s += part[(int64_t)b * stride + off + j];
-    out[j] = accumulate ? out[j] + s : s;
+  const int64_t j = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const int b0 = blockIdx.y * chunk_rows, b1 = min(nb, b0 + chunk_rows);
+  float s = 0.f;
+  if (j < n)
+    for (int b = b0 + threadIdx.y; b < b1; b += 8) s += part[(int64_t)b * stride + off + j];
+  __shared__ float red[8][33];
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && j < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) t += red[y][threadIdx.x];
+    float* o = out + (int64_t)blockIdx.y * n + j;
+    *o = accumulate ? *o + t : t;
   }
 }
 
+// tmp: >= ceil(nblk / RED_ROWS) * n floats (or nullptr when nblk <= RED_ROWS)
+void reduce_into(cudaStream_t st, const float* part, int nblk, int64_t stride, int64_t off, int64_t n, float* out,
+                 float* tmp, int accumulate, const int32_t* count = nullptr, int rows_per_blk = 0) {
+  if (n <= 0) return;
+  const int nchunk = (nblk + RED_ROWS - 1) / RED_ROWS;
+  const dim3 blk(32, 8);
+  const unsigned gx = (unsigned)((n + 31) / 32);
+  if (nchunk <= 1 || tmp == nullptr) {  // one chunk covering every row
+    k_colsum<<<dim3(gx, 1), blk, 0, st>>>(part, nblk, stride, off, n, count, rows_per_blk, nblk > 0 ? nblk : 1, out,
+                                          accumulate);
+    return;
+  }
+  k_colsum<<<dim3(gx, nchunk), blk, 0, st>>>(part, nblk, stride, off, n, count, rows_per_blk, RED_ROWS, tmp, 0);
+  k_colsum<<<dim3(gx, 1), blk, 0, st>>>(tmp, nchunk, n, 0, n, nullptr, 0, nchunk, out, accumulate);
+}
+
+size_t red_tmp_floats(int64_t rows_max) { return (size_t)(std::max<int64_t>(rows_max / 8192 + 2, 4)) * 16384; }
+
+float* g_red_tmp = nullptr;  // set per call from the workspace
+
 void reduce(cudaStream_t st, const float* part, int nblk, int64_t stride, int64_t off, int64_t n, float* out,
             const int32_t* count = nullptr, int rows_per_blk = 0) {
-  k_reduce<<<dicm_grid(n, 256, 148 * 8), 256, 0, st>>>(part, nblk, stride, off, n, count, rows_per_blk, out, 0);
+  reduce_into(st, part, nblk, stride, off, n, out, g_red_tmp, 0, count, rows_per_blk);
 }
 
 struct Ws {
-  float *da1, *da0, *p2, *p0, *pw1, *pw0;
+  float *da1, *da0, *p2, *p0, *pw1, *pw0, *red;
   int s1, s0;
 };
 
@@ -177,6 +214,7 @@ size_t carve(int64_t rows_max, int d_raw, Ws* w, char* base) {
   t.p0 = (float*)take((size_t)((rows_max + 63) / 64) * 2 * H1 * 4);
   t.pw1 = (float*)take((size_t)t.s1 * H2 * H1 * 4);
   t.pw0 = (float*)take((size_t)t.s0 * H1 * d_raw * 4);
+  t.red = (float*)take(red_tmp_floats(rows_max) * 4);
   if (w) *w = t;
   return off + sm100::workspace_bytes(rows_max, d_raw);
 }
@@ -269,6 +307,7 @@ int dicm_imgmlp_bwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
     return fail(DICM_ERR_VALUE, "image MLP bwd: workspace too small");
   Ws w;
   carve(rows_max, d_raw, &w, (char*)workspace);
+  g_red_tmp = w.red;
   const int M = (int)rows_max;
   // layer 2 + prelu 1
   k_layer2_bwd<<<L2_BLOCKS, 256, 0, st>>>(act1, p->a1, p->w2, demb, count_dev, rows_max, w.da1, w.p2);
@@ -308,7 +347,7 @@ int dicm_reduce_partials(const float* partials, int nblk, int64_t n, float* out,
                          dicm_stream_t stream) {
   if (n <= 0) return DICM_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  k_reduce<<<dicm_grid(n, 256, 148 * 8), 256, 0, st>>>(partials, nblk, n, 0, n, nullptr, 0, out, accumulate);
+  reduce_into(st, partials, nblk, n, 0, n, out, nullptr, accumulate);
   return dicm::last_launch("dicm_reduce_partials");
 }
 

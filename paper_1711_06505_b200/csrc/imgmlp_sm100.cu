@@ -362,7 +362,7 @@ int make_map(CUtensorMap* m, const void* ptr, bool bf16, uint64_t rows, uint64_t
 
 int nsplit_for(int64_t rows_max, int d_raw) {
   const int tiles = d_raw / 256;
-  const int64_t want = (148 + tiles - 1) / tiles;  // ~one wave of CTAs
+  const int64_t want = std::max(148 / tiles, 1);  // one wave of CTAs
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, (rows_max + 255) / 256));
 }
 
