@@ -7,14 +7,18 @@
 // Both kernels keep a 256 x 256 fp32 accumulator tile in TMEM (two M=128
 // halves, all 512 columns) fed by a 3-stage shared-memory ring:
 //   * the dense operand (W0 forward, da0 backward) arrives by TMA tile loads
-//     (SWIZZLE_128B) signalled through mbarrier transaction counts;
+//     (128-B swizzle) signalled through mbarrier transaction counts;
 //   * the gathered operand -- pool rows picked by the dedup's unique ids --
 //     arrives by 16-byte cp.async (LDGSTS) gathers written straight into the
-//     same 128-byte-swizzled layout, so no gathered copy of X is ever formed;
+//     same swizzled layout (no gathered copy of X is ever formed); each
+//     gather thread signals the stage with cp.async.mbarrier.arrive, so the
+//     producers never block on their own loads;
 //   * one elected thread issues tcgen05.mma (kind::tf32 on an fp32 pool,
-//     kind::f16 on a bf16 pool) and releases each stage with tcgen05.commit;
-//   * four warps drain TMEM with tcgen05.ld and apply the epilogue.
-// Forward tiles are 256 rows; the backward reduction over rows is split into
+//     kind::f16 on a bf16 pool) and releases stages with tcgen05.commit;
+//   * tcgen05.ld drains TMEM in the epilogue.
+// The forward kernel is persistent (one CTA per SM looping over 256-row
+// tiles) with dedicated epilogue warps, so the gather of tile i+1 overlaps
+// the drain of tile i.  The backward reduction over rows is split into
 // nsplit chunks per 256-feature tile and finished by a deterministic reduce.
 #include <cudaTypedefs.h>
 
@@ -30,17 +34,18 @@ namespace {
 using namespace tc;
 
 constexpr int STAGES = 3;
-constexpr int LAG = STAGES - 1;  // cp.async groups kept in flight per producer thread
 constexpr uint32_t OPB = 256 * 128;  // bytes per operand per stage (256 x 128 B)
 constexpr uint32_t STAGE_BYTES = 2 * OPB;
 constexpr size_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int THREADS = 192;  // warps 0-3 producers+epilogue, 4 MMA, 5 TMA
+constexpr int THREADS_F = 320;  // fwd: warps 0-3 gather, 4 MMA, 5 TMA, 6-9 epilogue
+constexpr int THREADS_B = 192;  // bwd: warps 0-3 gather + epilogue, 4 MMA, 5 TMA
+constexpr unsigned FULL = 0xffffffffu;
 
 template <int KIND>
 using Elem = typename std::conditional<KIND == 0, float, __nv_bfloat16>::type;
 
 struct Smem {
-  uint32_t base, full, empty, acc, slot;
+  uint32_t base, full, empty, acc_full, acc_empty, slot;
   uint32_t* slot_ptr;
 };
 
@@ -50,19 +55,21 @@ __device__ __forceinline__ Smem carve(uint8_t* raw) {
   s.base = (r + 1023u) & ~1023u;
   s.full = s.base + STAGES * STAGE_BYTES;
   s.empty = s.full + 8 * STAGES;
-  s.acc = s.empty + 8 * STAGES;
-  s.slot = s.acc + 8;
+  s.acc_full = s.empty + 8 * STAGES;
+  s.acc_empty = s.acc_full + 8;
+  s.slot = s.acc_empty + 8;
   s.slot_ptr = reinterpret_cast<uint32_t*>(raw + (s.slot - r));
   return s;
 }
 
-__device__ __forceinline__ uint32_t setup(const Smem& s, int warp) {
+__device__ __forceinline__ uint32_t setup(const Smem& s, int warp, uint32_t acc_empty_count) {
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
-      mbar_init(s.full + 8 * i, 128 + 1);  // 128 gather threads + the TMA thread's expect_tx
+      mbar_init(s.full + 8 * i, 128 + 1);  // 128 gather threads (cp.async arrive) + TMA expect_tx
       mbar_init(s.empty + 8 * i, 1);       // tcgen05.commit
     }
-    mbar_init(s.acc, 1);
+    mbar_init(s.acc_full, 1);
+    mbar_init(s.acc_empty, acc_empty_count);
     fence_mbar_init();
   }
   if (warp == 4) {
@@ -75,107 +82,121 @@ __device__ __forceinline__ uint32_t setup(const Smem& s, int warp) {
   return *reinterpret_cast<volatile uint32_t*>(s.slot_ptr);
 }
 
+__device__ __forceinline__ void wait_stage(uint32_t bar, uint32_t g, bool producer) {
+  const uint32_t it = g / STAGES;
+  mbar_wait(bar + 8 * (g % STAGES), producer ? ((it & 1) ^ 1) : (it & 1));
+}
+
 // ---------------------------------------------------------------------------
-// forward: act0 = X[rows] W0^T + b0, one CTA per 256 rows
+// forward: act0 = X[rows] W0^T + b0, persistent over 256-row tiles
 // ---------------------------------------------------------------------------
 template <int KIND>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS_F, 1)
     k_fwd(const __grid_constant__ CUtensorMap tmW, const void* __restrict__ pool_, int d_raw,
           const int32_t* __restrict__ rows, const int32_t* __restrict__ count, const float* __restrict__ bias,
           float* __restrict__ act0) {
   using T = Elem<KIND>;
   constexpr int EPB = 128 / sizeof(T);  // elements per 128-byte row slice
   const int U = *count;
-  const int m0 = blockIdx.x * 256;
-  if (m0 >= U) return;
+  const int ntiles = (U + 255) / 256;
+  if ((int)blockIdx.x >= ntiles) return;
   extern __shared__ uint8_t smem_raw[];
   const Smem s = carve(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t tmem = setup(s, warp);
+  const uint32_t tmem = setup(s, warp, 128);
   const int nk = d_raw / EPB;
   const T* pool = reinterpret_cast<const T*>(pool_);
 
   if (warp < 4) {
     // ---- gather producer: 16 rows x one 16-B chunk per thread and stage
     const int t = threadIdx.x, c = t & 7, rb = t >> 3;
-    const T* src[16];
-    uint32_t ok[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int gr = m0 + rb + 16 * i;
-      const bool v = gr < U;
-      src[i] = pool + (int64_t)(v ? rows[gr] : 0) * d_raw + c * (16 / sizeof(T));
-      ok[i] = v ? 16u : 0u;
-    }
     const uint32_t dst0 = (uint32_t)(rb * 128 + ((c ^ (rb & 7)) << 4));  // (rb + 16 i) & 7 == rb & 7
-    for (int kb = 0; kb < nk; ++kb) {
-      const int st = kb % STAGES, it = kb / STAGES;
-      mbar_wait(s.empty + 8 * st, (it & 1) ^ 1);
-      const uint32_t a = s.base + st * STAGE_BYTES + dst0;
+    uint32_t g = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int m0 = tile * 256;
+      const T* src[16];
+      uint32_t ok[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) cp_async16(a + i * 16 * 128, src[i] + (int64_t)kb * EPB, ok[i]);
-      cp_async_commit();
-      if (kb >= LAG) {
-        cp_async_wait<LAG>();
-        fence_proxy_async();
-        mbar_arrive(s.full + 8 * ((kb - LAG) % STAGES));
+      for (int i = 0; i < 16; ++i) {
+        const int gr = m0 + rb + 16 * i;
+        const bool v = gr < U;
+        src[i] = pool + (int64_t)(v ? __ldg(rows + gr) : 0) * d_raw + c * (16 / sizeof(T));
+        ok[i] = v ? 16u : 0u;
+      }
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        wait_stage(s.empty, g, true);
+        const uint32_t a = s.base + (g % STAGES) * STAGE_BYTES + dst0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) cp_async16(a + i * 16 * 128, src[i] + (int64_t)kb * EPB, ok[i]);
+        cp_async_arrive_noinc(s.full + 8 * (g % STAGES));
       }
     }
     cp_async_wait<0>();
-    fence_proxy_async();
-    for (int kb = (nk > LAG ? nk - LAG : 0); kb < nk; ++kb) mbar_arrive(s.full + 8 * (kb % STAGES));
   } else if (warp == 5) {
     if (lane == 0) {
       // ---- TMA producer for W0 [256, d_raw] (K-major, 128-B swizzle)
       prefetch_tmap(&tmW);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int st = kb % STAGES, it = kb / STAGES;
-        mbar_wait(s.empty + 8 * st, (it & 1) ^ 1);
-        mbar_arrive_expect_tx(s.full + 8 * st, OPB);
-        tma_load_2d(s.base + st * STAGE_BYTES + OPB, &tmW, s.full + 8 * st, kb * EPB, 0);
-      }
+      uint32_t g = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          wait_stage(s.empty, g, true);
+          const uint32_t st = g % STAGES;
+          mbar_arrive_expect_tx(s.full + 8 * st, OPB);
+          tma_load_2d(s.base + st * STAGE_BYTES + OPB, &tmW, s.full + 8 * st, kb * EPB, 0);
+        }
     }
-  } else {
+  } else if (warp == 4) {
     if (lane == 0) {
       // ---- MMA issuer: 2 halves (rows 0-127, 128-255) x 4 k-steps of 32 B
       const uint32_t idesc = instr_desc(KIND == 0 ? 2u : 1u, 128, 256, 0, 0);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int st = kb % STAGES, it = kb / STAGES;
-        mbar_wait(s.full + 8 * st, it & 1);
+      uint32_t g = 0, tl = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
+        mbar_wait(s.acc_empty, (tl & 1) ^ 1);  // epilogue drained the previous tile
         tc_fence_after();
-        const uint32_t a = s.base + st * STAGE_BYTES, b = a + OPB;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          wait_stage(s.full, g, false);
+          tc_fence_after();
+          fence_proxy_async();
+          const uint32_t a = s.base + (g % STAGES) * STAGE_BYTES, b = a + OPB;
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+          for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            mma<KIND>(tmem + h * 256, smem_desc(a + h * 16384 + k * 32, 16, 1024), smem_desc(b + k * 32, 16, 1024),
-                      idesc, (kb | k) != 0);
-        mma_commit(s.empty + 8 * st);
+            for (int k = 0; k < 4; ++k)
+              mma<KIND>(tmem + h * 256, smem_desc(a + h * 16384 + k * 32, 16, 1024), smem_desc(b + k * 32, 16, 1024),
+                        idesc, (kb | k) != 0);
+          mma_commit(s.empty + 8 * (g % STAGES));
+        }
+        mma_commit(s.acc_full);
       }
-      mma_commit(s.acc);
     }
-  }
-  // ---- epilogue: TMEM -> registers (+ bias) -> act0
-  if (warp < 4) {
-    mbar_wait(s.acc, 0);
-    tc_fence_after();
+  } else {
+    // ---- epilogue warps 6-9: TMEM lane quarter = warp % 4
+    const int q = warp & 3;
+    uint32_t tl = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
+      mbar_wait(s.acc_full, tl & 1);
+      tc_fence_after();
+      const int m0 = tile * 256;
 #pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-      const int row = m0 + h * 128 + warp * 32 + lane;
+      for (int h = 0; h < 2; ++h) {
+        const int row = m0 + h * 128 + q * 32 + lane;
 #pragma unroll 1
-      for (int cb = 0; cb < 8; ++cb) {
-        float v[32];
-        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + h * 256 + cb * 32, v);
-        if (row < U) {
-          float4* out = reinterpret_cast<float4*>(act0 + (int64_t)row * 256 + cb * 32);
-          const float4* bb = reinterpret_cast<const float4*>(bias + cb * 32);
+        for (int cb = 0; cb < 8; ++cb) {
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + h * 256 + cb * 32, v);
+          if (row < U) {
+            float4* out = reinterpret_cast<float4*>(act0 + (int64_t)row * 256 + cb * 32);
+            const float4* bb = reinterpret_cast<const float4*>(bias + cb * 32);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 b4 = __ldg(bb + q);
-            out[q] = make_float4(v[4 * q] + b4.x, v[4 * q + 1] + b4.y, v[4 * q + 2] + b4.z, v[4 * q + 3] + b4.w);
+            for (int j = 0; j < 8; ++j) {
+              const float4 b4 = __ldg(bb + j);
+              out[j] = make_float4(v[4 * j] + b4.x, v[4 * j + 1] + b4.y, v[4 * j + 2] + b4.z, v[4 * j + 3] + b4.w);
+            }
           }
         }
       }
+      tc_fence_before();
+      mbar_arrive(s.acc_empty);
     }
   }
   tc_fence_before();
@@ -188,7 +209,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 // grid = (d_raw/256 feature tiles, nsplit row chunks)
 // ---------------------------------------------------------------------------
 template <int KIND>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS_B, 1)
     k_dw0(const __grid_constant__ CUtensorMap tmA, const void* __restrict__ pool_, int d_raw,
           const int32_t* __restrict__ rows, const int32_t* __restrict__ count, float* __restrict__ part) {
   using T = Elem<KIND>;
@@ -197,6 +218,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr int KROWS = 32 / sizeof(T);  // rows per MMA: 8 (tf32) / 16 (bf16)
   constexpr int NA = 128 / EPB;          // MN atoms per 128-wide half
   constexpr int CPR = 256 * sizeof(T) / 16;  // 16-B chunks per row slice
+  constexpr int RPI = 128 / CPR;             // rows covered per gather round
   // MN-major layouts: tf32 -> SWIZZLE_128B_BASE32B (4-row k groups of 512 B),
   // bf16 -> SWIZZLE_128B (8-row groups of 1024 B)
   constexpr uint32_t MN_LAYOUT = KIND == 0 ? 1u : 2u;
@@ -210,52 +232,51 @@ __global__ void __launch_bounds__(THREADS, 1)
   float* out = part + (int64_t)split * 256 * d_raw;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (nk == 0) {  // empty chunk: its partial is zero
-    for (int i = threadIdx.x; i < 256 * 256; i += THREADS) out[(int64_t)(i >> 8) * d_raw + f0 + (i & 255)] = 0.f;
+    for (int i = threadIdx.x; i < 256 * 256; i += THREADS_B) out[(int64_t)(i >> 8) * d_raw + f0 + (i & 255)] = 0.f;
     return;
   }
   extern __shared__ uint8_t smem_raw[];
   const Smem s = carve(smem_raw);
-  const uint32_t tmem = setup(s, warp);
+  const uint32_t tmem = setup(s, warp, 1);
   const T* pool = reinterpret_cast<const T*>(pool_);
 
   if (warp < 4) {
-    // ---- gather producer: X[rows] feature slice [f0, f0+256) of BK rows
-    const int t = threadIdx.x;
+    // ---- gather producer: X[rows] feature slice [f0, f0+256) of BK rows.
+    // Thread t owns 16-B chunk c of rows kw + i*RPI (i < 16); lane i < 16 of
+    // the warp fetches row id i one stage ahead and the warp shuffles it.
+    const int t = threadIdx.x, c = t % CPR, kw = t / CPR;
+    const T* colbase = pool + f0 + c * (16 / sizeof(T));
+    const uint32_t atom_off = (c >> 3) * (BK * 128);
+    auto fetch = [&](int kb) {
+      const int gr = r0 + kb * BK + lane * RPI + kw;
+      return (lane < 16 && kb < nk && gr < r1) ? __ldg(rows + gr) : -1;
+    };
+    int rid_next = fetch(0);
     for (int kb = 0; kb < nk; ++kb) {
-      const int st = kb % STAGES, it = kb / STAGES;
-      mbar_wait(s.empty + 8 * st, (it & 1) ^ 1);
-      const uint32_t b = s.base + st * STAGE_BYTES + OPB;
-#pragma unroll 4
+      const int rid_cur = rid_next;
+      rid_next = fetch(kb + 1);
+      wait_stage(s.empty, kb, true);
+      const uint32_t b = s.base + (kb % STAGES) * STAGE_BYTES + OPB + atom_off;
+#pragma unroll
       for (int i = 0; i < 16; ++i) {
-        const int q = i * 128 + t;
-        const int k = q / CPR, c = q % CPR;
-        const int gr = r0 + kb * BK + k;
-        const bool v = gr < r1;
-        const T* src = pool + (int64_t)(v ? rows[gr] : 0) * d_raw + f0 + c * (16 / sizeof(T));
+        const int rid = __shfl_sync(FULL, rid_cur, i);
+        const int k = i * RPI + kw;
         // tf32 MN-major operands need the 32-B-granule 128-B swizzle
         // (Swizzle<2,5,2>: granule ^= row & 3); bf16 uses the 16-B one
         const uint32_t sw = KIND == 0 ? ((((c & 7) >> 1) ^ (k & 3)) << 5) | ((c & 1) << 4)
                                       : (((c & 7) ^ (k & 7)) << 4);
-        const uint32_t dst = b + (c >> 3) * (BK * 128) + k * 128 + sw;
-        cp_async16(dst, src, v ? 16u : 0u);
+        cp_async16(b + k * 128 + sw, colbase + (int64_t)(rid < 0 ? 0 : rid) * d_raw, rid < 0 ? 0u : 16u);
       }
-      cp_async_commit();
-      if (kb >= LAG) {
-        cp_async_wait<LAG>();
-        fence_proxy_async();
-        mbar_arrive(s.full + 8 * ((kb - LAG) % STAGES));
-      }
+      cp_async_arrive_noinc(s.full + 8 * (kb % STAGES));
     }
     cp_async_wait<0>();
-    fence_proxy_async();
-    for (int kb = (nk > LAG ? nk - LAG : 0); kb < nk; ++kb) mbar_arrive(s.full + 8 * (kb % STAGES));
   } else if (warp == 5) {
     if (lane == 0) {
       // ---- TMA producer: da0 [rows, 256] MN-major atoms (EPB hidden x BK rows)
       prefetch_tmap(&tmA);
       for (int kb = 0; kb < nk; ++kb) {
-        const int st = kb % STAGES, it = kb / STAGES;
-        mbar_wait(s.empty + 8 * st, (it & 1) ^ 1);
+        wait_stage(s.empty, kb, true);
+        const uint32_t st = kb % STAGES;
         mbar_arrive_expect_tx(s.full + 8 * st, OPB);
         const uint32_t a = s.base + st * STAGE_BYTES;
 #pragma unroll
@@ -269,23 +290,23 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       const uint32_t idesc = instr_desc(KIND == 0 ? 2u : 1u, 128, 256, 1, 1);
       for (int kb = 0; kb < nk; ++kb) {
-        const int st = kb % STAGES, it = kb / STAGES;
-        mbar_wait(s.full + 8 * st, it & 1);
+        wait_stage(s.full, kb, false);
         tc_fence_after();
-        const uint32_t a = s.base + st * STAGE_BYTES, b = a + OPB;
+        fence_proxy_async();
+        const uint32_t a = s.base + (kb % STAGES) * STAGE_BYTES, b = a + OPB;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int k = 0; k < BK / KROWS; ++k)
             mma<KIND>(tmem + h * 256, smem_desc(a + h * 16384 + k * KROWS * 128, BK * 128, MN_SBO, MN_LAYOUT),
                       smem_desc(b + k * KROWS * 128, BK * 128, MN_SBO, MN_LAYOUT), idesc, (kb | k) != 0);
-        mma_commit(s.empty + 8 * st);
+        mma_commit(s.empty + 8 * (kb % STAGES));
       }
-      mma_commit(s.acc);
+      mma_commit(s.acc_full);
     }
   }
   if (warp < 4) {
-    mbar_wait(s.acc, 0);
+    mbar_wait(s.acc_full, 0);
     tc_fence_after();
 #pragma unroll 1
     for (int h = 0; h < 2; ++h) {
@@ -414,15 +435,15 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
     wsrc = w.w0_bf16;
   }
   if ((rc = make_map(&map, wsrc, bf16, 256, d_raw, 256))) return rc;
-  const int grid = (int)((rows_max + 255) / 256);
+  const int grid = (int)std::min<int64_t>(148, (rows_max + 255) / 256);  // persistent: <= one CTA per SM
   if (bf16) {
     static int once = set_smem(k_fwd<1>);
     if (once) return once;
-    k_fwd<1><<<grid, THREADS, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, b0, act0);
+    k_fwd<1><<<grid, THREADS_F, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, b0, act0);
   } else {
     static int once = set_smem(k_fwd<0>);
     if (once) return once;
-    k_fwd<0><<<grid, THREADS, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, b0, act0);
+    k_fwd<0><<<grid, THREADS_F, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, b0, act0);
   }
   return last_launch("tcgen05 layer-0 forward");
 }
@@ -451,11 +472,11 @@ int bwd_dw0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows, co
   if (bf16) {
     static int once = set_smem(k_dw0<1>);
     if (once) return once;
-    k_dw0<1><<<grid, THREADS, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, w.part);
+    k_dw0<1><<<grid, THREADS_B, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, w.part);
   } else {
     static int once = set_smem(k_dw0<0>);
     if (once) return once;
-    k_dw0<0><<<grid, THREADS, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, w.part);
+    k_dw0<0><<<grid, THREADS_B, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, w.part);
   }
   const int64_t n = (int64_t)256 * d_raw;
   k_sum_splits<<<dicm_grid(n / 4, 256, 148 * 8), 256, 0, st>>>(w.part, nsplit, n, gw0);
