@@ -191,7 +191,7 @@ void reduce(cudaStream_t st, const float* part, int nblk, int64_t stride, int64_
 }
 
 struct Ws {
-  float *da1, *da0, *p2, *p0, *pw1, *pw0, *red;
+  float *da1, *da0, *p2, *p0, *pw1, *pw0, *red, *pl12, *pdw1;
   int s1, s0;
 };
 
@@ -215,6 +215,8 @@ size_t carve(int64_t rows_max, int d_raw, Ws* w, char* base) {
   t.pw1 = (float*)take((size_t)t.s1 * H2 * H1 * 4);
   t.pw0 = (float*)take((size_t)t.s0 * H1 * d_raw * 4);
   t.red = (float*)take(red_tmp_floats(rows_max) * 4);
+  t.pl12 = (float*)take((size_t)sm100::small_bwd_blocks(rows_max) * sm100::small_part_size() * 4);
+  t.pdw1 = (float*)take((size_t)sm100::small_dw1_blocks(rows_max) * H2 * H1 * 4);
   if (w) *w = t;
   return off + sm100::workspace_bytes(rows_max, d_raw);
 }
@@ -269,6 +271,10 @@ int dicm_imgmlp_fwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
     rc = sm100::fwd_layer0(pool, pool_dtype, d_raw, rows, count_dev, rows_max, p->w0, p->b0, act0, precision,
                            tc_ws, st);
     if (rc) return rc;
+    // layers 1-2 on tcgen05 (tf32) with the layer-2 epilogue fused
+    rc = sm100::fwd_layers12(act0, count_dev, rows_max, p->a0, p->w1, p->b1, p->a1, p->w2, p->b2, act1, emb, st);
+    if (rc) return rc;
+    return last_launch("dicm_imgmlp_fwd");
   }
   // layer 1: act1 = prelu(act0) W1^T + b1   (fp32, CUDA cores)
   gemm(st, LoadA_Rows<float>{act0, H1, nullptr, p->a0}, LoadB_WT{p->w1, H1}, EpBias{act1, H2, p->b1}, M, H2,
@@ -309,6 +315,27 @@ int dicm_imgmlp_bwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
   carve(rows_max, d_raw, &w, (char*)workspace);
   g_red_tmp = w.red;
   const int M = (int)rows_max;
+  if (precision != DICM_PREC_FP32) {
+    // tensor-core path: layers 2-1 fused on tcgen05, dW1 on tcgen05, then dW0
+    char* tc_ws = (char*)workspace + carve(rows_max, d_raw, nullptr, nullptr) - sm100::workspace_bytes(rows_max, d_raw);
+    const bool bf16 = precision == DICM_PREC_BF16;
+    __nv_bfloat16* da0_bf16 = bf16 ? sm100::da0_bf16_ptr(tc_ws, rows_max, d_raw) : nullptr;
+    rc = sm100::bwd_layers12(demb, act1, act0, count_dev, rows_max, p->a0, p->a1, p->w1, p->w2, w.da1, w.da0,
+                             da0_bf16, w.pl12, w.pdw1, st);
+    if (rc) return rc;
+    const int nb = sm100::small_bwd_blocks(rows_max), ps = sm100::small_part_size();
+    reduce(st, w.pl12, nb, ps, 0, DICM_D * H2, g->w2);
+    reduce(st, w.pl12, nb, ps, DICM_D * H2, DICM_D, g->b2);
+    reduce(st, w.pl12, nb, ps, DICM_D * H2 + DICM_D, H2, g->a1);
+    reduce(st, w.pl12, nb, ps, DICM_D * H2 + DICM_D + H2, H2, g->b1);
+    reduce(st, w.pl12, nb, ps, L2_PART, H1, g->a0);
+    reduce(st, w.pl12, nb, ps, L2_PART + H1, H1, g->b0);
+    reduce(st, w.pdw1, sm100::small_dw1_blocks(rows_max), (int64_t)H2 * H1, 0, (int64_t)H2 * H1, g->w1);
+    rc = sm100::bwd_dw0(pool, pool_dtype, d_raw, rows, count_dev, rows_max, w.da0, g->w0, precision, tc_ws, st,
+                        bf16);
+    if (rc) return rc;
+    return last_launch("dicm_imgmlp_bwd");
+  }
   // layer 2 + prelu 1
   k_layer2_bwd<<<L2_BLOCKS, 256, 0, st>>>(act1, p->a1, p->w2, demb, count_dev, rows_max, w.da1, w.p2);
   reduce(st, w.p2, L2_BLOCKS, L2_PART, 0, DICM_D * H2, g->w2);

@@ -417,6 +417,12 @@ int set_smem(K kernel) {
 
 size_t workspace_bytes(int64_t rows_max, int d_raw) { return carve_ws(rows_max, d_raw, nullptr, nullptr); }
 
+__nv_bfloat16* da0_bf16_ptr(void* ws, int64_t rows_max, int d_raw) {
+  TcWs w;
+  carve_ws(rows_max, d_raw, &w, (char*)ws);
+  return w.da0_bf16;
+}
+
 int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows, const int32_t* count,
                int64_t rows_max, const float* w0, const float* b0, float* act0, int precision, void* ws,
                cudaStream_t st) {
@@ -449,7 +455,8 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
 }
 
 int bwd_dw0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows, const int32_t* count,
-            int64_t rows_max, const float* da0, float* gw0, int precision, void* ws, cudaStream_t st) {
+            int64_t rows_max, const float* da0, float* gw0, int precision, void* ws, cudaStream_t st,
+            bool da0_bf16_ready) {
   const bool bf16 = precision == DICM_PREC_BF16;
   if (bf16 != (pool_dtype == DICM_POOL_BF16))
     return fail(DICM_ERR_VALUE, "precision %s needs a %s pool", bf16 ? "bf16" : "tf32", bf16 ? "bf16" : "fp32");
@@ -458,7 +465,8 @@ int bwd_dw0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows, co
   carve_ws(rows_max, d_raw, &w, (char*)ws);
   const void* asrc = da0;
   if (bf16) {
-    k_to_bf16<<<dicm_grid(rows_max * 128, 256, 148 * 8), 256, 0, st>>>(da0, count, 256, rows_max * 256, w.da0_bf16);
+    if (!da0_bf16_ready)
+      k_to_bf16<<<dicm_grid(rows_max * 128, 256, 148 * 8), 256, 0, st>>>(da0, count, 256, rows_max * 256, w.da0_bf16);
     asrc = w.da0_bf16;
   }
   CUtensorMap map;

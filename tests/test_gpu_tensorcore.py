@@ -79,8 +79,10 @@ def test_layer0_tensorcore_matches_fp32(U, prec, tol):
     gr = _bwd(L, pool, p, rt, cnt, cap, L0.PREC_FP32, ref[0], ref[1], demb, ref[3], ref[4])
     gg = _bwd(L, pool, p, rt, cnt, cap, L0.PRECISIONS[prec], ref[0], ref[1], demb, got[3], got[4])
     assert _relmax(gg["w0"], gr["w0"]) < tol
-    for k in ("b0", "a0", "w1", "b1", "a1", "w2", "b2"):  # fp32 layers agree tightly
-        assert _relmax(gg[k], gr[k]) < 1e-5, k
+    for k in ("b0", "a0", "w1", "b1", "a1", "w2", "b2"):  # layers 1-2 run on tf32 tensor cores
+        assert _relmax(gg[k], gr[k]) < max(tol, 3e-3), k
+    assert _relmax(got[1][:U], ref[1][:U]) < max(tol, 3e-3)  # act1
+    assert _relmax(got[2][:U], ref[2][:U]) < max(tol, 3e-3)  # emb
 
 
 @pytest.mark.parametrize("kind", ["sum", "attn", "multiquery-attn"])
