@@ -191,7 +191,7 @@ void reduce(cudaStream_t st, const float* part, int nblk, int64_t stride, int64_
 }
 
 struct Ws {
-  float *da1, *da0, *p2, *p0, *pw1, *pw0, *red, *pl12, *pdw1;
+  float *da1, *da0, *p2, *p0, *pw1, *pw0, *red, *pl12, *pdw1, *h1;
   int s1, s0;
 };
 
@@ -217,6 +217,7 @@ size_t carve(int64_t rows_max, int d_raw, Ws* w, char* base) {
   t.red = (float*)take(red_tmp_floats(rows_max) * 4);
   t.pl12 = (float*)take((size_t)sm100::small_bwd_blocks(rows_max) * sm100::small_part_size() * 4);
   t.pdw1 = (float*)take((size_t)sm100::small_dw1_blocks(rows_max) * H2 * H1 * 4);
+  t.h1 = (float*)take((size_t)rows_max * H1 * 4);
   if (w) *w = t;
   return off + sm100::workspace_bytes(rows_max, d_raw);
 }
@@ -272,7 +273,8 @@ int dicm_imgmlp_fwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
                            tc_ws, st);
     if (rc) return rc;
     // layers 1-2 on tcgen05 (tf32) with the layer-2 epilogue fused
-    rc = sm100::fwd_layers12(act0, count_dev, rows_max, p->a0, p->w1, p->b1, p->a1, p->w2, p->b2, act1, emb, st);
+    rc = sm100::fwd_layers12(act0, count_dev, rows_max, p->a0, p->w1, p->b1, p->a1, p->w2, p->b2, act1, emb, w.h1,
+                             st);
     if (rc) return rc;
     return last_launch("dicm_imgmlp_fwd");
   }
@@ -320,7 +322,7 @@ int dicm_imgmlp_bwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
     char* tc_ws = (char*)workspace + carve(rows_max, d_raw, nullptr, nullptr) - sm100::workspace_bytes(rows_max, d_raw);
     const bool bf16 = precision == DICM_PREC_BF16;
     __nv_bfloat16* da0_bf16 = bf16 ? sm100::da0_bf16_ptr(tc_ws, rows_max, d_raw) : nullptr;
-    rc = sm100::bwd_layers12(demb, act1, act0, count_dev, rows_max, p->a0, p->a1, p->w1, p->w2, w.da1, w.da0,
+    rc = sm100::bwd_layers12(demb, act1, act0, w.h1, count_dev, rows_max, p->a0, p->a1, p->w1, p->w2, w.da1, w.da0,
                              da0_bf16, w.pl12, w.pdw1, st);
     if (rc) return rc;
     const int nb = sm100::small_bwd_blocks(rows_max), ps = sm100::small_part_size();

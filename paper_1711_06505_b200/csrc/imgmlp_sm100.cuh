@@ -25,10 +25,10 @@ int small_dw1_blocks(int64_t rows_max);
 int small_bwd_blocks(int64_t rows_max);
 int fwd_layers12(const float* act0, const int32_t* count, int64_t rows_max, const float* al0, const float* w1,
                  const float* b1, const float* al1, const float* w2, const float* b2, float* act1, float* emb,
-                 cudaStream_t st);
-int bwd_layers12(const float* demb, const float* act1, const float* act0, const int32_t* count, int64_t rows_max,
-                 const float* al0, const float* al1, const float* w1, const float* w2, float* da1, float* da0,
-                 __nv_bfloat16* da0_bf16, float* part_l12, float* part_dw1, cudaStream_t st);
+                 float* h1, cudaStream_t st);
+int bwd_layers12(const float* demb, const float* act1, const float* act0, const float* h1, const int32_t* count,
+                 int64_t rows_max, const float* al0, const float* al1, const float* w1, const float* w2, float* da1,
+                 float* da0, __nv_bfloat16* da0_bf16, float* part_l12, float* part_dw1, cudaStream_t st);
 
 }  // namespace sm100
 }  // namespace dicm

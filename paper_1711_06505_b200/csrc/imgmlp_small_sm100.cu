@@ -49,15 +49,20 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
 // ===========================================================================
 // forward layers 1-2, persistent over 128-row tiles
 // ===========================================================================
-constexpr uint32_t F_A = 128 * 1024;  // h1 tile, tf32 K-major SW128 (8 atoms x 16 KB)
+constexpr uint32_t F_A = 128 * 1024;  // a0 -> h1 tile, tf32 K-major SW128 (8 atoms x 16 KB)
 constexpr uint32_t F_B = 64 * 1024;   // W1 [64 x 256], K-major SW128 (8 atoms x 8 KB)
 constexpr size_t F_SMEM = 1024 + F_A + F_B + 4 * (256 + 64 + 64 + 768 + 16) + 64;
 
+// The a0 tile arrives by TMA (8 boxes of 32 columns x 128 rows, 128-B swizzle
+// = the UMMA K-major layout), PReLU is applied in place, the h1 tile is
+// written back to HBM by TMA store (the dW1 kernel consumes it) and multiplied
+// by W1; the next tile's TMA load is issued as soon as the MMA has read A, so
+// it overlaps the TMEM epilogue.
 __global__ void __launch_bounds__(256, 1)
-    k_l12_fwd(const float* __restrict__ act0, const float* __restrict__ al0, const float* __restrict__ w1,
-              const float* __restrict__ b1, const float* __restrict__ al1, const float* __restrict__ w2,
-              const float* __restrict__ b2, const int32_t* __restrict__ count, float* __restrict__ act1,
-              float* __restrict__ emb) {
+    k_l12_fwd(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmH1,
+              const float* __restrict__ al0, const float* __restrict__ w1, const float* __restrict__ b1,
+              const float* __restrict__ al1, const float* __restrict__ w2, const float* __restrict__ b2,
+              const int32_t* __restrict__ count, float* __restrict__ act1, float* __restrict__ emb) {
   const int U = *count;
   const int ntiles = (U + 127) / 128;
   if ((int)blockIdx.x >= ntiles) return;
@@ -70,24 +75,28 @@ __global__ void __launch_bounds__(256, 1)
   float* sw2 = sal1 + 64;
   float* sb2 = sw2 + 768;
   const uint32_t bar = B + F_B + 4 * (256 + 64 + 64 + 768 + 16);
-  const uint32_t slot = bar + 8;
+  const uint32_t fullA = bar + 8;
+  const uint32_t slot = fullA + 8;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  if (t == 0) {
+    mbar_init(bar, 1);
+    mbar_init(fullA, 1);
+    fence_mbar_init();
+    prefetch_tmap(&tmA0);
+    prefetch_tmap(&tmH1);
+  }
   // W1 -> K-major SW128: row n (64), 16-B chunk q of k
   for (int i = t; i < 64 * 64; i += 256) {
     const int n = i >> 6, q = i & 63, j = q >> 3, c = q & 7;
     *at<float4>(raw, r0, B + j * 8192 + n * 128 + ((c ^ (n & 7)) << 4)) = __ldg(reinterpret_cast<const float4*>(w1) + i);
   }
-  for (int i = t; i < 256; i += 256) sal0[i] = al0[i];
+  sal0[t] = al0[t];
   if (t < 64) {
     sb1[t] = b1[t];
     sal1[t] = al1[t];
   }
   for (int i = t; i < 768; i += 256) sw2[i] = w2[i];
   if (t < 12) sb2[t] = b2[t];
-  if (t == 0) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-  }
   if (warp == 0) {
     tmem_alloc(slot, 64);
     tmem_relinquish();
@@ -98,23 +107,25 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem = *at<volatile uint32_t>(raw, r0, slot);
   const uint32_t idesc = instr_desc(2, 128, 64, 0, 0);
+  if (t == 0) {
+    mbar_arrive_expect_tx(fullA, F_A);
+    for (int j = 0; j < 8; ++j) tma_load_2d(A + j * 16384, &tmA0, fullA, j * 32, blockIdx.x * 128);
+  }
   uint32_t it = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int m0 = tile * 128;
-    // h1 = prelu(a0) -> A (K-major SW128)
-#pragma unroll 4
+    mbar_wait(fullA, it & 1);
+    // h1 = prelu(a0) in place (each 16-B chunk keeps its swizzled slot)
+#pragma unroll 8
     for (int i = t; i < 128 * 64; i += 256) {
       const int r = i >> 6, q = i & 63, j = q >> 3, c = q & 7;
-      const int gr = m0 + r;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (gr < U) {
-        v = __ldg(reinterpret_cast<const float4*>(act0 + (int64_t)gr * H1) + q);
-        v.x = prelu(v.x, sal0[4 * q]);
-        v.y = prelu(v.y, sal0[4 * q + 1]);
-        v.z = prelu(v.z, sal0[4 * q + 2]);
-        v.w = prelu(v.w, sal0[4 * q + 3]);
-      }
-      *at<float4>(raw, r0, A + j * 16384 + r * 128 + ((c ^ (r & 7)) << 4)) = v;
+      float4* p = at<float4>(raw, r0, A + j * 16384 + r * 128 + ((c ^ (r & 7)) << 4));
+      float4 v = *p;
+      v.x = prelu(v.x, sal0[4 * q]);
+      v.y = prelu(v.y, sal0[4 * q + 1]);
+      v.z = prelu(v.z, sal0[4 * q + 2]);
+      v.w = prelu(v.w, sal0[4 * q + 3]);
+      *p = v;
     }
     fence_proxy_async();
     __syncthreads();
@@ -127,10 +138,22 @@ __global__ void __launch_bounds__(256, 1)
                k > 0);
       }
       mma_commit(bar);
+      // h1 tile -> HBM (consumed by dW1), overlapping the MMA (both only read A)
+      for (int j = 0; j < 8; ++j) tma_store_2d(&tmH1, A + j * 16384, j * 32, m0);
+      bulk_commit();
+    }
+    mbar_wait(bar, it & 1);
+    tc_fence_after();
+    if (t == 0) {
+      // A may be refilled once the MMA and the h1 store have read it
+      bulk_wait_read0();
+      const int next = tile + gridDim.x;
+      if (next < ntiles) {
+        mbar_arrive_expect_tx(fullA, F_A);
+        for (int j = 0; j < 8; ++j) tma_load_2d(A + j * 16384, &tmA0, fullA, j * 32, next * 128);
+      }
     }
     if (warp < 4) {
-      mbar_wait(bar, it & 1);
-      tc_fence_after();
       float a[64];
       tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16), *reinterpret_cast<float(*)[32]>(a));
       tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + 32, *reinterpret_cast<float(*)[32]>(a + 32));
@@ -159,6 +182,7 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_before();
     __syncthreads();
   }
+  if (t == 0) bulk_wait0();
   if (warp == 0) tmem_dealloc(tmem, 64);
 }
 
@@ -171,10 +195,11 @@ constexpr int PART_L2 = 12 * 64 + 12 + 64 + 64;  // w2 | b2 | a1 | b1
 constexpr int PART_B = PART_L2 + 256 + 256;      // ... | a0 | b0
 constexpr size_t G_SMEM = 1024 + G_A + G_B + 4 * (128 * 12 + 256 + 64 + 768) + 64;
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, 2)
     k_l12_bwd(const float* __restrict__ demb, const float* __restrict__ act1, const float* __restrict__ act0,
               const float* __restrict__ al0, const float* __restrict__ al1, const float* __restrict__ w1,
-              const float* __restrict__ w2, const int32_t* __restrict__ count, float* __restrict__ da1_out,
+              const float* __restrict__ w2, const int32_t* __restrict__ count, int64_t rows_max,
+              float* __restrict__ da1_out,
               float* __restrict__ da0_out, __nv_bfloat16* __restrict__ da0_bf16, float* __restrict__ part) {
   const int U = *count;
   const int ntiles = (U + 127) / 128;
@@ -239,15 +264,23 @@ __global__ void __launch_bounds__(256, 1)
     }
     __syncthreads();
     // da1 = prelu'(a1) (dE W2)  -> global + operand A (K-major SW128)
-    for (int r = grp; r < 128; r += 4) {
-      const int gr = m0 + r;
+    float apre[32];  // all of this thread's act1 values in flight at once
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int gr = m0 + grp + 4 * i;
+      apre[i] = gr < U ? __ldg(act1 + (int64_t)gr * H2 + j) : 0.f;
+    }
+#pragma unroll 4
+    for (int i = 0; i < 32; ++i) {
+      const int r = grp + 4 * i, gr = m0 + r;
       const float* d = sdE + r * 12;
       float dh = 0.f;
 #pragma unroll
       for (int c = 0; c < 12; ++c) dh = fmaf(d[c], w2col[c], dh);
-      const float a = gr < U ? __ldg(act1 + (int64_t)gr * H2 + j) : 0.f;
+      const float a = apre[i];
       const float dd = a > 0.f ? dh : alj * dh;
-      if (gr < U) da1_out[(int64_t)gr * H2 + j] = dd;
+      // rows past the count get 0: the dW1 reduction reads whole 32-row stages
+      if (gr < rows_max) da1_out[(int64_t)gr * H2 + j] = dd;
       if (!(a > 0.f)) acc_a1 = fmaf(a, dh, acc_a1);
       acc_b1 += dd;
       const float h = prelu(a, alj);
@@ -336,12 +369,15 @@ __global__ void __launch_bounds__(256, 1)
 // ===========================================================================
 constexpr int W_STAGES = 4;
 constexpr uint32_t W_A = 32 * 1024;  // h1^T: 2 halves x 4 atoms x 32 rows x 128 B (BASE32B)
-constexpr uint32_t W_B = 8 * 1024;   // da1:  2 atoms x 32 rows x 128 B (BASE32B, via TMA ATOM_32B)
+constexpr uint32_t W_B = 8 * 1024;   // da1:  2 atoms x 32 rows x 128 B (BASE32B)
 constexpr uint32_t W_STAGE = W_A + W_B;
 constexpr size_t W_SMEM = 1024 + W_STAGES * W_STAGE + 256;
 
+// Both operands are MN-major tiles loaded by TMA with the 32-B-atom 128-B
+// swizzle (tf32 MN-major): h1 (written by k_l12_fwd) and da1 (k_l12_bwd).
+// Rows past the live count are zero in da1, so partial stages add nothing.
 __global__ void __launch_bounds__(192, 1)
-    k_dw1(const __grid_constant__ CUtensorMap tmD, const float* __restrict__ act0, const float* __restrict__ al0,
+    k_dw1(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmD,
           const int32_t* __restrict__ count, float* __restrict__ part /*[grid][64*256]*/) {
   const int U = *count;
   const int per = (((U + gridDim.x - 1) / gridDim.x) + 31) / 32 * 32;
@@ -359,7 +395,7 @@ __global__ void __launch_bounds__(192, 1)
                  slot = accb + 8;
   if (t == 0) {
     for (int i = 0; i < W_STAGES; ++i) {
-      mbar_init(full + 8 * i, 128 + 1);
+      mbar_init(full + 8 * i, 1);
       mbar_init(empty + 8 * i, 1);
     }
     mbar_init(accb, 1);
@@ -373,51 +409,32 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *at<volatile uint32_t>(raw, r0, slot);
-  if (warp < 4) {
-    // h1 = prelu(a0) rows -> MN-major BASE32B: feature m = 4*q4 .. +3 of row k
-    const float4 alq = __ldg(reinterpret_cast<const float4*>(al0) + (t & 63));  // column block of every row
-    for (int kb = 0; kb < nk; ++kb) {
-      const uint32_t st = kb % W_STAGES, itn = kb / W_STAGES;
-      mbar_wait(empty + 8 * st, (itn & 1) ^ 1);
-      const uint32_t a = base + st * W_STAGE;
-#pragma unroll 4
-      for (int i = 0; i < 16; ++i) {
-        const int idx = i * 128 + t, k = idx >> 6, q4 = idx & 63;
-        const int gr = rb + kb * 32 + k;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (gr < re) {
-          v = __ldg(reinterpret_cast<const float4*>(act0 + (int64_t)gr * H1) + q4);
-          v.x = prelu(v.x, alq.x);
-          v.y = prelu(v.y, alq.y);
-          v.z = prelu(v.z, alq.z);
-          v.w = prelu(v.w, alq.w);
-        }
-        const int m = 4 * q4, h = m >> 7, atom = (m & 127) >> 5, g = (m & 31) >> 3, lo = (m & 7) * 4;
-        *at<float4>(raw, r0, a + h * 16384 + atom * 4096 + k * 128 + ((g ^ (k & 3)) << 5) + lo) = v;
-      }
-      fence_proxy_async();
-      mbar_arrive(full + 8 * st);
-    }
-  } else if (warp == 5) {
+  if (warp == 5) {
     if (lane == 0) {
+      prefetch_tmap(&tmH);
       prefetch_tmap(&tmD);
       for (int kb = 0; kb < nk; ++kb) {
         const uint32_t st = kb % W_STAGES, itn = kb / W_STAGES;
         mbar_wait(empty + 8 * st, (itn & 1) ^ 1);
-        mbar_arrive_expect_tx(full + 8 * st, W_B);
-        const uint32_t b = base + st * W_STAGE + W_A;
-        tma_load_2d(b, &tmD, full + 8 * st, 0, rb + kb * 32);
-        tma_load_2d(b + 4096, &tmD, full + 8 * st, 32, rb + kb * 32);
+        mbar_arrive_expect_tx(full + 8 * st, W_STAGE);
+        const uint32_t a = base + st * W_STAGE, b = a + W_A;
+        const int row = rb + kb * 32;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int at4 = 0; at4 < 4; ++at4)
+            tma_load_2d(a + h * 16384 + at4 * 4096, &tmH, full + 8 * st, h * 128 + at4 * 32, row);
+        tma_load_2d(b, &tmD, full + 8 * st, 0, row);
+        tma_load_2d(b + 4096, &tmD, full + 8 * st, 32, row);
       }
     }
-  } else {
+  } else if (warp == 4) {
     if (lane == 0) {
       const uint32_t idesc = instr_desc(2, 128, 64, 1, 1);
       for (int kb = 0; kb < nk; ++kb) {
         const uint32_t st = kb % W_STAGES, itn = kb / W_STAGES;
         mbar_wait(full + 8 * st, itn & 1);
         tc_fence_after();
-        fence_proxy_async();
         const uint32_t a = base + st * W_STAGE, b = a + W_A;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
@@ -429,8 +446,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       mma_commit(accb);
     }
-  }
-  if (warp < 4) {
+  } else {
     mbar_wait(accb, 0);
     tc_fence_after();
 #pragma unroll 1
@@ -449,6 +465,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   if (warp == 4) tmem_dealloc(tmem, 128);
 }
+
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn2() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -472,42 +489,52 @@ int smem_attr(K kernel, size_t bytes) {
 
 int small_part_size() { return PART_B; }
 int small_dw1_blocks(int64_t rows_max) { return (int)std::max<int64_t>(1, std::min<int64_t>(148, (rows_max + 255) / 256)); }
-int small_bwd_blocks(int64_t rows_max) { return (int)std::max<int64_t>(1, std::min<int64_t>(148, (rows_max + 127) / 128)); }
+int small_bwd_blocks(int64_t rows_max) { return (int)std::max<int64_t>(1, std::min<int64_t>(296, (rows_max + 127) / 128)); }
+
+// row-major fp32 [rows, cols] map with box {32 cols, box_rows}
+int map_f32(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows, CUtensorMapSwizzle swz) {
+  auto fn = encode_fn2();
+  if (!fn) return fail(DICM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 4};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DICM_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return DICM_OK;
+}
 
 int fwd_layers12(const float* act0, const int32_t* count, int64_t rows_max, const float* al0, const float* w1,
                  const float* b1, const float* al1, const float* w2, const float* b2, float* act1, float* emb,
-                 cudaStream_t st) {
+                 float* h1, cudaStream_t st) {
   static int once = smem_attr(k_l12_fwd, F_SMEM);
   if (once) return once;
+  CUtensorMap ma, mh;
+  int rc = map_f32(&ma, act0, rows_max, H1, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = map_f32(&mh, h1, rows_max, H1, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148, (rows_max + 127) / 128));
-  k_l12_fwd<<<grid, 256, F_SMEM, st>>>(act0, al0, w1, b1, al1, w2, b2, count, act1, emb);
+  k_l12_fwd<<<grid, 256, F_SMEM, st>>>(ma, mh, al0, w1, b1, al1, w2, b2, count, act1, emb);
   return last_launch("tcgen05 layers 1-2 forward");
 }
 
-int bwd_layers12(const float* demb, const float* act1, const float* act0, const int32_t* count, int64_t rows_max,
-                 const float* al0, const float* al1, const float* w1, const float* w2, float* da1, float* da0,
-                 __nv_bfloat16* da0_bf16, float* part_l12, float* part_dw1, cudaStream_t st) {
+int bwd_layers12(const float* demb, const float* act1, const float* act0, const float* h1, const int32_t* count,
+                 int64_t rows_max, const float* al0, const float* al1, const float* w1, const float* w2, float* da1,
+                 float* da0, __nv_bfloat16* da0_bf16, float* part_l12, float* part_dw1, cudaStream_t st) {
   static int once = smem_attr(k_l12_bwd, G_SMEM);
   if (once) return once;
   static int once2 = smem_attr(k_dw1, W_SMEM);
   if (once2) return once2;
-  k_l12_bwd<<<small_bwd_blocks(rows_max), 256, G_SMEM, st>>>(demb, act1, act0, al0, al1, w1, w2, count, da1, da0,
-                                                             da0_bf16, part_l12);
+  k_l12_bwd<<<small_bwd_blocks(rows_max), 256, G_SMEM, st>>>(demb, act1, act0, al0, al1, w1, w2, count, rows_max,
+                                                             da1, da0, da0_bf16, part_l12);
   int rc = last_launch("tcgen05 layers 2-1 backward");
   if (rc) return rc;
-  // da1 [rows_max, 64] fp32 map, box {32 cols, 32 rows}, 32-B-atom 128-B swizzle
-  auto fn = encode_fn2();
-  if (!fn) return fail(DICM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  CUtensorMap map;
-  cuuint64_t dims[2] = {64, (cuuint64_t)rows_max};
-  cuuint64_t strides[1] = {64 * 4};
-  cuuint32_t box[2] = {32, 32};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, da1, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(DICM_ERR_CUDA, "cuTensorMapEncodeTiled(da1) failed (%d)", (int)r);
-  k_dw1<<<small_dw1_blocks(rows_max), 192, W_SMEM, st>>>(map, act0, al0, count, part_dw1);
+  CUtensorMap mh, md;
+  rc = map_f32(&mh, h1, rows_max, H1, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  if (!rc) rc = map_f32(&md, da1, rows_max, H2, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  if (rc) return rc;
+  k_dw1<<<small_dw1_blocks(rows_max), 192, W_SMEM, st>>>(mh, md, count, part_dw1);
   return last_launch("tcgen05 dW1");
 }
 
