@@ -59,7 +59,7 @@ constexpr size_t F_SMEM = 1024 + F_A + F_B + 4 * (256 + 64 + 64 + 768 + 16) + 64
 // by W1; the next tile's TMA load is issued as soon as the MMA has read A, so
 // it overlaps the TMEM epilogue.
 __global__ void __launch_bounds__(256, 1)
-    k_l12_fwd(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmH1,
+    k_l12_fwd(const __grid_constant__ CUtensorMap tmA0, float* __restrict__ h1, int64_t rows_max,
               const float* __restrict__ al0, const float* __restrict__ w1, const float* __restrict__ b1,
               const float* __restrict__ al1, const float* __restrict__ w2, const float* __restrict__ b2,
               const int32_t* __restrict__ count, float* __restrict__ act1, float* __restrict__ emb) {
@@ -83,7 +83,6 @@ __global__ void __launch_bounds__(256, 1)
     mbar_init(fullA, 1);
     fence_mbar_init();
     prefetch_tmap(&tmA0);
-    prefetch_tmap(&tmH1);
   }
   // W1 -> K-major SW128: row n (64), 16-B chunk q of k
   for (int i = t; i < 64 * 64; i += 256) {
@@ -126,6 +125,8 @@ __global__ void __launch_bounds__(256, 1)
       v.z = prelu(v.z, sal0[4 * q + 2]);
       v.w = prelu(v.w, sal0[4 * q + 3]);
       *p = v;
+      // h1 -> HBM (consumed by the dW1 reduction); coalesced along the row
+      if (m0 + r < rows_max) reinterpret_cast<float4*>(h1 + (int64_t)(m0 + r) * H1)[q] = v;
     }
     fence_proxy_async();
     __syncthreads();
@@ -138,15 +139,11 @@ __global__ void __launch_bounds__(256, 1)
                k > 0);
       }
       mma_commit(bar);
-      // h1 tile -> HBM (consumed by dW1), overlapping the MMA (both only read A)
-      for (int j = 0; j < 8; ++j) tma_store_2d(&tmH1, A + j * 16384, j * 32, m0);
-      bulk_commit();
     }
     mbar_wait(bar, it & 1);
     tc_fence_after();
     if (t == 0) {
-      // A may be refilled once the MMA and the h1 store have read it
-      bulk_wait_read0();
+      // A may be refilled once the MMA has read it
       const int next = tile + gridDim.x;
       if (next < ntiles) {
         mbar_arrive_expect_tx(fullA, F_A);
@@ -182,7 +179,6 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_before();
     __syncthreads();
   }
-  if (t == 0) bulk_wait0();
   if (warp == 0) tmem_dealloc(tmem, 64);
 }
 
@@ -195,7 +191,7 @@ constexpr int PART_L2 = 12 * 64 + 12 + 64 + 64;  // w2 | b2 | a1 | b1
 constexpr int PART_B = PART_L2 + 256 + 256;      // ... | a0 | b0
 constexpr size_t G_SMEM = 1024 + G_A + G_B + 4 * (128 * 12 + 256 + 64 + 768) + 64;
 
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, 1)
     k_l12_bwd(const float* __restrict__ demb, const float* __restrict__ act1, const float* __restrict__ act0,
               const float* __restrict__ al0, const float* __restrict__ al1, const float* __restrict__ w1,
               const float* __restrict__ w2, const int32_t* __restrict__ count, int64_t rows_max,
@@ -270,7 +266,7 @@ __global__ void __launch_bounds__(256, 2)
       const int gr = m0 + grp + 4 * i;
       apre[i] = gr < U ? __ldg(act1 + (int64_t)gr * H2 + j) : 0.f;
     }
-#pragma unroll 4
+#pragma unroll
     for (int i = 0; i < 32; ++i) {
       const int r = grp + 4 * i, gr = m0 + r;
       const float* d = sdE + r * 12;
@@ -304,16 +300,25 @@ __global__ void __launch_bounds__(256, 2)
     {
       const int row = m0 + q * 32 + lane;
       const bool ok = row < U;
-#pragma unroll 1
+      const float4* arow = reinterpret_cast<const float4*>(act0 + (int64_t)(ok ? row : 0) * H1 + cb0 * 32);
+      float4 anext[8];  // a0 of the next column block in flight while this one computes
+#pragma unroll
+      for (int v = 0; v < 8; ++v) anext[v] = ok ? __ldg(arow + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
         const int cb = cb0 + cc;
+        float4 acur[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acur[v] = anext[v];
+        if (cc < 3) {
+#pragma unroll
+          for (int v = 0; v < 8; ++v) anext[v] = ok ? __ldg(arow + (cc + 1) * 8 + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
         float dh[32], sa[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + cb * 32, dh);
-        const float4* ap = reinterpret_cast<const float4*>(act0 + (int64_t)(ok ? row : 0) * H1 + cb * 32);
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
-          float4 a4 = ok ? __ldg(ap + v) : make_float4(0.f, 0.f, 0.f, 0.f);
-          const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+          const float av[4] = {acur[v].x, acur[v].y, acur[v].z, acur[v].w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int i = 4 * v + e;
@@ -489,7 +494,7 @@ int smem_attr(K kernel, size_t bytes) {
 
 int small_part_size() { return PART_B; }
 int small_dw1_blocks(int64_t rows_max) { return (int)std::max<int64_t>(1, std::min<int64_t>(148, (rows_max + 255) / 256)); }
-int small_bwd_blocks(int64_t rows_max) { return (int)std::max<int64_t>(1, std::min<int64_t>(296, (rows_max + 127) / 128)); }
+int small_bwd_blocks(int64_t rows_max) { return (int)std::max<int64_t>(1, std::min<int64_t>(148, (rows_max + 127) / 128)); }
 
 // row-major fp32 [rows, cols] map with box {32 cols, box_rows}
 int map_f32(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows, CUtensorMapSwizzle swz) {
@@ -510,12 +515,11 @@ int fwd_layers12(const float* act0, const int32_t* count, int64_t rows_max, cons
                  float* h1, cudaStream_t st) {
   static int once = smem_attr(k_l12_fwd, F_SMEM);
   if (once) return once;
-  CUtensorMap ma, mh;
+  CUtensorMap ma;
   int rc = map_f32(&ma, act0, rows_max, H1, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (!rc) rc = map_f32(&mh, h1, rows_max, H1, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148, (rows_max + 127) / 128));
-  k_l12_fwd<<<grid, 256, F_SMEM, st>>>(ma, mh, al0, w1, b1, al1, w2, b2, count, act1, emb);
+  k_l12_fwd<<<grid, 256, F_SMEM, st>>>(ma, h1, rows_max, al0, w1, b1, al1, w2, b2, count, act1, emb);
   return last_launch("tcgen05 layers 1-2 forward");
 }
 
