@@ -16,6 +16,7 @@
 #include <cudaTypedefs.h>
 
 #include "imgmlp_sm100.cuh"
+#include "epi.cuh"
 #include "tc_ptx.cuh"
 
 namespace dicm {
@@ -189,7 +190,7 @@ constexpr uint32_t G_A = 32 * 1024;  // da1 tile, K-major SW128 (2 atoms x 16 KB
 constexpr uint32_t G_B = 64 * 1024;  // W1 as MN-major (n x k) SWIZZLE_128B_BASE32B: 8 atoms x 64 k x 128 B
 constexpr int PART_L2 = 12 * 64 + 12 + 64 + 64;  // w2 | b2 | a1 | b1
 constexpr int PART_B = PART_L2 + 256 + 256;      // ... | a0 | b0
-constexpr size_t G_SMEM = 1024 + G_A + G_B + 4 * (128 * 12 + 256 + 64 + 768) + 64;
+constexpr size_t G_SMEM = 1024 + G_A + G_B + 4 * (128 * 12 + 256 + 64 + 768) + 64 + 8 * epi::SCRATCH_FLOATS * 4;
 
 __global__ void __launch_bounds__(256, 1)
     k_l12_bwd(const float* __restrict__ demb, const float* __restrict__ act1, const float* __restrict__ act0,
@@ -214,6 +215,7 @@ __global__ void __launch_bounds__(256, 1)
   float* sw2 = sal1 + 64;
   const uint32_t bar = B + G_B + 4 * (128 * 12 + 256 + 64 + 768);
   const uint32_t slot = bar + 8;
+  float* scr = at<float>(raw, r0, bar + 64) + (threadIdx.x >> 5) * epi::SCRATCH_FLOATS;
   // W1 [k=64][n=256] -> MN-major BASE32B: atom n/32, row k, 32-B granule ^ (k & 3)
   for (int i = t; i < 64 * 64; i += 256) {
     const int k = i >> 6, q = i & 63;  // float4 q covers n = 4q .. 4q+3
@@ -328,16 +330,13 @@ __global__ void __launch_bounds__(256, 1)
             sa[i] = pos ? 0.f : x * g;
           }
         }
-        if (ok) {
-          float4* o = reinterpret_cast<float4*>(da0_out + (int64_t)row * H1 + cb * 32);
-#pragma unroll
-          for (int v = 0; v < 8; ++v) o[v] = make_float4(dh[4 * v], dh[4 * v + 1], dh[4 * v + 2], dh[4 * v + 3]);
-          if (da0_bf16) {
-            __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(da0_bf16 + (int64_t)row * H1 + cb * 32);
-#pragma unroll
-            for (int v = 0; v < 16; ++v) ob[v] = __floats2bfloat162_rn(dh[2 * v], dh[2 * v + 1]);
-          }
-        }
+        // coalesced row stores through the warp's scratch; the bf16 path
+        // (kind::f16 dW0) needs only the bf16 copy, the tf32 path the fp32 one
+        if (da0_bf16)
+          epi::store_bf16(dh, scr, lane, m0 + q * 32, U,
+                          [&](int r) { return da0_bf16 + (int64_t)r * H1 + cb * 32; });
+        else
+          epi::store_f32(dh, scr, lane, m0 + q * 32, U, [&](int r) { return da0_out + (int64_t)r * H1 + cb * 32; });
         acc_b0[cc] += reduce_scatter32(dh, lane);
         acc_a0[cc] += reduce_scatter32(sa, lane);
       }
