@@ -25,6 +25,7 @@
 #include <mutex>
 
 #include "imgmlp_sm100.cuh"
+#include "epi.cuh"
 #include "tc_ptx.cuh"
 
 namespace dicm {
@@ -36,7 +37,8 @@ using namespace tc;
 constexpr int STAGES = 3;
 constexpr uint32_t OPB = 256 * 128;  // bytes per operand per stage (256 x 128 B)
 constexpr uint32_t STAGE_BYTES = 2 * OPB;
-constexpr size_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr size_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
+                              4 * epi::SCRATCH_FLOATS * 4 /*epilogue transpose*/;
 constexpr int THREADS_F = 320;  // fwd: warps 0-3 gather, 4 MMA, 5 TMA, 6-9 epilogue
 constexpr int THREADS_B = 192;  // bwd: warps 0-3 gather + epilogue, 4 MMA, 5 TMA
 constexpr unsigned FULL = 0xffffffffu;
@@ -172,6 +174,7 @@ __global__ void __launch_bounds__(THREADS_F, 1)
   } else {
     // ---- epilogue warps 6-9: TMEM lane quarter = warp % 4
     const int q = warp & 3;
+    float* scr = reinterpret_cast<float*>(smem_raw + (s.slot + 16 - smem_u32(smem_raw))) + q * epi::SCRATCH_FLOATS;
     uint32_t tl = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
       mbar_wait(s.acc_full, tl & 1);
@@ -179,20 +182,14 @@ __global__ void __launch_bounds__(THREADS_F, 1)
       const int m0 = tile * 256;
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {
-        const int row = m0 + h * 128 + q * 32 + lane;
 #pragma unroll 1
         for (int cb = 0; cb < 8; ++cb) {
           float v[32];
           tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + h * 256 + cb * 32, v);
-          if (row < U) {
-            float4* out = reinterpret_cast<float4*>(act0 + (int64_t)row * 256 + cb * 32);
-            const float4* bb = reinterpret_cast<const float4*>(bias + cb * 32);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 b4 = __ldg(bb + j);
-              out[j] = make_float4(v[4 * j] + b4.x, v[4 * j + 1] + b4.y, v[4 * j + 2] + b4.z, v[4 * j + 3] + b4.w);
-            }
-          }
+          for (int j = 0; j < 32; ++j) v[j] += __ldg(bias + cb * 32 + j);
+          epi::store_f32(v, scr, lane, m0 + h * 128 + q * 32, U,
+                         [&](int r) { return act0 + (int64_t)r * 256 + cb * 32; });
         }
       }
       tc_fence_before();

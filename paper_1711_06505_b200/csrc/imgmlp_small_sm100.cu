@@ -52,7 +52,7 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
 // ===========================================================================
 constexpr uint32_t F_A = 128 * 1024;  // a0 -> h1 tile, tf32 K-major SW128 (8 atoms x 16 KB)
 constexpr uint32_t F_B = 64 * 1024;   // W1 [64 x 256], K-major SW128 (8 atoms x 8 KB)
-constexpr size_t F_SMEM = 1024 + F_A + F_B + 4 * (256 + 64 + 64 + 768 + 16) + 64;
+constexpr size_t F_SMEM = 1024 + F_A + F_B + 4 * (256 + 64 + 64 + 768 + 16) + 64 + 4 * epi::SCRATCH_FLOATS * 4;
 
 // The a0 tile arrives by TMA (8 boxes of 32 columns x 128 rows, 128-B swizzle
 // = the UMMA K-major layout), PReLU is applied in place, the h1 tile is
@@ -156,12 +156,14 @@ __global__ void __launch_bounds__(256, 1)
       tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16), *reinterpret_cast<float(*)[32]>(a));
       tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + 32, *reinterpret_cast<float(*)[32]>(a + 32));
       const int row = m0 + warp * 32 + lane;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) a[i] += sb1[i];
+      float* scr = at<float>(raw, r0, slot + 16) + warp * epi::SCRATCH_FLOATS;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh)
+        epi::store_f32(*reinterpret_cast<float(*)[32]>(a + 32 * hh), scr, lane, m0 + warp * 32, U,
+                       [&](int r) { return act1 + (int64_t)r * H2 + 32 * hh; });
       if (row < U) {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) a[i] += sb1[i];
-        float4* o = reinterpret_cast<float4*>(act1 + (int64_t)row * H2);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) o[q] = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
         float e[12];
 #pragma unroll
         for (int c = 0; c < 12; ++c) e[c] = sb2[c];
