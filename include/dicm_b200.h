@@ -267,6 +267,20 @@ int dicm_bucket_by_owner(const int32_t* keys, const int32_t* count_dev, int64_t 
 size_t dicm_bucket_workspace(int64_t n_max, int world);
 int dicm_permute_rows12(const float* in, const int32_t* perm, const int32_t* count_dev,
                         int64_t n_max, int scatter, float* out, dicm_stream_t stream);
+/* out[i] = row (key_i - base_f) of the table whose key range holds key_i
+ * (the compact ID rows of a batch; the owner's answer to an ID-row pull,
+ * reference ServerNode.handle_id_pull runtime.py:155-163) */
+int dicm_gather_rows_by_key(const dicm_table_state_t* tabs, int ntab, const int32_t* keys,
+                            const int32_t* count_dev, int64_t n_max, float* out, dicm_stream_t stream);
+/* owner-side reduction of pushed gradient rows: out[u] = sum over sources in
+ * ascending order of the row each source pushed for unique key u (reference
+ * ServerNode.local_model_gradient runtime.py:177-185, apply_id_updates
+ * 208-219).  recv rows are grouped by source (segment offsets seg_dev[nsrc+1]
+ * on the device), inv maps each received row to its unique key; idx_ws holds
+ * nsrc * ucap int32.  Deterministic: no floating-point atomics. */
+int dicm_owner_reduce_rows12(const float* recv, const int32_t* inv, const int64_t* seg_dev, int nsrc,
+                             int64_t n_recv_max, const int32_t* count_dev, int64_t ucap, int32_t* idx_ws,
+                             float* out, dicm_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -138,6 +138,8 @@ _sig("dicm_adam_rows", C.c_int, C.POINTER(TableState), C.c_int, P, P, I64, P, F,
 _sig("dicm_bucket_workspace", S, I64, C.c_int)
 _sig("dicm_bucket_by_owner", C.c_int, P, P, I64, C.c_int, P, P, P, P, S, ST)
 _sig("dicm_permute_rows12", C.c_int, P, P, P, I64, C.c_int, P, ST)
+_sig("dicm_gather_rows_by_key", C.c_int, C.POINTER(TableState), C.c_int, P, P, I64, P, ST)
+_sig("dicm_owner_reduce_rows12", C.c_int, P, P, P, C.c_int, I64, P, I64, P, P, ST)
 
 EXPORTED = [
     "dicm_last_error", "dicm_version", "dicm_device_arch", "dicm_dedup_workspace", "dicm_dedup",
@@ -145,7 +147,8 @@ EXPORTED = [
     "dicm_attn_partial_size", "dicm_sample_blocks", "dicm_sample_fwd", "dicm_sample_bwd",
     "dicm_head_partial_size", "dicm_head_blocks", "dicm_head_fwd_bwd", "dicm_reduce_partials",
     "dicm_loss_finalize", "dicm_check_finite", "dicm_adam_dense_workspace", "dicm_adam_dense", "dicm_adam_rows",
-    "dicm_bucket_workspace", "dicm_bucket_by_owner", "dicm_permute_rows12",
+    "dicm_bucket_workspace", "dicm_bucket_by_owner", "dicm_permute_rows12", "dicm_gather_rows_by_key",
+    "dicm_owner_reduce_rows12",
 ]
 
 

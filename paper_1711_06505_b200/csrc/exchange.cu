@@ -117,3 +117,99 @@ int dicm_permute_rows12(const float* in, const int32_t* perm, const int32_t* cou
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// rows of several tables addressed by combined keys (tables back to back in
+// one key space, ascending bases): out[i] = table_f[key_i - base_f]
+// ---------------------------------------------------------------------------
+namespace {
+struct TabRows {
+  const float* t[DICM_MAX_FIELDS];
+  int64_t base[DICM_MAX_FIELDS];
+  int n;
+};
+
+__global__ void k_gather_keyed(const __grid_constant__ TabRows tb, const int32_t* __restrict__ keys,
+                               const int32_t* __restrict__ count, int64_t n_max, float* __restrict__ out) {
+  const int64_t n = count ? min((int64_t)*count, n_max) : n_max;
+  const int lane = threadIdx.x & 31, part = lane % 3, slot = lane / 3;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w * 10 < n; w += warps) {
+    const int64_t i = w * 10 + slot;
+    if (slot >= 10 || i >= n) continue;
+    const int64_t key = keys[i];
+    int k = 0;
+    while (k + 1 < tb.n && key >= tb.base[k + 1]) ++k;
+    reinterpret_cast<float4*>(out + i * DICM_D)[part] =
+        __ldg(reinterpret_cast<const float4*>(tb.t[k] + (key - tb.base[k]) * DICM_D) + part);
+  }
+}
+
+// idx[s][inv[i]] = i for reference i of source segment s (offsets seg[s]..seg[s+1])
+__global__ void k_scatter_index(const int32_t* __restrict__ inv, const int64_t* __restrict__ seg, int nsrc,
+                                int64_t ucap, int32_t* __restrict__ idx) {
+  const int64_t total = seg[nsrc];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int s = 0;
+    while (s + 1 < nsrc && i >= seg[s + 1]) ++s;
+    idx[(int64_t)s * ucap + inv[i]] = (int32_t)i;
+  }
+}
+
+// out[u] = sum over sources s = 0..nsrc-1 (ascending, as the reference sums
+// pushes in ascending worker order, runtime.py:177-185) of src[idx[s][u]]
+__global__ void k_gather_sum12(const float* __restrict__ src, const int32_t* __restrict__ idx, int nsrc, int64_t ucap,
+                               const int32_t* __restrict__ count, float* __restrict__ out) {
+  const int64_t n = min((int64_t)*count, ucap);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n * 3; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = q / 3;
+    const int part = (int)(q % 3);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < nsrc; ++s) {
+      const int32_t i = idx[(int64_t)s * ucap + u];
+      if (i < 0) continue;
+      const float4 v = __ldg(reinterpret_cast<const float4*>(src + (int64_t)i * DICM_D) + part);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    reinterpret_cast<float4*>(out + u * DICM_D)[part] = acc;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int dicm_gather_rows_by_key(const dicm_table_state_t* tabs, int ntab, const int32_t* keys, const int32_t* count_dev,
+                            int64_t n_max, float* out, dicm_stream_t stream) {
+  using namespace dicm;
+  if (ntab < 1 || ntab > DICM_MAX_FIELDS) return fail(DICM_ERR_VALUE, "gather_rows_by_key: %d tables", ntab);
+  if (n_max <= 0) return DICM_OK;
+  TabRows tb{};
+  tb.n = ntab;
+  for (int i = 0; i < ntab; ++i) {
+    tb.t[i] = tabs[i].table;
+    tb.base[i] = tabs[i].base;
+  }
+  k_gather_keyed<<<dicm_grid((n_max + 9) / 10 * 32, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(tb, keys, count_dev,
+                                                                                                 n_max, out);
+  return last_launch("dicm_gather_rows_by_key");
+}
+
+int dicm_owner_reduce_rows12(const float* recv, const int32_t* inv, const int64_t* seg_dev, int nsrc,
+                             int64_t n_recv_max, const int32_t* count_dev, int64_t ucap, int32_t* idx_ws,
+                             float* out, dicm_stream_t stream) {
+  using namespace dicm;
+  if (nsrc < 1) return fail(DICM_ERR_VALUE, "owner_reduce: nsrc %d", nsrc);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (ucap <= 0) return DICM_OK;
+  int rc = check_cuda(cudaMemsetAsync(idx_ws, 0xFF, (size_t)nsrc * ucap * 4, st), "owner_reduce memset");
+  if (rc) return rc;
+  if (n_recv_max > 0)
+    k_scatter_index<<<dicm_grid(n_recv_max, 256, 148 * 8), 256, 0, st>>>(inv, seg_dev, nsrc, ucap, idx_ws);
+  k_gather_sum12<<<dicm_grid(ucap * 3, 256, 148 * 8), 256, 0, st>>>(recv, idx_ws, nsrc, ucap, count_dev, out);
+  return last_launch("dicm_owner_reduce_rows12");
+}
+
+}  // extern "C"

@@ -92,37 +92,49 @@ struct Tables {
   int n;
 };
 
+// three lanes per row, one float4 (4 of the 12 columns) each: consecutive
+// unique keys are ascending rows, so a warp's 10 rows stream contiguously
+// through dense tables
 __global__ void k_rows(const __grid_constant__ Tables tb, const int32_t* __restrict__ keys,
                        const int32_t* __restrict__ count, int64_t max_rows, const float* __restrict__ grads, float lr,
                        float b1, float b2, float eps, const int32_t* __restrict__ status) {
   if (status[DICM_ST_NONFINITE] || status[DICM_ST_KEY_FLAG]) return;
   const int64_t n = min((int64_t)*count, max_rows);
-  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
-    const Row12 g = load_row12_cg(grads + u * DICM_D);
-    bool any = false;
-#pragma unroll
-    for (int c = 0; c < DICM_D; ++c) any |= g.v[c] != 0.f;
-    if (!any) continue;  // optim.py:93-94
+  const int lane = threadIdx.x & 31, part = lane % 3, slot = lane / 3;  // lanes 30, 31 idle
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w * 10 < n; w += warps) {
+    const int64_t u = w * 10 + slot;
+    const bool live = slot < 10 && u < n;
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live) g = __ldcg(reinterpret_cast<const float4*>(grads + u * DICM_D) + part);
+    const bool nz = g.x != 0.f || g.y != 0.f || g.z != 0.f || g.w != 0.f;
+    const unsigned any = __ballot_sync(0xffffffffu, nz);
+    const unsigned grp = 7u << (3 * (lane / 3));
+    if (!live || !(any & grp)) continue;  // all-zero row: skipped (optim.py:93-94)
     const int64_t key = keys[u];
     int k = 0;
     while (k + 1 < tb.n && key >= tb.t[k + 1].base) ++k;
     const dicm_table_state_t& T = tb.t[k];
     const int64_t row = key - T.base;
     const int tt = T.t[row] + 1;
-    T.t[row] = tt;
     const float c1 = (float)(1.0 / (1.0 - pow((double)b1, (double)tt)));
     const float c2 = (float)(1.0 / (1.0 - pow((double)b2, (double)tt)));
-    float* pm = T.m + row * DICM_D;
-    float* pv = T.v + row * DICM_D;
-    float* pp = T.table + row * DICM_D;
+    float4* pm = reinterpret_cast<float4*>(T.m + row * DICM_D) + part;
+    float4* pv = reinterpret_cast<float4*>(T.v + row * DICM_D) + part;
+    float4* pp = reinterpret_cast<float4*>(T.table + row * DICM_D) + part;
+    float4 m4 = *pm, v4 = *pv, p4 = *pp;
+    const float gv[4] = {g.x, g.y, g.z, g.w};
+    float mv[4] = {m4.x, m4.y, m4.z, m4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w}, pv4[4] = {p4.x, p4.y, p4.z, p4.w};
 #pragma unroll
-    for (int c = 0; c < DICM_D; ++c) {
-      const float mi = b1 * pm[c] + (1.f - b1) * g.v[c];
-      const float vi = b2 * pv[c] + (1.f - b2) * g.v[c] * g.v[c];
-      pm[c] = mi;
-      pv[c] = vi;
-      pp[c] -= lr * (mi * c1) / (sqrtf(vi * c2) + eps);
+    for (int c = 0; c < 4; ++c) {
+      mv[c] = b1 * mv[c] + (1.f - b1) * gv[c];
+      vv[c] = b2 * vv[c] + (1.f - b2) * gv[c] * gv[c];
+      pv4[c] -= lr * (mv[c] * c1) / (sqrtf(vv[c] * c2) + eps);
     }
+    *pm = make_float4(mv[0], mv[1], mv[2], mv[3]);
+    *pv = make_float4(vv[0], vv[1], vv[2], vv[3]);
+    *pp = make_float4(pv4[0], pv4[1], pv4[2], pv4[3]);
+    if (part == 0) T.t[row] = tt;
   }
 }
 
@@ -171,7 +183,7 @@ int dicm_adam_rows(const dicm_table_state_t* tabs, int ntab, const int32_t* uniq
     if (i && tabs[i].base < tabs[i - 1].base + tabs[i - 1].vocab)
       return fail(DICM_ERR_VALUE, "adam_rows: table key ranges must be ascending and disjoint");
   }
-  k_rows<<<dicm_grid(max_rows, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(tb, uniq_keys, count_dev, max_rows,
+  k_rows<<<dicm_grid((max_rows + 9) / 10 * 32, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(tb, uniq_keys, count_dev, max_rows,
                                                                               grads, lr, beta1, beta2, eps, status);
   return last_launch("dicm_adam_rows");
 }

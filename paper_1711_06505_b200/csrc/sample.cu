@@ -79,7 +79,7 @@ __device__ __forceinline__ void load_query(const Args& a, int ch, int b, float (
 #pragma unroll
     for (int f = 0; f < DQ / DICM_D; ++f) {
       const int fi = a.L.query_field[f];
-      const Row12 r = load_row12(a.V.tables[fi] + (int64_t)a.V.field_ids[fi][b] * DICM_D);
+      const Row12 r = load_row12(a.V.tables[fi] + (int64_t)a.V.field_inv[fi][b] * DICM_D);
 #pragma unroll
       for (int c = 0; c < DICM_D; ++c) q[f * DICM_D + c] = r.v[c];
     }
@@ -179,10 +179,10 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_sample_fwd(const __grid_cons
     for (int f = 0; f < a.L.n_fields; ++f) {
       const float* T = a.V.tables[f];
       if (!a.L.field_multi[f]) {
-        if (lane < DICM_D) row[a.L.field_col[f] + lane] = __ldg(T + (int64_t)a.V.field_ids[f][b] * DICM_D + lane);
+        if (lane < DICM_D) row[a.L.field_col[f] + lane] = __ldg(T + (int64_t)a.V.field_inv[f][b] * DICM_D + lane);
       } else {
         const int32_t* off = a.V.field_off[f];
-        const int32_t* ids = a.V.field_ids[f];
+        const int32_t* ids = a.V.field_inv[f];  // rows of the compact table
         float acc[DICM_D];
 #pragma unroll
         for (int c = 0; c < DICM_D; ++c) acc[c] = 0.f;

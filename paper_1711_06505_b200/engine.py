@@ -1,21 +1,23 @@
-"""The device training step (single GPU): the kernel sequence behind
-``LocalTrainer.train_batch`` (reference training.py:66-91).
+"""The device training step: the kernel sequence behind ``LocalTrainer.train_batch``
+(reference training.py:66-91) and, in ``runtime.ClusterEngine``, behind one
+rank of ``Cluster.run_iteration`` (runtime.py:370-470).
 
 One step, all on one CUDA stream, no host round trip until the loss is read:
 
-  H2D   one packed copy of the CSR batch (ids, offsets, labels)
-  a2    dicm_dedup over the image keys  -> unique rows + inverse
-  a2    dicm_dedup over every ID field  -> unique (field,row) keys + inverse
-  a3-a4 dicm_imgmlp_fwd on the unique rows -> E [U,12]
-  a6-10 dicm_sample_fwd -> head input x [B, W]
-  a11-12 dicm_head_fwd_bwd -> logits, dLoss/dx, head-grad partials
-  a6-10 dicm_sample_bwd -> dE [U,12], dRows [K,12], attention-grad partials
-  a5    dicm_imgmlp_bwd -> img/* gradients
-  a14   dicm_adam_dense (all dense params) + dicm_adam_rows (unique ID rows)
+  H2D    one packed copy of the CSR batch (ids, offsets, labels)
+  a2     dicm_dedup over the image keys    -> unique pool rows + inverse
+  a2     dicm_dedup over every ID field    -> unique (field,row) keys + inverse
+  a3-a4  dicm_imgmlp_fwd on the unique rows -> E [U,12]
+  a10    dicm_gather_rows_by_key           -> compact ID rows [K,12]
+  a6-10  dicm_sample_fwd                   -> head input x [B, W]
+  a11-12 dicm_head_fwd_bwd                 -> logits, dLoss/dx, head-grad partials
+  a6-10  dicm_sample_bwd                   -> dE [U,12], dRows [K,12], attention partials
+  a5     dicm_imgmlp_bwd                   -> img/* gradients
+  a14    dicm_adam_dense + dicm_adam_rows
 
-Buffers are sized by capacity and reused; the dedup counts never leave the
-device.  Status words latch out-of-vocabulary ids and non-finite values; the
-update kernels refuse to run on a flagged step and the host raises the
+Buffers are sized by capacity and reused; data-dependent counts never leave
+the device.  Status words latch out-of-vocabulary ids and non-finite values;
+the update kernels refuse to run on a flagged step and the host raises the
 reference's exception when it reads the status.
 """
 
@@ -39,8 +41,9 @@ def lr_schedule(iteration, lr0=0.001, decay=0.9, interval=24000):
     return lr0 * decay ** (iteration // interval)
 
 
-def _u8(n, dev):
-    return torch.empty(max(int(n), 1), dtype=torch.uint8, device=dev)
+def _u8(n, dev, zero=False):
+    f = torch.zeros if zero else torch.empty
+    return f(max(int(n), 1), dtype=torch.uint8, device=dev)
 
 
 class Packed:
@@ -82,6 +85,9 @@ class Packed:
         host[self.beh_off:self.beh_off + self.B + 1] = batch.beh_off
         host[self.labels:self.labels + self.B] = np.asarray(batch.labels, dtype=np.float32).view(np.int32)
 
+    def n_id(self, fields):
+        return sum(self.B if not f.multi else self.multi[f.name][1] for f in fields)
+
 
 class DeviceBatch:
     __slots__ = ("pk", "packed")
@@ -90,10 +96,31 @@ class DeviceBatch:
         self.pk, self.packed = pk, packed
 
 
-class StepEngine:
-    """Owns the optimizer state and the step buffers of one model replica."""
+class ImageNetBuffers:
+    """Activations + workspace of one image-MLP pass over up to ``cap`` rows."""
 
-    def __init__(self, model, pool, precision="fp32", lr0=0.001, lr_decay=0.9, lr_interval=24000):
+    def __init__(self, cap, d_raw, prec_code, dev):
+        cu = max(int(cap), 1)
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.cap = int(cap)
+        self.act0 = torch.empty((cu, 256), **f32)
+        self.act1 = torch.empty((cu, 64), **f32)
+        self.emb = torch.empty((cu, 12), **f32)
+        self.d_emb = torch.empty((cu, 12), **f32)
+        # zeroed once: rows past the live count are read (and multiplied by
+        # zero-filled gathers) by the tensor-core backward, so they must be finite
+        self.ws = _u8(L.lib.dicm_imgmlp_workspace(self.cap, d_raw, prec_code), dev, zero=True)
+
+
+class StepEngine:
+    """Owns the optimizer state and the step buffers of one model replica.
+
+    ``world``/``id_align``: the ID key space puts table f at base_f, aligned to
+    ``id_align`` so that a key's owner in a sharded run is simply key % world
+    (see runtime.ClusterEngine); a single GPU uses id_align = 1.
+    """
+
+    def __init__(self, model, pool, precision="fp32", lr0=0.001, lr_decay=0.9, lr_interval=24000, id_align=1):
         if precision not in L.PRECISIONS:
             raise ValueError(f"precision must be one of {tuple(L.PRECISIONS)}")
         if precision == "bf16" and pool.dtype_name != "bf16":
@@ -108,11 +135,11 @@ class StepEngine:
         dev = self.dev = model.device
         lay = model.layout
         self.fields = list(model.schema.fields)
-        # ID key space: tables back to back
+        # global ID key space: field f at bases[f] (aligned), vocab = schema vocab
         self.bases, base = [], 0
         for f in self.fields:
             self.bases.append(base)
-            base += model.tables[f.name].shape[0]
+            base += -(-f.vocab // id_align) * id_align
         self.id_key_space = base
         self.status = torch.zeros(L.STATUS_WORDS, dtype=torch.int32, device=dev)
         # optimizer state (reference training.py:53-60)
@@ -131,14 +158,9 @@ class StepEngine:
         self.tv = {f.name: torch.zeros_like(model.tables[f.name]) for f in self.fields}
         self.tt = {f.name: torch.zeros(model.tables[f.name].shape[0], dtype=torch.int32, device=dev)
                    for f in self.fields}
-        self.tabstate = (L.TableState * len(self.fields))()
-        for i, f in enumerate(self.fields):
-            ts = self.tabstate[i]
-            ts.table, ts.m, ts.v, ts.t = (model.tables[f.name].data_ptr(), self.tm[f.name].data_ptr(),
-                                         self.tv[f.name].data_ptr(), self.tt[f.name].data_ptr())
-            ts.base, ts.vocab = self.bases[i], model.tables[f.name].shape[0]
+        self.tabstate = self._table_states(self.bases, 1)
         self.ws_id = _u8(L.lib.dicm_dedup_workspace(max(self.id_key_space, 1)), dev)
-        self.ws_img = _u8(L.lib.dicm_dedup_workspace(max(pool.local_rows, 1)), dev)
+        self.ws_img = _u8(L.lib.dicm_dedup_workspace(max(self.image_key_space, 1)), dev)
         # static kernel descriptors
         self.layout = self._layout_struct()
         self.attn = (L.AttnParams * 2)()
@@ -174,6 +196,22 @@ class StepEngine:
         self._pin_i = 0
 
     # ------------------------------------------------------------------
+    @property
+    def image_key_space(self):
+        """Image ids are pool rows of THIS engine's pool."""
+        return self.pool.local_rows
+
+    def _table_states(self, bases, divisor):
+        """Row-Adam / row-gather descriptors over the local tables, keyed by
+        global combined keys divided by ``divisor`` (owner-local keys)."""
+        ts_arr = (L.TableState * len(self.fields))()
+        for i, f in enumerate(self.fields):
+            ts = ts_arr[i]
+            ts.table, ts.m, ts.v, ts.t = (self.model.tables[f.name].data_ptr(), self.tm[f.name].data_ptr(),
+                                         self.tv[f.name].data_ptr(), self.tt[f.name].data_ptr())
+            ts.base, ts.vocab = bases[i] // divisor, self.model.tables[f.name].shape[0]
+        return ts_arr
+
     def _layout_struct(self):
         m = self.model
         lay = m.layout
@@ -198,19 +236,21 @@ class StepEngine:
             st.query_col[i] = ho["field/" + q]
         return st
 
+    def _n_img(self, B, R):
+        lay = self.model.layout
+        return (B if lay.use_ad_image else 0) + (R if lay.use_behavior_images else 0)
+
     def _ensure(self, pk):
         B, R = pk.B, pk.R
-        n_id = sum(B if not f.multi else pk.multi[f.name][1] for f in self.fields)
-        need = (pk.total, B, R, n_id)
+        need = (pk.total, B, R, pk.n_id(self.fields))
         if self.cap is not None and all(a <= b for a, b in zip(need, self.cap)):
             return
         if self.cap is not None:  # grow with headroom
             need = tuple(max(int(a * 1.25), b) for a, b in zip(need, self.cap))
         total, B, R, n_id = need
         dev = self.dev
-        lay = self.model.layout
-        n_img = (B if lay.use_ad_image else 0) + (R if lay.use_behavior_images else 0)
-        self.cap_u = min(n_img, self.pool.local_rows)
+        n_img = self._n_img(B, R)
+        self.cap_u = min(n_img, self.image_key_space)
         self.cap_k = min(n_id, self.id_key_space)
         i32 = dict(dtype=torch.int32, device=dev)
         f32 = dict(dtype=torch.float32, device=dev)
@@ -219,12 +259,8 @@ class StepEngine:
         self.inv_img = torch.empty(max(n_img, 1), **i32)
         self.uniq_id = torch.empty(max(self.cap_k, 1), **i32)
         self.inv_id = torch.empty(max(n_id, 1), **i32)
-        self.counts = torch.zeros(4, **i32)  # [U_img, K_id, ...]
-        cu = max(self.cap_u, 1)
-        self.act0 = torch.empty((cu, 256), **f32)
-        self.act1 = torch.empty((cu, 64), **f32)
-        self.emb = torch.empty((cu, 12), **f32)
-        self.d_emb = torch.empty((cu, 12), **f32)
+        self.counts = torch.zeros(8, **i32)  # [U_img, K_id, U_owner, K_owner, ...]
+        self.id_rows = torch.empty((max(self.cap_k, 1), 12), **f32)
         self.d_rows = torch.empty((max(self.cap_k, 1), 12), **f32)
         self.head_in = torch.empty((max(B, 1), self.width), **f32)
         self.d_head_in = torch.empty((max(B, 1), self.width), **f32)
@@ -236,11 +272,20 @@ class StepEngine:
         self.loss_part = torch.empty(L.lib.dicm_head_blocks(max(B, 1)), **f32)
         self.attn_partial = torch.empty((L.lib.dicm_sample_blocks(max(B, 1)), max(self.attn_part, 1)), **f32)
         self.loss = torch.zeros(1, **f32)
-        # zeroed once: rows past the live count are read (and multiplied by
-        # zero-filled gathers) by the tensor-core backward, so they must be finite
-        self.mlp_ws = torch.zeros(max(int(L.lib.dicm_imgmlp_workspace(self.cap_u, self.pool.d_raw, self.prec_code)),
-                                      1), dtype=torch.uint8, device=dev)
+        self._alloc_image_net(self.cap_u)
         self.cap = need
+
+    def _alloc_image_net(self, cap):
+        self.net = ImageNetBuffers(cap, self.pool.d_raw, self.prec_code, self.dev)
+
+    # views kept for callers / tests
+    @property
+    def emb(self):
+        return self.net.emb
+
+    @property
+    def d_emb(self):
+        return self.net.d_emb
 
     def _pinned_buf(self, n):
         i = self._pin_i
@@ -272,54 +317,80 @@ class StepEngine:
     def h2d_bytes(self, batch):
         return Packed(self.model, batch).total * 4
 
-    def forward_backward(self, db, denominator=None):
-        """Everything up to (and including) the dense gradients."""
-        m, lay = self.model, self.model.layout
-        pk = db.pk
+    # ---- phases --------------------------------------------------------
+    def _begin(self, db):
+        self.pk = db.pk
         base_ptr = db.packed.data_ptr()
         self._dptr = lambda off: base_ptr + 4 * off
-        s = L.stream_handle()
-        B, R = pk.B, pk.R
-        denom = float(B if denominator is None else denominator)
-        st = self.status.data_ptr()
-        cnt = self.counts
-        # a2: image-key dedup (model.py:182-187)
-        img_segs, inv_off = [], 0
+        self.s = L.stream_handle()
+
+    def _dedup_images(self):
+        """a2 over the image keys (model.py:182-187) -> uniq_img, inv_img, counts[0]."""
+        lay, pk = self.model.layout, self.pk
+        segs, inv_off = [], 0
+        space = self.pool.global_size if getattr(self, "world", 1) > 1 else self.image_key_space
         if lay.use_ad_image:
-            img_segs.append(L.KeySeg(self._dptr(pk.ad), B, 0, self.pool.local_rows, inv_off))
-            inv_off += B
+            segs.append(L.KeySeg(self._dptr(pk.ad), pk.B, 0, space, inv_off))
+            inv_off += pk.B
         if lay.use_behavior_images:
-            img_segs.append(L.KeySeg(self._dptr(pk.beh), R, 0, self.pool.local_rows, inv_off))
-        n_img = len(img_segs)
-        if n_img:
-            arr = (L.KeySeg * n_img)(*img_segs)
-            L.check(L.lib.dicm_dedup(arr, n_img, self.pool.local_rows, self.ws_img.data_ptr(), self.ws_img.numel(),
-                                     self.uniq_img.data_ptr(), self.inv_img.data_ptr(), cnt[0:].data_ptr(), 0, st, s))
-        # a2: ID dedup over all tables (Batch.unique_field_ids, model.py:152-155)
-        id_segs, inv_id_off, off = [], {}, 0
+            segs.append(L.KeySeg(self._dptr(pk.beh), pk.R, 0, space, inv_off))
+        self.n_img_segs = len(segs)
+        if segs:
+            arr = (L.KeySeg * len(segs))(*segs)
+            L.check(L.lib.dicm_dedup(arr, len(segs), space, self.ws_img.data_ptr(), self.ws_img.numel(),
+                                     self.uniq_img.data_ptr(), self.inv_img.data_ptr(), self.counts.data_ptr(), 0,
+                                     self.status.data_ptr(), self.s))
+
+    def _dedup_ids(self):
+        """a2 over every ID field (Batch.unique_field_ids, model.py:152-155)."""
+        pk = self.pk
+        segs, self.inv_id_off, off = [], {}, 0
         for i, f in enumerate(self.fields):
             if f.multi:
                 a, n, _ = pk.multi[f.name]
-                id_segs.append(L.KeySeg(self._dptr(a), n, self.bases[i], m.tables[f.name].shape[0], off))
+                segs.append(L.KeySeg(self._dptr(a), n, self.bases[i], f.vocab, off))
             else:
-                n = B
-                id_segs.append(L.KeySeg(self._dptr(pk.onehot[f.name]), n, self.bases[i],
-                                        m.tables[f.name].shape[0], off))
-            inv_id_off[f.name] = off
+                n = pk.B
+                segs.append(L.KeySeg(self._dptr(pk.onehot[f.name]), n, self.bases[i], f.vocab, off))
+            self.inv_id_off[f.name] = off
             off += n
-        arr = (L.KeySeg * len(id_segs))(*id_segs)
-        L.check(L.lib.dicm_dedup(arr, len(id_segs), self.id_key_space, self.ws_id.data_ptr(), self.ws_id.numel(),
-                                 self.uniq_id.data_ptr(), self.inv_id.data_ptr(), cnt[1:].data_ptr(), 1, st, s))
-        # a3-a4: image MLP forward on the unique rows
-        cu = self.cap_u
+        arr = (L.KeySeg * len(segs))(*segs)
+        L.check(L.lib.dicm_dedup(arr, len(segs), self.id_key_space, self.ws_id.data_ptr(), self.ws_id.numel(),
+                                 self.uniq_id.data_ptr(), self.inv_id.data_ptr(), self.counts[1:].data_ptr(), 1,
+                                 self.status.data_ptr(), self.s))
+
+    def _image_forward(self, net, rows, count_ptr):
+        """a3-a4: image MLP on pool rows rows[0..*count) -> net.emb."""
         ev = self._ev("imgmlp_fwd")
-        if n_img:
-            L.check(L.lib.dicm_imgmlp_fwd(self.pool.rows.data_ptr(), self.pool.dtype_code, self.pool.d_raw,
-                                          self.uniq_img.data_ptr(), cnt[0:].data_ptr(), cu, C.byref(self.img_p),
-                                          self.act0.data_ptr(), self.act1.data_ptr(), self.emb.data_ptr(),
-                                          self.prec_code, self.mlp_ws.data_ptr(), self.mlp_ws.numel(), s))
+        L.check(L.lib.dicm_imgmlp_fwd(self.pool.rows.data_ptr(), self.pool.dtype_code, self.pool.d_raw,
+                                      rows.data_ptr(), count_ptr, net.cap, C.byref(self.img_p), net.act0.data_ptr(),
+                                      net.act1.data_ptr(), net.emb.data_ptr(), self.prec_code, net.ws.data_ptr(),
+                                      net.ws.numel(), self.s))
         self._ev_end(ev)
-        # a6-a10 forward
+
+    def _image_backward(self, net, rows, count_ptr, cap):
+        """a5: reverse path into the shared image MLP (img/* gradients)."""
+        ev = self._ev("imgmlp_bwd")
+        L.check(L.lib.dicm_imgmlp_bwd(self.pool.rows.data_ptr(), self.pool.dtype_code, self.pool.d_raw,
+                                      rows.data_ptr(), count_ptr, cap, C.byref(self.img_p), net.act0.data_ptr(),
+                                      net.act1.data_ptr(), net.d_emb.data_ptr(), C.byref(self.img_g), self.prec_code,
+                                      net.ws.data_ptr(), net.ws.numel(), self.s))
+        self._ev_end(ev)
+
+    def _gather_id_rows(self):
+        """Compact ID rows of the batch's unique keys (rows(table, ids) with
+        the dedup applied, model.py:407-408)."""
+        L.check(L.lib.dicm_gather_rows_by_key(self.tabstate, len(self.fields), self.uniq_id.data_ptr(),
+                                              self.counts[1:].data_ptr(), self.cap_k, self.id_rows.data_ptr(),
+                                              self.s))
+
+    def _local_step(self, emb, d_emb, denom):
+        """a6-a12 forward and backward on the local batch: pooling, head, BCE.
+        Reads image embeddings ``emb`` and compact ID rows ``self.id_rows``;
+        writes ``d_emb`` / ``self.d_rows`` and the head/attention gradients."""
+        lay, pk, s = self.model.layout, self.pk, self.s
+        B, R = pk.B, pk.R
+        st = self.status.data_ptr()
         bv = L.BatchView()
         bv.batch, bv.refs = B, R
         for i, f in enumerate(self.fields):
@@ -329,29 +400,25 @@ class StepEngine:
                 bv.field_off[i] = self._dptr(o)
             else:
                 bv.field_ids[i] = self._dptr(pk.onehot[f.name])
-            bv.tables[i] = m.tables[f.name].data_ptr()
-            bv.field_inv[i] = self.inv_id.data_ptr() + 4 * inv_id_off[f.name]
+            bv.tables[i] = self.id_rows.data_ptr()
+            bv.field_inv[i] = self.inv_id.data_ptr() + 4 * self.inv_id_off[f.name]
         bv.ad_local = self.inv_img.data_ptr() if lay.use_ad_image else None
         bv.beh_local = self.inv_img.data_ptr() + 4 * (B if lay.use_ad_image else 0)
         bv.beh_off = self._dptr(pk.beh_off)
-        bv.emb = self.emb.data_ptr()
-        self._bv = bv
+        bv.emb = emb.data_ptr()
         L.check(L.lib.dicm_sample_fwd(C.byref(self.layout), C.byref(bv), self.attn, self.head_in.data_ptr(),
                                       self.scores.data_ptr(), self.stats.data_ptr(), s))
-        # a11-a12 head forward + backward
         L.check(L.lib.dicm_head_fwd_bwd(self.head_in.data_ptr(), B, self.width, self._dptr(pk.labels),
                                         1.0 / denom, C.byref(self.head_p), self.logits.data_ptr(),
                                         self.d_head_in.data_ptr(), self.head_part.data_ptr(),
                                         self.loss_part.data_ptr(), s))
         nhb = L.lib.dicm_head_blocks(B)
         L.check(L.lib.dicm_loss_finalize(self.loss_part.data_ptr(), nhb, 1.0 / denom, self.loss.data_ptr(), st, s))
-        # a6-a10 backward
-        self.d_emb.zero_()
+        d_emb.zero_()
         self.d_rows.zero_()
         L.check(L.lib.dicm_sample_bwd(C.byref(self.layout), C.byref(bv), self.attn, self.head_in.data_ptr(),
                                       self.d_head_in.data_ptr(), self.scores.data_ptr(), self.stats.data_ptr(),
-                                      self.d_emb.data_ptr(), self.d_rows.data_ptr(), self.attn_partial.data_ptr(),
-                                      s))
+                                      d_emb.data_ptr(), self.d_rows.data_ptr(), self.attn_partial.data_ptr(), s))
         h0, h1 = self.head_range
         L.check(L.lib.dicm_reduce_partials(self.head_part.data_ptr(), nhb, h1 - h0,
                                            self.grad.data_ptr() + 4 * h0, 0, s))
@@ -359,53 +426,34 @@ class StepEngine:
             a0, a1 = self.attn_range
             L.check(L.lib.dicm_reduce_partials(self.attn_partial.data_ptr(), L.lib.dicm_sample_blocks(B), a1 - a0,
                                                self.grad.data_ptr() + 4 * a0, 0, s))
-        # a5: image MLP backward
-        ev = self._ev("imgmlp_bwd")
-        L.check(L.lib.dicm_imgmlp_bwd(self.pool.rows.data_ptr(), self.pool.dtype_code, self.pool.d_raw,
-                                      self.uniq_img.data_ptr(), cnt[0:].data_ptr(), cu if n_img else 0,
-                                      C.byref(self.img_p), self.act0.data_ptr(), self.act1.data_ptr(),
-                                      self.d_emb.data_ptr(), C.byref(self.img_g), self.prec_code,
-                                      self.mlp_ws.data_ptr(), self.mlp_ws.numel(), s))
-        self._ev_end(ev)
+
+    def forward_backward(self, db, denominator=None):
+        """Everything up to (and including) the dense gradients."""
+        self._begin(db)
+        denom = float(db.pk.B if denominator is None else denominator)
+        self._dedup_images()
+        self._dedup_ids()
+        if self.n_img_segs:
+            self._image_forward(self.net, self.uniq_img, self.counts.data_ptr())
+        self._gather_id_rows()
+        self._local_step(self.net.emb, self.net.d_emb, denom)
+        self._image_backward(self.net, self.uniq_img, self.counts.data_ptr(), self.cap_u if self.n_img_segs else 0)
         return self.loss
 
-    def _ev(self, name):
-        if self.probe is None:
-            return None
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        self.probe.setdefault(name, []).append((a, b))
-        return b
-
-    @staticmethod
-    def _ev_end(ev):
-        if ev is not None:
-            ev.record()
-
-    @property
-    def launches_per_step(self):
-        """Kernels this engine launches per step (memsets included), counted
-        from the kernel sequence of each C-ABI call (see DESIGN.md)."""
-        lay = self.model.layout
-        n = 6 + 6  # two dedups: memset + mark + tile sums + scan + emit + inverse
-        n += 3 if self.prec_code == L.PREC_FP32 else 3  # image MLP fwd: layer0, layer1, layer2
-        n += 1 + 1 + 1  # sample fwd, head, loss
-        n += 2 + 1 + 1 + (1 if lay.attentive else 0)  # zero dE/dRows, sample bwd, reduces
-        n += 12  # image MLP bwd (layer-2 bwd + 4 reduces, dh1 GEMM + 2 reduces, dW1 + reduce, dW0 + reduce)
-        n += 1 + 4 + 1  # check_finite, adam dense (memset + 3), adam rows
-        return n
-
-    def optimizer_step(self, lr):
+    def optimizer_step(self, lr, row_keys=None, row_count=None, row_grads=None, row_cap=None, tabstate=None):
         s = L.stream_handle()
         st = self.status.data_ptr()
-        L.check(L.lib.dicm_check_finite(self.d_rows.data_ptr(), self.d_rows.numel(), self.counts[1:].data_ptr(), 12,
-                                        4, st, s))
+        row_keys = self.uniq_id if row_keys is None else row_keys
+        row_count = self.counts[1:] if row_count is None else row_count
+        row_grads = self.d_rows if row_grads is None else row_grads
+        row_cap = self.cap_k if row_cap is None else row_cap
+        tabstate = self.tabstate if tabstate is None else tabstate
+        L.check(L.lib.dicm_check_finite(row_grads.data_ptr(), row_cap * 12, row_count.data_ptr(), 12, 4, st, s))
         L.check(L.lib.dicm_adam_dense(self.model.dense.data_ptr(), self.grad.data_ptr(), self.m.data_ptr(),
                                       self.v.data_ptr(), self.t.data_ptr(), self.spans, len(self.spans), lr, BETA1,
                                       BETA2, EPS, self.adam_ws.data_ptr(), self.adam_ws.numel(), st, s))
-        L.check(L.lib.dicm_adam_rows(self.tabstate, len(self.fields), self.uniq_id.data_ptr(),
-                                     self.counts[1:].data_ptr(), self.cap_k, self.d_rows.data_ptr(), lr, BETA1, BETA2,
-                                     EPS, st, s))
+        L.check(L.lib.dicm_adam_rows(tabstate, len(self.fields), row_keys.data_ptr(), row_count.data_ptr(), row_cap,
+                                     row_grads.data_ptr(), lr, BETA1, BETA2, EPS, st, s))
 
     def lr(self):
         return lr_schedule(self.iteration, self.lr0, self.lr_decay, self.lr_interval)
@@ -426,8 +474,10 @@ class StepEngine:
             tag, seg = divmod(int(st[L.ST_KEY_SEG]), 16)
             if tag == 0:
                 raise KeyError(f"unknown image id {int(st[L.ST_KEY_VALUE])} (store holds 0.."
-                               f"{self.pool.local_rows - 1})")
-            f = self.fields[seg]
+                               f"{self.pool.global_size - 1})")
+            f = self.fields[seg] if tag == 1 else None
+            if f is None:
+                raise KeyError(f"key {int(st[L.ST_KEY_VALUE])} outside this shard")
             raise KeyError(f"id {int(st[L.ST_KEY_VALUE])} outside vocabulary of size {f.vocab} "
                            f"(field {f.name})")
         if st[L.ST_NONFINITE]:
@@ -436,6 +486,34 @@ class StepEngine:
             if bits & 1:
                 raise FloatingPointError(f"non-finite loss at iteration {self.iteration - 1}")
             raise FloatingPointError("adam: non-finite gradient, parameter untouched")
+
+    # -- instrumentation ---------------------------------------------
+    def _ev(self, name):
+        if self.probe is None:
+            return None
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        self.probe.setdefault(name, []).append((a, b))
+        return b
+
+    @staticmethod
+    def _ev_end(ev):
+        if ev is not None:
+            ev.record()
+
+    @property
+    def launches_per_step(self):
+        """Kernels this engine launches per step (memsets included), counted
+        from the kernel sequence of each C-ABI call (see DESIGN.md)."""
+        lay = self.model.layout
+        n = 6 + 6  # two dedups: memset + mark + tile sums + scan + emit + inverse
+        if self.prec_code == L.PREC_FP32:
+            n += 3 + 1 + 2 + 1 + (1 if lay.attentive else 0) + 1 + 4 + 12  # fwd, gather, zero, sample, reduces, bwd
+        else:
+            n += 2 + 1 + 2 + 1 + (1 if lay.attentive else 0) + 1 + 4 + 11
+        n += 1 + 1 + 1  # sample fwd, head, loss
+        n += 1 + 4 + 1  # check_finite, adam dense (memset + 3), adam rows
+        return n
 
     # -- inspection ---------------------------------------------------
     def unique_images(self):

@@ -79,7 +79,22 @@ class DicmModel:
 
     def __init__(self, schema, aggregator, extractor=None, seed=0, mlp_widths=(128, 64),
                  use_ad_image=True, use_behavior_images=True, device="cuda", params=None,
-                 table_rows=None):
+                 table_rows=None, shard=None):
+        """``shard=(world, rank)``: hold only the ID-table rows this rank owns
+        (row % world == rank, at local row row // world), with exactly the
+        values the full reference init gives them."""
+        if shard is not None and table_rows is None:
+            world, rank = shard
+
+            def table_rows(f, name):
+                full = host[name] if name in (params or {}) else S.init_param(seed, name, (f.vocab, schema.d_id),
+                                                                             "table")
+                local = np.asarray(full)[rank::world]
+                n_local = -(-f.vocab // world)
+                out = np.zeros((n_local, schema.d_id))
+                out[:len(local)] = local
+                return torch.as_tensor(out, dtype=torch.float32).to(device)
+        self.shard = shard
         layout = ModelLayout(schema, aggregator, tuple(mlp_widths), use_ad_image, use_behavior_images)
         S.validate_layout(layout, None if extractor is None else extractor.out_dim)
         check_hot_path(layout)

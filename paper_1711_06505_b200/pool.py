@@ -64,10 +64,13 @@ class ImagePool:
         return self.rows.shape[0]
 
     @classmethod
-    def from_rows(cls, rows, dtype="fp32", device="cuda"):
+    def from_rows(cls, rows, dtype="fp32", device="cuda", world=1, rank=0):
+        """``rows``: the GLOBAL [P, d_raw] matrix; a sharded pool keeps rows
+        id % world == rank (reference placement: shard_of, runtime.py:60-68)."""
         tdt, _ = _DT[dtype]
-        t = torch.as_tensor(np.asarray(rows, dtype=np.float32)).to(device=device, dtype=tdt)
-        return cls(t)
+        rows = np.asarray(rows, dtype=np.float32)
+        t = torch.as_tensor(rows[rank::world]).to(device=device, dtype=tdt)
+        return cls(t, world, rank, rows.shape[0])
 
     @classmethod
     def from_latents(cls, latents, extractor, dtype="fp32", device="cuda", world=1, rank=0,

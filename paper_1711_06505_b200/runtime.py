@@ -1,0 +1,342 @@
+"""Multi-GPU AMS training: the drop-in for the reference ``Cluster``
+(runtime.py:313-516) and ``run_training`` (runtime.py:519-554).
+
+One process per GPU; every GPU hosts one worker (a contiguous slice of the
+union batch, runtime.py:379-382) and one server (the image-pool rows and
+ID-table rows it owns, runtime.py:98-124).  A key is owned by rank
+key % world and stored there at row key // world (any balanced placement is
+valid).  One iteration (reference phases, runtime.py:378-463):
+
+  1. local dedup of image keys and ID keys              (a2, on device)
+  2. bucket unique keys by owner; all-to-all of counts (the one host sync),
+     then all-to-all-v of the keys                       (C1, C3 of SURVEY 2.2)
+  3. owner: dedup across sources, image MLP forward once per distinct image,
+     gather ID rows; all-to-all-v the rows back          (C2, C3)
+  4. local pooling + head forward/backward               (a6-a12)
+  5. all-to-all-v the embedding and ID-row gradients to the owners; owners
+     reduce per key in ascending source order (no float atomics) (C4, C5)
+  6. owner: image MLP backward; ONE all-reduce(sum) over the fused buffer of
+     every dense gradient (head, attention, image net)   (C6 + C7)
+  7. Adam on the (bit-identical) dense replicas, row Adam on owned ID rows.
+
+Collectives are NCCL calls through torch.distributed on the compute stream.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import zlib
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib as L
+from .batch import Batch, encode_batch
+from .engine import ImageNetBuffers, StepEngine, _u8, lr_schedule
+
+MODES = ("ams", "ps-store-in-server", "store-in-worker")
+
+
+@dataclass
+class ClusterConfig:
+    workers: int = 4
+    servers: int = 2
+    mode: str = "ams"
+    batch_per_worker: int = 64
+    deterministic: bool = True
+
+    def __post_init__(self):
+        if self.workers < 1 or self.servers < 1:
+            raise ValueError("cluster needs at least one worker and one server")
+        if self.mode not in MODES:
+            raise ValueError(f"unknown mode {self.mode!r}; use one of {MODES}")
+
+
+def shard_of(key, n):
+    """Stable hash placement (reference runtime.py:60-68), kept for API parity;
+    the device path places key k on rank k % n."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    if not isinstance(key, (str, bytes)):
+        key = repr(key)
+    if isinstance(key, str):
+        key = key.encode()
+    return zlib.crc32(key) % n
+
+
+def params_digest(params):
+    """Order-independent fingerprint of a named parameter set (runtime.py:79-86)."""
+    h = hashlib.sha256()
+    for name in sorted(params):
+        arr = params[name]
+        arr = arr.data if hasattr(arr, "data") and not isinstance(arr, np.ndarray) else arr
+        h.update(name.encode())
+        h.update(np.ascontiguousarray(arr).tobytes())
+    return h.hexdigest()
+
+
+@dataclass
+class RunLog:
+    losses: list = field(default_factory=list)
+    lrs: list = field(default_factory=list)
+    embed_forwards: list = field(default_factory=list)
+    unique_images: list = field(default_factory=list)
+    replica_digests: list = field(default_factory=list)
+
+
+def _a2a(out, inp, out_splits, in_splits, group=None):
+    """all-to-all-v along dim 0 (NCCL on GPU tensors, gloo on CPU tensors)."""
+    dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
+
+
+def exchange_counts(send_counts, group=None):
+    """[world, k] int32 per-destination counts -> ([world, k] send, [world, k]
+    recv) on the host; the single host synchronisation of an iteration."""
+    recv = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv, send_counts.contiguous(), group=group)
+    both = torch.cat([send_counts, recv]).cpu()
+    w = send_counts.shape[0]
+    return both[:w], both[w:]
+
+
+class ClusterEngine(StepEngine):
+    """One rank of the sharded AMS step."""
+
+    def __init__(self, model, pool, precision="fp32", lr0=0.001, lr_decay=0.9, lr_interval=24000, world=1, rank=0,
+                 group=None):
+        if pool.world != world or pool.rank != rank:
+            raise ValueError(f"pool shard ({pool.world}, {pool.rank}) != rank ({world}, {rank})")
+        self.world, self.rank, self.group = world, rank, group
+        super().__init__(model, pool, precision, lr0, lr_decay, lr_interval, id_align=world)
+        dev = self.dev
+        # owner-side descriptors: owner-local key = global key // world
+        self.owner_tabstate = self._table_states(self.bases, world)
+        self.local_id_space = self.id_key_space // world
+        self.ws_id_owner = _u8(L.lib.dicm_dedup_workspace(max(self.local_id_space, 1)), dev)
+        self.ws_img_owner = _u8(L.lib.dicm_dedup_workspace(max(pool.local_rows, 1)), dev)
+        self.segs_img = torch.zeros(world + 1, dtype=torch.int64, device=dev)
+        self.segs_id = torch.zeros(world + 1, dtype=torch.int64, device=dev)
+        self._seg_host = torch.zeros(2 * (world + 1), dtype=torch.int64, pin_memory=True)
+
+    @property
+    def image_key_space(self):
+        return self.pool.global_size  # requests are in global image ids
+
+    def _alloc_image_net(self, cap):
+        dev, G = self.dev, self.world
+        i32 = dict(dtype=torch.int32, device=dev)
+        f32 = dict(dtype=torch.float32, device=dev)
+        cu, ck = max(self.cap_u, 1), max(self.cap_k, 1)
+        # requester side
+        self.emb_l = torch.empty((cu, 12), **f32)
+        self.d_emb_l = torch.empty((cu, 12), **f32)
+        self.send_img = torch.empty(cu, **i32)
+        self.perm_img = torch.empty(cu, **i32)
+        self.send_id = torch.empty(ck, **i32)
+        self.perm_id = torch.empty(ck, **i32)
+        self.cnt_pair = torch.zeros((G, 2), **i32)
+        self.ws_bucket = _u8(L.lib.dicm_bucket_workspace(max(cu, ck), G), dev)
+        self.rows_buf = torch.empty((max(cu, ck), 12), **f32)  # responses in / pushes out
+        # owner side (worst case: every rank asks for all its keys here)
+        self.cap_ri, self.cap_rk = G * cu, G * ck
+        self.recv_img = torch.empty(self.cap_ri, **i32)
+        self.recv_id = torch.empty(self.cap_rk, **i32)
+        self.cap_o = min(self.cap_ri, self.pool.local_rows)
+        self.cap_ko = min(self.cap_rk, self.local_id_space)
+        self.uniq_o = torch.empty(max(self.cap_o, 1), **i32)
+        self.inv_o = torch.empty(self.cap_ri, **i32)
+        self.uniq_id_o = torch.empty(max(self.cap_ko, 1), **i32)
+        self.inv_id_o = torch.empty(self.cap_rk, **i32)
+        self.resp = torch.empty((max(self.cap_ri, self.cap_rk), 12), **f32)
+        self.d_rows_o = torch.empty((max(self.cap_ko, 1), 12), **f32)
+        self.idx_ws = torch.empty(G * max(self.cap_o, self.cap_ko, 1), **i32)
+        self.net = ImageNetBuffers(self.cap_o, self.pool.d_raw, self.prec_code, dev)
+        self.cnt_dev = torch.zeros(4, dtype=torch.int32, device=dev)  # n_recv_img, n_recv_id, n_send_img, n_send_id
+
+    @property
+    def emb(self):
+        return self.emb_l
+
+    @property
+    def d_emb(self):
+        return self.d_emb_l
+
+    def _dedup_owner(self, keys, n, space, ws, uniq, inv, count_slot):
+        seg = (L.KeySeg * 1)(L.KeySeg(keys.data_ptr(), n, 0, space, 0))
+        L.check(L.lib.dicm_dedup(seg, 1, space, ws.data_ptr(), ws.numel(), uniq.data_ptr(), inv.data_ptr(),
+                                 self.counts[count_slot:].data_ptr(), 2, self.status.data_ptr(), self.s))
+
+    def forward_backward(self, db, denominator=None):
+        G, s = self.world, None
+        self._begin(db)
+        s = self.s
+        denom = float(db.pk.B * G if denominator is None else denominator)
+        self._dedup_images()
+        self._dedup_ids()
+        cnt = self.counts
+        # (2) requests: bucket by owner, exchange counts, then keys
+        L.check(L.lib.dicm_bucket_by_owner(self.uniq_img.data_ptr(), cnt.data_ptr(), self.cap_u, G,
+                                           self.send_img.data_ptr(), self._col(0), self.perm_img.data_ptr(),
+                                           self.ws_bucket.data_ptr(), self.ws_bucket.numel(), s))
+        L.check(L.lib.dicm_bucket_by_owner(self.uniq_id.data_ptr(), cnt[1:].data_ptr(), self.cap_k, G,
+                                           self.send_id.data_ptr(), self._col(1), self.perm_id.data_ptr(),
+                                           self.ws_bucket.data_ptr(), self.ws_bucket.numel(), s))
+        pair = torch.stack([self._cnt_cols[0], self._cnt_cols[1]], dim=1)
+        sent, recv = exchange_counts(pair, self.group)
+        si, sk = sent[:, 0].tolist(), sent[:, 1].tolist()
+        ri, rk = recv[:, 0].tolist(), recv[:, 1].tolist()
+        nsi, nsk, nri, nrk = sum(si), sum(sk), sum(ri), sum(rk)
+        self._splits = (si, sk, ri, rk)
+        h = self._seg_host
+        h[0] = 0
+        h[1:G + 1] = torch.tensor(np.cumsum(ri), dtype=torch.int64)
+        h[G + 1] = 0
+        h[G + 2:] = torch.tensor(np.cumsum(rk), dtype=torch.int64)
+        self.segs_img.copy_(h[:G + 1], non_blocking=True)
+        self.segs_id.copy_(h[G + 1:], non_blocking=True)
+        self.cnt_dev.copy_(torch.tensor([nri, nrk, nsi, nsk], dtype=torch.int32), non_blocking=True)
+        _a2a(self.recv_img[:nri], self.send_img[:nsi], ri, si, self.group)
+        _a2a(self.recv_id[:nrk], self.send_id[:nsk], rk, sk, self.group)
+        # (3) owner: one image-MLP forward per distinct image, ID rows
+        self._dedup_owner(self.recv_img, nri, self.pool.local_rows, self.ws_img_owner, self.uniq_o, self.inv_o, 2)
+        if self.n_img_segs:
+            self._image_forward(self.net, self.uniq_o, cnt[2:].data_ptr())
+        L.check(L.lib.dicm_permute_rows12(self.net.emb.data_ptr(), self.inv_o.data_ptr(), self.cnt_dev.data_ptr(),
+                                          max(nri, 0), 0, self.resp.data_ptr(), s))
+        _a2a(self.rows_buf[:nsi], self.resp[:nri], si, ri, self.group)
+        L.check(L.lib.dicm_permute_rows12(self.rows_buf.data_ptr(), self.perm_img.data_ptr(), cnt.data_ptr(),
+                                          self.cap_u, 0, self.emb_l.data_ptr(), s))
+        L.check(L.lib.dicm_gather_rows_by_key(self.owner_tabstate, len(self.fields), self.recv_id.data_ptr(),
+                                              self.cnt_dev[1:].data_ptr(), max(nrk, 0), self.resp.data_ptr(), s))
+        _a2a(self.rows_buf[:nsk], self.resp[:nrk], sk, rk, self.group)
+        L.check(L.lib.dicm_permute_rows12(self.rows_buf.data_ptr(), self.perm_id.data_ptr(), cnt[1:].data_ptr(),
+                                          self.cap_k, 0, self.id_rows.data_ptr(), s))
+        # (4) local pooling + head
+        self._local_step(self.emb_l, self.d_emb_l, denom)
+        # (5) push gradients to the owners; owners reduce in ascending source order
+        L.check(L.lib.dicm_permute_rows12(self.d_emb_l.data_ptr(), self.perm_img.data_ptr(), cnt.data_ptr(),
+                                          self.cap_u, 1, self.rows_buf.data_ptr(), s))
+        _a2a(self.resp[:nri], self.rows_buf[:nsi], ri, si, self.group)
+        L.check(L.lib.dicm_owner_reduce_rows12(self.resp.data_ptr(), self.inv_o.data_ptr(), self.segs_img.data_ptr(),
+                                               G, max(nri, 0), cnt[2:].data_ptr(), self.cap_o, self.idx_ws.data_ptr(),
+                                               self.net.d_emb.data_ptr(), s))
+        # (6) owner image-MLP backward
+        self._image_backward(self.net, self.uniq_o, cnt[2:].data_ptr(), self.cap_o if self.n_img_segs else 0)
+        L.check(L.lib.dicm_permute_rows12(self.d_rows.data_ptr(), self.perm_id.data_ptr(), cnt[1:].data_ptr(),
+                                          self.cap_k, 1, self.rows_buf.data_ptr(), s))
+        _a2a(self.resp[:nrk], self.rows_buf[:nsk], rk, sk, self.group)
+        self._dedup_owner(self.recv_id, nrk, self.local_id_space, self.ws_id_owner, self.uniq_id_o, self.inv_id_o, 3)
+        L.check(L.lib.dicm_owner_reduce_rows12(self.resp.data_ptr(), self.inv_id_o.data_ptr(), self.segs_id.data_ptr(),
+                                               G, max(nrk, 0), cnt[3:].data_ptr(), self.cap_ko,
+                                               self.idx_ws.data_ptr(), self.d_rows_o.data_ptr(), s))
+        # (6) every dense gradient in one all-reduce (sum: the loss is already
+        # divided by the union batch, runtime.py:374, training.py:42)
+        dist.all_reduce(self.grad, group=self.group)
+        dist.all_reduce(self.loss, group=self.group)
+        return self.loss
+
+    def _col(self, j):
+        if not hasattr(self, "_cnt_cols") or self._cnt_cols[0].numel() != self.world:
+            self._cnt_cols = [torch.zeros(self.world, dtype=torch.int32, device=self.dev) for _ in range(2)]
+        return self._cnt_cols[j].data_ptr()
+
+    def optimizer_step(self, lr):
+        super().optimizer_step(lr, row_keys=self.uniq_id_o, row_count=self.counts[3:], row_grads=self.d_rows_o,
+                               row_cap=self.cap_ko, tabstate=self.owner_tabstate)
+
+    def forwards(self):
+        """Image-MLP forwards this rank ran in the last iteration."""
+        return int(self.counts[2].item())
+
+
+class Cluster:
+    """Multi-GPU AMS cluster (reference runtime.py:313-516), one rank per
+    process.  ``workers == servers == world size``: each GPU is a worker and a
+    server.  Every rank calls ``run_iteration`` with the same union batch."""
+
+    def __init__(self, cfg, model, store, lr0=0.001, lr_decay=0.9, lr_interval=24000, precision="fp32",
+                 group=None):
+        if cfg.mode != "ams":
+            raise ValueError(
+                f"training runs under mode 'ams' only; {cfg.mode!r} is an "
+                "accounting-only storage strategy (see dicm.accounting)")
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if cfg.workers != world or cfg.servers != world:
+            raise ValueError(f"this build runs one worker and one server per GPU: workers = servers = world size "
+                             f"({world}), got workers={cfg.workers}, servers={cfg.servers}")
+        self.cfg, self.model, self.store = cfg, model, store
+        self.world, self.rank = world, rank
+        self.lr0, self.lr_decay, self.lr_interval = lr0, lr_decay, lr_interval
+        if world > 1:
+            self.engine = ClusterEngine(model, store, precision, lr0, lr_decay, lr_interval, world, rank, group)
+        else:
+            self.engine = StepEngine(model, store, precision, lr0, lr_decay, lr_interval)
+        self.group = group
+
+    @property
+    def iteration(self):
+        return self.engine.iteration
+
+    def local_slice(self, union):
+        b = union if isinstance(union, Batch) else encode_batch(union, self.model)
+        bpw = self.cfg.batch_per_worker
+        lo = min(self.rank * bpw, b.size)
+        return b.slice(lo, min(b.size, lo + bpw)), b
+
+    def run_iteration(self, union_batch, digests=False):
+        """-> (loss, union_unique, forwards, digests) like runtime.py:465-470."""
+        local, union = self.local_slice(union_batch)
+        e = self.engine
+        loss = e.forward_backward(e.upload(local), denominator=union.size)
+        e.optimizer_step(e.lr())
+        e.iteration += 1
+        value = float(loss.item())
+        e.raise_status()
+        if self.world > 1:
+            fw = torch.tensor([e.forwards()], dtype=torch.int64, device=e.dev)
+            dist.all_reduce(fw, group=self.group)
+            forwards = int(fw.item())
+        else:
+            forwards = len(e.unique_images())
+        lay = self.model.layout
+        union_unique = len(union.unique_images(lay.use_ad_image, lay.use_behavior_images))
+        dig = []
+        if digests:
+            d = params_digest({n: p.data for n, p in self.model.params.items() if not n.startswith("id_emb/")})
+            dig = [None] * self.world
+            if self.world > 1:
+                dist.all_gather_object(dig, d, group=self.group)
+            else:
+                dig = [d]
+        return value, union_unique, forwards, dig
+
+    def snapshot(self):
+        """Dense params (replicated) + this rank's ID-table rows."""
+        return self.model.snapshot()
+
+
+def run_training(cluster_cfg, model, store, train_samples, train_cfg, log=None, precision="fp32"):
+    """Synchronous distributed training (reference runtime.py:519-554)."""
+    from .training import minibatches
+    cluster = Cluster(cluster_cfg, model, store, train_cfg.lr0, train_cfg.lr_decay, train_cfg.lr_interval,
+                      precision)
+    log = log or RunLog()
+    union_size = cluster_cfg.workers * cluster_cfg.batch_per_worker
+    stop = train_cfg.max_iterations or None
+    for epoch in range(train_cfg.epochs):
+        for union in minibatches(train_samples, union_size, train_cfg.seed, epoch):
+            log.lrs.append(lr_schedule(cluster.iteration, train_cfg.lr0, train_cfg.lr_decay, train_cfg.lr_interval))
+            loss, unique, forwards, digests = cluster.run_iteration(union, digests=True)
+            if not np.isfinite(loss):
+                raise FloatingPointError(f"non-finite loss at iteration {cluster.iteration}")
+            log.losses.append(loss)
+            log.unique_images.append(unique)
+            log.embed_forwards.append(forwards)
+            log.replica_digests.append(digests)
+            if stop and cluster.iteration >= stop:
+                return cluster, log
+    return cluster, log

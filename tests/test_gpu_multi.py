@@ -1,0 +1,24 @@
+"""Multi-GPU AMS parity (needs >= 2 GPUs; skipped otherwise): the cluster
+against the single-process oracle on the union batch (scripts/cluster_check.py)."""
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("kind,precision", [("multiquery-attn", "fp32"), ("sum", "tf32"), ("attn", "bf16")])
+def test_cluster_matches_oracle_on_union(kind, precision):
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = 4 if n >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29531", os.path.join(ROOT, "scripts", "cluster_check.py"),
+           kind, precision]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
