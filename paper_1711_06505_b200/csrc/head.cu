@@ -108,11 +108,11 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
     if (t < nb) {
       const float y = labels[b0 + t];
       l = fmaxf(z, 0.f) - z * y + log1pf(expf(-fabsf(z)));
-      // sigmoid(z) - y as (1-y) sigmoid(z) - y sigmoid(-z): equal for any y, and
-      // free of the cancellation that rounds 1 - sigmoid(20) to 0 in fp32 (the
-      // f64 reference keeps ~2e-9 there, and Adam skips exactly-zero rows)
-      const float sp = 1.f / (1.f + expf(-z)), sn = 1.f / (1.f + expf(z));
-      dz = ((1.f - y) * sp - y * sn) * inv_denom;
+      // dz = sigmoid(z) - y evaluated like the reference (autograd.py:241-244):
+      // in fp64, so that it is exactly zero where the reference's is (fp32
+      // would round 1 - sigmoid(20) to 0, and Adam skips all-zero rows)
+      const double sig = 1.0 / (1.0 + exp(-(double)z));
+      dz = (float)((sig - (double)y) * (double)inv_denom);
       logits[b0 + t] = z;
     }
     s.dz[t] = dz;
