@@ -113,7 +113,9 @@ def build_workload(name, rank, world, precision, seed=0, device="cuda"):
     schema = default_schema(v, 4, v, 8, c["P"], b_max=b_max)
     pool_dtype = "bf16" if precision == "bf16" else "fp32"
     pool = ImagePool.synthetic(c["P"], seed=seed, dtype=pool_dtype, device=device, world=world, rank=rank)
-    model = DicmModel(schema, AggregatorSpec(c["kind"]), None, seed=0, device=device)
+    big = max(f.vocab for f in schema.fields) > (1 << 21)
+    model = DicmModel(schema, AggregatorSpec(c["kind"]), None, seed=0, device=device,
+                      shard=(world, rank) if world > 1 else None, table_init="device" if big else "reference")
     torch.cuda.synchronize()
     return schema, model, pool
 
@@ -260,7 +262,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
-    ap.add_argument("--precision", default="auto")
+    ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "tf32", "bf16"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -274,29 +276,36 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    name = args.config
+    kind = CONFIGS[name]["kind"]
     precision = args.precision
     if precision == "auto":
-        precision = os.environ.get("DICM_PRECISION", "fp32")
-    from paper_1711_06505_b200.engine import StepEngine
-    from paper_1711_06505_b200.training import LocalTrainer, TrainConfig
-    name = args.config
-    schema, model, pool = build_workload(name, 0, 1, precision)
+        # bf16 layer-0 operands stay inside the north star's 2e-2 on logits for
+        # attentive pooling; sum pooling's large logits need tf32
+        precision = os.environ.get("DICM_PRECISION", "tf32" if kind == "sum" else "bf16")
+    from paper_1711_06505_b200.runtime import Cluster, ClusterConfig
+    B = CONFIGS[name]["B"]
+    schema, model, pool = build_workload(name, rank, world, precision)
+    cluster = Cluster(ClusterConfig(workers=world, servers=world, batch_per_worker=B), model, pool,
+                      precision=precision)
+    eng = cluster.engine
     batches = make_batches(name, schema, args.warmup + args.steps, seed=1000 + rank)
-    tr = LocalTrainer(model, pool, TrainConfig(batch_size=CONFIGS[name]["B"]), precision=precision)
-    eng = tr.engine
     staged = [eng.upload(b, own=True) for b in batches]
     torch.cuda.synchronize()
+    union = world * B
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up (untimed)
-    for db in staged[:args.warmup]:
-        eng.forward_backward(db)
+    def step(db):
+        eng.forward_backward(db, denominator=union)
         eng.optimizer_step(eng.lr())
         eng.iteration += 1
+
+    for db in staged[:args.warmup]:
+        step(db)
     barrier()
     eng.probe = {"imgmlp_fwd": [], "imgmlp_bwd": []}
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -304,9 +313,7 @@ def main():
         barrier()
         start.record()
         for db in staged[args.warmup:]:
-            eng.forward_backward(db)
-            eng.optimizer_step(eng.lr())
-            eng.iteration += 1
+            step(db)
         end.record()
         barrier()
     ms = start.elapsed_time(end)
@@ -317,11 +324,11 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    B = CONFIGS[name]["B"]
     ms_step = ms / max(args.steps, 1)
-    value = world * B * args.steps / (ms / 1000.0)
+    value = union * args.steps / (ms / 1000.0)
 
-    # e2e through the public API with host batches
+    # e2e through the public API with host batches: H2D inside the region,
+    # the loss read back (async D2H into pinned memory) every step
     e2e = None
     if not args.no_e2e:
         host = batches[args.warmup:]
@@ -330,7 +337,7 @@ def main():
         s2, e2_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s2.record()
         for i, b in enumerate(host):
-            loss = tr.train_batch_async(b)
+            loss = cluster.train_batch_async(b, union)
             pinned_loss[i:i + 1].copy_(loss, non_blocking=True)
         e2_.record()
         barrier()
@@ -340,11 +347,13 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         ems = float(te.item())
-        e2e = {"value": world * B * len(host) / (ems / 1000.0), "unit": "samples/s",
-               "h2d_bytes_per_step": int(np.mean([eng.h2d_bytes(b) for b in host])), "d2h_bytes_per_step": 4}
+        e2e = {"value": union * len(host) / (ems / 1000.0), "unit": "samples/s",
+               "h2d_bytes_per_step": int(np.mean([eng.h2d_bytes(b) for b in host])), "d2h_bytes_per_step": 4,
+               "api": "Cluster.train_batch_async (host CSR batch -> pinned H2D -> step -> loss D2H)"}
 
-    # roofline of the dominant kernel (image-MLP layer-0 forward)
-    U = int(eng.counts[0].item())
+    # roofline of the dominant launch pair: dicm_imgmlp_fwd (tcgen05 layer 0 +
+    # fused layers 1-2) per step, algorithmic bytes
+    U = int(eng.counts[2].item()) if world > 1 else int(eng.counts[0].item())
     fwd_ms = statistics.mean(probes["imgmlp_fwd"]) if probes.get("imgmlp_fwd") else None
     peaks = {}
     try:
@@ -355,14 +364,25 @@ def main():
     elem = 2 if precision == "bf16" else 4
     roof = None
     if fwd_ms:
-        bytes_fwd = U * schema.d_raw * elem + 256 * schema.d_raw * 4 + U * (256 + 64 + 12) * 4
+        # X rows once, W0 once, act0 write + re-read, h1 write, act1 + emb write
+        bytes_fwd = U * schema.d_raw * elem + 256 * schema.d_raw * elem + U * (256 * 4 * 3 + 64 * 4 + 12 * 4)
         ach = bytes_fwd / (fwd_ms / 1000.0) / 1e9
-        roof = {"bound": "hbm", "kernel": "dicm_imgmlp_fwd (layer-0 GEMM + layers 1-2)", "achieved": ach,
-                "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
-                "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback",
+        traffic = None
+        try:
+            prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            ent = prof.get(f"{name}/{precision}")
+            if ent:
+                traffic = ent["dram_bytes_per_launch"]
+        except Exception:
+            pass
+        roof = {"bound": "hbm", "kernel": "dicm_imgmlp_fwd (tcgen05 layer-0 GEMM + fused layers 1-2)",
+                "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak, "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json (measured)" if peaks else "fallback",
                 "algorithmic_bytes_per_launch": bytes_fwd, "ms_per_launch": fwd_ms,
                 "bwd_ms_per_launch": statistics.mean(probes["imgmlp_bwd"]) if probes.get("imgmlp_bwd") else None,
-                "unique_images_per_step": U}
+                "unique_images_per_step": U,
+                "tensor_tflops_fwd_bwd": (U * 4297216 / 1e12) / ((fwd_ms + (statistics.mean(
+                    probes["imgmlp_bwd"]) if probes.get("imgmlp_bwd") else 0)) / 1000.0)}
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -372,12 +392,14 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "fp32" if precision == "fp32" else f"{precision}-gemm/fp32",
-                "data": "synthetic",
-                "config": {"workload": name, "description": DESC[name], "global_batch": world * B,
-                           "behaviors_per_user": CONFIGS[name]["L"], "pool_images": CONFIGS[name]["P"],
-                           "precision": precision, "parallelism": f"replicas{world}" if world > 1 else "single",
-                           "l2": "inputs larger than L2 (each step gathers ~U x 16 KB of distinct pool rows)"},
+                "vs_baseline": None, "dtype": precision, "data": "synthetic",
+                "config": {"workload": name, "description": DESC[name], "global_batch": union,
+                           "batch_per_gpu": B, "behaviors_per_user": CONFIGS[name]["L"],
+                           "pool_images": CONFIGS[name]["P"], "aggregator": kind,
+                           "precision": f"image-MLP layer-0 operands {precision}, fp32 accumulate; "
+                                        "layers 1-2 tf32 tensor cores; pooling/head/Adam fp32",
+                           "parallelism": f"AMS: pool + ID tables sharded over {world} GPU(s), dense dp{world}",
+                           "l2": "inputs larger than L2 (each step gathers ~U x 8-16 KB of distinct pool rows)"},
                 "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": eng.launches_per_step * args.steps,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

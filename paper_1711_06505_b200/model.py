@@ -15,6 +15,8 @@ on the device).  Storage is laid out for the kernels:
 
 from __future__ import annotations
 
+import zlib
+
 import numpy as np
 import torch
 
@@ -79,11 +81,22 @@ class DicmModel:
 
     def __init__(self, schema, aggregator, extractor=None, seed=0, mlp_widths=(128, 64),
                  use_ad_image=True, use_behavior_images=True, device="cuda", params=None,
-                 table_rows=None, shard=None):
+                 table_rows=None, shard=None, table_init="reference"):
         """``shard=(world, rank)``: hold only the ID-table rows this rank owns
         (row % world == rank, at local row row // world), with exactly the
-        values the full reference init gives them."""
-        if shard is not None and table_rows is None:
+        values the full reference init gives them.  ``table_init="device"``
+        draws 0.05 N(0,1) rows on the device instead (same distribution as
+        model.py:316-319, not the same values) -- for 100M-row tables whose
+        reference init would not fit host memory."""
+        if table_init == "device" and table_rows is None:
+            world, rank = shard if shard is not None else (1, 0)
+
+            def table_rows(f, name):
+                n_local = -(-f.vocab // world)
+                g = torch.Generator(device=device).manual_seed(
+                    (int(seed) * 1315423911 + zlib.crc32(name.encode()) * 31 + rank) & 0x7FFFFFFF)
+                return 0.05 * torch.randn((n_local, schema.d_id), generator=g, dtype=torch.float32, device=device)
+        elif shard is not None and table_rows is None:
             world, rank = shard
 
             def table_rows(f, name):

@@ -97,11 +97,20 @@ class ImagePool:
     def synthetic(cls, n_rows, d_raw=4096, latent_dim=32, seed=0, dtype="fp32", device="cuda",
                   world=1, rank=0, extractor_seed=0x5EED):
         """Benchmark pool: latents ~ N(0,1)^k (reference data.py:137),
-        features tanh(z R^T)."""
+        features tanh(z R^T).  Large sharded pools draw each
+        shard's latents on its own device (seeded by (seed, rank)), so a
+        20M-row pool never passes through host memory."""
+        ext = FixedExtractor(extractor_seed, latent_dim, d_raw)
+        if world > 1 and n_rows > (1 << 22):
+            n_local = len(range(rank, n_rows, world))
+            gen = torch.Generator(device=device).manual_seed(seed * 1000003 + rank)
+            lat = torch.randn((n_local, latent_dim), generator=gen, dtype=torch.float32, device=device)
+            pool = cls.from_latents(lat, ext, dtype, device, 1, 0)
+            pool.world, pool.rank, pool.global_size = world, rank, n_rows
+            return pool
         gen = torch.Generator(device="cpu").manual_seed(seed)
         lat = torch.randn((n_rows, latent_dim), generator=gen, dtype=torch.float32)
-        return cls.from_latents(lat, FixedExtractor(extractor_seed, latent_dim, d_raw), dtype, device,
-                                world, rank)
+        return cls.from_latents(lat, ext, dtype, device, world, rank)
 
     def gather(self, ids):
         """Rows for local ids as fp32 on the device (dicm_pool_gather)."""

@@ -314,6 +314,15 @@ class Cluster:
                 dig = [d]
         return value, union_unique, forwards, dig
 
+    def train_batch_async(self, local_batch, union_size):
+        """This rank's part of an iteration on its already-sliced local batch
+        (no host sync): upload, step, optimizer; returns the device loss."""
+        e = self.engine
+        loss = e.forward_backward(e.upload(local_batch), denominator=union_size)
+        e.optimizer_step(e.lr())
+        e.iteration += 1
+        return loss
+
     def snapshot(self):
         """Dense params (replicated) + this rank's ID-table rows."""
         return self.model.snapshot()
