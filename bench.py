@@ -56,7 +56,9 @@ def env_rank():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region:
+    one `nvidia-smi -lms 20` stream started before the region, samples kept
+    between enter() and exit()."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -65,29 +67,39 @@ class ClockSampler:
     def __init__(self, gpu_index):
         self.idx = gpu_index
         self.samples = []
-        self._stop = threading.Event()
+        self._proc = None
         self._t = None
+        self._window = [None, None]
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                                           "--format=csv,noheader,nounits", "-lms", "20"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.3)  # let the stream start before the timed region
+        except Exception:
+            self._proc = None
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+    def _read(self):
+        for line in self._proc.stdout:
+            now = time.perf_counter()
+            w0, w1 = self._window
+            if w0 is not None and now >= w0 and (w1 is None or now <= w1):
+                self.samples.append([x.strip() for x in line.split(",")])
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        self._window[0] = time.perf_counter()
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        self._window[1] = time.perf_counter()
+        if self._proc is not None:
+            time.sleep(0.05)
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
 
     def summary(self):
         if not self.samples:
@@ -120,6 +132,28 @@ def build_workload(name, rank, world, precision, seed=0, device="cuda"):
     return schema, model, pool
 
 
+def kernel_work(U, B, R, W, D, e):
+    """Algorithmic (bytes, flops) per launch of each probed kernel, counting
+    only what the math needs: U unique images, B samples, R
+    behaviors, W head-input width, D = d_raw, e = layer-0 operand bytes."""
+    Rimg = B + R
+    return {
+        # X rows + W0 in, act0 out
+        "img_fwd_l0": (U * D * e + 256 * D * e + U * 256 * 4, 2 * U * D * 256),
+        # act0 in, act1 + emb out
+        "img_fwd_l12": (U * (256 + 64 + 12) * 4, 2 * U * (256 * 64 + 64 * 12)),
+        # dE, act1, act0 in; da1, da0 out (dh2, dW2, dh1)
+        "img_bwd_l12": (U * (12 + 64 + 256 + 64) * 4 + U * 256 * e, 2 * U * (2 * 12 * 64 + 64 * 256)),
+        # act0 (-> h1), da1 in
+        "img_bwd_dw1": (U * (256 + 64) * 4, 2 * U * 64 * 256),
+        # X rows + da0 in, dW0 out
+        "img_bwd_dw0": (U * D * e + U * 256 * e + 256 * D * 4, 2 * U * D * 256),
+        # inverse ids + embedding rows per reference, head input out
+        "sample_fwd": (Rimg * (4 + 48) + B * W * 4, 0),
+        "sample_bwd": (Rimg * (4 + 48) + U * 48 + B * W * 4, 0),
+    }
+
+
 def make_batches(name, schema, n, seed):
     from paper_1711_06505_b200.batch import synthetic_batch
     c = CONFIGS[name]
@@ -139,7 +173,7 @@ def make_batches(name, schema, n, seed):
 # else the oracle port), timed on this host's cores on a bounded sample
 # ---------------------------------------------------------------------------
 
-def cpu_baseline(name, schema, pool, batch, max_seconds=25.0, sample_b=256):
+def cpu_baseline(name, schema, pool, batch, max_seconds=25.0, sample_b=256, return_step=False):
     import torch
     threads = os.cpu_count() or 1
     sub = batch.slice(0, min(sample_b, batch.size))
@@ -192,6 +226,8 @@ def cpu_baseline(name, schema, pool, batch, max_seconds=25.0, sample_b=256):
               "beh_off": sub.beh_off.astype(np.int64)}
         tr = O.OracleTrainer(params, cfg, rows)
         step = lambda: tr.train_batch(ob)  # noqa: E731
+    if return_step:
+        return step, kind, threads, sub.size
     # one warm-up, then as many steps as fit the budget (>= 1)
     step()
     while True:
@@ -227,28 +263,38 @@ def _samples_of(b):
 # ---------------------------------------------------------------------------
 
 def run_reference_arm(args):
+    """The reference's own CPU implementation (LocalTrainer from baseline/_ref,
+    else the oracle port) on this host's cores: W warm-up + K timed steps, each
+    one train_batch over a bounded 256-sample slice of the same workload."""
     rank, world, local = env_rank()
     if rank != 0:
         return
     import torch
     name = args.config
-    if torch.cuda.is_available():
-        torch.cuda.set_device(local)
-        schema, model, pool = build_workload(name, 0, 1, "fp32")
-    else:
+    if not torch.cuda.is_available():
         raise SystemExit("reference arm needs the GPU box to materialize the same pool rows")
+    torch.cuda.set_device(local)
+    schema, model, pool = build_workload(name, 0, 1, "fp32")
     batch = make_batches(name, schema, 1, seed=1234)[0]
+    # ~10 ms of host work per sample: size the slice so W + K steps take ~2.5 min
+    sample_b = int(max(16, min(256, 150.0 / max(args.warmup + args.steps, 1) / 0.01)))
+    step, kind, threads, n = cpu_baseline(name, schema, pool, batch, sample_b=sample_b, return_step=True)
+    for _ in range(args.warmup):
+        step()
     times = []
-    cb = None
-    for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(name, schema, pool, batch, max_seconds=20.0)
-        times.append(cb["value"])
-    v = statistics.median(times[args.warmup:]) if args.steps else times[-1]
+    for _ in range(max(args.steps, 1)):
+        a = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - a)
+    med = statistics.median(times)
+    v = n / med
+    sample = (f"{n} samples of {name} (L={CONFIGS[name]['L']}, pool {CONFIGS[name]['P']}) per step, "
+              f"{args.warmup} warm-up + median of {len(times)} steps, f64, {threads} host threads")
     line = {"metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1000.0 * 256 / v, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": 1000.0 * med, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": name, "description": DESC[name], "sample_batch": 256},
-            "cpu_baseline": {**cb, "value": v},
+            "config": {"workload": name, "description": DESC[name], "sample_batch": n},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": kind, "sample": sample},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -259,7 +305,7 @@ METRIC = "DICM train samples/sec (fwd+bwd)"
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "tf32", "bf16"])
@@ -289,8 +335,12 @@ def main():
     cluster = Cluster(ClusterConfig(workers=world, servers=world, batch_per_worker=B), model, pool,
                       precision=precision)
     eng = cluster.engine
-    batches = make_batches(name, schema, args.warmup + args.steps, seed=1000 + rank)
-    staged = [eng.upload(b, own=True) for b in batches]
+    # up to 64 distinct batches, cycled (each step still gathers GBs of pool
+    # rows, far beyond L2)
+    distinct = make_batches(name, schema, min(args.warmup + args.steps, 64), seed=1000 + rank)
+    batches = [distinct[i % len(distinct)] for i in range(args.warmup + args.steps)]
+    staged_d = [eng.upload(b, own=True) for b in distinct]
+    staged = [staged_d[i % len(staged_d)] for i in range(args.warmup + args.steps)]
     torch.cuda.synchronize()
     union = world * B
 
@@ -307,7 +357,8 @@ def main():
     for db in staged[:args.warmup]:
         step(db)
     barrier()
-    eng.probe = {"imgmlp_fwd": [], "imgmlp_bwd": []}
+    from paper_1711_06505_b200 import _lib as LIB
+    LIB.check(LIB.lib.dicm_probe_enable(1))
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
@@ -318,8 +369,8 @@ def main():
         barrier()
     ms = start.elapsed_time(end)
     eng.raise_status()
-    probes = {k: [a.elapsed_time(b) for a, b in v] for k, v in eng.probe.items()}
-    eng.probe = None
+    probes = {k: LIB.probe_read(k) for k in LIB.PROBE_KERNELS}
+    LIB.check(LIB.lib.dicm_probe_enable(0))
     t = torch.tensor([ms], device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -351,38 +402,57 @@ def main():
                "h2d_bytes_per_step": int(np.mean([eng.h2d_bytes(b) for b in host])), "d2h_bytes_per_step": 4,
                "api": "Cluster.train_batch_async (host CSR batch -> pinned H2D -> step -> loss D2H)"}
 
-    # roofline of the dominant launch pair: dicm_imgmlp_fwd (tcgen05 layer 0 +
-    # fused layers 1-2) per step, algorithmic bytes
+    # roofline: per-kernel algorithmic bytes / flops over the
+    # kernel times the library's own event probe measured on its stream
     U = int(eng.counts[2].item()) if world > 1 else int(eng.counts[0].item())
-    fwd_ms = statistics.mean(probes["imgmlp_fwd"]) if probes.get("imgmlp_fwd") else None
+    last = batches[-1]
+    R = int(last.beh_off[-1])
+    width = model.layout.mlp_input_width()
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    src = "MEASURED_PEAKS.json (measured)" if peaks else "B200_PROFILING.md fallback"
+    hbm_peak = peaks.get("hbm_gbs", 6550.1)
+    tc_peak = peaks.get("bf16_tflops_sustained", 1362.2) if precision == "bf16" else \
+        peaks.get("bf16_tflops_sustained", 1362.2) / 2.0
     elem = 2 if precision == "bf16" else 4
+    kern = kernel_work(U, B, R, width, schema.d_raw, elem)
+    table = {}
+    for k, (nbytes, flops) in kern.items():
+        t = probes.get(k) or []
+        if not t:
+            continue
+        ms_k = statistics.mean(t)
+        ideal = max(nbytes / (hbm_peak * 1e9), flops / (tc_peak * 1e12) if k.startswith("img") else 0.0)
+        table[k] = {"ms": ms_k, "launches": len(t), "alg_bytes": nbytes, "GB_s": nbytes / (ms_k / 1e3) / 1e9,
+                    "flops": flops, "TFLOP_s": flops / (ms_k / 1e3) / 1e12,
+                    "roofline_frac": ideal / (ms_k / 1e3)}
+    img = [k for k in table if k.startswith("img")]
+    mlp_ms = sum(table[k]["ms"] for k in img)
+    mlp_flops = sum(table[k]["flops"] for k in img)
     roof = None
-    if fwd_ms:
-        # X rows once, W0 once, act0 write + re-read, h1 write, act1 + emb write
-        bytes_fwd = U * schema.d_raw * elem + 256 * schema.d_raw * elem + U * (256 * 4 * 3 + 64 * 4 + 12 * 4)
-        ach = bytes_fwd / (fwd_ms / 1000.0) / 1e9
+    if "img_fwd_l0" in table:
+        top = table["img_fwd_l0"]
         traffic = None
         try:
             prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-            ent = prof.get(f"{name}/{precision}")
+            ent = prof.get(f"{name}/{precision}/img_fwd_l0")
             if ent:
-                traffic = ent["dram_bytes_per_launch"]
+                # ncu's DRAM bytes for the captured launch, rescaled to this run's U
+                traffic = ent["dram_bytes"] * U / ent["unique_images"]
         except Exception:
             pass
-        roof = {"bound": "hbm", "kernel": "dicm_imgmlp_fwd (tcgen05 layer-0 GEMM + fused layers 1-2)",
-                "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak, "traffic": traffic,
-                "peak_source": "MEASURED_PEAKS.json (measured)" if peaks else "fallback",
-                "algorithmic_bytes_per_launch": bytes_fwd, "ms_per_launch": fwd_ms,
-                "bwd_ms_per_launch": statistics.mean(probes["imgmlp_bwd"]) if probes.get("imgmlp_bwd") else None,
-                "unique_images_per_step": U,
-                "tensor_tflops_fwd_bwd": (U * 4297216 / 1e12) / ((fwd_ms + (statistics.mean(
-                    probes["imgmlp_bwd"]) if probes.get("imgmlp_bwd") else 0)) / 1000.0)}
+        roof = {"bound": "hbm", "kernel": "k_fwd: pool-row gather + layer-0 tcgen05 GEMM (dicm_imgmlp_fwd)",
+                "achieved": top["GB_s"], "peak": hbm_peak, "unit": "GB/s", "frac": top["GB_s"] / hbm_peak,
+                "traffic": traffic, "peak_source": src, "algorithmic_bytes_per_launch": top["alg_bytes"],
+                "ms_per_launch": top["ms"], "unique_images_per_step": U,
+                "tensor": {"image_mlp_TFLOP_s": mlp_flops / (mlp_ms / 1e3) / 1e12, "peak": tc_peak,
+                           "frac": mlp_flops / (mlp_ms / 1e3) / 1e12 / tc_peak,
+                           "peak_kind": "dense bf16 sustained" if precision == "bf16" else "tf32 = bf16/2",
+                           "flops_per_unique_image": 4297216, "kernels": img},
+                "kernels": table}
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

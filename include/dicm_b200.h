@@ -282,6 +282,25 @@ int dicm_owner_reduce_rows12(const float* recv, const int32_t* inv, const int64_
                              int64_t n_recv_max, const int32_t* count_dev, int64_t ucap, int32_t* idx_ws,
                              float* out, dicm_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * Timing probe (instrumentation, no reference counterpart): while enabled,
+ * the library records a CUDA event pair on the launching stream around each
+ * of its dominant kernels; dicm_probe_read returns the elapsed ms of the
+ * recorded launches of one kernel (waits on their end events).  Enabling
+ * clears earlier records.
+ * ---------------------------------------------------------------------- */
+enum {
+  DICM_PROBE_IMG_FWD_L0 = 0,  /* layer-0 forward GEMM (gather + tcgen05) */
+  DICM_PROBE_IMG_FWD_L12 = 1, /* layers 1-2 forward */
+  DICM_PROBE_IMG_BWD_L12 = 2, /* layers 2-1 backward (dE -> da0) */
+  DICM_PROBE_IMG_BWD_DW1 = 3, /* dW1 */
+  DICM_PROBE_IMG_BWD_DW0 = 4, /* dW0 = da0^T X (gather + tcgen05) */
+  DICM_PROBE_SAMPLE_FWD = 5,  /* per-sample gather / pooling forward */
+  DICM_PROBE_SAMPLE_BWD = 6   /* per-sample pooling backward */
+};
+int dicm_probe_enable(int on);
+int dicm_probe_read(int kernel, float* ms, int max, int* n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -140,6 +140,19 @@ _sig("dicm_bucket_by_owner", C.c_int, P, P, I64, C.c_int, P, P, P, P, S, ST)
 _sig("dicm_permute_rows12", C.c_int, P, P, P, I64, C.c_int, P, ST)
 _sig("dicm_gather_rows_by_key", C.c_int, C.POINTER(TableState), C.c_int, P, P, I64, P, ST)
 _sig("dicm_owner_reduce_rows12", C.c_int, P, P, P, C.c_int, I64, P, I64, P, P, ST)
+_sig("dicm_probe_enable", C.c_int, C.c_int)
+_sig("dicm_probe_read", C.c_int, C.c_int, C.POINTER(F), C.c_int, C.POINTER(C.c_int))
+
+PROBE_KERNELS = {"img_fwd_l0": 0, "img_fwd_l12": 1, "img_bwd_l12": 2, "img_bwd_dw1": 3, "img_bwd_dw0": 4,
+                 "sample_fwd": 5, "sample_bwd": 6}
+
+
+def probe_read(kernel, max_n=4096):
+    """Elapsed ms of every recorded launch of one probed kernel."""
+    buf = (F * max_n)()
+    n = C.c_int(0)
+    check(lib.dicm_probe_read(PROBE_KERNELS[kernel], buf, max_n, C.byref(n)))
+    return list(buf[:n.value])
 
 EXPORTED = [
     "dicm_last_error", "dicm_version", "dicm_device_arch", "dicm_dedup_workspace", "dicm_dedup",
@@ -148,7 +161,7 @@ EXPORTED = [
     "dicm_head_partial_size", "dicm_head_blocks", "dicm_head_fwd_bwd", "dicm_reduce_partials",
     "dicm_loss_finalize", "dicm_check_finite", "dicm_adam_dense_workspace", "dicm_adam_dense", "dicm_adam_rows",
     "dicm_bucket_workspace", "dicm_bucket_by_owner", "dicm_permute_rows12", "dicm_gather_rows_by_key",
-    "dicm_owner_reduce_rows12",
+    "dicm_owner_reduce_rows12", "dicm_probe_enable", "dicm_probe_read",
 ]
 
 

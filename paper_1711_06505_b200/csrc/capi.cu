@@ -2,6 +2,9 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <mutex>
+#include <vector>
+
 #include "common.cuh"
 
 namespace {
@@ -25,6 +28,53 @@ int check_cuda(cudaError_t e, const char* where) {
 
 int last_launch(const char* where) { return check_cuda(cudaGetLastError(), where); }
 
+// Kernel timing probe: CUDA events recorded on the launching stream around
+// the dominant kernels, read back by bench.py for the roofline.
+namespace {
+struct ProbeRec {
+  int kernel;
+  cudaEvent_t a, b;
+};
+std::mutex g_probe_mu;
+bool g_probe_on = false;
+std::vector<ProbeRec> g_probe;
+std::vector<cudaEvent_t> g_probe_free;
+
+cudaEvent_t probe_event() {
+  if (!g_probe_free.empty()) {
+    cudaEvent_t e = g_probe_free.back();
+    g_probe_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void probe_recycle() {
+  for (auto& r : g_probe) {
+    g_probe_free.push_back(r.a);
+    g_probe_free.push_back(r.b);
+  }
+  g_probe.clear();
+}
+}  // namespace
+
+int probe_begin(int kernel, cudaStream_t st) {
+  if (!g_probe_on) return -1;
+  std::lock_guard<std::mutex> lk(g_probe_mu);
+  ProbeRec r{kernel, probe_event(), probe_event()};
+  cudaEventRecord(r.a, st);
+  g_probe.push_back(r);
+  return (int)g_probe.size() - 1;
+}
+
+void probe_end(int slot, cudaStream_t st) {
+  if (slot < 0) return;
+  std::lock_guard<std::mutex> lk(g_probe_mu);
+  if (slot < (int)g_probe.size()) cudaEventRecord(g_probe[slot].b, st);
+}
+
 }  // namespace dicm
 
 extern "C" {
@@ -39,6 +89,30 @@ int dicm_device_arch(void) {
   cudaDeviceProp p;
   if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return -1;
   return p.major * 10 + p.minor;
+}
+
+int dicm_probe_enable(int on) {
+  std::lock_guard<std::mutex> lk(dicm::g_probe_mu);
+  dicm::probe_recycle();
+  dicm::g_probe_on = on != 0;
+  return DICM_OK;
+}
+
+int dicm_probe_read(int kernel, float* ms, int max, int* n) {
+  std::lock_guard<std::mutex> lk(dicm::g_probe_mu);
+  int k = 0;
+  for (auto& r : dicm::g_probe) {
+    if (r.kernel != kernel) continue;
+    if (k < max) {
+      int rc = dicm::check_cuda(cudaEventSynchronize(r.b), "dicm_probe_read");
+      if (rc) return rc;
+      rc = dicm::check_cuda(cudaEventElapsedTime(&ms[k], r.a, r.b), "dicm_probe_read");
+      if (rc) return rc;
+    }
+    ++k;
+  }
+  *n = k < max ? k : max;
+  return DICM_OK;
 }
 
 }  // extern "C"

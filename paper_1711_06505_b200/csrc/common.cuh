@@ -22,6 +22,8 @@ namespace dicm {
 int fail(int code, const char* fmt, ...);
 int check_cuda(cudaError_t e, const char* where);
 int last_launch(const char* where);
+int probe_begin(int kernel, cudaStream_t st);  // -1 when probing is off
+void probe_end(int slot, cudaStream_t st);
 
 // ---- device helpers -------------------------------------------------------
 __device__ __forceinline__ float prelu(float x, float a) { return x > 0.f ? x : a * x; }

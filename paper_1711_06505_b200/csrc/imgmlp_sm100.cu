@@ -442,11 +442,15 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
   if (bf16) {
     static int once = set_smem(k_fwd<1>);
     if (once) return once;
+    const int probe_slot = probe_begin(DICM_PROBE_IMG_FWD_L0, st);
     k_fwd<1><<<grid, THREADS_F, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, b0, act0);
+    probe_end(probe_slot, st);
   } else {
     static int once = set_smem(k_fwd<0>);
     if (once) return once;
+    const int probe_slot = probe_begin(DICM_PROBE_IMG_FWD_L0, st);
     k_fwd<0><<<grid, THREADS_F, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, b0, act0);
+    probe_end(probe_slot, st);
   }
   return last_launch("tcgen05 layer-0 forward");
 }
@@ -477,11 +481,15 @@ int bwd_dw0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows, co
   if (bf16) {
     static int once = set_smem(k_dw0<1>);
     if (once) return once;
+    const int probe_slot = probe_begin(DICM_PROBE_IMG_BWD_DW0, st);
     k_dw0<1><<<grid, THREADS_B, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, w.part);
+    probe_end(probe_slot, st);
   } else {
     static int once = set_smem(k_dw0<0>);
     if (once) return once;
+    const int probe_slot = probe_begin(DICM_PROBE_IMG_BWD_DW0, st);
     k_dw0<0><<<grid, THREADS_B, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, w.part);
+    probe_end(probe_slot, st);
   }
   const int64_t n = (int64_t)256 * d_raw;
   k_sum_splits<<<dicm_grid(n / 4, 256, 148 * 8), 256, 0, st>>>(w.part, nsplit, n, gw0);

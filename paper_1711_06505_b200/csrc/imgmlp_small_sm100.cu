@@ -520,7 +520,11 @@ int fwd_layers12(const float* act0, const int32_t* count, int64_t rows_max, cons
   int rc = map_f32(&ma, act0, rows_max, H1, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148, (rows_max + 127) / 128));
-  k_l12_fwd<<<grid, 256, F_SMEM, st>>>(ma, h1, rows_max, al0, w1, b1, al1, w2, b2, count, act1, emb);
+  {
+    const int probe_slot = probe_begin(DICM_PROBE_IMG_FWD_L12, st);
+    k_l12_fwd<<<grid, 256, F_SMEM, st>>>(ma, h1, rows_max, al0, w1, b1, al1, w2, b2, count, act1, emb);
+    probe_end(probe_slot, st);
+  }
   return last_launch("tcgen05 layers 1-2 forward");
 }
 
@@ -531,15 +535,23 @@ int bwd_layers12(const float* demb, const float* act1, const float* act0, const 
   if (once) return once;
   static int once2 = smem_attr(k_dw1, W_SMEM);
   if (once2) return once2;
-  k_l12_bwd<<<small_bwd_blocks(rows_max), 256, G_SMEM, st>>>(demb, act1, act0, al0, al1, w1, w2, count, rows_max,
+  {
+    const int probe_slot = probe_begin(DICM_PROBE_IMG_BWD_L12, st);
+    k_l12_bwd<<<small_bwd_blocks(rows_max), 256, G_SMEM, st>>>(demb, act1, act0, al0, al1, w1, w2, count, rows_max,
                                                              da1, da0, da0_bf16, part_l12);
+    probe_end(probe_slot, st);
+  }
   int rc = last_launch("tcgen05 layers 2-1 backward");
   if (rc) return rc;
   CUtensorMap mh, md;
   rc = map_f32(&mh, h1, rows_max, H1, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (!rc) rc = map_f32(&md, da1, rows_max, H2, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (rc) return rc;
-  k_dw1<<<small_dw1_blocks(rows_max), 192, W_SMEM, st>>>(mh, md, count, part_dw1);
+  {
+    const int probe_slot = probe_begin(DICM_PROBE_IMG_BWD_DW1, st);
+    k_dw1<<<small_dw1_blocks(rows_max), 192, W_SMEM, st>>>(mh, md, count, part_dw1);
+    probe_end(probe_slot, st);
+  }
   return last_launch("tcgen05 dW1");
 }
 

@@ -531,7 +531,11 @@ int dicm_sample_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
   a.scores = scores;
   a.stats = stats;
   const int grid = (bv->batch + FWD_WARPS - 1) / FWD_WARPS;
-  k_sample_fwd<<<grid, FWD_WARPS * 32, 0, (cudaStream_t)stream>>>(a);
+  {
+    const int probe_slot = probe_begin(DICM_PROBE_SAMPLE_FWD, (cudaStream_t)stream);
+    k_sample_fwd<<<grid, FWD_WARPS * 32, 0, (cudaStream_t)stream>>>(a);
+    probe_end(probe_slot, (cudaStream_t)stream);
+  }
   return last_launch("dicm_sample_fwd");
 }
 
@@ -557,7 +561,11 @@ int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
     if (rc) return rc;
     attr_set = true;
   }
-  k_sample_bwd<<<bwd_grid(bv->batch), BWD_WARPS * 32, smem, (cudaStream_t)stream>>>(a, part_size(layout));
+  {
+    const int probe_slot = probe_begin(DICM_PROBE_SAMPLE_BWD, (cudaStream_t)stream);
+    k_sample_bwd<<<bwd_grid(bv->batch), BWD_WARPS * 32, smem, (cudaStream_t)stream>>>(a, part_size(layout));
+    probe_end(probe_slot, (cudaStream_t)stream);
+  }
   return last_launch("dicm_sample_bwd");
 }
 
