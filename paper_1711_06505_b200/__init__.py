@@ -14,7 +14,8 @@ from .batch import Batch, encode_batch, synthetic_batch  # noqa: F401
 
 __all__ = ["AGGREGATOR_KINDS", "AggregatorSpec", "FeatureSchema", "FieldSpec", "ModelLayout", "default_schema",
            "image_net_widths", "init_params", "param_specs", "Batch", "encode_batch", "synthetic_batch",
-           "DicmModel", "ImagePool", "FixedExtractor", "LocalTrainer", "TrainConfig", "StepEngine"]
+           "DicmModel", "ImagePool", "FixedExtractor", "LocalTrainer", "TrainConfig", "StepEngine", "Cluster",
+           "ClusterConfig", "run_training"]
 
 
 def __getattr__(name):
