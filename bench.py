@@ -135,17 +135,20 @@ def build_workload(name, rank, world, precision, seed=0, device="cuda"):
 def kernel_work(U, B, R, W, D, e):
     """Algorithmic (bytes, flops) per launch of each probed kernel, counting
     only what the math needs: U unique images, B samples, R
-    behaviors, W head-input width, D = d_raw, e = layer-0 operand bytes."""
+    behaviors, W head-input width, D = d_raw, e = layer-0 operand bytes.  The
+    saved activations act0/act1 (and da1/da0) are stored in the operand dtype
+    in bf16 mode (e = 2) and in fp32 otherwise."""
     Rimg = B + R
+    a = e  # bytes per saved activation
     return {
         # X rows + W0 in, act0 out
-        "img_fwd_l0": (U * D * e + 256 * D * e + U * 256 * 4, 2 * U * D * 256),
+        "img_fwd_l0": (U * D * e + 256 * D * e + U * 256 * a, 2 * U * D * 256),
         # act0 in, act1 + emb out
-        "img_fwd_l12": (U * (256 + 64 + 12) * 4, 2 * U * (256 * 64 + 64 * 12)),
+        "img_fwd_l12": (U * ((256 + 64) * a + 12 * 4), 2 * U * (256 * 64 + 64 * 12)),
         # dE, act1, act0 in; da1, da0 out (dh2, dW2, dh1)
-        "img_bwd_l12": (U * (12 + 64 + 256 + 64) * 4 + U * 256 * e, 2 * U * (2 * 12 * 64 + 64 * 256)),
+        "img_bwd_l12": (U * (12 * 4 + (64 + 256 + 64 + 256) * a), 2 * U * (2 * 12 * 64 + 64 * 256)),
         # act0 (-> h1), da1 in
-        "img_bwd_dw1": (U * (256 + 64) * 4, 2 * U * 64 * 256),
+        "img_bwd_dw1": (U * (256 + 64) * a, 2 * U * 64 * 256),
         # X rows + da0 in, dW0 out
         "img_bwd_dw0": (U * D * e + U * 256 * e + 256 * D * 4, 2 * U * D * 256),
         # inverse ids + embedding rows per reference, head input out

@@ -191,7 +191,7 @@ void reduce(cudaStream_t st, const float* part, int nblk, int64_t stride, int64_
 }
 
 struct Ws {
-  float *da1, *da0, *p2, *p0, *pw1, *pw0, *red, *pl12, *pdw1, *h1;
+  float *da1, *da0, *p2, *p0, *pw1, *pw0, *red, *pl12, *pdw1, *h1, *g3;
   int s1, s0;
 };
 
@@ -216,7 +216,8 @@ size_t carve(int64_t rows_max, int d_raw, Ws* w, char* base) {
   t.pw0 = (float*)take((size_t)t.s0 * H1 * d_raw * 4);
   t.red = (float*)take(red_tmp_floats(rows_max) * 4);
   t.pl12 = (float*)take((size_t)sm100::small_bwd_blocks(rows_max) * sm100::small_part_size() * 4);
-  t.pdw1 = (float*)take((size_t)sm100::small_dw1_blocks(rows_max) * H2 * H1 * 4);
+  t.pdw1 = (float*)take((size_t)sm100::small_dw1_blocks(rows_max) * sm100::dw1_bf16_part_size() * 4);
+  t.g3 = (float*)take((size_t)sm100::dw1_bf16_part_size() * 4);
   t.h1 = (float*)take((size_t)rows_max * H1 * 4);
   if (w) *w = t;
   return off + sm100::workspace_bytes(rows_max, d_raw);
@@ -272,6 +273,13 @@ int dicm_imgmlp_fwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
     rc = sm100::fwd_layer0(pool, pool_dtype, d_raw, rows, count_dev, rows_max, p->w0, p->b0, act0, precision,
                            tc_ws, st);
     if (rc) return rc;
+    if (precision == DICM_PREC_BF16) {
+      // bf16 saved activations: act0 / act1 buffers hold bf16 rows
+      rc = sm100::fwd_layers12_bf16(reinterpret_cast<const __nv_bfloat16*>(act0), count_dev, rows_max, p->a0, p->w1,
+                                    p->b1, p->a1, p->w2, p->b2, reinterpret_cast<__nv_bfloat16*>(act1), emb, st);
+      if (rc) return rc;
+      return last_launch("dicm_imgmlp_fwd");
+    }
     // layers 1-2 on tcgen05 (tf32) with the layer-2 epilogue fused
     rc = sm100::fwd_layers12(act0, count_dev, rows_max, p->a0, p->w1, p->b1, p->a1, p->w2, p->b2, act1, emb, w.h1,
                              st);
@@ -322,7 +330,13 @@ int dicm_imgmlp_bwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
     char* tc_ws = (char*)workspace + carve(rows_max, d_raw, nullptr, nullptr) - sm100::workspace_bytes(rows_max, d_raw);
     const bool bf16 = precision == DICM_PREC_BF16;
     __nv_bfloat16* da0_bf16 = bf16 ? sm100::da0_bf16_ptr(tc_ws, rows_max, d_raw) : nullptr;
-    rc = sm100::bwd_layers12(demb, act1, act0, w.h1, count_dev, rows_max, p->a0, p->a1, p->w1, p->w2, w.da1, w.da0,
+    if (bf16)
+      rc = sm100::bwd_layers12_bf16(demb, reinterpret_cast<const __nv_bfloat16*>(act1),
+                                    reinterpret_cast<const __nv_bfloat16*>(act0), count_dev, rows_max, p->a0, p->a1,
+                                    p->w1, p->w2, reinterpret_cast<__nv_bfloat16*>(w.da1), da0_bf16, w.pl12, w.pdw1,
+                                    st);
+    else
+      rc = sm100::bwd_layers12(demb, act1, act0, w.h1, count_dev, rows_max, p->a0, p->a1, p->w1, p->w2, w.da1, w.da0,
                              da0_bf16, w.pl12, w.pdw1, st);
     if (rc) return rc;
     const int nb = sm100::small_bwd_blocks(rows_max), ps = sm100::small_part_size();
@@ -330,9 +344,17 @@ int dicm_imgmlp_bwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
     reduce(st, w.pl12, nb, ps, DICM_D * H2, DICM_D, g->b2);
     reduce(st, w.pl12, nb, ps, DICM_D * H2 + DICM_D, H2, g->a1);
     reduce(st, w.pl12, nb, ps, DICM_D * H2 + DICM_D + H2, H2, g->b1);
-    reduce(st, w.pl12, nb, ps, L2_PART, H1, g->a0);
-    reduce(st, w.pl12, nb, ps, L2_PART + H1, H1, g->b0);
-    reduce(st, w.pdw1, sm100::small_dw1_blocks(rows_max), (int64_t)H2 * H1, 0, (int64_t)H2 * H1, g->w1);
+    if (bf16) {
+      // dW1 / dalpha0 / db0 from the three row GEMMs of k_dw1b
+      const int gp = sm100::dw1_bf16_part_size();
+      reduce(st, w.pdw1, sm100::small_dw1_blocks(rows_max), gp, 0, gp, w.g3);
+      rc = sm100::l1_finish_bf16(w.g3, p->w1, p->a0, g->b1, g->w1, g->a0, g->b0, st);
+      if (rc) return rc;
+    } else {
+      reduce(st, w.pl12, nb, ps, L2_PART, H1, g->a0);
+      reduce(st, w.pl12, nb, ps, L2_PART + H1, H1, g->b0);
+      reduce(st, w.pdw1, sm100::small_dw1_blocks(rows_max), (int64_t)H2 * H1, 0, (int64_t)H2 * H1, g->w1);
+    }
     rc = sm100::bwd_dw0(pool, pool_dtype, d_raw, rows, count_dev, rows_max, w.da0, g->w0, precision, tc_ws, st,
                         bf16);
     if (rc) return rc;

@@ -96,7 +96,7 @@ template <int KIND>
 __global__ void __launch_bounds__(THREADS_F, 1)
     k_fwd(const __grid_constant__ CUtensorMap tmW, const void* __restrict__ pool_, int d_raw,
           const int32_t* __restrict__ rows, const int32_t* __restrict__ count, const float* __restrict__ bias,
-          float* __restrict__ act0) {
+          void* __restrict__ act0_) {
   using T = Elem<KIND>;
   constexpr int EPB = 128 / sizeof(T);  // elements per 128-byte row slice
   const int U = *count;
@@ -188,8 +188,14 @@ __global__ void __launch_bounds__(THREADS_F, 1)
           tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + h * 256 + cb * 32, v);
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] += __ldg(bias + cb * 32 + j);
-          epi::store_f32(v, scr, lane, m0 + h * 128 + q * 32, U,
-                         [&](int r) { return act0 + (int64_t)r * 256 + cb * 32; });
+          // bf16 mode saves act0 as bf16 (the layer-1 operand precision)
+          if constexpr (KIND == 1)
+            epi::store_bf16(v, scr, lane, m0 + h * 128 + q * 32, U, [&](int r) {
+              return reinterpret_cast<__nv_bfloat16*>(act0_) + (int64_t)r * 256 + cb * 32;
+            });
+          else
+            epi::store_f32(v, scr, lane, m0 + h * 128 + q * 32, U,
+                           [&](int r) { return reinterpret_cast<float*>(act0_) + (int64_t)r * 256 + cb * 32; });
         }
       }
       tc_fence_before();

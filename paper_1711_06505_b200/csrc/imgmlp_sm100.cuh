@@ -7,7 +7,7 @@ namespace sm100 {
 
 size_t workspace_bytes(int64_t rows_max, int d_raw);
 
-// act0[r, 0:256] = X[rows[r]] . W0^T + b0 for r < *count
+// act0[r, 0:256] = X[rows[r]] . W0^T + b0 for r < *count (bf16 in bf16 mode)
 int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows, const int32_t* count,
                int64_t rows_max, const float* w0, const float* b0, float* act0, int precision, void* ws,
                cudaStream_t st);
@@ -29,6 +29,18 @@ int fwd_layers12(const float* act0, const int32_t* count, int64_t rows_max, cons
 int bwd_layers12(const float* demb, const float* act1, const float* act0, const float* h1, const int32_t* count,
                  int64_t rows_max, const float* al0, const float* al1, const float* w1, const float* w2, float* da1,
                  float* da0, __nv_bfloat16* da0_bf16, float* part_l12, float* part_dw1, cudaStream_t st);
+
+// bf16 mode (imgmlp_bf16_sm100.cu): saved activations act0/act1 are bf16
+int fwd_layers12_bf16(const __nv_bfloat16* act0, const int32_t* count, int64_t rows_max, const float* al0,
+                      const float* w1, const float* b1, const float* al1, const float* w2, const float* b2,
+                      __nv_bfloat16* act1, float* emb, cudaStream_t st);
+int bwd_layers12_bf16(const float* demb, const __nv_bfloat16* act1, const __nv_bfloat16* act0, const int32_t* count,
+                      int64_t rows_max, const float* al0, const float* al1, const float* w1, const float* w2,
+                      __nv_bfloat16* da1, __nv_bfloat16* da0, float* part_l12, float* part_dw1, cudaStream_t st);
+// dW1 / dalpha0 / db0 from the reduced row GEMMs G = [Gp | Gn | Gm] ([3][64][256])
+int l1_finish_bf16(const float* G, const float* w1, const float* al0, const float* db1, float* gw1, float* ga0,
+                   float* gb0, cudaStream_t st);
+int dw1_bf16_part_size();  // floats per k_dw1b block partial
 
 }  // namespace sm100
 }  // namespace dicm
