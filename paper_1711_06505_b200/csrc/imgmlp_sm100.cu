@@ -22,6 +22,7 @@
 // nsplit chunks per 256-feature tile and finished by a deterministic reduce.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "imgmlp_sm100.cuh"
@@ -205,6 +206,179 @@ __global__ void __launch_bounds__(THREADS_F, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 4) tmem_dealloc(tmem, 512);
+}
+
+// ---------------------------------------------------------------------------
+// forward on CTA pairs (cta_group::2): a cluster of two CTAs computes a
+// 256-row tile with one M256 x N256 MMA per k-step.  Each CTA gathers its own
+// 128 rows and TMA-loads its half of W0 (128 of the 256 output features), so
+// per SM the MMA reads half the B operand from shared memory, and the
+// accumulator (128 lanes x 256 columns per CTA) is double-buffered in TMEM:
+// the epilogue of tile i overlaps the MMAs of tile i+1.  The peer CTA's
+// stage completion is relayed to the leader's barrier by one peer thread.
+// ---------------------------------------------------------------------------
+constexpr uint32_t OPB2 = 128 * 128;  // 16 KB: one CTA's operand half per k-block
+__host__ __device__ constexpr size_t smem2(int sa, int sb) {
+  return (size_t)(sa + sb) * OPB2 + 1024 + 256 + 4 * epi::SCRATCH_FLOATS * 4;
+}
+
+// SA2 gathered-row slots (HBM latency), SB2 W0 slots (L2-resident)
+template <int KIND, int SA2, int SB2>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F, 1)
+    k_fwd2(const __grid_constant__ CUtensorMap tmW, const void* __restrict__ pool_, int d_raw,
+           const int32_t* __restrict__ rows, const int32_t* __restrict__ count, const float* __restrict__ bias,
+           void* __restrict__ act0_) {
+  using T = Elem<KIND>;
+  constexpr int EPB = 128 / sizeof(T);
+  const int U = *count;
+  const int ntiles = (U + 255) / 256;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  if (pair >= ntiles) return;  // uniform across the pair
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t r0s = smem_u32(smem_raw);
+  const uint32_t base = (r0s + 1023u) & ~1023u, bbase = base + SA2 * OPB2;
+  const uint32_t fullA = bbase + SB2 * OPB2, emptyA = fullA + 8 * SA2, fullB = emptyA + 8 * SA2,
+                 emptyB = fullB + 8 * SB2, accf = emptyB + 8 * SB2, acce = accf + 16, slot = acce + 16;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < SA2; ++i) {
+      mbar_init(fullA + 8 * i, 128 + (rank == 0 ? 1 : 0));  // gathers (+ the peer's relay)
+      mbar_init(emptyA + 8 * i, 1);                         // pair MMA commit (multicast)
+    }
+    for (int i = 0; i < SB2; ++i) {
+      mbar_init(fullB + 8 * i, 1);
+      mbar_init(emptyB + 8 * i, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(accf + 8 * b, 1);
+      mbar_init(acce + 8 * b, 8);  // both CTAs' 4 epilogue warps (leader's copy is used)
+    }
+    fence_mbar_init();
+  }
+  if (warp == 4) {
+    tmem_alloc2(slot, 512);
+    tmem_relinquish2();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem_raw + (slot - r0s));
+  const int nk = d_raw / EPB;
+  const T* pool = reinterpret_cast<const T*>(pool_);
+
+  if (warp < 4) {
+    // ---- gather producer: 8 rows x one 16-B chunk per thread and stage
+    const int t = threadIdx.x, c = t & 7, rb = t >> 3;
+    const uint32_t dst0 = (uint32_t)(rb * 128 + ((c ^ (rb & 7)) << 4));
+    uint32_t g = 0;
+    for (int tile = pair; tile < ntiles; tile += npairs) {
+      const int m0 = tile * 256 + (int)rank * 128;
+      const T* src[8];
+      uint32_t ok[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int gr = m0 + rb + 16 * i;
+        const bool v = gr < U;
+        src[i] = pool + (int64_t)(v ? __ldg(rows + gr) : 0) * d_raw + c * (16 / sizeof(T));
+        ok[i] = v ? 16u : 0u;
+      }
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const uint32_t st = g % SA2, it = g / SA2;
+        mbar_wait(emptyA + 8 * st, (it & 1) ^ 1);
+        const uint32_t a = base + st * OPB2 + dst0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cp_async16(a + i * 16 * 128, src[i] + (int64_t)kb * EPB, ok[i]);
+        cp_async_arrive_noinc(fullA + 8 * st);
+      }
+    }
+    cp_async_wait<0>();
+  } else if (warp == 5) {
+    if (lane == 0) {
+      // ---- TMA producer: this CTA's half of W0 (rows rank*128 .. +127)
+      prefetch_tmap(&tmW);
+      uint32_t g = 0;
+      for (int tile = pair; tile < ntiles; tile += npairs)
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const uint32_t st = g % SB2, it = g / SB2;
+          mbar_wait(emptyB + 8 * st, (it & 1) ^ 1);
+          mbar_arrive_expect_tx(fullB + 8 * st, OPB2);
+          tma_load_2d(bbase + st * OPB2, &tmW, fullB + 8 * st, kb * EPB, (int)rank * 128);
+        }
+    }
+  } else if (warp == 4) {
+    if (lane == 0) {
+      if (rank == 0) {
+        // ---- MMA issuer (leader): M256 x N256 per k-step into TMEM buffer tl&1
+        const uint32_t idesc = instr_desc(KIND == 0 ? 2u : 1u, 256, 256, 0, 0);
+        uint32_t g = 0, tl = 0;
+        for (int tile = pair; tile < ntiles; tile += npairs, ++tl) {
+          const uint32_t buf = tl & 1;
+          mbar_wait(acce + 8 * buf, ((tl >> 1) & 1) ^ 1);
+          tc_fence_after();
+          for (int kb = 0; kb < nk; ++kb, ++g) {
+            const uint32_t sa = g % SA2, sb = g % SB2;
+            mbar_wait(fullA + 8 * sa, (g / SA2) & 1);
+            mbar_wait(fullB + 8 * sb, (g / SB2) & 1);
+            tc_fence_after();
+            fence_proxy_async();
+            const uint32_t a = base + sa * OPB2, b = bbase + sb * OPB2;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma2<KIND>(tmem + buf * 256, smem_desc(a + k * 32, 16, 1024), smem_desc(b + k * 32, 16, 1024), idesc,
+                         (kb | k) != 0);
+            mma_commit2(emptyA + 8 * sa, 0x3);
+            mma_commit2(emptyB + 8 * sb, 0x3);
+          }
+          mma_commit2(accf + 8 * buf, 0x3);
+        }
+      } else {
+        // ---- relay (peer): this CTA's stage landed -> the leader's full barrier
+        const uint32_t lfull = mapa(fullA, 0);
+        uint32_t g = 0;
+        for (int tile = pair; tile < ntiles; tile += npairs)
+          for (int kb = 0; kb < nk; ++kb, ++g) {
+            const uint32_t sa = g % SA2;
+            mbar_wait(fullA + 8 * sa, (g / SA2) & 1);
+            mbar_wait(fullB + 8 * (g % SB2), (g / SB2) & 1);
+            fence_proxy_async();
+            mbar_arrive_cluster(lfull + 8 * sa);
+          }
+      }
+    }
+  } else {
+    // ---- epilogue warps 6-9: this CTA's 128 rows, TMEM lane quarter = warp % 4
+    const int q = warp & 3;
+    float* scr = reinterpret_cast<float*>(smem_raw + (slot + 16 - r0s)) + q * epi::SCRATCH_FLOATS;
+    const uint32_t lacce = mapa(acce, 0);
+    uint32_t tl = 0;
+    for (int tile = pair; tile < ntiles; tile += npairs, ++tl) {
+      const uint32_t buf = tl & 1;
+      mbar_wait(accf + 8 * buf, (tl >> 1) & 1);
+      tc_fence_after();
+      const int m0 = tile * 256 + (int)rank * 128 + q * 32;
+#pragma unroll 1
+      for (int cb = 0; cb < 8; ++cb) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * 256 + cb * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] += __ldg(bias + cb * 32 + j);
+        if constexpr (KIND == 1)
+          epi::store_bf16(v, scr, lane, m0, U, [&](int r) {
+            return reinterpret_cast<__nv_bfloat16*>(act0_) + (int64_t)r * 256 + cb * 32;
+          });
+        else
+          epi::store_f32(v, scr, lane, m0, U,
+                         [&](int r) { return reinterpret_cast<float*>(act0_) + (int64_t)r * 256 + cb * 32; });
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(lacce + 8 * buf);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 4) tmem_dealloc2(tmem, 512);
 }
 
 // ---------------------------------------------------------------------------
@@ -442,6 +616,36 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
     k_to_bf16<<<dicm_grid(256 * d_raw / 2, 256, 148 * 4), 256, 0, st>>>(w0, nullptr, 0, (int64_t)256 * d_raw,
                                                                           w.w0_bf16);
     wsrc = w.w0_bf16;
+  }
+  static const bool pair = [] {
+    const char* e = getenv("DICM_FWD_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  if (pair) {
+    if ((rc = make_map(&map, wsrc, bf16, 256, d_raw, 128))) return rc;
+    // persistent CTA pairs: <= 74 clusters of 2 (one CTA per SM)
+    const int grid = 2 * (int)std::min<int64_t>(74, (rows_max + 255) / 256);
+    auto launch = [&](auto kern, size_t smem) -> int {
+      static std::once_flag f;
+      static int rc0 = 0;
+      std::call_once(f, [&] {
+        rc0 = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                         "k_fwd2 smem");
+      });
+      if (rc0) return rc0;
+      kern<<<grid, THREADS_F, smem, st>>>(map, pool, d_raw, rows, count, b0, act0);
+      return 0;
+    };
+    const int probe_slot = probe_begin(DICM_PROBE_IMG_FWD_L0, st);
+    int lrc;
+    if (bf16) {
+      lrc = launch(k_fwd2<1, 6, 6>, smem2(6, 6));
+    } else {
+      lrc = launch(k_fwd2<0, 6, 6>, smem2(6, 6));
+    }
+    probe_end(probe_slot, st);
+    if (lrc) return lrc;
+    return last_launch("tcgen05 layer-0 forward (CTA pairs)");
   }
   if ((rc = make_map(&map, wsrc, bf16, 256, d_raw, 256))) return rc;
   const int grid = (int)std::min<int64_t>(148, (rows_max + 255) / 256);  // persistent: <= one CTA per SM
