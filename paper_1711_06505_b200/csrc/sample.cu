@@ -13,8 +13,15 @@
 // Backward reverses the graph (segment_softmax bwd autograd.py:334-337,
 // col_scale bwd 348-350, linear/prelu bwd 201-204/222-225) and scatter-adds
 // embedding and ID-row gradients into the deduplicated row buffers
-// (np.add.at, autograd.py:267-271).  Attention-parameter gradients are
-// accumulated lane-per-hidden-unit and written as deterministic block partials.
+// (np.add.at, autograd.py:267-271) with 16-byte vector reductions
+// (red.global.add.v4.f32: three per 12-float row).  It runs as one scatter
+// kernel (fields, ad image, sum pooling) plus one kernel per attention channel,
+// so each launch carries only the registers its own work needs.
+// Attention-parameter gradients are accumulated lane-per-hidden-unit and
+// written as deterministic block partials.
+//
+// Every per-reference loop keeps several independent row loads in flight per
+// lane (the index -> row gather chain is L2-latency bound otherwise).
 #include <math.h>
 
 #include "common.cuh"
@@ -26,6 +33,69 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int FWD_WARPS = 8;
 constexpr int BWD_WARPS = 8;
 constexpr int MAXQ = 2 * DICM_D;
+constexpr int UNR = 4;  // rows in flight per lane in the gather loops
+
+__device__ __forceinline__ void red_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+// += v into a 12-float row with three 16-byte reductions
+__device__ __forceinline__ void red_row12(float* p, const float (&v)[DICM_D]) {
+  red_v4(p, v[0], v[1], v[2], v[3]);
+  red_v4(p + 4, v[4], v[5], v[6], v[7]);
+  red_v4(p + 8, v[8], v[9], v[10], v[11]);
+}
+// lanes 0-2 add one 16-byte quarter each of the row v (same in every lane)
+__device__ __forceinline__ void red_row12_lanes(float* p, const float (&v)[DICM_D], int lane) {
+  if (lane < 3) {
+    float a = v[0], b = v[1], c = v[2], d = v[3];
+    if (lane == 1) a = v[4], b = v[5], c = v[6], d = v[7];
+    if (lane == 2) a = v[8], b = v[9], c = v[10], d = v[11];
+    red_v4(p + 4 * lane, a, b, c, d);
+  }
+}
+__device__ __forceinline__ void load12(const float* p, float (&v)[DICM_D]) {
+  const Row12 r = load_row12(p);
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) v[c] = r.v[c];
+}
+
+// acc += sum_{i in [i0, i1)} T[ids[i]]  (lane-strided, UNR rows in flight)
+__device__ __forceinline__ void seg_sum(const int32_t* __restrict__ ids, int64_t i0, int64_t i1,
+                                        const float* __restrict__ T, int lane, float (&acc)[DICM_D]) {
+  for (int64_t b = i0 + lane; b < i1; b += 32 * UNR) {
+    int id[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) id[u] = b + 32 * u < i1 ? __ldg(ids + b + 32 * u) : -1;
+    Row12 r[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (id[u] >= 0) {
+        r[u] = load_row12(T + (int64_t)id[u] * DICM_D);
+      } else {
+#pragma unroll
+        for (int c = 0; c < DICM_D; ++c) r[u].v[c] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) acc[c] += r[u].v[c];
+  }
+}
+
+// rows[ids[i]] += v for i in [i0, i1)  (lane-strided, UNR indices in flight)
+__device__ __forceinline__ void seg_scatter(const int32_t* __restrict__ ids, int64_t i0, int64_t i1, float* rows,
+                                            const float (&v)[DICM_D], int lane) {
+  for (int64_t b = i0 + lane; b < i1; b += 32 * UNR) {
+    int id[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) id[u] = b + 32 * u < i1 ? __ldg(ids + b + 32 * u) : -1;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+      if (id[u] >= 0) red_row12(rows + (int64_t)id[u] * DICM_D, v);
+  }
+}
 
 struct __align__(16) AttnSmem {
   float wq[DICM_ATT][MAXQ];
@@ -94,11 +164,11 @@ __device__ __forceinline__ float query_proj(const AttnSmem& s, const float (&q)[
   return p;
 }
 
-__device__ __forceinline__ float attn_score(const AttnSmem& s, const float (&P)[DICM_ATT], const Row12& k) {
+__device__ __forceinline__ float attn_score(const AttnSmem& s, const float* P, const Row12& k) {
   float sc = s.b1;
 #pragma unroll 8
   for (int j = 0; j < DICM_ATT; ++j) {
-    float pre = P[j];
+    float pre = P[j];  // shared-memory broadcast
 #pragma unroll
     for (int c = 0; c < DICM_D; ++c) pre = fmaf(s.wk[j][c], k.v[c], pre);
     sc = fmaf(s.w1[j], prelu(pre, s.a0[j]), sc);
@@ -111,20 +181,26 @@ __device__ __forceinline__ float attn_score(const AttnSmem& s, const float (&P)[
 // ---------------------------------------------------------------------------
 
 template <int DQ>
-__device__ void attn_fwd(const Args& a, const AttnSmem& s, int ch, int b, int lane) {
-  float q[DQ];
-  load_query<DQ>(a, ch, b, q);
-  const float pj = query_proj<DQ>(s, q, lane);
-  float P[DICM_ATT];
-#pragma unroll
-  for (int j = 0; j < DICM_ATT; ++j) P[j] = __shfl_sync(FULL, pj, j);
+__device__ void attn_fwd(const Args& a, const AttnSmem& s, int ch, int b, int lane, float* P) {
+  {
+    float q[DQ];
+    load_query<DQ>(a, ch, b, q);
+    const float pj = query_proj<DQ>(s, q, lane);
+    __syncwarp();
+    P[lane] = pj;
+    __syncwarp();
+  }
   const int64_t i0 = a.V.beh_off[b], i1 = a.V.beh_off[b + 1];
   float m = -INFINITY, ssum = 0.f, acc[DICM_D];
 #pragma unroll
   for (int c = 0; c < DICM_D; ++c) acc[c] = 0.f;
   const bool norm = a.L.normalize != 0;
+  // the next reference's row is in flight while this one is scored
+  Row12 kn;
+  if (i0 + lane < i1) kn = load_row12(a.V.emb + (int64_t)__ldg(a.V.beh_local + i0 + lane) * DICM_D);
   for (int64_t i = i0 + lane; i < i1; i += 32) {
-    const Row12 k = load_row12(a.V.emb + (int64_t)a.V.beh_local[i] * DICM_D);
+    const Row12 k = kn;
+    if (i + 32 < i1) kn = load_row12(a.V.emb + (int64_t)__ldg(a.V.beh_local + i + 32) * DICM_D);
     const float sc = attn_score(s, P, k);
     a.scores[(int64_t)ch * a.V.refs + i] = sc;
     if (norm) {
@@ -164,8 +240,9 @@ __device__ void attn_fwd(const Args& a, const AttnSmem& s, int ch, int b, int la
     if (lane == c) dst[c] = out[c];
 }
 
-__global__ void __launch_bounds__(FWD_WARPS * 32) k_sample_fwd(const __grid_constant__ Args a) {
+__global__ void __launch_bounds__(FWD_WARPS * 32, 3) k_sample_fwd(const __grid_constant__ Args a) {
   __shared__ AttnSmem sa[2];
+  __shared__ float Pw[FWD_WARPS][DICM_ATT];  // per-warp query projection
   const bool att = a.L.use_behavior_images && a.L.kind != 0;
   if (att) {
     load_attn(sa[0], a.A[0], DICM_D);
@@ -182,15 +259,10 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_sample_fwd(const __grid_cons
         if (lane < DICM_D) row[a.L.field_col[f] + lane] = __ldg(T + (int64_t)a.V.field_inv[f][b] * DICM_D + lane);
       } else {
         const int32_t* off = a.V.field_off[f];
-        const int32_t* ids = a.V.field_inv[f];  // rows of the compact table
         float acc[DICM_D];
 #pragma unroll
         for (int c = 0; c < DICM_D; ++c) acc[c] = 0.f;
-        for (int64_t i = off[b] + lane; i < off[b + 1]; i += 32) {
-          const Row12 r = load_row12(T + (int64_t)ids[i] * DICM_D);
-#pragma unroll
-          for (int c = 0; c < DICM_D; ++c) acc[c] += r.v[c];
-        }
+        seg_sum(a.V.field_inv[f], off[b], off[b + 1], T, lane, acc);  // rows of the compact table
 #pragma unroll
         for (int c = 0; c < DICM_D; ++c) acc[c] = warp_sum(acc[c]);
 #pragma unroll
@@ -205,23 +277,19 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_sample_fwd(const __grid_cons
       float acc[DICM_D];
 #pragma unroll
       for (int c = 0; c < DICM_D; ++c) acc[c] = 0.f;
-      for (int64_t i = a.V.beh_off[b] + lane; i < a.V.beh_off[b + 1]; i += 32) {
-        const Row12 r = load_row12(a.V.emb + (int64_t)a.V.beh_local[i] * DICM_D);
-#pragma unroll
-        for (int c = 0; c < DICM_D; ++c) acc[c] += r.v[c];
-      }
+      seg_sum(a.V.beh_local, a.V.beh_off[b], a.V.beh_off[b + 1], a.V.emb, lane, acc);
 #pragma unroll
       for (int c = 0; c < DICM_D; ++c) acc[c] = warp_sum(acc[c]);
 #pragma unroll
       for (int c = 0; c < DICM_D; ++c)
         if (lane == c) row[a.L.pool_col + c] = acc[c];
     } else {
-      attn_fwd<DICM_D>(a, sa[0], 0, b, lane);
+      attn_fwd<DICM_D>(a, sa[0], 0, b, lane, Pw[warp]);
       if (a.L.kind == 2) {
         if (a.L.n_query == 2)
-          attn_fwd<2 * DICM_D>(a, sa[1], 1, b, lane);
+          attn_fwd<2 * DICM_D>(a, sa[1], 1, b, lane, Pw[warp]);
         else
-          attn_fwd<DICM_D>(a, sa[1], 1, b, lane);
+          attn_fwd<DICM_D>(a, sa[1], 1, b, lane, Pw[warp]);
       }
     }
   }
@@ -235,6 +303,7 @@ struct __align__(16) WarpScratch {
   float ds[32];
   float ks[32][DICM_D];
   float dp[32][DICM_ATT + 1];
+  float wq[32][MAXQ + 1];  // lane j's dWq accumulators (kept out of registers)
 };
 
 __host__ __device__ constexpr int chan_part(int dq) { return 3 * DICM_ATT + 1 + DICM_ATT * (dq + DICM_D); }
@@ -253,9 +322,12 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
                          AttnAcc<DQ>& acc) {
   const int64_t i0 = a.V.beh_off[b], i1 = a.V.beh_off[b + 1];
   if (i1 <= i0) return;
-  float q[DQ];
-  load_query<DQ>(a, ch, b, q);
-  const float Pj = query_proj<DQ>(s, q, lane);
+  float Pj;
+  {
+    float q[DQ];  // reloaded at the end: not live across the reference loops
+    load_query<DQ>(a, ch, b, q);
+    Pj = query_proj<DQ>(s, q, lane);
+  }
   float wkj[DICM_D];
 #pragma unroll
   for (int c = 0; c < DICM_D; ++c) wkj[c] = s.wk[lane][c];
@@ -275,30 +347,57 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
   // pass 1: dot = sum_i w_i (dout . k_i)   (softmax backward, autograd.py:335-337)
   float dot = 0.f;
   if (norm) {
-    for (int64_t i = i0 + lane; i < i1; i += 32) {
-      const Row12 k = load_row12(a.V.emb + (int64_t)a.V.beh_local[i] * DICM_D);
-      float dw = 0.f;
+    for (int64_t b0 = i0 + lane; b0 < i1; b0 += 32 * UNR) {
+      int id[UNR];
+      float scv[UNR];
 #pragma unroll
-      for (int c = 0; c < DICM_D; ++c) dw = fmaf(dout[c], k.v[c], dw);
-      dot = fmaf(expf(sc[i] - M) * invS, dw, dot);
+      for (int u = 0; u < UNR; ++u) {
+        const bool v = b0 + 32 * u < i1;
+        id[u] = v ? __ldg(a.V.beh_local + b0 + 32 * u) : -1;
+        scv[u] = v ? sc[b0 + 32 * u] : 0.f;
+      }
+      Row12 k[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+        if (id[u] >= 0) k[u] = load_row12(a.V.emb + (int64_t)id[u] * DICM_D);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        if (id[u] < 0) continue;
+        float dw = 0.f;
+#pragma unroll
+        for (int c = 0; c < DICM_D; ++c) dw = fmaf(dout[c], k[u].v[c], dw);
+        dot = fmaf(expf(scv[u] - M) * invS, dw, dot);
+      }
     }
     dot = warp_sum(dot);
   }
   float dP = 0.f;
-  // pass 2: chunks of 32 references, lane r owns reference r of the chunk
+  // pass 2: chunks of 32 references, lane r owns reference r of the chunk;
+  // the next chunk's row and score are in flight while this one is processed
+  int32_t row_n = i0 + lane < i1 ? __ldg(a.V.beh_local + i0 + lane) : 0;
+  Row12 k_n;
+  float sc_n = 0.f;
+  if (i0 + lane < i1) {
+    k_n = load_row12(a.V.emb + (int64_t)row_n * DICM_D);
+    sc_n = sc[i0 + lane];
+  }
   for (int64_t c0 = i0; c0 < i1; c0 += 32) {
     const int64_t i = c0 + lane;
     const bool valid = i < i1;
-    Row12 k;
+    Row12 k = k_n;
+    const int32_t row = row_n;
+    const float sci = sc_n;
+    if (i + 32 < i1) {
+      row_n = __ldg(a.V.beh_local + i + 32);
+      k_n = load_row12(a.V.emb + (int64_t)row_n * DICM_D);
+      sc_n = sc[i + 32];
+    }
     float w = 0.f, ds = 0.f;
-    int32_t row = 0;
     if (valid) {
-      row = a.V.beh_local[i];
-      k = load_row12(a.V.emb + (int64_t)row * DICM_D);
       float dw = 0.f;
 #pragma unroll
       for (int c = 0; c < DICM_D; ++c) dw = fmaf(dout[c], k.v[c], dw);
-      w = norm ? expf(sc[i] - M) * invS : sc[i];
+      w = norm ? expf(sci - M) * invS : sci;
       ds = norm ? w * (dw - dot) : dw;
     } else {
 #pragma unroll
@@ -338,35 +437,26 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
 #pragma unroll
         for (int c = 0; c < DICM_D; ++c) dk[c] = fmaf(s.wk[j][c], d, dk[c]);
       }
-      atomic_add_row12(a.d_emb + (int64_t)row * DICM_D, dk);
+      red_row12(a.d_emb + (int64_t)row * DICM_D, dk);
     }
     __syncwarp();
   }
   // query side: dWq[j] += dP_j q ; dq = Wq^T dP
+  float q[DQ];
+  load_query<DQ>(a, ch, b, q);
 #pragma unroll
-  for (int t = 0; t < DQ; ++t) acc.wq[t] = fmaf(dP, q[t], acc.wq[t]);
+  for (int t = 0; t < DQ; ++t) ws.wq[lane][t] = fmaf(dP, q[t], ws.wq[lane][t]);
   float dq[DQ];
 #pragma unroll
   for (int t = 0; t < DQ; ++t) dq[t] = warp_sum(s.wq[lane][t] * dP);
   if (ch == 0) {
-    if (lane < DICM_D) {
-      float v = 0.f;
-#pragma unroll
-      for (int c = 0; c < DICM_D; ++c)
-        if (c == lane) v = dq[c];
-      atomicAdd(a.d_emb + (int64_t)a.V.ad_local[b] * DICM_D + lane, v);
-    }
+    red_row12_lanes(a.d_emb + (int64_t)a.V.ad_local[b] * DICM_D, *reinterpret_cast<float(*)[DICM_D]>(dq), lane);
   } else {
 #pragma unroll
     for (int f = 0; f < DQ / DICM_D; ++f) {
       const int fi = a.L.query_field[f];
-      if (lane < DICM_D) {
-        float v = 0.f;
-#pragma unroll
-        for (int c = 0; c < DICM_D; ++c)
-          if (c == lane) v = dq[f * DICM_D + c];
-        atomicAdd(a.d_rows + (int64_t)a.V.field_inv[fi][b] * DICM_D + lane, v);
-      }
+      red_row12_lanes(a.d_rows + (int64_t)a.V.field_inv[fi][b] * DICM_D,
+                      *reinterpret_cast<float(*)[DICM_D]>(dq + f * DICM_D), lane);
     }
   }
 }
@@ -402,8 +492,12 @@ __device__ void attn_channel_bwd(const Args& a, const AttnSmem& s, WarpScratch& 
                                  float* red, float* part_base) {
   AttnAcc<DQ> acc;
   zero_acc(acc);
+#pragma unroll
+  for (int t = 0; t < DQ; ++t) ws.wq[lane][t] = 0.f;
   for (int b = blockIdx.x * BWD_WARPS + warp; b < a.V.batch; b += gridDim.x * BWD_WARPS)
     attn_bwd<DQ>(a, s, ws, ch, b, lane, acc);
+#pragma unroll
+  for (int t = 0; t < DQ; ++t) acc.wq[t] = ws.wq[lane][t];
   __syncthreads();  // scratch -> reduction buffer
   const int n = chan_part(DQ);
   dump_acc<DQ>(acc, red + warp * n, lane);
@@ -416,55 +510,44 @@ __device__ void attn_channel_bwd(const Args& a, const AttnSmem& s, WarpScratch& 
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(BWD_WARPS * 32) k_sample_bwd(const __grid_constant__ Args a, int64_t part_stride) {
-  __shared__ AttnSmem sa[2];
+// one attention channel per launch (its DQ fixed at compile time)
+template <int DQ>
+__global__ void __launch_bounds__(BWD_WARPS * 32, 2)
+    k_attn_bwd(const __grid_constant__ Args a, int ch, int64_t part_stride, int64_t part_off) {
+  __shared__ AttnSmem sa;
   extern __shared__ float dyn[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool att = a.L.use_behavior_images && a.L.kind != 0;
-  if (att) {
-    load_attn(sa[0], a.A[0], DICM_D);
-    if (a.L.kind == 2) load_attn(sa[1], a.A[1], DICM_D * a.L.n_query);
-    __syncthreads();
-    WarpScratch& ws = reinterpret_cast<WarpScratch*>(dyn)[warp];
-    float* base = a.attn_part + (int64_t)blockIdx.x * part_stride;
-    // sorted names: attn/id/* before attn/img/*
-    if (a.L.kind == 2) {
-      const int id_size = chan_part(DICM_D * a.L.n_query);
-      if (a.L.n_query == 2)
-        attn_channel_bwd<2 * DICM_D>(a, sa[1], ws, 1, lane, warp, dyn, base);
-      else
-        attn_channel_bwd<DICM_D>(a, sa[1], ws, 1, lane, warp, dyn, base);
-      attn_channel_bwd<DICM_D>(a, sa[0], ws, 0, lane, warp, dyn, base + id_size);
-    } else {
-      attn_channel_bwd<DICM_D>(a, sa[0], ws, 0, lane, warp, dyn, base);
-    }
-  }
-  // field / embedding scatters
+  load_attn(sa, a.A[ch], DQ);
+  __syncthreads();
+  WarpScratch& ws = reinterpret_cast<WarpScratch*>(dyn)[warp];
+  attn_channel_bwd<DQ>(a, sa, ws, ch, lane, warp, dyn, a.attn_part + (int64_t)blockIdx.x * part_stride + part_off);
+}
+
+// field / ad-image / sum-pooling scatters: the gradient row of the sample is
+// added to every row it was gathered from
+__global__ void __launch_bounds__(BWD_WARPS * 32, 4) k_sample_scatter(const __grid_constant__ Args a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int b = blockIdx.x * BWD_WARPS + warp; b < a.V.batch; b += gridDim.x * BWD_WARPS) {
     const float* drow = a.d_head_in + (int64_t)b * a.L.width;
     for (int f = 0; f < a.L.n_fields; ++f) {
-      const float* dsrc = drow + a.L.field_col[f];
+      float dv[DICM_D];
+      load12(drow + a.L.field_col[f], dv);
       if (!a.L.field_multi[f]) {
-        if (lane < DICM_D)
-          atomicAdd(a.d_rows + (int64_t)a.V.field_inv[f][b] * DICM_D + lane, __ldg(dsrc + lane));
+        red_row12_lanes(a.d_rows + (int64_t)a.V.field_inv[f][b] * DICM_D, dv, lane);
       } else {
-        float dv[DICM_D];
-#pragma unroll
-        for (int c = 0; c < DICM_D; ++c) dv[c] = __ldg(dsrc + c);
         const int32_t* off = a.V.field_off[f];
-        const int32_t* inv = a.V.field_inv[f];
-        for (int64_t i = off[b] + lane; i < off[b + 1]; i += 32)
-          atomic_add_row12(a.d_rows + (int64_t)inv[i] * DICM_D, dv);
+        seg_scatter(a.V.field_inv[f], off[b], off[b + 1], a.d_rows, dv, lane);
       }
     }
-    if (a.L.use_ad_image && lane < DICM_D)
-      atomicAdd(a.d_emb + (int64_t)a.V.ad_local[b] * DICM_D + lane, __ldg(drow + a.L.ad_col + lane));
+    if (a.L.use_ad_image) {
+      float dv[DICM_D];
+      load12(drow + a.L.ad_col, dv);
+      red_row12_lanes(a.d_emb + (int64_t)a.V.ad_local[b] * DICM_D, dv, lane);
+    }
     if (a.L.use_behavior_images && a.L.kind == 0) {
       float dv[DICM_D];
-#pragma unroll
-      for (int c = 0; c < DICM_D; ++c) dv[c] = __ldg(drow + a.L.pool_col + c);
-      for (int64_t i = a.V.beh_off[b] + lane; i < a.V.beh_off[b + 1]; i += 32)
-        atomic_add_row12(a.d_emb + (int64_t)a.V.beh_local[i] * DICM_D, dv);
+      load12(drow + a.L.pool_col, dv);
+      seg_scatter(a.V.beh_local, a.V.beh_off[b], a.V.beh_off[b + 1], a.d_emb, dv, lane);
     }
   }
 }
@@ -472,6 +555,12 @@ __global__ void __launch_bounds__(BWD_WARPS * 32) k_sample_bwd(const __grid_cons
 int bwd_grid(int batch) {
   const int g = (batch + BWD_WARPS - 1) / BWD_WARPS;
   return g < 1 ? 1 : (g > 148 * 8 ? 148 * 8 : g);
+}
+
+template <typename K>
+int dyn_smem_attr(K kernel, size_t bytes) {
+  return check_cuda(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes),
+                    "sample_bwd smem attribute");
 }
 
 size_t bwd_smem() {
@@ -554,17 +643,27 @@ int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
   a.d_rows = d_rows;
   a.attn_part = attn_partials;
   const size_t smem = bwd_smem();
-  static bool attr_set = false;
-  if (!attr_set) {
-    rc = check_cuda(cudaFuncSetAttribute(k_sample_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                    "sample_bwd smem attribute");
-    if (rc) return rc;
-    attr_set = true;
-  }
+  static int attr_rc = dyn_smem_attr(k_attn_bwd<DICM_D>, smem) | dyn_smem_attr(k_attn_bwd<2 * DICM_D>, smem);
+  if (attr_rc) return attr_rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int grid = bwd_grid(bv->batch);
+  const int64_t stride = part_size(layout);
   {
-    const int probe_slot = probe_begin(DICM_PROBE_SAMPLE_BWD, (cudaStream_t)stream);
-    k_sample_bwd<<<bwd_grid(bv->batch), BWD_WARPS * 32, smem, (cudaStream_t)stream>>>(a, part_size(layout));
-    probe_end(probe_slot, (cudaStream_t)stream);
+    const int probe_slot = probe_begin(DICM_PROBE_SAMPLE_BWD, st);
+    k_sample_scatter<<<grid, BWD_WARPS * 32, 0, st>>>(a);
+    if (layout->use_behavior_images && layout->kind != 0) {
+      // partial row layout in sorted names: attn/id/* before attn/img/*
+      int64_t img_off = 0;
+      if (layout->kind == 2) {
+        img_off = chan_part(DICM_D * layout->n_query);
+        if (layout->n_query == 2)
+          k_attn_bwd<2 * DICM_D><<<grid, BWD_WARPS * 32, smem, st>>>(a, 1, stride, 0);
+        else
+          k_attn_bwd<DICM_D><<<grid, BWD_WARPS * 32, smem, st>>>(a, 1, stride, 0);
+      }
+      k_attn_bwd<DICM_D><<<grid, BWD_WARPS * 32, smem, st>>>(a, 0, stride, img_off);
+    }
+    probe_end(probe_slot, st);
   }
   return last_launch("dicm_sample_bwd");
 }
