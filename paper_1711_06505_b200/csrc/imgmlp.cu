@@ -165,6 +165,44 @@ __global__ void __launch_bounds__(256) k_colsum(const float* __restrict__ part, 
   }
 }
 
+// several column ranges of one partial array, each into its own output, in
+// one launch (blockIdx.y = range); same fixed association as k_colsum
+struct ColSegs {
+  int64_t off[8], n[8];
+  float* out[8];
+};
+__global__ void __launch_bounds__(256) k_colsum_multi(const float* __restrict__ part, int nblk, int64_t stride,
+                                                      const __grid_constant__ ColSegs segs) {
+  const int sg = blockIdx.y;
+  const int64_t j = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const int64_t n = segs.n[sg];
+  float s = 0.f;
+  if (j < n)
+    for (int b = threadIdx.y; b < nblk; b += 8) s += part[(int64_t)b * stride + segs.off[sg] + j];
+  __shared__ float red[8][33];
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && j < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) t += red[y][threadIdx.x];
+    segs.out[sg][j] = t;
+  }
+}
+
+void reduce_multi(cudaStream_t st, const float* part, int nblk, int64_t stride, int nseg, const int64_t* off,
+                  const int64_t* n, float* const* out) {
+  ColSegs c{};
+  int64_t mx = 1;
+  for (int i = 0; i < nseg; ++i) {
+    c.off[i] = off[i];
+    c.n[i] = n[i];
+    c.out[i] = out[i];
+    mx = std::max(mx, n[i]);
+  }
+  k_colsum_multi<<<dim3((unsigned)((mx + 31) / 32), nseg), dim3(32, 8), 0, st>>>(part, nblk, stride, c);
+}
+
 // tmp: >= ceil(nblk / RED_ROWS) * n floats (or nullptr when nblk <= RED_ROWS)
 void reduce_into(cudaStream_t st, const float* part, int nblk, int64_t stride, int64_t off, int64_t n, float* out,
                  float* tmp, int accumulate, const int32_t* count = nullptr, int rows_per_blk = 0) {
@@ -340,10 +378,13 @@ int dicm_imgmlp_bwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
                              da0_bf16, w.pl12, w.pdw1, st);
     if (rc) return rc;
     const int nb = sm100::small_bwd_blocks(rows_max), ps = sm100::small_part_size();
-    reduce(st, w.pl12, nb, ps, 0, DICM_D * H2, g->w2);
-    reduce(st, w.pl12, nb, ps, DICM_D * H2, DICM_D, g->b2);
-    reduce(st, w.pl12, nb, ps, DICM_D * H2 + DICM_D, H2, g->a1);
-    reduce(st, w.pl12, nb, ps, DICM_D * H2 + DICM_D + H2, H2, g->b1);
+    {
+      // w2 | b2 | a1 | b1 (| a0 | b0 on the tf32 path) in one launch
+      const int64_t off[6] = {0, DICM_D * H2, DICM_D * H2 + DICM_D, DICM_D * H2 + DICM_D + H2, L2_PART, L2_PART + H1};
+      const int64_t n[6] = {DICM_D * H2, DICM_D, H2, H2, H1, H1};
+      float* const out[6] = {g->w2, g->b2, g->a1, g->b1, g->a0, g->b0};
+      reduce_multi(st, w.pl12, nb, ps, bf16 ? 4 : 6, off, n, out);
+    }
     if (bf16) {
       // dW1 / dalpha0 / db0 from the three row GEMMs of k_dw1b
       const int gp = sm100::dw1_bf16_part_size();
@@ -351,8 +392,6 @@ int dicm_imgmlp_bwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
       rc = sm100::l1_finish_bf16(w.g3, p->w1, p->a0, g->b1, g->w1, g->a0, g->b0, st);
       if (rc) return rc;
     } else {
-      reduce(st, w.pl12, nb, ps, L2_PART, H1, g->a0);
-      reduce(st, w.pl12, nb, ps, L2_PART + H1, H1, g->b0);
       reduce(st, w.pdw1, sm100::small_dw1_blocks(rows_max), (int64_t)H2 * H1, 0, (int64_t)H2 * H1, g->w1);
     }
     rc = sm100::bwd_dw0(pool, pool_dtype, d_raw, rows, count_dev, rows_max, w.da0, g->w0, precision, tc_ws, st,

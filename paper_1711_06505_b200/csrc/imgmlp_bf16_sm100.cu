@@ -660,6 +660,7 @@ __global__ void __launch_bounds__(256) k_l1_finish(const float* __restrict__ G, 
   const int f = threadIdx.x;
   const float a = al0[f];
   float sa = 0.f, sb = 0.f;
+#pragma unroll 16
   for (int j = 0; j < 64; ++j) {
     const float gp = G[j * 256 + f], gn = G[16384 + j * 256 + f], gm = G[32768 + j * 256 + f];
     const float w = w1[j * 256 + f];

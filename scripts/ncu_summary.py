@@ -18,8 +18,10 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-PROBE = {"k_fwd": "img_fwd_l0", "k_l12_fwd": "img_fwd_l12", "k_l12_bwd": "img_bwd_l12", "k_dw1": "img_bwd_dw1",
-         "k_dw0": "img_bwd_dw0", "k_sample_fwd": "sample_fwd", "k_sample_bwd": "sample_bwd"}
+PROBE = {"k_fwd": "img_fwd_l0", "k_fwd2": "img_fwd_l0", "k_l12_fwd": "img_fwd_l12", "k_l12f": "img_fwd_l12",
+         "k_l12_bwd": "img_bwd_l12", "k_l12b": "img_bwd_l12", "k_dw1": "img_bwd_dw1", "k_dw1b": "img_bwd_dw1",
+         "k_dw0": "img_bwd_dw0", "k_sample_fwd": "sample_fwd", "k_sample_bwd": "sample_bwd",
+         "k_attn_bwd": "sample_bwd", "k_sample_scatter": "sample_bwd"}
 METRICS = [
     ("gpu__time_duration.sum", "time"),
     ("dram__bytes_read.sum", "DRAM read"),
@@ -40,7 +42,9 @@ SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9,
 
 def short(name):
     """Bare function name: 'void dicm::<unnamed>::k_fwd<1>(CUtensorMap ...)' -> 'k_fwd'."""
-    m = re.search(r"([A-Za-z_][A-Za-z0-9_]*)\s*(<[^()]*>)?\s*\(", name)
+    head = name.split("(")[0]
+    head = re.sub(r"<[^<>]*>$", "", head.strip())  # trailing template arguments
+    m = re.search(r"([A-Za-z_][A-Za-z0-9_]*)\s*$", head)
     return m.group(1) if m else name[:40]
 
 
@@ -88,7 +92,7 @@ def main():
     kern = read_raw(rep)
     agg, cnt = launch_share(launches)
     tot = sum(agg.values())
-    steps = max(cnt.get("k_fwd", 1), 1)
+    steps = max(cnt.get("k_fwd2", 0) or cnt.get("k_fwd", 1), 1)
     lines = [f"# ncu summary: {cfg} / {prec} ({tag})", "",
              f"Source: `{os.path.basename(rep)}` (`ncu --set full --clock-control none --import-source on`, "
              "one launch per kernel, cold-cache replay) and the launch list "
@@ -101,6 +105,7 @@ def main():
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp))
+    seen, fresh = set(), {}
     for d in kern:
         t = d.get("gpu__time_duration.sum") or 0
         rd, wr = d.get("dram__bytes_read.sum") or 0, d.get("dram__bytes_write.sum") or 0
@@ -117,9 +122,14 @@ def main():
                 cells.append(f"{v:.1f}" if v % 1 else f"{int(v)}")
         gbs = (rd + wr) / t / 1e9 if t else 0
         lines.append(f"| {d['name']} | " + " | ".join(cells) + f" | {gbs:.0f} |")
-        if d["name"] in PROBE:
-            traffic[f"{cfg}/{prec}/{PROBE[d['name']]}"] = {"dram_bytes": rd + wr, "unique_images": U,
-                                                           "ncu_time_s": t, "source": f"{tag}:{rep}"}
+        if d["name"] in PROBE and d["name"] not in seen:  # one launch per kernel; probes may span kernels
+            seen.add(d["name"])
+            key = f"{cfg}/{prec}/{PROBE[d['name']]}"
+            e = fresh.setdefault(key, {"dram_bytes": 0.0, "unique_images": U, "ncu_time_s": 0.0,
+                                       "source": f"{tag}:{rep}"})
+            e["dram_bytes"] += rd + wr
+            e["ncu_time_s"] += t
+    traffic.update(fresh)
     lines += ["", "## Launch list: share of the step (serialized, cold-cache)", "",
               "| kernel | launches | total us | us / step | share |", "|---|---|---|---|---|"]
     for k, v in sorted(agg.items(), key=lambda x: -x[1])[:25]:
