@@ -372,6 +372,11 @@ def main():
         barrier()
     ms = start.elapsed_time(end)
     eng.raise_status()
+    if os.environ.get("DICM_PHASE_TIMING") == "1" and hasattr(eng, "phase_times"):
+        step(staged[-1])
+        pt = eng.phase_times()
+        if rank == 0:
+            print("phases(ms):", json.dumps({k: round(v, 3) for k, v in pt.items()}), flush=True)
     probes = {k: LIB.probe_read(k) for k in LIB.PROBE_KERNELS}
     LIB.check(LIB.lib.dicm_probe_enable(0))
     t = torch.tensor([ms], device="cuda")

@@ -283,6 +283,58 @@ int dicm_owner_reduce_rows12(const float* recv, const int32_t* inv, const int64_
                              float* out, dicm_stream_t stream);
 
 /* ------------------------------------------------------------------------
+ * a16 over NVLink peer memory: the all-to-all-v exchanges of the AMS step
+ * (reference Cluster._route of EmbedRequest / EmbedResponse / IdParamPull /
+ * IdParamResponse / EmbedGradPush / IdParamPush, runtime.py:337-343,
+ * 387-422) written directly into the peers' receive
+ * buffers by copy kernels, with every count staying on the device (no host
+ * round trip per iteration).
+ * Each rank allocates one exchange region with dicm_p2p_alloc (same size and
+ * layout on every rank), shares it with dicm_ipc_handle / dicm_ipc_open, and
+ * fills dicm_peers_t.region[r] with rank r's region as mapped locally.
+ * barrier: every rank stores `epoch` (increasing) into slot [rank] of the
+ *   uint32 flag array at `flags_off` of every region (release, system scope)
+ *   and waits until its own slots all reach `epoch`; a peer that never
+ *   arrives latches status[DICM_ST_P2P_TIMEOUT] after ~10 s instead of hanging.
+ * counts: writes this rank's per-destination counts send_counts[world][2]
+ *   (column 0 images, 1 ID rows) into row [rank] of the [world][world][2]
+ *   int32 count matrix at cmat_off of every region.
+ * plan: from the local count matrix: the receive segments seg_img / seg_id
+ *   [world+1] (int64, by source), cnt_dev = {n_recv_img, n_recv_id,
+ *   n_send_img, n_send_id} and the placement table plan[2][4][world+1].
+ * scatter: dir 0 (requester -> owners): rows [send_off[d], +cnt[d]) of src go
+ *   to region[d] + dst_off at the position this rank's segment has there;
+ *   dir 1 (owner -> requesters): the rows of source s's segment (in receive
+ *   order) go back to region[s] + dst_off where s expects them.  row_bytes is
+ *   4 (keys) or 48 (12-float rows).
+ * ---------------------------------------------------------------------- */
+#define DICM_MAX_PEERS 8
+#define DICM_ST_P2P_TIMEOUT 4 /* != 0: a peer missed a barrier */
+typedef struct {
+  int32_t world, rank;
+  void* region[DICM_MAX_PEERS];
+} dicm_peers_t;
+
+int dicm_p2p_alloc(size_t bytes, void** out);
+int dicm_p2p_free(void* ptr);
+int dicm_ipc_handle(const void* ptr, void* handle /* 64 bytes */);
+int dicm_ipc_open(const void* handle, void** out);
+int dicm_ipc_close(void* ptr);
+int dicm_p2p_barrier(const dicm_peers_t* peers, int64_t flags_off, uint32_t epoch, int32_t* status,
+                     dicm_stream_t stream);
+int dicm_p2p_counts(const dicm_peers_t* peers, const int32_t* send_counts, int64_t cmat_off,
+                    dicm_stream_t stream);
+int dicm_p2p_plan(const dicm_peers_t* peers, int64_t cmat_off, int64_t* seg_img, int64_t* seg_id,
+                  int32_t* cnt_dev, int64_t* plan, dicm_stream_t stream);
+int dicm_p2p_scatter(const dicm_peers_t* peers, const int64_t* plan, int kind /* 0 img, 1 id */,
+                     int dir, const void* src, int row_bytes, int64_t dst_off, dicm_stream_t stream);
+/* dedup of keys[0..*n_dev) (n_dev on the device, n_max its bound) over
+ * [0, vocab): the owner-side dedup across sources (runtime.py:143-150) */
+int dicm_dedup_devn(const int32_t* keys, const int32_t* n_dev, int64_t n_max, int64_t vocab, void* workspace,
+                    size_t workspace_bytes, int32_t* uniq_out, int32_t* inv_out, int32_t* count_dev,
+                    int32_t tag, int32_t* status, dicm_stream_t stream);
+
+/* ------------------------------------------------------------------------
  * Timing probe (instrumentation, no reference counterpart): while enabled,
  * the library records a CUDA event pair on the launching stream around each
  * of its dominant kernels; dicm_probe_read returns the elapsed ms of the

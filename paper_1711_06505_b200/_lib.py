@@ -22,7 +22,8 @@ lib = C.CDLL(LIB_PATH)
 
 DICM_OK, DICM_ERR_CUDA, DICM_ERR_SHAPE, DICM_ERR_KEY, DICM_ERR_VALUE, DICM_ERR_FLOAT, DICM_ERR_UNSUPPORTED = range(7)
 STATUS_WORDS = 8
-ST_KEY_FLAG, ST_KEY_VALUE, ST_KEY_SEG, ST_NONFINITE = 0, 1, 2, 3
+ST_KEY_FLAG, ST_KEY_VALUE, ST_KEY_SEG, ST_NONFINITE, ST_P2P_TIMEOUT = 0, 1, 2, 3, 4
+MAX_PEERS = 8
 POOL_F32, POOL_BF16 = 0, 1
 PREC_FP32, PREC_TF32, PREC_BF16 = 0, 1, 2
 PRECISIONS = {"fp32": PREC_FP32, "tf32": PREC_TF32, "bf16": PREC_BF16}
@@ -109,6 +110,12 @@ def _sig(name, restype, *argtypes):
 S = C.c_size_t
 F = C.c_float
 ST = P  # stream
+
+
+class Peers(C.Structure):
+    _fields_ = [("world", I32), ("rank", I32), ("region", P * MAX_PEERS)]
+
+
 _sig("dicm_last_error", C.c_char_p)
 _sig("dicm_version", C.c_int)
 _sig("dicm_device_arch", C.c_int)
@@ -140,6 +147,16 @@ _sig("dicm_bucket_by_owner", C.c_int, P, P, I64, C.c_int, P, P, P, P, S, ST)
 _sig("dicm_permute_rows12", C.c_int, P, P, P, I64, C.c_int, P, ST)
 _sig("dicm_gather_rows_by_key", C.c_int, C.POINTER(TableState), C.c_int, P, P, I64, P, ST)
 _sig("dicm_owner_reduce_rows12", C.c_int, P, P, P, C.c_int, I64, P, I64, P, P, ST)
+_sig("dicm_p2p_alloc", C.c_int, S, C.POINTER(P))
+_sig("dicm_p2p_free", C.c_int, P)
+_sig("dicm_ipc_handle", C.c_int, P, P)
+_sig("dicm_ipc_open", C.c_int, P, C.POINTER(P))
+_sig("dicm_ipc_close", C.c_int, P)
+_sig("dicm_p2p_barrier", C.c_int, C.POINTER(Peers), I64, C.c_uint32, P, ST)
+_sig("dicm_p2p_counts", C.c_int, C.POINTER(Peers), P, I64, ST)
+_sig("dicm_p2p_plan", C.c_int, C.POINTER(Peers), I64, P, P, P, P, ST)
+_sig("dicm_p2p_scatter", C.c_int, C.POINTER(Peers), P, C.c_int, C.c_int, P, C.c_int, I64, ST)
+_sig("dicm_dedup_devn", C.c_int, P, P, I64, I64, P, S, P, P, P, C.c_int, P, ST)
 _sig("dicm_probe_enable", C.c_int, C.c_int)
 _sig("dicm_probe_read", C.c_int, C.c_int, C.POINTER(F), C.c_int, C.POINTER(C.c_int))
 
@@ -162,6 +179,8 @@ EXPORTED = [
     "dicm_loss_finalize", "dicm_check_finite", "dicm_adam_dense_workspace", "dicm_adam_dense", "dicm_adam_rows",
     "dicm_bucket_workspace", "dicm_bucket_by_owner", "dicm_permute_rows12", "dicm_gather_rows_by_key",
     "dicm_owner_reduce_rows12", "dicm_probe_enable", "dicm_probe_read",
+    "dicm_p2p_alloc", "dicm_p2p_free", "dicm_ipc_handle", "dicm_ipc_open", "dicm_ipc_close", "dicm_p2p_barrier",
+    "dicm_p2p_counts", "dicm_p2p_plan", "dicm_p2p_scatter", "dicm_dedup_devn",
 ]
 
 

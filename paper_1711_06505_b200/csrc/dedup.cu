@@ -24,7 +24,13 @@ struct Segs {
   int64_t inv_off[DICM_MAX_SEGS];
   int64_t start[DICM_MAX_SEGS + 1];
   int nseg;
+  const int32_t* n_dev;  // optional device-side length of a single segment
 };
+
+__device__ __forceinline__ int64_t seg_total(const Segs& s) {
+  const int64_t t = s.start[s.nseg];
+  return s.n_dev ? min(t, (int64_t)*s.n_dev) : t;
+}
 
 __device__ __forceinline__ int find_seg(const Segs& s, int64_t i) {
   int k = 0;
@@ -34,7 +40,7 @@ __device__ __forceinline__ int find_seg(const Segs& s, int64_t i) {
 
 __global__ void k_mark(const __grid_constant__ Segs segs, uint32_t* __restrict__ bitmap, int tag,
                        int32_t* __restrict__ status) {
-  const int64_t total = segs.start[segs.nseg];
+  const int64_t total = seg_total(segs);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int s = find_seg(segs, i);
@@ -178,7 +184,7 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
 
 __global__ void k_inverse(const __grid_constant__ Segs segs, const uint32_t* __restrict__ bitmap,
                           const int32_t* __restrict__ word_prefix, int32_t* __restrict__ inv) {
-  const int64_t total = segs.start[segs.nseg];
+  const int64_t total = seg_total(segs);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int s = find_seg(segs, i);
@@ -193,6 +199,9 @@ __global__ void k_inverse(const __grid_constant__ Segs segs, const uint32_t* __r
     inv[segs.inv_off[s] + j] = r;
   }
 }
+
+int run_dedup(const Segs& s, int64_t key_space, void* workspace, int32_t* uniq_out, int32_t* inv_out,
+              int32_t* count_dev, int32_t tag, int32_t* status, cudaStream_t st);
 
 int64_t padded_words(int64_t key_space) {
   const int64_t w = (key_space + 31) / 32;
@@ -230,6 +239,32 @@ int dicm_dedup(const dicm_keyseg_t* segs, int nseg, int64_t key_space, void* wor
       return fail(DICM_ERR_VALUE, "dedup: segment %d [%lld, +%lld) exceeds key space %lld", i,
                   (long long)segs[i].base, (long long)segs[i].vocab, (long long)key_space);
   }
+  return run_dedup(s, key_space, workspace, uniq_out, inv_out, count_dev, tag, status, st);
+}
+
+int dicm_dedup_devn(const int32_t* keys, const int32_t* n_dev, int64_t n_max, int64_t vocab, void* workspace,
+                    size_t workspace_bytes, int32_t* uniq_out, int32_t* inv_out, int32_t* count_dev,
+                    int32_t tag, int32_t* status, dicm_stream_t stream) {
+  using namespace dicm;
+  if (vocab < 1 || vocab > (int64_t)1 << 31) return fail(DICM_ERR_VALUE, "dedup: vocab %lld", (long long)vocab);
+  if (n_max < 0) return fail(DICM_ERR_VALUE, "dedup: n_max < 0");
+  if (workspace_bytes < dicm_dedup_workspace(vocab)) return fail(DICM_ERR_VALUE, "dedup: workspace too small");
+  Segs s{};
+  s.nseg = 1;
+  s.ids[0] = keys;
+  s.vocab[0] = vocab;
+  s.start[1] = n_max;
+  s.n_dev = n_dev;
+  return run_dedup(s, vocab, workspace, uniq_out, inv_out, count_dev, tag, status, (cudaStream_t)stream);
+}
+
+}  // extern "C"
+
+namespace {
+int run_dedup(const Segs& s, int64_t key_space, void* workspace, int32_t* uniq_out, int32_t* inv_out,
+              int32_t* count_dev, int32_t tag, int32_t* status, cudaStream_t st) {
+  using namespace dicm;
+  const int nseg = s.nseg;
   const int64_t W = padded_words(key_space);
   const int ntiles = (int)(W / kTile);
   uint32_t* bitmap = (uint32_t*)workspace;
@@ -246,5 +281,4 @@ int dicm_dedup(const dicm_keyseg_t* segs, int nseg, int64_t key_space, void* wor
     k_inverse<<<dicm_grid(total, 256, 148 * 32), 256, 0, st>>>(s, bitmap, word_prefix, inv_out);
   return last_launch("dicm_dedup");
 }
-
-}  // extern "C"
+}  // namespace

@@ -25,25 +25,47 @@ __global__ void k_block_counts(const int32_t* __restrict__ keys, const int32_t* 
   if (threadIdx.x < world) blkcnt[(int64_t)blockIdx.x * world + threadIdx.x] = c[threadIdx.x];
 }
 
-// owner-major exclusive scan over (owner, block); send_counts[o] = totals
-__global__ void k_scan_counts(int32_t* __restrict__ blkcnt, int nblk, int world, int32_t* __restrict__ send_counts) {
-  if (threadIdx.x != 0) return;
-  int run = 0;
-  for (int o = 0; o < world; ++o) {
-    int tot = 0;
-    for (int b = 0; b < nblk; ++b) {
-      const int v = blkcnt[(int64_t)b * world + o];
-      blkcnt[(int64_t)b * world + o] = run;
-      run += v;
-      tot += v;
+// per owner (block o): exclusive scan over the blocks' counts, relative to
+// the owner's segment; send_counts[o] = its total
+__global__ void __launch_bounds__(256) k_scan_counts(int32_t* __restrict__ blkcnt, int nblk, int world,
+                                                     int32_t* __restrict__ send_counts) {
+  __shared__ int wsum[8];
+  const int o = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int carry = 0;
+  for (int b0 = 0; b0 < nblk; b0 += 256) {
+    const int b = b0 + threadIdx.x;
+    const int v = b < nblk ? blkcnt[(int64_t)b * world + o] : 0;
+    int x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
     }
-    send_counts[o] = tot;
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    int before = carry;
+    for (int w = 0; w < warp; ++w) before += wsum[w];
+    int tot = 0;
+    for (int w = 0; w < 8; ++w) tot += wsum[w];
+    if (b < nblk) blkcnt[(int64_t)b * world + o] = before + x - v;
+    carry += tot;
+    __syncthreads();
   }
+  if (threadIdx.x == 0) send_counts[o] = carry;
 }
 
 __global__ void k_place(const int32_t* __restrict__ keys, const int32_t* __restrict__ count, int64_t n_max, int world,
-                        const int32_t* __restrict__ base, int32_t* __restrict__ send_keys, int32_t* __restrict__ perm) {
+                        const int32_t* __restrict__ base, const int32_t* __restrict__ send_counts,
+                        int32_t* __restrict__ send_keys, int32_t* __restrict__ perm) {
   __shared__ int warp_cnt[BLK / 32][MAXW];
+  __shared__ int owner_base[MAXW];
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int o = 0; o < world; ++o) {
+      owner_base[o] = run;
+      run += send_counts[o];
+    }
+  }
   const int64_t n = min((int64_t)*count, n_max);
   const int64_t i = (int64_t)blockIdx.x * BLK + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -60,7 +82,7 @@ __global__ void k_place(const int32_t* __restrict__ keys, const int32_t* __restr
   if (valid) {
     int before = 0;
     for (int w = 0; w < warp; ++w) before += warp_cnt[w][own];
-    const int pos = base[(int64_t)blockIdx.x * world + own] + before + rank;
+    const int pos = owner_base[own] + base[(int64_t)blockIdx.x * world + own] + before + rank;
     send_keys[pos] = key / world;
     perm[i] = pos;
   }
@@ -103,8 +125,8 @@ int dicm_bucket_by_owner(const int32_t* keys, const int32_t* count_dev, int64_t 
   }
   int32_t* blkcnt = (int32_t*)workspace;
   k_block_counts<<<nblk, BLK, 0, st>>>(keys, count_dev, n_max, world, blkcnt);
-  k_scan_counts<<<1, 32, 0, st>>>(blkcnt, nblk, world, send_counts);
-  k_place<<<nblk, BLK, 0, st>>>(keys, count_dev, n_max, world, blkcnt, send_keys, perm);
+  k_scan_counts<<<world, 256, 0, st>>>(blkcnt, nblk, world, send_counts);
+  k_place<<<nblk, BLK, 0, st>>>(keys, count_dev, n_max, world, blkcnt, send_counts, send_keys, perm);
   return last_launch("dicm_bucket_by_owner");
 }
 

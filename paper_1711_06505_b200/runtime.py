@@ -102,6 +102,109 @@ def exchange_counts(send_counts, group=None):
     return both[:w], both[w:]
 
 
+class _ExtMem:
+    """A device allocation the library owns, seen by torch through
+    __cuda_array_interface__ (no copy)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class PeerExchange:
+    """The AMS exchanges over NVLink peer memory (include/dicm_b200.h, a16 over
+    NVLink): one exchange region per rank, identical layout on every rank,
+    mapped into every peer with CUDA IPC.  Layout (byte offsets):
+
+        flags      [64] uint32            barrier epochs, slot = source rank
+        cmat       [world][world][2] i32  per-pair counts (row = source)
+        recv_img   [cap_ri] i32           keys this owner receives
+        recv_id    [cap_rk] i32
+        push_img   [cap_ri, 12] f32       embedding gradients this owner receives
+        push_id    [cap_rk, 12] f32       ID-row gradients this owner receives
+        back_img   [cap_u, 12] f32        embeddings this requester receives
+        back_id    [cap_k, 12] f32        ID rows this requester receives
+
+    Capacities are agreed once (max over ranks) when the region is built."""
+
+    def __init__(self, world, rank, cap_u, cap_k, local_rows, local_id_space, group=None):
+        dev = torch.device("cuda", torch.cuda.current_device())
+        caps = torch.tensor([cap_u, cap_k], dtype=torch.int64, device=dev)
+        dist.all_reduce(caps, op=dist.ReduceOp.MAX, group=group)
+        cap_u, cap_k = (int(x) for x in caps.cpu().tolist())
+        self.world, self.rank = world, rank
+        self.cap_u, self.cap_k = cap_u, cap_k
+        self.cap_ri = min(world * cap_u, world * max(local_rows, 1))
+        self.cap_rk = min(world * cap_k, world * max(local_id_space, 1))
+        off, layout = 0, {}
+
+        def take(name, nbytes):
+            nonlocal off
+            layout[name] = off
+            off += (int(nbytes) + 255) // 256 * 256
+
+        take("flags", 64 * 4)
+        take("cmat", world * world * 2 * 4)
+        take("recv_img", self.cap_ri * 4)
+        take("recv_id", self.cap_rk * 4)
+        take("push_img", self.cap_ri * 48)
+        take("push_id", self.cap_rk * 48)
+        take("back_img", cap_u * 48)
+        take("back_id", cap_k * 48)
+        self.off, self.bytes = layout, off
+        base = C.c_void_p()
+        L.check(L.lib.dicm_p2p_alloc(off, C.byref(base)))
+        self.base = base.value
+        h = (C.c_char * 64)()
+        L.check(L.lib.dicm_ipc_handle(self.base, h))
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(h), group=group)
+        self.peers = L.Peers()
+        self.peers.world, self.peers.rank = world, rank
+        self._opened = []
+        for r in range(world):
+            if r == rank:
+                self.peers.region[r] = self.base
+            else:
+                p = C.c_void_p()
+                L.check(L.lib.dicm_ipc_open((C.c_char * 64).from_buffer_copy(handles[r]), C.byref(p)))
+                self.peers.region[r] = p.value
+                self._opened.append(p.value)
+        self.epoch = 0
+        self.plan = torch.zeros(2 * 4 * (L.MAX_PEERS + 1), dtype=torch.int64, device=dev)
+        i32, f32 = "<i4", "<f4"
+        self.recv_img = self._view("recv_img", (self.cap_ri,), i32)
+        self.recv_id = self._view("recv_id", (self.cap_rk,), i32)
+        self.push_img = self._view("push_img", (self.cap_ri, 12), f32)
+        self.push_id = self._view("push_id", (self.cap_rk, 12), f32)
+        self.back_img = self._view("back_img", (cap_u, 12), f32)
+        self.back_id = self._view("back_id", (cap_k, 12), f32)
+        dist.barrier(group=group)
+
+    def _view(self, name, shape, typestr):
+        return torch.as_tensor(_ExtMem(self.base + self.off[name], shape, typestr), device="cuda")
+
+    def barrier(self, status, s):
+        self.epoch += 1
+        L.check(L.lib.dicm_p2p_barrier(C.byref(self.peers), self.off["flags"], self.epoch, status, s))
+
+    def counts(self, send_counts, s):
+        L.check(L.lib.dicm_p2p_counts(C.byref(self.peers), send_counts, self.off["cmat"], s))
+
+    def plan_from_counts(self, seg_img, seg_id, cnt_dev, s):
+        L.check(L.lib.dicm_p2p_plan(C.byref(self.peers), self.off["cmat"], seg_img, seg_id, cnt_dev,
+                                    self.plan.data_ptr(), s))
+
+    def scatter(self, kind, direction, src, row_bytes, dst, s):
+        L.check(L.lib.dicm_p2p_scatter(C.byref(self.peers), self.plan.data_ptr(), kind, direction, src, row_bytes,
+                                       self.off[dst], s))
+
+    def close(self):
+        for p in self._opened:
+            L.lib.dicm_ipc_close(p)
+        self._opened = []
+
+
 class ClusterEngine(StepEngine):
     """One rank of the sharded AMS step."""
 
@@ -110,6 +213,12 @@ class ClusterEngine(StepEngine):
         if pool.world != world or pool.rank != rank:
             raise ValueError(f"pool shard ({pool.world}, {pool.rank}) != rank ({world}, {rank})")
         self.world, self.rank, self.group = world, rank, group
+        import os
+        # sparse exchanges: NVLink peer-memory copies (default) or NCCL all-to-all-v
+        self.exchange = os.environ.get("DICM_EXCHANGE", "p2p")
+        if self.exchange not in ("p2p", "nccl"):
+            raise ValueError(f"DICM_EXCHANGE must be p2p or nccl, got {self.exchange!r}")
+        self.px = None
         super().__init__(model, pool, precision, lr0, lr_decay, lr_interval, id_align=world)
         dev = self.dev
         # owner-side descriptors: owner-local key = global key // world
@@ -120,6 +229,8 @@ class ClusterEngine(StepEngine):
         self.segs_img = torch.zeros(world + 1, dtype=torch.int64, device=dev)
         self.segs_id = torch.zeros(world + 1, dtype=torch.int64, device=dev)
         self._seg_host = torch.zeros(2 * (world + 1), dtype=torch.int64, pin_memory=True)
+        self._timing = os.environ.get("DICM_PHASE_TIMING") == "1"
+        self._marks = None
 
     @property
     def image_key_space(self):
@@ -141,9 +252,17 @@ class ClusterEngine(StepEngine):
         self.ws_bucket = _u8(L.lib.dicm_bucket_workspace(max(cu, ck), G), dev)
         self.rows_buf = torch.empty((max(cu, ck), 12), **f32)  # responses in / pushes out
         # owner side (worst case: every rank asks for all its keys here)
-        self.cap_ri, self.cap_rk = G * cu, G * ck
-        self.recv_img = torch.empty(self.cap_ri, **i32)
-        self.recv_id = torch.empty(self.cap_rk, **i32)
+        self._alloc_owner(G * cu, G * ck)
+        self.cnt_dev = torch.zeros(4, dtype=torch.int32, device=dev)  # n_recv_img, n_recv_id, n_send_img, n_send_id
+
+    def _alloc_owner(self, cap_ri, cap_rk):
+        dev, G = self.dev, self.world
+        i32 = dict(dtype=torch.int32, device=dev)
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.cap_ri, self.cap_rk = cap_ri, cap_rk
+        if self.exchange == "nccl":
+            self.recv_img = torch.empty(self.cap_ri, **i32)
+            self.recv_id = torch.empty(self.cap_rk, **i32)
         self.cap_o = min(self.cap_ri, self.pool.local_rows)
         self.cap_ko = min(self.cap_rk, self.local_id_space)
         self.uniq_o = torch.empty(max(self.cap_o, 1), **i32)
@@ -154,7 +273,6 @@ class ClusterEngine(StepEngine):
         self.d_rows_o = torch.empty((max(self.cap_ko, 1), 12), **f32)
         self.idx_ws = torch.empty(G * max(self.cap_o, self.cap_ko, 1), **i32)
         self.net = ImageNetBuffers(self.cap_o, self.pool.d_raw, self.prec_code, dev)
-        self.cnt_dev = torch.zeros(4, dtype=torch.int32, device=dev)  # n_recv_img, n_recv_id, n_send_img, n_send_id
 
     @property
     def emb(self):
@@ -169,8 +287,31 @@ class ClusterEngine(StepEngine):
         L.check(L.lib.dicm_dedup(seg, 1, space, ws.data_ptr(), ws.numel(), uniq.data_ptr(), inv.data_ptr(),
                                  self.counts[count_slot:].data_ptr(), 2, self.status.data_ptr(), self.s))
 
+    def _mark(self, name):
+        """Phase timing (DICM_PHASE_TIMING=1): an event on the compute stream."""
+        if self._marks is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self._marks.append((name, ev))
+
+    def phase_times(self):
+        """{phase: ms} of the last iteration (needs DICM_PHASE_TIMING=1)."""
+        if not self._marks:
+            return {}
+        torch.cuda.synchronize()
+        out, prev = {}, None
+        for name, ev in self._marks:
+            if prev is not None:
+                out[name] = out.get(name, 0.0) + prev.elapsed_time(ev)
+            prev = ev
+        return out
+
     def forward_backward(self, db, denominator=None):
+        if self.exchange == "p2p":
+            return self._forward_backward_p2p(db, denominator)
         G, s = self.world, None
+        self._marks = [] if self._timing else None
+        self._mark("start")
         self._begin(db)
         s = self.s
         denom = float(db.pk.B * G if denominator is None else denominator)
@@ -184,8 +325,10 @@ class ClusterEngine(StepEngine):
         L.check(L.lib.dicm_bucket_by_owner(self.uniq_id.data_ptr(), cnt[1:].data_ptr(), self.cap_k, G,
                                            self.send_id.data_ptr(), self._col(1), self.perm_id.data_ptr(),
                                            self.ws_bucket.data_ptr(), self.ws_bucket.numel(), s))
+        self._mark("dedup+bucket")
         pair = torch.stack([self._cnt_cols[0], self._cnt_cols[1]], dim=1)
         sent, recv = exchange_counts(pair, self.group)
+        self._mark("count exchange (host sync)")
         si, sk = sent[:, 0].tolist(), sent[:, 1].tolist()
         ri, rk = recv[:, 0].tolist(), recv[:, 1].tolist()
         nsi, nsk, nri, nrk = sum(si), sum(sk), sum(ri), sum(rk)
@@ -200,13 +343,17 @@ class ClusterEngine(StepEngine):
         self.cnt_dev.copy_(torch.tensor([nri, nrk, nsi, nsk], dtype=torch.int32), non_blocking=True)
         _a2a(self.recv_img[:nri], self.send_img[:nsi], ri, si, self.group)
         _a2a(self.recv_id[:nrk], self.send_id[:nsk], rk, sk, self.group)
+        self._mark("a2a keys")
         # (3) owner: one image-MLP forward per distinct image, ID rows
         self._dedup_owner(self.recv_img, nri, self.pool.local_rows, self.ws_img_owner, self.uniq_o, self.inv_o, 2)
+        self._mark("owner dedup")
         if self.n_img_segs:
             self._image_forward(self.net, self.uniq_o, cnt[2:].data_ptr())
+        self._mark("image MLP fwd")
         L.check(L.lib.dicm_permute_rows12(self.net.emb.data_ptr(), self.inv_o.data_ptr(), self.cnt_dev.data_ptr(),
                                           max(nri, 0), 0, self.resp.data_ptr(), s))
         _a2a(self.rows_buf[:nsi], self.resp[:nri], si, ri, self.group)
+        self._mark("a2a E rows")
         L.check(L.lib.dicm_permute_rows12(self.rows_buf.data_ptr(), self.perm_img.data_ptr(), cnt.data_ptr(),
                                           self.cap_u, 0, self.emb_l.data_ptr(), s))
         L.check(L.lib.dicm_gather_rows_by_key(self.owner_tabstate, len(self.fields), self.recv_id.data_ptr(),
@@ -214,8 +361,10 @@ class ClusterEngine(StepEngine):
         _a2a(self.rows_buf[:nsk], self.resp[:nrk], sk, rk, self.group)
         L.check(L.lib.dicm_permute_rows12(self.rows_buf.data_ptr(), self.perm_id.data_ptr(), cnt[1:].data_ptr(),
                                           self.cap_k, 0, self.id_rows.data_ptr(), s))
+        self._mark("ID rows + a2a")
         # (4) local pooling + head
         self._local_step(self.emb_l, self.d_emb_l, denom)
+        self._mark("pooling+head")
         # (5) push gradients to the owners; owners reduce in ascending source order
         L.check(L.lib.dicm_permute_rows12(self.d_emb_l.data_ptr(), self.perm_img.data_ptr(), cnt.data_ptr(),
                                           self.cap_u, 1, self.rows_buf.data_ptr(), s))
@@ -223,8 +372,10 @@ class ClusterEngine(StepEngine):
         L.check(L.lib.dicm_owner_reduce_rows12(self.resp.data_ptr(), self.inv_o.data_ptr(), self.segs_img.data_ptr(),
                                                G, max(nri, 0), cnt[2:].data_ptr(), self.cap_o, self.idx_ws.data_ptr(),
                                                self.net.d_emb.data_ptr(), s))
+        self._mark("a2a dE + owner reduce")
         # (6) owner image-MLP backward
         self._image_backward(self.net, self.uniq_o, cnt[2:].data_ptr(), self.cap_o if self.n_img_segs else 0)
+        self._mark("image MLP bwd")
         L.check(L.lib.dicm_permute_rows12(self.d_rows.data_ptr(), self.perm_id.data_ptr(), cnt[1:].data_ptr(),
                                           self.cap_k, 1, self.rows_buf.data_ptr(), s))
         _a2a(self.resp[:nrk], self.rows_buf[:nsk], rk, sk, self.group)
@@ -234,8 +385,99 @@ class ClusterEngine(StepEngine):
                                                self.idx_ws.data_ptr(), self.d_rows_o.data_ptr(), s))
         # (6) every dense gradient in one all-reduce (sum: the loss is already
         # divided by the union batch, runtime.py:374, training.py:42)
+        self._mark("ID grads a2a + reduce")
         dist.all_reduce(self.grad, group=self.group)
         dist.all_reduce(self.loss, group=self.group)
+        self._mark("allreduce")
+        return self.loss
+
+    def _forward_backward_p2p(self, db, denominator=None):
+        """The same iteration with every sparse exchange done by peer-memory
+        copy kernels and device-side counts: no host synchronisation."""
+        G = self.world
+        self._marks = [] if self._timing else None
+        self._mark("start")
+        self._begin(db)
+        s, st = self.s, self.status.data_ptr()
+        denom = float(db.pk.B * G if denominator is None else denominator)
+        if self.px is None or self.px.cap_u < self.cap_u or self.px.cap_k < self.cap_k:
+            if self.px is not None:
+                raise RuntimeError("batch outgrew the peer exchange region built at the first iteration")
+            self.px = PeerExchange(G, self.rank, self.cap_u, self.cap_k, self.pool.local_rows,
+                                   self.local_id_space, self.group)
+            self._alloc_owner(self.px.cap_ri, self.px.cap_rk)  # every owner buffer at the agreed capacity
+            self.resp_id = torch.empty((max(self.px.cap_rk, 1), 12), dtype=torch.float32, device=self.dev)
+            self.push_out_id = torch.empty((max(self.cap_k, 1), 12), dtype=torch.float32, device=self.dev)
+        px = self.px
+        self._dedup_images()
+        self._dedup_ids()
+        cnt = self.counts
+        L.check(L.lib.dicm_bucket_by_owner(self.uniq_img.data_ptr(), cnt.data_ptr(), self.cap_u, G,
+                                           self.send_img.data_ptr(), self._col(0), self.perm_img.data_ptr(),
+                                           self.ws_bucket.data_ptr(), self.ws_bucket.numel(), s))
+        L.check(L.lib.dicm_bucket_by_owner(self.uniq_id.data_ptr(), cnt[1:].data_ptr(), self.cap_k, G,
+                                           self.send_id.data_ptr(), self._col(1), self.perm_id.data_ptr(),
+                                           self.ws_bucket.data_ptr(), self.ws_bucket.numel(), s))
+        torch.stack([self._cnt_cols[0], self._cnt_cols[1]], dim=1, out=self.cnt_pair)
+        self._mark("dedup+bucket")
+        # (2) counts -> every peer, then the request keys (C1, C3)
+        px.counts(self.cnt_pair.data_ptr(), s)
+        px.barrier(st, s)
+        px.plan_from_counts(self.segs_img.data_ptr(), self.segs_id.data_ptr(), self.cnt_dev.data_ptr(), s)
+        px.scatter(0, 0, self.send_img.data_ptr(), 4, "recv_img", s)
+        px.scatter(1, 0, self.send_id.data_ptr(), 4, "recv_id", s)
+        px.barrier(st, s)
+        self._mark("counts + keys")
+        # (3) owner: dedup across sources, one image-MLP forward per distinct image, ID rows back (C2, C3)
+        L.check(L.lib.dicm_dedup_devn(px.recv_img.data_ptr(), self.cnt_dev.data_ptr(), px.cap_ri,
+                                      self.pool.local_rows, self.ws_img_owner.data_ptr(), self.ws_img_owner.numel(),
+                                      self.uniq_o.data_ptr(), self.inv_o.data_ptr(), cnt[2:].data_ptr(), 2, st, s))
+        self._mark("owner dedup")
+        if self.n_img_segs:
+            self._image_forward(self.net, self.uniq_o, cnt[2:].data_ptr())
+        self._mark("image MLP fwd")
+        L.check(L.lib.dicm_permute_rows12(self.net.emb.data_ptr(), self.inv_o.data_ptr(), self.cnt_dev.data_ptr(),
+                                          px.cap_ri, 0, self.resp.data_ptr(), s))
+        px.scatter(0, 1, self.resp.data_ptr(), 48, "back_img", s)
+        L.check(L.lib.dicm_gather_rows_by_key(self.owner_tabstate, len(self.fields), px.recv_id.data_ptr(),
+                                              self.cnt_dev[1:].data_ptr(), px.cap_rk, self.resp_id.data_ptr(), s))
+        px.scatter(1, 1, self.resp_id.data_ptr(), 48, "back_id", s)
+        px.barrier(st, s)
+        L.check(L.lib.dicm_permute_rows12(px.back_img.data_ptr(), self.perm_img.data_ptr(), cnt.data_ptr(),
+                                          self.cap_u, 0, self.emb_l.data_ptr(), s))
+        L.check(L.lib.dicm_permute_rows12(px.back_id.data_ptr(), self.perm_id.data_ptr(), cnt[1:].data_ptr(),
+                                          self.cap_k, 0, self.id_rows.data_ptr(), s))
+        self._mark("rows back")
+        # (4) local pooling + head
+        self._local_step(self.emb_l, self.d_emb_l, denom)
+        self._mark("pooling+head")
+        # (5) gradients to the owners (C4, C5); owners reduce in ascending source order
+        L.check(L.lib.dicm_permute_rows12(self.d_emb_l.data_ptr(), self.perm_img.data_ptr(), cnt.data_ptr(),
+                                          self.cap_u, 1, self.rows_buf.data_ptr(), s))
+        L.check(L.lib.dicm_permute_rows12(self.d_rows.data_ptr(), self.perm_id.data_ptr(), cnt[1:].data_ptr(),
+                                          self.cap_k, 1, self.push_out_id.data_ptr(), s))
+        px.scatter(0, 0, self.rows_buf.data_ptr(), 48, "push_img", s)
+        px.scatter(1, 0, self.push_out_id.data_ptr(), 48, "push_id", s)
+        px.barrier(st, s)
+        L.check(L.lib.dicm_owner_reduce_rows12(px.push_img.data_ptr(), self.inv_o.data_ptr(),
+                                               self.segs_img.data_ptr(), G, px.cap_ri, cnt[2:].data_ptr(),
+                                               self.cap_o, self.idx_ws.data_ptr(), self.net.d_emb.data_ptr(), s))
+        self._mark("grads to owners")
+        # (6) owner image-MLP backward; ID rows
+        self._image_backward(self.net, self.uniq_o, cnt[2:].data_ptr(), self.cap_o if self.n_img_segs else 0)
+        self._mark("image MLP bwd")
+        L.check(L.lib.dicm_dedup_devn(px.recv_id.data_ptr(), self.cnt_dev[1:].data_ptr(), px.cap_rk,
+                                      self.local_id_space, self.ws_id_owner.data_ptr(), self.ws_id_owner.numel(),
+                                      self.uniq_id_o.data_ptr(), self.inv_id_o.data_ptr(), cnt[3:].data_ptr(), 3,
+                                      st, s))
+        L.check(L.lib.dicm_owner_reduce_rows12(px.push_id.data_ptr(), self.inv_id_o.data_ptr(),
+                                               self.segs_id.data_ptr(), G, px.cap_rk, cnt[3:].data_ptr(),
+                                               self.cap_ko, self.idx_ws.data_ptr(), self.d_rows_o.data_ptr(), s))
+        self._mark("ID grads")
+        # (7) every dense gradient in one all-reduce
+        dist.all_reduce(self.grad, group=self.group)
+        dist.all_reduce(self.loss, group=self.group)
+        self._mark("allreduce")
         return self.loss
 
     def _col(self, j):
