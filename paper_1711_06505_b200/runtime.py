@@ -102,6 +102,24 @@ def exchange_counts(send_counts, group=None):
     return both[:w], both[w:]
 
 
+def p2p_plan(cmat, rank):
+    """Host restatement of the device placement plan (csrc/p2p.cu k_plan) for
+    one kind of key: cmat[s][d] = rows source s sends to owner d.  Returns
+    (send_off[d], pos_at_dest[d], recv_off[s], back_pos[s]):
+      send_off     where this rank's segment for owner d starts in its send buffer
+      pos_at_dest  where that segment lands in owner d's receive buffer
+      recv_off     where source s's segment starts in this rank's receive buffer
+      back_pos     where this rank's answers for requester s land in s's buffer
+    (= s's send offset for this rank, so answers come back in send order)."""
+    c = np.asarray(cmat, dtype=np.int64)
+    w = c.shape[0]
+    send_off = np.concatenate([[0], np.cumsum(c[rank])])
+    pos_at_dest = np.array([c[:rank, d].sum() for d in range(w)], dtype=np.int64)
+    recv_off = np.concatenate([[0], np.cumsum(c[:, rank])])
+    back_pos = np.array([c[s, :rank].sum() for s in range(w)], dtype=np.int64)
+    return send_off, pos_at_dest, recv_off, back_pos
+
+
 class _ExtMem:
     """A device allocation the library owns, seen by torch through
     __cuda_array_interface__ (no copy)."""
