@@ -75,7 +75,84 @@ __global__ void __launch_bounds__(192, 1) gather(const __grid_constant__ CUtenso
   }
 }
 
-CUtensorMap g_map;
+CUtensorMap g_map, g_pool_map;
+
+// the same k-block-by-k-block gather issued by ONE thread as TMA tile::gather4
+// (4 rows x 128 B per instruction) into a STAGES-deep ring
+template <int STAGES>
+__global__ void __launch_bounds__(64, 1) gather_tma(const __grid_constant__ CUtensorMap pm, const int* rows, int U,
+                                                   unsigned long long* sink) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[STAGES], empty[STAGES];
+  __shared__ int rid[128];
+  constexpr uint32_t SLOT = 128 * 128;
+  const uint32_t base = (smem_u32(smem) + 1023u) & ~1023u;
+  const int ntiles = (U + 127) / 128, nk = 64;
+  const int t = threadIdx.x;
+  if (t == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(smem_u32(&full[i]), 1);
+      mbar_init(smem_u32(&empty[i]), 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (t < 32) {
+    uint32_t g = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int i = t; i < 128; i += 32) {
+        const int gr = tile * 128 + i;
+        rid[i] = gr < U ? rows[gr] : 0;
+      }
+      __syncwarp();
+      if (t == 0) {
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const uint32_t s = g % STAGES, it = g / STAGES;
+          mbar_wait(smem_u32(&empty[s]), (it & 1) ^ 1);
+          mbar_arrive_expect_tx(smem_u32(&full[s]), SLOT);
+          for (int q = 0; q < 32; ++q)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes "
+                "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(base + s * SLOT + q * 512),
+                "l"(&pm), "r"(kb * 64), "r"(rid[4 * q]), "r"(rid[4 * q + 1]), "r"(rid[4 * q + 2]),
+                "r"(rid[4 * q + 3]), "r"(smem_u32(&full[s]))
+                : "memory");
+        }
+      }
+      __syncwarp();
+    }
+  } else if (t == 32) {
+    uint32_t g = 0;
+    unsigned long long acc = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const uint32_t s = g % STAGES, it = g / STAGES;
+        mbar_wait(smem_u32(&full[s]), it & 1);
+        acc += *reinterpret_cast<volatile uint32_t*>(smem + (base - smem_u32(smem)) + s * SLOT);
+        mbar_arrive(smem_u32(&empty[s]));
+      }
+    sink[blockIdx.x] = acc;
+  }
+}
+
+template <int STAGES>
+void run_tma(const int* rows, int U, unsigned long long* sink) {
+  const size_t smem = 1024 + (size_t)STAGES * 128 * 128;
+  cudaFuncSetAttribute(gather_tma<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  gather_tma<STAGES><<<148, 64, smem>>>(g_pool_map, rows, U, sink);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  const int reps = 5;
+  for (int i = 0; i < reps; ++i) gather_tma<STAGES><<<148, 64, smem>>>(g_pool_map, rows, U, sink);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("TMA gather4 128 B/row/stage, %2d stages: %7.1f GB/s  %s\n", STAGES, (double)U * 8192 * reps / (ms * 1e-3) / 1e9,
+         cudaGetErrorString(cudaGetLastError()));
+}
 
 template <int CHUNK, int STAGES, int WTMA = 0>
 void run(const uint8_t* pool, const int* rows, int U, int row_bytes, unsigned long long* sink) {
@@ -125,9 +202,21 @@ int main() {
         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
+  {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    cuuint64_t dims[2] = {4096, (cuuint64_t)P}, strides[1] = {4096 * 2};
+    cuuint32_t box[2] = {64, 1}, es[2] = {1, 1};
+    CUresult r = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn)(&g_pool_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+        pool, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    printf("pool map encode: %d\n", (int)r);
+  }
+  run_tma<6>(rows, U, sink);
+  run_tma<8>(rows, U, sink);
+  run_tma<12>(rows, U, sink);
   run<128, 6, 1>(pool, rows, U, row_bytes, sink);
-  run<128, 6, 2>(pool, rows, U, row_bytes, sink);
-  run<128, 4, 2>(pool, rows, U, row_bytes, sink);
   run<128, 6>(pool, rows, U, row_bytes, sink);
   run<128, 8>(pool, rows, U, row_bytes, sink);
   run<128, 12>(pool, rows, U, row_bytes, sink);
