@@ -296,6 +296,8 @@ int dicm_owner_reduce_rows12(const float* recv, const int32_t* inv, const int64_
  *   uint32 flag array at `flags_off` of every region (release, system scope)
  *   and waits until its own slots all reach `epoch`; a peer that never
  *   arrives latches status[DICM_ST_P2P_TIMEOUT] after ~10 s instead of hanging.
+ *   epoch 0 = the next value of a counter kept in slot 63 of the local flag
+ *   array (advanced on the device, so captured CUDA graphs replay correctly).
  * counts: writes this rank's per-destination counts send_counts[world][2]
  *   (column 0 images, 1 ID rows) into row [rank] of the [world][world][2]
  *   int32 count matrix at cmat_off of every region.

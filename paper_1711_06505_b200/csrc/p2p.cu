@@ -34,8 +34,19 @@ Peers to_dev(const dicm_peers_t* p) {
   return q;
 }
 
-__global__ void k_barrier(const __grid_constant__ Peers P, int64_t off, uint32_t epoch, int32_t* status) {
+// epoch: the barrier's sequence number.  epoch == 0 takes it from (and
+// advances) a counter at flags[63] of this rank's own region, so a captured
+// CUDA graph replays with fresh epochs; every rank calls the same sequence.
+__global__ void k_barrier(const __grid_constant__ Peers P, int64_t off, uint32_t epoch_in, int32_t* status) {
   const int t = threadIdx.x;
+  __shared__ uint32_t ep;
+  if (t == 0) {
+    uint32_t* ctr = reinterpret_cast<uint32_t*>(P.region[P.rank] + off) + 63;
+    ep = epoch_in ? epoch_in : *ctr + 1;
+    if (!epoch_in) *ctr = ep;
+  }
+  __syncthreads();
+  const uint32_t epoch = ep;
   if (t < P.world) {
     uint32_t* remote = reinterpret_cast<uint32_t*>(P.region[t] + off) + P.rank;
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(remote), "r"(epoch) : "memory");

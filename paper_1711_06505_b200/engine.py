@@ -88,6 +88,11 @@ class Packed:
     def n_id(self, fields):
         return sum(self.B if not f.multi else self.multi[f.name][1] for f in fields)
 
+    def signature(self):
+        """Everything a captured step depends on: batches with equal signatures
+        share one CUDA graph."""
+        return (self.B, self.R, self.total, tuple(sorted(self.multi.items())), tuple(sorted(self.onehot.items())))
+
 
 class DeviceBatch:
     __slots__ = ("pk", "packed")
@@ -274,6 +279,7 @@ class StepEngine:
         self.loss = torch.zeros(1, **f32)
         self._alloc_image_net(self.cap_u)
         self.cap = need
+        self._graphs, self._graph_warm = None, False  # captured steps point at the old buffers
 
     def _alloc_image_net(self, cap):
         self.net = ImageNetBuffers(cap, self.pool.d_raw, self.prec_code, self.dev)
@@ -461,10 +467,50 @@ class StepEngine:
     def step(self, batch, denominator=None):
         """Upload + full step; returns the device loss (no sync)."""
         db = self.upload(batch)
+        if self.use_graphs:
+            return self.step_graphed(db, denominator)
         loss = self.forward_backward(db, denominator)
         self.optimizer_step(self.lr())
         self.iteration += 1
         return loss
+
+    # -- CUDA graphs ---------------------------------------------------
+    use_graphs = False
+    _graphs = None
+    _graph_warm = False
+
+    def step_graphed(self, db, denominator=None):
+        """One full step (forward_backward + optimizer_step) replayed from a
+        CUDA graph captured once per (batch layout, denominator, lr): the ~50
+        library launches of a step become one graph launch.  The batch is
+        copied into the engine's own upload buffer first when it lives
+        elsewhere.  The first call for an engine runs eagerly (it sets kernel
+        attributes and builds communicators, which must not happen inside a
+        capture)."""
+        lr = self.lr()
+        if db.packed.data_ptr() != self.packed.data_ptr():
+            self.packed[:db.pk.total].copy_(db.packed[:db.pk.total], non_blocking=True)
+            db = DeviceBatch(db.pk, self.packed)
+        if not self._graph_warm:
+            self._graph_warm = True
+            loss = self.forward_backward(db, denominator)
+            self.optimizer_step(lr)
+            self.iteration += 1
+            return loss
+        if self._graphs is None:
+            self._graphs = {}
+        key = (db.pk.signature(), None if denominator is None else float(denominator), lr)
+        g = self._graphs.get(key)
+        if g is None:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.forward_backward(db, denominator)
+                self.optimizer_step(lr)
+            self._graphs[key] = g
+        g.replay()
+        self.iteration += 1
+        return self.loss
 
     def raise_status(self):
         """Sync point: raise the reference's exception for a flagged step."""

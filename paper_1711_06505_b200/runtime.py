@@ -203,8 +203,8 @@ class PeerExchange:
         return torch.as_tensor(_ExtMem(self.base + self.off[name], shape, typestr), device="cuda")
 
     def barrier(self, status, s):
-        self.epoch += 1
-        L.check(L.lib.dicm_p2p_barrier(C.byref(self.peers), self.off["flags"], self.epoch, status, s))
+        # epoch 0: the kernel advances a device-side counter (CUDA-graph safe)
+        L.check(L.lib.dicm_p2p_barrier(C.byref(self.peers), self.off["flags"], 0, status, s))
 
     def counts(self, send_counts, s):
         L.check(L.lib.dicm_p2p_counts(C.byref(self.peers), send_counts, self.off["cmat"], s))
@@ -576,12 +576,28 @@ class Cluster:
 
     def train_batch_async(self, local_batch, union_size):
         """This rank's part of an iteration on its already-sliced local batch
-        (no host sync): upload, step, optimizer; returns the device loss."""
+        (no host sync): upload, step, optimizer; returns the device loss.
+        With ``use_graphs`` the step replays a captured CUDA graph."""
         e = self.engine
-        loss = e.forward_backward(e.upload(local_batch), denominator=union_size)
+        db = e.upload(local_batch)
+        if self.use_graphs:
+            return e.step_graphed(db, denominator=union_size)
+        loss = e.forward_backward(db, denominator=union_size)
         e.optimizer_step(e.lr())
         e.iteration += 1
         return loss
+
+    @property
+    def use_graphs(self):
+        return self.engine.use_graphs
+
+    @use_graphs.setter
+    def use_graphs(self, on):
+        """CUDA-graph replay of whole steps: single GPU, or the peer-memory
+        exchange (the NCCL exchange path has a host sync per iteration)."""
+        if on and self.world > 1 and getattr(self.engine, "exchange", "p2p") != "p2p":
+            raise ValueError("CUDA graphs need the peer-memory exchange (DICM_EXCHANGE=p2p)")
+        self.engine.use_graphs = bool(on)
 
     def snapshot(self):
         """Dense params (replicated) + this rank's ID-table rows."""
