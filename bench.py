@@ -496,8 +496,16 @@ def main():
                 "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": eng.launches_per_step * args.steps,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
+    dbg = os.environ.get("DICM_EXIT_DEBUG") == "1"
+    if dbg:
+        print(f"[rank {rank}] releasing graphs", flush=True)
+    cluster.close()
     if world > 1:
+        if dbg:
+            print(f"[rank {rank}] destroy", flush=True)
         dist.destroy_process_group()
+    if dbg:
+        print(f"[rank {rank}] done", flush=True)
 
 
 if __name__ == "__main__":

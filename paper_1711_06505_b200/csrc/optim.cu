@@ -54,10 +54,15 @@ __global__ void k_dense_flags(const float* __restrict__ g, const __grid_constant
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&status[DICM_ST_NONFINITE], 2);
 }
 
+// bias corrections 1 / (1 - beta^t) = -1 / expm1(t ln beta): no cancellation
+// at small t and no FP64 (which is a slow path on this part); ln beta is
+// computed once on the host in double
+__device__ __forceinline__ float inv_one_minus_pow(float ln_beta, int t) { return -1.f / expm1f((float)t * ln_beta); }
+
 __global__ void k_dense_update(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                                float* __restrict__ v, const int32_t* __restrict__ t, const __grid_constant__ Spans s,
                                const int32_t* __restrict__ nz, const int32_t* __restrict__ status, float lr, float b1,
-                               float b2, float eps) {
+                               float b2, float eps, float ln_b1, float ln_b2) {
   if (status[DICM_ST_NONFINITE] || status[DICM_ST_KEY_FLAG]) return;
   const int64_t total = s.off[s.n];
   int cur = -1;
@@ -68,8 +73,8 @@ __global__ void k_dense_update(float* __restrict__ p, const float* __restrict__ 
     if (k != cur) {
       cur = k;
       const int tt = t[k] + 1;
-      c1 = (float)(1.0 / (1.0 - pow((double)b1, (double)tt)));
-      c2 = (float)(1.0 / (1.0 - pow((double)b2, (double)tt)));
+      c1 = inv_one_minus_pow(ln_b1, tt);
+      c2 = inv_one_minus_pow(ln_b2, tt);
     }
     const float gi = g[i];
     const float mi = b1 * m[i] + (1.f - b1) * gi;
@@ -97,7 +102,7 @@ struct Tables {
 // through dense tables
 __global__ void k_rows(const __grid_constant__ Tables tb, const int32_t* __restrict__ keys,
                        const int32_t* __restrict__ count, int64_t max_rows, const float* __restrict__ grads, float lr,
-                       float b1, float b2, float eps, const int32_t* __restrict__ status) {
+                       float b1, float b2, float eps, float ln_b1, float ln_b2, const int32_t* __restrict__ status) {
   if (status[DICM_ST_NONFINITE] || status[DICM_ST_KEY_FLAG]) return;
   const int64_t n = min((int64_t)*count, max_rows);
   const int lane = threadIdx.x & 31, part = lane % 3, slot = lane / 3;  // lanes 30, 31 idle
@@ -117,8 +122,8 @@ __global__ void k_rows(const __grid_constant__ Tables tb, const int32_t* __restr
     const dicm_table_state_t& T = tb.t[k];
     const int64_t row = key - T.base;
     const int tt = T.t[row] + 1;
-    const float c1 = (float)(1.0 / (1.0 - pow((double)b1, (double)tt)));
-    const float c2 = (float)(1.0 / (1.0 - pow((double)b2, (double)tt)));
+    const float c1 = inv_one_minus_pow(ln_b1, tt);
+    const float c2 = inv_one_minus_pow(ln_b2, tt);
     float4* pm = reinterpret_cast<float4*>(T.m + row * DICM_D) + part;
     float4* pv = reinterpret_cast<float4*>(T.v + row * DICM_D) + part;
     float4* pp = reinterpret_cast<float4*>(T.table + row * DICM_D) + part;
@@ -165,7 +170,8 @@ int dicm_adam_dense(float* param, const float* grad, float* m, float* v, int32_t
   if (rc) return rc;
   const int grid = dicm_grid(off, 256, 148 * 8);
   k_dense_flags<<<grid, 256, 0, st>>>(grad, s, nz, status);
-  k_dense_update<<<grid, 256, 0, st>>>(param, grad, m, v, t, s, nz, status, lr, beta1, beta2, eps);
+  k_dense_update<<<grid, 256, 0, st>>>(param, grad, m, v, t, s, nz, status, lr, beta1, beta2, eps,
+                                       (float)log((double)beta1), (float)log((double)beta2));
   k_dense_steps<<<1, MAXSPANS, 0, st>>>(t, nz, nspans, status);
   return last_launch("dicm_adam_dense");
 }
@@ -184,7 +190,9 @@ int dicm_adam_rows(const dicm_table_state_t* tabs, int ntab, const int32_t* uniq
       return fail(DICM_ERR_VALUE, "adam_rows: table key ranges must be ascending and disjoint");
   }
   k_rows<<<dicm_grid((max_rows + 9) / 10 * 32, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(tb, uniq_keys, count_dev, max_rows,
-                                                                              grads, lr, beta1, beta2, eps, status);
+                                                                              grads, lr, beta1, beta2, eps,
+                                                                              (float)log((double)beta1),
+                                                                              (float)log((double)beta2), status);
   return last_launch("dicm_adam_rows");
 }
 

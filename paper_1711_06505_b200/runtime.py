@@ -551,9 +551,7 @@ class Cluster:
         """-> (loss, union_unique, forwards, digests) like runtime.py:465-470."""
         local, union = self.local_slice(union_batch)
         e = self.engine
-        loss = e.forward_backward(e.upload(local), denominator=union.size)
-        e.optimizer_step(e.lr())
-        e.iteration += 1
+        loss = self.train_batch_async(local, union.size)
         value = float(loss.item())
         e.raise_status()
         if self.world > 1:
@@ -586,6 +584,21 @@ class Cluster:
         e.optimizer_step(e.lr())
         e.iteration += 1
         return loss
+
+    def close(self):
+        """Release captured CUDA graphs and the peer-memory mappings (call
+        before destroy_process_group; graphs that captured collectives and
+        live IPC mappings must not outlive the communicator)."""
+        e = self.engine
+        e.use_graphs = False
+        e._graphs = None
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+        px = getattr(e, "px", None)
+        if px is not None:
+            if self.world > 1 and dist.is_initialized():
+                dist.barrier(group=self.group)  # no peer may still be writing into our region
+            px.close()
 
     @property
     def use_graphs(self):

@@ -98,6 +98,16 @@ class LocalTrainer:
         return self.model.snapshot()
 
     @property
+    def use_graphs(self):
+        """Replay whole steps from captured CUDA graphs (one capture per batch
+        layout; see StepEngine.step_graphed)."""
+        return self.engine.use_graphs
+
+    @use_graphs.setter
+    def use_graphs(self, on):
+        self.engine.use_graphs = bool(on)
+
+    @property
     def dense_state(self):
         """name -> (m, v, t) host copies (checkpoint interop, reference
         training.py:54-56)."""

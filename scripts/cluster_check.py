@@ -48,6 +48,8 @@ def main():
     pool = ImagePool.from_latents(lat, ext, dtype=pdt, world=world, rank=rank)
     full_rows = ImagePool.from_latents(lat, ext, dtype=pdt).rows.double().cpu().numpy()
     cl = Cluster(ClusterConfig(workers=world, servers=world, batch_per_worker=bpw), model, pool, precision=precision)
+    graphs = len(sys.argv) > 3 and sys.argv[3] == "graphs"
+    cl.use_graphs = graphs  # steps 2.. replay a captured CUDA graph
     rng = np.random.default_rng(5)
     lengths = rng.integers(0, 31, world * bpw)
     unions = [synthetic_batch(rng, schema, world * bpw, lengths, P) for _ in range(iters)]
@@ -88,10 +90,11 @@ def main():
             ok &= (d.max() <= lim + 1e-6) if noise else (frac_bad <= 0.05 and d.max() <= lim + tol)
         report["worst"] = max(worst.values())
         report["worst_param"] = max(worst, key=worst.get)
-        print(json.dumps({"ok": bool(ok), "world": world, "kind": kind, "precision": precision, **report}),
-              flush=True)
+        print(json.dumps({"ok": bool(ok), "world": world, "kind": kind, "precision": precision,
+                          "graphs": graphs, **report}), flush=True)
     flag = torch.tensor([1 if ok else 0], device="cuda")
     dist.broadcast(flag, 0)
+    cl.close()
     dist.destroy_process_group()
     sys.exit(0 if flag.item() else 1)
 

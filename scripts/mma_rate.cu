@@ -57,6 +57,9 @@ __global__ void __launch_bounds__(128, 1) rate(int iters, int N, int mn, long lo
   if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
 }
 
+__device__ float g_src[65536 * 4];  // 1 MB, L2-resident fill source
+__device__ unsigned long long g_fill_bytes;
+
 // pair (cta_group::2) MMA rate; `fill` warps stream STS.128 into a spare
 // smem region meanwhile (simulated operand fills), `fill_bytes` per MMA slot
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
@@ -101,7 +104,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   } else if (threadIdx.x == 0 && rank == 1) {
     mbar_wait(smem_u32(&bar), 0);
     *stop = 1;
-  } else if (threadIdx.x >= 128 && fill) {
+  } else if (threadIdx.x >= 128 && fill == 1) {
     // 4 warps hammer a 64 KB smem region with 16-B stores until the MMAs finish
     uint4* p = reinterpret_cast<uint4*>(smem + (base - smem_u32(smem)) + 65536 + 1024);
     const uint4 v = make_uint4(1, 2, 3, 4);
@@ -110,6 +113,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 #pragma unroll 8
       for (int j = 0; j < 64; ++j) p[(i + j * 128) & 4095] = v;
     }
+  } else if (threadIdx.x >= 128 && fill >= 2) {
+    // 4 warps stream cp.async (LDGSTS) 16-B copies from an L2-resident 1 MB
+    // buffer into a 64 KB smem region: the operand-fill traffic of a GEMM
+    const uint32_t dst = base + 65536 + 1024;
+    const int i = threadIdx.x - 128;
+    int k = 0;
+    while (!*stop) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        cp_async16(dst + (((i + j * 128) & 4095) << 4), g_src + (((size_t)(k * 2048 + i + j * 128)) & 65535) * 4, 16);
+      cp_async_commit();
+      cp_async_wait<4>();
+      ++k;
+    }
+    cp_async_wait<0>();
+    if (fill == 2) atomicAdd(&g_fill_bytes, (unsigned long long)k * 16 * 16);
   }
   tc_fence_before();
   cluster_sync();
@@ -144,7 +163,7 @@ int main() {
              N, cyc / n_mma, N / 2, flops / (ms * 1e-3) / 1e12, ms, cudaGetErrorString(cudaGetLastError()));
     }
   cudaFuncSetAttribute(rate2, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
-  for (int fill = 0; fill < 2; ++fill)
+  for (int fill = 0; fill < 3; ++fill)
     for (int N : {128, 256}) {
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
@@ -163,8 +182,12 @@ int main() {
       cyc /= 74;
       const double n_mma = 4.0 * iters;
       const double flops = 2.0 * 256 * N * 16 * n_mma * 74;
-      printf("pair M256 N=%3d fill=%d: %.1f cycles/MMA, %.0f TFLOP/s  err=%s\n", N, fill, cyc / n_mma,
-             flops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+      unsigned long long fb = 0;
+      cudaMemcpyFromSymbol(&fb, g_fill_bytes, sizeof(fb));
+      unsigned long long z = 0;
+      cudaMemcpyToSymbol(g_fill_bytes, &z, sizeof(z));
+      printf("pair M256 N=%3d fill=%d: %.1f cycles/MMA, %.0f TFLOP/s, fills %.1f B/clk/SM  err=%s\n", N, fill,
+             cyc / n_mma, flops / (ms * 1e-3) / 1e12, fb / 2.0 / 148.0 / cyc, cudaGetErrorString(cudaGetLastError()));
     }
   // single-CTA with smem fill pressure for comparison
   return 0;

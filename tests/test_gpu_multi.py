@@ -11,14 +11,15 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("kind,precision", [("multiquery-attn", "fp32"), ("sum", "tf32"), ("attn", "bf16")])
-def test_cluster_matches_oracle_on_union(kind, precision):
+@pytest.mark.parametrize("kind,precision,mode", [("multiquery-attn", "fp32", "eager"), ("sum", "tf32", "eager"),
+                                                 ("attn", "bf16", "eager"), ("multiquery-attn", "fp32", "graphs")])
+def test_cluster_matches_oracle_on_union(kind, precision, mode):
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     world = 4 if n >= 4 else 2
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29531", os.path.join(ROOT, "scripts", "cluster_check.py"),
-           kind, precision]
+           kind, precision, mode]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])

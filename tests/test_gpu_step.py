@@ -225,3 +225,28 @@ def test_training_loss_decreases(kind):
     tr = LocalTrainer(model, pool, TrainConfig(lr0=0.003))
     losses = [tr.train_batch(batch) for _ in range(30)]
     assert np.mean(losses[-5:]) < np.mean(losses[:5]) - 0.05
+
+
+@pytest.mark.parametrize("kind", ["sum", "multiquery-attn"])
+def test_graphed_steps_match_eager(kind):
+    """Whole steps replayed from captured CUDA graphs (StepEngine.step_graphed)
+    follow the eager trajectory: same losses and parameters up to the last-bit
+    noise of the fp32 scatter reductions."""
+    from paper_1711_06505_b200.training import LocalTrainer, TrainConfig
+    runs = []
+    for graphs in (False, True):
+        model, pool, batch = _bench_like(kind, B=96, L=12, P=500)
+        tr = LocalTrainer(model, pool, TrainConfig(lr0=1e-4))
+        tr.engine.use_graphs = graphs
+        losses = [tr.train_batch(batch) for _ in range(4)]
+        runs.append((losses, model.snapshot(), tr))
+    (l0, s0, _), (l1, s1, tr1) = runs
+    assert tr1.engine._graphs, "no graph was captured"
+    # run-to-run noise only: the fp32 scatter reductions may sum in another
+    # order, and Adam's normalised step can flip +-lr where a gradient nearly
+    # cancels; two eager runs differ the same way
+    np.testing.assert_allclose(l1, l0, rtol=1e-4, atol=1e-6)
+    for n in s0:
+        d = np.abs(s1[n] - s0[n])
+        off = d > 1e-5 * np.abs(s0[n]) + 1e-6
+        assert (_noise(n) or off.mean() <= 1e-3) and d.max() <= 2 * 1e-4 * 4, (n, off.mean(), d.max())
