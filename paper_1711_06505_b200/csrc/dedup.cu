@@ -13,9 +13,9 @@
 
 namespace {
 
-constexpr int kScanThreads = 256;
-constexpr int kWordsPerThread = 16;
-constexpr int kTile = kScanThreads * kWordsPerThread;  // 4096 words = 131072 keys
+constexpr int kScanThreads = 128;
+constexpr int kWordsPerThread = 4;
+constexpr int kTile = kScanThreads * kWordsPerThread;  // 512 words = 16384 keys: many blocks per pass
 
 struct Segs {
   const int32_t* ids[DICM_MAX_SEGS];
@@ -116,70 +116,49 @@ __global__ void k_scan_tiles(int32_t* __restrict__ tile_sums, int ntiles, int32_
 }
 
 // word prefixes + emission of the unique keys.  Warp w of the block owns
-// words [w*512, w*512+512) of the tile, taken 32 at a time; the set bits of
-// such a 32-word chunk are emitted cooperatively: output slot j of the chunk
-// goes to lane j % 32, which finds its word by a binary search over the
-// lanes' prefix counts and its bit with __fns, so every store instruction
-// writes consecutive addresses.
+// words [w*WPW, (w+1)*WPW) of the tile, 32 at a time with one word per lane:
+// a warp scan of the popcounts places each lane's keys, which it then writes
+// in ascending bit order (at most 32 short iterations per chunk).
 __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restrict__ bitmap,
                                                        const int32_t* __restrict__ tile_off,
                                                        int32_t* __restrict__ word_prefix, int32_t* __restrict__ uniq) {
-  constexpr int WPW = kTile / (kScanThreads / 32);  // words per warp (512)
-  __shared__ uint32_t sw[kTile];
-  __shared__ int32_t sp[kTile];
+  constexpr int WPW = kTile / (kScanThreads / 32);  // words per warp
   __shared__ int32_t wtot[kScanThreads / 32];
-  __shared__ int32_t cpre[kScanThreads / 32][32];  // per-warp chunk scratch: inclusive prefix of the chunk
   const int64_t tile_base = (int64_t)blockIdx.x * kTile;
-  const uint4* p = reinterpret_cast<const uint4*>(bitmap + tile_base);
-  uint4* s4 = reinterpret_cast<uint4*>(sw);
-#pragma unroll
-  for (int q = 0; q < kWordsPerThread / 4; ++q)
-    s4[q * kScanThreads + threadIdx.x] = __ldcg(p + q * kScanThreads + threadIdx.x);
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t* mw = sw + warp * WPW;
+  const uint32_t* mw = bitmap + tile_base + warp * WPW;
+  uint32_t bits[WPW / 32];
   int c = 0;
 #pragma unroll
-  for (int q = 0; q < WPW / 32; ++q) c += __popc(mw[q * 32 + lane]);
+  for (int q = 0; q < WPW / 32; ++q) {
+    bits[q] = __ldcg(mw + q * 32 + lane);
+    c += __popc(bits[q]);
+  }
   c = __reduce_add_sync(0xffffffffu, c);
   if (lane == 0) wtot[warp] = c;
   __syncthreads();
   int run = tile_off[blockIdx.x];
   for (int w = 0; w < warp; ++w) run += wtot[w];
+#pragma unroll
   for (int q = 0; q < WPW / 32; ++q) {
-    const int wi = warp * WPW + q * 32 + lane;
-    const uint32_t bits = sw[wi];
-    const int n = __popc(bits);
+    const int n = __popc(bits[q]);
     int incl = n;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += y;
     }
-    sp[wi] = run + incl - n;
-    cpre[warp][lane] = incl;
-    __syncwarp();
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    for (int j = lane; j < total; j += 32) {
-      // the word holding slot j: first lane l with cpre[l] > j
-      int lo = 0;
-#pragma unroll
-      for (int step = 16; step >= 1; step >>= 1)
-        if (cpre[warp][lo + step - 1] <= j) lo += step;
-      const int before = lo ? cpre[warp][lo - 1] : 0;
-      const uint32_t wb = sw[warp * WPW + q * 32 + lo];
-      const int bit = __fns(wb, 0, j - before + 1);
-      uniq[run + j] = (int32_t)(((tile_base + warp * WPW + q * 32 + lo) << 5) + bit);
+    const int64_t wi = tile_base + warp * WPW + q * 32 + lane;
+    int pos = run + incl - n;
+    word_prefix[wi] = pos;
+    uint32_t b = bits[q];
+    const int32_t wkey = (int32_t)(wi << 5);
+    while (b) {
+      uniq[pos++] = wkey + (__ffs(b) - 1);
+      b &= b - 1;
     }
-    run += total;
-    __syncwarp();
+    run += __shfl_sync(0xffffffffu, incl, 31);
   }
-  __syncthreads();
-  int4* dst = reinterpret_cast<int4*>(word_prefix + tile_base);
-  const int4* src = reinterpret_cast<const int4*>(sp);
-#pragma unroll
-  for (int q = 0; q < kWordsPerThread / 4; ++q)
-    dst[q * kScanThreads + threadIdx.x] = src[q * kScanThreads + threadIdx.x];
 }
 
 __global__ void k_inverse(const __grid_constant__ Segs segs, const uint32_t* __restrict__ bitmap,
