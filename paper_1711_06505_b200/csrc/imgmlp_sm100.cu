@@ -625,18 +625,19 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
     if ((rc = make_map(&map, wsrc, bf16, 256, d_raw, 128))) return rc;
     // persistent CTA pairs: <= 74 clusters of 2 (one CTA per SM)
     const int grid = 2 * (int)std::min<int64_t>(74, (rows_max + 255) / 256);
-    static const int attr_rc =
-        check_cuda(cudaFuncSetAttribute(k_fwd2<1, 6, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem2(6, 6)), "k_fwd2 smem") |
-        check_cuda(cudaFuncSetAttribute(k_fwd2<0, 6, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem2(6, 6)), "k_fwd2 smem");
-    if (attr_rc) return attr_rc;
+    // ring depths: 6 gather slots and 6 W0 slots; deeper rings (8/5, 7/6)
+    // measured no faster (the pipeline is not bound by stage turnaround)
+    static int a66 = -1, t66 = -1;
+    auto launch = [&](auto kern, size_t bytes, int& attr) -> int {
+      if (attr < 0)
+        attr = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes),
+                          "k_fwd2 smem");
+      if (attr) return attr;
+      kern<<<grid, THREADS_F, bytes, st>>>(map, pool, d_raw, rows, count, b0, act0);
+      return 0;
+    };
     const int probe_slot = probe_begin(DICM_PROBE_IMG_FWD_L0, st);
-    if (bf16)
-      k_fwd2<1, 6, 6><<<grid, THREADS_F, smem2(6, 6), st>>>(map, pool, d_raw, rows, count, b0, act0);
-    else
-      k_fwd2<0, 6, 6><<<grid, THREADS_F, smem2(6, 6), st>>>(map, pool, d_raw, rows, count, b0, act0);
-    const int lrc = 0;
+    const int lrc = bf16 ? launch(k_fwd2<1, 6, 6>, smem2(6, 6), a66) : launch(k_fwd2<0, 6, 6>, smem2(6, 6), t66);
     probe_end(probe_slot, st);
     if (lrc) return lrc;
     return last_launch("tcgen05 layer-0 forward (CTA pairs)");
