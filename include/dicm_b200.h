@@ -210,6 +210,11 @@ int dicm_head_fwd_bwd(const float* head_in, int batch, int width, const float* l
                       float* d_head_in, float* partials, float* loss_partials,
                       dicm_stream_t stream);
 
+/* forward only (inference, reference KvPredictor.predict / predict_logits,
+ * inference.py:72-81, training.py:109-118): logits[b] for b < batch */
+int dicm_head_fwd(const float* head_in, int batch, int width, const dicm_head_params_t* p, float* logits,
+                  dicm_stream_t stream);
+
 /* partials [nblk, n] -> out[n] (deterministic, fixed order; += if accumulate) */
 int dicm_reduce_partials(const float* partials, int nblk, int64_t n, float* out, int accumulate,
                          dicm_stream_t stream);

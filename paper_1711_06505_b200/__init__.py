@@ -15,7 +15,8 @@ from .batch import Batch, encode_batch, synthetic_batch  # noqa: F401
 __all__ = ["AGGREGATOR_KINDS", "AggregatorSpec", "FeatureSchema", "FieldSpec", "ModelLayout", "default_schema",
            "image_net_widths", "init_params", "param_specs", "Batch", "encode_batch", "synthetic_batch",
            "DicmModel", "ImagePool", "FixedExtractor", "LocalTrainer", "TrainConfig", "StepEngine", "Cluster",
-           "ClusterConfig", "run_training"]
+           "ClusterConfig", "run_training", "InferenceTable", "KvPredictor", "export_inference",
+           "predict_logits"]
 
 
 def __getattr__(name):
@@ -32,6 +33,9 @@ def __getattr__(name):
     if name == "StepEngine":
         from .engine import StepEngine
         return StepEngine
+    if name in ("InferenceTable", "KvPredictor", "export_inference", "predict_logits"):
+        from . import inference
+        return getattr(inference, name)
     if name in ("Cluster", "ClusterConfig", "run_training"):
         from . import runtime
         return getattr(runtime, name)

@@ -136,6 +136,7 @@ _sig("dicm_sample_bwd", C.c_int, C.POINTER(Layout), C.POINTER(BatchView), C.POIN
 _sig("dicm_head_partial_size", I64, C.c_int)
 _sig("dicm_head_blocks", C.c_int, C.c_int)
 _sig("dicm_head_fwd_bwd", C.c_int, P, C.c_int, C.c_int, P, F, C.POINTER(HeadParams), P, P, P, P, ST)
+_sig("dicm_head_fwd", C.c_int, P, C.c_int, C.c_int, C.POINTER(HeadParams), P, ST)
 _sig("dicm_reduce_partials", C.c_int, P, C.c_int, I64, P, C.c_int, ST)
 _sig("dicm_loss_finalize", C.c_int, P, C.c_int, F, P, P, ST)
 _sig("dicm_check_finite", C.c_int, P, I64, P, C.c_int, C.c_int, P, ST)
@@ -180,7 +181,7 @@ EXPORTED = [
     "dicm_bucket_workspace", "dicm_bucket_by_owner", "dicm_permute_rows12", "dicm_gather_rows_by_key",
     "dicm_owner_reduce_rows12", "dicm_probe_enable", "dicm_probe_read",
     "dicm_p2p_alloc", "dicm_p2p_free", "dicm_ipc_handle", "dicm_ipc_open", "dicm_ipc_close", "dicm_p2p_barrier",
-    "dicm_p2p_counts", "dicm_p2p_plan", "dicm_p2p_scatter", "dicm_dedup_devn",
+    "dicm_p2p_counts", "dicm_p2p_plan", "dicm_p2p_scatter", "dicm_dedup_devn", "dicm_head_fwd",
 ]
 
 

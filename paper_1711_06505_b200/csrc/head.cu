@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
     float z = p.b2[0];
     for (int j = 0; j < H1; ++j) z = fmaf(__ldg(p.w2 + j), prelu(s.a1[j][t], __ldg(p.a1 + j)), z);
     float l = 0.f, dz = 0.f;
-    if (t < nb) {
+    if (t < nb && !labels) logits[b0 + t] = z;  // forward only (inference)
+    if (t < nb && labels) {
       const float y = labels[b0 + t];
       l = fmaxf(z, 0.f) - z * y + log1pf(expf(-fabsf(z)));
       // dz = sigmoid(z) - y evaluated like the reference (autograd.py:241-244):
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
     s.loss[t] = l;
   }
   __syncthreads();
+  if (!labels) return;  // forward only: no loss, no backward
   float* out = part + (int64_t)blockIdx.x * part_size(W);
   const int64_t o_a0 = 0, o_b0 = H0, o_w0 = 2 * H0, o_a1 = o_w0 + (int64_t)H0 * W, o_b1 = o_a1 + H1,
                 o_w1 = o_b1 + H1, o_b2 = o_w1 + (int64_t)H1 * H0, o_w2 = o_b2 + 1;
@@ -282,6 +284,20 @@ int dicm_head_fwd_bwd(const float* head_in, int batch, int width, const float* l
   k_head<<<dicm_head_blocks(batch), THREADS, smem, (cudaStream_t)stream>>>(
       head_in, batch, width, labels, inv_denominator, *p, logits, d_head_in, partials, loss_partials);
   return last_launch("dicm_head_fwd_bwd");
+}
+
+int dicm_head_fwd(const float* head_in, int batch, int width, const dicm_head_params_t* p, float* logits,
+                  dicm_stream_t stream) {
+  using namespace dicm;
+  if (width < 1 || width > MAXW) return fail(DICM_ERR_UNSUPPORTED, "head: input width %d not in [1, %d]", width, MAXW);
+  if (batch <= 0) return DICM_OK;
+  const size_t smem = sizeof(Smem);
+  static int attr = check_cuda(cudaFuncSetAttribute(k_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                               "head smem attribute");
+  if (attr) return attr;
+  k_head<<<dicm_head_blocks(batch), THREADS, smem, (cudaStream_t)stream>>>(head_in, batch, width, nullptr, 0.f, *p,
+                                                                         logits, nullptr, nullptr, nullptr);
+  return last_launch("dicm_head_fwd");
 }
 
 int dicm_loss_finalize(const float* loss_partials, int nblk, float scale, float* loss_out, int32_t* status,

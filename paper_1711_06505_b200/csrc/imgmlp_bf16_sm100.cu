@@ -652,24 +652,39 @@ __global__ void __launch_bounds__(D_THREADS, 1)
 }
 
 // gw1[j][f] = Gp + a0[f] Gn ; ga0[f] = sum_j W1[j][f] Gn[j][f] ;
-// gb0[f] = sum_j W1[j][f] (db1[j] - (1 - a0[f]) Gm[j][f])   (one thread per f, fixed order)
+// gb0[f] = sum_j W1[j][f] (db1[j] - (1 - a0[f]) Gm[j][f])
+// block = 32 features x 8 j-groups of 8; the 8 partial sums of a feature are
+// combined in a fixed order (deterministic)
 __global__ void __launch_bounds__(256) k_l1_finish(const float* __restrict__ G, const float* __restrict__ w1,
                                                    const float* __restrict__ al0, const float* __restrict__ db1,
                                                    float* __restrict__ gw1, float* __restrict__ ga0,
                                                    float* __restrict__ gb0) {
-  const int f = threadIdx.x;
+  __shared__ float ra[8][33], rb[8][33];
+  const int fl = threadIdx.x & 31, jg = threadIdx.x >> 5, f = blockIdx.x * 32 + fl;
   const float a = al0[f];
   float sa = 0.f, sb = 0.f;
-#pragma unroll 16
-  for (int j = 0; j < 64; ++j) {
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    const int j = jg * 8 + jj;
     const float gp = G[j * 256 + f], gn = G[16384 + j * 256 + f], gm = G[32768 + j * 256 + f];
     const float w = w1[j * 256 + f];
     gw1[j * 256 + f] = gp + a * gn;
     sa = fmaf(w, gn, sa);
     sb = fmaf(w, db1[j] - (1.f - a) * gm, sb);
   }
-  ga0[f] = sa;
-  gb0[f] = sb;
+  ra[jg][fl] = sa;
+  rb[jg][fl] = sb;
+  __syncthreads();
+  if (jg == 0) {
+    float ta = 0.f, tb = 0.f;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      ta += ra[g][fl];
+      tb += rb[g][fl];
+    }
+    ga0[f] = ta;
+    gb0[f] = tb;
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn3() {
@@ -760,7 +775,7 @@ int bwd_layers12_bf16(const float* demb, const bf16* act1, const bf16* act0, con
 
 int l1_finish_bf16(const float* G, const float* w1, const float* al0, const float* db1, float* gw1, float* ga0,
                    float* gb0, cudaStream_t st) {
-  k_l1_finish<<<1, 256, 0, st>>>(G, w1, al0, db1, gw1, ga0, gb0);
+  k_l1_finish<<<8, 256, 0, st>>>(G, w1, al0, db1, gw1, ga0, gb0);
   return last_launch("layer-1 backward finish");
 }
 

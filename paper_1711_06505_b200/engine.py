@@ -390,13 +390,10 @@ class StepEngine:
                                               self.counts[1:].data_ptr(), self.cap_k, self.id_rows.data_ptr(),
                                               self.s))
 
-    def _local_step(self, emb, d_emb, denom):
-        """a6-a12 forward and backward on the local batch: pooling, head, BCE.
-        Reads image embeddings ``emb`` and compact ID rows ``self.id_rows``;
-        writes ``d_emb`` / ``self.d_rows`` and the head/attention gradients."""
-        lay, pk, s = self.model.layout, self.pk, self.s
+    def _batch_view(self, emb):
+        """Device pointers of the current batch for the per-sample kernels."""
+        lay, pk = self.model.layout, self.pk
         B, R = pk.B, pk.R
-        st = self.status.data_ptr()
         bv = L.BatchView()
         bv.batch, bv.refs = B, R
         for i, f in enumerate(self.fields):
@@ -412,6 +409,16 @@ class StepEngine:
         bv.beh_local = self.inv_img.data_ptr() + 4 * (B if lay.use_ad_image else 0)
         bv.beh_off = self._dptr(pk.beh_off)
         bv.emb = emb.data_ptr()
+        return bv
+
+    def _local_step(self, emb, d_emb, denom):
+        """a6-a12 forward and backward on the local batch: pooling, head, BCE.
+        Reads image embeddings ``emb`` and compact ID rows ``self.id_rows``;
+        writes ``d_emb`` / ``self.d_rows`` and the head/attention gradients."""
+        pk, s = self.pk, self.s
+        B = pk.B
+        st = self.status.data_ptr()
+        bv = self._batch_view(emb)
         L.check(L.lib.dicm_sample_fwd(C.byref(self.layout), C.byref(bv), self.attn, self.head_in.data_ptr(),
                                       self.scores.data_ptr(), self.stats.data_ptr(), s))
         L.check(L.lib.dicm_head_fwd_bwd(self.head_in.data_ptr(), B, self.width, self._dptr(pk.labels),
@@ -463,6 +470,64 @@ class StepEngine:
 
     def lr(self):
         return lr_schedule(self.iteration, self.lr0, self.lr_decay, self.lr_interval)
+
+    # -- forward only (inference: reference KvPredictor, predict_logits) ---
+    def _infer_net(self, cap):
+        net = getattr(self, "_inet", None)
+        if net is None or net.cap < cap:
+            net = self._inet = ImageNetBuffers(cap, self.pool.d_raw, self.prec_code, self.dev)
+        return net
+
+    def embed_rows(self, rows, n, out, chunk=1 << 19):
+        """out[i] = image-net embedding of pool row rows[i] for i < n (rows:
+        device int32; out: device [>= n, 12] fp32), in chunks through the
+        training forward kernels (reference model.embed_images,
+        model.py:355-356)."""
+        if n <= 0:
+            return
+        net = self._infer_net(min(chunk, n))
+        cnt = torch.empty(1, dtype=torch.int32, device=self.dev)
+        s = L.stream_handle()
+        for s0 in range(0, n, net.cap):
+            m = min(net.cap, n - s0)
+            cnt.fill_(m)
+            L.check(L.lib.dicm_imgmlp_fwd(self.pool.rows.data_ptr(), self.pool.dtype_code, self.pool.d_raw,
+                                          rows.data_ptr() + 4 * s0, cnt.data_ptr(), net.cap, C.byref(self.img_p),
+                                          net.act0.data_ptr(), net.act1.data_ptr(), out.data_ptr() + 48 * s0,
+                                          self.prec_code, net.ws.data_ptr(), net.ws.numel(), s))
+
+    def forward_logits(self, db, table=None):
+        """Logits of one uploaded batch (no loss, no gradients).  Image
+        embeddings come from the live image net, or -- with ``table`` (a device
+        [T, 12] fp32 tensor of exported embeddings, row = image id) -- from the
+        table for ids < T and the live net for the cold ids >= T (reference
+        KvPredictor._embedding_matrix, inference.py:61-70)."""
+        self._begin(db)
+        self._dedup_images()
+        self._dedup_ids()
+        U = int(self.counts[0].item()) if self.n_img_segs else 0
+        if U:
+            if table is None:
+                self.embed_rows(self.uniq_img, U, self.net.emb)
+            else:
+                T = int(table.shape[0])
+                k = int(torch.searchsorted(self.uniq_img[:U], torch.tensor([T], dtype=torch.int32,
+                                                                             device=self.dev)).item())
+                if k:
+                    ts = (L.TableState * 1)()
+                    ts[0].table, ts[0].base, ts[0].vocab = table.data_ptr(), 0, T
+                    cnt = torch.tensor([k], dtype=torch.int32, device=self.dev)
+                    L.check(L.lib.dicm_gather_rows_by_key(ts, 1, self.uniq_img.data_ptr(), cnt.data_ptr(), k,
+                                                          self.net.emb.data_ptr(), self.s))
+                if k < U:  # cold path: ids beyond the table
+                    self.embed_rows(self.uniq_img[k:U], U - k, self.net.emb[k:U])
+        self._gather_id_rows()
+        bv = self._batch_view(self.net.emb)
+        L.check(L.lib.dicm_sample_fwd(C.byref(self.layout), C.byref(bv), self.attn, self.head_in.data_ptr(),
+                                      self.scores.data_ptr(), self.stats.data_ptr(), self.s))
+        L.check(L.lib.dicm_head_fwd(self.head_in.data_ptr(), self.pk.B, self.width, C.byref(self.head_p),
+                                    self.logits.data_ptr(), self.s))
+        return self.logits[:self.pk.B]
 
     def step(self, batch, denominator=None):
         """Upload + full step; returns the device loss (no sync)."""
