@@ -173,12 +173,20 @@ typedef struct {
   const int32_t* beh_local;     /* [R] inverse of the behavior images into emb */
   const int32_t* beh_off;       /* [B+1] */
   const float* emb;             /* [U,12] image embeddings */
+  const float* keyproj;         /* attentive: [channels][kp_stride][32] from dicm_attn_keyproj */
+  int64_t kp_stride;            /* rows per channel in keyproj (>= U) */
 } dicm_batch_view_t;
 
 typedef struct {
   const float *w0, *b0, *a0, *w1, *b1; /* attn/<ch>/0/{w,b,a}, attn/<ch>/1/{w,b} */
 } dicm_attn_params_t;
 
+/* key projections of the attention nets, once per unique image (the key half
+ * of W0 [q || k], model.py:208-210, restructured W0 [q||k] = Wq q + Wk k):
+ * keyproj[ch][u][j] = Wk_ch[j] . emb[u] for u < *count_dev (channel 1 only for
+ * multiquery-attn); no-op for sum pooling */
+int dicm_attn_keyproj(const dicm_layout_t* layout, const dicm_attn_params_t* attn, const float* emb,
+                      const int32_t* count_dev, int64_t u_cap, float* keyproj, dicm_stream_t stream);
 /* number of float partial slots one block writes (attention grads, both channels) */
 int64_t dicm_attn_partial_size(const dicm_layout_t* layout);
 int dicm_sample_blocks(int batch);

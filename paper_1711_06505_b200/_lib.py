@@ -81,7 +81,8 @@ class Layout(C.Structure):
 
 class BatchView(C.Structure):
     _fields_ = [("batch", I32), ("refs", I64), ("field_ids", P * 8), ("field_off", P * 8), ("tables", P * 8),
-                ("field_inv", P * 8), ("ad_local", P), ("beh_local", P), ("beh_off", P), ("emb", P)]
+                ("field_inv", P * 8), ("ad_local", P), ("beh_local", P), ("beh_off", P), ("emb", P),
+                ("keyproj", P), ("kp_stride", I64)]
 
 
 class AttnParams(C.Structure):
@@ -129,6 +130,7 @@ _sig("dicm_imgmlp_fwd", C.c_int, P, C.c_int, C.c_int, P, P, I64, C.POINTER(ImgMl
 _sig("dicm_imgmlp_bwd", C.c_int, P, C.c_int, C.c_int, P, P, I64, C.POINTER(ImgMlpParams), P, P, P,
      C.POINTER(ImgMlpGrads), C.c_int, P, S, ST)
 _sig("dicm_attn_partial_size", I64, C.POINTER(Layout))
+_sig("dicm_attn_keyproj", C.c_int, C.POINTER(Layout), C.POINTER(AttnParams), P, P, I64, P, ST)
 _sig("dicm_sample_blocks", C.c_int, C.c_int)
 _sig("dicm_sample_fwd", C.c_int, C.POINTER(Layout), C.POINTER(BatchView), C.POINTER(AttnParams), P, P, P, ST)
 _sig("dicm_sample_bwd", C.c_int, C.POINTER(Layout), C.POINTER(BatchView), C.POINTER(AttnParams), P, P, P, P,
@@ -182,6 +184,7 @@ EXPORTED = [
     "dicm_owner_reduce_rows12", "dicm_probe_enable", "dicm_probe_read",
     "dicm_p2p_alloc", "dicm_p2p_free", "dicm_ipc_handle", "dicm_ipc_open", "dicm_ipc_close", "dicm_p2p_barrier",
     "dicm_p2p_counts", "dicm_p2p_plan", "dicm_p2p_scatter", "dicm_dedup_devn", "dicm_head_fwd",
+    "dicm_attn_keyproj",
 ]
 
 

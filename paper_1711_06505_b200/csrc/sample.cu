@@ -164,6 +164,47 @@ __device__ __forceinline__ float query_proj(const AttnSmem& s, const float (&q)[
   return p;
 }
 
+// the key half of the attention net's first layer, once per unique image:
+// kp[u][j] = Wk[j] . E[u]  (warp per image, lane = hidden unit)
+__global__ void __launch_bounds__(256) k_keyproj(const float* __restrict__ w0, int dq, const float* __restrict__ emb,
+                                                 const int32_t* __restrict__ count, int64_t u_cap,
+                                                 float* __restrict__ kp) {
+  const int lane = threadIdx.x & 31;
+  float wk[DICM_D];
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) wk[c] = __ldg(w0 + lane * (dq + DICM_D) + dq + c);
+  const int64_t n = min((int64_t)*count, u_cap);
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < n; u += warps) {
+    const Row12 e = load_row12(emb + u * DICM_D);
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) acc = fmaf(wk[c], e.v[c], acc);
+    kp[u * DICM_ATT + lane] = acc;
+  }
+}
+
+// score of one reference from its precomputed key projection kp[0..31]
+__device__ __forceinline__ float attn_score_kp(const AttnSmem& s, const float* P, const float4 (&kp)[8]) {
+  float sc = s.b1;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float k4[4] = {kp[q].x, kp[q].y, kp[q].z, kp[q].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = 4 * q + e;
+      sc = fmaf(s.w1[j], prelu(P[j] + k4[e], s.a0[j]), sc);
+    }
+  }
+  return sc;
+}
+
+__device__ __forceinline__ void load_kp(const float* p, float4 (&kp)[8]) {
+  const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) kp[i] = __ldg(q + i);
+}
+
 __device__ __forceinline__ float attn_score(const AttnSmem& s, const float* P, const Row12& k) {
   float sc = s.b1;
 #pragma unroll 8
@@ -195,13 +236,16 @@ __device__ void attn_fwd(const Args& a, const AttnSmem& s, int ch, int b, int la
 #pragma unroll
   for (int c = 0; c < DICM_D; ++c) acc[c] = 0.f;
   const bool norm = a.L.normalize != 0;
-  // the next reference's row is in flight while this one is scored
-  Row12 kn;
-  if (i0 + lane < i1) kn = load_row12(a.V.emb + (int64_t)__ldg(a.V.beh_local + i0 + lane) * DICM_D);
+  // the next reference's rows are in flight while this one is scored
+  const float* kpb = a.V.keyproj + (int64_t)ch * a.V.kp_stride * DICM_ATT;
+  int32_t un = i0 + lane < i1 ? __ldg(a.V.beh_local + i0 + lane) : 0;
   for (int64_t i = i0 + lane; i < i1; i += 32) {
-    const Row12 k = kn;
-    if (i + 32 < i1) kn = load_row12(a.V.emb + (int64_t)__ldg(a.V.beh_local + i + 32) * DICM_D);
-    const float sc = attn_score(s, P, k);
+    const int32_t u = un;
+    if (i + 32 < i1) un = __ldg(a.V.beh_local + i + 32);
+    float4 kp[8];
+    load_kp(kpb + (int64_t)u * DICM_ATT, kp);
+    const Row12 k = load_row12(a.V.emb + (int64_t)u * DICM_D);
+    const float sc = attn_score_kp(s, P, kp);
     a.scores[(int64_t)ch * a.V.refs + i] = sc;
     if (norm) {
       const float mn = fmaxf(m, sc);
@@ -240,7 +284,7 @@ __device__ void attn_fwd(const Args& a, const AttnSmem& s, int ch, int b, int la
     if (lane == c) dst[c] = out[c];
 }
 
-__global__ void __launch_bounds__(FWD_WARPS * 32, 3) k_sample_fwd(const __grid_constant__ Args a) {
+__global__ void __launch_bounds__(FWD_WARPS * 32, 2) k_sample_fwd(const __grid_constant__ Args a) {
   __shared__ AttnSmem sa[2];
   __shared__ float Pw[FWD_WARPS][DICM_ATT];  // per-warp query projection
   const bool att = a.L.use_behavior_images && a.L.kind != 0;
@@ -302,8 +346,9 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, 3) k_sample_fwd(const __grid_c
 struct __align__(16) WarpScratch {
   float ds[32];
   float ks[32][DICM_D];
-  float dp[32][DICM_ATT + 1];
-  float wq[32][MAXQ + 1];  // lane j's dWq accumulators (kept out of registers)
+  float dp[32][DICM_ATT + 4];  // the chunk's key projections, overwritten by dpre (row = reference);
+                               // stride 36: 16-B rows for cp.async, conflict-free column reads
+  float wq[32][MAXQ + 1];      // lane j's dWq accumulators (kept out of registers)
 };
 
 __host__ __device__ constexpr int chan_part(int dq) { return 3 * DICM_ATT + 1 + DICM_ATT * (dq + DICM_D); }
@@ -328,10 +373,8 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
     load_query<DQ>(a, ch, b, q);
     Pj = query_proj<DQ>(s, q, lane);
   }
-  float wkj[DICM_D];
-#pragma unroll
-  for (int c = 0; c < DICM_D; ++c) wkj[c] = s.wk[lane][c];
   const float w1j = s.w1[lane], a0j = s.a0[lane];
+  const float* kpb = a.V.keyproj + (int64_t)ch * a.V.kp_stride * DICM_ATT;
   float dout[DICM_D];
   const float* dsrc = a.d_head_in + (int64_t)b * a.L.width + a.L.pool_col + ch * DICM_D;
 #pragma unroll
@@ -387,6 +430,16 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
     Row12 k = k_n;
     const int32_t row = row_n;
     const float sci = sc_n;
+    {  // this chunk's key projections -> shared memory, asynchronously
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ws.dp[lane]);
+      const float* src = kpb + (int64_t)row * DICM_ATT;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + 16 * q), "l"(src + 4 * q),
+                     "r"(valid ? 16 : 0)
+                     : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     if (i + 32 < i1) {
       row_n = __ldg(a.V.beh_local + i + 32);
       k_n = load_row12(a.V.emb + (int64_t)row_n * DICM_D);
@@ -407,13 +460,12 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
 #pragma unroll
     for (int c = 0; c < DICM_D; ++c) ws.ks[lane][c] = k.v[c];
     acc.b1 += ds;
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
     // lane j: hidden unit j across the chunk's references
     const int nr = (int)min((int64_t)32, i1 - c0);
     for (int r = 0; r < nr; ++r) {
-      float pre = Pj;
-#pragma unroll
-      for (int c = 0; c < DICM_D; ++c) pre = fmaf(wkj[c], ws.ks[r][c], pre);
+      const float pre = Pj + ws.dp[r][lane];  // read before dpre replaces it below
       const float dsr = ws.ds[r];
       const float dh = dsr * w1j;
       const bool pos = pre > 0.f;
@@ -431,11 +483,13 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
       float dk[DICM_D];
 #pragma unroll
       for (int c = 0; c < DICM_D; ++c) dk[c] = w * dout[c];
-#pragma unroll 4
-      for (int j = 0; j < DICM_ATT; ++j) {
-        const float d = ws.dp[lane][j];
+      for (int q = 0; q < DICM_ATT / 4; ++q) {  // 16-B reads: conflict-free at stride 36
+        const float4 d4 = reinterpret_cast<const float4*>(ws.dp[lane])[q];
+        const float dq4[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
-        for (int c = 0; c < DICM_D; ++c) dk[c] = fmaf(s.wk[j][c], d, dk[c]);
+        for (int e = 0; e < 4; ++e)
+#pragma unroll
+          for (int c = 0; c < DICM_D; ++c) dk[c] = fmaf(s.wk[4 * q + e][c], dq4[e], dk[c]);
       }
       red_row12(a.d_emb + (int64_t)row * DICM_D, dk);
     }
@@ -588,6 +642,8 @@ int validate(const dicm_layout_t* L, const dicm_batch_view_t* V) {
       if (L->query_field[f] < 0 || L->query_field[f] >= L->n_fields || L->field_multi[L->query_field[f]])
         return fail(DICM_ERR_UNSUPPORTED, "multiquery-attn: query fields must be one-hot fields");
   if (V->batch < 0) return fail(DICM_ERR_VALUE, "sample: negative batch");
+  if (L->kind != 0 && L->use_behavior_images && !V->keyproj)
+    return fail(DICM_ERR_VALUE, "attentive pooling needs the key projections (dicm_attn_keyproj)");
   return DICM_OK;
 }
 
@@ -609,6 +665,19 @@ extern "C" {
 int64_t dicm_attn_partial_size(const dicm_layout_t* layout) { return part_size(layout); }
 
 int dicm_sample_blocks(int batch) { return bwd_grid(batch); }
+
+int dicm_attn_keyproj(const dicm_layout_t* layout, const dicm_attn_params_t* attn, const float* emb,
+                      const int32_t* count_dev, int64_t u_cap, float* keyproj, dicm_stream_t stream) {
+  using namespace dicm;
+  if (layout->kind == 0 || !layout->use_behavior_images || u_cap <= 0) return DICM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int grid = dicm_grid(u_cap * 32, 256, 148 * 8);
+  k_keyproj<<<grid, 256, 0, st>>>(attn[0].w0, DICM_D, emb, count_dev, u_cap, keyproj);
+  if (layout->kind == 2)
+    k_keyproj<<<grid, 256, 0, st>>>(attn[1].w0, DICM_D * layout->n_query, emb, count_dev, u_cap,
+                                    keyproj + u_cap * DICM_ATT);
+  return last_launch("dicm_attn_keyproj");
+}
 
 int dicm_sample_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const dicm_attn_params_t* attn,
                     float* head_in, float* scores, float* stats, dicm_stream_t stream) {

@@ -277,6 +277,9 @@ class StepEngine:
         self.loss_part = torch.empty(L.lib.dicm_head_blocks(max(B, 1)), **f32)
         self.attn_partial = torch.empty((L.lib.dicm_sample_blocks(max(B, 1)), max(self.attn_part, 1)), **f32)
         self.loss = torch.zeros(1, **f32)
+        lay = self.model.layout
+        nch = (2 if lay.multiquery else 1) if (lay.attentive and lay.use_behavior_images) else 0
+        self.keyproj = torch.empty((max(nch, 1), max(self.cap_u, 1) if nch else 1, 32), **f32)
         self._alloc_image_net(self.cap_u)
         self.cap = need
         self._graphs, self._graph_warm = None, False  # captured steps point at the old buffers
@@ -409,6 +412,12 @@ class StepEngine:
         bv.beh_local = self.inv_img.data_ptr() + 4 * (B if lay.use_ad_image else 0)
         bv.beh_off = self._dptr(pk.beh_off)
         bv.emb = emb.data_ptr()
+        bv.keyproj = self.keyproj.data_ptr()
+        bv.kp_stride = self.keyproj.shape[1]
+        # key projections of the attention nets, once per unique image
+        L.check(L.lib.dicm_attn_keyproj(C.byref(self.layout), self.attn, emb.data_ptr(), self.counts.data_ptr(),
+                                        self.keyproj.shape[1] if self.keyproj.shape[1] > 1 else 0,
+                                        self.keyproj.data_ptr(), self.s))
         return bv
 
     def _local_step(self, emb, d_emb, denom):
