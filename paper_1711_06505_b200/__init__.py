@@ -16,7 +16,7 @@ __all__ = ["AGGREGATOR_KINDS", "AggregatorSpec", "FeatureSchema", "FieldSpec", "
            "image_net_widths", "init_params", "param_specs", "Batch", "encode_batch", "synthetic_batch",
            "DicmModel", "ImagePool", "FixedExtractor", "LocalTrainer", "TrainConfig", "StepEngine", "Cluster",
            "ClusterConfig", "run_training", "InferenceTable", "KvPredictor", "export_inference",
-           "predict_logits"]
+           "predict_logits", "checkpoint"]
 
 
 def __getattr__(name):

@@ -119,6 +119,37 @@ class LocalTrainer:
                                    m.dense_view(e.v, n).double().cpu().numpy(), int(t[e.span_index[n]]))
         return out
 
+    def set_adam_state(self, name, m=None, v=None, t=None):
+        """Write Adam state of one parameter into the device buffers
+        (checkpoint restore, reference checkpoint.py:228-243)."""
+        import torch
+        e, mdl = self.engine, self.model
+        if name.startswith("id_emb/"):
+            f = name.split("/", 1)[1]
+            if m is not None:
+                e.tm[f].copy_(torch.as_tensor(np.asarray(m), dtype=torch.float32))
+            if v is not None:
+                e.tv[f].copy_(torch.as_tensor(np.asarray(v), dtype=torch.float32))
+            if t is not None:
+                e.tt[f].copy_(torch.as_tensor(np.asarray(t), dtype=torch.int32))
+            return
+        if m is not None:
+            mdl.dense_view(e.m, name).copy_(torch.as_tensor(np.asarray(m), dtype=torch.float32))
+        if v is not None:
+            mdl.dense_view(e.v, name).copy_(torch.as_tensor(np.asarray(v), dtype=torch.float32))
+        if t is not None:
+            e.t[e.span_index[name]] = int(np.asarray(t))
+
+    def reset_adam_state(self, name):
+        """Fresh optimizer state for a re-initialised parameter."""
+        if name.startswith("id_emb/"):
+            f = name.split("/", 1)[1]
+            self.set_adam_state(name, m=np.zeros(self.engine.tm[f].shape), v=np.zeros(self.engine.tv[f].shape),
+                                t=np.zeros(self.engine.tt[f].shape, dtype=np.int64))
+        else:
+            shp = tuple(self.model.params[name].shape)
+            self.set_adam_state(name, m=np.zeros(shp), v=np.zeros(shp), t=0)
+
     @property
     def table_state(self):
         e = self.engine

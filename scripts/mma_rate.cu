@@ -9,7 +9,9 @@
 using namespace dicm::tc;
 
 // smem: A 128 rows x 64 k (16 KB), B 256 rows x 64 k (32 KB), bf16 SW128
-__global__ void __launch_bounds__(128, 1) rate(int iters, int N, int mn, long long* cycles) {
+__device__ float g_src1[65536 * 4];
+__device__ unsigned long long g_fill1;
+__global__ void __launch_bounds__(256, 1) rate(int iters, int N, int mn, long long* cycles, int fill) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
@@ -30,6 +32,24 @@ __global__ void __launch_bounds__(128, 1) rate(int iters, int N, int mn, long lo
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = slot;
+  volatile int* stop1 = reinterpret_cast<volatile int*>(smem + (base - smem_u32(smem)) + 49152);
+  if (threadIdx.x == 0) *stop1 = 0;
+  __syncthreads();
+  if (threadIdx.x >= 128 && fill) {
+    const uint32_t dst = base + 49152 + 1024;
+    const int i = threadIdx.x - 128;
+    int k = 0;
+    while (!*stop1) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        cp_async16(dst + (((i + j * 128) & 4095) << 4), g_src1 + (((size_t)(k * 2048 + i + j * 128)) & 65535) * 4, 16);
+      cp_async_commit();
+      cp_async_wait<4>();
+      ++k;
+    }
+    cp_async_wait<0>();
+    atomicAdd(&g_fill1, (unsigned long long)k * 16 * 16);
+  }
   if (threadIdx.x == 0) {
     const uint32_t idesc = instr_desc(1, 128, N, mn, mn);
     const long long t0 = clock64();
@@ -51,6 +71,7 @@ __global__ void __launch_bounds__(128, 1) rate(int iters, int N, int mn, long lo
     mbar_wait(smem_u32(&bar), 0);
     const long long t1 = clock64();
     cycles[blockIdx.x] = t1 - t0;
+    *stop1 = 1;
   }
   tc_fence_before();
   __syncthreads();
@@ -138,16 +159,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 int main() {
   long long* d;
   cudaMalloc(&d, 148 * sizeof(long long));
-  cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
   const int iters = 20000;
+  for (int fill = 0; fill < 2; ++fill)
   for (int mn = 0; mn < 2; ++mn)
-    for (int N : {64, 128, 256}) {
+    for (int N : {256}) {
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
-      rate<<<148, 128, 64 * 1024>>>(100, N, mn, d);
+      rate<<<148, 256, 128 * 1024>>>(100, N, mn, d, fill);
+      unsigned long long z1 = 0;
+      cudaMemcpyToSymbol(g_fill1, &z1, sizeof(z1));
       cudaEventRecord(e0);
-      rate<<<148, 128, 64 * 1024>>>(iters, N, mn, d);
+      rate<<<148, 256, 128 * 1024>>>(iters, N, mn, d, fill);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
@@ -159,8 +183,11 @@ int main() {
       cyc /= 148;
       const double n_mma = 4.0 * iters;
       const double flops = 2.0 * 128 * N * 16 * n_mma * 148;
-      printf("%s N=%3d: %.1f cycles/MMA (floor %d), %.0f TFLOP/s (%.3f ms) err=%s\n", mn ? "MN-major" : "K-major ",
-             N, cyc / n_mma, N / 2, flops / (ms * 1e-3) / 1e12, ms, cudaGetErrorString(cudaGetLastError()));
+      unsigned long long fb1 = 0;
+      cudaMemcpyFromSymbol(&fb1, g_fill1, sizeof(fb1));
+      printf("%s N=%3d fill=%d: %.1f cycles/MMA (floor %d), %.0f TFLOP/s (%.3f ms), fills %.1f B/clk/SM err=%s\n",
+             mn ? "MN-major" : "K-major ", N, fill, cyc / n_mma, N / 2, flops / (ms * 1e-3) / 1e12, ms,
+             fb1 / 148.0 / cyc, cudaGetErrorString(cudaGetLastError()));
     }
   cudaFuncSetAttribute(rate2, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
   for (int fill = 0; fill < 3; ++fill)

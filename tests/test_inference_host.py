@@ -47,3 +47,37 @@ def test_lookup_beyond_table_raises():
     with pytest.raises(KeyError, match="exported table"):
         table.lookup([-1])
     assert table.lookup([0, 4]).shape == (2, 12)
+
+
+def test_checkpoint_host_format(tmp_path):
+    """DCK1 writer/reader on host arrays (duck-typed model), checksum and
+    mask validation (reference tests/test_checkpoint.py:36-44, 122-129)."""
+    from paper_1711_06505_b200.checkpoint import CheckpointError, WarmupMask, load, save
+
+    class P:
+        def __init__(self, a):
+            self.data = a
+
+    class M:
+        params = {"img/0/w": P(np.arange(6.0).reshape(2, 3)), "id_emb/user": P(np.ones((3, 12))),
+                  "mlp/2/b": P(np.zeros(1))}
+
+    path = tmp_path / "c.ckpt"
+    save(path, M(), optimizer={"mlp/2/b#t": np.array(4, dtype=np.int64)}, meta={"k": 1})
+    ck = load(path)
+    assert ck.meta == {"k": "1"}
+    assert set(ck.groups) == {"image-embedding-model", "id-embeddings", "mlp"}
+    assert np.array_equal(ck.tensors()["img/0/w"], M.params["img/0/w"].data)
+    assert ck.tensors()["mlp/2/b#t"] == 4
+    raw = bytearray(path.read_bytes())
+    raw[-1] ^= 0xFF
+    path.write_bytes(bytes(raw))
+    with pytest.raises(CheckpointError, match="checksum"):
+        load(path)
+    with pytest.raises(CheckpointError, match="unknown parameter group"):
+        WarmupMask({"bogus": "restore"})
+    with pytest.raises(CheckpointError, match="bad warm-up flag"):
+        WarmupMask({"mlp": "maybe"})
+    with pytest.raises(CheckpointError, match="unknown warm-up strategy"):
+        WarmupMask.named("half")
+    assert WarmupMask.named("partial").flags["id-embeddings"] == "reinitialize"
