@@ -5,7 +5,10 @@ NVFLAGS ?= -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xptxas -v --expt-r
 SRC_DIR := paper_1711_06505_b200/csrc
 OBJ_DIR := build/obj
 SRCS := $(wildcard $(SRC_DIR)/*.cu)
-OBJS := $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(SRCS))
+CPPS := $(wildcard $(SRC_DIR)/*.cpp)
+OBJS := $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(SRCS)) $(patsubst $(SRC_DIR)/%.cpp,$(OBJ_DIR)/%.cpp.o,$(CPPS))
+CXX ?= g++
+CXXFLAGS ?= -O3 -std=c++17 -fPIC -pthread -Wall
 HDRS := $(wildcard $(SRC_DIR)/*.cuh) include/dicm_b200.h
 LIB := paper_1711_06505_b200/libdicm_b200.so
 
@@ -15,8 +18,12 @@ $(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
 	@mkdir -p $(OBJ_DIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJ_DIR)/$*.ptxas.log || (cat $(OBJ_DIR)/$*.ptxas.log; false)
 
+$(OBJ_DIR)/%.cpp.o: $(SRC_DIR)/%.cpp include/dicm_b200.h
+	@mkdir -p $(OBJ_DIR)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
 $(LIB): $(OBJS)
-	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS)
+	$(NVCC) $(ARCH) -shared -cudart static -Xcompiler -pthread -o $@ $(OBJS)
 
 clean:
 	rm -rf build $(LIB)

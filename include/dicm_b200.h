@@ -350,6 +350,28 @@ int dicm_dedup_devn(const int32_t* keys, const int32_t* n_dev, int64_t n_max, in
                     int32_t tag, int32_t* status, dicm_stream_t stream);
 
 /* ------------------------------------------------------------------------
+ * Host input pipeline (reference data.py:293-311 read_samples + encode_batch
+ * model.py:158-198): JSONL sample records parsed natively on `nthreads`
+ * threads (0 = all cores) into columns.  Keys are the JSON field names; a
+ * list key keeps the most recent b_max entries of each record.  parse
+ * returns a handle (NULL on a malformed record: *bad_line = its 1-based line
+ * and dicm_last_error() says why); export copies column `key` out: int32
+ * values (+ CSR offsets [n+1] for list keys), or float32 labels for "label".
+ * Host-only: needs no GPU.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_keys;
+  const char* keys[16];
+  int32_t key_is_list[16];
+  int32_t b_max;
+} dicm_jsonl_spec_t;
+void* dicm_jsonl_parse(const char* buf, int64_t len, const dicm_jsonl_spec_t* spec, int nthreads,
+                       int64_t* n_records, int64_t* bad_line);
+int64_t dicm_jsonl_list_total(void* handle, int key);
+int dicm_jsonl_export(void* handle, int key, int32_t* values, int32_t* offsets, float* labels);
+void dicm_jsonl_free(void* handle);
+
+/* ------------------------------------------------------------------------
  * Timing probe (instrumentation, no reference counterpart): while enabled,
  * the library records a CUDA event pair on the launching stream around each
  * of its dominant kernels; dicm_probe_read returns the elapsed ms of the

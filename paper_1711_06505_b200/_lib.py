@@ -113,6 +113,10 @@ F = C.c_float
 ST = P  # stream
 
 
+class JsonlSpec(C.Structure):
+    _fields_ = [("n_keys", I32), ("keys", C.c_char_p * 16), ("key_is_list", I32 * 16), ("b_max", I32)]
+
+
 class Peers(C.Structure):
     _fields_ = [("world", I32), ("rank", I32), ("region", P * MAX_PEERS)]
 
@@ -160,6 +164,10 @@ _sig("dicm_p2p_counts", C.c_int, C.POINTER(Peers), P, I64, ST)
 _sig("dicm_p2p_plan", C.c_int, C.POINTER(Peers), I64, P, P, P, P, ST)
 _sig("dicm_p2p_scatter", C.c_int, C.POINTER(Peers), P, C.c_int, C.c_int, P, C.c_int, I64, ST)
 _sig("dicm_dedup_devn", C.c_int, P, P, I64, I64, P, S, P, P, P, C.c_int, P, ST)
+_sig("dicm_jsonl_parse", P, C.c_char_p, I64, C.POINTER(JsonlSpec), C.c_int, C.POINTER(I64), C.POINTER(I64))
+_sig("dicm_jsonl_list_total", I64, P, C.c_int)
+_sig("dicm_jsonl_export", C.c_int, P, C.c_int, P, P, P)
+_sig("dicm_jsonl_free", None, P)
 _sig("dicm_probe_enable", C.c_int, C.c_int)
 _sig("dicm_probe_read", C.c_int, C.c_int, C.POINTER(F), C.c_int, C.POINTER(C.c_int))
 
@@ -184,7 +192,7 @@ EXPORTED = [
     "dicm_owner_reduce_rows12", "dicm_probe_enable", "dicm_probe_read",
     "dicm_p2p_alloc", "dicm_p2p_free", "dicm_ipc_handle", "dicm_ipc_open", "dicm_ipc_close", "dicm_p2p_barrier",
     "dicm_p2p_counts", "dicm_p2p_plan", "dicm_p2p_scatter", "dicm_dedup_devn", "dicm_head_fwd",
-    "dicm_attn_keyproj",
+    "dicm_attn_keyproj", "dicm_jsonl_parse", "dicm_jsonl_list_total", "dicm_jsonl_export", "dicm_jsonl_free",
 ]
 
 

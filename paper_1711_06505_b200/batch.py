@@ -53,6 +53,23 @@ class Batch:
             parts.append(self.beh_image_ids)
         return np.unique(np.concatenate(parts).astype(np.int64)) if parts else np.zeros(0, np.int64)
 
+    def take(self, idx):
+        """Samples ``idx`` (any order) as a new batch: the vectorised CSR
+        gather behind shuffled minibatches (reference data.py:284-290)."""
+        idx = np.asarray(idx, dtype=np.int64)
+
+        def gather(flat, off):
+            lens = (off[1:] - off[:-1])[idx]
+            o = np.zeros(len(idx) + 1, dtype=np.int32)
+            np.cumsum(lens, out=o[1:])
+            starts = np.repeat(off[:-1][idx].astype(np.int64) - o[:-1], lens)
+            return flat[starts + np.arange(int(o[-1]))], o
+
+        mh = {f: gather(fl, of) for f, (fl, of) in self.multihot.items()}
+        beh, boff = gather(self.beh_image_ids, self.beh_off)
+        return Batch(len(idx), self.labels[idx], {f: v[idx] for f, v in self.onehot.items()}, mh,
+                     self.ad_image_ids[idx], beh, boff, dict(self.meta))
+
     def slice(self, start, stop):
         """Samples [start, stop) as a new batch (the contiguous per-worker split
         of reference runtime.py:379-382)."""
@@ -107,6 +124,75 @@ def encode_batch(samples, model):
         beh_image_ids=beh,
         beh_off=beh_off,
     )
+
+
+def read_jsonl(path, schema, nthreads=0):
+    """All samples of a JSONL file (reference data.py:293-311) as one Batch,
+    parsed by the native reader (csrc/host_io.cpp) straight into CSR columns
+    -- no per-sample Python objects.  Same result as
+    ``encode_batch(read_samples(path), model)``; a malformed record raises
+    ``ValueError`` naming its line, like the reference."""
+    import ctypes as C
+    from . import _lib as L
+    keys, is_list = [], []
+    for f in schema.fields:
+        keys.append(f.name)
+        is_list.append(bool(f.multi))
+    for k, lst in (("ad_image", False), ("behavior_images", True), ("label", False)):
+        if k not in keys:
+            keys.append(k)
+            is_list.append(lst)
+    spec = L.JsonlSpec()
+    spec.n_keys = len(keys)
+    enc = [k.encode() for k in keys]
+    for i, k in enumerate(enc):
+        spec.keys[i] = k
+        spec.key_is_list[i] = int(is_list[i])
+    spec.b_max = int(schema.b_max)
+    with open(path, "rb") as fh:
+        raw = fh.read()
+    n, bad = C.c_int64(0), C.c_int64(-1)
+    h = L.lib.dicm_jsonl_parse(raw, len(raw), C.byref(spec), int(nthreads), C.byref(n), C.byref(bad))
+    if not h:
+        raise ValueError(f"{path}:{bad.value}: {L.lib.dicm_last_error().decode()}")
+    try:
+        n = n.value
+        cols = {}
+        for i, k in enumerate(keys):
+            if k == "label":
+                lab = np.empty(n, dtype=np.float32)
+                L.check(L.lib.dicm_jsonl_export(h, i, None, None, lab.ctypes.data))
+                cols[k] = lab
+            elif is_list[i]:
+                vals = np.empty(L.lib.dicm_jsonl_list_total(h, i), dtype=np.int32)
+                off = np.empty(n + 1, dtype=np.int32)
+                L.check(L.lib.dicm_jsonl_export(h, i, vals.ctypes.data, off.ctypes.data, None))
+                cols[k] = (vals, off)
+            else:
+                vals = np.empty(n, dtype=np.int32)
+                L.check(L.lib.dicm_jsonl_export(h, i, vals.ctypes.data, None, None))
+                cols[k] = vals
+    finally:
+        L.lib.dicm_jsonl_free(h)
+    onehot = {f.name: cols[f.name] for f in schema.fields if not f.multi}
+    multihot = {f.name: cols[f.name] for f in schema.fields if f.multi}
+    beh, beh_off = cols["behavior_images"]
+    return Batch(n, cols["label"], onehot, multihot, cols["ad_image"], beh, beh_off)
+
+
+def minibatch_order(n, seed, epoch=0):
+    """The reference's deterministic shuffle (data.py:284-290)."""
+    return np.random.default_rng([int(seed) & 0xFFFFFFFF, epoch]).permutation(n)
+
+
+def iter_minibatches(batch, batch_size, seed, epoch=0):
+    """Shuffled minibatches of a columnar Batch in the reference's order
+    (data.py:284-290: the final short batch is emitted)."""
+    if batch_size < 1:
+        raise ValueError("batch_size must be >= 1")
+    order = minibatch_order(batch.size, seed, epoch)
+    for start in range(0, batch.size, batch_size):
+        yield batch.take(order[start:start + batch_size])
 
 
 def zipf_keys(rng, n, pool, s=1.1, perm_seed=0):

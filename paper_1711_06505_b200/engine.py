@@ -101,6 +101,66 @@ class DeviceBatch:
         self.pk, self.packed = pk, packed
 
 
+class Prefetcher:
+    """Host input pipeline: while step i runs, a worker
+    thread assembles batch i+1 on the host (the columnar take + packing into
+    pinned memory) and its H2D copy runs on a side stream; the compute stream
+    waits for that copy only when it reaches the batch.  Device buffers rotate
+    through a ring whose slots are reused only after the step that read them
+    has passed (an event on the compute stream)."""
+
+    def __init__(self, engine, batches, depth=2):
+        import queue
+        import threading
+        self.e, self.depth = engine, max(1, int(depth))
+        self.copy_stream = torch.cuda.Stream(device=engine.dev)
+        self.q = queue.Queue(maxsize=self.depth)
+        self.ring = [None] * (self.depth + 2)
+        self.freed = [None] * (self.depth + 2)
+        self._err = None
+
+        def work():
+            try:
+                for b in batches:
+                    pk = Packed(engine.model, b)
+                    host = torch.empty(max(pk.total, 1), dtype=torch.int32, pin_memory=True)
+                    pk.fill(engine.model, b, host.numpy())
+                    self.q.put((b, pk, host))
+            except BaseException as ex:  # surfaced in the consumer
+                self._err = ex
+            self.q.put(None)
+
+        self.t = threading.Thread(target=work, daemon=True)
+        self.t.start()
+
+    def __iter__(self):
+        i = 0
+        while True:
+            item = self.q.get()
+            if item is None:
+                if self._err is not None:
+                    raise self._err
+                return
+            b, pk, host = item
+            self.e._ensure(pk)
+            slot = i % len(self.ring)
+            buf = self.ring[slot]
+            if buf is None or buf.numel() < pk.total:
+                buf = self.ring[slot] = torch.empty(max(pk.total, 1), dtype=torch.int32, device=self.e.dev)
+            with torch.cuda.stream(self.copy_stream):
+                if self.freed[slot] is not None:
+                    self.copy_stream.wait_event(self.freed[slot])  # the step that read this slot is done
+                buf[:pk.total].copy_(host[:pk.total], non_blocking=True)
+                ready = torch.cuda.Event()
+                ready.record(self.copy_stream)
+            torch.cuda.current_stream().wait_event(ready)
+            yield b, DeviceBatch(pk, buf)
+            done = torch.cuda.Event()
+            done.record(torch.cuda.current_stream())
+            self.freed[slot] = done
+            i += 1
+
+
 class ImageNetBuffers:
     """Activations + workspace of one image-MLP pass over up to ``cap`` rows."""
 
@@ -537,6 +597,15 @@ class StepEngine:
         L.check(L.lib.dicm_head_fwd(self.head_in.data_ptr(), self.pk.B, self.width, C.byref(self.head_p),
                                     self.logits.data_ptr(), self.s))
         return self.logits[:self.pk.B]
+
+    def step_device(self, db, denominator=None):
+        """Full step on an already-uploaded batch; returns the device loss."""
+        if self.use_graphs:
+            return self.step_graphed(db, denominator)
+        loss = self.forward_backward(db, denominator)
+        self.optimizer_step(self.lr())
+        self.iteration += 1
+        return loss
 
     def step(self, batch, denominator=None):
         """Upload + full step; returns the device loss (no sync)."""

@@ -94,6 +94,31 @@ class LocalTrainer:
                     return log
         return log
 
+    def run_file(self, path, log=None, prefetch=2, nthreads=0):
+        """Train on a JSONL sample file (reference data.py:293-311 format) with
+        the native reader and the prefetching input pipeline: same batches, in
+        the same order, as ``run(read_samples(path))``."""
+        from .batch import iter_minibatches, read_jsonl
+        from .engine import Prefetcher
+        data = read_jsonl(path, self.model.schema, nthreads)
+        log = log or TrainLog()
+        stop = self.cfg.max_iterations or None
+        e = self.engine
+        for epoch in range(self.cfg.epochs):
+            for b, db in Prefetcher(e, iter_minibatches(data, self.cfg.batch_size, self.cfg.seed, epoch), prefetch):
+                log.lrs.append(self.lr())
+                loss = e.step_device(db)
+                value = float(loss.item())
+                try:
+                    e.raise_status()
+                except Exception:
+                    e.iteration -= 1
+                    raise
+                log.losses.append(value)
+                if stop and self.iteration >= stop:
+                    return log
+        return log
+
     def snapshot(self):
         return self.model.snapshot()
 
