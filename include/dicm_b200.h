@@ -147,7 +147,7 @@ int dicm_imgmlp_bwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
  *   attention-parameter gradients are written as per-block partial sums.
  * ---------------------------------------------------------------------- */
 typedef struct {
-  int32_t kind;                 /* 0 sum, 1 attn, 2 multiquery-attn */
+  int32_t kind;                 /* 0 sum, 1 attn, 2 multiquery-attn, 3 max (segment_max, autograd.py:289-319) */
   int32_t normalize;            /* softmax over scores (model.py:211-214) */
   int32_t use_ad_image;
   int32_t use_behavior_images;

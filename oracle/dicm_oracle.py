@@ -72,6 +72,27 @@ def segment_sum(x, seg, n):
     return out
 
 
+def segment_max(x, seg, n):
+    """Per-segment elementwise max, empty segments -> 0, first argmax per
+    column (reference autograd.py:289-319)."""
+    x = np.asarray(x, dtype=np.float64)
+    R, d = x.shape
+    out = np.zeros((n, d))
+    arg = np.full((n, d), -1, dtype=np.int64)
+    filled = np.zeros(n, dtype=bool)
+    for r in range(R):
+        s_ = seg[r]
+        if not filled[s_]:
+            out[s_] = x[r]
+            arg[s_] = r
+            filled[s_] = True
+        else:
+            better = x[r] > out[s_]
+            out[s_] = np.where(better, x[r], out[s_])
+            arg[s_] = np.where(better, r, arg[s_])
+    return out, arg
+
+
 def segment_softmax(s, seg, n):
     """autograd.py:322-332."""
     hi = np.full(n, -np.inf)
@@ -256,6 +277,9 @@ def forward_backward(p, cfg, batch, pool, denominator=None, want_grads=True):
         kind = cfg["kind"]
         if kind == "sum":
             pooled = segment_sum(K, beh_seg, B)
+        elif kind == "max":
+            pooled, argmax = segment_max(K, beh_seg, B)
+            agg_cache = (argmax,)
         elif kind == "attn":
             pooled, c1 = attention_fwd(p, "attn/img/", ad_vec, K, beh_seg, B, cfg["normalize"])
             agg_cache = (c1,)
@@ -311,6 +335,13 @@ def forward_backward(p, cfg, batch, pool, denominator=None, want_grads=True):
         kind = cfg["kind"]
         if kind == "sum":
             dK = dpool[beh_seg]
+        elif kind == "max":                          # segment_max bwd (autograd.py:307-315)
+            dK = np.zeros_like(K)
+            argmax = agg_cache[0]
+            for s_ in range(B):
+                for c in range(K.shape[1]):
+                    if argmax[s_, c] >= 0:
+                        dK[argmax[s_, c], c] += dpool[s_, c]
         elif kind == "attn":
             dQ, dK = attention_bwd(p, "attn/img/", K, beh_seg, B, cfg["normalize"], agg_cache[0],
                                    dpool, grads)

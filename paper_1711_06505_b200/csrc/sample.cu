@@ -22,6 +22,7 @@
 //
 // Every per-reference loop keeps several independent row loads in flight per
 // lane (the index -> row gather chain is L2-latency bound otherwise).
+#include <climits>
 #include <math.h>
 
 #include "common.cuh"
@@ -217,6 +218,40 @@ __device__ __forceinline__ float attn_score(const AttnSmem& s, const float* P, c
   return sc;
 }
 
+// per-column max over a sample's behaviors and its FIRST argmax (the reference
+// keeps the earliest row on ties); every lane ends with the warp result;
+// am[c] = -1 for an empty segment
+__device__ __forceinline__ void seg_max(const Args& a, int b, int lane, float (&m)[DICM_D], int (&am)[DICM_D]) {
+  const int64_t i0 = a.V.beh_off[b], i1 = a.V.beh_off[b + 1];
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) {
+    m[c] = -INFINITY;
+    am[c] = INT_MAX;
+  }
+  for (int64_t i = i0 + lane; i < i1; i += 32) {
+    const Row12 r = load_row12(a.V.emb + (int64_t)__ldg(a.V.beh_local + i) * DICM_D);
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c)
+      if (r.v[c] > m[c] || am[c] == INT_MAX) {  // first row of this lane, or strictly larger
+        m[c] = r.v[c];
+        am[c] = (int)(i - i0);
+      }
+  }
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float mo = __shfl_xor_sync(FULL, m[c], o);
+      const int ao = __shfl_xor_sync(FULL, am[c], o);
+      if (ao != INT_MAX && (am[c] == INT_MAX || mo > m[c] || (mo == m[c] && ao < am[c]))) {
+        m[c] = mo;
+        am[c] = ao;
+      }
+    }
+    if (am[c] == INT_MAX) am[c] = -1;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------
@@ -287,7 +322,7 @@ __device__ void attn_fwd(const Args& a, const AttnSmem& s, int ch, int b, int la
 __global__ void __launch_bounds__(FWD_WARPS * 32, 2) k_sample_fwd(const __grid_constant__ Args a) {
   __shared__ AttnSmem sa[2];
   __shared__ float Pw[FWD_WARPS][DICM_ATT];  // per-warp query projection
-  const bool att = a.L.use_behavior_images && a.L.kind != 0;
+  const bool att = a.L.use_behavior_images && (a.L.kind == 1 || a.L.kind == 2);
   if (att) {
     load_attn(sa[0], a.A[0], DICM_D);
     if (a.L.kind == 2) load_attn(sa[1], a.A[1], DICM_D * a.L.n_query);
@@ -317,6 +352,15 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, 2) k_sample_fwd(const __grid_c
     if (a.L.use_ad_image && lane < DICM_D)
       row[a.L.ad_col + lane] = __ldg(a.V.emb + (int64_t)a.V.ad_local[b] * DICM_D + lane);
     if (!a.L.use_behavior_images) continue;
+    if (a.L.kind == 3) {  // max pooling (reference segment_max, autograd.py:289-319)
+      float m[DICM_D];
+      int am[DICM_D];
+      seg_max(a, b, lane, m, am);
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c)
+        if (lane == c) row[a.L.pool_col + c] = am[c] < 0 ? 0.f : m[c];  // empty segment -> 0
+      continue;
+    }
     if (a.L.kind == 0) {
       float acc[DICM_D];
 #pragma unroll
@@ -603,6 +647,16 @@ __global__ void __launch_bounds__(BWD_WARPS * 32, 4) k_sample_scatter(const __gr
       load12(drow + a.L.pool_col, dv);
       seg_scatter(a.V.beh_local, a.V.beh_off[b], a.V.beh_off[b + 1], a.d_emb, dv, lane);
     }
+    if (a.L.use_behavior_images && a.L.kind == 3) {  // gradient to the first argmax row of each column
+      float m[DICM_D];
+      int am[DICM_D];
+      seg_max(a, b, lane, m, am);
+      const int64_t i0 = a.V.beh_off[b];
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c)
+        if (lane == c && am[c] >= 0)
+          atomicAdd(a.d_emb + (int64_t)__ldg(a.V.beh_local + i0 + am[c]) * DICM_D + c, __ldg(drow + a.L.pool_col + c));
+    }
   }
 }
 
@@ -624,7 +678,7 @@ size_t bwd_smem() {
 }
 
 int64_t part_size(const dicm_layout_t* L) {
-  if (!L->use_behavior_images || L->kind == 0) return 0;
+  if (!L->use_behavior_images || L->kind == 0 || L->kind == 3) return 0;
   int64_t n = chan_part(DICM_D);
   if (L->kind == 2) n += chan_part(DICM_D * L->n_query);
   return n;
@@ -632,8 +686,8 @@ int64_t part_size(const dicm_layout_t* L) {
 
 int validate(const dicm_layout_t* L, const dicm_batch_view_t* V) {
   if (L->n_fields < 0 || L->n_fields > DICM_MAX_FIELDS) return fail(DICM_ERR_VALUE, "sample: %d fields (max 8)", L->n_fields);
-  if (L->kind < 0 || L->kind > 2) return fail(DICM_ERR_UNSUPPORTED, "sample: aggregator kind %d", L->kind);
-  if (L->kind != 0 && L->use_behavior_images && !L->use_ad_image)
+  if (L->kind < 0 || L->kind > 3) return fail(DICM_ERR_UNSUPPORTED, "sample: aggregator kind %d", L->kind);
+  if ((L->kind == 1 || L->kind == 2) && L->use_behavior_images && !L->use_ad_image)
     return fail(DICM_ERR_VALUE, "attentive aggregator needs the ad image as query");
   if (L->kind == 2 && (L->n_query < 1 || L->n_query > 2))
     return fail(DICM_ERR_VALUE, "multiquery-attn needs 1 or 2 one-hot query fields");
@@ -642,7 +696,7 @@ int validate(const dicm_layout_t* L, const dicm_batch_view_t* V) {
       if (L->query_field[f] < 0 || L->query_field[f] >= L->n_fields || L->field_multi[L->query_field[f]])
         return fail(DICM_ERR_UNSUPPORTED, "multiquery-attn: query fields must be one-hot fields");
   if (V->batch < 0) return fail(DICM_ERR_VALUE, "sample: negative batch");
-  if (L->kind != 0 && L->use_behavior_images && !V->keyproj)
+  if ((L->kind == 1 || L->kind == 2) && L->use_behavior_images && !V->keyproj)
     return fail(DICM_ERR_VALUE, "attentive pooling needs the key projections (dicm_attn_keyproj)");
   return DICM_OK;
 }
@@ -669,7 +723,7 @@ int dicm_sample_blocks(int batch) { return bwd_grid(batch); }
 int dicm_attn_keyproj(const dicm_layout_t* layout, const dicm_attn_params_t* attn, const float* emb,
                       const int32_t* count_dev, int64_t u_cap, float* keyproj, dicm_stream_t stream) {
   using namespace dicm;
-  if (layout->kind == 0 || !layout->use_behavior_images || u_cap <= 0) return DICM_OK;
+  if (!(layout->kind == 1 || layout->kind == 2) || !layout->use_behavior_images || u_cap <= 0) return DICM_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = dicm_grid(u_cap * 32, 256, 148 * 8);
   k_keyproj<<<grid, 256, 0, st>>>(attn[0].w0, DICM_D, emb, count_dev, u_cap, keyproj);
@@ -720,7 +774,7 @@ int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
   {
     const int probe_slot = probe_begin(DICM_PROBE_SAMPLE_BWD, st);
     k_sample_scatter<<<grid, BWD_WARPS * 32, 0, st>>>(a);
-    if (layout->use_behavior_images && layout->kind != 0) {
+    if (layout->use_behavior_images && (layout->kind == 1 || layout->kind == 2)) {
       // partial row layout in sorted names: attn/id/* before attn/img/*
       int64_t img_off = 0;
       if (layout->kind == 2) {

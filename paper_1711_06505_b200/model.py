@@ -23,7 +23,7 @@ import torch
 from . import schema as S
 from .schema import AggregatorSpec, FeatureSchema, FieldSpec, ModelLayout  # noqa: F401
 
-KIND_CODE = {"sum": 0, "attn": 1, "multiquery-attn": 2}
+KIND_CODE = {"sum": 0, "attn": 1, "multiquery-attn": 2, "max": 3}
 
 
 class Parameter:

@@ -13,8 +13,8 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 BIG = 50_000
 PROBE_SEED = 1234
 
-TINY = ["tiny_sum", "tiny_attn", "tiny_multiquery-attn"]
-FULL = ["full_sum", "full_attn", "full_attn_raw", "full_mq", "full_sum_noad"]
+TINY = ["tiny_sum", "tiny_attn", "tiny_multiquery-attn", "tiny_max"]
+FULL = ["full_sum", "full_attn", "full_attn_raw", "full_mq", "full_sum_noad", "full_max"]
 
 
 def load(name):

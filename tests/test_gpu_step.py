@@ -143,7 +143,7 @@ def _bench_like(kind, B=256, L=50, P=3000, vocab=20_000, seed=0, lengths=None, z
     return model, pool, batch
 
 
-@pytest.mark.parametrize("kind", ["sum", "attn", "multiquery-attn"])
+@pytest.mark.parametrize("kind", ["sum", "attn", "multiquery-attn", "max"])
 def test_bench_shape_step_matches_oracle(kind):
     """cfg-1-like shapes (B=256, L=50, 4096-d pool) against the oracle."""
     from paper_1711_06505_b200.engine import StepEngine
