@@ -223,6 +223,37 @@ int dicm_head_fwd_bwd(const float* head_in, int batch, int width, const float* l
 int dicm_head_fwd(const float* head_in, int batch, int width, const dicm_head_params_t* p, float* logits,
                   dicm_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * Two-tower pre-rank scoring (reference PrerankModel, model.py:420-531;
+ * replaces tower_reps + logits_graph, model.py:508-526): per sample, each
+ * tower maps its input (12-wide blocks of the head input, in the reference's
+ * hstack order) through PReLU(x W0^T + b0) W1^T + b1, the score is the
+ * row-wise inner product of the two representations (autograd.py:388-398),
+ * then BCE as in the head.  d_head_in = dLoss/dx for the head-input layout
+ * (columns outside both towers are zero).  Tower weight gradients go to one
+ * partial row per block at the offsets given (the fused dense buffer's sorted
+ * order), reduced by dicm_reduce_partials.
+ * ---------------------------------------------------------------------- */
+#define DICM_TOWER_MAX_PARTS 10
+#define DICM_TOWER_MAX_HIDDEN 128
+#define DICM_TOWER_MAX_REP 64
+typedef struct {
+  const float *w0, *b0, *a0; /* [hidden][n_in], [hidden], [hidden] */
+  const float *w1, *b1;      /* [rep][hidden], [rep] */
+  int32_t n_parts;           /* input blocks, each 12 wide: n_in = 12 * n_parts */
+  int32_t part_col[DICM_TOWER_MAX_PARTS]; /* head-input column of each block */
+  int64_t g_w0, g_b0, g_a0, g_w1, g_b1;   /* gradient offsets inside one partial row */
+} dicm_tower_t;
+
+int dicm_towers_blocks(int batch);
+/* towers[0] = user tower, towers[1] = ad tower; part_stride = partial row length */
+int dicm_towers_fwd_bwd(const float* head_in, int batch, int width, const dicm_tower_t* towers, int hidden,
+                        int rep, const float* labels, float inv_denominator, float* logits, float* d_head_in,
+                        float* partials, int64_t part_stride, float* loss_partials, dicm_stream_t stream);
+/* forward only (reference forward_prerank, model.py:529-535): logits[b] = score */
+int dicm_towers_fwd(const float* head_in, int batch, int width, const dicm_tower_t* towers, int hidden, int rep,
+                    float* logits, dicm_stream_t stream);
+
 /* partials [nblk, n] -> out[n] (deterministic, fixed order; += if accumulate) */
 int dicm_reduce_partials(const float* partials, int nblk, int64_t n, float* out, int accumulate,
                          dicm_stream_t stream);

@@ -31,15 +31,27 @@ BETA1, BETA2, EPS = 0.9, 0.999, 1e-8  # reference optim.py:16-19
 
 def make_cfg(fields, d_id=12, d_raw=4096, d_img=12, b_max=32, query_fields=("ad", "ad_category"),
              kind="sum", normalize=True, hidden=32, mlp_widths=(128, 64), use_ad_image=True,
-             use_behavior_images=True):
-    """Plain-dict model description. ``fields`` = [(name, vocab, multi)]."""
+             use_behavior_images=True, towers=None):
+    """Plain-dict model description. ``fields`` = [(name, vocab, multi)].
+
+    ``towers`` = dict(user_fields, ad_fields, hidden, rep) describes the
+    two-tower pre-rank model (reference PrerankModel, model.py:420-531)
+    instead of the MLP head; ``fields`` are then the tower fields only (the
+    reference builds tables for those alone, model.py:470-475), the
+    aggregator is "sum" and both image flags equal ``use_images``."""
     h1, h2 = max(d_raw // 16, d_img), max(d_raw // 64, d_img)  # reference model.py:88-91
     names = [f[0] for f in fields]
     qf = [q for q in query_fields if q in names]
+    if towers is not None:
+        towers = dict(user_fields=tuple(towers["user_fields"]), ad_fields=tuple(towers["ad_fields"]),
+                      hidden=int(towers["hidden"]), rep=int(towers["rep"]))
+        keep = set(towers["user_fields"]) | set(towers["ad_fields"])
+        fields = [f for f in fields if f[0] in keep]
+        kind = "sum"
     return dict(fields=[tuple(f) for f in fields], d_id=d_id, d_raw=d_raw, d_img=d_img,
                 b_max=b_max, query_fields=qf, kind=kind, normalize=normalize, hidden=hidden,
                 mlp_widths=tuple(mlp_widths), use_ad_image=use_ad_image,
-                use_behavior_images=use_behavior_images, h1=h1, h2=h2)
+                use_behavior_images=use_behavior_images, h1=h1, h2=h2, towers=towers)
 
 
 # ---------------------------------------------------------------------------
@@ -293,15 +305,19 @@ def forward_backward(p, cfg, batch, pool, denominator=None, want_grads=True):
             raise ValueError(f"aggregator {kind!r} is outside the hot path")
         parts.append(pooled)
     x = np.hstack(parts)
-    acts = [x]
-    nh = len(cfg["mlp_widths"])
-    pre_acts = []
-    for i in range(nh):
-        a = acts[-1] @ p[f"mlp/{i}/w"].T + p[f"mlp/{i}/b"]
-        pre_acts.append(a)
-        acts.append(prelu(a, p[f"mlp/{i}/a"]))
-    z = (acts[-1] @ p[f"mlp/{nh}/w"].T + p[f"mlp/{nh}/b"])[:, 0]
     y = np.asarray(batch["labels"], dtype=np.float64)
+    if cfg.get("towers"):
+        z, tower_cache = towers_fwd(p, cfg, field_vecs, ad_vec if cfg["use_ad_image"] else None,
+                                    pooled if cfg["use_behavior_images"] else None)
+    else:
+        acts = [x]
+        nh = len(cfg["mlp_widths"])
+        pre_acts = []
+        for i in range(nh):
+            a = acts[-1] @ p[f"mlp/{i}/w"].T + p[f"mlp/{i}/b"]
+            pre_acts.append(a)
+            acts.append(prelu(a, p[f"mlp/{i}/a"]))
+        z = (acts[-1] @ p[f"mlp/{nh}/w"].T + p[f"mlp/{nh}/b"])[:, 0]
     per, sig = bce(z, y)
     loss = per.sum() / denom
     out = {"loss": loss, "logits": z, "uniq": uniq, "E": E, "ad_local": ad_local,
@@ -311,15 +327,18 @@ def forward_backward(p, cfg, batch, pool, denominator=None, want_grads=True):
 
     grads = {}
     dz = (sig - y) / denom                           # autograd.py:243-244 * scale(1/denominator)
-    grads[f"mlp/{nh}/w"] = dz[None, :] @ acts[-1]
-    grads[f"mlp/{nh}/b"] = np.array([dz.sum()])
-    dh = dz[:, None] @ p[f"mlp/{nh}/w"]
-    for i in reversed(range(nh)):
-        da, grads[f"mlp/{i}/a"] = prelu_bwd(pre_acts[i], p[f"mlp/{i}/a"], dh)
-        grads[f"mlp/{i}/w"] = da.T @ acts[i]
-        grads[f"mlp/{i}/b"] = da.sum(axis=0)
-        dh = da @ p[f"mlp/{i}/w"]
-    dx = dh
+    if cfg.get("towers"):
+        dx = towers_bwd(p, cfg, tower_cache, dz, x.shape[1], grads)
+    else:
+        grads[f"mlp/{nh}/w"] = dz[None, :] @ acts[-1]
+        grads[f"mlp/{nh}/b"] = np.array([dz.sum()])
+        dh = dz[:, None] @ p[f"mlp/{nh}/w"]
+        for i in reversed(range(nh)):
+            da, grads[f"mlp/{i}/a"] = prelu_bwd(pre_acts[i], p[f"mlp/{i}/a"], dh)
+            grads[f"mlp/{i}/w"] = da.T @ acts[i]
+            grads[f"mlp/{i}/b"] = da.sum(axis=0)
+            dh = da @ p[f"mlp/{i}/w"]
+        dx = dh
 
     dE = np.zeros_like(E)
     dfield = {}
@@ -375,6 +394,70 @@ def forward_backward(p, cfg, batch, pool, denominator=None, want_grads=True):
     grads.update(ig)
     out.update(grads=grads, tgrads=tgrads, dE=dE, da0=da0)
     return out
+
+
+# ---------------------------------------------------------------------------
+# two-tower pre-rank (reference PrerankModel, model.py:420-531)
+# ---------------------------------------------------------------------------
+
+def _tower_parts(cfg, tower):
+    """Column blocks of one tower's input in hstack order (model.py:510-520):
+    its fields in the tower's order, then the pooled behavior images (user
+    tower) or the ad image (ad tower) when images are used.  Each entry is
+    the block's (column offset, width) in the head-input layout of ``forward_backward``
+    (fields in schema order, ad image, pooled)."""
+    d = cfg["d_id"]
+    names = [f[0] for f in cfg["fields"]]
+    tw = cfg["towers"]
+    cols = [(names.index(f) * d, d) for f in tw[tower + "_fields"]]
+    img_col, di = len(names) * d, cfg["d_img"]
+    if tower == "user" and cfg["use_behavior_images"]:
+        cols.append((img_col + (di if cfg["use_ad_image"] else 0), di))
+    if tower == "ad" and cfg["use_ad_image"]:
+        cols.append((img_col, di))
+    return cols
+
+
+def towers_fwd(p, cfg, field_vecs, ad_vec, pooled):
+    """Both towers (``_tower``, model.py:503-506: PReLU layer, then a linear
+    layer) and the row-wise inner product (autograd.py:388-392)."""
+    tw = cfg["towers"]
+    cache = {}
+    reps = {}
+    for tower, extra in (("user", pooled), ("ad", ad_vec)):
+        parts = [field_vecs[f] for f in tw[tower + "_fields"]]
+        if extra is not None:
+            parts.append(extra)
+        xin = np.hstack(parts) if len(parts) > 1 else parts[0]
+        pre = xin @ p[f"{tower}_tower/0/w"].T + p[f"{tower}_tower/0/b"]
+        h = prelu(pre, p[f"{tower}_tower/0/a"])
+        reps[tower] = h @ p[f"{tower}_tower/1/w"].T + p[f"{tower}_tower/1/b"]
+        cache[tower] = (xin, pre, h)
+    cache["reps"] = reps
+    return np.einsum("ij,ij->i", reps["user"], reps["ad"]), cache
+
+
+def towers_bwd(p, cfg, cache, dz, width, grads):
+    """rowwise_dot bwd (autograd.py:394-396), then each tower's linear / PReLU
+    backward; returns d(head input) in the ``forward_backward`` column layout."""
+    reps = cache["reps"]
+    dx = np.zeros((len(dz), width))
+    for tower, other in (("user", "ad"), ("ad", "user")):
+        xin, pre, h = cache[tower]
+        pre_ = f"{tower}_tower/"
+        dr = dz[:, None] * reps[other]
+        grads[pre_ + "1/w"] = dr.T @ h
+        grads[pre_ + "1/b"] = dr.sum(axis=0)
+        dh = dr @ p[pre_ + "1/w"]
+        dpre, grads[pre_ + "0/a"] = prelu_bwd(pre, p[pre_ + "0/a"], dh)
+        grads[pre_ + "0/w"] = dpre.T @ xin
+        grads[pre_ + "0/b"] = dpre.sum(axis=0)
+        dxin = dpre @ p[pre_ + "0/w"]
+        k = 0
+        for c, w in _tower_parts(cfg, tower):
+            dx[:, c:c + w] += dxin[:, k:k + w]
+            k += w
+    return dx
 
 
 # ---------------------------------------------------------------------------

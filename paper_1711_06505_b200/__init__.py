@@ -9,21 +9,21 @@ Importing the package does not need a GPU; constructing a model or a pool does.
 """
 
 from .schema import (AGGREGATOR_KINDS, AggregatorSpec, FeatureSchema, FieldSpec, ModelLayout,  # noqa: F401
-                     default_schema, image_net_widths, init_params, param_specs)
+                     TowerSpec, default_schema, image_net_widths, init_params, param_specs)
 from .batch import Batch, encode_batch, synthetic_batch  # noqa: F401
 
 __all__ = ["AGGREGATOR_KINDS", "AggregatorSpec", "FeatureSchema", "FieldSpec", "ModelLayout", "default_schema",
            "image_net_widths", "init_params", "param_specs", "Batch", "encode_batch", "synthetic_batch",
            "DicmModel", "ImagePool", "FixedExtractor", "LocalTrainer", "TrainConfig", "StepEngine", "Cluster",
            "ClusterConfig", "run_training", "InferenceTable", "KvPredictor", "export_inference",
-           "predict_logits", "checkpoint"]
+           "predict_logits", "checkpoint", "PrerankModel", "forward_ctr", "forward_prerank", "TowerSpec"]
 
 
 def __getattr__(name):
     # device-side classes load the kernel library lazily (ImportError if missing)
-    if name == "DicmModel":
-        from .model import DicmModel
-        return DicmModel
+    if name in ("DicmModel", "PrerankModel"):
+        from . import model
+        return getattr(model, name)
     if name in ("ImagePool", "FixedExtractor"):
         from . import pool
         return getattr(pool, name)
@@ -33,7 +33,8 @@ def __getattr__(name):
     if name == "StepEngine":
         from .engine import StepEngine
         return StepEngine
-    if name in ("InferenceTable", "KvPredictor", "export_inference", "predict_logits"):
+    if name in ("InferenceTable", "KvPredictor", "export_inference", "predict_logits", "forward_ctr",
+                "forward_prerank"):
         from . import inference
         return getattr(inference, name)
     if name in ("Cluster", "ClusterConfig", "run_training"):

@@ -93,6 +93,15 @@ class HeadParams(C.Structure):
     _fields_ = [(n, P) for n in ("w0", "b0", "a0", "w1", "b1", "a1", "w2", "b2")]
 
 
+TOWER_MAX_PARTS = 10
+
+
+class Tower(C.Structure):
+    _fields_ = ([(n, P) for n in ("w0", "b0", "a0", "w1", "b1")] + [("n_parts", I32),
+                                                                    ("part_col", I32 * TOWER_MAX_PARTS)]
+                + [(n, I64) for n in ("g_w0", "g_b0", "g_a0", "g_w1", "g_b1")])
+
+
 class Span(C.Structure):
     _fields_ = [("offset", I64), ("size", I64)]
 
@@ -168,6 +177,10 @@ _sig("dicm_jsonl_parse", P, C.c_char_p, I64, C.POINTER(JsonlSpec), C.c_int, C.PO
 _sig("dicm_jsonl_list_total", I64, P, C.c_int)
 _sig("dicm_jsonl_export", C.c_int, P, C.c_int, P, P, P)
 _sig("dicm_jsonl_free", None, P)
+_sig("dicm_towers_blocks", C.c_int, C.c_int)
+_sig("dicm_towers_fwd_bwd", C.c_int, P, C.c_int, C.c_int, C.POINTER(Tower), C.c_int, C.c_int, P, F, P, P, P, I64, P,
+     ST)
+_sig("dicm_towers_fwd", C.c_int, P, C.c_int, C.c_int, C.POINTER(Tower), C.c_int, C.c_int, P, ST)
 _sig("dicm_probe_enable", C.c_int, C.c_int)
 _sig("dicm_probe_read", C.c_int, C.c_int, C.POINTER(F), C.c_int, C.POINTER(C.c_int))
 
@@ -193,6 +206,7 @@ EXPORTED = [
     "dicm_p2p_alloc", "dicm_p2p_free", "dicm_ipc_handle", "dicm_ipc_open", "dicm_ipc_close", "dicm_p2p_barrier",
     "dicm_p2p_counts", "dicm_p2p_plan", "dicm_p2p_scatter", "dicm_dedup_devn", "dicm_head_fwd",
     "dicm_attn_keyproj", "dicm_jsonl_parse", "dicm_jsonl_list_total", "dicm_jsonl_export", "dicm_jsonl_free",
+    "dicm_towers_blocks", "dicm_towers_fwd_bwd", "dicm_towers_fwd",
 ]
 
 

@@ -28,6 +28,20 @@ void probe_end(int slot, cudaStream_t st);
 // ---- device helpers -------------------------------------------------------
 __device__ __forceinline__ float prelu(float x, float a) { return x > 0.f ? x : a * x; }
 
+// dLoss/dz of the scaled BCE, (sigmoid(z) - y) * inv_denom, evaluated like
+// the reference (autograd.py:241-244): in fp64, so that it is exactly zero
+// where the reference's is (fp32 would round 1 - sigmoid(20) to 0, and Adam
+// skips all-zero rows).  A nonzero f64 value below 1e-30 (a saturated logit,
+// e.g. sigmoid(-240) ~ 1e-105, which fp32 cannot hold) is kept at +-1e-30:
+// the row it reaches still counts as touched (Adam's t advances as in the
+// reference) while its update, ~lr * g / eps, stays below 1e-24.
+__device__ __forceinline__ float bce_grad(float z, float y, float inv_denom) {
+  const double sig = 1.0 / (1.0 + exp(-(double)z));
+  const double g = (sig - (double)y) * (double)inv_denom;
+  if (g != 0.0 && fabs(g) < 1e-30) return g > 0.0 ? 1e-30f : -1e-30f;
+  return (float)g;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -109,11 +109,7 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
     if (t < nb && labels) {
       const float y = labels[b0 + t];
       l = fmaxf(z, 0.f) - z * y + log1pf(expf(-fabsf(z)));
-      // dz = sigmoid(z) - y evaluated like the reference (autograd.py:241-244):
-      // in fp64, so that it is exactly zero where the reference's is (fp32
-      // would round 1 - sigmoid(20) to 0, and Adam skips all-zero rows)
-      const double sig = 1.0 / (1.0 + exp(-(double)z));
-      dz = (float)((sig - (double)y) * (double)inv_denom);
+      dz = bce_grad(z, y, inv_denom);  // fp64, zero exactly where the reference's is
       logits[b0 + t] = z;
     }
     s.dz[t] = dz;

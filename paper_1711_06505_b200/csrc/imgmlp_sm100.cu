@@ -383,19 +383,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F, 1)
 
 // ---------------------------------------------------------------------------
 // backward: part[split][256][d_raw] = da0[chunk]^T X[rows[chunk]]
-// grid = (d_raw/256 feature tiles, nsplit row chunks)
+// grid = (d_raw/256 feature tiles, nsplit row chunks).  BK rows of K per
+// stage and NST stages: 32-row stages x 6 keep as many gathered bytes in
+// flight as 64 x 3 but release each slot after half the MMAs, which
+// shortens the slot turnaround the HBM gather is bound by.
 // ---------------------------------------------------------------------------
-template <int KIND>
+template <int KIND, int BK, int NST>
 __global__ void __launch_bounds__(THREADS_B, 1)
     k_dw0(const __grid_constant__ CUtensorMap tmA, const void* __restrict__ pool_, int d_raw,
           const int32_t* __restrict__ rows, const int32_t* __restrict__ count, float* __restrict__ part) {
   using T = Elem<KIND>;
-  constexpr int EPB = 128 / sizeof(T);   // MN-atom width (elements)
-  constexpr int BK = EPB;                // rows per stage: 32 (tf32) / 64 (bf16)
-  constexpr int KROWS = 32 / sizeof(T);  // rows per MMA: 8 (tf32) / 16 (bf16)
-  constexpr int NA = 128 / EPB;          // MN atoms per 128-wide half
+  constexpr int EPB = 128 / sizeof(T);       // MN-atom width (elements)
+  constexpr int KROWS = 32 / sizeof(T);      // rows per MMA: 8 (tf32) / 16 (bf16)
+  constexpr int NA = 128 / EPB;              // MN atoms per 128-wide half
   constexpr int CPR = 256 * sizeof(T) / 16;  // 16-B chunks per row slice
   constexpr int RPI = 128 / CPR;             // rows covered per gather round
+  constexpr int NI = BK / RPI;               // gather rounds per stage (<= 32)
+  constexpr uint32_t OPB_ = 256u * BK * sizeof(T);  // one operand per stage
+  constexpr uint32_t STG = 2 * OPB_;
+  constexpr uint32_t HALF = NA * BK * 128;   // one 128-wide half of the A operand
+  static_assert(NI <= 32, "row ids are shuffled from one warp");
   // MN-major layouts: tf32 -> SWIZZLE_128B_BASE32B (4-row k groups of 512 B),
   // bf16 -> SWIZZLE_128B (8-row groups of 1024 B)
   constexpr uint32_t MN_LAYOUT = KIND == 0 ? 1u : 2u;
@@ -413,38 +420,56 @@ __global__ void __launch_bounds__(THREADS_B, 1)
     return;
   }
   extern __shared__ uint8_t smem_raw[];
-  const Smem s = carve(smem_raw);
-  const uint32_t tmem = setup(s, warp, 1);
+  const uint32_t rs = smem_u32(smem_raw);
+  const uint32_t base = (rs + 1023u) & ~1023u;
+  const uint32_t full = base + NST * STG, empty = full + 8 * NST, acc_full = empty + 8 * NST, slot = acc_full + 8;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(full + 8 * i, 128 + 1);  // 128 gather threads (cp.async arrive) + TMA expect_tx
+      mbar_init(empty + 8 * i, 1);       // tcgen05.commit
+    }
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 4) {
+    tmem_alloc(slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem_raw + (slot - rs));
   const T* pool = reinterpret_cast<const T*>(pool_);
 
   if (warp < 4) {
     // ---- gather producer: X[rows] feature slice [f0, f0+256) of BK rows.
-    // Thread t owns 16-B chunk c of rows kw + i*RPI (i < 16); lane i < 16 of
+    // Thread t owns 16-B chunk c of rows kw + i*RPI (i < NI); lane i < NI of
     // the warp fetches row id i one stage ahead and the warp shuffles it.
     const int t = threadIdx.x, c = t % CPR, kw = t / CPR;
     const T* colbase = pool + f0 + c * (16 / sizeof(T));
     const uint32_t atom_off = (c >> 3) * (BK * 128);
     auto fetch = [&](int kb) {
       const int gr = r0 + kb * BK + lane * RPI + kw;
-      return (lane < 16 && kb < nk && gr < r1) ? __ldg(rows + gr) : -1;
+      return (lane < NI && kb < nk && gr < r1) ? __ldg(rows + gr) : -1;
     };
     int rid_next = fetch(0);
     for (int kb = 0; kb < nk; ++kb) {
       const int rid_cur = rid_next;
       rid_next = fetch(kb + 1);
-      wait_stage(s.empty, kb, true);
-      const uint32_t b = s.base + (kb % STAGES) * STAGE_BYTES + OPB + atom_off;
+      const uint32_t st = kb % NST, itn = kb / NST;
+      mbar_wait(empty + 8 * st, (itn & 1) ^ 1);
+      const uint32_t bb = base + st * STG + OPB_ + atom_off;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < NI; ++i) {
         const int rid = __shfl_sync(FULL, rid_cur, i);
         const int k = i * RPI + kw;
         // tf32 MN-major operands need the 32-B-granule 128-B swizzle
         // (Swizzle<2,5,2>: granule ^= row & 3); bf16 uses the 16-B one
         const uint32_t sw = KIND == 0 ? ((((c & 7) >> 1) ^ (k & 3)) << 5) | ((c & 1) << 4)
                                       : (((c & 7) ^ (k & 7)) << 4);
-        cp_async16(b + k * 128 + sw, colbase + (int64_t)(rid < 0 ? 0 : rid) * d_raw, rid < 0 ? 0u : 16u);
+        cp_async16(bb + k * 128 + sw, colbase + (int64_t)(rid < 0 ? 0 : rid) * d_raw, rid < 0 ? 0u : 16u);
       }
-      cp_async_arrive_noinc(s.full + 8 * (kb % STAGES));
+      cp_async_arrive_noinc(full + 8 * st);
     }
     cp_async_wait<0>();
   } else if (warp == 5) {
@@ -452,38 +477,39 @@ __global__ void __launch_bounds__(THREADS_B, 1)
       // ---- TMA producer: da0 [rows, 256] MN-major atoms (EPB hidden x BK rows)
       prefetch_tmap(&tmA);
       for (int kb = 0; kb < nk; ++kb) {
-        wait_stage(s.empty, kb, true);
-        const uint32_t st = kb % STAGES;
-        mbar_arrive_expect_tx(s.full + 8 * st, OPB);
-        const uint32_t a = s.base + st * STAGE_BYTES;
+        const uint32_t st = kb % NST, itn = kb / NST;
+        mbar_wait(empty + 8 * st, (itn & 1) ^ 1);
+        mbar_arrive_expect_tx(full + 8 * st, OPB_);
+        const uint32_t a = base + st * STG;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int j = 0; j < NA; ++j)
-            tma_load_2d(a + h * 16384 + j * (BK * 128), &tmA, s.full + 8 * st, h * 128 + j * EPB, r0 + kb * BK);
+            tma_load_2d(a + h * HALF + j * (BK * 128), &tmA, full + 8 * st, h * 128 + j * EPB, r0 + kb * BK);
       }
     }
   } else {
     if (lane == 0) {
       const uint32_t idesc = instr_desc(KIND == 0 ? 2u : 1u, 128, 256, 1, 1);
       for (int kb = 0; kb < nk; ++kb) {
-        wait_stage(s.full, kb, false);
+        const uint32_t st = kb % NST, itn = kb / NST;
+        mbar_wait(full + 8 * st, itn & 1);
         tc_fence_after();
         fence_proxy_async();
-        const uint32_t a = s.base + (kb % STAGES) * STAGE_BYTES, b = a + OPB;
+        const uint32_t a = base + st * STG, bb = a + OPB_;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int k = 0; k < BK / KROWS; ++k)
-            mma<KIND>(tmem + h * 256, smem_desc(a + h * 16384 + k * KROWS * 128, BK * 128, MN_SBO, MN_LAYOUT),
-                      smem_desc(b + k * KROWS * 128, BK * 128, MN_SBO, MN_LAYOUT), idesc, (kb | k) != 0);
-        mma_commit(s.empty + 8 * (kb % STAGES));
+            mma<KIND>(tmem + h * 256, smem_desc(a + h * HALF + k * KROWS * 128, BK * 128, MN_SBO, MN_LAYOUT),
+                      smem_desc(bb + k * KROWS * 128, BK * 128, MN_SBO, MN_LAYOUT), idesc, (kb | k) != 0);
+        mma_commit(empty + 8 * st);
       }
-      mma_commit(s.acc_full);
+      mma_commit(acc_full);
     }
   }
   if (warp < 4) {
-    mbar_wait(s.acc_full, 0);
+    mbar_wait(acc_full, 0);
     tc_fence_after();
 #pragma unroll 1
     for (int h = 0; h < 2; ++h) {
@@ -501,6 +527,11 @@ __global__ void __launch_bounds__(THREADS_B, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 4) tmem_dealloc(tmem, 512);
+}
+
+template <int KIND, int BK, int NST>
+constexpr size_t dw0_smem() {
+  return (size_t)NST * 2 * 256 * BK * (KIND == 0 ? 4 : 2) + 1024 + 256;
 }
 
 __global__ void k_sum_splits(const float* __restrict__ part, int nsplit, int64_t n, float* __restrict__ out) {
@@ -677,23 +708,27 @@ int bwd_dw0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows, co
   }
   CUtensorMap map;
   int rc;
-  const uint32_t box_rows = bf16 ? 64 : 32;
+  constexpr int BKB = 64, NSB = 3;  // bf16: 64-row stages x 3 (32 x 6 measured slower: 1.10 vs 0.89 ms)
+  constexpr int BKT = 32, NST_ = 3;  // tf32: 32-row stages x 3 (32 KB + 32 KB each)
+  const uint32_t box_rows = bf16 ? BKB : BKT;
   if ((rc = make_map(&map, asrc, bf16, (uint64_t)rows_max, 256, box_rows,
                      bf16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)))
     return rc;
   const int nsplit = nsplit_for(rows_max, d_raw);
   dim3 grid(d_raw / 256, nsplit);
   if (bf16) {
-    static int once = set_smem(k_dw0<1>);
+    static int once = check_cuda(cudaFuncSetAttribute(k_dw0<1, BKB, NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      (int)dw0_smem<1, BKB, NSB>()), "k_dw0 smem");
     if (once) return once;
     const int probe_slot = probe_begin(DICM_PROBE_IMG_BWD_DW0, st);
-    k_dw0<1><<<grid, THREADS_B, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, w.part);
+    k_dw0<1, BKB, NSB><<<grid, THREADS_B, dw0_smem<1, BKB, NSB>(), st>>>(map, pool, d_raw, rows, count, w.part);
     probe_end(probe_slot, st);
   } else {
-    static int once = set_smem(k_dw0<0>);
+    static int once = check_cuda(cudaFuncSetAttribute(k_dw0<0, BKT, NST_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      (int)dw0_smem<0, BKT, NST_>()), "k_dw0 smem");
     if (once) return once;
     const int probe_slot = probe_begin(DICM_PROBE_IMG_BWD_DW0, st);
-    k_dw0<0><<<grid, THREADS_B, SMEM_BYTES, st>>>(map, pool, d_raw, rows, count, w.part);
+    k_dw0<0, BKT, NST_><<<grid, THREADS_B, dw0_smem<0, BKT, NST_>(), st>>>(map, pool, d_raw, rows, count, w.part);
     probe_end(probe_slot, st);
   }
   const int64_t n = (int64_t)256 * d_raw;

@@ -11,6 +11,7 @@ One step, all on one CUDA stream, no host round trip until the loss is read:
   a10    dicm_gather_rows_by_key           -> compact ID rows [K,12]
   a6-10  dicm_sample_fwd                   -> head input x [B, W]
   a11-12 dicm_head_fwd_bwd                 -> logits, dLoss/dx, head-grad partials
+         (pre-rank model: dicm_towers_fwd_bwd, the two towers + inner product)
   a6-10  dicm_sample_bwd                   -> dE [U,12], dRows [K,12], attention partials
   a5     dicm_imgmlp_bwd                   -> img/* gradients
   a14    dicm_adam_dense + dicm_adam_rows
@@ -54,7 +55,7 @@ class Packed:
         self.R = batch.refs
         off = 0
         self.onehot, self.multi = {}, {}
-        for f in model.schema.fields:
+        for f in model.layout.schema.fields:
             if f.multi:
                 flat, o = batch.multihot[f.name]
                 self.multi[f.name] = (off, len(flat), off + len(flat))
@@ -72,7 +73,7 @@ class Packed:
         self.total = off
 
     def fill(self, model, batch, host):
-        for f in model.schema.fields:
+        for f in model.layout.schema.fields:
             if f.multi:
                 a, n, o = self.multi[f.name]
                 flat, offs = batch.multihot[f.name]
@@ -199,7 +200,7 @@ class StepEngine:
         self.iteration = 0
         dev = self.dev = model.device
         lay = model.layout
-        self.fields = list(model.schema.fields)
+        self.fields = list(lay.schema.fields)  # the fields with tables (pre-rank: tower fields)
         # global ID key space: field f at bases[f] (aligned), vocab = schema vocab
         self.bases, base = [], 0
         for f in self.fields:
@@ -245,11 +246,14 @@ class StepEngine:
         pnames = ("img/0/w", "img/0/b", "img/0/a", "img/1/w", "img/1/b", "img/1/a", "img/2/w", "img/2/b")
         self.img_p = L.ImgMlpParams(**{k: p(n) for k, n in zip(names, pnames)})
         self.img_g = L.ImgMlpGrads(**{k: g(n) for k, n in zip(names, pnames)})
-        hn = ("mlp/0/w", "mlp/0/b", "mlp/0/a", "mlp/1/w", "mlp/1/b", "mlp/1/a", "mlp/2/w", "mlp/2/b")
-        self.head_p = L.HeadParams(**{k: p(n) for k, n in zip(names, hn)})
         self.width = lay.mlp_input_width()
-        self.head_range = model.group_range("mlp/")
-        assert self.head_range[1] - self.head_range[0] == L.lib.dicm_head_partial_size(self.width)
+        if lay.towers is None:
+            hn = ("mlp/0/w", "mlp/0/b", "mlp/0/a", "mlp/1/w", "mlp/1/b", "mlp/1/a", "mlp/2/w", "mlp/2/b")
+            self.head_p = L.HeadParams(**{k: p(n) for k, n in zip(names, hn)})
+            self.head_range = model.group_range("mlp/")
+            assert self.head_range[1] - self.head_range[0] == L.lib.dicm_head_partial_size(self.width)
+        else:
+            self._setup_towers(model)
         self.attn_range = model.group_range("attn/")
         self.attn_part = int(L.lib.dicm_attn_partial_size(C.byref(self.layout)))
         if self.attn_range is not None:
@@ -259,6 +263,56 @@ class StepEngine:
         self._pinned = [None, None]
         self._pin_ev = [None, None]
         self._pin_i = 0
+
+    def _setup_towers(self, model):
+        """Pre-rank head (csrc/towers.cu): tower descriptors whose gradient
+        offsets index one partial row laid out like the fused buffer's
+        ad_tower/* + user_tower/* range (contiguous in sorted order)."""
+        lay = model.layout
+        names = [n for n in model.dense_names if n.split("/")[0] in ("user_tower", "ad_tower")]
+        start = min(model.dense_offsets[n][0] for n in names)
+        end = max(model.dense_offsets[n][0] + model.dense_offsets[n][1] for n in names)
+        assert end - start == sum(model.dense_offsets[n][1] for n in names), "tower params not contiguous"
+        self.head_range = (start, end)
+        self.towers = (L.Tower * 2)()
+        for i, t in enumerate(("user", "ad")):
+            tw = self.towers[i]
+            pre = f"{t}_tower/"
+            for k, n in (("w0", "0/w"), ("b0", "0/b"), ("a0", "0/a"), ("w1", "1/w"), ("b1", "1/b")):
+                setattr(tw, k, model.params[pre + n].tensor.data_ptr())
+                setattr(tw, "g_" + k, model.dense_offsets[pre + n][0] - start)
+            parts = lay.tower_parts(t)
+            tw.n_parts = len(parts)
+            for j, (col, _w) in enumerate(parts):
+                tw.part_col[j] = col
+
+    def _head_blocks(self, B):
+        return L.lib.dicm_towers_blocks(B) if self.model.layout.towers else L.lib.dicm_head_blocks(B)
+
+    def _head_fwd_bwd(self, B, denom):
+        """a11-a12: MLP head (or the two towers) + BCE -> logits, d_head_in,
+        gradient partials, loss partials."""
+        pk, s = self.pk, self.s
+        tw = self.model.layout.towers
+        if tw is None:
+            L.check(L.lib.dicm_head_fwd_bwd(self.head_in.data_ptr(), B, self.width, self._dptr(pk.labels),
+                                            1.0 / denom, C.byref(self.head_p), self.logits.data_ptr(),
+                                            self.d_head_in.data_ptr(), self.head_part.data_ptr(),
+                                            self.loss_part.data_ptr(), s))
+        else:
+            L.check(L.lib.dicm_towers_fwd_bwd(self.head_in.data_ptr(), B, self.width, self.towers, tw.hidden, tw.rep,
+                                              self._dptr(pk.labels), 1.0 / denom, self.logits.data_ptr(),
+                                              self.d_head_in.data_ptr(), self.head_part.data_ptr(),
+                                              self.head_part.shape[1], self.loss_part.data_ptr(), s))
+
+    def _head_fwd(self, B):
+        tw = self.model.layout.towers
+        if tw is None:
+            L.check(L.lib.dicm_head_fwd(self.head_in.data_ptr(), B, self.width, C.byref(self.head_p),
+                                        self.logits.data_ptr(), self.s))
+        else:
+            L.check(L.lib.dicm_towers_fwd(self.head_in.data_ptr(), B, self.width, self.towers, tw.hidden, tw.rep,
+                                          self.logits.data_ptr(), self.s))
 
     # ------------------------------------------------------------------
     @property
@@ -332,9 +386,8 @@ class StepEngine:
         self.logits = torch.empty(max(B, 1), **f32)
         self.scores = torch.empty((2, max(R, 1)), **f32)
         self.stats = torch.empty((2, max(B, 1), 2), **f32)
-        self.head_part = torch.empty((L.lib.dicm_head_blocks(max(B, 1)), self.head_range[1] - self.head_range[0]),
-                                     **f32)
-        self.loss_part = torch.empty(L.lib.dicm_head_blocks(max(B, 1)), **f32)
+        self.head_part = torch.empty((self._head_blocks(max(B, 1)), self.head_range[1] - self.head_range[0]), **f32)
+        self.loss_part = torch.empty(self._head_blocks(max(B, 1)), **f32)
         self.attn_partial = torch.empty((L.lib.dicm_sample_blocks(max(B, 1)), max(self.attn_part, 1)), **f32)
         self.loss = torch.zeros(1, **f32)
         lay = self.model.layout
@@ -490,11 +543,8 @@ class StepEngine:
         bv = self._batch_view(emb)
         L.check(L.lib.dicm_sample_fwd(C.byref(self.layout), C.byref(bv), self.attn, self.head_in.data_ptr(),
                                       self.scores.data_ptr(), self.stats.data_ptr(), s))
-        L.check(L.lib.dicm_head_fwd_bwd(self.head_in.data_ptr(), B, self.width, self._dptr(pk.labels),
-                                        1.0 / denom, C.byref(self.head_p), self.logits.data_ptr(),
-                                        self.d_head_in.data_ptr(), self.head_part.data_ptr(),
-                                        self.loss_part.data_ptr(), s))
-        nhb = L.lib.dicm_head_blocks(B)
+        self._head_fwd_bwd(B, denom)
+        nhb = self._head_blocks(B)
         L.check(L.lib.dicm_loss_finalize(self.loss_part.data_ptr(), nhb, 1.0 / denom, self.loss.data_ptr(), st, s))
         d_emb.zero_()
         self.d_rows.zero_()
@@ -594,8 +644,7 @@ class StepEngine:
         bv = self._batch_view(self.net.emb)
         L.check(L.lib.dicm_sample_fwd(C.byref(self.layout), C.byref(bv), self.attn, self.head_in.data_ptr(),
                                       self.scores.data_ptr(), self.stats.data_ptr(), self.s))
-        L.check(L.lib.dicm_head_fwd(self.head_in.data_ptr(), self.pk.B, self.width, C.byref(self.head_p),
-                                    self.logits.data_ptr(), self.s))
+        self._head_fwd(self.pk.B)
         return self.logits[:self.pk.B]
 
     def step_device(self, db, denominator=None):

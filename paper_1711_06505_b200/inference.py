@@ -134,6 +134,19 @@ def predict_logits(model, samples, store, chunk=1024, precision="fp32"):
     return out
 
 
+def forward_ctr(model, samples, store, precision="fp32"):
+    """Score samples with the live model -> (probabilities, logits)
+    (reference forward_ctr, model.py:411-417)."""
+    z = predict_logits(model, samples, store, precision=precision)
+    return 1.0 / (1.0 + np.exp(-z)), z
+
+
+def forward_prerank(model, samples, store, precision="fp32"):
+    """Two-tower scores (inner products) -> (probabilities, scores)
+    (reference forward_prerank, model.py:529-535)."""
+    return forward_ctr(model, samples, store, precision)
+
+
 class KvPredictor:
     """Scores samples from frozen parameters plus the exported table
     (reference inference.py:49-81); ids beyond the table take the cold path

@@ -54,6 +54,8 @@ class Parameter:
 def check_hot_path(layout):
     """The kernels are compiled for the paper's configuration."""
     s = layout.schema
+    if layout.towers is not None:
+        return _check_towers(layout)
     if layout.aggregator.kind not in S.HOT_PATH_AGGREGATORS:
         raise NotImplementedError(
             f"aggregator {layout.aggregator.kind!r} is outside this build's hot path "
@@ -76,6 +78,29 @@ def check_hot_path(layout):
                 raise NotImplementedError("multiquery-attn query fields must be one-hot")
 
 
+def _check_image_net(layout):
+    s = layout.schema
+    if s.d_id != 12 or s.d_img != 12:
+        raise NotImplementedError("kernels are built for d_id = d_img = 12")
+    if layout.h1 != 256 or layout.h2 != 64 or s.d_raw % 64:
+        raise NotImplementedError("kernels are built for the 4096 -> 256 -> 64 -> 12 image net")
+    if len(s.fields) > 8:
+        raise NotImplementedError("at most 8 ID fields")
+
+
+def _check_towers(layout):
+    from . import _lib as L
+    _check_image_net(layout)
+    tw = layout.towers
+    if not 1 <= tw.hidden <= 128 or not 1 <= tw.rep <= 64:
+        raise NotImplementedError("tower kernels take hidden <= 128 and rep_dim <= 64")
+    for t in ("user", "ad"):
+        if not 1 <= len(layout.tower_parts(t)) <= L.TOWER_MAX_PARTS:
+            raise NotImplementedError(f"{t} tower needs 1..{L.TOWER_MAX_PARTS} input blocks")
+    if layout.mlp_input_width() > 128:
+        raise NotImplementedError(f"tower input layout width {layout.mlp_input_width()} > 128")
+
+
 class DicmModel:
     """Embedding&MLP CTR net with ad-image and behavior-image paths."""
 
@@ -88,6 +113,23 @@ class DicmModel:
         draws 0.05 N(0,1) rows on the device instead (same distribution as
         model.py:316-319, not the same values) -- for 100M-row tables whose
         reference init would not fit host memory."""
+        layout = ModelLayout(schema, aggregator, tuple(mlp_widths), use_ad_image, use_behavior_images)
+        S.validate_layout(layout, None if extractor is None else extractor.out_dim)
+        check_hot_path(layout)
+        self.schema = schema
+        self.aggregator = aggregator
+        self.extractor = extractor
+        self.seed = seed
+        self.mlp_widths = tuple(mlp_widths)
+        self.use_ad_image = use_ad_image
+        self.use_behavior_images = use_behavior_images
+        self._build(layout, seed, device, params, table_rows, shard, table_init)
+
+    def _build(self, layout, seed, device, params, table_rows, shard, table_init):
+        """Device storage of every parameter of ``layout`` (tables of
+        ``layout.schema``'s fields)."""
+        schema = layout.schema
+        host = params if params is not None else {}
         if table_init == "device" and table_rows is None:
             world, rank = shard if shard is not None else (1, 0)
 
@@ -100,24 +142,13 @@ class DicmModel:
             world, rank = shard
 
             def table_rows(f, name):
-                full = host[name] if name in (params or {}) else S.init_param(seed, name, (f.vocab, schema.d_id),
-                                                                             "table")
+                full = host[name] if name in host else S.init_param(seed, name, (f.vocab, schema.d_id), "table")
                 local = np.asarray(full)[rank::world]
                 n_local = -(-f.vocab // world)
                 out = np.zeros((n_local, schema.d_id))
                 out[:len(local)] = local
                 return torch.as_tensor(out, dtype=torch.float32).to(device)
         self.shard = shard
-        layout = ModelLayout(schema, aggregator, tuple(mlp_widths), use_ad_image, use_behavior_images)
-        S.validate_layout(layout, None if extractor is None else extractor.out_dim)
-        check_hot_path(layout)
-        self.schema = schema
-        self.aggregator = aggregator
-        self.extractor = extractor
-        self.seed = seed
-        self.mlp_widths = tuple(mlp_widths)
-        self.use_ad_image = use_ad_image
-        self.use_behavior_images = use_behavior_images
         self.layout = layout
         self.device = torch.device(device)
         self.specs = S.param_specs(layout)
@@ -140,7 +171,6 @@ class DicmModel:
         self.dense_size = off
         self.dense = torch.zeros(off, dtype=torch.float32, device=self.device)
         self.params = {}
-        host = params if params is not None else {}
         kinds = {nm: k for nm, _, k in self.specs}
         for n in self.dense_names:
             o, size, shp = self.dense_offsets[n]
@@ -171,7 +201,7 @@ class DicmModel:
         return S.image_param_names(self.layout)
 
     def table_fields(self):
-        return [f.name for f in self.schema.fields]
+        return [f.name for f in self.layout.schema.fields]
 
     def mlp_input_width(self):
         return self.layout.mlp_input_width()
@@ -191,3 +221,33 @@ class DicmModel:
 
     def snapshot(self):
         return {n: p.data for n, p in self.params.items()}
+
+
+class PrerankModel(DicmModel):
+    """Two-tower pre-rank variant (reference PrerankModel, model.py:420-531):
+    user and ad representations scored by their inner product.  Behavior
+    images enter the user tower through sum pooling, the ad image enters the
+    ad tower; only the tower fields get tables.  Same constructor arguments
+    and validation errors as the reference; the image net, the ID tables and
+    the per-sample kernels are the DICM ones, the head is the tower kernel
+    (csrc/towers.cu)."""
+
+    def __init__(self, schema, extractor=None, seed=0, user_fields=("user", "behavior_items"),
+                 ad_fields=("ad", "ad_category"), tower_hidden=64, rep_dim=16, use_images=True, device="cuda",
+                 params=None, table_rows=None, shard=None, table_init="reference"):
+        layout = S.prerank_layout(schema, tuple(user_fields), tuple(ad_fields), tower_hidden, rep_dim, use_images,
+                                  None if extractor is None else extractor.out_dim)
+        check_hot_path(layout)
+        self.schema = schema
+        self.extractor = extractor
+        self.seed = seed
+        self.user_fields = tuple(user_fields)
+        self.ad_fields = tuple(ad_fields)
+        self.tower_hidden = tower_hidden
+        self.rep_dim = rep_dim
+        self.use_images = use_images
+        self.use_ad_image = use_images
+        self.use_behavior_images = use_images
+        self.aggregator = layout.aggregator
+        self.mlp_widths = ()
+        self._build(layout, seed, device, params, table_rows, shard, table_init)

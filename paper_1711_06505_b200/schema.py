@@ -120,14 +120,47 @@ def rng_for(seed, name):
 
 
 @dataclass(frozen=True)
+class TowerSpec:
+    """The two towers of the pre-rank model (reference PrerankModel,
+    model.py:420-531): field lists in hstack order, hidden and output width."""
+
+    user_fields: tuple
+    ad_fields: tuple
+    hidden: int = 64
+    rep: int = 16
+
+
+@dataclass(frozen=True)
 class ModelLayout:
-    """Everything the kernels need to know about one DICM configuration."""
+    """Everything the kernels need to know about one DICM configuration.
+
+    ``towers`` set: the two-tower pre-rank model -- ``schema`` then holds the
+    tower fields only (the reference builds tables for those alone,
+    model.py:470-475), pooling is "sum", and the head input feeds the towers
+    instead of the MLP head."""
 
     schema: FeatureSchema
     aggregator: AggregatorSpec
     mlp_widths: tuple
     use_ad_image: bool
     use_behavior_images: bool
+    towers: TowerSpec = None
+
+    def tower_parts(self, tower):
+        """(head-input column, width) blocks of one tower's input in the
+        reference's hstack order (model.py:510-520): the tower's fields, then
+        the pooled behavior images (user) or the ad image (ad)."""
+        s, off = self.schema, self.head_offsets()
+        tw = self.towers
+        out = [(off["field/" + f], s.d_id) for f in (tw.user_fields if tower == "user" else tw.ad_fields)]
+        if tower == "user" and self.use_behavior_images:
+            out.append((off["pool"], s.d_img))
+        if tower == "ad" and self.use_ad_image:
+            out.append((off["ad_image_emb"], s.d_img))
+        return out
+
+    def tower_input_width(self, tower):
+        return sum(w for _, w in self.tower_parts(tower))
 
     @property
     def h1(self):
@@ -180,6 +213,24 @@ class ModelLayout:
         return out
 
 
+def prerank_layout(schema, user_fields=("user", "behavior_items"), ad_fields=("ad", "ad_category"),
+                   tower_hidden=64, rep_dim=16, use_images=True, extractor_out_dim=None):
+    """Layout of the reference ``PrerankModel`` (model.py:427-458), with its
+    constructor checks: the extractor width and every tower field present."""
+    if extractor_out_dim is not None and extractor_out_dim != schema.d_raw:
+        raise ValueError(f"extractor emits {extractor_out_dim}-D features, schema expects {schema.d_raw}")
+    names = [f.name for f in schema.fields]
+    for fn in (*user_fields, *ad_fields):
+        if fn not in names:
+            raise ValueError(f"tower field {fn!r} missing from schema")
+    keep = set(user_fields) | set(ad_fields)
+    sub = FeatureSchema(fields=[f for f in schema.fields if f.name in keep], d_id=schema.d_id,
+                        d_raw=schema.d_raw, d_img=schema.d_img, b_max=schema.b_max,
+                        query_fields=tuple(schema.query_fields))
+    return ModelLayout(sub, AggregatorSpec("sum"), (), bool(use_images), bool(use_images),
+                       TowerSpec(tuple(user_fields), tuple(ad_fields), int(tower_hidden), int(rep_dim)))
+
+
 def validate_layout(layout, extractor_out_dim=None):
     """The constructor checks of reference model.py:279-288."""
     agg = layout.aggregator
@@ -211,6 +262,12 @@ def param_specs(layout):
     lin("img/0/", s.d_raw, h1)
     lin("img/1/", h1, h2)
     lin("img/2/", h2, s.d_img, alpha=False)
+    if layout.towers is not None:  # reference model.py:477-481
+        tw = layout.towers
+        for t in ("user", "ad"):
+            lin(f"{t}_tower/0/", layout.tower_input_width(t), tw.hidden)
+            lin(f"{t}_tower/1/", tw.hidden, tw.rep, alpha=False)
+        return out
     if layout.attentive:
         hidden = layout.aggregator.attention_hidden
         lin("attn/img/0/", 2 * s.d_img, hidden)

@@ -31,16 +31,20 @@ def main():
     from oracle import dicm_oracle as O
     import gpu_helpers as H
     from paper_1711_06505_b200.batch import synthetic_batch
-    from paper_1711_06505_b200.model import DicmModel
+    from paper_1711_06505_b200.model import DicmModel, PrerankModel
     from paper_1711_06505_b200.pool import FixedExtractor, ImagePool
     from paper_1711_06505_b200.runtime import Cluster, ClusterConfig
-    from paper_1711_06505_b200.schema import AggregatorSpec, default_schema, init_params, ModelLayout
+    from paper_1711_06505_b200.schema import AggregatorSpec, default_schema, init_params, ModelLayout, prerank_layout
 
     P, bpw, iters = 2000, 96, 3
     schema = default_schema(3001, 4, 2999, 8, P, b_max=30)
-    agg = AggregatorSpec(kind)
-    full = init_params(ModelLayout(schema, agg, (128, 64), True, True), 0)
-    model = DicmModel(schema, agg, None, seed=0, shard=(world, rank))
+    if kind == "prerank":  # two-tower pre-rank model (reference model.py:420-531)
+        full = init_params(prerank_layout(schema), 0)
+        model = PrerankModel(schema, None, seed=0, shard=(world, rank))
+    else:
+        agg = AggregatorSpec(kind)
+        full = init_params(ModelLayout(schema, agg, (128, 64), True, True), 0)
+        model = DicmModel(schema, agg, None, seed=0, shard=(world, rank))
     gen = torch.Generator().manual_seed(11)
     lat = torch.randn((P, 32), generator=gen)
     ext = FixedExtractor(0x5EED, 32, 4096)
@@ -57,7 +61,7 @@ def main():
     # gather every rank's table shard
     snap = cl.snapshot()
     tables = {}
-    for f in schema.fields:
+    for f in model.layout.schema.fields:
         t = torch.as_tensor(snap[f"id_emb/{f.name}"], device="cuda")
         parts = [torch.empty_like(t) for _ in range(world)]
         dist.all_gather(parts, t)

@@ -33,7 +33,8 @@ sys.path.insert(0, REF)
 from dicm import autograd as ag  # noqa: E402
 from dicm.data import Sample  # noqa: E402
 from dicm.images import FixedExtractor  # noqa: E402
-from dicm.model import AggregatorSpec, DicmModel, FeatureSchema, FieldSpec, encode_batch  # noqa: E402
+from dicm.model import (AggregatorSpec, DicmModel, FeatureSchema, FieldSpec, PrerankModel,  # noqa: E402
+                        encode_batch)
 from dicm.runtime import Cluster, ClusterConfig  # noqa: E402
 from dicm.training import LocalTrainer, TrainConfig, batch_loss_graph  # noqa: E402
 
@@ -112,9 +113,14 @@ def build(case):
     schema = FeatureSchema(fields=fields, d_id=case["d_id"], d_raw=case["d_raw"],
                            d_img=case["d_img"], b_max=case["b_max"],
                            query_fields=tuple(case["query_fields"]))
+    ext = FixedExtractor(seed=7, latent_dim=4, out_dim=case["d_raw"])
+    if case.get("towers"):  # two-tower pre-rank (reference model.py:420-531)
+        tw = case["towers"]
+        return PrerankModel(schema, ext, seed=case["seed"], user_fields=tuple(tw["user_fields"]),
+                            ad_fields=tuple(tw["ad_fields"]), tower_hidden=tw["hidden"],
+                            rep_dim=tw["rep"], use_images=case["use_ad_image"])
     agg = AggregatorSpec(case["kind"], attention_hidden=case["hidden"],
                          normalize=case["normalize"])
-    ext = FixedExtractor(seed=7, latent_dim=4, out_dim=case["d_raw"])
     return DicmModel(schema, agg, ext, seed=case["seed"], mlp_widths=tuple(case["mlp_widths"]),
                      use_ad_image=case["use_ad_image"],
                      use_behavior_images=case["use_behavior_images"])
@@ -199,6 +205,15 @@ def full_case(kind, normalize=True, use_ad_image=True, seed=0):
                 seed=seed), vocabs
 
 
+def prerank_case(base, user_fields=("user", "behavior_items"), ad_fields=("ad", "ad_category"),
+                 hidden=64, rep=16, use_images=True):
+    case = dict(base)
+    case.update(kind="sum", use_ad_image=use_images, use_behavior_images=use_images,
+                towers=dict(user_fields=list(user_fields), ad_fields=list(ad_fields), hidden=hidden,
+                            rep=rep))
+    return case
+
+
 def main():
     # tiny dims: pool rows straight from the reference extractor
     rng = np.random.default_rng(99)
@@ -214,6 +229,13 @@ def main():
         if os.environ.get("GOLDEN_ONLY") and f"tiny_{kind}" not in os.environ["GOLDEN_ONLY"].split(","):
             continue
         run_case(f"tiny_{kind}", tiny_case(kind), tiny_pool, tiny_batches)
+    if not os.environ.get("GOLDEN_ONLY") or "tiny_prerank" in os.environ["GOLDEN_ONLY"].split(","):
+        # the reference test's pre-rank schema (tests/test_model.py:236-247)
+        case = prerank_case(dict(tiny_case("sum"), fields=[["user", 5, False], ["ad", 7, False],
+                                                           ["ad_category", 3, False],
+                                                           ["behavior_items", 9, True]]),
+                            hidden=6, rep=5)
+        run_case("tiny_prerank", case, tiny_pool, tiny_batches)
 
     # full dims (4096 -> 256 -> 64 -> 12), fp32 pool rows = tanh(z R^T)
     prng = np.random.default_rng(2024)
@@ -231,6 +253,18 @@ def main():
         batches = [make_samples(brng, 24, vocabs, 40, 20) for _ in range(2)]
         cluster = (2, 2) if tag in ("mq", "sum") else None
         run_case(f"full_{tag}", case, full_pool, batches, union_cluster=cluster)
+    for tag, kw in (("prerank", {}),
+                    ("prerank_img_ids", dict(user_fields=("behavior_images", "user", "behavior_items"),
+                                             ad_fields=("ad_image", "ad_category", "ad"), hidden=32, rep=8)),
+                    ("prerank_noimg", dict(use_images=False))):
+        if os.environ.get("GOLDEN_ONLY") and f"full_{tag}" not in os.environ["GOLDEN_ONLY"].split(","):
+            continue
+        base, vocabs = full_case("sum")
+        case = prerank_case(base, **kw)
+        brng = np.random.default_rng(len(tag) * 1013 + ord(tag[-1]))
+        batches = [make_samples(brng, 24, vocabs, 40, 20) for _ in range(2)]
+        run_case(f"full_{tag}", case, full_pool, batches,
+                 union_cluster=(2, 2) if tag == "prerank" else None)
 
 
 if __name__ == "__main__":

@@ -13,8 +13,9 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 BIG = 50_000
 PROBE_SEED = 1234
 
-TINY = ["tiny_sum", "tiny_attn", "tiny_multiquery-attn", "tiny_max"]
-FULL = ["full_sum", "full_attn", "full_attn_raw", "full_mq", "full_sum_noad", "full_max"]
+TINY = ["tiny_sum", "tiny_attn", "tiny_multiquery-attn", "tiny_max", "tiny_prerank"]
+FULL = ["full_sum", "full_attn", "full_attn_raw", "full_mq", "full_sum_noad", "full_max", "full_prerank",
+        "full_prerank_img_ids", "full_prerank_noimg"]
 
 
 def load(name):
@@ -26,10 +27,20 @@ def meta(fx):
     return json.loads(str(fx["meta"]))
 
 
-def layout_of(m):
+def full_schema(m):
+    """The case's schema with every field (a pre-rank layout keeps only the
+    tower fields)."""
     fields = [S.FieldSpec(n, v, mu) for n, v, mu in m["fields"]]
-    schema = S.FeatureSchema(fields=fields, d_id=m["d_id"], d_raw=m["d_raw"], d_img=m["d_img"],
-                             b_max=m["b_max"], query_fields=tuple(m["query_fields"]))
+    return S.FeatureSchema(fields=fields, d_id=m["d_id"], d_raw=m["d_raw"], d_img=m["d_img"],
+                           b_max=m["b_max"], query_fields=tuple(m["query_fields"]))
+
+
+def layout_of(m):
+    schema = full_schema(m)
+    if m.get("towers"):
+        tw = m["towers"]
+        return S.prerank_layout(schema, tuple(tw["user_fields"]), tuple(tw["ad_fields"]), tw["hidden"],
+                                tw["rep"], m["use_ad_image"])
     agg = S.AggregatorSpec(m["kind"], attention_hidden=m["hidden"], normalize=m["normalize"])
     return S.ModelLayout(schema, agg, tuple(m["mlp_widths"]), m["use_ad_image"],
                          m["use_behavior_images"])
@@ -40,7 +51,8 @@ def oracle_cfg(m):
     return make_cfg(m["fields"], d_id=m["d_id"], d_raw=m["d_raw"], d_img=m["d_img"],
                     b_max=m["b_max"], query_fields=m["query_fields"], kind=m["kind"],
                     normalize=m["normalize"], hidden=m["hidden"], mlp_widths=m["mlp_widths"],
-                    use_ad_image=m["use_ad_image"], use_behavior_images=m["use_behavior_images"])
+                    use_ad_image=m["use_ad_image"], use_behavior_images=m["use_behavior_images"],
+                    towers=m.get("towers"))
 
 
 def samples(fx, bi):

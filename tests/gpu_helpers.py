@@ -11,9 +11,15 @@ from oracle import dicm_oracle as O
 
 
 def device_model(m, pool_rows, pool_dtype="fp32", params=None):
-    from paper_1711_06505_b200.model import DicmModel
+    from paper_1711_06505_b200.model import DicmModel, PrerankModel
     from paper_1711_06505_b200.pool import ImagePool
     lay = G.layout_of(m)
+    if lay.towers is not None:
+        tw = lay.towers
+        model = PrerankModel(G.full_schema(m), None, seed=m["seed"], user_fields=tw.user_fields,
+                             ad_fields=tw.ad_fields, tower_hidden=tw.hidden, rep_dim=tw.rep,
+                             use_images=lay.use_ad_image, params=params)
+        return model, ImagePool.from_rows(pool_rows, dtype=pool_dtype)
     model = DicmModel(lay.schema, lay.aggregator, None, seed=m["seed"], mlp_widths=lay.mlp_widths,
                       use_ad_image=lay.use_ad_image, use_behavior_images=lay.use_behavior_images, params=params)
     pool = ImagePool.from_rows(pool_rows, dtype=pool_dtype)
@@ -62,7 +68,10 @@ def oracle_cfg_of(model):
                       b_max=s.b_max, query_fields=s.query_fields, kind=lay.aggregator.kind,
                       normalize=lay.aggregator.normalize, hidden=lay.aggregator.attention_hidden,
                       mlp_widths=lay.mlp_widths, use_ad_image=lay.use_ad_image,
-                      use_behavior_images=lay.use_behavior_images)
+                      use_behavior_images=lay.use_behavior_images,
+                      towers=None if lay.towers is None else dict(
+                          user_fields=lay.towers.user_fields, ad_fields=lay.towers.ad_fields,
+                          hidden=lay.towers.hidden, rep=lay.towers.rep))
 
 
 def worst(a, b):

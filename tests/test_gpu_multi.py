@@ -12,7 +12,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("kind,precision,mode", [("multiquery-attn", "fp32", "eager"), ("sum", "tf32", "eager"),
-                                                 ("attn", "bf16", "eager"), ("multiquery-attn", "fp32", "graphs")])
+                                                 ("attn", "bf16", "eager"), ("multiquery-attn", "fp32", "graphs"),
+                                                 ("prerank", "fp32", "eager")])
 def test_cluster_matches_oracle_on_union(kind, precision, mode):
     n = torch.cuda.device_count()
     if n < 2:

@@ -78,7 +78,7 @@ def test_oracle_training_matches_reference(name):
         assert np.array_equal(st["t"], fx[f"train/tt/{f}"]), f
 
 
-@pytest.mark.parametrize("name", ["full_sum", "full_mq"])
+@pytest.mark.parametrize("name", ["full_sum", "full_mq", "full_prerank"])
 def test_cluster_equals_single_process_on_union(name):
     """runtime.py:19-21: the distributed step's oracle is LocalTrainer on the
     union batch; the reference cluster (2 workers x 2 servers) agrees with the
