@@ -147,7 +147,8 @@ int dicm_imgmlp_bwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
  *   attention-parameter gradients are written as per-block partial sums.
  * ---------------------------------------------------------------------- */
 typedef struct {
-  int32_t kind;                 /* 0 sum, 1 attn, 2 multiquery-attn, 3 max (segment_max, autograd.py:289-319) */
+  int32_t kind;                 /* 0 sum, 1 attn, 2 multiquery-attn, 3 max (segment_max, autograd.py:289-319),
+                                   4 concat (scatter_concat, autograd.py:370-385: width - pool_col = 12 b_max) */
   int32_t normalize;            /* softmax over scores (model.py:211-214) */
   int32_t use_ad_image;
   int32_t use_behavior_images;
@@ -253,6 +254,21 @@ int dicm_towers_fwd_bwd(const float* head_in, int batch, int width, const dicm_t
 /* forward only (reference forward_prerank, model.py:529-535): logits[b] = score */
 int dicm_towers_fwd(const float* head_in, int batch, int width, const dicm_tower_t* towers, int hidden, int rep,
                     float* logits, dicm_stream_t stream);
+
+/* Wide head input (> 128 columns: the concat aggregator, reference
+ * scatter_concat, autograd.py:370-385): layer 0 runs as fp32 GEMMs, the rest
+ * of the head as in dicm_head_fwd_bwd.  Gradients of the whole mlp/ group are
+ * written (not accumulated) straight into ``grads`` -- the fused buffer's
+ * mlp/ range in sorted order (a0, b0, w0, a1, b1, w1, b2, w2), the same layout
+ * as one head partial row -- and loss_partials feed dicm_loss_finalize. */
+#define DICM_HEAD_MAX_WIDE 16384
+size_t dicm_head_wide_workspace(int batch, int width);
+int dicm_head_wide_fwd_bwd(const float* head_in, int batch, int width, const float* labels,
+                           float inv_denominator, const dicm_head_params_t* p, float* logits,
+                           float* d_head_in, float* grads, float* loss_partials, void* workspace,
+                           size_t workspace_bytes, dicm_stream_t stream);
+int dicm_head_wide_fwd(const float* head_in, int batch, int width, const dicm_head_params_t* p,
+                       float* logits, void* workspace, size_t workspace_bytes, dicm_stream_t stream);
 
 /* partials [nblk, n] -> out[n] (deterministic, fixed order; += if accumulate) */
 int dicm_reduce_partials(const float* partials, int nblk, int64_t n, float* out, int accumulate,

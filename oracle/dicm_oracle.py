@@ -292,6 +292,13 @@ def forward_backward(p, cfg, batch, pool, denominator=None, want_grads=True):
         elif kind == "max":
             pooled, argmax = segment_max(K, beh_seg, B)
             agg_cache = (argmax,)
+        elif kind == "concat":                       # scatter_concat (autograd.py:370-385)
+            pos = np.arange(len(beh_seg)) - np.asarray(batch["beh_off"])[beh_seg]
+            d = cfg["d_img"]
+            pooled = np.zeros((B, cfg["b_max"] * d))
+            cols = pos[:, None] * d + np.arange(d)[None, :]
+            np.add.at(pooled, (beh_seg[:, None], cols), K)
+            agg_cache = (cols,)
         elif kind == "attn":
             pooled, c1 = attention_fwd(p, "attn/img/", ad_vec, K, beh_seg, B, cfg["normalize"])
             agg_cache = (c1,)
@@ -354,6 +361,8 @@ def forward_backward(p, cfg, batch, pool, denominator=None, want_grads=True):
         kind = cfg["kind"]
         if kind == "sum":
             dK = dpool[beh_seg]
+        elif kind == "concat":
+            dK = dpool[beh_seg[:, None], agg_cache[0]]
         elif kind == "max":                          # segment_max bwd (autograd.py:307-315)
             dK = np.zeros_like(K)
             argmax = agg_cache[0]

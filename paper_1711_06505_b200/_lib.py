@@ -177,6 +177,9 @@ _sig("dicm_jsonl_parse", P, C.c_char_p, I64, C.POINTER(JsonlSpec), C.c_int, C.PO
 _sig("dicm_jsonl_list_total", I64, P, C.c_int)
 _sig("dicm_jsonl_export", C.c_int, P, C.c_int, P, P, P)
 _sig("dicm_jsonl_free", None, P)
+_sig("dicm_head_wide_workspace", S, C.c_int, C.c_int)
+_sig("dicm_head_wide_fwd_bwd", C.c_int, P, C.c_int, C.c_int, P, F, C.POINTER(HeadParams), P, P, P, P, P, S, ST)
+_sig("dicm_head_wide_fwd", C.c_int, P, C.c_int, C.c_int, C.POINTER(HeadParams), P, P, S, ST)
 _sig("dicm_towers_blocks", C.c_int, C.c_int)
 _sig("dicm_towers_fwd_bwd", C.c_int, P, C.c_int, C.c_int, C.POINTER(Tower), C.c_int, C.c_int, P, F, P, P, P, I64, P,
      ST)
@@ -206,7 +209,8 @@ EXPORTED = [
     "dicm_p2p_alloc", "dicm_p2p_free", "dicm_ipc_handle", "dicm_ipc_open", "dicm_ipc_close", "dicm_p2p_barrier",
     "dicm_p2p_counts", "dicm_p2p_plan", "dicm_p2p_scatter", "dicm_dedup_devn", "dicm_head_fwd",
     "dicm_attn_keyproj", "dicm_jsonl_parse", "dicm_jsonl_list_total", "dicm_jsonl_export", "dicm_jsonl_free",
-    "dicm_towers_blocks", "dicm_towers_fwd_bwd", "dicm_towers_fwd",
+    "dicm_towers_blocks", "dicm_towers_fwd_bwd", "dicm_towers_fwd", "dicm_head_wide_workspace",
+    "dicm_head_wide_fwd_bwd", "dicm_head_wide_fwd",
 ]
 
 

@@ -47,6 +47,12 @@ __device__ __forceinline__ void load32(const float* p, float (&v)[BT]) {
   }
 }
 
+// WIDE: the input is wider than the shared-memory-resident W0 allows (the
+// concat aggregator); layer 0 then runs as separate GEMMs (k_sgemm below):
+// ``x`` holds the layer-0 pre-activations [B][H0] on entry, and on exit
+// ``dx`` receives da0 [B][H0] instead of dLoss/dx.  The partial row then
+// omits the w0 block (o_w0 has zero length).
+template <bool WIDE>
 __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, int B, int W,
                                                   const float* __restrict__ labels, float inv_denom,
                                                   dicm_head_params_t p, float* __restrict__ logits,
@@ -57,16 +63,23 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
   const int t = threadIdx.x;
   const int b0 = blockIdx.x * BT;
   const int nb = min(BT, B - b0);
-  for (int i = t; i < H0 * W; i += THREADS) s.w0[i] = p.w0[i];
-  for (int i = t; i < H1 * H0; i += THREADS) s.w1[i] = p.w1[i];
-  for (int i = t; i < BT * W; i += THREADS) {
-    const int r = i / W, c = i % W;
-    s.xs[c][r] = r < nb ? x[(int64_t)(b0 + r) * W + c] : 0.f;
+  if (!WIDE) {
+    for (int i = t; i < H0 * W; i += THREADS) s.w0[i] = p.w0[i];
+    for (int i = t; i < BT * W; i += THREADS) {
+      const int r = i / W, c = i % W;
+      s.xs[c][r] = r < nb ? x[(int64_t)(b0 + r) * W + c] : 0.f;
+    }
+  } else {
+    for (int i = t; i < BT * H0; i += THREADS) {
+      const int r = i / H0, j = i % H0;
+      s.a0[j][r] = r < nb ? x[(int64_t)(b0 + r) * H0 + j] : 0.f;
+    }
   }
+  for (int i = t; i < H1 * H0; i += THREADS) s.w1[i] = p.w1[i];
   __syncthreads();
 
   // layer 0: thread = unit j
-  {
+  if (!WIDE) {
     const int j = t;
     float acc[BT];
     const float bj = p.b0[j];
@@ -117,8 +130,9 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
   }
   __syncthreads();
   if (!labels) return;  // forward only: no loss, no backward
-  float* out = part + (int64_t)blockIdx.x * part_size(W);
-  const int64_t o_a0 = 0, o_b0 = H0, o_w0 = 2 * H0, o_a1 = o_w0 + (int64_t)H0 * W, o_b1 = o_a1 + H1,
+  const int64_t w0len = WIDE ? 0 : (int64_t)H0 * W;
+  float* out = part + (int64_t)blockIdx.x * (part_size(W) - (WIDE ? (int64_t)H0 * W : 0));
+  const int64_t o_a0 = 0, o_b0 = H0, o_w0 = 2 * H0, o_a1 = o_w0 + w0len, o_b1 = o_a1 + H1,
                 o_w1 = o_b1 + H1, o_b2 = o_w1 + (int64_t)H1 * H0, o_w2 = o_b2 + 1;
   if (t == 0) {
     float l = 0.f, d = 0.f;
@@ -198,6 +212,13 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
     out[o_b0 + k] = sb;
   }
   __syncthreads();
+  if (WIDE) {  // da0 rows for the dW0 / dx GEMMs
+    for (int i = t; i < nb * H0; i += THREADS) {
+      const int r = i / H0, j = i % H0;
+      dx[(int64_t)(b0 + r) * H0 + j] = s.da0[j][r];
+    }
+    return;
+  }
   // dW0[k][c] = sum_r da0[r][k] x[r][c]: thread = k
   {
     const int k = t;
@@ -226,6 +247,98 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
     }
     for (int r = 0; r < nb; ++r) dx[(int64_t)(b0 + r) * W + c] = acc[r];
   }
+}
+
+// ---------------------------------------------------------------------------
+// wide head (concat aggregator): layer 0 as fp32 GEMMs on the CUDA cores.
+// C[m][n] = sum_k A(m,k) B(k,n) (+ bias[n]) with A(m,k) = A[m*sam + k*sak],
+// B(k,n) = B[k*sbk + n*sbn]: 64x64 tiles, 16-deep k slices staged in shared
+// memory, 4x4 outputs per thread, every output summed in k order by one thread
+// (deterministic).  Covers a0 = X W0^T + b0, dW0 = da0^T X and dX = da0 W0.
+// ---------------------------------------------------------------------------
+constexpr int GB = 64, GK = 16;
+
+__global__ void __launch_bounds__(256) k_sgemm(int M, int N, int K, const float* __restrict__ A, int64_t sam,
+                                               int64_t sak, const float* __restrict__ Bm, int64_t sbk, int64_t sbn,
+                                               const float* __restrict__ bias, float* __restrict__ C, int64_t ldc) {
+  __shared__ float As[GK][GB + 4], Bs[GK][GB + 4];
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  const int m0 = blockIdx.y * GB, n0 = blockIdx.x * GB;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += GK) {
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int i = t + l * 256;
+      // walk the unit-stride dimension with consecutive threads
+      const int am = sak == 1 ? i / GK : i % GB, ak = sak == 1 ? i % GK : i / GB;
+      const int bn = sbn == 1 ? i % GB : i / GK, bk = sbn == 1 ? i / GB : i % GK;
+      const int gm = m0 + am, gk = k0 + ak;
+      As[ak][am] = (gm < M && gk < K) ? __ldg(A + gm * sam + gk * sak) : 0.f;
+      const int gn = n0 + bn, gk2 = k0 + bk;
+      Bs[bk][bn] = (gn < N && gk2 < K) ? __ldg(Bm + gk2 * sbk + gn * sbn) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty + 16 * i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx + 16 * j;
+      if (n < N) C[m * ldc + n] = acc[i][j] + (bias ? __ldg(bias + n) : 0.f);
+    }
+  }
+}
+
+void sgemm(cudaStream_t st, int M, int N, int K, const float* A, int64_t sam, int64_t sak, const float* Bm,
+           int64_t sbk, int64_t sbn, const float* bias, float* C, int64_t ldc) {
+  dim3 grid((N + GB - 1) / GB, (M + GB - 1) / GB);
+  k_sgemm<<<grid, 256, 0, st>>>(M, N, K, A, sam, sak, Bm, sbk, sbn, bias, C, ldc);
+}
+
+// out[c] = sum over blocks (in order) of part[blk * stride + col0 + c]
+__global__ void k_reduce_cols(const float* __restrict__ part, int nblk, int64_t stride, int64_t col0, int64_t n,
+                              float* __restrict__ out) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int b = 0; b < nblk; ++b) acc += part[b * stride + col0 + c];
+    out[c] = acc;
+  }
+}
+
+struct WideWs {
+  float *a0, *da0, *part;
+  int64_t prow;
+};
+
+size_t wide_carve(int batch, int W, void* base, WideWs* w) {
+  const int64_t B = batch > 0 ? batch : 1;
+  const int nblk = (int)((B + BT - 1) / BT);
+  const int64_t prow = part_size(W) - (int64_t)H0 * W;
+  const size_t n_a = (size_t)B * H0 * sizeof(float);
+  const size_t n_p = (size_t)nblk * prow * sizeof(float);
+  if (w) {
+    char* p = (char*)base;
+    w->a0 = (float*)p;
+    w->da0 = (float*)(p + n_a);
+    w->part = (float*)(p + 2 * n_a);
+    w->prow = prow;
+  }
+  return 2 * n_a + n_p;
 }
 
 __global__ void k_loss_finalize(const float* __restrict__ part, int n, float scale, float* __restrict__ out,
@@ -272,12 +385,12 @@ int dicm_head_fwd_bwd(const float* head_in, int batch, int width, const float* l
   const size_t smem = sizeof(Smem);
   static bool attr = false;
   if (!attr) {
-    int rc = check_cuda(cudaFuncSetAttribute(k_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+    int rc = check_cuda(cudaFuncSetAttribute(k_head<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                         "head smem attribute");
     if (rc) return rc;
     attr = true;
   }
-  k_head<<<dicm_head_blocks(batch), THREADS, smem, (cudaStream_t)stream>>>(
+  k_head<false><<<dicm_head_blocks(batch), THREADS, smem, (cudaStream_t)stream>>>(
       head_in, batch, width, labels, inv_denominator, *p, logits, d_head_in, partials, loss_partials);
   return last_launch("dicm_head_fwd_bwd");
 }
@@ -288,12 +401,69 @@ int dicm_head_fwd(const float* head_in, int batch, int width, const dicm_head_pa
   if (width < 1 || width > MAXW) return fail(DICM_ERR_UNSUPPORTED, "head: input width %d not in [1, %d]", width, MAXW);
   if (batch <= 0) return DICM_OK;
   const size_t smem = sizeof(Smem);
-  static int attr = check_cuda(cudaFuncSetAttribute(k_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+  static int attr = check_cuda(cudaFuncSetAttribute(k_head<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                                "head smem attribute");
   if (attr) return attr;
-  k_head<<<dicm_head_blocks(batch), THREADS, smem, (cudaStream_t)stream>>>(head_in, batch, width, nullptr, 0.f, *p,
+  k_head<false><<<dicm_head_blocks(batch), THREADS, smem, (cudaStream_t)stream>>>(head_in, batch, width, nullptr, 0.f, *p,
                                                                          logits, nullptr, nullptr, nullptr);
   return last_launch("dicm_head_fwd");
+}
+
+size_t dicm_head_wide_workspace(int batch, int width) { return wide_carve(batch, width, nullptr, nullptr); }
+
+int dicm_head_wide_fwd_bwd(const float* head_in, int batch, int width, const float* labels, float inv_denominator,
+                           const dicm_head_params_t* p, float* logits, float* d_head_in, float* grads,
+                           float* loss_partials, void* workspace, size_t workspace_bytes, dicm_stream_t stream) {
+  using namespace dicm;
+  if (width < 1 || width > DICM_HEAD_MAX_WIDE)
+    return fail(DICM_ERR_UNSUPPORTED, "head: input width %d not in [1, %d]", width, DICM_HEAD_MAX_WIDE);
+  if (!labels) return fail(DICM_ERR_VALUE, "dicm_head_wide_fwd_bwd: labels required");
+  if (batch <= 0) return DICM_OK;
+  if (workspace_bytes < wide_carve(batch, width, nullptr, nullptr))
+    return fail(DICM_ERR_VALUE, "dicm_head_wide_fwd_bwd: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  WideWs w;
+  wide_carve(batch, width, workspace, &w);
+  const size_t smem = sizeof(Smem);
+  static int attr = check_cuda(cudaFuncSetAttribute(k_head<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)smem), "head smem attribute");
+  if (attr) return attr;
+  const int W = width;
+  // a0 = X W0^T + b0
+  sgemm(st, batch, H0, W, head_in, W, 1, p->w0, 1, W, p->b0, w.a0, H0);
+  const int nblk = dicm_head_blocks(batch);
+  k_head<true><<<nblk, THREADS, smem, st>>>(w.a0, batch, W, labels, inv_denominator, *p, logits, w.da0, w.part,
+                                            loss_partials);
+  // partial rows [a0 b0 | a1 b1 w1 b2 w2] -> the mlp/ gradient range around w0
+  const int64_t rest = w.prow - 2 * H0;
+  k_reduce_cols<<<1, 2 * H0, 0, st>>>(w.part, nblk, w.prow, 0, 2 * H0, grads);
+  k_reduce_cols<<<(int)((rest + 255) / 256), 256, 0, st>>>(w.part, nblk, w.prow, 2 * H0, rest,
+                                                           grads + 2 * H0 + (int64_t)H0 * W);
+  // dW0 = da0^T X  -> grads[2 H0 ..), dX = da0 W0
+  sgemm(st, H0, W, batch, w.da0, 1, H0, head_in, W, 1, nullptr, grads + 2 * H0, W);
+  sgemm(st, batch, W, H0, w.da0, H0, 1, p->w0, W, 1, nullptr, d_head_in, W);
+  return last_launch("dicm_head_wide_fwd_bwd");
+}
+
+int dicm_head_wide_fwd(const float* head_in, int batch, int width, const dicm_head_params_t* p, float* logits,
+                       void* workspace, size_t workspace_bytes, dicm_stream_t stream) {
+  using namespace dicm;
+  if (width < 1 || width > DICM_HEAD_MAX_WIDE)
+    return fail(DICM_ERR_UNSUPPORTED, "head: input width %d not in [1, %d]", width, DICM_HEAD_MAX_WIDE);
+  if (batch <= 0) return DICM_OK;
+  if (workspace_bytes < wide_carve(batch, width, nullptr, nullptr))
+    return fail(DICM_ERR_VALUE, "dicm_head_wide_fwd: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  WideWs w;
+  wide_carve(batch, width, workspace, &w);
+  const size_t smem = sizeof(Smem);
+  static int attr = check_cuda(cudaFuncSetAttribute(k_head<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)smem), "head smem attribute");
+  if (attr) return attr;
+  sgemm(st, batch, H0, width, head_in, width, 1, p->w0, 1, width, p->b0, w.a0, H0);
+  k_head<true><<<dicm_head_blocks(batch), THREADS, smem, st>>>(w.a0, batch, width, nullptr, 0.f, *p, logits, nullptr,
+                                                              nullptr, nullptr);
+  return last_launch("dicm_head_wide_fwd");
 }
 
 int dicm_loss_finalize(const float* loss_partials, int nblk, float scale, float* loss_out, int32_t* status,

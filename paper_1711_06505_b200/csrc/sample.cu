@@ -352,6 +352,17 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, 2) k_sample_fwd(const __grid_c
     if (a.L.use_ad_image && lane < DICM_D)
       row[a.L.ad_col + lane] = __ldg(a.V.emb + (int64_t)a.V.ad_local[b] * DICM_D + lane);
     if (!a.L.use_behavior_images) continue;
+    if (a.L.kind == 4) {  // concat (reference scatter_concat, autograd.py:370-385): slot j = j-th kept behavior
+      const int64_t i0 = a.V.beh_off[b];
+      const int len = (int)(a.V.beh_off[b + 1] - i0);
+      const int n = a.L.width - a.L.pool_col;  // capacity * 12
+      for (int e = lane; e < n; e += 32) {
+        const int j = e / DICM_D;
+        row[a.L.pool_col + e] = j < len ? __ldg(a.V.emb + (int64_t)__ldg(a.V.beh_local + i0 + j) * DICM_D + e % DICM_D)
+                                        : 0.f;
+      }
+      continue;
+    }
     if (a.L.kind == 3) {  // max pooling (reference segment_max, autograd.py:289-319)
       float m[DICM_D];
       int am[DICM_D];
@@ -647,6 +658,13 @@ __global__ void __launch_bounds__(BWD_WARPS * 32, 4) k_sample_scatter(const __gr
       load12(drow + a.L.pool_col, dv);
       seg_scatter(a.V.beh_local, a.V.beh_off[b], a.V.beh_off[b + 1], a.d_emb, dv, lane);
     }
+    if (a.L.use_behavior_images && a.L.kind == 4) {  // concat: slot j's gradient to its row
+      const int64_t i0 = a.V.beh_off[b];
+      const int n = min((int)(a.V.beh_off[b + 1] - i0) * DICM_D, a.L.width - a.L.pool_col);
+      for (int e = lane; e < n; e += 32)
+        atomicAdd(a.d_emb + (int64_t)__ldg(a.V.beh_local + i0 + e / DICM_D) * DICM_D + e % DICM_D,
+                  __ldg(drow + a.L.pool_col + e));
+    }
     if (a.L.use_behavior_images && a.L.kind == 3) {  // gradient to the first argmax row of each column
       float m[DICM_D];
       int am[DICM_D];
@@ -678,7 +696,7 @@ size_t bwd_smem() {
 }
 
 int64_t part_size(const dicm_layout_t* L) {
-  if (!L->use_behavior_images || L->kind == 0 || L->kind == 3) return 0;
+  if (!L->use_behavior_images || L->kind == 0 || L->kind >= 3) return 0;
   int64_t n = chan_part(DICM_D);
   if (L->kind == 2) n += chan_part(DICM_D * L->n_query);
   return n;
@@ -686,7 +704,9 @@ int64_t part_size(const dicm_layout_t* L) {
 
 int validate(const dicm_layout_t* L, const dicm_batch_view_t* V) {
   if (L->n_fields < 0 || L->n_fields > DICM_MAX_FIELDS) return fail(DICM_ERR_VALUE, "sample: %d fields (max 8)", L->n_fields);
-  if (L->kind < 0 || L->kind > 3) return fail(DICM_ERR_UNSUPPORTED, "sample: aggregator kind %d", L->kind);
+  if (L->kind < 0 || L->kind > 4) return fail(DICM_ERR_UNSUPPORTED, "sample: aggregator kind %d", L->kind);
+  if (L->kind == 4 && L->use_behavior_images && (L->width - L->pool_col) % DICM_D)
+    return fail(DICM_ERR_VALUE, "concat: pooled width %d is not a multiple of 12", L->width - L->pool_col);
   if ((L->kind == 1 || L->kind == 2) && L->use_behavior_images && !L->use_ad_image)
     return fail(DICM_ERR_VALUE, "attentive aggregator needs the ad image as query");
   if (L->kind == 2 && (L->n_query < 1 || L->n_query > 2))

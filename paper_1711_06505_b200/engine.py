@@ -30,7 +30,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from .model import KIND_CODE
+from .model import HEAD_SMEM_WIDTH, KIND_CODE
 
 BETA1, BETA2, EPS = 0.9, 0.999, 1e-8  # reference optim.py:16-19
 
@@ -123,6 +123,7 @@ class Prefetcher:
         def work():
             try:
                 for b in batches:
+                    engine._check_capacity(b)
                     pk = Packed(engine.model, b)
                     host = torch.empty(max(pk.total, 1), dtype=torch.int32, pin_memory=True)
                     pk.fill(engine.model, b, host.numpy())
@@ -289,12 +290,26 @@ class StepEngine:
     def _head_blocks(self, B):
         return L.lib.dicm_towers_blocks(B) if self.model.layout.towers else L.lib.dicm_head_blocks(B)
 
+    @property
+    def wide_head(self):
+        """Head input too wide for the shared-memory W0 (concat aggregator):
+        layer 0 runs as GEMMs and the mlp/ gradients land directly in
+        ``self.grad`` (dicm_head_wide_fwd_bwd)."""
+        return self.model.layout.towers is None and self.width > HEAD_SMEM_WIDTH
+
     def _head_fwd_bwd(self, B, denom):
         """a11-a12: MLP head (or the two towers) + BCE -> logits, d_head_in,
         gradient partials, loss partials."""
         pk, s = self.pk, self.s
         tw = self.model.layout.towers
-        if tw is None:
+        if self.wide_head:
+            h0, _ = self.head_range
+            L.check(L.lib.dicm_head_wide_fwd_bwd(self.head_in.data_ptr(), B, self.width, self._dptr(pk.labels),
+                                                 1.0 / denom, C.byref(self.head_p), self.logits.data_ptr(),
+                                                 self.d_head_in.data_ptr(), self.grad.data_ptr() + 4 * h0,
+                                                 self.loss_part.data_ptr(), self.head_ws.data_ptr(),
+                                                 self.head_ws.numel(), s))
+        elif tw is None:
             L.check(L.lib.dicm_head_fwd_bwd(self.head_in.data_ptr(), B, self.width, self._dptr(pk.labels),
                                             1.0 / denom, C.byref(self.head_p), self.logits.data_ptr(),
                                             self.d_head_in.data_ptr(), self.head_part.data_ptr(),
@@ -307,7 +322,11 @@ class StepEngine:
 
     def _head_fwd(self, B):
         tw = self.model.layout.towers
-        if tw is None:
+        if self.wide_head:
+            L.check(L.lib.dicm_head_wide_fwd(self.head_in.data_ptr(), B, self.width, C.byref(self.head_p),
+                                             self.logits.data_ptr(), self.head_ws.data_ptr(), self.head_ws.numel(),
+                                             self.s))
+        elif tw is None:
             L.check(L.lib.dicm_head_fwd(self.head_in.data_ptr(), B, self.width, C.byref(self.head_p),
                                         self.logits.data_ptr(), self.s))
         else:
@@ -386,7 +405,12 @@ class StepEngine:
         self.logits = torch.empty(max(B, 1), **f32)
         self.scores = torch.empty((2, max(R, 1)), **f32)
         self.stats = torch.empty((2, max(B, 1), 2), **f32)
-        self.head_part = torch.empty((self._head_blocks(max(B, 1)), self.head_range[1] - self.head_range[0]), **f32)
+        if self.wide_head:  # no per-block partial rows: the GEMMs write the gradients
+            self.head_part = torch.empty((1, 1), **f32)
+            self.head_ws = _u8(L.lib.dicm_head_wide_workspace(max(B, 1), self.width), dev)
+        else:
+            self.head_part = torch.empty((self._head_blocks(max(B, 1)), self.head_range[1] - self.head_range[0]),
+                                         **f32)
         self.loss_part = torch.empty(self._head_blocks(max(B, 1)), **f32)
         self.attn_partial = torch.empty((L.lib.dicm_sample_blocks(max(B, 1)), max(self.attn_part, 1)), **f32)
         self.loss = torch.zeros(1, **f32)
@@ -421,10 +445,21 @@ class StepEngine:
         return i, buf
 
     # ------------------------------------------------------------------
+    def _check_capacity(self, batch):
+        """concat: every kept behavior needs a slot (reference scatter_concat
+        raises ShapeError for pos >= capacity, autograd.py:375-376)."""
+        lay = self.model.layout
+        if lay.aggregator.kind == "concat" and lay.use_behavior_images and batch.size:
+            longest = int(np.max(np.diff(np.asarray(batch.beh_off))))
+            if longest > lay.schema.b_max:
+                raise ValueError(f"scatter_concat: slot out of range for capacity {lay.schema.b_max} "
+                                 f"(a sample has {longest} behaviors)")
+
     def upload(self, batch, own=False):
         """H2D of one batch (async).  ``own=True`` gives the batch its own
         device buffer (pre-staged inputs); otherwise the engine's buffer is
         reused."""
+        self._check_capacity(batch)
         pk = Packed(self.model, batch)
         self._ensure(pk)
         dst = torch.empty(max(pk.total, 1), dtype=torch.int32, device=self.dev) if own else self.packed
@@ -552,8 +587,9 @@ class StepEngine:
                                       self.d_head_in.data_ptr(), self.scores.data_ptr(), self.stats.data_ptr(),
                                       d_emb.data_ptr(), self.d_rows.data_ptr(), self.attn_partial.data_ptr(), s))
         h0, h1 = self.head_range
-        L.check(L.lib.dicm_reduce_partials(self.head_part.data_ptr(), nhb, h1 - h0,
-                                           self.grad.data_ptr() + 4 * h0, 0, s))
+        if not self.wide_head:
+            L.check(L.lib.dicm_reduce_partials(self.head_part.data_ptr(), nhb, h1 - h0,
+                                               self.grad.data_ptr() + 4 * h0, 0, s))
         if self.attn_range is not None:
             a0, a1 = self.attn_range
             L.check(L.lib.dicm_reduce_partials(self.attn_partial.data_ptr(), L.lib.dicm_sample_blocks(B), a1 - a0,
@@ -750,6 +786,8 @@ class StepEngine:
         else:
             n += 2 + 1 + 2 + 1 + (1 if lay.attentive else 0) + 1 + 4 + 11
         n += 1 + 1 + 1  # sample fwd, head, loss
+        if self.wide_head:
+            n += 3 + 2 - 1  # layer-0 GEMMs + two column reduces instead of the partial reduce
         n += 1 + 4 + 1  # check_finite, adam dense (memset + 3), adam rows
         return n
 

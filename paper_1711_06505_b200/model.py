@@ -23,7 +23,9 @@ import torch
 from . import schema as S
 from .schema import AggregatorSpec, FeatureSchema, FieldSpec, ModelLayout  # noqa: F401
 
-KIND_CODE = {"sum": 0, "attn": 1, "multiquery-attn": 2, "max": 3}
+KIND_CODE = {"sum": 0, "attn": 1, "multiquery-attn": 2, "max": 3, "concat": 4}
+HEAD_SMEM_WIDTH = 128   # widest head input whose W0 stays in shared memory (csrc/head.cu)
+HEAD_MAX_WIDE = 16384   # DICM_HEAD_MAX_WIDE
 
 
 class Parameter:
@@ -68,8 +70,8 @@ def check_hot_path(layout):
         raise NotImplementedError("kernels are built for the (128, 64) head")
     if layout.attentive and layout.aggregator.attention_hidden != 32:
         raise NotImplementedError("kernels are built for a 32-unit attention net")
-    if layout.mlp_input_width() > 128:
-        raise NotImplementedError(f"head input width {layout.mlp_input_width()} > 128")
+    if layout.mlp_input_width() > HEAD_MAX_WIDE:
+        raise NotImplementedError(f"head input width {layout.mlp_input_width()} > {HEAD_MAX_WIDE}")
     if len(s.fields) > 8:
         raise NotImplementedError("at most 8 ID fields")
     if layout.multiquery:

@@ -23,7 +23,7 @@ import numpy as np
 
 AGGREGATOR_KINDS = ("concat", "max", "sum", "attn", "multiquery-attn")
 # aggregators built on the B200 hot path
-HOT_PATH_AGGREGATORS = ("sum", "attn", "multiquery-attn", "max")
+HOT_PATH_AGGREGATORS = ("sum", "attn", "multiquery-attn", "max", "concat")
 
 GROUP_ID = "id-embeddings"
 GROUP_IMAGE = "image-embedding-model"

@@ -225,7 +225,7 @@ def main():
         bs = make_samples(trng, 6, {"user": 5, "scenario": 1, "ad": 7, "ad_category": 1,
                                     "behavior_items": 1}, 10, 6, empty_every=4)
         tiny_batches.append(bs)
-    for kind in ("sum", "attn", "multiquery-attn", "max"):
+    for kind in ("sum", "attn", "multiquery-attn", "max", "concat"):
         if os.environ.get("GOLDEN_ONLY") and f"tiny_{kind}" not in os.environ["GOLDEN_ONLY"].split(","):
             continue
         run_case(f"tiny_{kind}", tiny_case(kind), tiny_pool, tiny_batches)
@@ -245,7 +245,8 @@ def main():
     for kind, norm, use_ad, tag in (("sum", True, True, "sum"), ("attn", True, True, "attn"),
                                     ("attn", False, True, "attn_raw"),
                                     ("multiquery-attn", True, True, "mq"),
-                                    ("sum", True, False, "sum_noad"), ("max", True, True, "max")):
+                                    ("sum", True, False, "sum_noad"), ("max", True, True, "max"),
+                                    ("concat", True, True, "concat")):
         if os.environ.get("GOLDEN_ONLY") and f"full_{tag}" not in os.environ["GOLDEN_ONLY"].split(","):
             continue
         case, vocabs = full_case(kind, norm, use_ad)

@@ -13,8 +13,9 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 BIG = 50_000
 PROBE_SEED = 1234
 
-TINY = ["tiny_sum", "tiny_attn", "tiny_multiquery-attn", "tiny_max", "tiny_prerank"]
-FULL = ["full_sum", "full_attn", "full_attn_raw", "full_mq", "full_sum_noad", "full_max", "full_prerank",
+TINY = ["tiny_sum", "tiny_attn", "tiny_multiquery-attn", "tiny_max", "tiny_concat", "tiny_prerank"]
+FULL = ["full_sum", "full_attn", "full_attn_raw", "full_mq", "full_sum_noad", "full_max", "full_concat",
+        "full_prerank",
         "full_prerank_img_ids", "full_prerank_noimg"]
 
 

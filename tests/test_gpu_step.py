@@ -143,7 +143,7 @@ def _bench_like(kind, B=256, L=50, P=3000, vocab=20_000, seed=0, lengths=None, z
     return model, pool, batch
 
 
-@pytest.mark.parametrize("kind", ["sum", "attn", "multiquery-attn", "max"])
+@pytest.mark.parametrize("kind", ["sum", "attn", "multiquery-attn", "max", "concat"])
 def test_bench_shape_step_matches_oracle(kind):
     """cfg-1-like shapes (B=256, L=50, 4096-d pool) against the oracle."""
     from paper_1711_06505_b200.engine import StepEngine
@@ -250,3 +250,40 @@ def test_graphed_steps_match_eager(kind):
         d = np.abs(s1[n] - s0[n])
         off = d > 1e-5 * np.abs(s0[n]) + 1e-6
         assert (_noise(n) or off.mean() <= 1e-3) and d.max() <= 2 * 1e-4 * 4, (n, off.mean(), d.max())
+
+
+@pytest.mark.parametrize("L", [2, 9])
+def test_concat_narrow_and_wide_heads_match_oracle(L):
+    """concat (reference scatter_concat, autograd.py:370-385): b_max = 2 keeps
+    the head input at 120 columns (shared-memory W0, csrc/head.cu k_head);
+    b_max = 9 makes it 204 (layer-0 GEMMs, dicm_head_wide_fwd_bwd).  Rows
+    shorter than b_max leave zero slots; empty rows included."""
+    from paper_1711_06505_b200.engine import StepEngine
+    rng = np.random.default_rng(3)
+    lengths = rng.integers(0, L + 1, 96)
+    lengths[:3] = (0, L, 1)
+    model, pool, _ = _bench_like("concat", B=4, L=L, P=700)
+    from paper_1711_06505_b200.batch import synthetic_batch
+    batch = synthetic_batch(rng, model.schema, 96, lengths, 700)
+    e = StepEngine(model, pool, "fp32")
+    assert e.wide_head == (L == 9)
+    params = H.host_params(model)
+    loss = e.forward_backward(e.upload(batch))
+    torch.cuda.synchronize()
+    e.raise_status()
+    out = O.forward_backward(params, H.oracle_cfg_of(model), H.oracle_batch(batch), pool.rows.double().cpu().numpy())
+    assert O.rel_err(loss.item(), out["loss"]) < FP32_TOL
+    assert O.rel_err(e.logits[:batch.size].cpu().numpy(), out["logits"]) < FP32_TOL
+    for n, g in H.dense_grads(e).items():
+        assert O.rel_err(g, out["grads"][n]) < FP32_TOL, n
+    for f, (ids, rows_) in H.table_grads(e).items():
+        assert O.rel_err(rows_, out["tgrads"][f][1]) < FP32_TOL, f
+
+
+def test_concat_rejects_rows_beyond_capacity():
+    from paper_1711_06505_b200.engine import StepEngine
+    model, pool, batch = _bench_like("concat", B=16, L=4, P=300)
+    e = StepEngine(model, pool, "fp32")
+    _, _, long_batch = _bench_like("concat", B=16, L=6, P=300)
+    with pytest.raises(ValueError, match="capacity"):
+        e.upload(long_batch)
