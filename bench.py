@@ -409,12 +409,17 @@ def main():
         barrier()
         s2, e2_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s2.record()
+        t_cpu = time.perf_counter()
         for i, b in enumerate(host):
             loss = cluster.train_batch_async(b, union)
             pinned_loss[i:i + 1].copy_(loss, non_blocking=True)
+        t_cpu = time.perf_counter() - t_cpu
         e2_.record()
         barrier()
         ems = s2.elapsed_time(e2_)
+        if os.environ.get("DICM_E2E_DEBUG") and rank == 0:
+            print(f"e2e: cpu enqueue {1e3 * t_cpu / len(host):.3f} ms/step, device {ems / len(host):.3f} ms/step",
+                  flush=True)
         eng.raise_status()
         te = torch.tensor([ems], device="cuda")
         if world > 1:

@@ -417,6 +417,12 @@ void* dicm_jsonl_parse(const char* buf, int64_t len, const dicm_jsonl_spec_t* sp
 int64_t dicm_jsonl_list_total(void* handle, int key);
 int dicm_jsonl_export(void* handle, int key, int32_t* values, int32_t* offsets, float* labels);
 void dicm_jsonl_free(void* handle);
+/* Host-side packing of a batch's columns into the pinned upload buffer on
+ * several threads (replaces the per-column copies behind the reference's
+ * encode_batch arrays, model.py:158-198): segment i = bytes[i] bytes from
+ * srcs[i] to (char*)dst + dst_off[i]. */
+int dicm_host_pack(void* dst, const void* const* srcs, const int64_t* bytes, const int64_t* dst_off, int n,
+                   int nthreads);
 
 /* ------------------------------------------------------------------------
  * Timing probe (instrumentation, no reference counterpart): while enabled,

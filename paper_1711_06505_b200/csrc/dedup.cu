@@ -38,25 +38,44 @@ __device__ __forceinline__ int find_seg(const Segs& s, int64_t i) {
   return k;
 }
 
+// Keys that share a bitmap word within a warp are combined first (one
+// atomicOr per distinct word and warp): small-vocabulary fields (scenario,
+// ad_category: a handful of ids over the whole batch) would otherwise queue
+// thousands of atomics on one word.
 __global__ void k_mark(const __grid_constant__ Segs segs, uint32_t* __restrict__ bitmap, int tag,
                        int32_t* __restrict__ status) {
   const int64_t total = seg_total(segs);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int s = find_seg(segs, i);
-    const int64_t id = segs.ids[s][i - segs.start[s]];
-    if (id < 0 || id >= segs.vocab[s]) {
-      if (atomicCAS(&status[DICM_ST_KEY_FLAG], 0, 1) == 0) {
-        status[DICM_ST_KEY_VALUE] = (int32_t)id;
-        status[DICM_ST_KEY_SEG] = tag * 16 + s;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; i0 < total; i0 += stride) {
+    const int64_t i = i0 + lane;
+    uint32_t w = 0xffffffffu, bit = 0;
+    if (i < total) {
+      const int s = find_seg(segs, i);
+      const int64_t id = segs.ids[s][i - segs.start[s]];
+      if (id < 0 || id >= segs.vocab[s]) {
+        if (atomicCAS(&status[DICM_ST_KEY_FLAG], 0, 1) == 0) {
+          status[DICM_ST_KEY_VALUE] = (int32_t)id;
+          status[DICM_ST_KEY_SEG] = tag * 16 + s;
+        }
+      } else {
+        const uint32_t key = (uint32_t)(segs.base[s] + id);
+        w = key >> 5;
+        bit = 1u << (key & 31);
       }
-      continue;
     }
-    const uint32_t key = (uint32_t)(segs.base[s] + id);
-    const uint32_t bit = 1u << (key & 31);
-    uint32_t* w = bitmap + (key >> 5);
-    // test before set: hot keys (Zipf) would otherwise serialize on one word
-    if ((__ldcg(w) & bit) == 0) atomicOr(w, bit);
+    const unsigned peers = __match_any_sync(0xffffffffu, w);
+    uint32_t bits = 0;
+#pragma unroll 8
+    for (int src = 0; src < 32; ++src) {
+      const uint32_t b = __shfl_sync(0xffffffffu, bit, src);
+      if ((peers >> src) & 1u) bits |= b;
+    }
+    if (w != 0xffffffffu && lane == __ffs(peers) - 1) {
+      uint32_t* p = bitmap + w;
+      // test before set: hot words are already complete after their first wave
+      if ((__ldcg(p) & bits) != bits) atomicOr(p, bits);
+    }
   }
 }
 

@@ -293,4 +293,34 @@ int dicm_jsonl_export(void* h, int key, int32_t* vals, int32_t* offsets, float* 
 
 void dicm_jsonl_free(void* h) { delete static_cast<Parsed*>(h); }
 
+// Packs n host segments into one buffer (the pinned upload staging of a
+// batch): segment i = bytes[i] bytes from srcs[i] to dst + dst_off[i].  The
+// total is cut into equal byte ranges, one per thread, so a batch of a few
+// large columns still spreads over every thread.
+int dicm_host_pack(void* dst, const void* const* srcs, const int64_t* bytes, const int64_t* dst_off, int n,
+                   int nthreads) {
+  int64_t total = 0;
+  for (int i = 0; i < n; ++i) total += bytes[i];
+  int nt = nthreads > 0 ? nthreads : (int)std::max(1u, std::thread::hardware_concurrency());
+  nt = (int)std::max<int64_t>(1, std::min<int64_t>(nt, total / (256 << 10) + 1));
+  auto work = [&](int64_t lo, int64_t hi) {  // byte range [lo, hi) of the concatenated segments
+    int64_t pos = 0;
+    for (int i = 0; i < n && pos < hi; ++i) {
+      const int64_t a = std::max(lo, pos), b = std::min(hi, pos + bytes[i]);
+      if (a < b)
+        memcpy(static_cast<char*>(dst) + dst_off[i] + (a - pos), static_cast<const char*>(srcs[i]) + (a - pos), b - a);
+      pos += bytes[i];
+    }
+  };
+  if (nt == 1) {
+    work(0, total);
+    return DICM_OK;
+  }
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) th.emplace_back(work, total * t / nt, total * (t + 1) / nt);
+  work(0, total / nt);
+  for (auto& x : th) x.join();
+  return DICM_OK;
+}
+
 }  // extern "C"

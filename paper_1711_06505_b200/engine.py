@@ -73,18 +73,25 @@ class Packed:
         self.total = off
 
     def fill(self, model, batch, host):
+        """Pack the batch's columns into ``host`` (int32) with the library's
+        multithreaded copy (dicm_host_pack)."""
+        segs = []  # (array, int32 offset in host)
         for f in model.layout.schema.fields:
             if f.multi:
                 a, n, o = self.multi[f.name]
                 flat, offs = batch.multihot[f.name]
-                host[a:a + n] = flat
-                host[o:o + self.B + 1] = offs
+                segs += [(flat, a), (offs, o)]
             else:
-                host[self.onehot[f.name]:self.onehot[f.name] + self.B] = batch.onehot[f.name]
-        host[self.ad:self.ad + self.B] = batch.ad_image_ids
-        host[self.beh:self.beh + self.R] = batch.beh_image_ids
-        host[self.beh_off:self.beh_off + self.B + 1] = batch.beh_off
-        host[self.labels:self.labels + self.B] = np.asarray(batch.labels, dtype=np.float32).view(np.int32)
+                segs.append((batch.onehot[f.name], self.onehot[f.name]))
+        segs += [(batch.ad_image_ids, self.ad), (batch.beh_image_ids, self.beh), (batch.beh_off, self.beh_off),
+                 (np.asarray(batch.labels, dtype=np.float32).view(np.int32), self.labels)]
+        keep = [np.ascontiguousarray(a, dtype=np.int32) for a, _ in segs]
+        n = len(keep)
+        srcs = (C.c_void_p * n)(*[a.ctypes.data for a in keep])
+        nbytes = (C.c_int64 * n)(*[a.nbytes for a in keep])
+        offs = (C.c_int64 * n)(*[4 * o for _, o in segs])
+        assert host.dtype == np.int32 and host.flags.c_contiguous and host.size >= self.total
+        L.check(L.lib.dicm_host_pack(host.ctypes.data, srcs, nbytes, offs, n, 0))
 
     def n_id(self, fields):
         return sum(self.B if not f.multi else self.multi[f.name][1] for f in fields)
@@ -264,6 +271,7 @@ class StepEngine:
         self._pinned = [None, None]
         self._pin_ev = [None, None]
         self._pin_i = 0
+        self._copy_stream, self._up_ring, self._up_mark, self._up_n = None, [None, None], None, 0
 
     def _setup_towers(self, model):
         """Pre-rank head (csrc/towers.cu): tower descriptors whose gradient
@@ -457,18 +465,45 @@ class StepEngine:
 
     def upload(self, batch, own=False):
         """H2D of one batch (async).  ``own=True`` gives the batch its own
-        device buffer (pre-staged inputs); otherwise the engine's buffer is
-        reused."""
+        device buffer (pre-staged inputs) and copies on the current stream.
+        Otherwise the copy runs on a side stream into one of two staging
+        buffers, so it overlaps the step still running on the compute stream;
+        the compute stream waits for the copy only where it reaches this
+        batch.  A staging slot is rewritten only after the step that read it
+        (two uploads back) has finished."""
         self._check_capacity(batch)
         pk = Packed(self.model, batch)
         self._ensure(pk)
-        dst = torch.empty(max(pk.total, 1), dtype=torch.int32, device=self.dev) if own else self.packed
         i, buf = self._pinned_buf(pk.total)
         pk.fill(self.model, batch, buf.numpy())
-        dst[:pk.total].copy_(buf[:pk.total], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
-        self._pin_ev[i] = ev
+        cur = torch.cuda.current_stream()
+        if own:
+            dst = torch.empty(max(pk.total, 1), dtype=torch.int32, device=self.dev)
+            dst[:pk.total].copy_(buf[:pk.total], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            self._pin_ev[i] = ev
+            return DeviceBatch(pk, dst)
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(device=self.dev)
+        k = self._up_n % 2
+        self._up_n += 1
+        mark = torch.cuda.Event()
+        mark.record(cur)  # the work enqueued so far: every step before this batch's
+        prev, self._up_mark = self._up_mark, mark
+        dst = self._up_ring[k]
+        if dst is None or dst.numel() < pk.total:
+            torch.cuda.synchronize()  # the old slot may still be read or written
+            dst = self._up_ring[k] = torch.empty(max(pk.total, 1), dtype=torch.int32, device=self.dev)
+        cs = self._copy_stream
+        with torch.cuda.stream(cs):
+            if prev is not None:
+                cs.wait_event(prev)  # slot k's last reader (two uploads back) has run
+            dst[:pk.total].copy_(buf[:pk.total], non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(cs)
+        cur.wait_event(ready)
+        self._pin_ev[i] = ready
         return DeviceBatch(pk, dst)
 
     def h2d_bytes(self, batch):

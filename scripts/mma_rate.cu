@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(256, 1) rate(int iters, int N, int mn, long lo
 }
 
 __device__ float g_src[65536 * 4];  // 1 MB, L2-resident fill source
+__device__ const float* g_big;     // 4 GB HBM fill source (fill == 3)
 __device__ unsigned long long g_fill_bytes;
 
 // pair (cta_group::2) MMA rate; `fill` warps stream STS.128 into a spare
@@ -140,16 +141,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     const uint32_t dst = base + 65536 + 1024;
     const int i = threadIdx.x - 128;
     int k = 0;
+    const float* src = fill == 3 ? g_big + (size_t)blockIdx.x * (1 << 22) : g_src;
+    const size_t mask = fill == 3 ? ((size_t)1 << 22) / 4 - 1 : 65535;
     while (!*stop) {
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        cp_async16(dst + (((i + j * 128) & 4095) << 4), g_src + (((size_t)(k * 2048 + i + j * 128)) & 65535) * 4, 16);
+        cp_async16(dst + (((i + j * 128) & 4095) << 4), src + (((size_t)(k * 2048 + i + j * 128)) & mask) * 4, 16);
       cp_async_commit();
       cp_async_wait<4>();
       ++k;
     }
     cp_async_wait<0>();
-    if (fill == 2) atomicAdd(&g_fill_bytes, (unsigned long long)k * 16 * 16);
+    if (fill >= 2) atomicAdd(&g_fill_bytes, (unsigned long long)k * 16 * 16);
   }
   tc_fence_before();
   cluster_sync();
@@ -190,7 +193,11 @@ int main() {
              fb1 / 148.0 / cyc, cudaGetErrorString(cudaGetLastError()));
     }
   cudaFuncSetAttribute(rate2, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
-  for (int fill = 0; fill < 3; ++fill)
+  float* big;
+  cudaMalloc(&big, (size_t)148 << 24);
+  cudaMemset(big, 0, (size_t)148 << 24);
+  cudaMemcpyToSymbol(g_big, &big, sizeof(big));
+  for (int fill = 0; fill < 4; ++fill)
     for (int N : {128, 256}) {
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
