@@ -39,9 +39,9 @@ __device__ __forceinline__ int find_seg(const Segs& s, int64_t i) {
 }
 
 // Keys that share a bitmap word within a warp are combined first (one
-// atomicOr per distinct word and warp): small-vocabulary fields (scenario,
-// ad_category: a handful of ids over the whole batch) would otherwise queue
-// thousands of atomics on one word.
+// fire-and-forget RED.OR per distinct word and warp): small-vocabulary fields
+// (scenario, ad_category: a handful of ids over the whole batch) and Zipf-hot
+// keys would otherwise queue thousands of reductions on one word.
 __global__ void k_mark(const __grid_constant__ Segs segs, uint32_t* __restrict__ bitmap, int tag,
                        int32_t* __restrict__ status) {
   const int64_t total = seg_total(segs);
@@ -71,11 +71,7 @@ __global__ void k_mark(const __grid_constant__ Segs segs, uint32_t* __restrict__
       const uint32_t b = __shfl_sync(0xffffffffu, bit, src);
       if ((peers >> src) & 1u) bits |= b;
     }
-    if (w != 0xffffffffu && lane == __ffs(peers) - 1) {
-      uint32_t* p = bitmap + w;
-      // test before set: hot words are already complete after their first wave
-      if ((__ldcg(p) & bits) != bits) atomicOr(p, bits);
-    }
+    if (w != 0xffffffffu && lane == __ffs(peers) - 1) atomicOr(bitmap + w, bits);  // result unused: RED.OR
   }
 }
 

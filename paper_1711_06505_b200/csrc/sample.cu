@@ -174,16 +174,20 @@ __global__ void __launch_bounds__(256) k_keyproj(const float* __restrict__ w0, i
                                                  float* __restrict__ kp) {
   const int64_t n = min((int64_t)*count, u_cap);
   const int j0 = (threadIdx.x & 7) * 4;
+  float wk[4][DICM_D];  // this thread's 4 rows of Wk, kept in registers
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) wk[q][c] = __ldg(w0 + (j0 + q) * (dq + DICM_D) + dq + c);
   const int64_t step = (int64_t)gridDim.x * (blockDim.x >> 3);
   for (int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); u < n; u += step) {
     const Row12 e = load_row12(emb + u * DICM_D);
     float o[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float* w = w0 + (j0 + q) * (dq + DICM_D) + dq;
       float acc = 0.f;
 #pragma unroll
-      for (int c = 0; c < DICM_D; ++c) acc = fmaf(__ldg(w + c), e.v[c], acc);
+      for (int c = 0; c < DICM_D; ++c) acc = fmaf(wk[q][c], e.v[c], acc);
       o[q] = acc;
     }
     *reinterpret_cast<float4*>(kp + u * DICM_ATT + j0) = make_float4(o[0], o[1], o[2], o[3]);
@@ -750,7 +754,7 @@ int dicm_attn_keyproj(const dicm_layout_t* layout, const dicm_attn_params_t* att
   using namespace dicm;
   if (!(layout->kind == 1 || layout->kind == 2) || !layout->use_behavior_images || u_cap <= 0) return DICM_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  const int grid = dicm_grid(u_cap * 8, 256, 148 * 64);
+  const int grid = dicm_grid(u_cap * 8, 256, 148 * 8);
   k_keyproj<<<grid, 256, 0, st>>>(attn[0].w0, DICM_D, emb, count_dev, u_cap, keyproj);
   if (layout->kind == 2)
     k_keyproj<<<grid, 256, 0, st>>>(attn[1].w0, DICM_D * layout->n_query, emb, count_dev, u_cap,
