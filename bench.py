@@ -486,6 +486,13 @@ def main():
             cb = cpu_baseline(name, schema, pool, batches[-1])
         except Exception as ex:  # reported, never fatal
             cb = {"value": None, "error": repr(ex)[:200]}
+    # kernel launches inside the timed region: the captured step graph's kernel
+    # nodes (this library's only; NCCL / torch nodes excluded) x steps, or the
+    # engine's per-call kernel sequence for eager steps
+    kn = eng.kernel_nodes() if graphs else None
+    launches = kn[0] * args.steps if kn else eng.launches_per_step * args.steps
+    launch_src = ({"own_kernels_per_step": kn[0], "kernel_nodes_per_step": kn[1], "source": "captured step graph"}
+                  if kn else {"source": "engine kernel sequence"})
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -498,7 +505,7 @@ def main():
                            "parallelism": f"AMS: pool + ID tables sharded over {world} GPU(s), dense dp{world}",
                            "cuda_graph": graphs,
                            "l2": "inputs larger than L2 (each step gathers ~U x 8-16 KB of distinct pool rows)"},
-                "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": eng.launches_per_step * args.steps,
+                "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": launches, "gpu_launches_detail": launch_src,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     dbg = os.environ.get("DICM_EXIT_DEBUG") == "1"

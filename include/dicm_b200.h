@@ -270,6 +270,9 @@ int dicm_head_wide_fwd_bwd(const float* head_in, int batch, int width, const flo
 int dicm_head_wide_fwd(const float* head_in, int batch, int width, const dicm_head_params_t* p,
                        float* logits, void* workspace, size_t workspace_bytes, dicm_stream_t stream);
 
+/* zero a device buffer on the stream (a memset node, no kernel) */
+int dicm_zero_async(void* ptr, size_t bytes, dicm_stream_t stream);
+
 /* partials [nblk, n] -> out[n] (deterministic, fixed order; += if accumulate) */
 int dicm_reduce_partials(const float* partials, int nblk, int64_t n, float* out, int accumulate,
                          dicm_stream_t stream);

@@ -177,6 +177,7 @@ _sig("dicm_jsonl_parse", P, C.c_char_p, I64, C.POINTER(JsonlSpec), C.c_int, C.PO
 _sig("dicm_jsonl_list_total", I64, P, C.c_int)
 _sig("dicm_jsonl_export", C.c_int, P, C.c_int, P, P, P)
 _sig("dicm_jsonl_free", None, P)
+_sig("dicm_zero_async", C.c_int, P, S, ST)
 _sig("dicm_host_pack", C.c_int, P, C.POINTER(P), C.POINTER(I64), C.POINTER(I64), C.c_int, C.c_int)
 _sig("dicm_head_wide_workspace", S, C.c_int, C.c_int)
 _sig("dicm_head_wide_fwd_bwd", C.c_int, P, C.c_int, C.c_int, P, F, C.POINTER(HeadParams), P, P, P, P, P, S, ST)
@@ -211,7 +212,7 @@ EXPORTED = [
     "dicm_p2p_counts", "dicm_p2p_plan", "dicm_p2p_scatter", "dicm_dedup_devn", "dicm_head_fwd",
     "dicm_attn_keyproj", "dicm_jsonl_parse", "dicm_jsonl_list_total", "dicm_jsonl_export", "dicm_jsonl_free",
     "dicm_towers_blocks", "dicm_towers_fwd_bwd", "dicm_towers_fwd", "dicm_head_wide_workspace",
-    "dicm_head_wide_fwd_bwd", "dicm_head_wide_fwd", "dicm_host_pack",
+    "dicm_head_wide_fwd_bwd", "dicm_head_wide_fwd", "dicm_host_pack", "dicm_zero_async",
 ]
 
 

@@ -115,4 +115,9 @@ int dicm_probe_read(int kernel, float* ms, int max, int* n) {
   return DICM_OK;
 }
 
+int dicm_zero_async(void* ptr, size_t bytes, dicm_stream_t stream) {
+  if (!bytes) return DICM_OK;
+  return dicm::check_cuda(cudaMemsetAsync(ptr, 0, bytes, (cudaStream_t)stream), "dicm_zero_async");
+}
+
 }  // extern "C"

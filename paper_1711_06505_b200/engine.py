@@ -616,8 +616,8 @@ class StepEngine:
         self._head_fwd_bwd(B, denom)
         nhb = self._head_blocks(B)
         L.check(L.lib.dicm_loss_finalize(self.loss_part.data_ptr(), nhb, 1.0 / denom, self.loss.data_ptr(), st, s))
-        d_emb.zero_()
-        self.d_rows.zero_()
+        L.check(L.lib.dicm_zero_async(d_emb.data_ptr(), d_emb.numel() * 4, s))
+        L.check(L.lib.dicm_zero_async(self.d_rows.data_ptr(), self.d_rows.numel() * 4, s))
         L.check(L.lib.dicm_sample_bwd(C.byref(self.layout), C.byref(bv), self.attn, self.head_in.data_ptr(),
                                       self.d_head_in.data_ptr(), self.scores.data_ptr(), self.stats.data_ptr(),
                                       d_emb.data_ptr(), self.d_rows.data_ptr(), self.attn_partial.data_ptr(), s))
@@ -766,14 +766,42 @@ class StepEngine:
         g = self._graphs.get(key)
         if g is None:
             torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
+            g = torch.cuda.CUDAGraph(keep_graph=True)  # the node list stays inspectable (kernel_nodes)
             with torch.cuda.graph(g):
                 self.forward_backward(db, denominator)
                 self.optimizer_step(lr)
+            g.instantiate()
             self._graphs[key] = g
+        self._last_graph = g
         g.replay()
         self.iteration += 1
         return self.loss
+
+    _OWN_SOURCES = ("capi", "dedup", "exchange", "head", "imgmlp", "imgmlp_bf16_sm100", "imgmlp_sm100",
+                    "imgmlp_small_sm100", "optim", "p2p", "pool", "sample", "towers")
+
+    def kernel_nodes(self):
+        """(own, total) kernel nodes of the last captured step graph: every
+        kernel the step launches, and those of this library (csrc/*.cu) --
+        NCCL or torch kernels in the graph are counted in total only."""
+        g = getattr(self, "_last_graph", None)
+        if g is None:
+            return None
+        from cuda.bindings import driver as cu
+        err, _, n = cu.cuGraphGetNodes(g.raw_cuda_graph(), 0)
+        err, nodes, n = cu.cuGraphGetNodes(g.raw_cuda_graph(), n)
+        own = total = 0
+        for nd in nodes[:n]:
+            err, ty = cu.cuGraphNodeGetType(nd)
+            if ty != cu.CUgraphNodeType.CU_GRAPH_NODE_TYPE_KERNEL:
+                continue
+            total += 1
+            err, prm = cu.cuGraphKernelNodeGetParams(nd)
+            err, name = cu.cuFuncGetName(prm.func)
+            name = name.decode() if isinstance(name, bytes) else str(name)
+            if "4dicm" in name or any(f"_{s}_cu_" in name for s in self._OWN_SOURCES):
+                own += 1
+        return own, total
 
     def raise_status(self):
         """Sync point: raise the reference's exception for a flagged step."""
@@ -812,18 +840,26 @@ class StepEngine:
 
     @property
     def launches_per_step(self):
-        """Kernels this engine launches per step (memsets included), counted
-        from the kernel sequence of each C-ABI call."""
+        """Kernels this engine launches per eager step, from the kernel
+        sequence of each C-ABI call (memsets excluded).  A fallback estimate:
+        ``bench.py`` counts the kernel nodes of the captured step graph
+        (``kernel_nodes``) whenever steps run as graphs.  bf16 attn: 35, as
+        in the ncu launch list (profiles/r01e_cfg2_bf16_launches.csv)."""
         lay = self.model.layout
-        n = 6 + 6  # two dedups: memset + mark + tile sums + scan + emit + inverse
-        if self.prec_code == L.PREC_FP32:
-            n += 3 + 1 + 2 + 1 + (1 if lay.attentive else 0) + 1 + 4 + 12  # fwd, gather, zero, sample, reduces, bwd
+        n = 5 + 5  # two dedups: mark, tile sums, scan, emit, inverse
+        if self.prec_code == L.PREC_BF16:
+            n += 3 + 6 + 2  # to_bf16, fwd2, l12f | l12b, dw1b, colsum_multi, l1_finish, dw0, sum_splits | 2 colsums
         else:
-            n += 2 + 1 + 2 + 1 + (1 if lay.attentive else 0) + 1 + 4 + 11
-        n += 1 + 1 + 1  # sample fwd, head, loss
+            n += 4 + 9
+        n += 1  # gather_keyed
+        if lay.attentive:
+            n += 2 if lay.multiquery else 1  # keyproj per channel
+            n += 2 if lay.multiquery else 1  # attn_bwd per channel
+            n += 1  # attention partial reduce
+        n += 1 + 1 + 1 + 1 + 1  # sample fwd, head, loss, sample scatter, head partial reduce
         if self.wide_head:
             n += 3 + 2 - 1  # layer-0 GEMMs + two column reduces instead of the partial reduce
-        n += 1 + 4 + 1  # check_finite, adam dense (memset + 3), adam rows
+        n += 1 + 3 + 1  # check_finite, adam dense (flags, update, steps), adam rows
         return n
 
     # -- inspection ---------------------------------------------------
