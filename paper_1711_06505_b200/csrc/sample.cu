@@ -451,35 +451,17 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
     invS = S > 0.f ? 1.f / S : 0.f;
   }
   const float* sc = a.scores + (int64_t)ch * a.V.refs;
-  // pass 1: dot = sum_i w_i (dout . k_i)   (softmax backward, autograd.py:335-337)
+  // softmax backward (autograd.py:335-337) needs dot = sum_i w_i (dout . k_i)
+  // = dout . (sum_i w_i k_i) = dout . out: the forward's pooled output, read
+  // back from the head input instead of a second pass over the references
   float dot = 0.f;
   if (norm) {
-    for (int64_t b0 = i0 + lane; b0 < i1; b0 += 32 * UNR) {
-      int id[UNR];
-      float scv[UNR];
+    const float* outp = a.head_in + (int64_t)b * a.L.width + a.L.pool_col + ch * DICM_D;
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const bool v = b0 + 32 * u < i1;
-        id[u] = v ? __ldg(a.V.beh_local + b0 + 32 * u) : -1;
-        scv[u] = v ? sc[b0 + 32 * u] : 0.f;
-      }
-      Row12 k[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u)
-        if (id[u] >= 0) k[u] = load_row12(a.V.emb + (int64_t)id[u] * DICM_D);
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        if (id[u] < 0) continue;
-        float dw = 0.f;
-#pragma unroll
-        for (int c = 0; c < DICM_D; ++c) dw = fmaf(dout[c], k[u].v[c], dw);
-        dot = fmaf(expf(scv[u] - M) * invS, dw, dot);
-      }
-    }
-    dot = warp_sum(dot);
+    for (int c = 0; c < DICM_D; ++c) dot = fmaf(dout[c], __ldg(outp + c), dot);
   }
   float dP = 0.f;
-  // pass 2: chunks of 32 references, lane r owns reference r of the chunk;
+  // chunks of 32 references, lane r owns reference r of the chunk;
   // the next chunk's row and score are in flight while this one is processed
   int32_t row_n = i0 + lane < i1 ? __ldg(a.V.beh_local + i0 + lane) : 0;
   Row12 k_n;
