@@ -840,11 +840,11 @@ class StepEngine:
 
     @property
     def launches_per_step(self):
-        """Kernels this engine launches per eager step, from the kernel
-        sequence of each C-ABI call (memsets excluded).  A fallback estimate:
-        ``bench.py`` counts the kernel nodes of the captured step graph
-        (``kernel_nodes``) whenever steps run as graphs.  bf16 attn: 35, as
-        in the ncu launch list (profiles/r01e_cfg2_bf16_launches.csv)."""
+        """Estimated kernels per eager step, from the kernel sequence of each
+        C-ABI call (memsets excluded; some reductions depend on the shape).
+        Only a fallback: ``bench.py`` counts the kernel nodes of the captured
+        step graph (``kernel_nodes``) whenever steps run as graphs.  cfg2 bf16
+        attn: 35, as in the ncu launch list and the graph."""
         lay = self.model.layout
         n = 5 + 5  # two dedups: mark, tile sums, scan, emit, inverse
         if self.prec_code == L.PREC_BF16:

@@ -287,3 +287,23 @@ def test_concat_rejects_rows_beyond_capacity():
     _, _, long_batch = _bench_like("concat", B=16, L=6, P=300)
     with pytest.raises(ValueError, match="capacity"):
         e.upload(long_batch)
+
+
+@pytest.mark.parametrize("kind,precision", [("attn", "bf16"), ("multiquery-attn", "bf16"), ("sum", "tf32"),
+                                            ("attn", "fp32"), ("max", "fp32")])
+def test_step_graph_launches_only_library_kernels(kind, precision):
+    """Every kernel node of a captured step graph is one of this library's
+    kernels: no torch or fallback kernels on the hot path (bench.py reports
+    gpu_launches from these nodes)."""
+    from paper_1711_06505_b200.pool import ImagePool
+    from paper_1711_06505_b200.training import LocalTrainer, TrainConfig
+    model, pool, batch = _bench_like(kind, B=64, L=10, P=400)
+    if precision == "bf16":
+        pool = ImagePool.from_rows(pool.rows.cpu().numpy(), dtype="bf16")
+    tr = LocalTrainer(model, pool, TrainConfig(lr0=1e-4), precision=precision)
+    tr.engine.use_graphs = True
+    for _ in range(3):
+        tr.train_batch(batch)
+    own, total = tr.engine.kernel_nodes()
+    assert own == total, (own, total)
+    assert 25 <= own <= 50, own

@@ -142,3 +142,56 @@ def test_model_validation_errors_mirror_reference():
         S.validate_layout(lay)
     with pytest.raises(ValueError, match="unknown aggregator"):
         S.AggregatorSpec("bogus")
+
+
+def test_host_pack_matches_numpy_layout():
+    """dicm_host_pack (the multithreaded batch packing behind Packed.fill):
+    every segment lands at its offset, any thread count, ragged sizes."""
+    _ensure_lib()
+    from paper_1711_06505_b200 import _lib as L
+    rng = np.random.default_rng(4)
+    sizes = [0, 1, 7, 100_003, 3, 65_536, 250_001]
+    arrs = [rng.integers(-2**31, 2**31 - 1, n, dtype=np.int64).astype(np.int32) for n in sizes]
+    offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]) + 5  # a gap in front
+    total = int(offs[-1] + sizes[-1])
+    ref = np.zeros(total, np.int32)
+    for a, o in zip(arrs, offs):
+        ref[o:o + len(a)] = a
+    n = len(arrs)
+    for nt in (1, 3, 0):
+        out = np.zeros(total, np.int32)
+        L.check(L.lib.dicm_host_pack(out.ctypes.data, (ctypes.c_void_p * n)(*[a.ctypes.data for a in arrs]),
+                                     (ctypes.c_int64 * n)(*[a.nbytes for a in arrs]),
+                                     (ctypes.c_int64 * n)(*[4 * int(o) for o in offs]), n, nt))
+        assert np.array_equal(out, ref), nt
+
+
+def test_packed_fill_matches_column_copies():
+    """Packed.fill (one dicm_host_pack call) == the per-column layout."""
+    _ensure_lib()
+    from paper_1711_06505_b200.engine import Packed
+    schema = S.default_schema(500, 4, 600, 8, 900, b_max=20)
+
+    class M:
+        pass
+
+    m = M()
+    m.schema = schema
+    m.layout = S.ModelLayout(schema, S.AggregatorSpec("attn"), (128, 64), True, True)
+    b = synthetic_batch(np.random.default_rng(1), schema, 64, np.arange(64) % 21, 900)
+    pk = Packed(m, b)
+    host = np.full(pk.total, -7, np.int32)
+    pk.fill(m, b, host)
+    ref = np.full(pk.total, -7, np.int32)
+    for f in schema.fields:
+        if f.multi:
+            a, n, o = pk.multi[f.name]
+            fl, of = b.multihot[f.name]
+            ref[a:a + n], ref[o:o + pk.B + 1] = fl, of
+        else:
+            ref[pk.onehot[f.name]:pk.onehot[f.name] + pk.B] = b.onehot[f.name]
+    ref[pk.ad:pk.ad + pk.B] = b.ad_image_ids
+    ref[pk.beh:pk.beh + pk.R] = b.beh_image_ids
+    ref[pk.beh_off:pk.beh_off + pk.B + 1] = b.beh_off
+    ref[pk.labels:pk.labels + pk.B] = np.asarray(b.labels, np.float32).view(np.int32)
+    assert np.array_equal(host, ref)
