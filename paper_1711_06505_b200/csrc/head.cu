@@ -17,7 +17,7 @@ using namespace dicm;
 
 constexpr int BT = 32;  // samples per block
 constexpr int H0 = DICM_HEAD0, H1 = DICM_HEAD1;
-constexpr int THREADS = 128;
+constexpr int THREADS = 256;  // 8 warps: each phase splits its units or samples over two halves
 constexpr int MAXW = 128;
 
 __host__ __device__ inline int64_t part_size(int W) {
@@ -29,12 +29,26 @@ struct Smem {
   float w1[H1 * H0];    // mlp/1/w [64][128]
   float xs[MAXW][BT];   // x^T
   float a0[H0][BT];     // layer-0 pre-activation^T
+  float h0[H0][BT];     // PReLU(a0), evaluated once
   float a1[H1][BT];     // layer-1 pre-activation^T
   float da1[H1][BT];
   float da0[H0][BT];
   float dz[BT];
   float loss[BT];
+  float red[4][3][H0];  // cross-half / cross-quarter partial sums (fixed order)
 };
+
+template <int N>
+__device__ __forceinline__ void loadn(const float* p, float (&v)[N]) {
+#pragma unroll
+  for (int q = 0; q < N / 4; ++q) {
+    const float4 t = *reinterpret_cast<const float4*>(p + 4 * q);
+    v[4 * q] = t.x;
+    v[4 * q + 1] = t.y;
+    v[4 * q + 2] = t.z;
+    v[4 * q + 3] = t.w;
+  }
+}
 
 __device__ __forceinline__ void load32(const float* p, float (&v)[BT]) {
 #pragma unroll
@@ -58,6 +72,7 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
                                                   dicm_head_params_t p, float* __restrict__ logits,
                                                   float* __restrict__ dx, float* __restrict__ part,
                                                   float* __restrict__ loss_part) {
+  constexpr int HB = BT / 2, QB = BT / 4;  // samples per half / quarter
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   const int t = threadIdx.x;
@@ -72,45 +87,52 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
   } else {
     for (int i = t; i < BT * H0; i += THREADS) {
       const int r = i / H0, j = i % H0;
-      s.a0[j][r] = r < nb ? x[(int64_t)(b0 + r) * H0 + j] : 0.f;
+      const float a = r < nb ? x[(int64_t)(b0 + r) * H0 + j] : 0.f;
+      s.a0[j][r] = a;
+      s.h0[j][r] = prelu(a, __ldg(p.a0 + j));
     }
   }
   for (int i = t; i < H1 * H0; i += THREADS) s.w1[i] = p.w1[i];
   __syncthreads();
 
-  // layer 0: thread = unit j
+  // layer 0: thread = (unit j, half of the tile)
   if (!WIDE) {
-    const int j = t;
-    float acc[BT];
+    const int j = t & (H0 - 1), h = t >> 7;
+    float acc[HB];
     const float bj = p.b0[j];
 #pragma unroll
-    for (int r = 0; r < BT; ++r) acc[r] = bj;
+    for (int r = 0; r < HB; ++r) acc[r] = bj;
     for (int k = 0; k < W; ++k) {
       const float w = s.w0[j * W + k];
-      float xv[BT];
-      load32(s.xs[k], xv);
+      float xv[HB];
+      loadn<HB>(&s.xs[k][h * HB], xv);
 #pragma unroll
-      for (int r = 0; r < BT; ++r) acc[r] = fmaf(w, xv[r], acc[r]);
+      for (int r = 0; r < HB; ++r) acc[r] = fmaf(w, xv[r], acc[r]);
     }
+    const float al = __ldg(p.a0 + j);
 #pragma unroll
-    for (int r = 0; r < BT; ++r) s.a0[j][r] = acc[r];
+    for (int r = 0; r < HB; ++r) {
+      s.a0[j][h * HB + r] = acc[r];
+      s.h0[j][h * HB + r] = prelu(acc[r], al);
+    }
   }
   __syncthreads();
-  // layer 1: thread = (unit j, half of the tile)
+  // layer 1: thread = (unit j, quarter of the tile)
   {
-    const int j = t & (H1 - 1), half = t >> 6;
-    float acc[BT / 2];
+    const int j = t & (H1 - 1), q = t >> 6;
+    float acc[QB];
     const float bj = p.b1[j];
 #pragma unroll
-    for (int r = 0; r < BT / 2; ++r) acc[r] = bj;
+    for (int r = 0; r < QB; ++r) acc[r] = bj;
     for (int k = 0; k < H0; ++k) {
       const float w = s.w1[j * H0 + k];
-      const float al = __ldg(p.a0 + k);
+      float hv[QB];
+      loadn<QB>(&s.h0[k][q * QB], hv);
 #pragma unroll
-      for (int r = 0; r < BT / 2; ++r) acc[r] = fmaf(w, prelu(s.a0[k][half * (BT / 2) + r], al), acc[r]);
+      for (int r = 0; r < QB; ++r) acc[r] = fmaf(w, hv[r], acc[r]);
     }
 #pragma unroll
-    for (int r = 0; r < BT / 2; ++r) s.a1[j][half * (BT / 2) + r] = acc[r];
+    for (int r = 0; r < QB; ++r) s.a1[j][q * QB + r] = acc[r];
   }
   __syncthreads();
   // layer 2 + loss: thread = sample
@@ -143,13 +165,14 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
     loss_part[blockIdx.x] = l;
     out[o_b2] = d;
   }
-  // layer 2 / prelu 1 backward: thread = unit j of layer 1 (two halves)
+  // layer 2 / PReLU 1 backward: thread = (unit j of layer 1, quarter)
   {
-    const int j = t & (H1 - 1), half = t >> 6;
+    const int j = t & (H1 - 1), q = t >> 6;
     const float al = __ldg(p.a1 + j), w2j = __ldg(p.w2 + j);
     float sw = 0.f, sa = 0.f, sb = 0.f;
-    for (int rr = 0; rr < BT / 2; ++rr) {
-      const int r = half * (BT / 2) + rr;
+#pragma unroll
+    for (int rr = 0; rr < QB; ++rr) {
+      const int r = q * QB + rr;
       const float a = s.a1[j][r], dz = s.dz[r];
       sw = fmaf(dz, prelu(a, al), sw);
       const float dh = dz * w2j;
@@ -158,60 +181,72 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
       sb += d;
       s.da1[j][r] = d;
     }
-    // combine the two halves through shared memory (reuse loss[] is too small)
-    __shared__ float tmp[3][H1];
-    if (half == 1) {
-      tmp[0][j] = sw;
-      tmp[1][j] = sa;
-      tmp[2][j] = sb;
-    }
-    __syncthreads();
-    if (half == 0) {
-      out[o_w2 + j] = sw + tmp[0][j];
-      out[o_a1 + j] = sa + tmp[1][j];
-      out[o_b1 + j] = sb + tmp[2][j];
-    }
+    s.red[q][0][j] = sw;
+    s.red[q][1][j] = sa;
+    s.red[q][2][j] = sb;
   }
   __syncthreads();
-  // dW1[j][k] = sum_r da1[r][j] h0[r][k]: thread = k
-  {
-    const int k = t;
-    const float al = __ldg(p.a0 + k);
-    float h[BT];
+  if (t < H1) {
+    float v0 = 0.f, v1 = 0.f, v2 = 0.f;
 #pragma unroll
-    for (int r = 0; r < BT; ++r) h[r] = prelu(s.a0[k][r], al);
-    for (int j = 0; j < H1; ++j) {
-      float d[BT];
-      load32(s.da1[j], d);
-      float acc = 0.f;
-#pragma unroll
-      for (int r = 0; r < BT; ++r) acc = fmaf(d[r], h[r], acc);
-      out[o_w1 + (int64_t)j * H0 + k] = acc;
+    for (int q = 0; q < 4; ++q) {
+      v0 += s.red[q][0][t];
+      v1 += s.red[q][1][t];
+      v2 += s.red[q][2][t];
     }
-    // dh0[r][k] = sum_j da1[r][j] W1[j][k]; da0 = prelu'(a0) dh0
-    float dh[BT];
+    out[o_w2 + t] = v0;
+    out[o_a1 + t] = v1;
+    out[o_b1 + t] = v2;
+  }
+  // dW1[j][k] = sum_r da1[r][j] h0[r][k]: thread = (k, half of the j range);
+  // then dh0 = da1 W1 and da0 = PReLU'(a0) dh0: thread = (k, half of the tile)
+  {
+    const int k = t & (H0 - 1), h = t >> 7;
+    const float al = __ldg(p.a0 + k);
+    {
+      float hv[BT];
+      load32(s.h0[k], hv);
+      for (int j = h * (H1 / 2); j < (h + 1) * (H1 / 2); ++j) {
+        float d[BT];
+        load32(s.da1[j], d);
+        float acc = 0.f;
 #pragma unroll
-    for (int r = 0; r < BT; ++r) dh[r] = 0.f;
+        for (int r = 0; r < BT; ++r) acc = fmaf(d[r], hv[r], acc);
+        out[o_w1 + (int64_t)j * H0 + k] = acc;
+      }
+    }
+    float dh[HB];
+#pragma unroll
+    for (int r = 0; r < HB; ++r) dh[r] = 0.f;
     for (int j = 0; j < H1; ++j) {
       const float w = s.w1[j * H0 + k];
-      float d[BT];
-      load32(s.da1[j], d);
+      float d[HB];
+      loadn<HB>(&s.da1[j][h * HB], d);
 #pragma unroll
-      for (int r = 0; r < BT; ++r) dh[r] = fmaf(d[r], w, dh[r]);
+      for (int r = 0; r < HB; ++r) dh[r] = fmaf(d[r], w, dh[r]);
     }
     float sa = 0.f, sb = 0.f;
+    float av[HB];
+    loadn<HB>(&s.a0[k][h * HB], av);
 #pragma unroll
-    for (int r = 0; r < BT; ++r) {
-      const float a = s.a0[k][r];
+    for (int r = 0; r < HB; ++r) {
+      const float a = av[r];
       const float d = a > 0.f ? dh[r] : al * dh[r];
       if (!(a > 0.f)) sa = fmaf(a, dh[r], sa);
       sb += d;
-      s.da0[k][r] = d;
+      dh[r] = d;
     }
-    out[o_a0 + k] = sa;
-    out[o_b0 + k] = sb;
+    __syncthreads();  // every thread is done reading a0 / da1 for dW1 and dh0
+#pragma unroll
+    for (int r = 0; r < HB; ++r) s.da0[k][h * HB + r] = dh[r];
+    s.red[h][0][k] = sa;
+    s.red[h][1][k] = sb;
   }
   __syncthreads();
+  if (t < H0) {
+    out[o_a0 + t] = s.red[0][0][t] + s.red[1][0][t];
+    out[o_b0 + t] = s.red[0][1][t] + s.red[1][1][t];
+  }
   if (WIDE) {  // da0 rows for the dW0 / dx GEMMs
     for (int i = t; i < nb * H0; i += THREADS) {
       const int r = i / H0, j = i % H0;
@@ -219,12 +254,13 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
     }
     return;
   }
-  // dW0[k][c] = sum_r da0[r][k] x[r][c]: thread = k
+  // dW0[k][c] = sum_r da0[r][k] x[r][c]: thread = (k, half of the columns)
   {
-    const int k = t;
+    const int k = t & (H0 - 1), h = t >> 7;
+    const int c0 = h * ((W + 1) / 2), c1 = h ? W : (W + 1) / 2;
     float d[BT];
     load32(s.da0[k], d);
-    for (int c = 0; c < W; ++c) {
+    for (int c = c0; c < c1; ++c) {
       float xv[BT];
       load32(s.xs[c], xv);
       float acc = 0.f;
@@ -233,19 +269,23 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
       out[o_w0 + (int64_t)k * W + c] = acc;
     }
   }
-  // dx[r][c] = sum_k da0[r][k] W0[k][c]: thread = c
-  for (int c = t; c < W; c += THREADS) {
-    float acc[BT];
+  // dx[r][c] = sum_k da0[r][k] W0[k][c]: thread = (column c, half of the tile)
+  {
+    const int c = t & (H0 - 1), h = t >> 7;
+    if (c < W) {
+      float acc[HB];
 #pragma unroll
-    for (int r = 0; r < BT; ++r) acc[r] = 0.f;
-    for (int k = 0; k < H0; ++k) {
-      const float w = s.w0[k * W + c];
-      float d[BT];
-      load32(s.da0[k], d);
+      for (int r = 0; r < HB; ++r) acc[r] = 0.f;
+      for (int k = 0; k < H0; ++k) {
+        const float w = s.w0[k * W + c];
+        float d[HB];
+        loadn<HB>(&s.da0[k][h * HB], d);
 #pragma unroll
-      for (int r = 0; r < BT; ++r) acc[r] = fmaf(d[r], w, acc[r]);
+        for (int r = 0; r < HB; ++r) acc[r] = fmaf(d[r], w, acc[r]);
+      }
+      for (int r = 0; r < HB; ++r)
+        if (h * HB + r < nb) dx[(int64_t)(b0 + h * HB + r) * W + c] = acc[r];
     }
-    for (int r = 0; r < nb; ++r) dx[(int64_t)(b0 + r) * W + c] = acc[r];
   }
 }
 
