@@ -480,6 +480,24 @@ def main():
                            "peak_kind": "dense bf16 sustained" if precision == "bf16" else "tf32 = bf16/2",
                            "flops_per_unique_image": 4297216, "kernels": img},
                 "kernels": table}
+    if roof is not None:
+        # whole-step roofline: sum over the step's components of
+        # max(algorithmic bytes / HBM, tensor flops / TC), against the step time
+        n_id = sum(len(v) for v in last.onehot.values()) + sum(len(f) for f, _ in last.multihot.values())
+        K = int(eng.counts[3].item()) if world > 1 else int(eng.counts[1].item())
+        Rimg = B + R
+        comp = {k: max(kern[k][0] / (hbm_peak * 1e9), kern[k][1] / (tc_peak * 1e12)) for k in kern
+                if k.startswith("img")}
+        comp["dedup"] = (Rimg * 12 + U * 8 + n_id * 12 + K * 8) / (hbm_peak * 1e9)
+        comp["pooling"] = (kern["sample_fwd"][0] + kern["sample_bwd"][0]) / (hbm_peak * 1e9)
+        comp["id_rows"] = (2 * n_id * (4 + 48) + K * 48 + K * (6 * 48 + 16)) / (hbm_peak * 1e9)
+        comp["head"] = 2 * B * width * 4 / (hbm_peak * 1e9)
+        comp["dense_adam"] = int(model.dense.numel()) * 20 / (hbm_peak * 1e9)
+        t_roof = sum(comp.values())
+        roof["step"] = {"roofline_ms": 1e3 * t_roof, "measured_ms": ms_step, "frac": 1e3 * t_roof / ms_step,
+                        "components_ms": {k: round(1e3 * v, 4) for k, v in comp.items()},
+                        "note": "per-GPU step; image MLP at max(bytes/HBM, flops/TC) per kernel, the rest "
+                                "HBM-bound (SURVEY.md 8d byte counts)"}
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
