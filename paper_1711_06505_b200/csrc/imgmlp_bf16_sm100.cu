@@ -512,8 +512,10 @@ __global__ void __launch_bounds__(B_THREADS, 1)
 
 // ===========================================================================
 // k_dw1b: the three row reductions of layer 1's backward as GEMMs over rows
-//   Gp = max(a0,0)^T da1,  Gn = min(a0,0)^T da1,  Gm = [a0<=0]^T da1   [256 x 64]
-// from which (k_l1_finish, exact identities of the PReLU backward):
+//   Ga = a0^T da1,  Gp = max(a0,0)^T da1,  Gm = [a0<=0]^T da1   [256 x 64]
+// (Ga straight from the TMA-loaded a0 tile, so only two operands are built
+// on the CUDA cores); with Gn = min(a0,0)^T da1 = Ga - Gp, (k_l1_finish,
+// exact identities of the PReLU backward):
 //   dW1^T = Gp + alpha0 o Gn
 //   dalpha0[f] = sum_r [a0<=0] a0 dh1 = sum_j W1[j,f] Gn[f,j]
 //   db0[f]     = sum_r da0 = sum_j W1[j,f] (db1[j] - (1 - alpha0[f]) Gm[f,j])
@@ -523,7 +525,7 @@ constexpr int D_STAGES = 4;
 constexpr int DBK = 32;                  // rows per stage
 constexpr uint32_t DX = 4 * 4096;        // one operand: 4 boxes of 64 features x 32 rows (bf16 MN-major SW128)
 constexpr uint32_t DB = 4096;            // da1: 64 x 32 rows
-constexpr uint32_t DSTG = 3 * DX + DB;   // p (a0 transformed in place) | n | m | da1
+constexpr uint32_t DSTG = 3 * DX + DB;   // a0 (as loaded) | p | m | da1
 constexpr size_t D_SMEM = 1024 + D_STAGES * DSTG + 256;
 constexpr int D_THREADS = 192;  // w0-3 transform + epilogue, w4 MMA, w5 TMA
 constexpr int G_PART = 3 * 64 * 256;
@@ -615,16 +617,17 @@ __global__ void __launch_bounds__(D_THREADS, 1)
           const bool valid = row0 + r < re;
           const uint4 v = *reinterpret_cast<const uint4*>(a + off);
           const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-          uint32_t pp[4], nn[4], mm[4];
+          uint32_t pp[4], mm[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float2 x = bf2_to_f2(w[e]);
             pp[e] = valid ? f2_to_bf2(fmaxf(x.x, 0.f), fmaxf(x.y, 0.f)) : 0u;
-            nn[e] = valid ? f2_to_bf2(fminf(x.x, 0.f), fminf(x.y, 0.f)) : 0u;
             mm[e] = valid ? f2_to_bf2(x.x > 0.f ? 0.f : 1.f, x.y > 0.f ? 0.f : 1.f) : 0u;
           }
-          *reinterpret_cast<uint4*>(a + off) = make_uint4(pp[0], pp[1], pp[2], pp[3]);
-          *reinterpret_cast<uint4*>(a + DX + off) = make_uint4(nn[0], nn[1], nn[2], nn[3]);
+          // a0 itself is the third operand (Ga = a0^T da1); rows outside this
+          // CTA's range are zeroed so that no operand picks them up
+          if (!valid) *reinterpret_cast<uint4*>(a + off) = make_uint4(0u, 0u, 0u, 0u);
+          *reinterpret_cast<uint4*>(a + DX + off) = make_uint4(pp[0], pp[1], pp[2], pp[3]);
           *reinterpret_cast<uint4*>(a + 2 * DX + off) = make_uint4(mm[0], mm[1], mm[2], mm[3]);
         }
       fence_proxy_async();
@@ -651,7 +654,7 @@ __global__ void __launch_bounds__(D_THREADS, 1)
   if (warp == 4) tmem_dealloc(tmem, 512);
 }
 
-// gw1[j][f] = Gp + a0[f] Gn ; ga0[f] = sum_j W1[j][f] Gn[j][f] ;
+// Gn = Ga - Gp ; gw1[j][f] = Gp + a0[f] Gn ; ga0[f] = sum_j W1[j][f] Gn[j][f] ;
 // gb0[f] = sum_j W1[j][f] (db1[j] - (1 - a0[f]) Gm[j][f])
 // block = 32 features x 8 j-groups of 8; the 8 partial sums of a feature are
 // combined in a fixed order (deterministic)
@@ -666,7 +669,8 @@ __global__ void __launch_bounds__(256) k_l1_finish(const float* __restrict__ G, 
 #pragma unroll
   for (int jj = 0; jj < 8; ++jj) {
     const int j = jg * 8 + jj;
-    const float gp = G[j * 256 + f], gn = G[16384 + j * 256 + f], gm = G[32768 + j * 256 + f];
+    const float ga = G[j * 256 + f], gp = G[16384 + j * 256 + f], gm = G[32768 + j * 256 + f];
+    const float gn = ga - gp;
     const float w = w1[j * 256 + f];
     gw1[j * 256 + f] = gp + a * gn;
     sa = fmaf(w, gn, sa);
