@@ -382,6 +382,202 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F, 1)
 }
 
 // ---------------------------------------------------------------------------
+// forward, two sub-tiles per W0 pass: a pair tile is 512 rows = two 256-row
+// pair MMAs that share every W0 stage.  Per CTA and stage: 32 KB of gathered
+// rows (2 x 128 rows x 128 B) against 16 KB of W0, so the ring holds more
+// gathered bytes in flight per byte of W0 and W0 is re-read from L2 half as
+// often.  TMEM holds both sub-tile accumulators (2 x 256 columns), so the
+// MMAs of tile i+1 wait for the epilogue of tile i; 8 epilogue warps (two
+// per TMEM lane quarter, one per sub-tile) keep that drain short while the
+// gather ring keeps filling.
+// ---------------------------------------------------------------------------
+constexpr int THREADS_F4 = 448;  // w0-3 gather, w4 MMA / relay, w5 TMA, w6-13 epilogue
+__host__ __device__ constexpr size_t smem4(int sa, int sb, bool scr) {
+  return (size_t)sa * 2 * OPB2 + (size_t)sb * OPB2 + 1024 + 256 + (scr ? 8 * epi::SCRATCH_FLOATS * 4 : 0);
+}
+
+// SCR: transpose each 32x32 block through shared memory for whole-line stores;
+// without it the ring gets the space and every lane stores its own row
+template <int KIND, int SA, int SB, bool SCR>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F4, 1)
+    k_fwd4(const __grid_constant__ CUtensorMap tmW, const void* __restrict__ pool_, int d_raw,
+           const int32_t* __restrict__ rows, const int32_t* __restrict__ count, const float* __restrict__ bias,
+           void* __restrict__ act0_) {
+  using T = Elem<KIND>;
+  constexpr int EPB = 128 / sizeof(T);
+  constexpr uint32_t ASTG = 2 * OPB2;  // two sub-tiles of 128 rows
+  const int U = *count;
+  const int ntiles = (U + 511) / 512;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  if (pair >= ntiles) return;  // uniform across the pair
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t r0s = smem_u32(smem_raw);
+  const uint32_t base = (r0s + 1023u) & ~1023u, bbase = base + SA * ASTG;
+  const uint32_t fullA = bbase + SB * OPB2, emptyA = fullA + 8 * SA, fullB = emptyA + 8 * SA,
+                 emptyB = fullB + 8 * SB, accf = emptyB + 8 * SB, acce = accf + 8, slot = acce + 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < SA; ++i) {
+      mbar_init(fullA + 8 * i, 128 + (rank == 0 ? 1 : 0));  // gathers (+ the peer's relay)
+      mbar_init(emptyA + 8 * i, 1);                         // pair MMA commit (multicast)
+    }
+    for (int i = 0; i < SB; ++i) {
+      mbar_init(fullB + 8 * i, 1);
+      mbar_init(emptyB + 8 * i, 1);
+    }
+    mbar_init(accf, 1);
+    mbar_init(acce, 16);  // both CTAs' 8 epilogue warps (leader's copy is used)
+    fence_mbar_init();
+  }
+  if (warp == 4) {
+    tmem_alloc2(slot, 512);
+    tmem_relinquish2();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem_raw + (slot - r0s));
+  const int nk = d_raw / EPB;
+  const T* pool = reinterpret_cast<const T*>(pool_);
+  // this CTA's rows of sub-tile s of pair tile `tile`: tile*512 + s*256 + rank*128 + [0, 128)
+  if (warp < 4) {
+    // ---- gather producer: 16 rows x one 16-B chunk per thread and stage
+    const int t = threadIdx.x, c = t & 7, rb = t >> 3;
+    const uint32_t dst0 = (uint32_t)(rb * 128 + ((c ^ (rb & 7)) << 4));
+    uint32_t g = 0;
+    for (int tile = pair; tile < ntiles; tile += npairs) {
+      const T* src[16];
+      uint32_t ok[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int gr = tile * 512 + (i >> 3) * 256 + (int)rank * 128 + rb + 16 * (i & 7);
+        const bool v = gr < U;
+        src[i] = pool + (int64_t)(v ? __ldg(rows + gr) : 0) * d_raw + c * (16 / sizeof(T));
+        ok[i] = v ? 16u : 0u;
+      }
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const uint32_t st = g % SA, it = g / SA;
+        mbar_wait(emptyA + 8 * st, (it & 1) ^ 1);
+        const uint32_t a = base + st * ASTG + dst0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          cp_async16(a + (i >> 3) * OPB2 + (i & 7) * 16 * 128, src[i] + (int64_t)kb * EPB, ok[i]);
+        cp_async_arrive_noinc(fullA + 8 * st);
+      }
+    }
+    cp_async_wait<0>();
+  } else if (warp == 5) {
+    if (lane == 0) {
+      // ---- TMA producer: this CTA's half of W0 (rows rank*128 .. +127)
+      prefetch_tmap(&tmW);
+      uint32_t g = 0;
+      for (int tile = pair; tile < ntiles; tile += npairs)
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const uint32_t st = g % SB, it = g / SB;
+          mbar_wait(emptyB + 8 * st, (it & 1) ^ 1);
+          mbar_arrive_expect_tx(fullB + 8 * st, OPB2);
+          tma_load_2d(bbase + st * OPB2, &tmW, fullB + 8 * st, kb * EPB, (int)rank * 128);
+        }
+    }
+  } else if (warp == 4) {
+    if (lane == 0) {
+      if (rank == 0) {
+        // ---- MMA issuer (leader): per k-step two M256 x N256 MMAs (sub-tiles) on one W0 stage
+        const uint32_t idesc = instr_desc(KIND == 0 ? 2u : 1u, 256, 256, 0, 0);
+        uint32_t g = 0, tl = 0;
+        for (int tile = pair; tile < ntiles; tile += npairs, ++tl) {
+          mbar_wait(acce, (tl & 1) ^ 1);  // the epilogue has drained both accumulators
+          tc_fence_after();
+          for (int kb = 0; kb < nk; ++kb, ++g) {
+            const uint32_t sa = g % SA, sb = g % SB;
+            mbar_wait(fullA + 8 * sa, (g / SA) & 1);
+            mbar_wait(fullB + 8 * sb, (g / SB) & 1);
+            tc_fence_after();
+            fence_proxy_async();
+            const uint32_t a = base + sa * ASTG, b = bbase + sb * OPB2;
+#pragma unroll
+            for (int sub = 0; sub < 2; ++sub)
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma2<KIND>(tmem + sub * 256, smem_desc(a + sub * OPB2 + k * 32, 16, 1024),
+                           smem_desc(b + k * 32, 16, 1024), idesc, (kb | k) != 0);
+            mma_commit2(emptyA + 8 * sa, 0x3);
+            mma_commit2(emptyB + 8 * sb, 0x3);
+          }
+          mma_commit2(accf, 0x3);
+        }
+      } else {
+        // ---- relay (peer): this CTA's stage landed -> the leader's full barrier
+        const uint32_t lfull = mapa(fullA, 0);
+        uint32_t g = 0;
+        for (int tile = pair; tile < ntiles; tile += npairs)
+          for (int kb = 0; kb < nk; ++kb, ++g) {
+            const uint32_t sa = g % SA;
+            mbar_wait(fullA + 8 * sa, (g / SA) & 1);
+            mbar_wait(fullB + 8 * (g % SB), (g / SB) & 1);
+            fence_proxy_async();
+            mbar_arrive_cluster(lfull + 8 * sa);
+          }
+      }
+    }
+  } else {
+    // ---- epilogue warps 6-13: sub-tile (warp - 6) / 4, TMEM lane quarter warp % 4
+    const int q = warp & 3, sub = (warp - 6) >> 2;
+    float* scr = reinterpret_cast<float*>(smem_raw + (slot + 8 - r0s)) + (warp - 6) * epi::SCRATCH_FLOATS;
+    (void)scr;
+    const uint32_t lacce = mapa(acce, 0);
+    uint32_t tl = 0;
+    for (int tile = pair; tile < ntiles; tile += npairs, ++tl) {
+      mbar_wait(accf, tl & 1);
+      tc_fence_after();
+      const int m0 = tile * 512 + sub * 256 + (int)rank * 128 + q * 32;
+#pragma unroll 1
+      for (int cb = 0; cb < 8; ++cb) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + sub * 256 + cb * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] += __ldg(bias + cb * 32 + j);
+        if constexpr (SCR) {
+          if constexpr (KIND == 1)
+            epi::store_bf16(v, scr, lane, m0, U, [&](int r) {
+              return reinterpret_cast<__nv_bfloat16*>(act0_) + (int64_t)r * 256 + cb * 32;
+            });
+          else
+            epi::store_f32(v, scr, lane, m0, U,
+                           [&](int r) { return reinterpret_cast<float*>(act0_) + (int64_t)r * 256 + cb * 32; });
+        } else if (m0 + lane < U) {
+          if constexpr (KIND == 1) {
+            uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(act0_) + (int64_t)(m0 + lane) * 256 +
+                                                cb * 32);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              uint32_t w[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * q4 + 2 * e], v[8 * q4 + 2 * e + 1]);
+                w[e] = *reinterpret_cast<uint32_t*>(&h);
+              }
+              o[q4] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          } else {
+            float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(act0_) + (int64_t)(m0 + lane) * 256 + cb * 32);
+#pragma unroll
+            for (int q4 = 0; q4 < 8; ++q4) o[q4] = make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(lacce);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 4) tmem_dealloc2(tmem, 512);
+}
+
+// ---------------------------------------------------------------------------
 // backward: part[split][256][d_raw] = da0[chunk]^T X[rows[chunk]]
 // grid = (d_raw/256 feature tiles, nsplit row chunks).  BK rows of K per
 // stage and NST stages: 32-row stages x 6 keep as many gathered bytes in
@@ -667,8 +863,23 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
       kern<<<grid, THREADS_F, bytes, st>>>(map, pool, d_raw, rows, count, b0, act0);
       return 0;
     };
+    // default: 512-row pair tiles (k_fwd4); DICM_FWD4=0 selects the 256-row
+    // tiles with double-buffered accumulators (k_fwd2)
+    static const bool four = !(getenv("DICM_FWD4") && getenv("DICM_FWD4")[0] == '0');
+    static int a44 = -1, t44 = -1;
+    auto launch4 = [&](auto kern, size_t bytes, int& attr) -> int {
+      if (attr < 0)
+        attr = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes),
+                          "k_fwd4 smem");
+      if (attr) return attr;
+      const int grid4 = 2 * (int)std::min<int64_t>(74, (rows_max + 511) / 512);
+      kern<<<grid4, THREADS_F4, bytes, st>>>(map, pool, d_raw, rows, count, b0, act0);
+      return 0;
+    };
     const int probe_slot = probe_begin(DICM_PROBE_IMG_FWD_L0, st);
-    const int lrc = bf16 ? launch(k_fwd2<1, 6, 6>, smem2(6, 6), a66) : launch(k_fwd2<0, 6, 6>, smem2(6, 6), t66);
+    const int lrc = four ? (bf16 ? launch4(k_fwd4<1, 4, 4, true>, smem4(4, 4, true), a44)
+                                 : launch4(k_fwd4<0, 4, 4, true>, smem4(4, 4, true), t44))
+                         : (bf16 ? launch(k_fwd2<1, 6, 6>, smem2(6, 6), a66) : launch(k_fwd2<0, 6, 6>, smem2(6, 6), t66));
     probe_end(probe_slot, st);
     if (lrc) return lrc;
     return last_launch("tcgen05 layer-0 forward (CTA pairs)");

@@ -18,7 +18,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-PROBE = {"k_fwd": "img_fwd_l0", "k_fwd2": "img_fwd_l0", "k_l12_fwd": "img_fwd_l12", "k_l12f": "img_fwd_l12",
+PROBE = {"k_fwd": "img_fwd_l0", "k_fwd2": "img_fwd_l0", "k_fwd4": "img_fwd_l0", "k_l12_fwd": "img_fwd_l12", "k_l12f": "img_fwd_l12",
          "k_l12_bwd": "img_bwd_l12", "k_l12b": "img_bwd_l12", "k_dw1": "img_bwd_dw1", "k_dw1b": "img_bwd_dw1",
          "k_dw0": "img_bwd_dw0", "k_sample_fwd": "sample_fwd", "k_sample_bwd": "sample_bwd",
          "k_attn_bwd": "sample_bwd", "k_sample_scatter": "sample_bwd"}
@@ -92,7 +92,7 @@ def main():
     kern = read_raw(rep)
     agg, cnt = launch_share(launches)
     tot = sum(agg.values())
-    steps = max(cnt.get("k_fwd2", 0) or cnt.get("k_fwd", 1), 1)
+    steps = max(cnt.get("k_fwd4", 0) or cnt.get("k_fwd2", 0) or cnt.get("k_fwd", 1), 1)
     lines = [f"# ncu summary: {cfg} / {prec} ({tag})", "",
              f"Source: `{os.path.basename(rep)}` (`ncu --set full --clock-control none --import-source on`, "
              "one launch per kernel, cold-cache replay) and the launch list "
