@@ -725,6 +725,162 @@ __global__ void __launch_bounds__(THREADS_B, 1)
   if (warp == 4) tmem_dealloc(tmem, 512);
 }
 
+// ---------------------------------------------------------------------------
+// backward on CTA pairs (bf16): a pair covers 512 features of dW0 for one row
+// chunk.  M = 256 hidden units split over the pair (each CTA TMA-loads its 128
+// columns of da0), N = 2 x 256 features (each CTA gathers its 2 x 128-feature
+// halves of the X rows); both N halves accumulate in each CTA's 512 TMEM
+// columns.  da0 is thereby read once per 512 features instead of once per
+// 256.  The peer's stage completion is relayed to the leader's barrier, whose
+// MMA commits multicast to both CTAs.
+// ---------------------------------------------------------------------------
+template <int BK, int NST>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_B, 1)
+    k_dw0p(const __grid_constant__ CUtensorMap tmA, const void* __restrict__ pool_, int d_raw,
+           const int32_t* __restrict__ rows, const int32_t* __restrict__ count, float* __restrict__ part) {
+  using T = __nv_bfloat16;
+  constexpr int EPB = 64;    // MN-atom width (bf16 elements)
+  constexpr int KROWS = 16;  // rows per MMA
+  constexpr int CPR = 32;    // 16-B chunks per row: 2 segments x 128 features
+  constexpr int RPI = 128 / CPR;
+  constexpr int NI = BK / RPI;
+  constexpr uint32_t OPA = 128u * BK * 2;  // this CTA's 128 hidden columns of da0
+  constexpr uint32_t OPB_ = 256u * BK * 2;  // this CTA's 256 features of X
+  constexpr uint32_t STG = OPA + OPB_;
+  static_assert(NI <= 32, "row ids are shuffled from one warp");
+  const int U = *count;
+  const uint32_t rank = cluster_ctarank();
+  const int F0 = (blockIdx.x >> 1) * 512, split = blockIdx.y, nsplit = gridDim.y;
+  const int per = (((U + nsplit - 1) / nsplit) + BK - 1) / BK * BK;
+  const int r0 = split * per;
+  const int r1 = min(U, r0 + per);
+  const int nk = r1 > r0 ? (r1 - r0 + BK - 1) / BK : 0;
+  float* out = part + (int64_t)split * 256 * d_raw;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (nk == 0) {  // empty chunk (uniform across the pair): this CTA's partial rows are zero
+    for (int i = threadIdx.x; i < 128 * 512; i += THREADS_B)
+      out[(int64_t)(rank * 128 + (i >> 9)) * d_raw + F0 + (i & 511)] = 0.f;
+    return;
+  }
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t rs = smem_u32(smem_raw);
+  const uint32_t base = (rs + 1023u) & ~1023u;
+  const uint32_t full = base + NST * STG, empty = full + 8 * NST, acc_full = empty + 8 * NST, slot = acc_full + 8;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(full + 8 * i, 128 + 1 + (rank == 0 ? 1 : 0));  // gathers + TMA expect_tx (+ the peer's relay)
+      mbar_init(empty + 8 * i, 1);                             // pair MMA commit (multicast)
+    }
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 4) {
+    tmem_alloc2(slot, 512);
+    tmem_relinquish2();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem_raw + (slot - rs));
+  const T* pool = reinterpret_cast<const T*>(pool_);
+
+  if (warp < 4) {
+    // ---- gather producer: X[rows] features F0 + j*256 + rank*128 + [0,128), j = 0, 1
+    const int t = threadIdx.x, c = t % CPR, kw = t / CPR;
+    const T* colbase = pool + F0 + (c >> 4) * 256 + (int)rank * 128 + (c & 15) * 8;
+    const uint32_t atom_off = (c >> 3) * (BK * 128);
+    auto fetch = [&](int kb) {
+      const int gr = r0 + kb * BK + lane * RPI + kw;
+      return (lane < NI && kb < nk && gr < r1) ? __ldg(rows + gr) : -1;
+    };
+    int rid_next = fetch(0);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int rid_cur = rid_next;
+      rid_next = fetch(kb + 1);
+      const uint32_t st = kb % NST, itn = kb / NST;
+      mbar_wait(empty + 8 * st, (itn & 1) ^ 1);
+      const uint32_t bb = base + st * STG + OPA + atom_off;
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const int rid = __shfl_sync(FULL, rid_cur, i);
+        const int k = i * RPI + kw;
+        const uint32_t sw = ((c & 7) ^ (k & 7)) << 4;
+        cp_async16(bb + k * 128 + sw, colbase + (int64_t)(rid < 0 ? 0 : rid) * d_raw, rid < 0 ? 0u : 16u);
+      }
+      cp_async_arrive_noinc(full + 8 * st);
+    }
+    cp_async_wait<0>();
+  } else if (warp == 5) {
+    if (lane == 0) {
+      // ---- TMA producer: da0 columns rank*128 .. +127 (two MN atoms of 64 hidden x BK rows)
+      prefetch_tmap(&tmA);
+      for (int kb = 0; kb < nk; ++kb) {
+        const uint32_t st = kb % NST, itn = kb / NST;
+        mbar_wait(empty + 8 * st, (itn & 1) ^ 1);
+        mbar_arrive_expect_tx(full + 8 * st, OPA);
+        const uint32_t a = base + st * STG;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          tma_load_2d(a + j * (BK * 128), &tmA, full + 8 * st, (int)rank * 128 + j * EPB, r0 + kb * BK);
+      }
+    }
+  } else {
+    if (lane == 0) {
+      if (rank == 0) {
+        const uint32_t idesc = instr_desc(1u, 256, 256, 1, 1);
+        for (int kb = 0; kb < nk; ++kb) {
+          const uint32_t st = kb % NST, itn = kb / NST;
+          mbar_wait(full + 8 * st, itn & 1);
+          tc_fence_after();
+          fence_proxy_async();
+          const uint32_t a = base + st * STG, bb = a + OPA;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int k = 0; k < BK / KROWS; ++k)
+              mma2<1>(tmem + j * 256, smem_desc(a + k * KROWS * 128, BK * 128, 1024u, 2u),
+                      smem_desc(bb + j * 2 * (BK * 128) + k * KROWS * 128, BK * 128, 1024u, 2u), idesc,
+                      (kb | k) != 0);
+          mma_commit2(empty + 8 * st, 0x3);
+        }
+        mma_commit2(acc_full, 0x3);
+      } else {
+        // ---- relay (peer): this CTA's stage landed -> the leader's full barrier
+        const uint32_t lfull = mapa(full, 0);
+        for (int kb = 0; kb < nk; ++kb) {
+          const uint32_t st = kb % NST, itn = kb / NST;
+          mbar_wait(full + 8 * st, itn & 1);
+          fence_proxy_async();
+          mbar_arrive_cluster(lfull + 8 * st);
+        }
+      }
+    }
+  }
+  if (warp < 4) {
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const int hid = (int)rank * 128 + warp * 32 + lane;
+#pragma unroll 1
+    for (int j = 0; j < 2; ++j)
+#pragma unroll 1
+      for (int cb = 0; cb < 8; ++cb) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + j * 256 + cb * 32, v);
+        float4* o = reinterpret_cast<float4*>(out + (int64_t)hid * d_raw + F0 + j * 256 + cb * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 4) tmem_dealloc2(tmem, 512);
+}
+
+template <int BK, int NST>
+constexpr size_t dw0p_smem() {
+  return (size_t)NST * (128u * BK * 2 + 256u * BK * 2) + 1024 + 256;
+}
+
 template <int KIND, int BK, int NST>
 constexpr size_t dw0_smem() {
   return (size_t)NST * 2 * 256 * BK * (KIND == 0 ? 4 : 2) + 1024 + 256;
@@ -927,7 +1083,16 @@ int bwd_dw0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows, co
     return rc;
   const int nsplit = nsplit_for(rows_max, d_raw);
   dim3 grid(d_raw / 256, nsplit);
-  if (bf16) {
+  static const bool pairs = !(getenv("DICM_DW0_PAIR") && getenv("DICM_DW0_PAIR")[0] == '0');
+  if (bf16 && pairs && d_raw % 512 == 0) {
+    constexpr int NSP = 4;  // 4 x 48 KB stages
+    static int once = check_cuda(cudaFuncSetAttribute(k_dw0p<BKB, NSP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      (int)dw0p_smem<BKB, NSP>()), "k_dw0p smem");
+    if (once) return once;
+    const int probe_slot = probe_begin(DICM_PROBE_IMG_BWD_DW0, st);
+    k_dw0p<BKB, NSP><<<grid, THREADS_B, dw0p_smem<BKB, NSP>(), st>>>(map, pool, d_raw, rows, count, w.part);
+    probe_end(probe_slot, st);
+  } else if (bf16) {
     static int once = check_cuda(cudaFuncSetAttribute(k_dw0<1, BKB, NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                       (int)dw0_smem<1, BKB, NSB>()), "k_dw0 smem");
     if (once) return once;
