@@ -428,6 +428,7 @@ class StepEngine:
         self._alloc_image_net(self.cap_u)
         self.cap = need
         self._graphs, self._graph_warm = None, False  # captured steps point at the old buffers
+        self._last_graph = None
 
     def _alloc_image_net(self, cap):
         self.net = ImageNetBuffers(cap, self.pool.d_raw, self.prec_code, self.dev)

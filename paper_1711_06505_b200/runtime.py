@@ -592,6 +592,7 @@ class Cluster:
         e = self.engine
         e.use_graphs = False
         e._graphs = None
+        e._last_graph = None  # kept graphs hold NCCL nodes: release them before the communicator
         if torch.cuda.is_available():
             torch.cuda.synchronize()
         px = getattr(e, "px", None)
