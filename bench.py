@@ -471,7 +471,7 @@ def main():
                 traffic = ent["dram_bytes"] * U / ent["unique_images"]
         except Exception:
             pass
-        roof = {"bound": "hbm", "kernel": "k_fwd: pool-row gather + layer-0 tcgen05 GEMM (dicm_imgmlp_fwd)",
+        roof = {"bound": "hbm", "kernel": "k_fwd4: pool-row gather + layer-0 tcgen05 GEMM on CTA pairs (dicm_imgmlp_fwd)",
                 "achieved": top["GB_s"], "peak": hbm_peak, "unit": "GB/s", "frac": top["GB_s"] / hbm_peak,
                 "traffic": traffic, "peak_source": src, "algorithmic_bytes_per_launch": top["alg_bytes"],
                 "ms_per_launch": top["ms"], "unique_images_per_step": U,
