@@ -140,3 +140,18 @@ def test_step_logits_within_north_star_tolerance(kind, prec):
     # gradients inherit layer-0 operand rounding: same 2e-2 bound as logits
     for n, g in H.dense_grads(e).items():
         assert O.rel_err(g, out["grads"][n]) < 2e-2, n
+
+
+def test_alternative_layer0_kernels_still_match():
+    """The 256-row-tile forward (k_fwd2) and the single-CTA bf16 dW0 (k_dw0)
+    stay selectable (DICM_FWD4=0, DICM_DW0_PAIR=0; read once per process) and
+    must keep matching the fp32 path: rerun the layer-0 parity cases above in
+    a child process with both switched on."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, DICM_FWD4="0", DICM_DW0_PAIR="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.abspath(__file__),
+                        "-k", "test_layer0_tensorcore_matches_fp32"], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
