@@ -13,7 +13,7 @@
 // The inputs are the head-input rows the per-sample kernel already wrote
 // (fields in schema order, ad image, pooled behaviors), so each tower reads
 // its blocks by column.  All per-sample state of both towers stays in shared
-// memory (x^T, pre-activations, representations; [.][33] to keep the
+// memory (x^T, pre-activations and their PReLU, representations; [.][33] to keep the
 // column-wise passes conflict-free); the weights are small and read through
 // L1.  As in the head, dLoss/dz depends only on the sample, so forward, loss
 // and backward run in one pass per tile, and weight gradients leave as one
@@ -36,7 +36,7 @@ struct Dims {
 };
 
 __host__ __device__ inline size_t smem_floats(const Dims& d) {
-  return (size_t)LD * (d.nin[0] + d.nin[1] + 2 * d.H + 2 * d.R   // x^T, pre, rep of both towers
+  return (size_t)LD * (d.nin[0] + d.nin[1] + 4 * d.H + 2 * d.R   // x^T, pre, PReLU(pre), rep of both towers
                        + d.R + d.H                               // dr, dh (one tower at a time)
                        + d.W)                                    // dx^T
          + 2 * BT;                                               // dz, loss
@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(THREADS) k_towers(const float* __restrict__ x,
   const int H = d.H, R = d.R, W = d.W;
   float* xs[2];
   float* pre[2];
+  float* hs[2];  // PReLU(pre), evaluated once
   float* rep[2];
   float* q = sm;
   for (int k = 0; k < 2; ++k) {
@@ -67,6 +68,8 @@ __global__ void __launch_bounds__(THREADS) k_towers(const float* __restrict__ x,
   }
   for (int k = 0; k < 2; ++k) {
     pre[k] = q;
+    q += LD * H;
+    hs[k] = q;
     q += LD * H;
   }
   for (int k = 0; k < 2; ++k) {
@@ -105,17 +108,17 @@ __global__ void __launch_bounds__(THREADS) k_towers(const float* __restrict__ x,
       float acc = __ldg(tw[k].b0 + j);
       for (int c = 0; c < nin; ++c) acc = fmaf(__ldg(w0 + j * nin + c), xs[k][c * LD + r], acc);
       pre[k][j * LD + r] = acc;
+      hs[k][j * LD + r] = prelu(acc, __ldg(tw[k].a0 + j));
     }
   }
   __syncthreads();
   // layer 1: rep[o][r] = b1[o] + sum_j W1[o][j] prelu(pre[j][r])
   for (int k = 0; k < 2; ++k) {
     const float* w1 = tw[k].w1;
-    const float* a0 = tw[k].a0;
     for (int i = t; i < R * BT; i += THREADS) {
       const int o = i / BT, r = i % BT;
       float acc = __ldg(tw[k].b1 + o);
-      for (int j = 0; j < H; ++j) acc = fmaf(__ldg(w1 + o * H + j), prelu(pre[k][j * LD + r], __ldg(a0 + j)), acc);
+      for (int j = 0; j < H; ++j) acc = fmaf(__ldg(w1 + o * H + j), hs[k][j * LD + r], acc);
       rep[k][o * LD + r] = acc;
     }
   }
@@ -157,10 +160,9 @@ __global__ void __launch_bounds__(THREADS) k_towers(const float* __restrict__ x,
     // layer 1 weights: dW1[o][j] = sum_r dr[o][r] h[j][r]; db1[o] = sum_r dr[o][r]
     for (int i = t; i < R * H; i += THREADS) {
       const int o = i / H, j = i % H;
-      const float al = __ldg(T.a0 + j);
       float acc = 0.f;
 #pragma unroll 8
-      for (int r = 0; r < BT; ++r) acc = fmaf(dr[o * LD + r], prelu(pre[k][j * LD + r], al), acc);
+      for (int r = 0; r < BT; ++r) acc = fmaf(dr[o * LD + r], hs[k][j * LD + r], acc);
       out[T.g_w1 + i] = acc;
     }
     for (int o = t; o < R; o += THREADS) {
