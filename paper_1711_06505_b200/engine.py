@@ -2,7 +2,8 @@
 (reference training.py:66-91) and, in ``runtime.ClusterEngine``, behind one
 rank of ``Cluster.run_iteration`` (runtime.py:370-470).
 
-One step, all on one CUDA stream, no host round trip until the loss is read:
+One step, no host round trip until the loss is read (the ID chain and the
+partial reduces run on a forked stream, see forward_backward):
 
   H2D    one packed copy of the CSR batch (ids, offsets, labels)
   a2     dicm_dedup over the image keys    -> unique pool rows + inverse
@@ -25,6 +26,7 @@ reference's exception when it reads the status.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -604,7 +606,7 @@ class StepEngine:
                                         self.keyproj.data_ptr(), self.s))
         return bv
 
-    def _local_step(self, emb, d_emb, denom):
+    def _local_step(self, emb, d_emb, denom, reduce=True):
         """a6-a12 forward and backward on the local batch: pooling, head, BCE.
         Reads image embeddings ``emb`` and compact ID rows ``self.id_rows``;
         writes ``d_emb`` / ``self.d_rows`` and the head/attention gradients."""
@@ -622,26 +624,72 @@ class StepEngine:
         L.check(L.lib.dicm_sample_bwd(C.byref(self.layout), C.byref(bv), self.attn, self.head_in.data_ptr(),
                                       self.d_head_in.data_ptr(), self.scores.data_ptr(), self.stats.data_ptr(),
                                       d_emb.data_ptr(), self.d_rows.data_ptr(), self.attn_partial.data_ptr(), s))
+        if reduce:
+            self._reduce_partials(s)
+
+    def _reduce_partials(self, s):
+        """Head and attention parameter gradients from their block partials
+        (fixed-order reduces)."""
+        B = self.pk.B
         h0, h1 = self.head_range
         if not self.wide_head:
-            L.check(L.lib.dicm_reduce_partials(self.head_part.data_ptr(), nhb, h1 - h0,
+            L.check(L.lib.dicm_reduce_partials(self.head_part.data_ptr(), self._head_blocks(B), h1 - h0,
                                                self.grad.data_ptr() + 4 * h0, 0, s))
         if self.attn_range is not None:
             a0, a1 = self.attn_range
             L.check(L.lib.dicm_reduce_partials(self.attn_partial.data_ptr(), L.lib.dicm_sample_blocks(B), a1 - a0,
                                                self.grad.data_ptr() + 4 * a0, 0, s))
 
+    _rows_checked = False  # dRows already checked on the forked stream this step
+
+    def _side_stream(self):
+        """Stream for the forked ID chain (None: everything on one stream;
+        DICM_FORK=0 turns the fork off)."""
+        if os.environ.get("DICM_FORK", "1") == "0":
+            return None
+        side = getattr(self, "_side", None)
+        if side is None:
+            side = self._side = torch.cuda.Stream(device=self.dev)
+        return side
+
     def forward_backward(self, db, denominator=None):
         """Everything up to (and including) the dense gradients."""
         self._begin(db)
         denom = float(db.pk.B if denominator is None else denominator)
-        self._dedup_images()
-        self._dedup_ids()
+        side = self._side_stream()
+        if side is not None:
+            # the ID chain (dedup over every field -> compact rows) shares no
+            # buffer with the image chain; it runs on a forked stream and joins
+            # before the per-sample kernels (a graph branch once captured)
+            main = self.s
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                self.s = side.cuda_stream
+                self._dedup_ids()
+                self._gather_id_rows()
+            self.s = main
+            self._dedup_images()
+        else:
+            self._dedup_images()
+            self._dedup_ids()
         if self.n_img_segs:
             self._image_forward(self.net, self.uniq_img, self.counts.data_ptr())
-        self._gather_id_rows()
-        self._local_step(self.net.emb, self.net.d_emb, denom)
+        if side is not None:
+            torch.cuda.current_stream().wait_stream(side)
+        else:
+            self._gather_id_rows()
+        self._local_step(self.net.emb, self.net.d_emb, denom, reduce=side is None)
+        if side is not None:  # the partial reduces overlap the image-MLP backward
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                self._reduce_partials(side.cuda_stream)
+                # the row-gradient finite check (optimizer_step) needs only dRows
+                L.check(L.lib.dicm_check_finite(self.d_rows.data_ptr(), self.cap_k * 12, self.counts[1:].data_ptr(),
+                                                12, 4, self.status.data_ptr(), side.cuda_stream))
+            self._rows_checked = True
         self._image_backward(self.net, self.uniq_img, self.counts.data_ptr(), self.cap_u if self.n_img_segs else 0)
+        if side is not None:
+            torch.cuda.current_stream().wait_stream(side)
         return self.loss
 
     def optimizer_step(self, lr, row_keys=None, row_count=None, row_grads=None, row_cap=None, tabstate=None):
@@ -652,7 +700,9 @@ class StepEngine:
         row_grads = self.d_rows if row_grads is None else row_grads
         row_cap = self.cap_k if row_cap is None else row_cap
         tabstate = self.tabstate if tabstate is None else tabstate
-        L.check(L.lib.dicm_check_finite(row_grads.data_ptr(), row_cap * 12, row_count.data_ptr(), 12, 4, st, s))
+        if not (self._rows_checked and row_grads is self.d_rows):
+            L.check(L.lib.dicm_check_finite(row_grads.data_ptr(), row_cap * 12, row_count.data_ptr(), 12, 4, st, s))
+        self._rows_checked = False
         L.check(L.lib.dicm_adam_dense(self.model.dense.data_ptr(), self.grad.data_ptr(), self.m.data_ptr(),
                                       self.v.data_ptr(), self.t.data_ptr(), self.spans, len(self.spans), lr, BETA1,
                                       BETA2, EPS, self.adam_ws.data_ptr(), self.adam_ws.numel(), st, s))
