@@ -89,6 +89,19 @@ __device__ __forceinline__ int num_sms() {
   return 148;
 }
 
+// (d0, d1) = fma((a0, a1), (b, b), (d0, d1)) as one paired FFMA2: two
+// independent fma.rn results, bit-identical to two fmaf calls
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b) {
+  asm("{\n\t.reg .b64 ra, rb, rc;\n\t"
+      "mov.b64 ra, {%2, %3};\n\t"
+      "mov.b64 rb, {%4, %4};\n\t"
+      "mov.b64 rc, {%0, %1};\n\t"
+      "fma.rn.f32x2 rc, ra, rb, rc;\n\t"
+      "mov.b64 {%0, %1}, rc;\n\t}"
+      : "+f"(d0), "+f"(d1)
+      : "f"(a0), "f"(a1), "f"(b));
+}
+
 }  // namespace dicm
 
 // launch helpers ------------------------------------------------------------

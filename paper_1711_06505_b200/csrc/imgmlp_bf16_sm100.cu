@@ -133,7 +133,9 @@ __global__ void __launch_bounds__(F_THREADS, 1)
     sb1[t] = b1[t];
     sal1[t] = al1[t];
   }
-  for (int i = t; i < 768; i += F_THREADS) sw2[i] = w2[i];
+  // W2 [12][64] transposed to [64][12]: one hidden unit's 12 weights are
+  // three 16-B shared loads feeding six paired FMAs
+  for (int i = t; i < 768; i += F_THREADS) sw2[(i & 63) * 12 + (i >> 6)] = w2[i];
   if (t < 12) sb2[t] = b2[t];
   if (warp == 1) {
     tmem_alloc(slot, 128);
@@ -229,8 +231,14 @@ __global__ void __launch_bounds__(F_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const float h = prelu(a[i], sal1[32 * hh + i]);
-#pragma unroll
-          for (int c = 0; c < 12; ++c) e[c] = fmaf(sw2[c * 64 + 32 * hh + i], h, e[c]);
+          const float4* wv = reinterpret_cast<const float4*>(sw2 + (32 * hh + i) * 12);
+          const float4 w0 = wv[0], w1 = wv[1], w2v = wv[2];
+          ffma2(e[0], e[1], w0.x, w0.y, h);
+          ffma2(e[2], e[3], w0.z, w0.w, h);
+          ffma2(e[4], e[5], w1.x, w1.y, h);
+          ffma2(e[6], e[7], w1.z, w1.w, h);
+          ffma2(e[8], e[9], w2v.x, w2v.y, h);
+          ffma2(e[10], e[11], w2v.z, w2v.w, h);
         }
         epi::store_bf16(a, scr, lane, m0 + q * 32, U, [&](int r) { return act1 + (int64_t)r * H2 + 32 * hh; });
       }
@@ -401,10 +409,7 @@ __global__ void __launch_bounds__(B_THREADS, 1)
         }
         float dh0 = 0.f, dh1 = 0.f;
 #pragma unroll
-        for (int c = 0; c < 12; ++c) {
-          dh0 = fmaf(d[c], w2c[0][c], dh0);
-          dh1 = fmaf(d[c], w2c[1][c], dh1);
-        }
+        for (int c = 0; c < 12; ++c) ffma2(dh0, dh1, w2c[0][c], w2c[1][c], d[c]);  // paired fma.rn
         const bool p0 = a.x > 0.f, p1 = a.y > 0.f;
         const float dd0 = p0 ? dh0 : alj0 * dh0, dd1 = p1 ? dh1 : alj1 * dh1;
         acc_a1[0] = fmaf(p0 ? 0.f : a.x, dh0, acc_a1[0]);
@@ -413,10 +418,7 @@ __global__ void __launch_bounds__(B_THREADS, 1)
         acc_b1[1] += dd1;
         const float h0 = p0 ? a.x : alj0 * a.x, h1 = p1 ? a.y : alj1 * a.y;
 #pragma unroll
-        for (int c = 0; c < 12; ++c) {
-          accw[0][c] = fmaf(d[c], h0, accw[0][c]);
-          accw[1][c] = fmaf(d[c], h1, accw[1][c]);
-        }
+        for (int c = 0; c < 12; ++c) ffma2(accw[0][c], accw[1][c], h0, h1, d[c]);
         if (jp < 6 && valid) {
           const float2 db = reinterpret_cast<const float2*>(sdE + r * 3)[jp];
           acc_b2[0] += db.x;

@@ -520,8 +520,16 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
       if (!pos) acc.a0 = fmaf(pre, dh, acc.a0);
       acc.b0 += dpre;
       dP += dpre;
-#pragma unroll
-      for (int c = 0; c < DICM_D; ++c) acc.wk[c] = fmaf(dpre, ws.ks[r][c], acc.wk[c]);
+      {  // paired FMAs (FFMA2), same per-element fma.rn as before
+        const float4* kr = reinterpret_cast<const float4*>(ws.ks[r]);
+        const float4 k0 = kr[0], k1 = kr[1], k2 = kr[2];
+        ffma2(acc.wk[0], acc.wk[1], k0.x, k0.y, dpre);
+        ffma2(acc.wk[2], acc.wk[3], k0.z, k0.w, dpre);
+        ffma2(acc.wk[4], acc.wk[5], k1.x, k1.y, dpre);
+        ffma2(acc.wk[6], acc.wk[7], k1.z, k1.w, dpre);
+        ffma2(acc.wk[8], acc.wk[9], k2.x, k2.y, dpre);
+        ffma2(acc.wk[10], acc.wk[11], k2.z, k2.w, dpre);
+      }
       ws.dp[r][lane] = dpre;
     }
     __syncwarp();
@@ -533,9 +541,16 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
         const float4 d4 = reinterpret_cast<const float4*>(ws.dp[lane])[q];
         const float dq4[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-#pragma unroll
-          for (int c = 0; c < DICM_D; ++c) dk[c] = fmaf(s.wk[4 * q + e][c], dq4[e], dk[c]);
+        for (int e = 0; e < 4; ++e) {
+          const float4* wr = reinterpret_cast<const float4*>(s.wk[4 * q + e]);
+          const float4 w0 = wr[0], w1 = wr[1], w2 = wr[2];
+          ffma2(dk[0], dk[1], w0.x, w0.y, dq4[e]);
+          ffma2(dk[2], dk[3], w0.z, w0.w, dq4[e]);
+          ffma2(dk[4], dk[5], w1.x, w1.y, dq4[e]);
+          ffma2(dk[6], dk[7], w1.z, w1.w, dq4[e]);
+          ffma2(dk[8], dk[9], w2.x, w2.y, dq4[e]);
+          ffma2(dk[10], dk[11], w2.z, w2.w, dq4[e]);
+        }
       }
       red_row12(a.d_emb + (int64_t)row * DICM_D, dk);
     }
