@@ -166,31 +166,59 @@ __device__ __forceinline__ float query_proj(const AttnSmem& s, const float (&q)[
 }
 
 // the key half of the attention net's first layer, once per unique image:
-// kp[u][j] = Wk[j] . E[u].  Thread = (image, 4 hidden units): 8 threads share
-// an embedding row (one L1 line), each writes one float4 -- one independent
-// load chain per thread, so occupancy hides the latency.
+// kp[u][j] = Wk[j] . E[u].  Thread = image: one 48-B row load, 32 outputs
+// from Wk^T in shared memory (16-B broadcast reads feeding paired FMAs, the
+// same per-output fma order over the 12 columns as a scalar loop), one 128-B
+// row store -- so a thread has a single load latency per image and the whole
+// grid's rows are in flight at once.
 __global__ void __launch_bounds__(256) k_keyproj(const float* __restrict__ w0, int dq, const float* __restrict__ emb,
                                                  const int32_t* __restrict__ count, int64_t u_cap,
                                                  float* __restrict__ kp) {
+  __shared__ __align__(16) float wkT[DICM_D][DICM_ATT];
+  __shared__ __align__(16) float ob[8][32][DICM_ATT + 4];  // per-warp output rows, 144-B stride
+  for (int i = threadIdx.x; i < DICM_ATT * DICM_D; i += blockDim.x) {
+    const int j = i / DICM_D, c = i % DICM_D;
+    wkT[c][j] = __ldg(w0 + j * (dq + DICM_D) + dq + c);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = min((int64_t)*count, u_cap);
-  const int j0 = (threadIdx.x & 7) * 4;
-  float wk[4][DICM_D];  // this thread's 4 rows of Wk, kept in registers
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t wb = (int64_t)blockIdx.x * blockDim.x + warp * 32; wb < n; wb += step) {
+    const int64_t u = wb + lane;
+    Row12 e;
+    if (u < n) {
+      e = load_row12(emb + u * DICM_D);
+    } else {
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int c = 0; c < DICM_D; ++c) wk[q][c] = __ldg(w0 + (j0 + q) * (dq + DICM_D) + dq + c);
-  const int64_t step = (int64_t)gridDim.x * (blockDim.x >> 3);
-  for (int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); u < n; u += step) {
-    const Row12 e = load_row12(emb + u * DICM_D);
-    float o[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float acc = 0.f;
-#pragma unroll
-      for (int c = 0; c < DICM_D; ++c) acc = fmaf(wk[q][c], e.v[c], acc);
-      o[q] = acc;
+      for (int c = 0; c < DICM_D; ++c) e.v[c] = 0.f;
     }
-    *reinterpret_cast<float4*>(kp + u * DICM_ATT + j0) = make_float4(o[0], o[1], o[2], o[3]);
+    float o[DICM_ATT];
+#pragma unroll
+    for (int j = 0; j < DICM_ATT; ++j) o[j] = 0.f;
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) {
+      const float4* w = reinterpret_cast<const float4*>(wkT[c]);
+#pragma unroll
+      for (int q = 0; q < DICM_ATT / 4; ++q) {
+        const float4 wq = w[q];
+        ffma2(o[4 * q], o[4 * q + 1], wq.x, wq.y, e.v[c]);
+        ffma2(o[4 * q + 2], o[4 * q + 3], wq.z, wq.w, e.v[c]);
+      }
+    }
+    // the warp's 32 rows are one contiguous 4-KB block of kp: transpose
+    // through shared memory so every store instruction writes 512 B
+    float4* mine = reinterpret_cast<float4*>(ob[warp][lane]);
+#pragma unroll
+    for (int q = 0; q < DICM_ATT / 4; ++q) mine[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+    __syncwarp();
+    float4* dst = reinterpret_cast<float4*>(kp + wb * DICM_ATT);
+#pragma unroll
+    for (int q = 0; q < DICM_ATT / 4; ++q) {
+      const int f = q * 32 + lane, row = f >> 3;
+      if (wb + row < n) dst[f] = reinterpret_cast<const float4*>(ob[warp][row])[f & 7];
+    }
+    __syncwarp();
   }
 }
 
@@ -751,7 +779,7 @@ int dicm_attn_keyproj(const dicm_layout_t* layout, const dicm_attn_params_t* att
   using namespace dicm;
   if (!(layout->kind == 1 || layout->kind == 2) || !layout->use_behavior_images || u_cap <= 0) return DICM_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  const int grid = dicm_grid(u_cap * 8, 256, 148 * 8);
+  const int grid = dicm_grid(u_cap, 256, 148 * 8);
   k_keyproj<<<grid, 256, 0, st>>>(attn[0].w0, DICM_D, emb, count_dev, u_cap, keyproj);
   if (layout->kind == 2)
     k_keyproj<<<grid, 256, 0, st>>>(attn[1].w0, DICM_D * layout->n_query, emb, count_dev, u_cap,
