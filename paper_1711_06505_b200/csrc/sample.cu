@@ -23,6 +23,7 @@
 // Every per-reference loop keeps several independent row loads in flight per
 // lane (the index -> row gather chain is L2-latency bound otherwise).
 #include <climits>
+#include <stdlib.h>
 #include <math.h>
 
 #include "common.cuh"
@@ -805,6 +806,46 @@ int dicm_sample_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
   return last_launch("dicm_sample_fwd");
 }
 
+// k_sample_scatter shares no input it writes with k_attn_bwd (both only add
+// into d_emb / d_rows with red.add), so it runs on a forked stream beside the
+// attention backward and fills the SMs its second wave leaves idle.  One side
+// stream and event pair per host thread and device (event reuse across
+// threads would let one thread's fork wait on another's record); under graph
+// capture the fork/join become parallel branches.  DICM_FORK=0 (all forks)
+// or DICM_SAMPLE_FORK=0 (this one) turns it off.
+struct SideFork {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+static SideFork* side_fork() {
+  static const bool off = [] {
+    const char* e = getenv("DICM_FORK");
+    const char* e2 = getenv("DICM_SAMPLE_FORK");
+    return (e && e[0] == '0') || (e2 && e2[0] == '0');
+  }();
+  if (off) return nullptr;
+  constexpr int kMaxDev = 64;
+  thread_local SideFork forks[kMaxDev];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+  SideFork& f = forks[dev];
+  if (!f.side) {
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    const bool ok = cudaStreamCreateWithFlags(&f.side, cudaStreamNonBlocking) == cudaSuccess &&
+                    cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming) == cudaSuccess &&
+                    cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming) == cudaSuccess;
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    if (!ok) {
+      cudaGetLastError();
+      f.side = nullptr;
+      return nullptr;
+    }
+  }
+  return &f;
+}
+
 int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const dicm_attn_params_t* attn,
                     const float* head_in, const float* d_head_in, const float* scores, const float* stats,
                     float* d_emb, float* d_rows, float* attn_partials, dicm_stream_t stream) {
@@ -827,8 +868,17 @@ int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
   const int64_t stride = part_size(layout);
   {
     const int probe_slot = probe_begin(DICM_PROBE_SAMPLE_BWD, st);
-    k_sample_scatter<<<grid, BWD_WARPS * 32, 0, st>>>(a);
-    if (layout->use_behavior_images && (layout->kind == 1 || layout->kind == 2)) {
+    const bool attn_chan = layout->use_behavior_images && (layout->kind == 1 || layout->kind == 2);
+    SideFork* fk = attn_chan ? side_fork() : nullptr;
+    if (fk) {
+      cudaEventRecord(fk->fork, st);
+      cudaStreamWaitEvent(fk->side, fk->fork, 0);
+      k_sample_scatter<<<grid, BWD_WARPS * 32, 0, fk->side>>>(a);
+      cudaEventRecord(fk->join, fk->side);
+    } else {
+      k_sample_scatter<<<grid, BWD_WARPS * 32, 0, st>>>(a);
+    }
+    if (attn_chan) {
       // partial row layout in sorted names: attn/id/* before attn/img/*
       int64_t img_off = 0;
       if (layout->kind == 2) {
@@ -840,6 +890,7 @@ int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
       }
       k_attn_bwd<DICM_D><<<grid, BWD_WARPS * 32, smem, st>>>(a, 0, stride, img_off);
     }
+    if (fk) cudaStreamWaitEvent(st, fk->join, 0);
     probe_end(probe_slot, st);
   }
   return last_launch("dicm_sample_bwd");
