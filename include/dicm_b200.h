@@ -195,6 +195,10 @@ int dicm_sample_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv,
                     const dicm_attn_params_t* attn /* [2]: img, id */, float* head_in,
                     float* scores /* [2, R] */, float* stats /* [2, B, 2] */,
                     dicm_stream_t stream);
+/* Stream-ordered on `stream` like every entry point. For the attention
+ * aggregators the scatter kernel runs on a library-owned side stream forked
+ * from `stream` and joined before the call returns (a parallel branch under
+ * graph capture); DICM_FORK=0 or DICM_SAMPLE_FORK=0 keeps it on `stream`. */
 int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv,
                     const dicm_attn_params_t* attn, const float* head_in, const float* d_head_in,
                     const float* scores, const float* stats, float* d_emb /* [U,12], zeroed */,
