@@ -201,6 +201,35 @@ def image_mlp_bwd(p, cache, dE):
     return g, da0
 
 
+def image_mlp_fwd_rows(p, rows_of, uniq, chunk=1 << 15):
+    """image_mlp_fwd over ``rows_of(ids) -> [n, d_raw] f64`` in row chunks,
+    for row counts whose [U, d_raw] f64 feature matrix does not fit host
+    memory (the compact monotone remap of SURVEY.md 8c: every op is row-local,
+    so chunking changes nothing but the order of the f64 sums).  The cache
+    keeps the activations, not X: the backward re-reads the rows."""
+    U = len(uniq)
+    E = np.zeros((U, p["img/2/w"].shape[0]))
+    a0s, h1s, a1s, h2s = [], [], [], []
+    for s0 in range(0, U, chunk):
+        e, (_, a0, h1, a1, h2) = image_mlp_fwd(p, rows_of(uniq[s0:s0 + chunk]))
+        E[s0:s0 + len(e)] = e
+        a0s.append(a0), h1s.append(h1), a1s.append(a1), h2s.append(h2)
+    cat = (lambda xs, w: np.concatenate(xs) if xs else np.zeros((0, w)))
+    return E, (None, cat(a0s, p["img/0/w"].shape[0]), cat(h1s, p["img/0/w"].shape[0]),
+               cat(a1s, p["img/1/w"].shape[0]), cat(h2s, p["img/1/w"].shape[0]))
+
+
+def image_mlp_bwd_rows(p, cache, dE, rows_of, uniq, chunk=1 << 15):
+    """image_mlp_bwd with dW0 = da0^T X accumulated over row chunks of X."""
+    _, a0, h1, a1, h2 = cache
+    g, da0 = image_mlp_bwd(p, (np.zeros((len(uniq), 0)), a0, h1, a1, h2), dE)
+    gw0 = np.zeros((a0.shape[1], p["img/0/w"].shape[1]))
+    for s0 in range(0, len(uniq), chunk):
+        gw0 += da0[s0:s0 + chunk].T @ rows_of(uniq[s0:s0 + chunk])
+    g["img/0/w"] = gw0
+    return g, da0
+
+
 # ---------------------------------------------------------------------------
 # attentive pooling (reference model.py:206-215, autograd.py:322-352)
 # ---------------------------------------------------------------------------
@@ -259,8 +288,11 @@ def forward_backward(p, cfg, batch, pool, denominator=None, want_grads=True):
     d_id = cfg["d_id"]
     keys = needed_image_keys(cfg, batch)
     uniq, _ = dedup(keys)
-    X = np.asarray(pool, dtype=np.float64)[uniq] if len(uniq) else np.zeros((0, cfg["d_raw"]))
-    E, img_cache = image_mlp_fwd(p, X)
+    if callable(pool):  # rows on demand (chunked image MLP)
+        E, img_cache = image_mlp_fwd_rows(p, pool, uniq)
+    else:
+        X = np.asarray(pool, dtype=np.float64)[uniq] if len(uniq) else np.zeros((0, cfg["d_raw"]))
+        E, img_cache = image_mlp_fwd(p, X)
 
     parts, field_vecs, field_info = [], {}, {}
     for name, _vocab, multi in cfg["fields"]:
@@ -399,7 +431,10 @@ def forward_backward(p, cfg, batch, pool, denominator=None, want_grads=True):
         np.add.at(rows, inv, g)
         tgrads[name] = (u, rows)
 
-    ig, da0 = image_mlp_bwd(p, img_cache, dE)
+    if callable(pool):
+        ig, da0 = image_mlp_bwd_rows(p, img_cache, dE, pool, uniq)
+    else:
+        ig, da0 = image_mlp_bwd(p, img_cache, dE)
     grads.update(ig)
     out.update(grads=grads, tgrads=tgrads, dE=dE, da0=da0)
     return out

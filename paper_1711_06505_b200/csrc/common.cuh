@@ -1,5 +1,6 @@
 // Shared definitions for the DICM B200 kernels (sm_100a).
 #pragma once
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -110,4 +111,17 @@ static inline int dicm_grid(int64_t n, int tpb, int cap = 148 * 16) {
   if (g < 1) g = 1;
   if (g > cap) g = cap;
   return (int)g;
+}
+
+// Upper bound on the CTA count of the persistent image-MLP kernels
+// (DICM_GRID_CAP, read once per process; default one CTA per SM).  The parity
+// tests set it small so that every CTA loops over many row tiles -- the TMEM
+// double-buffer and mbarrier phase wrap-around the bench shapes exercise.
+static inline int64_t dicm_grid_cap() {
+  static const int64_t cap = [] {
+    const char* e = getenv("DICM_GRID_CAP");
+    const long v = e ? atol(e) : 0;
+    return v > 0 && v < 148 ? (int64_t)v : (int64_t)148;
+  }();
+  return cap;
 }

@@ -728,7 +728,9 @@ int smem_attr3(K kernel, size_t bytes) {
                     "bf16 small-layer smem attribute");
 }
 
-int grid_tiles(int64_t rows_max) { return (int)std::max<int64_t>(1, std::min<int64_t>(148, (rows_max + 127) / 128)); }
+int grid_tiles(int64_t rows_max) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(dicm_grid_cap(), (rows_max + 127) / 128));
+}
 
 }  // namespace
 

@@ -943,7 +943,7 @@ int make_map(CUtensorMap* m, const void* ptr, bool bf16, uint64_t rows, uint64_t
 
 int nsplit_for(int64_t rows_max, int d_raw) {
   const int tiles = d_raw / 256;
-  const int64_t want = std::max(148 / tiles, 1);  // one wave of CTAs
+  const int64_t want = std::max<int64_t>(dicm_grid_cap() / tiles, 1);  // one wave of CTAs
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, (rows_max + 255) / 256));
 }
 
@@ -1007,7 +1007,7 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
   if (pair) {
     if ((rc = make_map(&map, wsrc, bf16, 256, d_raw, 128))) return rc;
     // persistent CTA pairs: <= 74 clusters of 2 (one CTA per SM)
-    const int grid = 2 * (int)std::min<int64_t>(74, (rows_max + 255) / 256);
+    const int grid = 2 * (int)std::min<int64_t>(std::max<int64_t>(dicm_grid_cap() / 2, 1), (rows_max + 255) / 256);
     // ring depths: 6 gather slots and 6 W0 slots; deeper rings (8/5, 7/6)
     // measured no faster (the pipeline is not bound by stage turnaround)
     static int a66 = -1, t66 = -1;
@@ -1028,7 +1028,7 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
         attr = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes),
                           "k_fwd4 smem");
       if (attr) return attr;
-      const int grid4 = 2 * (int)std::min<int64_t>(74, (rows_max + 511) / 512);
+      const int grid4 = 2 * (int)std::min<int64_t>(std::max<int64_t>(dicm_grid_cap() / 2, 1), (rows_max + 511) / 512);
       kern<<<grid4, THREADS_F4, bytes, st>>>(map, pool, d_raw, rows, count, b0, act0);
       return 0;
     };
@@ -1041,7 +1041,7 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
     return last_launch("tcgen05 layer-0 forward (CTA pairs)");
   }
   if ((rc = make_map(&map, wsrc, bf16, 256, d_raw, 256))) return rc;
-  const int grid = (int)std::min<int64_t>(148, (rows_max + 255) / 256);  // persistent: <= one CTA per SM
+  const int grid = (int)std::min<int64_t>(dicm_grid_cap(), (rows_max + 255) / 256);  // persistent: <= one CTA per SM
   if (bf16) {
     static int once = set_smem(k_fwd<1>);
     if (once) return once;

@@ -494,8 +494,12 @@ int smem_attr(K kernel, size_t bytes) {
 }  // namespace
 
 int small_part_size() { return PART_B; }
-int small_dw1_blocks(int64_t rows_max) { return (int)std::max<int64_t>(1, std::min<int64_t>(148, (rows_max + 255) / 256)); }
-int small_bwd_blocks(int64_t rows_max) { return (int)std::max<int64_t>(1, std::min<int64_t>(148, (rows_max + 127) / 128)); }
+int small_dw1_blocks(int64_t rows_max) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(dicm_grid_cap(), (rows_max + 255) / 256));
+}
+int small_bwd_blocks(int64_t rows_max) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(dicm_grid_cap(), (rows_max + 127) / 128));
+}
 
 // row-major fp32 [rows, cols] map with box {32 cols, box_rows}
 int map_f32(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows, CUtensorMapSwizzle swz) {
@@ -519,7 +523,7 @@ int fwd_layers12(const float* act0, const int32_t* count, int64_t rows_max, cons
   CUtensorMap ma;
   int rc = map_f32(&ma, act0, rows_max, H1, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148, (rows_max + 127) / 128));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(dicm_grid_cap(), (rows_max + 127) / 128));
   {
     const int probe_slot = probe_begin(DICM_PROBE_IMG_FWD_L12, st);
     k_l12_fwd<<<grid, 256, F_SMEM, st>>>(ma, h1, rows_max, al0, w1, b1, al1, w2, b2, count, act1, emb);

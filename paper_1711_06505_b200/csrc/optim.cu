@@ -63,7 +63,7 @@ __global__ void k_dense_update(float* __restrict__ p, const float* __restrict__ 
                                float* __restrict__ v, const int32_t* __restrict__ t, const __grid_constant__ Spans s,
                                const int32_t* __restrict__ nz, const int32_t* __restrict__ status, float lr, float b1,
                                float b2, float eps, float ln_b1, float ln_b2) {
-  if (status[DICM_ST_NONFINITE] || status[DICM_ST_KEY_FLAG]) return;
+  if (status[DICM_ST_NONFINITE] || status[DICM_ST_KEY_FLAG] || status[DICM_ST_P2P_TIMEOUT]) return;
   const int64_t total = s.off[s.n];
   int cur = -1;
   float c1 = 0.f, c2 = 0.f;
@@ -87,7 +87,7 @@ __global__ void k_dense_update(float* __restrict__ p, const float* __restrict__ 
 
 __global__ void k_dense_steps(int32_t* __restrict__ t, const int32_t* __restrict__ nz, int n,
                               const int32_t* __restrict__ status) {
-  if (status[DICM_ST_NONFINITE] || status[DICM_ST_KEY_FLAG]) return;
+  if (status[DICM_ST_NONFINITE] || status[DICM_ST_KEY_FLAG] || status[DICM_ST_P2P_TIMEOUT]) return;
   const int k = threadIdx.x;
   if (k < n && nz[k]) t[k] += 1;
 }
@@ -103,7 +103,7 @@ struct Tables {
 __global__ void k_rows(const __grid_constant__ Tables tb, const int32_t* __restrict__ keys,
                        const int32_t* __restrict__ count, int64_t max_rows, const float* __restrict__ grads, float lr,
                        float b1, float b2, float eps, float ln_b1, float ln_b2, const int32_t* __restrict__ status) {
-  if (status[DICM_ST_NONFINITE] || status[DICM_ST_KEY_FLAG]) return;
+  if (status[DICM_ST_NONFINITE] || status[DICM_ST_KEY_FLAG] || status[DICM_ST_P2P_TIMEOUT]) return;
   const int64_t n = min((int64_t)*count, max_rows);
   const int lane = threadIdx.x & 31, part = lane % 3, slot = lane / 3;  // lanes 30, 31 idle
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);

@@ -388,13 +388,20 @@ class StepEngine:
         lay = self.model.layout
         return (B if lay.use_ad_image else 0) + (R if lay.use_behavior_images else 0)
 
+    def _need(self, pk):
+        return (pk.total, pk.B, pk.R, pk.n_id(self.fields))
+
     def _ensure(self, pk):
-        B, R = pk.B, pk.R
-        need = (pk.total, B, R, pk.n_id(self.fields))
+        need = self._need(pk)
         if self.cap is not None and all(a <= b for a, b in zip(need, self.cap)):
             return
         if self.cap is not None:  # grow with headroom
             need = tuple(max(int(a * 1.25), b) for a, b in zip(need, self.cap))
+        self._alloc_caps(need)
+
+    def _alloc_caps(self, need):
+        """Every per-batch buffer at capacity ``need`` = (packed int32 words,
+        samples, behaviors, ID references)."""
         total, B, R, n_id = need
         dev = self.dev
         n_img = self._n_img(B, R)
@@ -857,6 +864,9 @@ class StepEngine:
     def raise_status(self):
         """Sync point: raise the reference's exception for a flagged step."""
         st = self.status.cpu().numpy()
+        if st[L.ST_P2P_TIMEOUT]:
+            self.status.zero_()
+            raise RuntimeError("p2p barrier timeout: a peer missed a barrier (the step's updates were skipped)")
         if st[L.ST_KEY_FLAG]:
             self.status.zero_()
             tag, seg = divmod(int(st[L.ST_KEY_SEG]), 16)

@@ -224,6 +224,14 @@ class DicmModel:
     def snapshot(self):
         return {n: p.data for n, p in self.params.items()}
 
+    def sharded(self, world, rank):
+        """A copy that holds only the ID-table rows rank ``rank`` of ``world``
+        owns, with this model's current values (a Cluster rank's working copy
+        of a full model)."""
+        return DicmModel(self.schema, self.aggregator, self.extractor, self.seed, self.mlp_widths,
+                         self.use_ad_image, self.use_behavior_images, device=self.device,
+                         params=self.snapshot(), shard=(world, rank))
+
 
 class PrerankModel(DicmModel):
     """Two-tower pre-rank variant (reference PrerankModel, model.py:420-531):
@@ -253,3 +261,8 @@ class PrerankModel(DicmModel):
         self.aggregator = layout.aggregator
         self.mlp_widths = ()
         self._build(layout, seed, device, params, table_rows, shard, table_init)
+
+    def sharded(self, world, rank):
+        return PrerankModel(self.schema, self.extractor, self.seed, self.user_fields, self.ad_fields,
+                            self.tower_hidden, self.rep_dim, self.use_images, device=self.device,
+                            params=self.snapshot(), shard=(world, rank))

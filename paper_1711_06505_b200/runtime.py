@@ -147,9 +147,12 @@ class PeerExchange:
 
     def __init__(self, world, rank, cap_u, cap_k, local_rows, local_id_space, group=None):
         dev = torch.device("cuda", torch.cuda.current_device())
-        caps = torch.tensor([cap_u, cap_k], dtype=torch.int64, device=dev)
+        # every capacity the layout depends on is agreed (max over ranks):
+        # a peer writes into our region at ITS offsets, so the layout must be
+        # identical everywhere (pool shards differ by one row when P % world)
+        caps = torch.tensor([cap_u, cap_k, local_rows, local_id_space], dtype=torch.int64, device=dev)
         dist.all_reduce(caps, op=dist.ReduceOp.MAX, group=group)
-        cap_u, cap_k = (int(x) for x in caps.cpu().tolist())
+        cap_u, cap_k, local_rows, local_id_space = (int(x) for x in caps.cpu().tolist())
         self.world, self.rank = world, rank
         self.cap_u, self.cap_k = cap_u, cap_k
         self.cap_ri = min(world * cap_u, world * max(local_rows, 1))
@@ -170,6 +173,12 @@ class PeerExchange:
         take("back_img", cap_u * 48)
         take("back_id", cap_k * 48)
         self.off, self.bytes = layout, off
+        lay = torch.tensor([off] + [layout[k] for k in sorted(layout)], dtype=torch.int64, device=dev)
+        lo, hi = lay.clone(), lay.clone()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+        if not torch.equal(lo, hi):
+            raise RuntimeError("peer exchange regions differ between ranks")
         base = C.c_void_p()
         L.check(L.lib.dicm_p2p_alloc(off, C.byref(base)))
         self.base = base.value
@@ -253,6 +262,34 @@ class ClusterEngine(StepEngine):
     @property
     def image_key_space(self):
         return self.pool.global_size  # requests are in global image ids
+
+    declared = None  # (packed words, samples, behaviors, ID refs): Cluster's per-rank maximum
+
+    def declare_capacity(self, batch_per_worker):
+        """Size every buffer once for the largest local batch any rank can see
+        (``batch_per_worker`` samples of at most ``b_max`` behaviors, and
+        multi-hot fields tail-truncated to ``b_max`` like the reference,
+        model.py:168,176).  All ranks compute the same numbers, so the peer
+        exchange built from them never has to grow -- a one-sided regrowth
+        would desynchronise the collective layout."""
+        B, bm = int(batch_per_worker), int(self.model.schema.b_max)
+        fields = self.model.layout.schema.fields
+        n_multi = sum(1 for f in self.fields if f.multi)
+        n_one = len(self.fields) - n_multi
+        R = B * bm
+        n_id = B * n_one + R * n_multi
+        total = sum((R + B + 1) if f.multi else B for f in fields) + 2 * B + R + B + 1
+        self.declared = (total, B, R, n_id)
+
+    def _ensure(self, pk):
+        need = self._need(pk)
+        if self.declared is None:
+            return super()._ensure(pk)
+        if self.cap is None:
+            self._alloc_caps(tuple(max(a, b) for a, b in zip(need, self.declared)))
+        elif not all(a <= b for a, b in zip(need, self.cap)):
+            raise ValueError(f"local batch needs {need}, beyond the declared per-rank capacity {self.cap} "
+                             "(batch_per_worker samples of at most b_max behaviors)")
 
     def _alloc_image_net(self, cap):
         dev, G = self.dev, self.world
@@ -514,8 +551,23 @@ class ClusterEngine(StepEngine):
 
 class Cluster:
     """Multi-GPU AMS cluster (reference runtime.py:313-516), one rank per
-    process.  ``workers == servers == world size``: each GPU is a worker and a
-    server.  Every rank calls ``run_iteration`` with the same union batch."""
+    process; every rank calls ``run_iteration`` with the same union batch.
+
+    ``ClusterConfig(workers=M, servers=N)`` is the reference's LOGICAL actor
+    topology; the physical one is the G GPUs of the process group.  Worker w
+    runs on GPU w * G // M ... each GPU trains the contiguous union slice of
+    the workers it hosts (reference runtime.py:379-382: workers take
+    consecutive ``batch_per_worker`` slices, so a GPU's slice is contiguous
+    too).  Keys are sharded over the G GPUs (owner key % G); logical server s
+    is hosted by GPU s % G.  Placement never changes results (every
+    reduction is per key or a fixed-order sum), so any (M, N) trains exactly
+    like ``LocalTrainer`` on the union batch (runtime.py:19-21).
+
+    ``model`` may be the full model (its values are copied into this rank's
+    shard and ``collect_into_model`` writes the trained values back, like the
+    reference's node replicas, runtime.py:108-111,490-495) or an already
+    sharded one (``DicmModel(..., shard=(G, rank))``, trained in place: the
+    scalable form for tables that do not fit one host)."""
 
     def __init__(self, cfg, model, store, lr0=0.001, lr_decay=0.9, lr_interval=24000, precision="fp32",
                  group=None):
@@ -525,17 +577,20 @@ class Cluster:
                 "accounting-only storage strategy (see dicm.accounting)")
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
-        if cfg.workers != world or cfg.servers != world:
-            raise ValueError(f"this build runs one worker and one server per GPU: workers = servers = world size "
-                             f"({world}), got workers={cfg.workers}, servers={cfg.servers}")
-        self.cfg, self.model, self.store = cfg, model, store
+        self.cfg, self.source_model, self.store = cfg, model, store
         self.world, self.rank = world, rank
         self.lr0, self.lr_decay, self.lr_interval = lr0, lr_decay, lr_interval
+        self.group = group
+        # the contiguous block of logical workers this GPU hosts
+        self.w_lo, self.w_hi = rank * cfg.workers // world, (rank + 1) * cfg.workers // world
+        if world > 1 and getattr(model, "shard", None) is None:
+            model = model.sharded(world, rank)  # this rank's working copy
+        self.model = model
         if world > 1:
             self.engine = ClusterEngine(model, store, precision, lr0, lr_decay, lr_interval, world, rank, group)
+            self.engine.declare_capacity(max(self.w_hi - self.w_lo, 1) * cfg.batch_per_worker)
         else:
             self.engine = StepEngine(model, store, precision, lr0, lr_decay, lr_interval)
-        self.group = group
 
     @property
     def iteration(self):
@@ -544,11 +599,15 @@ class Cluster:
     def local_slice(self, union):
         b = union if isinstance(union, Batch) else encode_batch(union, self.model)
         bpw = self.cfg.batch_per_worker
-        lo = min(self.rank * bpw, b.size)
-        return b.slice(lo, min(b.size, lo + bpw)), b
+        lo = min(self.w_lo * bpw, b.size)
+        return b.slice(lo, min(b.size, self.w_hi * bpw)), b
 
-    def run_iteration(self, union_batch, digests=False):
-        """-> (loss, union_unique, forwards, digests) like runtime.py:465-470."""
+    def run_iteration(self, union_batch, digests=True):
+        """-> (loss, union_unique, forwards, digests) like runtime.py:465-470:
+        the union loss, the union's distinct images, the image-net forwards
+        summed over the servers (== union_unique: each distinct image is
+        embedded once per iteration), and one image-net replica digest per
+        logical server."""
         local, union = self.local_slice(union_batch)
         e = self.engine
         loss = self.train_batch_async(local, union.size)
@@ -559,18 +618,22 @@ class Cluster:
             dist.all_reduce(fw, group=self.group)
             forwards = int(fw.item())
         else:
-            forwards = len(e.unique_images())
+            forwards = len(e.unique_images()) if e.n_img_segs else 0
         lay = self.model.layout
         union_unique = len(union.unique_images(lay.use_ad_image, lay.use_behavior_images))
-        dig = []
-        if digests:
-            d = params_digest({n: p.data for n, p in self.model.params.items() if not n.startswith("id_emb/")})
-            dig = [None] * self.world
-            if self.world > 1:
-                dist.all_gather_object(dig, d, group=self.group)
-            else:
-                dig = [d]
+        dig = self.server_digests() if digests else []
         return value, union_unique, forwards, dig
+
+    def server_digests(self):
+        """params_digest of the image-net replica (reference ServerNode.digest,
+        runtime.py:221-222) for each logical server, computed on the GPU that
+        hosts it."""
+        d = params_digest({n: p.data for n, p in self.model.params.items() if n.startswith("img/")})
+        per_gpu = [d]
+        if self.world > 1:
+            per_gpu = [None] * self.world
+            dist.all_gather_object(per_gpu, d, group=self.group)
+        return [per_gpu[s % self.world] for s in range(self.cfg.servers)]
 
     def train_batch_async(self, local_batch, union_size):
         """This rank's part of an iteration on its already-sliced local batch
@@ -613,9 +676,59 @@ class Cluster:
             raise ValueError("CUDA graphs need the peer-memory exchange (DICM_EXCHANGE=p2p)")
         self.engine.use_graphs = bool(on)
 
+    # -- state assembled from the owning shards (reference runtime.py:474-516)
+
+    def _assemble(self, local, vocab):
+        """Full [vocab, ...] host array from every rank's shard (row r lives
+        on rank r % G at local row r // G); collective: every rank calls it."""
+        if self.world == 1:
+            return local.cpu().numpy()[:vocab]
+        parts = [torch.empty_like(local) for _ in range(self.world)]
+        dist.all_gather(parts, local.contiguous(), group=self.group)
+        out = np.zeros((vocab,) + tuple(local.shape[1:]), dtype=local.cpu().numpy().dtype)
+        for r in range(self.world):
+            n = len(range(r, vocab, self.world))
+            out[r::self.world] = parts[r][:n].cpu().numpy()
+        return out
+
     def snapshot(self):
-        """Dense params (replicated) + this rank's ID-table rows."""
-        return self.model.snapshot()
+        """Every parameter with the ID tables assembled from their shards
+        (reference Cluster.snapshot, runtime.py:474-488); f64 host arrays.
+        Collective when G > 1."""
+        out = {n: p.data for n, p in self.model.params.items() if not n.startswith("id_emb/")}
+        for f in self.model.layout.schema.fields:
+            out[f"id_emb/{f.name}"] = self._assemble(self.model.tables[f.name], f.vocab).astype(np.float64)
+        return out
+
+    def collect_into_model(self):
+        """Write the trained parameters back into the source model
+        (runtime.py:490-495).  A sharded source model already holds its
+        trained shard and is returned as is."""
+        src = self.source_model
+        if src is self.model:
+            return src
+        for n, v in self.snapshot().items():
+            src.params[n].copy_(v)
+        return src
+
+    def optimizer_tensors(self):
+        """Checkpoint-ready Adam state (runtime.py:497-516): ``<name>#m``,
+        ``#v``, ``#t`` for every dense parameter (one replica: they are
+        identical on every rank) and the row-Adam state of every table
+        assembled from the shards.  Collective when G > 1."""
+        e, m = self.engine, self.model
+        t = e.t.cpu().numpy()
+        out = {}
+        for n in m.dense_names:
+            out[f"{n}#m"] = m.dense_view(e.m, n).double().cpu().numpy()
+            out[f"{n}#v"] = m.dense_view(e.v, n).double().cpu().numpy()
+            out[f"{n}#t"] = np.array(int(t[e.span_index[n]]), dtype=np.int64)
+        for f in m.layout.schema.fields:
+            base = f"id_emb/{f.name}"
+            out[f"{base}#m"] = self._assemble(e.tm[f.name], f.vocab).astype(np.float64)
+            out[f"{base}#v"] = self._assemble(e.tv[f.name], f.vocab).astype(np.float64)
+            out[f"{base}#t"] = self._assemble(e.tt[f.name], f.vocab).astype(np.int64)
+        return out
 
 
 def run_training(cluster_cfg, model, store, train_samples, train_cfg, log=None, precision="fp32"):
@@ -637,5 +750,7 @@ def run_training(cluster_cfg, model, store, train_samples, train_cfg, log=None, 
             log.embed_forwards.append(forwards)
             log.replica_digests.append(digests)
             if stop and cluster.iteration >= stop:
+                cluster.collect_into_model()
                 return cluster, log
+    cluster.collect_into_model()
     return cluster, log

@@ -307,3 +307,32 @@ def test_step_graph_launches_only_library_kernels(kind, precision):
     own, total = tr.engine.kernel_nodes()
     assert own == total, (own, total)
     assert 25 <= own <= 50, own
+
+
+def test_single_gpu_cluster_topologies_match_local_trainer():
+    """Cluster(workers=4, servers=2) on one GPU trains the union batch like
+    LocalTrainer (reference tests/test_runtime.py:46-59 asserts <= 1e-6),
+    logs forwards == union unique and one replica digest per logical server,
+    and its snapshot/optimizer_tensors cover every parameter."""
+    from paper_1711_06505_b200.runtime import Cluster, ClusterConfig, run_training
+    from paper_1711_06505_b200.training import LocalTrainer, TrainConfig
+    from paper_1711_06505_b200.batch import synthetic_batch
+    model_c, pool, _ = _bench_like("multiquery-attn", B=32, L=8, P=500)
+    model_l, _, _ = _bench_like("multiquery-attn", B=32, L=8, P=500)
+    cl = Cluster(ClusterConfig(workers=4, servers=2, batch_per_worker=8), model_c, pool)
+    lt = LocalTrainer(model_l, pool, TrainConfig(batch_size=32))
+    rng = np.random.default_rng(4)
+    for _ in range(4):
+        union = synthetic_batch(rng, model_c.schema, 32, rng.integers(0, 9, 32), 500)
+        loss, unique, forwards, digests = cl.run_iteration(union)
+        ref = lt.train_batch(union)
+        assert abs(loss - ref) <= 1e-6 * max(1.0, abs(ref))
+        assert unique == forwards == len(union.unique_images())
+        assert len(digests) == 2 and len(set(digests)) == 1
+        sc, sl = cl.snapshot(), lt.snapshot()
+        worst = max(float(np.max(np.abs(sc[n] - sl[n]))) for n in sl)
+        assert worst < 1e-5, worst
+    opt = cl.optimizer_tensors()
+    for n in model_c.params:
+        assert {f"{n}#m", f"{n}#v", f"{n}#t"} <= set(opt), n
+    assert cl.collect_into_model() is model_c

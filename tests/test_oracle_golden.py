@@ -101,3 +101,35 @@ def test_dedup_is_unique_plus_searchsorted():
     assert np.all(np.diff(u) > 0)
     assert np.array_equal(u[inv], keys)
     assert np.array_equal(u, np.unique(keys))
+
+
+@pytest.mark.parametrize("name", G.FULL)
+def test_chunked_rows_oracle_matches_reference(name):
+    """The chunked image MLP (rows on demand, SURVEY.md 8c's compact remap,
+    used by the bench-shape GPU tests) reproduces the reference goldens."""
+    fx, m, cfg, lay, params = _setup(name)
+    pool = G.pool(fx)
+    batch = O.encode(G.samples(fx, 0), cfg)
+    out = O.forward_backward(params, cfg, batch, lambda ids: np.asarray(pool, np.float64)[ids])
+    assert O.rel_err(out["loss"], fx["s0/loss"]) < TOL
+    assert O.rel_err(out["logits"], fx["s0/logits"]) < TOL
+    for n, g in out["grads"].items():
+        for exp, got in G.golden_view(fx, f"s0/grad/{n}", g):
+            assert O.rel_err(got, exp) < TOL, n
+
+
+def test_chunked_image_mlp_equals_unchunked():
+    rng = np.random.default_rng(0)
+    p = {"img/0/w": rng.normal(size=(16, 64)), "img/0/b": rng.normal(size=16), "img/0/a": np.full(16, .25),
+         "img/1/w": rng.normal(size=(8, 16)), "img/1/b": rng.normal(size=8), "img/1/a": np.full(8, .25),
+         "img/2/w": rng.normal(size=(3, 8)), "img/2/b": rng.normal(size=3)}
+    pool = rng.normal(size=(500, 64))
+    uniq = np.sort(rng.choice(500, 300, replace=False))
+    E, c = O.image_mlp_fwd(p, pool[uniq])
+    dE = rng.normal(size=E.shape)
+    g, da0 = O.image_mlp_bwd(p, c, dE)
+    E2, c2 = O.image_mlp_fwd_rows(p, lambda ids: pool[ids], uniq, chunk=37)
+    g2, da02 = O.image_mlp_bwd_rows(p, c2, dE, lambda ids: pool[ids], uniq, chunk=37)
+    assert O.rel_err(E2, E) < 1e-12 and O.rel_err(da02, da0) < 1e-12
+    for k in g:
+        assert O.rel_err(g2[k], g[k]) < 1e-12, k
