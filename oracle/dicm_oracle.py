@@ -230,6 +230,17 @@ def image_mlp_bwd_rows(p, cache, dE, rows_of, uniq, chunk=1 << 15):
     return g, da0
 
 
+def image_mlp_bwd_from(p, a0, a1, dE, rows_of, uniq, chunk=1 << 15):
+    """image_mlp_bwd from given pre-activations a0 [U, h1], a1 [U, h2] (a
+    device's saved activations): the PReLU branches are those the device took,
+    so the comparison isolates the backward kernels' own rounding -- a flipped
+    branch (|a| below the forward's operand rounding) would otherwise move a
+    gradient entry by a full (1 - alpha) dh."""
+    h1 = prelu(a0, p["img/0/a"])
+    h2 = prelu(a1, p["img/1/a"])
+    return image_mlp_bwd_rows(p, (None, a0, h1, a1, h2), dE, rows_of, uniq, chunk)
+
+
 # ---------------------------------------------------------------------------
 # attentive pooling (reference model.py:206-215, autograd.py:322-352)
 # ---------------------------------------------------------------------------
@@ -275,20 +286,26 @@ def attention_bwd(p, prefix, K, seg, n, normalize, cache, dout, grads):
 # full forward / backward (reference model.py:358-401, training.py:39-42)
 # ---------------------------------------------------------------------------
 
-def forward_backward(p, cfg, batch, pool, denominator=None, want_grads=True):
+def forward_backward(p, cfg, batch, pool, denominator=None, want_grads=True, emb=None):
     """Loss, logits and every parameter gradient of one batch.
 
     ``p``: name -> float64 array (tables included).  ``pool``: [P, d_raw]
     rows the image ids index (the exact rows the device pool holds).
     Table gradients come back compact: ``tgrads[field] = (uniq_ids, rows)``,
     the dense reference gradient restricted to the rows touched.
+
+    ``emb``: image embeddings [U, d_img] aligned with the batch's sorted unique
+    images, used instead of the image MLP (whose gradients are then not
+    formed): checks everything downstream of E against a device's own E.
     """
     B = batch["size"]
     denom = B if denominator is None else denominator
     d_id = cfg["d_id"]
     keys = needed_image_keys(cfg, batch)
     uniq, _ = dedup(keys)
-    if callable(pool):  # rows on demand (chunked image MLP, SURVEY.md 8c)
+    if emb is not None:
+        E, img_cache = np.asarray(emb, dtype=np.float64), None
+    elif callable(pool):  # rows on demand (chunked image MLP, SURVEY.md 8c)
         E, img_cache = image_mlp_fwd_rows(p, pool, uniq)
     else:
         X = np.asarray(pool, dtype=np.float64)[uniq] if len(uniq) else np.zeros((0, cfg["d_raw"]))
@@ -431,7 +448,9 @@ def forward_backward(p, cfg, batch, pool, denominator=None, want_grads=True):
         np.add.at(rows, inv, g)
         tgrads[name] = (u, rows)
 
-    if callable(pool):
+    if img_cache is None:
+        ig, da0 = {}, None
+    elif callable(pool):
         ig, da0 = image_mlp_bwd_rows(p, img_cache, dE, pool, uniq)
     else:
         ig, da0 = image_mlp_bwd(p, img_cache, dE)

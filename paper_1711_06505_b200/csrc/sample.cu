@@ -102,6 +102,7 @@ __device__ __forceinline__ void seg_scatter(const int32_t* __restrict__ ids, int
 struct __align__(16) AttnSmem {
   float wq[DICM_ATT][MAXQ];
   float wk[DICM_ATT][DICM_D];
+  float wkT[DICM_D][DICM_ATT];  // Wk transposed: 8 hidden units per two 16-B reads
   float b0[DICM_ATT], a0[DICM_ATT], w1[DICM_ATT];
   float b1;
 };
@@ -126,10 +127,12 @@ __device__ void load_attn(AttnSmem& s, const dicm_attn_params_t& p, int dq) {
   for (int i = threadIdx.x; i < DICM_ATT * in; i += blockDim.x) {
     const int j = i / in, t = i % in;
     const float v = p.w0[i];
-    if (t < dq)
+    if (t < dq) {
       s.wq[j][t] = v;
-    else
+    } else {
       s.wk[j][t - dq] = v;
+      s.wkT[t - dq][j] = v;
+    }
   }
   for (int j = threadIdx.x; j < DICM_ATT; j += blockDim.x) {
     s.b0[j] = p.b0[j];
@@ -244,6 +247,31 @@ __device__ __forceinline__ void load_kp(const float* p, float4 (&kp)[8]) {
   for (int i = 0; i < 8; ++i) kp[i] = __ldg(q + i);
 }
 
+// score of one reference with its key projection recomputed from the 48-B
+// row (no per-reference projection gather): pre_j = P_j + sum_c Wk[j][c] k_c
+// in ascending c (the order the backward recomputes it in), eight hidden
+// units at a time as paired FMAs from the transposed Wk
+__device__ __forceinline__ float attn_score_rc(const AttnSmem& s, const float* P, const Row12& k) {
+  float sc = s.b1;
+#pragma unroll
+  for (int g = 0; g < DICM_ATT / 8; ++g) {
+    const float4 p0 = reinterpret_cast<const float4*>(P)[2 * g], p1 = reinterpret_cast<const float4*>(P)[2 * g + 1];
+    float pre[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) {
+      const float4* w = reinterpret_cast<const float4*>(&s.wkT[c][8 * g]);
+      const float4 wa = w[0], wb = w[1];
+      ffma2(pre[0], pre[1], wa.x, wa.y, k.v[c]);
+      ffma2(pre[2], pre[3], wa.z, wa.w, k.v[c]);
+      ffma2(pre[4], pre[5], wb.x, wb.y, k.v[c]);
+      ffma2(pre[6], pre[7], wb.z, wb.w, k.v[c]);
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sc = fmaf(s.w1[8 * g + e], prelu(pre[e], s.a0[8 * g + e]), sc);
+  }
+  return sc;
+}
+
 __device__ __forceinline__ float attn_score(const AttnSmem& s, const float* P, const Row12& k) {
   float sc = s.b1;
 #pragma unroll 8
@@ -309,16 +337,20 @@ __device__ void attn_fwd(const Args& a, const AttnSmem& s, int ch, int b, int la
 #pragma unroll
   for (int c = 0; c < DICM_D; ++c) acc[c] = 0.f;
   const bool norm = a.L.normalize != 0;
-  // the next reference's rows are in flight while this one is scored
-  const float* kpb = a.V.keyproj + (int64_t)ch * a.V.kp_stride * DICM_ATT;
-  int32_t un = i0 + lane < i1 ? __ldg(a.V.beh_local + i0 + lane) : 0;
+  // the next reference's row (and the one after's index) are in flight
+  // while this one is scored
+  Row12 k_n;
+  int32_t u_nn = 0;
+  {
+    const int64_t i = i0 + lane;
+    if (i < i1) k_n = load_row12(a.V.emb + (int64_t)__ldg(a.V.beh_local + i) * DICM_D);
+    if (i + 32 < i1) u_nn = __ldg(a.V.beh_local + i + 32);
+  }
   for (int64_t i = i0 + lane; i < i1; i += 32) {
-    const int32_t u = un;
-    if (i + 32 < i1) un = __ldg(a.V.beh_local + i + 32);
-    float4 kp[8];
-    load_kp(kpb + (int64_t)u * DICM_ATT, kp);
-    const Row12 k = load_row12(a.V.emb + (int64_t)u * DICM_D);
-    const float sc = attn_score_kp(s, P, kp);
+    const Row12 k = k_n;
+    if (i + 32 < i1) k_n = load_row12(a.V.emb + (int64_t)u_nn * DICM_D);
+    if (i + 64 < i1) u_nn = __ldg(a.V.beh_local + i + 64);
+    const float sc = attn_score_rc(s, P, k);
     a.scores[(int64_t)ch * a.V.refs + i] = sc;
     if (norm) {
       const float mn = fmaxf(m, sc);
@@ -359,7 +391,7 @@ __device__ void attn_fwd(const Args& a, const AttnSmem& s, int ch, int b, int la
 
 __global__ void __launch_bounds__(FWD_WARPS * 32, 2) k_sample_fwd(const __grid_constant__ Args a) {
   __shared__ AttnSmem sa[2];
-  __shared__ float Pw[FWD_WARPS][DICM_ATT];  // per-warp query projection
+  __shared__ __align__(16) float Pw[FWD_WARPS][DICM_ATT];  // per-warp query projection
   const bool att = a.L.use_behavior_images && (a.L.kind == 1 || a.L.kind == 2);
   if (att) {
     load_attn(sa[0], a.A[0], DICM_D);
@@ -467,7 +499,9 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
     Pj = query_proj<DQ>(s, q, lane);
   }
   const float w1j = s.w1[lane], a0j = s.a0[lane];
-  const float* kpb = a.V.keyproj + (int64_t)ch * a.V.kp_stride * DICM_ATT;
+  float wkj[DICM_D];  // lane j's row of Wk: the key projection is recomputed per reference
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) wkj[c] = s.wk[lane][c];
   float dout[DICM_D];
   const float* dsrc = a.d_head_in + (int64_t)b * a.L.width + a.L.pool_col + ch * DICM_D;
 #pragma unroll
@@ -505,16 +539,6 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
     Row12 k = k_n;
     const int32_t row = row_n;
     const float sci = sc_n;
-    {  // this chunk's key projections -> shared memory, asynchronously
-      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ws.dp[lane]);
-      const float* src = kpb + (int64_t)row * DICM_ATT;
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + 16 * q), "l"(src + 4 * q),
-                     "r"(valid ? 16 : 0)
-                     : "memory");
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
     if (i + 32 < i1) {
       row_n = __ldg(a.V.beh_local + i + 32);
       k_n = load_row12(a.V.emb + (int64_t)row_n * DICM_D);
@@ -535,12 +559,26 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
 #pragma unroll
     for (int c = 0; c < DICM_D; ++c) ws.ks[lane][c] = k.v[c];
     acc.b1 += ds;
-    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
     // lane j: hidden unit j across the chunk's references
     const int nr = (int)min((int64_t)32, i1 - c0);
     for (int r = 0; r < nr; ++r) {
-      const float pre = Pj + ws.dp[r][lane];  // read before dpre replaces it below
+      const float4* kr = reinterpret_cast<const float4*>(ws.ks[r]);
+      const float4 k0 = kr[0], k1 = kr[1], k2 = kr[2];
+      // the forward's pre-activation, same fma order (attn_score_rc)
+      float pre = Pj;
+      pre = fmaf(wkj[0], k0.x, pre);
+      pre = fmaf(wkj[1], k0.y, pre);
+      pre = fmaf(wkj[2], k0.z, pre);
+      pre = fmaf(wkj[3], k0.w, pre);
+      pre = fmaf(wkj[4], k1.x, pre);
+      pre = fmaf(wkj[5], k1.y, pre);
+      pre = fmaf(wkj[6], k1.z, pre);
+      pre = fmaf(wkj[7], k1.w, pre);
+      pre = fmaf(wkj[8], k2.x, pre);
+      pre = fmaf(wkj[9], k2.y, pre);
+      pre = fmaf(wkj[10], k2.z, pre);
+      pre = fmaf(wkj[11], k2.w, pre);
       const float dsr = ws.ds[r];
       const float dh = dsr * w1j;
       const bool pos = pre > 0.f;
@@ -550,8 +588,6 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
       acc.b0 += dpre;
       dP += dpre;
       {  // paired FMAs (FFMA2), same per-element fma.rn as before
-        const float4* kr = reinterpret_cast<const float4*>(ws.ks[r]);
-        const float4 k0 = kr[0], k1 = kr[1], k2 = kr[2];
         ffma2(acc.wk[0], acc.wk[1], k0.x, k0.y, dpre);
         ffma2(acc.wk[2], acc.wk[3], k0.z, k0.w, dpre);
         ffma2(acc.wk[4], acc.wk[5], k1.x, k1.y, dpre);
