@@ -604,9 +604,10 @@ def main():
     # kernel launches inside the timed region: the captured step graph's kernel
     # nodes (this library's only; NCCL / torch nodes excluded) x steps, or the
     # engine's per-call kernel sequence for eager steps
-    kn = eng.kernel_nodes() if graphs else None
+    kn = eng.kernel_nodes(detail=True) if graphs else None
     launches = kn[0] * args.steps if kn else eng.launches_per_step * args.steps
-    launch_src = ({"own_kernels_per_step": kn[0], "kernel_nodes_per_step": kn[1], "source": "captured step graph"}
+    launch_src = ({"own_kernels_per_step": kn[0], "cub_sort_kernels_per_step": kn[1],
+                   "kernel_nodes_per_step": kn[2], "source": "captured step graph"}
                   if kn else {"source": "engine kernel sequence"})
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,

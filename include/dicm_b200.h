@@ -142,8 +142,11 @@ int dicm_imgmlp_bwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
  *   (model.py:206-215, 225-226) and the complementary ID query
  *   (multi-query, model.py:227-229, 381-383).
  * Backward: the same graph reversed (segment_softmax bwd autograd.py:334-337,
- *   col_scale bwd 348-350); embedding and ID-row gradients are scatter-added
- *   into the deduplicated row buffers (np.add.at, autograd.py:267-271);
+ *   col_scale bwd 348-350); embedding and ID-row gradients are summed into
+ *   the deduplicated row buffers (np.add.at, autograd.py:267-271) WITHOUT
+ *   float atomics: every unique key sums its references in ascending
+ *   reference order (the dedup inverse transposed by dicm_ref_transpose), so
+ *   a step is bit-reproducible like the reference's (runtime.py:16-21);
  *   attention-parameter gradients are written as per-block partial sums.
  * ---------------------------------------------------------------------- */
 typedef struct {
@@ -174,20 +177,39 @@ typedef struct {
   const int32_t* beh_local;     /* [R] inverse of the behavior images into emb */
   const int32_t* beh_off;       /* [B+1] */
   const float* emb;             /* [U,12] image embeddings */
-  const float* keyproj;         /* attentive: [channels][kp_stride][32] from dicm_attn_keyproj */
-  int64_t kp_stride;            /* rows per channel in keyproj (>= U) */
+  /* backward only: the ordered per-key sums (see above) */
+  const int32_t* img_order;     /* image references [ad (B, if used) | behaviors (R, if used)] grouped by
+                                   unique image, ascending within a group (dicm_ref_transpose of the inverse) */
+  const int32_t* img_start;     /* [U+1] group starts in img_order */
+  const int32_t* id_order;      /* ID references (fields in schema order) grouped by unique key */
+  const int32_t* id_start;      /* [K+1] */
+  int64_t field_ref_begin[8];   /* first position of each field's references in the ID reference list */
+  const int32_t* beh_seg;       /* [R] sample of each behavior reference (dicm_csr_segments) */
+  const int32_t* field_seg[8];  /* multi-hot fields: [R_f] sample of each reference */
+  const int32_t* n_img_keys;    /* device: U */
+  const int32_t* n_id_keys;     /* device: K */
+  int64_t img_cap, id_cap;      /* capacities of d_emb / d_rows (>= U, K) */
+  float* ref_grad;              /* attn / max / concat: [R, 12] scratch, gradient per behavior reference */
+  float* q_grad;                /* attn: [B, 36] scratch, query gradients (ad image 12 | ID query fields 24) */
+  int32_t* hot;                 /* [2 + img_cap + id_cap] scratch: keys with > 128 references */
 } dicm_batch_view_t;
+
+/* Transpose of a dedup inverse (inv[p] = key of reference p, keys < key_cap):
+ * order[] = 0..n-1 stably sorted by key, start[k] = first slot of key k,
+ * start[last key + 1] = n.  Stream-ordered; ws of dicm_ref_transpose_workspace
+ * bytes.  Replaces nothing in the reference: it fixes the summation order of
+ * np.add.at (autograd.py:267-271) on the device. */
+size_t dicm_ref_transpose_workspace(int64_t n, int64_t key_cap);
+int dicm_ref_transpose(const int32_t* inv, int64_t n, int64_t key_cap, void* ws, size_t ws_bytes,
+                       int32_t* order, int32_t* start /* [key_cap + 1] */, dicm_stream_t stream);
+/* seg[i] = b for off[b] <= i < off[b+1]: the sample of every CSR reference
+ * (the reference's Batch.beh_seg / multihot segment arrays, model.py:144-150) */
+int dicm_csr_segments(const int32_t* off, int batch, int32_t* seg, dicm_stream_t stream);
 
 typedef struct {
   const float *w0, *b0, *a0, *w1, *b1; /* attn/<ch>/0/{w,b,a}, attn/<ch>/1/{w,b} */
 } dicm_attn_params_t;
 
-/* key projections of the attention nets, once per unique image (the key half
- * of W0 [q || k], model.py:208-210, restructured W0 [q||k] = Wq q + Wk k):
- * keyproj[ch][u][j] = Wk_ch[j] . emb[u] for u < *count_dev (channel 1 only for
- * multiquery-attn); no-op for sum pooling */
-int dicm_attn_keyproj(const dicm_layout_t* layout, const dicm_attn_params_t* attn, const float* emb,
-                      const int32_t* count_dev, int64_t u_cap, float* keyproj, dicm_stream_t stream);
 /* number of float partial slots one block writes (attention grads, both channels) */
 int64_t dicm_attn_partial_size(const dicm_layout_t* layout);
 int dicm_sample_blocks(int batch);
@@ -195,14 +217,13 @@ int dicm_sample_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv,
                     const dicm_attn_params_t* attn /* [2]: img, id */, float* head_in,
                     float* scores /* [2, R] */, float* stats /* [2, B, 2] */,
                     dicm_stream_t stream);
-/* Stream-ordered on `stream` like every entry point. For the attention
- * aggregators the scatter kernel runs on a library-owned side stream forked
- * from `stream` and joined before the call returns (a parallel branch under
- * graph capture); DICM_FORK=0 or DICM_SAMPLE_FORK=0 keeps it on `stream`. */
+/* Stream-ordered on `stream`.  Writes every row d_emb[0..U) and
+ * d_rows[0..K) (no zeroing needed); the scratch buffers of the batch view are
+ * overwritten. */
 int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv,
                     const dicm_attn_params_t* attn, const float* head_in, const float* d_head_in,
-                    const float* scores, const float* stats, float* d_emb /* [U,12], zeroed */,
-                    float* d_rows /* [K,12], zeroed */, float* attn_partials,
+                    const float* scores, const float* stats, float* d_emb /* [U,12] */,
+                    float* d_rows /* [K,12] */, float* attn_partials,
                     dicm_stream_t stream);
 
 /* ------------------------------------------------------------------------

@@ -81,10 +81,6 @@ __device__ __forceinline__ Row12 load_row12_cg(const float* p) {
   return r;
 }
 
-__device__ __forceinline__ void atomic_add_row12(float* p, const float* v) {
-#pragma unroll
-  for (int c = 0; c < DICM_D; ++c) atomicAdd(p + c, v[c]);
-}
 
 __device__ __forceinline__ int num_sms() {
   return 148;

@@ -11,14 +11,17 @@
 // the backward pass together with the raw scores.
 //
 // Backward reverses the graph (segment_softmax bwd autograd.py:334-337,
-// col_scale bwd 348-350, linear/prelu bwd 201-204/222-225) and scatter-adds
-// embedding and ID-row gradients into the deduplicated row buffers
-// (np.add.at, autograd.py:267-271) with 16-byte vector reductions
-// (red.global.add.v4.f32: three per 12-float row).  It runs as one scatter
-// kernel (fields, ad image, sum pooling) plus one kernel per attention channel,
-// so each launch carries only the registers its own work needs.
-// Attention-parameter gradients are accumulated lane-per-hidden-unit and
-// written as deterministic block partials.
+// col_scale bwd 348-350, linear/prelu bwd 201-204/222-225).  The embedding and
+// ID-row gradients (np.add.at into the deduplicated rows, autograd.py:267-271)
+// are NOT scattered with float atomics: per-reference gradient rows that are
+// not already a row of the head-input gradient (attention dk, max / concat
+// routing) are written once per reference, per-sample query gradients once
+// per sample, and k_ref_reduce then forms every unique row as the sum of its
+// references in ascending reference order (the dedup inverse transposed by
+// dicm_ref_transpose) -- bit-reproducible like the reference (runtime.py:16-21).
+// Attention runs one kernel per channel, so each launch carries only the
+// registers its own work needs; its parameter gradients are accumulated
+// lane-per-hidden-unit and written as deterministic block partials.
 //
 // Every per-reference loop keeps several independent row loads in flight per
 // lane (the index -> row gather chain is L2-latency bound otherwise).
@@ -37,25 +40,6 @@ constexpr int BWD_WARPS = 8;
 constexpr int MAXQ = 2 * DICM_D;
 constexpr int UNR = 4;  // rows in flight per lane in the gather loops
 
-__device__ __forceinline__ void red_v4(float* p, float a, float b, float c, float d) {
-  asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
-               : "memory");
-}
-// += v into a 12-float row with three 16-byte reductions
-__device__ __forceinline__ void red_row12(float* p, const float (&v)[DICM_D]) {
-  red_v4(p, v[0], v[1], v[2], v[3]);
-  red_v4(p + 4, v[4], v[5], v[6], v[7]);
-  red_v4(p + 8, v[8], v[9], v[10], v[11]);
-}
-// lanes 0-2 add one 16-byte quarter each of the row v (same in every lane)
-__device__ __forceinline__ void red_row12_lanes(float* p, const float (&v)[DICM_D], int lane) {
-  if (lane < 3) {
-    float a = v[0], b = v[1], c = v[2], d = v[3];
-    if (lane == 1) a = v[4], b = v[5], c = v[6], d = v[7];
-    if (lane == 2) a = v[8], b = v[9], c = v[10], d = v[11];
-    red_v4(p + 4 * lane, a, b, c, d);
-  }
-}
 __device__ __forceinline__ void load12(const float* p, float (&v)[DICM_D]) {
   const Row12 r = load_row12(p);
 #pragma unroll
@@ -83,19 +67,6 @@ __device__ __forceinline__ void seg_sum(const int32_t* __restrict__ ids, int64_t
     for (int u = 0; u < UNR; ++u)
 #pragma unroll
       for (int c = 0; c < DICM_D; ++c) acc[c] += r[u].v[c];
-  }
-}
-
-// rows[ids[i]] += v for i in [i0, i1)  (lane-strided, UNR indices in flight)
-__device__ __forceinline__ void seg_scatter(const int32_t* __restrict__ ids, int64_t i0, int64_t i1, float* rows,
-                                            const float (&v)[DICM_D], int lane) {
-  for (int64_t b = i0 + lane; b < i1; b += 32 * UNR) {
-    int id[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) id[u] = b + 32 * u < i1 ? __ldg(ids + b + 32 * u) : -1;
-#pragma unroll
-    for (int u = 0; u < UNR; ++u)
-      if (id[u] >= 0) red_row12(rows + (int64_t)id[u] * DICM_D, v);
   }
 }
 
@@ -167,84 +138,6 @@ __device__ __forceinline__ float query_proj(const AttnSmem& s, const float (&q)[
 #pragma unroll
   for (int t = 0; t < DQ; ++t) p = fmaf(s.wq[j][t], q[t], p);
   return p;
-}
-
-// the key half of the attention net's first layer, once per unique image:
-// kp[u][j] = Wk[j] . E[u].  Thread = image: one 48-B row load, 32 outputs
-// from Wk^T in shared memory (16-B broadcast reads feeding paired FMAs, the
-// same per-output fma order over the 12 columns as a scalar loop), one 128-B
-// row store -- so a thread has a single load latency per image and the whole
-// grid's rows are in flight at once.
-__global__ void __launch_bounds__(256) k_keyproj(const float* __restrict__ w0, int dq, const float* __restrict__ emb,
-                                                 const int32_t* __restrict__ count, int64_t u_cap,
-                                                 float* __restrict__ kp) {
-  __shared__ __align__(16) float wkT[DICM_D][DICM_ATT];
-  __shared__ __align__(16) float ob[8][32][DICM_ATT + 4];  // per-warp output rows, 144-B stride
-  for (int i = threadIdx.x; i < DICM_ATT * DICM_D; i += blockDim.x) {
-    const int j = i / DICM_D, c = i % DICM_D;
-    wkT[c][j] = __ldg(w0 + j * (dq + DICM_D) + dq + c);
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t n = min((int64_t)*count, u_cap);
-  const int64_t step = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t wb = (int64_t)blockIdx.x * blockDim.x + warp * 32; wb < n; wb += step) {
-    const int64_t u = wb + lane;
-    Row12 e;
-    if (u < n) {
-      e = load_row12(emb + u * DICM_D);
-    } else {
-#pragma unroll
-      for (int c = 0; c < DICM_D; ++c) e.v[c] = 0.f;
-    }
-    float o[DICM_ATT];
-#pragma unroll
-    for (int j = 0; j < DICM_ATT; ++j) o[j] = 0.f;
-#pragma unroll
-    for (int c = 0; c < DICM_D; ++c) {
-      const float4* w = reinterpret_cast<const float4*>(wkT[c]);
-#pragma unroll
-      for (int q = 0; q < DICM_ATT / 4; ++q) {
-        const float4 wq = w[q];
-        ffma2(o[4 * q], o[4 * q + 1], wq.x, wq.y, e.v[c]);
-        ffma2(o[4 * q + 2], o[4 * q + 3], wq.z, wq.w, e.v[c]);
-      }
-    }
-    // the warp's 32 rows are one contiguous 4-KB block of kp: transpose
-    // through shared memory so every store instruction writes 512 B
-    float4* mine = reinterpret_cast<float4*>(ob[warp][lane]);
-#pragma unroll
-    for (int q = 0; q < DICM_ATT / 4; ++q) mine[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-    __syncwarp();
-    float4* dst = reinterpret_cast<float4*>(kp + wb * DICM_ATT);
-#pragma unroll
-    for (int q = 0; q < DICM_ATT / 4; ++q) {
-      const int f = q * 32 + lane, row = f >> 3;
-      if (wb + row < n) dst[f] = reinterpret_cast<const float4*>(ob[warp][row])[f & 7];
-    }
-    __syncwarp();
-  }
-}
-
-// score of one reference from its precomputed key projection kp[0..31]
-__device__ __forceinline__ float attn_score_kp(const AttnSmem& s, const float* P, const float4 (&kp)[8]) {
-  float sc = s.b1;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const float k4[4] = {kp[q].x, kp[q].y, kp[q].z, kp[q].w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int j = 4 * q + e;
-      sc = fmaf(s.w1[j], prelu(P[j] + k4[e], s.a0[j]), sc);
-    }
-  }
-  return sc;
-}
-
-__device__ __forceinline__ void load_kp(const float* p, float4 (&kp)[8]) {
-  const float4* q = reinterpret_cast<const float4*>(p);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) kp[i] = __ldg(q + i);
 }
 
 // score of one reference with its key projection recomputed from the 48-B
@@ -487,11 +380,17 @@ struct AttnAcc {
   float b1;  // lane-partial, warp-summed at the end
 };
 
+constexpr int QG_STRIDE = 3 * DICM_D;  // q_grad row: ad image (12) | ID query fields (<= 24)
+
 template <int DQ>
 __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int ch, int b, int lane,
-                         AttnAcc<DQ>& acc) {
+                         AttnAcc<DQ>& acc, bool accumulate) {
   const int64_t i0 = a.V.beh_off[b], i1 = a.V.beh_off[b + 1];
-  if (i1 <= i0) return;
+  if (i1 <= i0) {  // empty segment: no references, a zero query gradient
+    float* qg = a.V.q_grad + (int64_t)b * QG_STRIDE + (ch == 0 ? 0 : DICM_D);
+    if (lane < DQ) qg[lane] = 0.f;
+    return;
+  }
   float Pj;
   {
     float q[DQ];  // reloaded at the end: not live across the reference loops
@@ -617,7 +516,15 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
           ffma2(dk[10], dk[11], w2.z, w2.w, dq4[e]);
         }
       }
-      red_row12(a.d_emb + (int64_t)row * DICM_D, dk);
+      float4* g = reinterpret_cast<float4*>(a.V.ref_grad + i * DICM_D);
+      if (accumulate) {  // the second channel adds to the first's row (fixed order)
+        const Row12 o = load_row12_cg(a.V.ref_grad + i * DICM_D);
+#pragma unroll
+        for (int c = 0; c < DICM_D; ++c) dk[c] = o.v[c] + dk[c];
+      }
+      g[0] = make_float4(dk[0], dk[1], dk[2], dk[3]);
+      g[1] = make_float4(dk[4], dk[5], dk[6], dk[7]);
+      g[2] = make_float4(dk[8], dk[9], dk[10], dk[11]);
     }
     __syncwarp();
   }
@@ -626,18 +533,13 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
   load_query<DQ>(a, ch, b, q);
 #pragma unroll
   for (int t = 0; t < DQ; ++t) ws.wq[lane][t] = fmaf(dP, q[t], ws.wq[lane][t]);
-  float dq[DQ];
+  // the query's gradient, once per sample: ad image (ch 0) at q_grad[b][0..12),
+  // the ID query fields (ch 1) at q_grad[b][12..12+DQ)
+  float* qg = a.V.q_grad + (int64_t)b * QG_STRIDE + (ch == 0 ? 0 : DICM_D);
 #pragma unroll
-  for (int t = 0; t < DQ; ++t) dq[t] = warp_sum(s.wq[lane][t] * dP);
-  if (ch == 0) {
-    red_row12_lanes(a.d_emb + (int64_t)a.V.ad_local[b] * DICM_D, *reinterpret_cast<float(*)[DICM_D]>(dq), lane);
-  } else {
-#pragma unroll
-    for (int f = 0; f < DQ / DICM_D; ++f) {
-      const int fi = a.L.query_field[f];
-      red_row12_lanes(a.d_rows + (int64_t)a.V.field_inv[fi][b] * DICM_D,
-                      *reinterpret_cast<float(*)[DICM_D]>(dq + f * DICM_D), lane);
-    }
+  for (int t = 0; t < DQ; ++t) {
+    const float v = warp_sum(s.wq[lane][t] * dP);
+    if (lane == t) qg[t] = v;
   }
 }
 
@@ -669,13 +571,13 @@ __device__ void zero_acc(AttnAcc<DQ>& acc) {
 
 template <int DQ>
 __device__ void attn_channel_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int ch, int lane, int warp,
-                                 float* red, float* part_base) {
+                                 float* red, float* part_base, bool accumulate) {
   AttnAcc<DQ> acc;
   zero_acc(acc);
 #pragma unroll
   for (int t = 0; t < DQ; ++t) ws.wq[lane][t] = 0.f;
   for (int b = blockIdx.x * BWD_WARPS + warp; b < a.V.batch; b += gridDim.x * BWD_WARPS)
-    attn_bwd<DQ>(a, s, ws, ch, b, lane, acc);
+    attn_bwd<DQ>(a, s, ws, ch, b, lane, acc, accumulate);
 #pragma unroll
   for (int t = 0; t < DQ; ++t) acc.wq[t] = ws.wq[lane][t];
   __syncthreads();  // scratch -> reduction buffer
@@ -693,59 +595,164 @@ __device__ void attn_channel_bwd(const Args& a, const AttnSmem& s, WarpScratch& 
 // one attention channel per launch (its DQ fixed at compile time)
 template <int DQ>
 __global__ void __launch_bounds__(BWD_WARPS * 32, 2)
-    k_attn_bwd(const __grid_constant__ Args a, int ch, int64_t part_stride, int64_t part_off) {
+    k_attn_bwd(const __grid_constant__ Args a, int ch, int64_t part_stride, int64_t part_off, int accumulate) {
   __shared__ AttnSmem sa;
   extern __shared__ float dyn[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   load_attn(sa, a.A[ch], DQ);
   __syncthreads();
   WarpScratch& ws = reinterpret_cast<WarpScratch*>(dyn)[warp];
-  attn_channel_bwd<DQ>(a, sa, ws, ch, lane, warp, dyn, a.attn_part + (int64_t)blockIdx.x * part_stride + part_off);
+  attn_channel_bwd<DQ>(a, sa, ws, ch, lane, warp, dyn, a.attn_part + (int64_t)blockIdx.x * part_stride + part_off,
+                       accumulate != 0);
 }
 
-// field / ad-image / sum-pooling scatters: the gradient row of the sample is
-// added to every row it was gathered from
-__global__ void __launch_bounds__(BWD_WARPS * 32, 4) k_sample_scatter(const __grid_constant__ Args a) {
+// max / concat: the gradient of every behavior reference as its own row
+// (ref_grad[i]): concat slot j of sample b carries dx[b][pool + 12 j ..];
+// max routes each column's gradient to the column's first argmax row
+// (segment_max bwd, autograd.py:307-315) and zero elsewhere
+__global__ void __launch_bounds__(BWD_WARPS * 32) k_ref_rows(const __grid_constant__ Args a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int b = blockIdx.x * BWD_WARPS + warp; b < a.V.batch; b += gridDim.x * BWD_WARPS) {
-    const float* drow = a.d_head_in + (int64_t)b * a.L.width;
-    for (int f = 0; f < a.L.n_fields; ++f) {
-      float dv[DICM_D];
-      load12(drow + a.L.field_col[f], dv);
-      if (!a.L.field_multi[f]) {
-        red_row12_lanes(a.d_rows + (int64_t)a.V.field_inv[f][b] * DICM_D, dv, lane);
-      } else {
-        const int32_t* off = a.V.field_off[f];
-        seg_scatter(a.V.field_inv[f], off[b], off[b + 1], a.d_rows, dv, lane);
-      }
-    }
-    if (a.L.use_ad_image) {
-      float dv[DICM_D];
-      load12(drow + a.L.ad_col, dv);
-      red_row12_lanes(a.d_emb + (int64_t)a.V.ad_local[b] * DICM_D, dv, lane);
-    }
-    if (a.L.use_behavior_images && a.L.kind == 0) {
-      float dv[DICM_D];
-      load12(drow + a.L.pool_col, dv);
-      seg_scatter(a.V.beh_local, a.V.beh_off[b], a.V.beh_off[b + 1], a.d_emb, dv, lane);
-    }
-    if (a.L.use_behavior_images && a.L.kind == 4) {  // concat: slot j's gradient to its row
-      const int64_t i0 = a.V.beh_off[b];
-      const int n = min((int)(a.V.beh_off[b + 1] - i0) * DICM_D, a.L.width - a.L.pool_col);
-      for (int e = lane; e < n; e += 32)
-        atomicAdd(a.d_emb + (int64_t)__ldg(a.V.beh_local + i0 + e / DICM_D) * DICM_D + e % DICM_D,
-                  __ldg(drow + a.L.pool_col + e));
-    }
-    if (a.L.use_behavior_images && a.L.kind == 3) {  // gradient to the first argmax row of each column
+    const float* dpool = a.d_head_in + (int64_t)b * a.L.width + a.L.pool_col;
+    const int64_t i0 = a.V.beh_off[b], i1 = a.V.beh_off[b + 1];
+    if (a.L.kind == 4) {
+      const int n = (int)(i1 - i0) * DICM_D;  // <= width - pool_col (checked at upload)
+      for (int e = lane; e < n; e += 32) a.V.ref_grad[i0 * DICM_D + e] = __ldg(dpool + e);
+    } else {
       float m[DICM_D];
       int am[DICM_D];
       seg_max(a, b, lane, m, am);
-      const int64_t i0 = a.V.beh_off[b];
+      float dv[DICM_D];
+      load12(dpool, dv);
+      for (int64_t i = i0 + lane; i < i1; i += 32) {
+        float r[DICM_D];
 #pragma unroll
-      for (int c = 0; c < DICM_D; ++c)
-        if (lane == c && am[c] >= 0)
-          atomicAdd(a.d_emb + (int64_t)__ldg(a.V.beh_local + i0 + am[c]) * DICM_D + c, __ldg(drow + a.L.pool_col + c));
+        for (int c = 0; c < DICM_D; ++c) r[c] = (am[c] == (int)(i - i0)) ? dv[c] : 0.f;
+        float4* g = reinterpret_cast<float4*>(a.V.ref_grad + i * DICM_D);
+        g[0] = make_float4(r[0], r[1], r[2], r[3]);
+        g[1] = make_float4(r[4], r[5], r[6], r[7]);
+        g[2] = make_float4(r[8], r[9], r[10], r[11]);
+      }
     }
+  }
+}
+
+// Where the gradient row of reference p of a reference list comes from:
+// the list is a concatenation of segments (image list: ad images | behavior
+// images; ID list: one segment per field in schema order).
+//   mode 0: one reference per sample, b = p - begin: dx[b][col..] (+ the
+//           attention query gradient q_grad[b][qcol..] when qgrad is set)
+//   mode 1: CSR references, b = map[p - begin]: dx[b][col..] (sum pooling
+//           and multi-hot sum fields: every reference gets the pooled row's
+//           gradient, segment_sum bwd autograd.py:284-285)
+//   mode 2: a row of its own, rows[p - begin] (attention dk, max, concat)
+struct RefSeg {
+  int64_t begin;
+  const int32_t* map;
+  const float* rows;
+  const float* qgrad;
+  int32_t mode, col, qcol, pad;
+};
+
+struct RefSrc {
+  RefSeg s[DICM_MAX_FIELDS + 1];
+  int32_t n, width;
+  const float* dx;
+};
+
+__device__ __forceinline__ void ref_contrib(const RefSrc& S, int64_t p, float (&v)[DICM_D]) {
+  int k = 0;
+  while (k + 1 < S.n && S.s[k + 1].begin <= p) ++k;
+  const RefSeg& g = S.s[k];
+  const int64_t i = p - g.begin;
+  if (g.mode == 2) {
+    const Row12 r = load_row12_cg(g.rows + i * DICM_D);
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) v[c] = r.v[c];
+    return;
+  }
+  const int64_t b = g.mode == 0 ? i : (int64_t)__ldg(g.map + i);
+  const Row12 r = load_row12(S.dx + b * S.width + g.col);
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) v[c] = r.v[c];
+  if (g.qgrad) {
+    const Row12 q = load_row12_cg(g.qgrad + b * QG_STRIDE + g.qcol);
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) v[c] += q.v[c];
+  }
+}
+
+constexpr int HOT_REFS = 128;  // keys with more references go to the block-wide reduction
+
+__device__ __forceinline__ void store_row12(float* p, const float (&v)[DICM_D]) {
+  float4* q = reinterpret_cast<float4*>(p);
+  q[0] = make_float4(v[0], v[1], v[2], v[3]);
+  q[1] = make_float4(v[4], v[5], v[6], v[7]);
+  q[2] = make_float4(v[8], v[9], v[10], v[11]);
+}
+
+// out[u] = sum of the gradient rows of key u's references, in ascending
+// reference order (thread per key; keys with > HOT_REFS references are
+// listed for k_ref_reduce_hot)
+__global__ void __launch_bounds__(256) k_ref_reduce(const __grid_constant__ RefSrc S, const int32_t* __restrict__ order,
+                                                    const int32_t* __restrict__ start,
+                                                    const int32_t* __restrict__ n_keys, int64_t cap,
+                                                    float* __restrict__ out, int32_t* __restrict__ hot_count,
+                                                    int32_t* __restrict__ hot_list) {
+  const int64_t n = min((int64_t)*n_keys, cap);
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s0 = __ldg(start + u), s1 = __ldg(start + u + 1);
+    if (s1 - s0 > HOT_REFS) {
+      hot_list[atomicAdd(hot_count, 1)] = (int32_t)u;
+      continue;
+    }
+    float acc[DICM_D];
+    ref_contrib(S, __ldg(order + s0), acc);
+    for (int32_t j = s0 + 1; j < s1; ++j) {
+      float v[DICM_D];
+      ref_contrib(S, __ldg(order + j), v);
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) acc[c] += v[c];
+    }
+    store_row12(out + u * DICM_D, acc);
+  }
+}
+
+// the listed keys, one block each: thread t sums references t, t + 256, ...
+// in order, then a fixed-shape tree over the threads -- the result does not
+// depend on which block takes the key
+__global__ void __launch_bounds__(256) k_ref_reduce_hot(const __grid_constant__ RefSrc S,
+                                                        const int32_t* __restrict__ order,
+                                                        const int32_t* __restrict__ start,
+                                                        const int32_t* __restrict__ hot_count,
+                                                        const int32_t* __restrict__ hot_list,
+                                                        float* __restrict__ out) {
+  __shared__ float red[256][DICM_D + 1];
+  const int t = threadIdx.x;
+  const int nh = *hot_count;
+  for (int h = blockIdx.x; h < nh; h += gridDim.x) {
+    const int32_t u = hot_list[h];
+    const int32_t s0 = start[u], s1 = start[u + 1];
+    float acc[DICM_D];
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) acc[c] = 0.f;
+    for (int32_t j = s0 + t; j < s1; j += 256) {
+      float v[DICM_D];
+      ref_contrib(S, __ldg(order + j), v);
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) acc[c] += v[c];
+    }
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) red[t][c] = acc[c];
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+      if (t < w)
+#pragma unroll
+        for (int c = 0; c < DICM_D; ++c) red[t][c] += red[t + w][c];
+      __syncthreads();
+    }
+    if (t < DICM_D) out[(int64_t)u * DICM_D + t] = red[0][t];
+    __syncthreads();
   }
 }
 
@@ -787,8 +794,6 @@ int validate(const dicm_layout_t* L, const dicm_batch_view_t* V) {
       if (L->query_field[f] < 0 || L->query_field[f] >= L->n_fields || L->field_multi[L->query_field[f]])
         return fail(DICM_ERR_UNSUPPORTED, "multiquery-attn: query fields must be one-hot fields");
   if (V->batch < 0) return fail(DICM_ERR_VALUE, "sample: negative batch");
-  if ((L->kind == 1 || L->kind == 2) && L->use_behavior_images && !V->keyproj)
-    return fail(DICM_ERR_VALUE, "attentive pooling needs the key projections (dicm_attn_keyproj)");
   return DICM_OK;
 }
 
@@ -811,19 +816,6 @@ int64_t dicm_attn_partial_size(const dicm_layout_t* layout) { return part_size(l
 
 int dicm_sample_blocks(int batch) { return bwd_grid(batch); }
 
-int dicm_attn_keyproj(const dicm_layout_t* layout, const dicm_attn_params_t* attn, const float* emb,
-                      const int32_t* count_dev, int64_t u_cap, float* keyproj, dicm_stream_t stream) {
-  using namespace dicm;
-  if (!(layout->kind == 1 || layout->kind == 2) || !layout->use_behavior_images || u_cap <= 0) return DICM_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  const int grid = dicm_grid(u_cap, 256, 148 * 8);
-  k_keyproj<<<grid, 256, 0, st>>>(attn[0].w0, DICM_D, emb, count_dev, u_cap, keyproj);
-  if (layout->kind == 2)
-    k_keyproj<<<grid, 256, 0, st>>>(attn[1].w0, DICM_D * layout->n_query, emb, count_dev, u_cap,
-                                    keyproj + u_cap * DICM_ATT);
-  return last_launch("dicm_attn_keyproj");
-}
-
 int dicm_sample_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const dicm_attn_params_t* attn,
                     float* head_in, float* scores, float* stats, dicm_stream_t stream) {
   int rc = validate(layout, bv);
@@ -842,44 +834,59 @@ int dicm_sample_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
   return last_launch("dicm_sample_fwd");
 }
 
-// k_sample_scatter shares no input it writes with k_attn_bwd (both only add
-// into d_emb / d_rows with red.add), so it runs on a forked stream beside the
-// attention backward and fills the SMs its second wave leaves idle.  One side
-// stream and event pair per host thread and device (event reuse across
-// threads would let one thread's fork wait on another's record); under graph
-// capture the fork/join become parallel branches.  DICM_FORK=0 (all forks)
-// or DICM_SAMPLE_FORK=0 (this one) turns it off.
-struct SideFork {
-  cudaStream_t side = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-};
-
-static SideFork* side_fork() {
-  static const bool off = [] {
-    const char* e = getenv("DICM_FORK");
-    const char* e2 = getenv("DICM_SAMPLE_FORK");
-    return (e && e[0] == '0') || (e2 && e2[0] == '0');
-  }();
-  if (off) return nullptr;
-  constexpr int kMaxDev = 64;
-  thread_local SideFork forks[kMaxDev];
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
-  SideFork& f = forks[dev];
-  if (!f.side) {
-    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
-    cudaThreadExchangeStreamCaptureMode(&mode);
-    const bool ok = cudaStreamCreateWithFlags(&f.side, cudaStreamNonBlocking) == cudaSuccess &&
-                    cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming) == cudaSuccess &&
-                    cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming) == cudaSuccess;
-    cudaThreadExchangeStreamCaptureMode(&mode);
-    if (!ok) {
-      cudaGetLastError();
-      f.side = nullptr;
-      return nullptr;
+// the reference lists of the image rows and the ID rows (see RefSeg)
+static RefSrc image_src(const dicm_layout_t* L, const dicm_batch_view_t* V, const float* dx) {
+  RefSrc S{};
+  S.dx = dx;
+  S.width = L->width;
+  const bool attn = L->kind == 1 || L->kind == 2;
+  int64_t pos = 0;
+  if (L->use_ad_image) {
+    RefSeg& g = S.s[S.n++];
+    g.begin = 0;
+    g.mode = 0;
+    g.col = L->ad_col;
+    g.qgrad = (attn && L->use_behavior_images) ? V->q_grad : nullptr;
+    g.qcol = 0;
+    pos = V->batch;
+  }
+  if (L->use_behavior_images) {
+    RefSeg& g = S.s[S.n++];
+    g.begin = pos;
+    if (L->kind == 0) {
+      g.mode = 1;
+      g.map = V->beh_seg;
+      g.col = L->pool_col;
+    } else {
+      g.mode = 2;
+      g.rows = V->ref_grad;
     }
   }
-  return &f;
+  return S;
+}
+
+static RefSrc id_src(const dicm_layout_t* L, const dicm_batch_view_t* V, const float* dx) {
+  RefSrc S{};
+  S.dx = dx;
+  S.width = L->width;
+  for (int f = 0; f < L->n_fields; ++f) {
+    RefSeg& g = S.s[S.n++];
+    g.begin = V->field_ref_begin[f];
+    g.col = L->field_col[f];
+    if (L->field_multi[f]) {
+      g.mode = 1;
+      g.map = V->field_seg[f];
+    } else {
+      g.mode = 0;
+      if (L->kind == 2 && L->use_behavior_images)
+        for (int q = 0; q < L->n_query; ++q)
+          if (L->query_field[q] == f) {
+            g.qgrad = V->q_grad;
+            g.qcol = DICM_D + DICM_D * q;
+          }
+    }
+  }
+  return S;
 }
 
 int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const dicm_attn_params_t* attn,
@@ -888,6 +895,11 @@ int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
   int rc = validate(layout, bv);
   if (rc) return rc;
   if (bv->batch == 0) return DICM_OK;
+  const bool attn_chan = layout->use_behavior_images && (layout->kind == 1 || layout->kind == 2);
+  const bool own_rows = layout->use_behavior_images && layout->kind != 0;
+  if ((own_rows && !bv->ref_grad) || (attn_chan && !bv->q_grad) || !bv->hot || !bv->img_order || !bv->id_order ||
+      (layout->use_behavior_images && layout->kind == 0 && !bv->beh_seg))
+    return fail(DICM_ERR_VALUE, "sample_bwd: the batch view lacks its backward buffers");
   Args a = make_args(layout, bv, attn);
   a.head_in = const_cast<float*>(head_in);
   a.d_head_in = d_head_in;
@@ -902,33 +914,39 @@ int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = bwd_grid(bv->batch);
   const int64_t stride = part_size(layout);
-  {
-    const int probe_slot = probe_begin(DICM_PROBE_SAMPLE_BWD, st);
-    const bool attn_chan = layout->use_behavior_images && (layout->kind == 1 || layout->kind == 2);
-    SideFork* fk = attn_chan ? side_fork() : nullptr;
-    if (fk) {
-      cudaEventRecord(fk->fork, st);
-      cudaStreamWaitEvent(fk->side, fk->fork, 0);
-      k_sample_scatter<<<grid, BWD_WARPS * 32, 0, fk->side>>>(a);
-      cudaEventRecord(fk->join, fk->side);
-    } else {
-      k_sample_scatter<<<grid, BWD_WARPS * 32, 0, st>>>(a);
+  const int probe_slot = probe_begin(DICM_PROBE_SAMPLE_BWD, st);
+  if (check_cuda(cudaMemsetAsync(bv->hot, 0, 2 * sizeof(int32_t), st), "sample_bwd hot counters")) return DICM_ERR_CUDA;
+  if (attn_chan) {
+    // partial row layout in sorted names: attn/id/* before attn/img/*; the
+    // id channel writes each reference's dk row, the img channel adds to it
+    int64_t img_off = 0;
+    if (layout->kind == 2) {
+      img_off = chan_part(DICM_D * layout->n_query);
+      if (layout->n_query == 2)
+        k_attn_bwd<2 * DICM_D><<<grid, BWD_WARPS * 32, smem, st>>>(a, 1, stride, 0, 0);
+      else
+        k_attn_bwd<DICM_D><<<grid, BWD_WARPS * 32, smem, st>>>(a, 1, stride, 0, 0);
     }
-    if (attn_chan) {
-      // partial row layout in sorted names: attn/id/* before attn/img/*
-      int64_t img_off = 0;
-      if (layout->kind == 2) {
-        img_off = chan_part(DICM_D * layout->n_query);
-        if (layout->n_query == 2)
-          k_attn_bwd<2 * DICM_D><<<grid, BWD_WARPS * 32, smem, st>>>(a, 1, stride, 0);
-        else
-          k_attn_bwd<DICM_D><<<grid, BWD_WARPS * 32, smem, st>>>(a, 1, stride, 0);
-      }
-      k_attn_bwd<DICM_D><<<grid, BWD_WARPS * 32, smem, st>>>(a, 0, stride, img_off);
-    }
-    if (fk) cudaStreamWaitEvent(st, fk->join, 0);
-    probe_end(probe_slot, st);
+    k_attn_bwd<DICM_D><<<grid, BWD_WARPS * 32, smem, st>>>(a, 0, stride, img_off, layout->kind == 2);
+  } else if (own_rows) {
+    k_ref_rows<<<grid, BWD_WARPS * 32, 0, st>>>(a);
   }
+  // every unique image row and ID row: its references summed in order
+  int32_t* hot_list_img = bv->hot + 2;
+  int32_t* hot_list_id = bv->hot + 2 + bv->img_cap;
+  if (layout->use_ad_image || layout->use_behavior_images) {
+    const RefSrc S = image_src(layout, bv, d_head_in);
+    k_ref_reduce<<<dicm_grid(bv->img_cap, 256, 148 * 16), 256, 0, st>>>(S, bv->img_order, bv->img_start, bv->n_img_keys,
+                                                                      bv->img_cap, d_emb, bv->hot, hot_list_img);
+    k_ref_reduce_hot<<<148, 256, 0, st>>>(S, bv->img_order, bv->img_start, bv->hot, hot_list_img, d_emb);
+  }
+  if (layout->n_fields > 0) {
+    const RefSrc S = id_src(layout, bv, d_head_in);
+    k_ref_reduce<<<dicm_grid(bv->id_cap, 256, 148 * 16), 256, 0, st>>>(S, bv->id_order, bv->id_start, bv->n_id_keys,
+                                                                     bv->id_cap, d_rows, bv->hot + 1, hot_list_id);
+    k_ref_reduce_hot<<<148, 256, 0, st>>>(S, bv->id_order, bv->id_start, bv->hot + 1, hot_list_id, d_rows);
+  }
+  probe_end(probe_slot, st);
   return last_launch("dicm_sample_bwd");
 }
 

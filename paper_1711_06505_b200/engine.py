@@ -432,8 +432,21 @@ class StepEngine:
         self.attn_partial = torch.empty((L.lib.dicm_sample_blocks(max(B, 1)), max(self.attn_part, 1)), **f32)
         self.loss = torch.zeros(1, **f32)
         lay = self.model.layout
-        nch = (2 if lay.multiquery else 1) if (lay.attentive and lay.use_behavior_images) else 0
-        self.keyproj = torch.empty((max(nch, 1), max(self.cap_u, 1) if nch else 1, 32), **f32)
+        # deterministic backward (dicm_ref_transpose / dicm_sample_bwd): the
+        # dedup inverses transposed, the sample of every CSR reference, and
+        # per-reference / per-sample gradient scratch
+        self.img_order = torch.empty(max(n_img, 1), **i32)
+        self.img_start = torch.empty(max(self.cap_u, 1) + 1, **i32)
+        self.id_order = torch.empty(max(n_id, 1), **i32)
+        self.id_start = torch.empty(max(self.cap_k, 1) + 1, **i32)
+        self.beh_seg = torch.empty(max(R, 1), **i32)
+        self.id_seg = torch.empty(max(n_id, 1), **i32)  # multi-hot field f's refs at their ID-list positions
+        own_rows = lay.use_behavior_images and lay.aggregator.kind != "sum"
+        self.ref_grad = torch.empty((max(R, 1) if own_rows else 1, 12), **f32)
+        self.q_grad = torch.empty((max(B, 1), 36), **f32)
+        self.hot = torch.empty(2 + max(self.cap_u, 1) + max(self.cap_k, 1), **i32)
+        self.ws_tr_img = _u8(L.lib.dicm_ref_transpose_workspace(n_img, max(self.cap_u, 1)), dev)
+        self.ws_tr_id = _u8(L.lib.dicm_ref_transpose_workspace(n_id, max(self.cap_k, 1)), dev)
         self._alloc_image_net(self.cap_u)
         self.cap = need
         self._graphs, self._graph_warm = None, False  # captured steps point at the old buffers
@@ -605,13 +618,44 @@ class StepEngine:
         bv.beh_local = self.inv_img.data_ptr() + 4 * (B if lay.use_ad_image else 0)
         bv.beh_off = self._dptr(pk.beh_off)
         bv.emb = emb.data_ptr()
-        bv.keyproj = self.keyproj.data_ptr()
-        bv.kp_stride = self.keyproj.shape[1]
-        # key projections of the attention nets, once per unique image
-        L.check(L.lib.dicm_attn_keyproj(C.byref(self.layout), self.attn, emb.data_ptr(), self.counts.data_ptr(),
-                                        self.keyproj.shape[1] if self.keyproj.shape[1] > 1 else 0,
-                                        self.keyproj.data_ptr(), self.s))
+        bv.img_order, bv.img_start = self.img_order.data_ptr(), self.img_start.data_ptr()
+        bv.id_order, bv.id_start = self.id_order.data_ptr(), self.id_start.data_ptr()
+        for i, f in enumerate(self.fields):
+            bv.field_ref_begin[i] = self.inv_id_off[f.name]
+            if f.multi:
+                bv.field_seg[i] = self.id_seg.data_ptr() + 4 * self.inv_id_off[f.name]
+        bv.beh_seg = self.beh_seg.data_ptr()
+        bv.n_img_keys, bv.n_id_keys = self.counts.data_ptr(), self.counts[1:].data_ptr()
+        bv.img_cap, bv.id_cap = max(self.cap_u, 1), max(self.cap_k, 1)
+        bv.ref_grad, bv.q_grad, bv.hot = self.ref_grad.data_ptr(), self.q_grad.data_ptr(), self.hot.data_ptr()
         return bv
+
+    def _transpose_images(self):
+        """The image-key dedup inverse transposed (stable by reference) and the
+        sample of every behavior reference: the fixed summation order of the
+        deterministic backward.  Depends only on the batch."""
+        pk = self.pk
+        n = self._n_img(pk.B, pk.R)
+        if n:
+            L.check(L.lib.dicm_ref_transpose(self.inv_img.data_ptr(), n, max(self.cap_u, 1), self.ws_tr_img.data_ptr(),
+                                             self.ws_tr_img.numel(), self.img_order.data_ptr(),
+                                             self.img_start.data_ptr(), self.s))
+        if self.model.layout.use_behavior_images and self.model.layout.aggregator.kind == "sum":
+            L.check(L.lib.dicm_csr_segments(self._dptr(pk.beh_off), pk.B, self.beh_seg.data_ptr(), self.s))
+
+    def _transpose_ids(self):
+        """The same for the ID keys (every field's references in schema order)."""
+        pk = self.pk
+        n = pk.n_id(self.fields)
+        if n:
+            L.check(L.lib.dicm_ref_transpose(self.inv_id.data_ptr(), n, max(self.cap_k, 1), self.ws_tr_id.data_ptr(),
+                                             self.ws_tr_id.numel(), self.id_order.data_ptr(), self.id_start.data_ptr(),
+                                             self.s))
+        for f in self.fields:
+            if f.multi:
+                _, _, o = pk.multi[f.name]
+                L.check(L.lib.dicm_csr_segments(self._dptr(o), pk.B, self.id_seg.data_ptr() + 4 * self.inv_id_off[f.name],
+                                                self.s))
 
     def _local_step(self, emb, d_emb, denom, reduce=True):
         """a6-a12 forward and backward on the local batch: pooling, head, BCE.
@@ -626,8 +670,6 @@ class StepEngine:
         self._head_fwd_bwd(B, denom)
         nhb = self._head_blocks(B)
         L.check(L.lib.dicm_loss_finalize(self.loss_part.data_ptr(), nhb, 1.0 / denom, self.loss.data_ptr(), st, s))
-        L.check(L.lib.dicm_zero_async(d_emb.data_ptr(), d_emb.numel() * 4, s))
-        L.check(L.lib.dicm_zero_async(self.d_rows.data_ptr(), self.d_rows.numel() * 4, s))
         L.check(L.lib.dicm_sample_bwd(C.byref(self.layout), C.byref(bv), self.attn, self.head_in.data_ptr(),
                                       self.d_head_in.data_ptr(), self.scores.data_ptr(), self.stats.data_ptr(),
                                       d_emb.data_ptr(), self.d_rows.data_ptr(), self.attn_partial.data_ptr(), s))
@@ -674,11 +716,20 @@ class StepEngine:
                 self.s = side.cuda_stream
                 self._dedup_ids()
                 self._gather_id_rows()
+                self._transpose_ids()
             self.s = main
             self._dedup_images()
+            # the image transpose runs on the branch too, beside the image-MLP forward
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                self.s = side.cuda_stream
+                self._transpose_images()
+            self.s = main
         else:
             self._dedup_images()
             self._dedup_ids()
+            self._transpose_images()
+            self._transpose_ids()
         if self.n_img_segs:
             self._image_forward(self.net, self.uniq_img, self.counts.data_ptr())
         if side is not None:
@@ -836,19 +887,22 @@ class StepEngine:
         return self.loss
 
     _OWN_SOURCES = ("capi", "dedup", "exchange", "head", "imgmlp", "imgmlp_bf16_sm100", "imgmlp_sm100",
-                    "imgmlp_small_sm100", "optim", "p2p", "pool", "sample", "towers")
+                    "imgmlp_small_sm100", "optim", "p2p", "pool", "sample", "towers", "transpose")
 
-    def kernel_nodes(self):
+    def kernel_nodes(self, detail=False):
         """(own, total) kernel nodes of the last captured step graph: every
-        kernel the step launches, and those of this library (csrc/*.cu) --
-        NCCL or torch kernels in the graph are counted in total only."""
+        kernel the step launches, and those written in this library
+        (csrc/*.cu).  The CUB radix-sort kernels instantiated inside the
+        library by dicm_ref_transpose (CUDA toolkit templates) are counted
+        apart (``detail=True`` -> (own, cub, total)); NCCL or torch kernels
+        in the graph are counted in total only."""
         g = getattr(self, "_last_graph", None)
         if g is None:
             return None
         from cuda.bindings import driver as cu
         err, _, n = cu.cuGraphGetNodes(g.raw_cuda_graph(), 0)
         err, nodes, n = cu.cuGraphGetNodes(g.raw_cuda_graph(), n)
-        own = total = 0
+        own = cub = total = 0
         for nd in nodes[:n]:
             err, ty = cu.cuGraphNodeGetType(nd)
             if ty != cu.CUgraphNodeType.CU_GRAPH_NODE_TYPE_KERNEL:
@@ -859,7 +913,9 @@ class StepEngine:
             name = name.decode() if isinstance(name, bytes) else str(name)
             if "4dicm" in name or any(f"_{s}_cu_" in name for s in self._OWN_SOURCES):
                 own += 1
-        return own, total
+            elif name.startswith("_ZN3cub"):
+                cub += 1
+        return (own, cub, total) if detail else (own, total)
 
     def raise_status(self):
         """Sync point: raise the reference's exception for a flagged step."""
@@ -914,10 +970,13 @@ class StepEngine:
             n += 4 + 9
         n += 1  # gather_keyed
         if lay.attentive:
-            n += 2 if lay.multiquery else 1  # keyproj per channel
             n += 2 if lay.multiquery else 1  # attn_bwd per channel
             n += 1  # attention partial reduce
-        n += 1 + 1 + 1 + 1 + 1  # sample fwd, head, loss, sample scatter, head partial reduce
+        elif lay.aggregator.kind in ("max", "concat"):
+            n += 1  # per-reference rows
+        n += 2 * 7 + (1 if lay.aggregator.kind == "sum" else 0) + sum(1 for f in self.fields if f.multi)  # transposes (iota, CUB radix sort, starts), CSR segments
+        n += 4  # ordered row sums (images, IDs) and their hot-key passes
+        n += 1 + 1 + 1 + 1  # sample fwd, head, loss, head partial reduce
         if self.wide_head:
             n += 3 + 2 - 1  # layer-0 GEMMs + two column reduces instead of the partial reduce
         n += 1 + 3 + 1  # check_finite, adam dense (flags, update, steps), adam rows

@@ -372,6 +372,8 @@ class ClusterEngine(StepEngine):
         denom = float(db.pk.B * G if denominator is None else denominator)
         self._dedup_images()
         self._dedup_ids()
+        self._transpose_images()
+        self._transpose_ids()
         cnt = self.counts
         # (2) requests: bucket by owner, exchange counts, then keys
         L.check(L.lib.dicm_bucket_by_owner(self.uniq_img.data_ptr(), cnt.data_ptr(), self.cap_u, G,
@@ -466,6 +468,8 @@ class ClusterEngine(StepEngine):
         px = self.px
         self._dedup_images()
         self._dedup_ids()
+        self._transpose_images()
+        self._transpose_ids()
         cnt = self.counts
         L.check(L.lib.dicm_bucket_by_owner(self.uniq_img.data_ptr(), cnt.data_ptr(), self.cap_u, G,
                                            self.send_img.data_ptr(), self._col(0), self.perm_img.data_ptr(),
