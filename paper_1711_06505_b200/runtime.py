@@ -680,6 +680,17 @@ class Cluster:
             raise ValueError("CUDA graphs need the peer-memory exchange (DICM_EXCHANGE=p2p)")
         self.engine.use_graphs = bool(on)
 
+    # -- checkpoint restore into this rank's state (checkpoint.load_warmup)
+
+    def set_adam_state(self, name, m=None, v=None, t=None):
+        """Adam state of one parameter; tables take this rank's rows."""
+        from .training import set_adam_state
+        set_adam_state(self.engine, self.model, name, m, v, t)
+
+    def reset_adam_state(self, name):
+        from .training import reset_adam_state
+        reset_adam_state(self.engine, self.model, name)
+
     # -- state assembled from the owning shards (reference runtime.py:474-516)
 
     def _assemble(self, local, vocab):

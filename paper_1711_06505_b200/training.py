@@ -147,36 +147,48 @@ class LocalTrainer:
     def set_adam_state(self, name, m=None, v=None, t=None):
         """Write Adam state of one parameter into the device buffers
         (checkpoint restore, reference checkpoint.py:228-243)."""
-        import torch
-        e, mdl = self.engine, self.model
-        if name.startswith("id_emb/"):
-            f = name.split("/", 1)[1]
-            if m is not None:
-                e.tm[f].copy_(torch.as_tensor(np.asarray(m), dtype=torch.float32))
-            if v is not None:
-                e.tv[f].copy_(torch.as_tensor(np.asarray(v), dtype=torch.float32))
-            if t is not None:
-                e.tt[f].copy_(torch.as_tensor(np.asarray(t), dtype=torch.int32))
-            return
-        if m is not None:
-            mdl.dense_view(e.m, name).copy_(torch.as_tensor(np.asarray(m), dtype=torch.float32))
-        if v is not None:
-            mdl.dense_view(e.v, name).copy_(torch.as_tensor(np.asarray(v), dtype=torch.float32))
-        if t is not None:
-            e.t[e.span_index[name]] = int(np.asarray(t))
+        set_adam_state(self.engine, self.model, name, m, v, t)
 
     def reset_adam_state(self, name):
         """Fresh optimizer state for a re-initialised parameter."""
-        if name.startswith("id_emb/"):
-            f = name.split("/", 1)[1]
-            self.set_adam_state(name, m=np.zeros(self.engine.tm[f].shape), v=np.zeros(self.engine.tv[f].shape),
-                                t=np.zeros(self.engine.tt[f].shape, dtype=np.int64))
-        else:
-            shp = tuple(self.model.params[name].shape)
-            self.set_adam_state(name, m=np.zeros(shp), v=np.zeros(shp), t=0)
+        reset_adam_state(self.engine, self.model, name)
 
     @property
     def table_state(self):
         e = self.engine
         return {f: AdamStateView(e.tm[f].double().cpu().numpy(), e.tv[f].double().cpu().numpy(),
                                  e.tt[f].cpu().numpy().astype(np.int64)) for f in e.tm}
+
+
+def set_adam_state(engine, model, name, m=None, v=None, t=None):
+    """Adam state of one parameter -> the engine's device buffers: dense
+    parameters into the fused m / v buffers and the per-span step counter,
+    tables into the per-row m / v / t (a sharded engine takes its local rows)."""
+    import torch
+    if name.startswith("id_emb/"):
+        f = name.split("/", 1)[1]
+        if m is not None:
+            engine.tm[f].copy_(torch.as_tensor(np.asarray(m), dtype=torch.float32))
+        if v is not None:
+            engine.tv[f].copy_(torch.as_tensor(np.asarray(v), dtype=torch.float32))
+        if t is not None:
+            engine.tt[f].copy_(torch.as_tensor(np.asarray(t), dtype=torch.int32))
+        return
+    if m is not None:
+        model.dense_view(engine.m, name).copy_(torch.as_tensor(np.asarray(m), dtype=torch.float32))
+    if v is not None:
+        model.dense_view(engine.v, name).copy_(torch.as_tensor(np.asarray(v), dtype=torch.float32))
+    if t is not None:
+        engine.t[engine.span_index[name]] = int(np.asarray(t))
+
+
+def reset_adam_state(engine, model, name):
+    if name.startswith("id_emb/"):
+        f = name.split("/", 1)[1]
+        engine.tm[f].zero_()
+        engine.tv[f].zero_()
+        engine.tt[f].zero_()
+    else:
+        model.dense_view(engine.m, name).zero_()
+        model.dense_view(engine.v, name).zero_()
+        engine.t[engine.span_index[name]] = 0
