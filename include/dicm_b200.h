@@ -202,6 +202,12 @@ typedef struct {
 size_t dicm_ref_transpose_workspace(int64_t n, int64_t key_cap);
 int dicm_ref_transpose(const int32_t* inv, int64_t n, int64_t key_cap, void* ws, size_t ws_bytes,
                        int32_t* order, int32_t* start /* [key_cap + 1] */, dicm_stream_t stream);
+/* Rank-invariant counter-based table init for tables too large for the
+ * reference's host init (model.py:316-319 draws 0.05 N(0,1) per row): row r,
+ * column c = scale * normal(hash(key, r*d + c)); this rank's rows
+ * r = local*world + rank, rows >= vocab zero. */
+int dicm_table_init(float* out, int64_t n_local, int d, int world, int rank, int64_t vocab, uint64_t key,
+                    float scale, dicm_stream_t stream);
 /* seg[i] = b for off[b] <= i < off[b+1]: the sample of every CSR reference
  * (the reference's Batch.beh_seg / multihot segment arrays, model.py:144-150) */
 int dicm_csr_segments(const int32_t* off, int batch, int32_t* seg, dicm_stream_t stream);

@@ -113,8 +113,9 @@ class DicmModel:
         (row % world == rank, at local row row // world), with exactly the
         values the full reference init gives them.  ``table_init="device"``
         draws 0.05 N(0,1) rows on the device instead (same distribution as
-        model.py:316-319, not the same values) -- for 100M-row tables whose
-        reference init would not fit host memory."""
+        model.py:316-319, not the same values; counter-based, so identical at
+        every world size) -- for 100M-row tables whose reference init would
+        not fit host memory."""
         layout = ModelLayout(schema, aggregator, tuple(mlp_widths), use_ad_image, use_behavior_images)
         S.validate_layout(layout, None if extractor is None else extractor.out_dim)
         check_hot_path(layout)
@@ -136,10 +137,15 @@ class DicmModel:
             world, rank = shard if shard is not None else (1, 0)
 
             def table_rows(f, name):
+                # counter-based: a row's values depend on (seed, name, row) only,
+                # so the model is the same at every world size (dicm_table_init)
+                from . import _lib as L
                 n_local = -(-f.vocab // world)
-                g = torch.Generator(device=device).manual_seed(
-                    (int(seed) * 1315423911 + zlib.crc32(name.encode()) * 31 + rank) & 0x7FFFFFFF)
-                return 0.05 * torch.randn((n_local, schema.d_id), generator=g, dtype=torch.float32, device=device)
+                out = torch.empty((n_local, schema.d_id), dtype=torch.float32, device=device)
+                key = ((int(seed) & 0xFFFFFFFF) << 32) | zlib.crc32(name.encode())
+                L.check(L.lib.dicm_table_init(out.data_ptr(), n_local, schema.d_id, world, rank, f.vocab, key, 0.05,
+                                              L.stream_handle()))
+                return out
         elif shard is not None and table_rows is None:
             world, rank = shard
 

@@ -129,3 +129,23 @@ def test_bucket_by_owner_stable_partition(L):
         p = perm.cpu().numpy()
         assert np.array_equal(np.sort(p), np.arange(n))
         assert np.array_equal(p[order], np.arange(n))
+
+
+def test_counter_based_table_init_is_rank_invariant():
+    """dicm_table_init: a row's values depend on (key, row) only -- the shards
+    of world 3 interleave to the world-1 table -- and follow 0.05 N(0,1)
+    (reference model.py:316-319)."""
+    from paper_1711_06505_b200 import _lib as L
+    V, d, key = 100_003, 12, (7 << 32) | 12345
+    full = torch.empty((V, d), device="cuda")
+    L.check(L.lib.dicm_table_init(full.data_ptr(), V, d, 1, 0, V, key, 0.05, L.stream_handle()))
+    world = 3
+    for r in range(world):
+        n_local = -(-V // world)
+        t = torch.full((n_local, d), float("nan"), device="cuda")
+        L.check(L.lib.dicm_table_init(t.data_ptr(), n_local, d, world, r, V, key, 0.05, L.stream_handle()))
+        mine = full[r::world]
+        assert torch.equal(t[:len(mine)], mine)
+        assert torch.count_nonzero(t[len(mine):]) == 0
+    x = full.double()
+    assert abs(x.mean().item()) < 1e-3 and abs(x.std().item() - 0.05) < 1e-3
