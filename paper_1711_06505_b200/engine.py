@@ -113,30 +113,51 @@ class DeviceBatch:
 
 class Prefetcher:
     """Host input pipeline: while step i runs, a worker
-    thread assembles batch i+1 on the host (the columnar take + packing into
+    thread assembles batch i+1 on the host (``transform`` -- e.g. a Cluster
+    rank's slice of the union batch -- the columnar take and the packing into
     pinned memory) and its H2D copy runs on a side stream; the compute stream
-    waits for that copy only when it reaches the batch.  Device buffers rotate
-    through a ring whose slots are reused only after the step that read them
-    has passed (an event on the compute stream)."""
+    waits for that copy only when it reaches the batch.
 
-    def __init__(self, engine, batches, depth=2):
+    Pinned host slots and device slots rotate through rings and are reused,
+    never reallocated per batch: a pinned slot returns to the worker once its
+    copy has been issued (the worker waits on the copy's event before
+    refilling it); a device slot is rewritten only after the step that read it
+    has passed (an event on the compute stream).  Yields (item, DeviceBatch)
+    with ``item = transform(batch)``."""
+
+    def __init__(self, engine, batches, depth=2, transform=None):
         import queue
         import threading
         self.e, self.depth = engine, max(1, int(depth))
         self.copy_stream = torch.cuda.Stream(device=engine.dev)
+        n = self.depth + 2
         self.q = queue.Queue(maxsize=self.depth)
-        self.ring = [None] * (self.depth + 2)
-        self.freed = [None] * (self.depth + 2)
+        self.free = queue.Queue()
+        for k in range(n):
+            self.free.put((k, None))
+        self.pinned = [None] * n
+        self.ring = [None] * n
+        self.freed = [None] * n
         self._err = None
+        self._stop = False
 
         def work():
             try:
                 for b in batches:
-                    engine._check_capacity(b)
-                    pk = Packed(engine.model, b)
-                    host = torch.empty(max(pk.total, 1), dtype=torch.int32, pin_memory=True)
-                    pk.fill(engine.model, b, host.numpy())
-                    self.q.put((b, pk, host))
+                    if self._stop:
+                        break
+                    item = transform(b) if transform is not None else b
+                    local = item[0] if transform is not None else item
+                    engine._check_capacity(local)
+                    pk = Packed(engine.model, local)
+                    k, ev = self.free.get()
+                    if ev is not None:
+                        ev.synchronize()  # the previous copy out of this slot has finished
+                    host = self.pinned[k]
+                    if host is None or host.numel() < pk.total:
+                        host = self.pinned[k] = torch.empty(max(pk.total, 1), dtype=torch.int32, pin_memory=True)
+                    pk.fill(engine.model, local, host.numpy())
+                    self.q.put((item, pk, k))
             except BaseException as ex:  # surfaced in the consumer
                 self._err = ex
             self.q.put(None)
@@ -144,15 +165,18 @@ class Prefetcher:
         self.t = threading.Thread(target=work, daemon=True)
         self.t.start()
 
+    def close(self):
+        self._stop = True
+
     def __iter__(self):
         i = 0
         while True:
-            item = self.q.get()
-            if item is None:
+            got = self.q.get()
+            if got is None:
                 if self._err is not None:
                     raise self._err
                 return
-            b, pk, host = item
+            item, pk, k = got
             self.e._ensure(pk)
             slot = i % len(self.ring)
             buf = self.ring[slot]
@@ -161,11 +185,12 @@ class Prefetcher:
             with torch.cuda.stream(self.copy_stream):
                 if self.freed[slot] is not None:
                     self.copy_stream.wait_event(self.freed[slot])  # the step that read this slot is done
-                buf[:pk.total].copy_(host[:pk.total], non_blocking=True)
+                buf[:pk.total].copy_(self.pinned[k][:pk.total], non_blocking=True)
                 ready = torch.cuda.Event()
                 ready.record(self.copy_stream)
+            self.free.put((k, ready))
             torch.cuda.current_stream().wait_event(ready)
-            yield b, DeviceBatch(pk, buf)
+            yield item, DeviceBatch(pk, buf)
             done = torch.cuda.Event()
             done.record(torch.cuda.current_stream())
             self.freed[slot] = done

@@ -652,6 +652,28 @@ class Cluster:
         e.iteration += 1
         return loss
 
+    def train_stream(self, unions, prefetch=2):
+        """Train on an iterable of union batches (``Batch`` or sample lists),
+        yielding each iteration's device loss without a host sync.  A worker
+        thread slices, packs and copies iteration i+1's input while iteration
+        i runs (engine.Prefetcher): the host pipeline of run_iteration hidden
+        behind the device step."""
+        from .engine import Prefetcher
+        e = self.engine
+
+        def prep(u):
+            local, union = self.local_slice(u)
+            return local, union.size
+
+        for (local, union_size), db in Prefetcher(e, unions, prefetch, transform=prep):
+            if self.use_graphs:
+                yield e.step_graphed(db, denominator=union_size)
+                continue
+            loss = e.forward_backward(db, denominator=union_size)
+            e.optimizer_step(e.lr())
+            e.iteration += 1
+            yield loss
+
     def close(self):
         """Release captured CUDA graphs and the peer-memory mappings (call
         before destroy_process_group; graphs that captured collectives and

@@ -382,3 +382,25 @@ def test_single_gpu_cluster_topologies_match_local_trainer():
     for n in model_c.params:
         assert {f"{n}#m", f"{n}#v", f"{n}#t"} <= set(opt), n
     assert cl.collect_into_model() is model_c
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_train_stream_matches_step_by_step(graphs):
+    """Cluster.train_stream (host slicing/packing of iteration i+1 in a worker
+    thread, pinned-slot ring, H2D on a copy stream) trains exactly like one
+    run_iteration per union batch: bit-identical losses and parameters."""
+    from paper_1711_06505_b200.batch import synthetic_batch
+    from paper_1711_06505_b200.runtime import Cluster, ClusterConfig
+    rng = np.random.default_rng(8)
+    model_a, pool, _ = _bench_like("attn", B=64, L=12, P=600)
+    model_b, _, _ = _bench_like("attn", B=64, L=12, P=600)
+    unions = [synthetic_batch(rng, model_a.schema, 64, 12, 600) for _ in range(7)]
+    ca = Cluster(ClusterConfig(workers=2, servers=1, batch_per_worker=32), model_a, pool)
+    cb = Cluster(ClusterConfig(workers=2, servers=1, batch_per_worker=32), model_b, pool)
+    ca.use_graphs = cb.use_graphs = graphs
+    la = [float(x.item()) for x in ca.train_stream(unions, prefetch=2)]
+    lb = [cb.run_iteration(u, digests=False)[0] for u in unions]
+    assert la == lb
+    sa, sb = model_a.snapshot(), model_b.snapshot()
+    for n in sa:
+        assert np.array_equal(sa[n], sb[n]), n
