@@ -14,6 +14,6 @@ $CMD > "$OUT/plain.log" 2>&1 || { echo "plain run failed"; tail -20 "$OUT/plain.
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file "$OUT/launches.csv" $CMD > "$OUT/ncu_launches.log" 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:'k_fwd|k_dw0|k_l12|k_dw1|k_sample|k_attn_bwd' --launch-skip 20 --launch-count 12 \
+    -k regex:'k_fwd|k_dw0|k_l12|k_dw1|k_sample|k_attn_bwd|k_ref|k_head|k_rows|k_mark' --launch-skip 40 --launch-count 16 \
     -o "$OUT/full" -f $CMD > "$OUT/ncu_full.log" 2>&1
 echo "done $OUT"
