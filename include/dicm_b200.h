@@ -418,8 +418,8 @@ int dicm_ipc_open(const void* handle, void** out);
 int dicm_ipc_close(void* ptr);
 int dicm_p2p_barrier(const dicm_peers_t* peers, int64_t flags_off, uint32_t epoch, int32_t* status,
                      dicm_stream_t stream);
-int dicm_p2p_counts(const dicm_peers_t* peers, const int32_t* send_counts, int64_t cmat_off,
-                    dicm_stream_t stream);
+int dicm_p2p_counts(const dicm_peers_t* peers, const int32_t* send_counts /* [2][world]: image, ID */,
+                    int64_t cmat_off, dicm_stream_t stream);
 int dicm_p2p_plan(const dicm_peers_t* peers, int64_t cmat_off, int64_t* seg_img, int64_t* seg_id,
                   int32_t* cnt_dev, int64_t* plan, dicm_stream_t stream);
 int dicm_p2p_scatter(const dicm_peers_t* peers, const int64_t* plan, int kind /* 0 img, 1 id */,

@@ -66,12 +66,14 @@ __global__ void k_barrier(const __grid_constant__ Peers P, int64_t off, uint32_t
   __syncthreads();
 }
 
-// my send counts [world][2] -> row [rank] of every peer's count matrix
+// my send counts [2][world] (image keys per owner, then ID keys per owner,
+// as the two bucket passes write them) -> row [rank] of every peer's
+// [world][world][2] count matrix
 __global__ void k_counts(const __grid_constant__ Peers P, const int32_t* __restrict__ cnt, int64_t off) {
   const int W = P.world;
   for (int i = threadIdx.x; i < W * W * 2; i += blockDim.x) {
     const int p = i / (2 * W), e = i % (2 * W);
-    reinterpret_cast<int32_t*>(P.region[p] + off)[P.rank * 2 * W + e] = cnt[e];
+    reinterpret_cast<int32_t*>(P.region[p] + off)[P.rank * 2 * W + e] = cnt[(e & 1) * W + (e >> 1)];
   }
 }
 

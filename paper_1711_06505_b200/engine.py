@@ -243,8 +243,11 @@ class StepEngine:
             base += -(-f.vocab // id_align) * id_align
         self.id_key_space = base
         self.status = torch.zeros(L.STATUS_WORDS, dtype=torch.int32, device=dev)
-        # optimizer state (reference training.py:53-60)
-        self.grad = torch.zeros_like(model.dense)
+        # optimizer state (reference training.py:53-60); the gradient buffer
+        # carries one more slot, the loss, so that a multi-GPU step sums both
+        # with a single all-reduce (Adam's spans never cover that slot)
+        self.grad_ext = torch.zeros(model.dense.numel() + 1, dtype=torch.float32, device=dev)
+        self.grad = self.grad_ext[:-1]
         self.m = torch.zeros_like(model.dense)
         self.v = torch.zeros_like(model.dense)
         self.spans = (L.Span * len(model.dense_spans))()
@@ -455,7 +458,7 @@ class StepEngine:
                                          **f32)
         self.loss_part = torch.empty(self._head_blocks(max(B, 1)), **f32)
         self.attn_partial = torch.empty((L.lib.dicm_sample_blocks(max(B, 1)), max(self.attn_part, 1)), **f32)
-        self.loss = torch.zeros(1, **f32)
+        self.loss = self.grad_ext[-1:]
         lay = self.model.layout
         # deterministic backward (dicm_ref_transpose / dicm_sample_bwd): the
         # dedup inverses transposed, the sample of every CSR reference, and
@@ -783,7 +786,7 @@ class StepEngine:
         row_grads = self.d_rows if row_grads is None else row_grads
         row_cap = self.cap_k if row_cap is None else row_cap
         tabstate = self.tabstate if tabstate is None else tabstate
-        if not (self._rows_checked and row_grads is self.d_rows):
+        if not self._rows_checked:  # the step checked these rows on its forked branch already
             L.check(L.lib.dicm_check_finite(row_grads.data_ptr(), row_cap * 12, row_count.data_ptr(), 12, 4, st, s))
         self._rows_checked = False
         L.check(L.lib.dicm_adam_dense(self.model.dense.data_ptr(), self.grad.data_ptr(), self.m.data_ptr(),

@@ -303,7 +303,6 @@ class ClusterEngine(StepEngine):
         self.perm_img = torch.empty(cu, **i32)
         self.send_id = torch.empty(ck, **i32)
         self.perm_id = torch.empty(ck, **i32)
-        self.cnt_pair = torch.zeros((G, 2), **i32)
         self.ws_bucket = _u8(L.lib.dicm_bucket_workspace(max(cu, ck), G), dev)
         self.rows_buf = torch.empty((max(cu, ck), 12), **f32)  # responses in / pushes out
         # owner side (worst case: every rank asks for all its keys here)
@@ -327,6 +326,7 @@ class ClusterEngine(StepEngine):
         self.resp = torch.empty((max(self.cap_ri, self.cap_rk), 12), **f32)
         self.d_rows_o = torch.empty((max(self.cap_ko, 1), 12), **f32)
         self.idx_ws = torch.empty(G * max(self.cap_o, self.cap_ko, 1), **i32)
+        self.idx_ws_img = torch.empty(G * max(self.cap_o, 1), **i32)  # the image reduce runs beside the ID one
         self.net = ImageNetBuffers(self.cap_o, self.pool.d_raw, self.prec_code, dev)
 
     @property
@@ -383,7 +383,7 @@ class ClusterEngine(StepEngine):
                                            self.send_id.data_ptr(), self._col(1), self.perm_id.data_ptr(),
                                            self.ws_bucket.data_ptr(), self.ws_bucket.numel(), s))
         self._mark("dedup+bucket")
-        pair = torch.stack([self._cnt_cols[0], self._cnt_cols[1]], dim=1)
+        pair = self._cnt_both.t().contiguous()
         sent, recv = exchange_counts(pair, self.group)
         self._mark("count exchange (host sync)")
         si, sk = sent[:, 0].tolist(), sent[:, 1].tolist()
@@ -443,14 +443,18 @@ class ClusterEngine(StepEngine):
         # (6) every dense gradient in one all-reduce (sum: the loss is already
         # divided by the union batch, runtime.py:374, training.py:42)
         self._mark("ID grads a2a + reduce")
-        dist.all_reduce(self.grad, group=self.group)
-        dist.all_reduce(self.loss, group=self.group)
+        dist.all_reduce(self.grad_ext, group=self.group)  # dense gradients and the loss
         self._mark("allreduce")
         return self.loss
 
     def _forward_backward_p2p(self, db, denominator=None):
         """The same iteration with every sparse exchange done by peer-memory
-        copy kernels and device-side counts: no host synchronisation."""
+        copy kernels and device-side counts: no host synchronisation.  The ID
+        chains run on a forked stream beside the image chain -- the owner's ID
+        rows go out while the image-MLP forward runs, the owner's ID-gradient
+        reduction and the head/attention partial reduces run beside the
+        image-MLP backward -- and one all-reduce sums the dense gradients and
+        the loss (a graph with parallel branches once captured)."""
         G = self.world
         self._marks = [] if self._timing else None
         self._mark("start")
@@ -466,6 +470,23 @@ class ClusterEngine(StepEngine):
             self.resp_id = torch.empty((max(self.px.cap_rk, 1), 12), dtype=torch.float32, device=self.dev)
             self.push_out_id = torch.empty((max(self.cap_k, 1), 12), dtype=torch.float32, device=self.dev)
         px = self.px
+        side = self._side_stream()
+        main_stream = torch.cuda.current_stream()
+
+        def on_side(fn):
+            """Run ``fn`` on the forked stream (ordered after everything queued
+            so far on the main stream), or inline without a fork."""
+            if side is None:
+                fn(s)
+                return
+            side.wait_stream(main_stream)
+            with torch.cuda.stream(side):
+                fn(side.cuda_stream)
+
+        def join():
+            if side is not None:
+                main_stream.wait_stream(side)
+
         self._dedup_images()
         self._dedup_ids()
         self._transpose_images()
@@ -477,17 +498,25 @@ class ClusterEngine(StepEngine):
         L.check(L.lib.dicm_bucket_by_owner(self.uniq_id.data_ptr(), cnt[1:].data_ptr(), self.cap_k, G,
                                            self.send_id.data_ptr(), self._col(1), self.perm_id.data_ptr(),
                                            self.ws_bucket.data_ptr(), self.ws_bucket.numel(), s))
-        torch.stack([self._cnt_cols[0], self._cnt_cols[1]], dim=1, out=self.cnt_pair)
         self._mark("dedup+bucket")
         # (2) counts -> every peer, then the request keys (C1, C3)
-        px.counts(self.cnt_pair.data_ptr(), s)
+        px.counts(self._col(0), s)
         px.barrier(st, s)
         px.plan_from_counts(self.segs_img.data_ptr(), self.segs_id.data_ptr(), self.cnt_dev.data_ptr(), s)
         px.scatter(0, 0, self.send_img.data_ptr(), 4, "recv_img", s)
         px.scatter(1, 0, self.send_id.data_ptr(), 4, "recv_id", s)
         px.barrier(st, s)
         self._mark("counts + keys")
-        # (3) owner: dedup across sources, one image-MLP forward per distinct image, ID rows back (C2, C3)
+
+        # (3) owner: ID rows back to the requesters (C3) on the branch, beside
+        # the image chain: dedup across sources, one image-MLP forward per
+        # distinct image, embeddings back (C2)
+        def id_rows_out(ss):
+            L.check(L.lib.dicm_gather_rows_by_key(self.owner_tabstate, len(self.fields), px.recv_id.data_ptr(),
+                                                  self.cnt_dev[1:].data_ptr(), px.cap_rk, self.resp_id.data_ptr(), ss))
+            px.scatter(1, 1, self.resp_id.data_ptr(), 48, "back_id", ss)
+
+        on_side(id_rows_out)
         L.check(L.lib.dicm_dedup_devn(px.recv_img.data_ptr(), self.cnt_dev.data_ptr(), px.cap_ri,
                                       self.pool.local_rows, self.ws_img_owner.data_ptr(), self.ws_img_owner.numel(),
                                       self.uniq_o.data_ptr(), self.inv_o.data_ptr(), cnt[2:].data_ptr(), 2, st, s))
@@ -498,17 +527,15 @@ class ClusterEngine(StepEngine):
         L.check(L.lib.dicm_permute_rows12(self.net.emb.data_ptr(), self.inv_o.data_ptr(), self.cnt_dev.data_ptr(),
                                           px.cap_ri, 0, self.resp.data_ptr(), s))
         px.scatter(0, 1, self.resp.data_ptr(), 48, "back_img", s)
-        L.check(L.lib.dicm_gather_rows_by_key(self.owner_tabstate, len(self.fields), px.recv_id.data_ptr(),
-                                              self.cnt_dev[1:].data_ptr(), px.cap_rk, self.resp_id.data_ptr(), s))
-        px.scatter(1, 1, self.resp_id.data_ptr(), 48, "back_id", s)
+        join()
         px.barrier(st, s)
         L.check(L.lib.dicm_permute_rows12(px.back_img.data_ptr(), self.perm_img.data_ptr(), cnt.data_ptr(),
                                           self.cap_u, 0, self.emb_l.data_ptr(), s))
         L.check(L.lib.dicm_permute_rows12(px.back_id.data_ptr(), self.perm_id.data_ptr(), cnt[1:].data_ptr(),
                                           self.cap_k, 0, self.id_rows.data_ptr(), s))
         self._mark("rows back")
-        # (4) local pooling + head
-        self._local_step(self.emb_l, self.d_emb_l, denom)
+        # (4) local pooling + head (the partial reduces wait for step 6)
+        self._local_step(self.emb_l, self.d_emb_l, denom, reduce=False)
         self._mark("pooling+head")
         # (5) gradients to the owners (C4, C5); owners reduce in ascending source order
         L.check(L.lib.dicm_permute_rows12(self.d_emb_l.data_ptr(), self.perm_img.data_ptr(), cnt.data_ptr(),
@@ -518,31 +545,41 @@ class ClusterEngine(StepEngine):
         px.scatter(0, 0, self.rows_buf.data_ptr(), 48, "push_img", s)
         px.scatter(1, 0, self.push_out_id.data_ptr(), 48, "push_id", s)
         px.barrier(st, s)
+        self._mark("grads to owners")
+
+        # (6) on the branch: the owner's ID-row gradients and the head /
+        # attention partial reduces; on the main stream the image-MLP backward
+        def id_grads_and_partials(ss):
+            L.check(L.lib.dicm_dedup_devn(px.recv_id.data_ptr(), self.cnt_dev[1:].data_ptr(), px.cap_rk,
+                                          self.local_id_space, self.ws_id_owner.data_ptr(), self.ws_id_owner.numel(),
+                                          self.uniq_id_o.data_ptr(), self.inv_id_o.data_ptr(), cnt[3:].data_ptr(), 3,
+                                          st, ss))
+            L.check(L.lib.dicm_owner_reduce_rows12(px.push_id.data_ptr(), self.inv_id_o.data_ptr(),
+                                                   self.segs_id.data_ptr(), G, px.cap_rk, cnt[3:].data_ptr(),
+                                                   self.cap_ko, self.idx_ws.data_ptr(), self.d_rows_o.data_ptr(), ss))
+            L.check(L.lib.dicm_check_finite(self.d_rows_o.data_ptr(), self.cap_ko * 12, cnt[3:].data_ptr(), 12, 4,
+                                            st, ss))
+            self._reduce_partials(ss)
+
         L.check(L.lib.dicm_owner_reduce_rows12(px.push_img.data_ptr(), self.inv_o.data_ptr(),
                                                self.segs_img.data_ptr(), G, px.cap_ri, cnt[2:].data_ptr(),
-                                               self.cap_o, self.idx_ws.data_ptr(), self.net.d_emb.data_ptr(), s))
-        self._mark("grads to owners")
-        # (6) owner image-MLP backward; ID rows
+                                               self.cap_o, self.idx_ws_img.data_ptr(), self.net.d_emb.data_ptr(), s))
+        on_side(id_grads_and_partials)
         self._image_backward(self.net, self.uniq_o, cnt[2:].data_ptr(), self.cap_o if self.n_img_segs else 0)
-        self._mark("image MLP bwd")
-        L.check(L.lib.dicm_dedup_devn(px.recv_id.data_ptr(), self.cnt_dev[1:].data_ptr(), px.cap_rk,
-                                      self.local_id_space, self.ws_id_owner.data_ptr(), self.ws_id_owner.numel(),
-                                      self.uniq_id_o.data_ptr(), self.inv_id_o.data_ptr(), cnt[3:].data_ptr(), 3,
-                                      st, s))
-        L.check(L.lib.dicm_owner_reduce_rows12(px.push_id.data_ptr(), self.inv_id_o.data_ptr(),
-                                               self.segs_id.data_ptr(), G, px.cap_rk, cnt[3:].data_ptr(),
-                                               self.cap_ko, self.idx_ws.data_ptr(), self.d_rows_o.data_ptr(), s))
-        self._mark("ID grads")
-        # (7) every dense gradient in one all-reduce
-        dist.all_reduce(self.grad, group=self.group)
-        dist.all_reduce(self.loss, group=self.group)
+        join()
+        self._rows_checked = True
+        self._mark("image MLP bwd || ID grads")
+        # (7) every dense gradient and the loss in one all-reduce
+        dist.all_reduce(self.grad_ext, group=self.group)
         self._mark("allreduce")
         return self.loss
-
     def _col(self, j):
-        if not hasattr(self, "_cnt_cols") or self._cnt_cols[0].numel() != self.world:
-            self._cnt_cols = [torch.zeros(self.world, dtype=torch.int32, device=self.dev) for _ in range(2)]
-        return self._cnt_cols[j].data_ptr()
+        """Per-owner send counts: row j of one [2][world] buffer (image keys,
+        ID keys) that dicm_p2p_counts reads as a whole."""
+        if not hasattr(self, "_cnt_both") or self._cnt_both.shape[1] != self.world:
+            self._cnt_both = torch.zeros((2, self.world), dtype=torch.int32, device=self.dev)
+            self._cnt_cols = [self._cnt_both[0], self._cnt_both[1]]
+        return self._cnt_both[j].data_ptr()
 
     def optimizer_step(self, lr):
         super().optimizer_step(lr, row_keys=self.uniq_id_o, row_count=self.counts[3:], row_grads=self.d_rows_o,

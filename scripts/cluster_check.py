@@ -148,6 +148,12 @@ def main():
             t_ok &= O.rel_err(opt[f"id_emb/{name}#m"], st["m"]) < max(tol, 1e-3)
         ok &= t_ok
         report["opt_t_ok"] = bool(t_ok)
+        if a.mode == "graphs":
+            # every kernel node of the captured step: this library's, the CUB
+            # sorts of dicm_ref_transpose, and the one NCCL all-reduce
+            own, cub, total = cl.engine.kernel_nodes(detail=True)
+            report["graph_nodes"] = {"own": own, "cub": cub, "total": total}
+            ok &= total - own - cub <= 1
         report["worst"] = max(worst.values())
         report["worst_param"] = max(worst, key=worst.get)
         print(json.dumps({"ok": bool(ok), "world": world, "workers": M, "servers": N, "kind": kind,
