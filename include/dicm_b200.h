@@ -225,12 +225,20 @@ int dicm_sample_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv,
                     dicm_stream_t stream);
 /* Stream-ordered on `stream`.  Writes every row d_emb[0..U) and
  * d_rows[0..K) (no zeroing needed); the scratch buffers of the batch view are
- * overwritten. */
+ * overwritten.  d_rows = NULL leaves the ID rows to dicm_id_row_grads, which
+ * may then run on another stream (after this call) beside the image-MLP
+ * backward. */
 int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv,
                     const dicm_attn_params_t* attn, const float* head_in, const float* d_head_in,
                     const float* scores, const float* stats, float* d_emb /* [U,12] */,
                     float* d_rows /* [K,12] */, float* attn_partials,
                     dicm_stream_t stream);
+
+/* The ID-row half of dicm_sample_bwd: d_rows[0..K), each unique (field, row)
+ * key the ordered sum of its references' gradients (np.add.at into the
+ * table gradient, autograd.py:267-271, model.py:407-408). */
+int dicm_id_row_grads(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const float* d_head_in,
+                      float* d_rows /* [K,12] */, dicm_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * a11-a12: head MLP width -> 128 -> 64 -> 1 and BCE (reference model.py:397-401,

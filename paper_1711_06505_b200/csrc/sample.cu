@@ -282,7 +282,8 @@ __device__ void attn_fwd(const Args& a, const AttnSmem& s, int ch, int b, int la
     if (lane == c) dst[c] = out[c];
 }
 
-__global__ void __launch_bounds__(FWD_WARPS * 32, 2) k_sample_fwd(const __grid_constant__ Args a) {
+template <int MINB>  // resident blocks per SM the register budget is cut for (DICM_FWD_OCC, default 3)
+__global__ void __launch_bounds__(FWD_WARPS * 32, MINB) k_sample_fwd(const __grid_constant__ Args a) {
   __shared__ AttnSmem sa[2];
   __shared__ __align__(16) float Pw[FWD_WARPS][DICM_ATT];  // per-warp query projection
   const bool att = a.L.use_behavior_images && (a.L.kind == 1 || a.L.kind == 2);
@@ -461,7 +462,8 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
     __syncwarp();
     // lane j: hidden unit j across the chunk's references
     const int nr = (int)min((int64_t)32, i1 - c0);
-    for (int r = 0; r < nr; ++r) {
+#pragma unroll 4
+    for (int r = 0; r < nr; ++r) {  // unrolled: independent pre-activation chains interleave
       const float4* kr = reinterpret_cast<const float4*>(ws.ks[r]);
       const float4 k0 = kr[0], k1 = kr[1], k2 = kr[2];
       // the forward's pre-activation, same fma order (attn_score_rc)
@@ -828,7 +830,14 @@ int dicm_sample_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
   const int grid = (bv->batch + FWD_WARPS - 1) / FWD_WARPS;
   {
     const int probe_slot = probe_begin(DICM_PROBE_SAMPLE_FWD, (cudaStream_t)stream);
-    k_sample_fwd<<<grid, FWD_WARPS * 32, 0, (cudaStream_t)stream>>>(a);
+    static const int occ = [] {
+      const char* e = getenv("DICM_FWD_OCC");
+      return e && e[0] == '2' ? 2 : 3;
+    }();
+    if (occ == 2)
+      k_sample_fwd<2><<<grid, FWD_WARPS * 32, 0, (cudaStream_t)stream>>>(a);
+    else
+      k_sample_fwd<3><<<grid, FWD_WARPS * 32, 0, (cudaStream_t)stream>>>(a);
     probe_end(probe_slot, (cudaStream_t)stream);
   }
   return last_launch("dicm_sample_fwd");
@@ -889,6 +898,18 @@ static RefSrc id_src(const dicm_layout_t* L, const dicm_batch_view_t* V, const f
   return S;
 }
 
+// every unique ID row's gradient (the hot-key counter bv->hot[1] must be
+// zero; dicm_sample_bwd clears both counters before its kernels)
+static void launch_id_reduce(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const float* d_head_in,
+                             float* d_rows, cudaStream_t st) {
+  if (layout->n_fields <= 0) return;
+  int32_t* hot_list_id = bv->hot + 2 + bv->img_cap;
+  const RefSrc S = id_src(layout, bv, d_head_in);
+  k_ref_reduce<<<dicm_grid(bv->id_cap, 256, 148 * 16), 256, 0, st>>>(S, bv->id_order, bv->id_start, bv->n_id_keys,
+                                                                   bv->id_cap, d_rows, bv->hot + 1, hot_list_id);
+  k_ref_reduce_hot<<<148, 256, 0, st>>>(S, bv->id_order, bv->id_start, bv->hot + 1, hot_list_id, d_rows);
+}
+
 int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const dicm_attn_params_t* attn,
                     const float* head_in, const float* d_head_in, const float* scores, const float* stats,
                     float* d_emb, float* d_rows, float* attn_partials, dicm_stream_t stream) {
@@ -940,14 +961,20 @@ int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
                                                                       bv->img_cap, d_emb, bv->hot, hot_list_img);
     k_ref_reduce_hot<<<148, 256, 0, st>>>(S, bv->img_order, bv->img_start, bv->hot, hot_list_img, d_emb);
   }
-  if (layout->n_fields > 0) {
-    const RefSrc S = id_src(layout, bv, d_head_in);
-    k_ref_reduce<<<dicm_grid(bv->id_cap, 256, 148 * 16), 256, 0, st>>>(S, bv->id_order, bv->id_start, bv->n_id_keys,
-                                                                     bv->id_cap, d_rows, bv->hot + 1, hot_list_id);
-    k_ref_reduce_hot<<<148, 256, 0, st>>>(S, bv->id_order, bv->id_start, bv->hot + 1, hot_list_id, d_rows);
-  }
+  (void)hot_list_id;
+  if (d_rows) launch_id_reduce(layout, bv, d_head_in, d_rows, st);
   probe_end(probe_slot, st);
   return last_launch("dicm_sample_bwd");
+}
+
+int dicm_id_row_grads(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const float* d_head_in,
+                      float* d_rows, dicm_stream_t stream) {
+  int rc = validate(layout, bv);
+  if (rc) return rc;
+  if (bv->batch == 0) return DICM_OK;
+  if (!bv->hot || !bv->id_order) return fail(DICM_ERR_VALUE, "id_row_grads: the batch view lacks its buffers");
+  launch_id_reduce(layout, bv, d_head_in, d_rows, (cudaStream_t)stream);
+  return last_launch("dicm_id_row_grads");
 }
 
 }  // extern "C"

@@ -685,14 +685,15 @@ class StepEngine:
                 L.check(L.lib.dicm_csr_segments(self._dptr(o), pk.B, self.id_seg.data_ptr() + 4 * self.inv_id_off[f.name],
                                                 self.s))
 
-    def _local_step(self, emb, d_emb, denom, reduce=True):
+    def _local_step(self, emb, d_emb, denom, reduce=True, id_rows=True):
         """a6-a12 forward and backward on the local batch: pooling, head, BCE.
         Reads image embeddings ``emb`` and compact ID rows ``self.id_rows``;
-        writes ``d_emb`` / ``self.d_rows`` and the head/attention gradients."""
+        writes ``d_emb`` / ``self.d_rows`` (``id_rows=False``: left to
+        ``_id_row_grads``) and the head/attention gradients."""
         pk, s = self.pk, self.s
         B = pk.B
         st = self.status.data_ptr()
-        bv = self._batch_view(emb)
+        bv = self._bv = self._batch_view(emb)
         L.check(L.lib.dicm_sample_fwd(C.byref(self.layout), C.byref(bv), self.attn, self.head_in.data_ptr(),
                                       self.scores.data_ptr(), self.stats.data_ptr(), s))
         self._head_fwd_bwd(B, denom)
@@ -700,9 +701,14 @@ class StepEngine:
         L.check(L.lib.dicm_loss_finalize(self.loss_part.data_ptr(), nhb, 1.0 / denom, self.loss.data_ptr(), st, s))
         L.check(L.lib.dicm_sample_bwd(C.byref(self.layout), C.byref(bv), self.attn, self.head_in.data_ptr(),
                                       self.d_head_in.data_ptr(), self.scores.data_ptr(), self.stats.data_ptr(),
-                                      d_emb.data_ptr(), self.d_rows.data_ptr(), self.attn_partial.data_ptr(), s))
+                                      d_emb.data_ptr(), self.d_rows.data_ptr() if id_rows else None,
+                                      self.attn_partial.data_ptr(), s))
         if reduce:
             self._reduce_partials(s)
+
+    def _id_row_grads(self, s):
+        L.check(L.lib.dicm_id_row_grads(C.byref(self.layout), C.byref(self._bv), self.d_head_in.data_ptr(),
+                                        self.d_rows.data_ptr(), s))
 
     def _reduce_partials(self, s):
         """Head and attention parameter gradients from their block partials
@@ -764,10 +770,11 @@ class StepEngine:
             torch.cuda.current_stream().wait_stream(side)
         else:
             self._gather_id_rows()
-        self._local_step(self.net.emb, self.net.d_emb, denom, reduce=side is None)
-        if side is not None:  # the partial reduces overlap the image-MLP backward
+        self._local_step(self.net.emb, self.net.d_emb, denom, reduce=side is None, id_rows=side is None)
+        if side is not None:  # the ID-row gradients and the partial reduces overlap the image-MLP backward
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):
+                self._id_row_grads(side.cuda_stream)
                 self._reduce_partials(side.cuda_stream)
                 # the row-gradient finite check (optimizer_step) needs only dRows
                 L.check(L.lib.dicm_check_finite(self.d_rows.data_ptr(), self.cap_k * 12, self.counts[1:].data_ptr(),
