@@ -28,6 +28,49 @@ int check_cuda(cudaError_t e, const char* where) {
 
 int last_launch(const char* where) { return check_cuda(cudaGetLastError(), where); }
 
+// Library-owned side streams: one per (host thread, device, purpose), created
+// outside any capture (relaxed capture mode), with a fork and a join event.
+// DICM_FORK=0 turns every fork off (the work stays on the caller's stream).
+Fork* side_fork(int purpose) {
+  static const bool off = [] {
+    const char* e = getenv("DICM_FORK");
+    return e && e[0] == '0';
+  }();
+  if (off || purpose < 0 || purpose >= kForkPurposes) return nullptr;
+  constexpr int kMaxDev = 64;
+  thread_local Fork forks[kMaxDev][kForkPurposes];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+  Fork& f = forks[dev][purpose];
+  if (!f.side) {
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    const bool ok = cudaStreamCreateWithFlags(&f.side, cudaStreamNonBlocking) == cudaSuccess &&
+                    cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming) == cudaSuccess &&
+                    cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming) == cudaSuccess;
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    if (!ok) {
+      cudaGetLastError();
+      f.side = nullptr;
+      return nullptr;
+    }
+  }
+  return &f;
+}
+
+cudaStream_t fork_begin(Fork* f, cudaStream_t main) {
+  if (!f) return main;
+  cudaEventRecord(f->fork, main);
+  cudaStreamWaitEvent(f->side, f->fork, 0);
+  return f->side;
+}
+
+void fork_end(Fork* f, cudaStream_t main) {
+  if (!f) return;
+  cudaEventRecord(f->join, f->side);
+  cudaStreamWaitEvent(main, f->join, 0);
+}
+
 // Kernel timing probe: CUDA events recorded on the launching stream around
 // the dominant kernels, read back by bench.py for the roofline.
 namespace {

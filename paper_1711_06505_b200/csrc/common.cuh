@@ -26,6 +26,17 @@ int last_launch(const char* where);
 int probe_begin(int kernel, cudaStream_t st);  // -1 when probing is off
 void probe_end(int slot, cudaStream_t st);
 
+// a side stream forked from the caller's stream and joined before the call
+// returns (parallel branches under graph capture); nullptr when forks are off
+struct Fork {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+constexpr int kForkPurposes = 2;  // 0: image-MLP backward reduces
+Fork* side_fork(int purpose);
+cudaStream_t fork_begin(Fork* f, cudaStream_t main);  // the stream to launch the branch on
+void fork_end(Fork* f, cudaStream_t main);
+
 // ---- device helpers -------------------------------------------------------
 __device__ __forceinline__ float prelu(float x, float a) { return x > 0.f ? x : a * x; }
 

@@ -377,26 +377,31 @@ int dicm_imgmlp_bwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
       rc = sm100::bwd_layers12(demb, act1, act0, w.h1, count_dev, rows_max, p->a0, p->a1, p->w1, p->w2, w.da1, w.da0,
                              da0_bf16, w.pl12, w.pdw1, st);
     if (rc) return rc;
+    // the layer-1/2 gradient reduces only feed the optimizer: they run on a
+    // forked stream beside the layer-0 dW0 kernel (joined before returning)
+    Fork* fk = side_fork(0);
+    cudaStream_t rs = fork_begin(fk, st);
     const int nb = sm100::small_bwd_blocks(rows_max), ps = sm100::small_part_size();
     {
       // w2 | b2 | a1 | b1 (| a0 | b0 on the tf32 path) in one launch
       const int64_t off[6] = {0, DICM_D * H2, DICM_D * H2 + DICM_D, DICM_D * H2 + DICM_D + H2, L2_PART, L2_PART + H1};
       const int64_t n[6] = {DICM_D * H2, DICM_D, H2, H2, H1, H1};
       float* const out[6] = {g->w2, g->b2, g->a1, g->b1, g->a0, g->b0};
-      reduce_multi(st, w.pl12, nb, ps, bf16 ? 4 : 6, off, n, out);
+      reduce_multi(rs, w.pl12, nb, ps, bf16 ? 4 : 6, off, n, out);
     }
     if (bf16) {
       // dW1 / dalpha0 / db0 from the three row GEMMs of k_dw1b
       const int gp = sm100::dw1_bf16_part_size();
-      reduce(st, w.pdw1, sm100::small_dw1_blocks(rows_max), gp, 0, gp, w.g3);
-      rc = sm100::l1_finish_bf16(w.g3, p->w1, p->a0, g->b1, g->w1, g->a0, g->b0, st);
-      if (rc) return rc;
+      reduce(rs, w.pdw1, sm100::small_dw1_blocks(rows_max), gp, 0, gp, w.g3);
+      rc = sm100::l1_finish_bf16(w.g3, p->w1, p->a0, g->b1, g->w1, g->a0, g->b0, rs);
     } else {
-      reduce(st, w.pdw1, sm100::small_dw1_blocks(rows_max), (int64_t)H2 * H1, 0, (int64_t)H2 * H1, g->w1);
+      reduce(rs, w.pdw1, sm100::small_dw1_blocks(rows_max), (int64_t)H2 * H1, 0, (int64_t)H2 * H1, g->w1);
     }
-    rc = sm100::bwd_dw0(pool, pool_dtype, d_raw, rows, count_dev, rows_max, w.da0, g->w0, precision, tc_ws, st,
-                        bf16);
+    int rc0 = sm100::bwd_dw0(pool, pool_dtype, d_raw, rows, count_dev, rows_max, w.da0, g->w0, precision, tc_ws, st,
+                             bf16);
+    fork_end(fk, st);
     if (rc) return rc;
+    if (rc0) return rc0;
     return last_launch("dicm_imgmlp_bwd");
   }
   // layer 2 + prelu 1
