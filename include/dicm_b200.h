@@ -432,6 +432,14 @@ int dicm_p2p_plan(const dicm_peers_t* peers, int64_t cmat_off, int64_t* seg_img,
                   int32_t* cnt_dev, int64_t* plan, dicm_stream_t stream);
 int dicm_p2p_scatter(const dicm_peers_t* peers, const int64_t* plan, int kind /* 0 img, 1 id */,
                      int dir, const void* src, int row_bytes, int64_t dst_off, dicm_stream_t stream);
+/* Sum of src[0..n) over every rank, into dst on every rank, over peer
+ * memory: stage into this rank's region (stage_off, float4-padded), barrier,
+ * each rank reduces 1/world of the elements in rank order and writes the sums
+ * into every rank's region (res_off), barrier, copy out.  The same order on
+ * every rank: bit-identical replicas (the dense all-reduce of runtime.py's
+ * WorkerSync/ServerSync phases 4-5, runtime.py:424-463). */
+int dicm_p2p_allreduce(const dicm_peers_t* peers, const float* src, int64_t n, int64_t stage_off,
+                       int64_t res_off, int64_t flags_off, int32_t* status, float* dst, dicm_stream_t stream);
 /* dedup of keys[0..*n_dev) (n_dev on the device, n_max its bound) over
  * [0, vocab): the owner-side dedup across sources (runtime.py:143-150) */
 int dicm_dedup_devn(const int32_t* keys, const int32_t* n_dev, int64_t n_max, int64_t vocab, void* workspace,

@@ -147,9 +147,57 @@ int check_peers(const dicm_peers_t* p) {
   return DICM_OK;
 }
 
+// one chunk of the all-reduce: this rank sums float4 i of every rank's staged
+// buffer in rank order (the same order on every rank: bit-identical results)
+// and writes the sum into every rank's result buffer over NVLink
+__global__ void __launch_bounds__(256) k_allreduce_chunk(const __grid_constant__ Peers P, int64_t stage_off,
+                                                         int64_t res_off, int64_t n4) {
+  const int W = P.world;
+  const int64_t per = (n4 + W - 1) / W, lo = per * P.rank, hi = min(n4, lo + per);
+  for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 v[DICM_MAX_PEERS];
+#pragma unroll
+    for (int q = 0; q < DICM_MAX_PEERS; ++q)
+      if (q < W) v[q] = __ldcv(reinterpret_cast<const float4*>(P.region[q] + stage_off) + i);
+    float4 s = v[0];
+#pragma unroll
+    for (int q = 1; q < DICM_MAX_PEERS; ++q)
+      if (q < W) {
+        s.x += v[q].x;
+        s.y += v[q].y;
+        s.z += v[q].z;
+        s.w += v[q].w;
+      }
+#pragma unroll
+    for (int q = 0; q < DICM_MAX_PEERS; ++q)
+      if (q < W) reinterpret_cast<float4*>(P.region[q] + res_off)[i] = s;
+  }
+}
+
 }  // namespace
 
 extern "C" {
+
+int dicm_p2p_allreduce(const dicm_peers_t* peers, const float* src, int64_t n, int64_t stage_off, int64_t res_off,
+                       int64_t flags_off, int32_t* status, float* dst, dicm_stream_t stream) {
+  int rc = check_peers(peers);
+  if (rc) return rc;
+  if (n <= 0) return DICM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Peers P = to_dev(peers);
+  const int64_t n4 = (n + 3) / 4;  // the staged buffers are float4-padded (the pad holds zeros)
+  rc = dicm::check_cuda(cudaMemcpyAsync(P.region[P.rank] + stage_off, src, n * sizeof(float),
+                                        cudaMemcpyDeviceToDevice, st), "p2p allreduce stage");
+  if (rc) return rc;
+  k_barrier<<<1, 32, 0, st>>>(P, flags_off, 0, status);  // every rank's gradients are staged
+  const int grid = (int)std::min<int64_t>(148 * 4, (n4 / P.world + 255) / 256 + 1);
+  k_allreduce_chunk<<<grid, 256, 0, st>>>(P, stage_off, res_off, n4);
+  k_barrier<<<1, 32, 0, st>>>(P, flags_off, 0, status);  // every chunk's sum has landed everywhere
+  rc = dicm::check_cuda(cudaMemcpyAsync(dst, P.region[P.rank] + res_off, n * sizeof(float),
+                                        cudaMemcpyDeviceToDevice, st), "p2p allreduce result");
+  if (rc) return rc;
+  return dicm::last_launch("dicm_p2p_allreduce");
+}
 
 int dicm_p2p_alloc(size_t bytes, void** out) {
   using namespace dicm;

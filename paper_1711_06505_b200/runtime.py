@@ -145,7 +145,7 @@ class PeerExchange:
 
     Capacities are agreed once (max over ranks) when the region is built."""
 
-    def __init__(self, world, rank, cap_u, cap_k, local_rows, local_id_space, group=None):
+    def __init__(self, world, rank, cap_u, cap_k, local_rows, local_id_space, group=None, dense_n=0):
         dev = torch.device("cuda", torch.cuda.current_device())
         # every capacity the layout depends on is agreed (max over ranks):
         # a peer writes into our region at ITS offsets, so the layout must be
@@ -172,6 +172,10 @@ class PeerExchange:
         take("push_id", self.cap_rk * 48)
         take("back_img", cap_u * 48)
         take("back_id", cap_k * 48)
+        # the dense all-reduce (dicm_p2p_allreduce): staged gradients and sums
+        self.dense_n = int(dense_n)
+        take("grad_stage", (self.dense_n + 3) // 4 * 16)
+        take("grad_sum", (self.dense_n + 3) // 4 * 16)
         self.off, self.bytes = layout, off
         lay = torch.tensor([off] + [layout[k] for k in sorted(layout)], dtype=torch.int64, device=dev)
         lo, hi = lay.clone(), lay.clone()
@@ -210,6 +214,12 @@ class PeerExchange:
 
     def _view(self, name, shape, typestr):
         return torch.as_tensor(_ExtMem(self.base + self.off[name], shape, typestr), device="cuda")
+
+    def allreduce(self, buf, status, s):
+        """buf (the fused gradient buffer + loss, float32, dense_n elements) <-
+        its sum over every rank, in rank order (bit-identical replicas)."""
+        L.check(L.lib.dicm_p2p_allreduce(C.byref(self.peers), buf.data_ptr(), self.dense_n, self.off["grad_stage"],
+                                         self.off["grad_sum"], self.off["flags"], status, buf.data_ptr(), s))
 
     def barrier(self, status, s):
         # epoch 0: the kernel advances a device-side counter (CUDA-graph safe)
@@ -257,6 +267,9 @@ class ClusterEngine(StepEngine):
         self.segs_id = torch.zeros(world + 1, dtype=torch.int64, device=dev)
         self._seg_host = torch.zeros(2 * (world + 1), dtype=torch.int64, pin_memory=True)
         self._timing = os.environ.get("DICM_PHASE_TIMING") == "1"
+        self._allreduce = os.environ.get("DICM_ALLREDUCE", "p2p")
+        if self._allreduce not in ("p2p", "nccl"):
+            raise ValueError(f"DICM_ALLREDUCE must be p2p or nccl, got {self._allreduce!r}")
         self._marks = None
 
     @property
@@ -304,6 +317,7 @@ class ClusterEngine(StepEngine):
         self.send_id = torch.empty(ck, **i32)
         self.perm_id = torch.empty(ck, **i32)
         self.ws_bucket = _u8(L.lib.dicm_bucket_workspace(max(cu, ck), G), dev)
+        self.ws_bucket_id = _u8(L.lib.dicm_bucket_workspace(max(cu, ck), G), dev)
         self.rows_buf = torch.empty((max(cu, ck), 12), **f32)  # responses in / pushes out
         # owner side (worst case: every rank asks for all its keys here)
         self._alloc_owner(G * cu, G * ck)
@@ -465,7 +479,7 @@ class ClusterEngine(StepEngine):
             if self.px is not None:
                 raise RuntimeError("batch outgrew the peer exchange region built at the first iteration")
             self.px = PeerExchange(G, self.rank, self.cap_u, self.cap_k, self.pool.local_rows,
-                                   self.local_id_space, self.group)
+                                   self.local_id_space, self.group, dense_n=self.grad_ext.numel())
             self._alloc_owner(self.px.cap_ri, self.px.cap_rk)  # every owner buffer at the agreed capacity
             self.resp_id = torch.empty((max(self.px.cap_rk, 1), 12), dtype=torch.float32, device=self.dev)
             self.push_out_id = torch.empty((max(self.cap_k, 1), 12), dtype=torch.float32, device=self.dev)
@@ -489,15 +503,21 @@ class ClusterEngine(StepEngine):
 
         self._dedup_images()
         self._dedup_ids()
-        self._transpose_images()
-        self._transpose_ids()
+
+        def transposes(ss):  # the backward's summation order: needed only at the local step
+            saved, self.s = self.s, ss
+            self._transpose_images()
+            self._transpose_ids()
+            self.s = saved
+
+        on_side(transposes)
         cnt = self.counts
         L.check(L.lib.dicm_bucket_by_owner(self.uniq_img.data_ptr(), cnt.data_ptr(), self.cap_u, G,
                                            self.send_img.data_ptr(), self._col(0), self.perm_img.data_ptr(),
                                            self.ws_bucket.data_ptr(), self.ws_bucket.numel(), s))
         L.check(L.lib.dicm_bucket_by_owner(self.uniq_id.data_ptr(), cnt[1:].data_ptr(), self.cap_k, G,
                                            self.send_id.data_ptr(), self._col(1), self.perm_id.data_ptr(),
-                                           self.ws_bucket.data_ptr(), self.ws_bucket.numel(), s))
+                                           self.ws_bucket_id.data_ptr(), self.ws_bucket_id.numel(), s))
         self._mark("dedup+bucket")
         # (2) counts -> every peer, then the request keys (C1, C3)
         px.counts(self._col(0), s)
@@ -569,8 +589,13 @@ class ClusterEngine(StepEngine):
         join()
         self._rows_checked = True
         self._mark("image MLP bwd || ID grads")
-        # (7) every dense gradient and the loss in one all-reduce
-        dist.all_reduce(self.grad_ext, group=self.group)
+        # (7) every dense gradient and the loss in one all-reduce over peer
+        # memory (rank-order sums: bit-identical replicas); DICM_ALLREDUCE=nccl
+        # uses NCCL instead
+        if self._allreduce == "nccl":
+            dist.all_reduce(self.grad_ext, group=self.group)
+        else:
+            px.allreduce(self.grad_ext, st, s)
         self._mark("allreduce")
         return self.loss
     def _col(self, j):

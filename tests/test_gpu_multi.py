@@ -20,7 +20,10 @@ def _run(world, args, env=None, port=29531):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "scripts", "cluster_check.py")]
     r = subprocess.run(cmd + args, capture_output=True, text=True, timeout=600, env=env)
-    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
+    if r.returncode:
+        print(r.stdout[-6000:])
+        print(r.stderr[-6000:])
+    assert r.returncode == 0
     return r
 
 
