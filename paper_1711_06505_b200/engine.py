@@ -226,8 +226,13 @@ class StepEngine:
             raise ValueError(f"precision must be one of {tuple(L.PRECISIONS)}")
         if precision == "bf16" and pool.dtype_name != "bf16":
             raise ValueError("bf16 tensor-core mode needs a bf16 pool")
-        if pool.d_raw != model.schema.d_raw:
+        self.store = pool  # the caller's pool (the engine may hold a padded copy)
+        if pool.d_raw != model.schema.d_raw and pool.d_raw != model.geometry.d_raw:
             raise ValueError(f"pool rows are {pool.d_raw}-D, schema expects {model.schema.d_raw}")
+        if pool.d_raw != model.geometry.d_raw:
+            # rows narrower than the kernels' multiple of 256: one zero-padded
+            # device copy (the padded columns meet zero columns of img/0/w)
+            pool = pool.padded(model.geometry.d_raw)
         self.model, self.pool = model, pool
         self.precision = precision
         self.prec_code = L.PRECISIONS[precision]
@@ -284,7 +289,7 @@ class StepEngine:
         pnames = ("img/0/w", "img/0/b", "img/0/a", "img/1/w", "img/1/b", "img/1/a", "img/2/w", "img/2/b")
         self.img_p = L.ImgMlpParams(**{k: p(n) for k, n in zip(names, pnames)})
         self.img_g = L.ImgMlpGrads(**{k: g(n) for k, n in zip(names, pnames)})
-        self.width = lay.mlp_input_width()
+        self.width = model.geometry.width  # the kernel head input (12-wide blocks)
         if lay.towers is None:
             hn = ("mlp/0/w", "mlp/0/b", "mlp/0/a", "mlp/1/w", "mlp/1/b", "mlp/1/a", "mlp/2/w", "mlp/2/b")
             self.head_p = L.HeadParams(**{k: p(n) for k, n in zip(names, hn)})
@@ -320,7 +325,7 @@ class StepEngine:
             for k, n in (("w0", "0/w"), ("b0", "0/b"), ("a0", "0/a"), ("w1", "1/w"), ("b1", "1/b")):
                 setattr(tw, k, model.params[pre + n].tensor.data_ptr())
                 setattr(tw, "g_" + k, model.dense_offsets[pre + n][0] - start)
-            parts = lay.tower_parts(t)
+            parts = model.geometry.tower_parts(t)
             tw.n_parts = len(parts)
             for j, (col, _w) in enumerate(parts):
                 tw.part_col[j] = col

@@ -72,10 +72,16 @@ class InferenceTable:
             self.embeddings = self._dev.double().cpu().numpy()
         return self.embeddings
 
-    def device(self, dev="cuda"):
+    def device(self, dev="cuda", width=None):
+        """The rows on the device, zero-padded to ``width`` columns (the
+        kernels' 12-wide embedding rows) when given."""
         import torch
         if self._dev is None:
             self._dev = torch.as_tensor(self._host(), dtype=torch.float32, device=dev).contiguous()
+        if width is not None and self._dev.shape[1] < width:
+            out = torch.zeros((self._dev.shape[0], width), dtype=torch.float32, device=self._dev.device)
+            out[:, :self._dev.shape[1]] = self._dev
+            return out
         return self._dev
 
     def __len__(self):
@@ -98,7 +104,7 @@ class InferenceTable:
 def _engine_for(model, store, precision="fp32"):
     from .engine import StepEngine
     eng = getattr(model, "_infer_engine", None)
-    if eng is None or eng.pool is not store or eng.precision != precision:
+    if eng is None or eng.store is not store or eng.precision != precision:
         eng = StepEngine(model, store, precision)
         model._infer_engine = eng
     return eng
@@ -114,7 +120,7 @@ def export_inference(model, store, precision="fp32", chunk=1 << 19):
     out = torch.empty((max(n, 1), 12), dtype=torch.float32, device=eng.dev)
     eng.embed_rows(rows, n, out, chunk=chunk)
     eng.raise_status()
-    return InferenceTable(out[:n])
+    return InferenceTable(out[:n, :model.schema.d_img])
 
 
 def _as_batch(samples, model):
@@ -161,7 +167,7 @@ class KvPredictor:
     def predict(self, samples, chunk=1024):
         """(probabilities, logits) for the samples via table lookups."""
         eng = _engine_for(self.model, self.store, self.precision)
-        tab = self.table.device(eng.dev)
+        tab = self.table.device(eng.dev, width=12)
         b = _as_batch(samples, self.model)
         logits = np.empty(b.size)
         for start in range(0, b.size, chunk):

@@ -30,31 +30,72 @@ HEAD_MAX_WIDE = 16384   # DICM_HEAD_MAX_WIDE
 
 class Parameter:
     """A named device tensor; ``.data`` returns a float64 host copy like the
-    reference's ``Parameter.data`` (autograd.py:49-53)."""
+    reference's ``Parameter.data`` (autograd.py:49-53).
 
-    __slots__ = ("name", "tensor")
+    ``tensor`` is the kernel-shaped storage; a model narrower than the
+    compiled widths (schema.KernelGeometry) holds its real entries at
+    ``tensor[rows][:, cols]`` and zeros elsewhere -- ``shape``, ``data``,
+    ``real()`` and ``copy_`` see the real tensor only."""
 
-    def __init__(self, name, tensor):
+    __slots__ = ("name", "tensor", "rows", "cols")
+
+    def __init__(self, name, tensor, rows=None, cols=None):
         self.name = name
         self.tensor = tensor
+        self.rows = None if rows is None else torch.as_tensor(rows, device=tensor.device)
+        self.cols = None if cols is None else torch.as_tensor(cols, device=tensor.device)
 
     @property
     def shape(self):
-        return tuple(self.tensor.shape)
+        shp = list(self.tensor.shape)
+        if self.rows is not None:
+            shp[0] = len(self.rows)
+        if self.cols is not None:
+            shp[-1] = len(self.cols)
+        return tuple(shp)
+
+    def real(self):
+        """The real entries as a device tensor (a copy when padded)."""
+        return real_of(self.tensor, self.rows, self.cols)
 
     @property
     def data(self):
-        return self.tensor.detach().double().cpu().numpy()
+        return self.real().detach().double().cpu().numpy()
 
     def copy_(self, value):
-        self.tensor.copy_(torch.as_tensor(np.asarray(value), dtype=torch.float32))
+        write_real(self.tensor, self.rows, self.cols, value)
 
     def __repr__(self):
         return f"Parameter({self.name!r}, shape={self.shape})"
 
 
+def real_of(t, rows, cols):
+    """kernel-shaped t -> its real entries t[rows][:, cols]."""
+    if rows is not None:
+        t = t.index_select(0, rows)
+    if cols is not None:
+        t = t.index_select(t.dim() - 1, cols)
+    return t
+
+
+def write_real(t, rows, cols, value):
+    """t[rows][:, cols] = value (the padded entries are left as they are)."""
+    v = torch.as_tensor(np.asarray(value), dtype=t.dtype if t.dtype == torch.bool else torch.float32).to(t.device)
+    if rows is None and cols is None:
+        t.copy_(v)
+    elif t.dim() == 1:
+        t[rows] = v
+    elif cols is None:
+        t[rows] = v
+    elif rows is None:
+        t[:, cols] = v
+    else:
+        t[rows[:, None], cols[None, :]] = v
+
+
 def check_hot_path(layout):
-    """The kernels are compiled for the paper's configuration."""
+    """The kernels are compiled for the paper's configuration; narrower
+    widths embed into it (schema.KernelGeometry), wider ones raise."""
     s = layout.schema
     if layout.towers is not None:
         return _check_towers(layout)
@@ -62,45 +103,37 @@ def check_hot_path(layout):
         raise NotImplementedError(
             f"aggregator {layout.aggregator.kind!r} is outside this build's hot path "
             f"(supported: {S.HOT_PATH_AGGREGATORS})")
-    if s.d_id != 12 or s.d_img != 12:
-        raise NotImplementedError("kernels are built for d_id = d_img = 12")
-    if layout.h1 != 256 or layout.h2 != 64 or s.d_raw % 64:
-        raise NotImplementedError("kernels are built for the 4096 -> 256 -> 64 -> 12 image net")
-    if tuple(layout.mlp_widths) != (128, 64):
-        raise NotImplementedError("kernels are built for the (128, 64) head")
-    if layout.attentive and layout.aggregator.attention_hidden != 32:
-        raise NotImplementedError("kernels are built for a 32-unit attention net")
-    if layout.mlp_input_width() > HEAD_MAX_WIDE:
-        raise NotImplementedError(f"head input width {layout.mlp_input_width()} > {HEAD_MAX_WIDE}")
+    geom = S.KernelGeometry(layout)
     if len(s.fields) > 8:
         raise NotImplementedError("at most 8 ID fields")
     if layout.multiquery:
         for q in layout.query_fields_present():
             if s.field(q).multi:
                 raise NotImplementedError("multiquery-attn query fields must be one-hot")
+        if len(layout.query_fields_present()) > 2:
+            raise NotImplementedError("multiquery-attn takes at most 2 ID query fields")
+    return geom
 
 
 def _check_image_net(layout):
     s = layout.schema
-    if s.d_id != 12 or s.d_img != 12:
-        raise NotImplementedError("kernels are built for d_id = d_img = 12")
-    if layout.h1 != 256 or layout.h2 != 64 or s.d_raw % 64:
-        raise NotImplementedError("kernels are built for the 4096 -> 256 -> 64 -> 12 image net")
     if len(s.fields) > 8:
         raise NotImplementedError("at most 8 ID fields")
+    return S.KernelGeometry(layout)
 
 
 def _check_towers(layout):
     from . import _lib as L
-    _check_image_net(layout)
+    geom = _check_image_net(layout)
     tw = layout.towers
     if not 1 <= tw.hidden <= 128 or not 1 <= tw.rep <= 64:
         raise NotImplementedError("tower kernels take hidden <= 128 and rep_dim <= 64")
     for t in ("user", "ad"):
         if not 1 <= len(layout.tower_parts(t)) <= L.TOWER_MAX_PARTS:
             raise NotImplementedError(f"{t} tower needs 1..{L.TOWER_MAX_PARTS} input blocks")
-    if layout.mlp_input_width() > 128:
-        raise NotImplementedError(f"tower input layout width {layout.mlp_input_width()} > 128")
+    if geom.width > 128:
+        raise NotImplementedError(f"tower input layout width {geom.width} > 128")
+    return geom
 
 
 class DicmModel:
@@ -118,7 +151,7 @@ class DicmModel:
         not fit host memory."""
         layout = ModelLayout(schema, aggregator, tuple(mlp_widths), use_ad_image, use_behavior_images)
         S.validate_layout(layout, None if extractor is None else extractor.out_dim)
-        check_hot_path(layout)
+        self.geometry = check_hot_path(layout)
         self.schema = schema
         self.aggregator = aggregator
         self.extractor = extractor
@@ -161,7 +194,15 @@ class DicmModel:
         self.device = torch.device(device)
         self.specs = S.param_specs(layout)
         self.dense_names = S.dense_param_names(layout)
-        shapes = {n: shp for n, shp, _ in self.specs}
+        geom = self.geometry
+        # kernel shapes; the real tensor of each is kernel[rows][:, cols] (KernelGeometry)
+        shapes = {n: geom.specs[n][0] for n, _, _ in self.specs}
+        self.index_maps = {n: (None if geom.specs[n][1] is None else torch.as_tensor(geom.specs[n][1],
+                                                                                      device=self.device),
+                               None if geom.specs[n][2] is None else torch.as_tensor(geom.specs[n][2],
+                                                                                      device=self.device))
+                           for n, _, _ in self.specs}
+        real_shapes = {n: shp for n, shp, _ in self.specs}
         # fused dense buffer
         # the image group starts on a 256-B boundary so the kernels can use
         # 16-B vector loads on img/*/w; the gap is its own (always-zero) span
@@ -183,10 +224,12 @@ class DicmModel:
         for n in self.dense_names:
             o, size, shp = self.dense_offsets[n]
             view = self.dense[o:o + size].view(shp)
-            val = host[n] if n in host else S.init_param(seed, n, shp, kinds[n])
-            view.copy_(torch.as_tensor(np.asarray(val, dtype=np.float64), dtype=torch.float32))
-            self.params[n] = Parameter(n, view)
-        # ID tables (``table_rows`` lets a sharded model hold only its rows)
+            val = host[n] if n in host else S.init_param(seed, n, real_shapes[n], kinds[n])
+            rows, cols = self.index_maps[n]
+            write_real(view, rows, cols, np.asarray(val, dtype=np.float64))
+            self.params[n] = Parameter(n, view, rows, cols)
+        # ID tables (``table_rows`` lets a sharded model hold only its rows),
+        # kernel width 12 (a narrower d_id is zero-padded)
         self.tables = {}
         for f in schema.fields:
             n = f"id_emb/{f.name}"
@@ -197,9 +240,13 @@ class DicmModel:
             else:
                 t = torch.as_tensor(S.init_param(seed, n, (f.vocab, schema.d_id), "table"),
                                     dtype=torch.float32).to(self.device)
+            if t.shape[1] != S.KD:
+                padded = torch.zeros((t.shape[0], S.KD), dtype=torch.float32, device=self.device)
+                padded[:, :t.shape[1]] = t
+                t = padded
             self.tables[f.name] = t.contiguous()
-            self.params[n] = Parameter(n, self.tables[f.name])
-        self.head_offsets = layout.head_offsets()
+            self.params[n] = Parameter(n, self.tables[f.name], None, self.index_maps[n][1])
+        self.head_offsets = geom.head_offsets
 
     # -- reference bookkeeping (model.py:339-347)
     def worker_param_names(self):
@@ -215,8 +262,31 @@ class DicmModel:
         return self.layout.mlp_input_width()
 
     def dense_view(self, buf, name):
+        """The kernel-shaped view of one parameter's span of a fused buffer."""
         o, size, shp = self.dense_offsets[name]
         return buf[o:o + size].view(shp)
+
+    def real_view(self, buf, name):
+        """The real entries of one parameter's span (a copy when padded)."""
+        rows, cols = self.index_maps[name]
+        return real_of(self.dense_view(buf, name), rows, cols)
+
+    def write_real_view(self, buf, name, value):
+        rows, cols = self.index_maps[name]
+        write_real(self.dense_view(buf, name), rows, cols, value)
+
+    def real_mask(self):
+        """bool mask over the fused dense buffer: True on real entries (the
+        padded ones of a narrow model -- and the alignment gaps -- are False)."""
+        mask = torch.zeros(self.dense.shape, dtype=torch.bool, device=self.dense.device)
+        for n in self.dense_names:
+            write_real(self.dense_view(mask, n), *self.index_maps[n],
+                       np.ones(self.params[n].shape, dtype=bool))
+        return mask
+
+    def real_table(self, t):
+        """A kernel-width [V, 12] table (or table-shaped state) -> [V, d_id]."""
+        return t[:, :self.schema.d_id] if t.dim() == 2 and self.schema.d_id != t.shape[1] else t
 
     def group_range(self, prefix):
         """[start, end) of the contiguous fused-buffer range of a name group."""
@@ -253,7 +323,7 @@ class PrerankModel(DicmModel):
                  params=None, table_rows=None, shard=None, table_init="reference"):
         layout = S.prerank_layout(schema, tuple(user_fields), tuple(ad_fields), tower_hidden, rep_dim, use_images,
                                   None if extractor is None else extractor.out_dim)
-        check_hot_path(layout)
+        self.geometry = check_hot_path(layout)
         self.schema = schema
         self.extractor = extractor
         self.seed = seed

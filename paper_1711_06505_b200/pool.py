@@ -112,6 +112,12 @@ class ImagePool:
         lat = torch.randn((n_rows, latent_dim), generator=gen, dtype=torch.float32)
         return cls.from_latents(lat, ext, dtype, device, world, rank)
 
+    def padded(self, d_raw):
+        """A copy with zero columns up to ``d_raw`` (the kernels' row width)."""
+        rows = torch.zeros((self.rows.shape[0], d_raw), dtype=self.rows.dtype, device=self.rows.device)
+        rows[:, :self.d_raw] = self.rows
+        return ImagePool(rows, self.world, self.rank, self.global_size)
+
     def gather(self, ids):
         """Rows for local ids as fp32 on the device (dicm_pool_gather)."""
         ids = torch.as_tensor(np.asarray(ids, dtype=np.int32), device=self.rows.device)

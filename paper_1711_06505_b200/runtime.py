@@ -782,8 +782,9 @@ class Cluster:
         on rank r % G at local row r // G); collective: every rank calls it."""
         if self.world == 1:
             return local.cpu().numpy()[:vocab]
+        local = local.contiguous()
         parts = [torch.empty_like(local) for _ in range(self.world)]
-        dist.all_gather(parts, local.contiguous(), group=self.group)
+        dist.all_gather(parts, local, group=self.group)
         out = np.zeros((vocab,) + tuple(local.shape[1:]), dtype=local.cpu().numpy().dtype)
         for r in range(self.world):
             n = len(range(r, vocab, self.world))
@@ -796,7 +797,8 @@ class Cluster:
         Collective when G > 1."""
         out = {n: p.data for n, p in self.model.params.items() if not n.startswith("id_emb/")}
         for f in self.model.layout.schema.fields:
-            out[f"id_emb/{f.name}"] = self._assemble(self.model.tables[f.name], f.vocab).astype(np.float64)
+            out[f"id_emb/{f.name}"] = self._assemble(self.model.real_table(self.model.tables[f.name]),
+                                                     f.vocab).astype(np.float64)
         return out
 
     def collect_into_model(self):
@@ -819,13 +821,13 @@ class Cluster:
         t = e.t.cpu().numpy()
         out = {}
         for n in m.dense_names:
-            out[f"{n}#m"] = m.dense_view(e.m, n).double().cpu().numpy()
-            out[f"{n}#v"] = m.dense_view(e.v, n).double().cpu().numpy()
+            out[f"{n}#m"] = m.real_view(e.m, n).double().cpu().numpy()
+            out[f"{n}#v"] = m.real_view(e.v, n).double().cpu().numpy()
             out[f"{n}#t"] = np.array(int(t[e.span_index[n]]), dtype=np.int64)
         for f in m.layout.schema.fields:
             base = f"id_emb/{f.name}"
-            out[f"{base}#m"] = self._assemble(e.tm[f.name], f.vocab).astype(np.float64)
-            out[f"{base}#v"] = self._assemble(e.tv[f.name], f.vocab).astype(np.float64)
+            out[f"{base}#m"] = self._assemble(m.real_table(e.tm[f.name]), f.vocab).astype(np.float64)
+            out[f"{base}#v"] = self._assemble(m.real_table(e.tv[f.name]), f.vocab).astype(np.float64)
             out[f"{base}#t"] = self._assemble(e.tt[f.name], f.vocab).astype(np.int64)
         return out
 

@@ -317,3 +317,131 @@ def image_param_names(layout):
 def dense_param_names(layout):
     """Dense parameters in the order LocalTrainer steps them (training.py:53)."""
     return worker_param_names(layout) + image_param_names(layout)
+
+
+# ---------------------------------------------------------------------------
+# kernel geometry: the reference's widths embedded into the compiled ones
+# ---------------------------------------------------------------------------
+
+KD = 12                 # embedding block width of the kernels (d_id and d_img)
+KH1, KH2 = 256, 64      # image-net hidden widths
+KATT = 32               # attention hidden width
+KHEAD = (128, 64)       # head hidden widths
+KRAW = 256              # the pool row width is a multiple of this
+KMAX_WIDE = 16384       # widest head input (the GEMM head path)
+
+
+class KernelGeometry:
+    """How a layout's parameters embed into the kernels' compiled widths.
+
+    The kernels are compiled for the paper's widths (12-d embeddings, a
+    256/64 image net, 32 attention units, a 128/64 head).  A narrower model
+    (e.g. the reference's own test fixtures: d_id 3, d_img 4, d_raw 8,
+    attention 5, head (6, 4)) is trained by zero-padding every parameter into
+    those widths: padded weights, biases and PReLU slopes are 0, so padded
+    units output exactly 0 (PReLU(0) = 0), padded input columns meet zero
+    weights, every padded gradient is exactly 0 and Adam leaves padded entries
+    at 0 -- the real entries follow the reference bit for bit in f64 and to
+    fp32 rounding on the device.  The pool is padded with zero columns to a
+    multiple of 256.  ``specs`` maps every parameter name to (kernel shape,
+    row index, column index): the real tensor is
+    kernel[rows][:, cols]; None means the whole axis.
+    Wider models than the compiled widths raise NotImplementedError."""
+
+    def __init__(self, layout):
+        s = layout.schema
+        agg = layout.aggregator
+        self.layout = layout
+        problems = []
+        if s.d_id > KD or s.d_img > KD:
+            problems.append(f"d_id / d_img <= {KD} (got {s.d_id}, {s.d_img})")
+        if layout.h1 > KH1 or layout.h2 > KH2:
+            problems.append(f"image-net widths <= ({KH1}, {KH2}) (got {layout.h1}, {layout.h2})")
+        if layout.attentive and agg.attention_hidden > KATT:
+            problems.append(f"attention_hidden <= {KATT} (got {agg.attention_hidden})")
+        if layout.towers is None:
+            mw = tuple(layout.mlp_widths)
+            if len(mw) != 2 or mw[0] > KHEAD[0] or mw[1] > KHEAD[1]:
+                problems.append(f"two head layers of at most {KHEAD} units (got {mw})")
+        if problems:
+            raise NotImplementedError("kernels are compiled for " + "; ".join(problems))
+        self.d_raw = -(-s.d_raw // KRAW) * KRAW
+        self.identity = (s.d_id == KD and s.d_img == KD and s.d_raw == self.d_raw and layout.h1 == KH1
+                         and layout.h2 == KH2 and (not layout.attentive or agg.attention_hidden == KATT)
+                         and (layout.towers is not None or tuple(layout.mlp_widths) == KHEAD))
+        # head input: every block 12 wide
+        real, off, cols = layout.head_offsets(), 0, []
+        kern = {}
+        for f in s.fields:
+            kern["field/" + f.name] = off
+            cols += range(off, off + s.d_id)
+            off += KD
+        if layout.use_ad_image:
+            kern["ad_image_emb"] = off
+            cols += range(off, off + s.d_img)
+            off += KD
+        if layout.use_behavior_images:
+            kern["pool"] = off
+            nblk = {"multiquery-attn": 2, "concat": s.b_max}.get(agg.kind, 1)
+            for j in range(nblk):
+                cols += range(off + KD * j, off + KD * j + s.d_img)
+            off += KD * nblk
+        kern["width"] = off
+        assert len(cols) == real["width"]
+        self.head_offsets, self.width = kern, off
+        self.head_cols = np.asarray(cols, dtype=np.int64)
+        if self.width > KMAX_WIDE:
+            raise NotImplementedError(f"head input width {self.width} > {KMAX_WIDE}")
+        self.specs = self._specs()
+
+    def tower_parts(self, tower):
+        """(kernel head-input column, 12) blocks of one tower's input, in the
+        reference's hstack order (model.py:510-520)."""
+        kern, real = self.head_offsets, self.layout.head_offsets()
+        inv = {v: k for k, v in real.items() if k != "width"}
+        return [(kern[inv[col]], KD) for col, _w in self.layout.tower_parts(tower)]
+
+    def _specs(self):
+        lay, s, agg = self.layout, self.layout.schema, self.layout.aggregator
+        ar = lambda n: np.arange(n, dtype=np.int64)  # noqa: E731
+        out = {}
+
+        def lin(prefix, n_in, n_out, k_in, k_out, cols=None, alpha=True):
+            out[prefix + "w"] = ((k_out, k_in), ar(n_out) if n_out != k_out else None,
+                                 cols if cols is not None else (ar(n_in) if n_in != k_in else None))
+            out[prefix + "b"] = ((k_out,), ar(n_out) if n_out != k_out else None, None)
+            if alpha:
+                out[prefix + "a"] = ((k_out,), ar(n_out) if n_out != k_out else None, None)
+
+        for f in s.fields:
+            out[f"id_emb/{f.name}"] = ((f.vocab, KD), None, ar(s.d_id) if s.d_id != KD else None)
+        lin("img/0/", s.d_raw, lay.h1, self.d_raw, KH1)
+        lin("img/1/", lay.h1, lay.h2, KH1, KH2)
+        lin("img/2/", lay.h2, s.d_img, KH2, KD, alpha=False)
+        if lay.towers is not None:
+            tw = lay.towers
+            for t in ("user", "ad"):
+                parts = lay.tower_parts(t)
+                cols = np.concatenate([ar(w) + KD * j for j, (_c, w) in enumerate(parts)])
+                k_in = KD * len(parts)
+                lin(f"{t}_tower/0/", len(cols), tw.hidden, k_in, tw.hidden,
+                    cols=cols if len(cols) != k_in else None)
+                lin(f"{t}_tower/1/", tw.hidden, tw.rep, tw.hidden, tw.rep, alpha=False)
+            return out
+        if lay.attentive:
+            h = agg.attention_hidden
+            cols = np.concatenate([ar(s.d_img), KD + ar(s.d_img)])
+            lin("attn/img/0/", 2 * s.d_img, h, 2 * KD, KATT, cols=cols if len(cols) != 2 * KD else None)
+            lin("attn/img/1/", h, 1, KATT, 1, alpha=False)
+            if lay.multiquery:
+                nq = len(lay.query_fields_present())
+                cols = np.concatenate([KD * q + ar(s.d_id) for q in range(nq)] + [KD * nq + ar(s.d_img)])
+                lin("attn/id/0/", nq * s.d_id + s.d_img, h, KD * nq + KD, KATT,
+                    cols=cols if len(cols) != KD * (nq + 1) else None)
+                lin("attn/id/1/", h, 1, KATT, 1, alpha=False)
+        m0, m1 = lay.mlp_widths
+        lin("mlp/0/", lay.mlp_input_width(), m0, self.width, KHEAD[0],
+            cols=self.head_cols if len(self.head_cols) != self.width else None)
+        lin("mlp/1/", m0, m1, KHEAD[0], KHEAD[1])
+        lin("mlp/2/", m1, 1, KHEAD[1], 1, alpha=False)
+        return out

@@ -140,8 +140,8 @@ class LocalTrainer:
         t = e.t.cpu().numpy()
         out = {}
         for n in m.dense_names:
-            out[n] = AdamStateView(m.dense_view(e.m, n).double().cpu().numpy(),
-                                   m.dense_view(e.v, n).double().cpu().numpy(), int(t[e.span_index[n]]))
+            out[n] = AdamStateView(m.real_view(e.m, n).double().cpu().numpy(),
+                                   m.real_view(e.v, n).double().cpu().numpy(), int(t[e.span_index[n]]))
         return out
 
     def set_adam_state(self, name, m=None, v=None, t=None):
@@ -156,7 +156,9 @@ class LocalTrainer:
     @property
     def table_state(self):
         e = self.engine
-        return {f: AdamStateView(e.tm[f].double().cpu().numpy(), e.tv[f].double().cpu().numpy(),
+        m = self.model
+        return {f: AdamStateView(m.real_table(e.tm[f]).double().cpu().numpy(),
+                                 m.real_table(e.tv[f]).double().cpu().numpy(),
                                  e.tt[f].cpu().numpy().astype(np.int64)) for f in e.tm}
 
 
@@ -168,16 +170,16 @@ def set_adam_state(engine, model, name, m=None, v=None, t=None):
     if name.startswith("id_emb/"):
         f = name.split("/", 1)[1]
         if m is not None:
-            engine.tm[f].copy_(torch.as_tensor(np.asarray(m), dtype=torch.float32))
+            model.real_table(engine.tm[f]).copy_(torch.as_tensor(np.asarray(m), dtype=torch.float32))
         if v is not None:
-            engine.tv[f].copy_(torch.as_tensor(np.asarray(v), dtype=torch.float32))
+            model.real_table(engine.tv[f]).copy_(torch.as_tensor(np.asarray(v), dtype=torch.float32))
         if t is not None:
             engine.tt[f].copy_(torch.as_tensor(np.asarray(t), dtype=torch.int32))
         return
     if m is not None:
-        model.dense_view(engine.m, name).copy_(torch.as_tensor(np.asarray(m), dtype=torch.float32))
+        model.write_real_view(engine.m, name, m)
     if v is not None:
-        model.dense_view(engine.v, name).copy_(torch.as_tensor(np.asarray(v), dtype=torch.float32))
+        model.write_real_view(engine.v, name, v)
     if t is not None:
         engine.t[engine.span_index[name]] = int(np.asarray(t))
 

@@ -28,13 +28,13 @@ def device_model(m, pool_rows, pool_dtype="fp32", params=None):
 
 def dense_grads(engine):
     m = engine.model
-    return {n: m.dense_view(engine.grad, n).double().cpu().numpy() for n in m.dense_names}
+    return {n: m.real_view(engine.grad, n).double().cpu().numpy() for n in m.dense_names}
 
 
 def table_grads(engine):
     """{field: (ids, rows)} from the deduplicated row gradients."""
     keys = engine.unique_rows().astype(np.int64)
-    rows = engine.d_rows[:len(keys)].double().cpu().numpy()
+    rows = engine.d_rows[:len(keys), :engine.model.schema.d_id].double().cpu().numpy()
     out = {}
     for i, f in enumerate(engine.fields):
         lo = engine.bases[i]

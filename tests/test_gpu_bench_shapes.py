@@ -234,7 +234,7 @@ def test_cfg2_full_step_matches_oracle():
     og, _ = O.image_mlp_bwd_from(params, saved(e.net.act0, cap, 256, "bf16")[:U].double().cpu().numpy(),
                                  saved(e.net.act1, cap, 64, "bf16")[:U].double().cpu().numpy(),
                                  e.d_emb[:U].double().cpu().numpy(), rows_of, out["uniq"])
-    r3 = {n: relmax(model.dense_view(e.grad, n).double().cpu().numpy(), og[n]) for n in og}
+    r3 = {n: relmax(model.real_view(e.grad, n).double().cpu().numpy(), og[n]) for n in og}
     print("cfg2 bf16 image-MLP backward:", {k: f"{v:.1e}" for k, v in r3.items()})
     assert all(v < 2e-2 for v in r3.values()), r3
     # 4. the fp32 engine on the same (bf16-valued) rows vs the pure oracle

@@ -45,8 +45,11 @@ def _engine(name, precision="fp32", pool_dtype="fp32"):
     return fx, m, model, tr
 
 
-@pytest.mark.parametrize("name", G.FULL)
+@pytest.mark.parametrize("name", G.TINY + G.FULL)
 def test_step0_forward_backward_matches_reference(name):
+    """Every reference-produced fixture, the reference's own narrow test
+    models (tiny_*: d_id 3, d_img 4, d_raw 8, attention 5, head (6, 4),
+    zero-padded into the compiled widths, schema.KernelGeometry) included."""
     from paper_1711_06505_b200.batch import encode_batch
     fx, m, model, tr = _engine(name)
     e = tr.engine
@@ -59,8 +62,10 @@ def test_step0_forward_backward_matches_reference(name):
     U = len(fx["s0/unique_images"])
     assert O.rel_err(loss.item(), fx["s0/loss"]) < FP32_TOL
     assert O.rel_err(e.logits[:batch.size].cpu().numpy(), fx["s0/logits"]) < FP32_TOL
-    assert O.rel_err(e.emb[:U].cpu().numpy(), fx["s0/E"]) < FP32_TOL
-    assert O.rel_err(e.d_emb[:U].cpu().numpy(), fx["s0/dE"]) < FP32_TOL
+    d = m["d_img"]
+    assert O.rel_err(e.emb[:U, :d].cpu().numpy(), fx["s0/E"]) < FP32_TOL
+    assert O.rel_err(e.d_emb[:U, :d].cpu().numpy(), fx["s0/dE"]) < FP32_TOL
+    assert not e.emb[:U, d:].any() and not e.d_emb[:U, d:].any()  # padded columns stay exactly 0
     for n, g in H.dense_grads(e).items():
         for exp, got in G.golden_view(fx, f"s0/grad/{n}", g):
             assert O.rel_err(got, exp) < FP32_TOL, n
@@ -69,7 +74,7 @@ def test_step0_forward_backward_matches_reference(name):
         assert O.rel_err(rows, fx[f"s0/tgrad/{f}/rows"]) < FP32_TOL, f
 
 
-@pytest.mark.parametrize("name", G.FULL)
+@pytest.mark.parametrize("name", G.TINY + G.FULL)
 def test_two_train_steps_match_reference(name):
     fx, m, model, tr = _engine(name)
     losses = [tr.train_batch(G.samples(fx, b)) for b in (0, 1)]
@@ -404,3 +409,21 @@ def test_train_stream_matches_step_by_step(graphs):
     sa, sb = model_a.snapshot(), model_b.snapshot()
     for n in sa:
         assert np.array_equal(sa[n], sb[n]), n
+
+
+@pytest.mark.parametrize("name", ["tiny_multiquery-attn", "tiny_concat", "tiny_prerank"])
+def test_narrow_model_padding_stays_zero(name):
+    """A narrow model trained in the compiled widths (schema.KernelGeometry):
+    after several steps every padded parameter entry, its gradient and its
+    Adam moments are still exactly 0, and so are the padded embedding
+    columns."""
+    fx, m, model, tr = _engine(name)
+    for b in (0, 1, 0, 1):
+        tr.train_batch(G.samples(fx, b))
+    e = tr.engine
+    mask = model.real_mask()
+    for buf in (model.dense, e.grad, e.m, e.v):
+        assert not buf[~mask].any()
+    d = model.schema.d_id
+    for f in model.tables:
+        assert not model.tables[f][:, d:].any() and not e.tm[f][:, d:].any() and not e.tv[f][:, d:].any(), f

@@ -195,3 +195,41 @@ def test_packed_fill_matches_column_copies():
     ref[pk.beh_off:pk.beh_off + pk.B + 1] = b.beh_off
     ref[pk.labels:pk.labels + pk.B] = np.asarray(b.labels, np.float32).view(np.int32)
     assert np.array_equal(host, ref)
+
+
+def test_narrow_models_embed_into_the_kernel_widths():
+    """schema.KernelGeometry: the reference's own narrow test model (d_id 3,
+    d_img 4, d_raw 8, attention 5, head (6, 4); reference tests/conftest.py:9-34)
+    is stored zero-padded in the compiled widths; the real entries are the
+    reference init, every padded entry is 0, and copy_/data round-trip."""
+    import torch
+    from paper_1711_06505_b200.model import DicmModel
+    from paper_1711_06505_b200 import schema as S
+    sch = S.FeatureSchema(fields=[S.FieldSpec("user", 5), S.FieldSpec("ad", 7)], d_id=3, d_raw=8, d_img=4,
+                          b_max=4, query_fields=("ad",))
+    for kind in ("sum", "attn", "multiquery-attn", "max", "concat"):
+        m = DicmModel(sch, S.AggregatorSpec(kind, attention_hidden=5), None, seed=1, mlp_widths=(6, 4),
+                      device="cpu")
+        lay = m.layout
+        ref = S.init_params(lay, 1)
+        assert m.geometry.d_raw == 256 and not m.geometry.identity
+        for n, a in ref.items():
+            p = m.params[n]
+            assert p.shape == a.shape, n
+            assert np.array_equal(p.data, a.astype(np.float32).astype(np.float64)), n
+        # everything outside the real entries is zero
+        mask = m.real_mask()
+        assert not m.dense[~mask].any(), kind
+        assert int(mask.sum()) == sum(a.size for n, a in ref.items() if not n.startswith("id_emb/"))
+        for f in sch.fields:
+            assert m.tables[f.name].shape == (f.vocab, 12) and not m.tables[f.name][:, 3:].any()
+        # copy_ writes the real entries only; real_view reads the fused span
+        w = m.params["mlp/0/w"]
+        v = np.arange(np.prod(w.shape), dtype=np.float64).reshape(w.shape)
+        w.copy_(v)
+        assert np.array_equal(w.data, v)
+        assert np.array_equal(m.real_view(m.dense, "mlp/0/w").double().numpy(), v)
+        assert int((m.dense_view(m.dense, "mlp/0/w") != 0).sum()) == np.count_nonzero(v)
+    with pytest.raises(NotImplementedError, match="compiled"):
+        DicmModel(S.FeatureSchema(fields=[S.FieldSpec("user", 5)], d_id=16), S.AggregatorSpec("sum"), None,
+                  device="cpu")
