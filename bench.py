@@ -508,8 +508,13 @@ def main():
         s2, e2_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s2.record()
         t_cpu = time.perf_counter()
-        for i, loss in enumerate(cluster.train_stream(host)):
-            pinned_loss[i:i + 1].copy_(loss, non_blocking=True)
+        if os.environ.get("DICM_E2E_API", "stream") == "stream":
+            for i, loss in enumerate(cluster.train_stream(host)):
+                pinned_loss[i:i + 1].copy_(loss, non_blocking=True)
+        else:  # one call per iteration, host side of step i+1 after step i is enqueued
+            for i, b in enumerate(host):
+                loss = cluster.train_batch_async(b, union)
+                pinned_loss[i:i + 1].copy_(loss, non_blocking=True)
         t_cpu = time.perf_counter() - t_cpu
         e2_.record()
         barrier()

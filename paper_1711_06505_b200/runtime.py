@@ -501,23 +501,37 @@ class ClusterEngine(StepEngine):
             if side is not None:
                 main_stream.wait_stream(side)
 
-        self._dedup_images()
-        self._dedup_ids()
-
-        def transposes(ss):  # the backward's summation order: needed only at the local step
-            saved, self.s = self.s, ss
-            self._transpose_images()
-            self._transpose_ids()
-            self.s = saved
-
-        on_side(transposes)
         cnt = self.counts
+
+        def swap(fn):  # run an engine phase (which launches on self.s) on stream ss
+            def run(ss):
+                saved, self.s = self.s, ss
+                try:
+                    fn(ss)
+                finally:
+                    self.s = saved
+            return run
+
+        def id_chain(ss):  # ID keys: dedup, bucket by owner, the backward's transpose
+            self._dedup_ids()
+            L.check(L.lib.dicm_bucket_by_owner(self.uniq_id.data_ptr(), cnt[1:].data_ptr(), self.cap_k, G,
+                                               self.send_id.data_ptr(), self._col(1), self.perm_id.data_ptr(),
+                                               self.ws_bucket_id.data_ptr(), self.ws_bucket_id.numel(), ss))
+
+        # the ID chain beside the image chain; the counts wait for both buckets
+        on_side(swap(id_chain))
+        id_bucketed = None
+        if side is not None:
+            id_bucketed = torch.cuda.Event()
+            id_bucketed.record(side)
+        self._dedup_images()
         L.check(L.lib.dicm_bucket_by_owner(self.uniq_img.data_ptr(), cnt.data_ptr(), self.cap_u, G,
                                            self.send_img.data_ptr(), self._col(0), self.perm_img.data_ptr(),
                                            self.ws_bucket.data_ptr(), self.ws_bucket.numel(), s))
-        L.check(L.lib.dicm_bucket_by_owner(self.uniq_id.data_ptr(), cnt[1:].data_ptr(), self.cap_k, G,
-                                           self.send_id.data_ptr(), self._col(1), self.perm_id.data_ptr(),
-                                           self.ws_bucket_id.data_ptr(), self.ws_bucket_id.numel(), s))
+        # the backward's summation order, needed only at the local step (joined before it)
+        on_side(swap(lambda ss: (self._transpose_ids(), self._transpose_images())))
+        if id_bucketed is not None:
+            main_stream.wait_event(id_bucketed)
         self._mark("dedup+bucket")
         # (2) counts -> every peer, then the request keys (C1, C3)
         px.counts(self._col(0), s)
