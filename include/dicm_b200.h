@@ -223,6 +223,15 @@ int dicm_sample_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv,
                     const dicm_attn_params_t* attn /* [2]: img, id */, float* head_in,
                     float* scores /* [2, R] */, float* stats /* [2, B, 2] */,
                     dicm_stream_t stream);
+/* dicm_sample_fwd in two parts that may run on different streams: the ID-field
+ * columns of the head input (needs only the compact ID rows) and the image
+ * columns (ad image, pooled behaviors; needs the embeddings and, for
+ * multiquery-attn, the ID rows of the query fields). */
+int dicm_fields_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, float* head_in,
+                    dicm_stream_t stream);
+int dicm_images_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv,
+                    const dicm_attn_params_t* attn, float* head_in, float* scores, float* stats,
+                    dicm_stream_t stream);
 /* Stream-ordered on `stream`.  Writes every row d_emb[0..U) and
  * d_rows[0..K) (no zeroing needed); the scratch buffers of the batch view are
  * overwritten.  d_rows = NULL leaves the ID rows to dicm_id_row_grads, which

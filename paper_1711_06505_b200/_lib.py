@@ -149,6 +149,8 @@ _sig("dicm_ref_transpose_workspace", S, I64, I64)
 _sig("dicm_ref_transpose", C.c_int, P, I64, I64, P, S, P, P, ST)
 _sig("dicm_csr_segments", C.c_int, P, C.c_int, P, ST)
 _sig("dicm_id_row_grads", C.c_int, C.POINTER(Layout), C.POINTER(BatchView), P, P, ST)
+_sig("dicm_fields_fwd", C.c_int, C.POINTER(Layout), C.POINTER(BatchView), P, ST)
+_sig("dicm_images_fwd", C.c_int, C.POINTER(Layout), C.POINTER(BatchView), C.POINTER(AttnParams), P, P, P, ST)
 _sig("dicm_p2p_allreduce", C.c_int, C.POINTER(Peers), P, I64, I64, I64, I64, P, P, ST)
 _sig("dicm_table_init", C.c_int, P, I64, C.c_int, C.c_int, C.c_int, I64, C.c_uint64, C.c_float, ST)
 _sig("dicm_sample_blocks", C.c_int, C.c_int)
@@ -217,7 +219,7 @@ EXPORTED = [
     "dicm_owner_reduce_rows12", "dicm_probe_enable", "dicm_probe_read",
     "dicm_p2p_alloc", "dicm_p2p_free", "dicm_ipc_handle", "dicm_ipc_open", "dicm_ipc_close", "dicm_p2p_barrier",
     "dicm_p2p_counts", "dicm_p2p_plan", "dicm_p2p_scatter", "dicm_dedup_devn", "dicm_head_fwd",
-    "dicm_ref_transpose_workspace", "dicm_ref_transpose", "dicm_csr_segments", "dicm_table_init", "dicm_id_row_grads", "dicm_p2p_allreduce", "dicm_jsonl_parse", "dicm_jsonl_list_total", "dicm_jsonl_export", "dicm_jsonl_free",
+    "dicm_ref_transpose_workspace", "dicm_ref_transpose", "dicm_csr_segments", "dicm_table_init", "dicm_id_row_grads", "dicm_p2p_allreduce", "dicm_fields_fwd", "dicm_images_fwd", "dicm_jsonl_parse", "dicm_jsonl_list_total", "dicm_jsonl_export", "dicm_jsonl_free",
     "dicm_towers_blocks", "dicm_towers_fwd_bwd", "dicm_towers_fwd", "dicm_head_wide_workspace",
     "dicm_head_wide_fwd_bwd", "dicm_head_wide_fwd", "dicm_host_pack", "dicm_zero_async",
 ]

@@ -282,21 +282,28 @@ __device__ void attn_fwd(const Args& a, const AttnSmem& s, int ch, int b, int la
     if (lane == c) dst[c] = out[c];
 }
 
-template <int MINB>  // resident blocks per SM the register budget is cut for (DICM_FWD_OCC, default 2)
+// PART: 0 = the whole head input; 1 = the ID-field columns only; 2 = the
+// image columns only (ad image, pooled behaviors).  The step runs part 1 on a
+// forked stream as soon as the compact ID rows exist (beside the image-MLP
+// forward) and part 2 on the main stream, each with only its own registers.
+template <int MINB, int PART, int KIND = -1>  // MINB: resident blocks per SM the register budget is cut for;
+                                             // KIND >= 0: only that aggregator's code (PART 2)
 __global__ void __launch_bounds__(FWD_WARPS * 32, MINB) k_sample_fwd(const __grid_constant__ Args a) {
-  __shared__ AttnSmem sa[2];
+  __shared__ AttnSmem sa[PART == 1 ? 1 : 2];
   __shared__ __align__(16) float Pw[FWD_WARPS][DICM_ATT];  // per-warp query projection
-  const bool att = a.L.use_behavior_images && (a.L.kind == 1 || a.L.kind == 2);
-  if (att) {
-    load_attn(sa[0], a.A[0], DICM_D);
-    if (a.L.kind == 2) load_attn(sa[1], a.A[1], DICM_D * a.L.n_query);
+  const bool att = PART != 1 && a.L.use_behavior_images && (a.L.kind == 1 || a.L.kind == 2);
+  if constexpr (PART != 1) {
+    if (att) {
+      load_attn(sa[0], a.A[0], DICM_D);
+      if (a.L.kind == 2) load_attn(sa[1], a.A[1], DICM_D * a.L.n_query);
+    }
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int b = blockIdx.x * FWD_WARPS + warp; b < a.V.batch; b += gridDim.x * FWD_WARPS) {
     float* row = a.head_in + (int64_t)b * a.L.width;
     // ID fields: one-hot rows and multi-hot sums
-    for (int f = 0; f < a.L.n_fields; ++f) {
+    for (int f = 0; PART != 2 && f < a.L.n_fields; ++f) {
       const float* T = a.V.tables[f];
       if (!a.L.field_multi[f]) {
         if (lane < DICM_D) row[a.L.field_col[f] + lane] = __ldg(T + (int64_t)a.V.field_inv[f][b] * DICM_D + lane);
@@ -313,10 +320,12 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, MINB) k_sample_fwd(const __gri
           if (lane == c) row[a.L.field_col[f] + c] = acc[c];
       }
     }
+    if constexpr (PART == 1) continue;
     if (a.L.use_ad_image && lane < DICM_D)
       row[a.L.ad_col + lane] = __ldg(a.V.emb + (int64_t)a.V.ad_local[b] * DICM_D + lane);
     if (!a.L.use_behavior_images) continue;
-    if (a.L.kind == 4) {  // concat (reference scatter_concat, autograd.py:370-385): slot j = j-th kept behavior
+    const int kind = KIND >= 0 ? KIND : a.L.kind;
+    if (kind == 4) {  // concat (reference scatter_concat, autograd.py:370-385): slot j = j-th kept behavior
       const int64_t i0 = a.V.beh_off[b];
       const int len = (int)(a.V.beh_off[b + 1] - i0);
       const int n = a.L.width - a.L.pool_col;  // capacity * 12
@@ -327,7 +336,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, MINB) k_sample_fwd(const __gri
       }
       continue;
     }
-    if (a.L.kind == 3) {  // max pooling (reference segment_max, autograd.py:289-319)
+    if (kind == 3) {  // max pooling (reference segment_max, autograd.py:289-319)
       float m[DICM_D];
       int am[DICM_D];
       seg_max(a, b, lane, m, am);
@@ -336,7 +345,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, MINB) k_sample_fwd(const __gri
         if (lane == c) row[a.L.pool_col + c] = am[c] < 0 ? 0.f : m[c];  // empty segment -> 0
       continue;
     }
-    if (a.L.kind == 0) {
+    if (kind == 0) {
       float acc[DICM_D];
 #pragma unroll
       for (int c = 0; c < DICM_D; ++c) acc[c] = 0.f;
@@ -347,12 +356,14 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, MINB) k_sample_fwd(const __gri
       for (int c = 0; c < DICM_D; ++c)
         if (lane == c) row[a.L.pool_col + c] = acc[c];
     } else {
-      attn_fwd<DICM_D>(a, sa[0], 0, b, lane, Pw[warp]);
-      if (a.L.kind == 2) {
-        if (a.L.n_query == 2)
-          attn_fwd<2 * DICM_D>(a, sa[1], 1, b, lane, Pw[warp]);
-        else
-          attn_fwd<DICM_D>(a, sa[1], 1, b, lane, Pw[warp]);
+      if constexpr (PART != 1) {
+        attn_fwd<DICM_D>(a, sa[0], 0, b, lane, Pw[warp]);
+        if (kind == 2) {
+          if (a.L.n_query == 2)
+            attn_fwd<2 * DICM_D>(a, sa[1], 1, b, lane, Pw[warp]);
+          else
+            attn_fwd<DICM_D>(a, sa[1], 1, b, lane, Pw[warp]);
+        }
       }
     }
   }
@@ -818,8 +829,9 @@ int64_t dicm_attn_partial_size(const dicm_layout_t* layout) { return part_size(l
 
 int dicm_sample_blocks(int batch) { return bwd_grid(batch); }
 
-int dicm_sample_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const dicm_attn_params_t* attn,
-                    float* head_in, float* scores, float* stats, dicm_stream_t stream) {
+static int sample_fwd_part(int part, const dicm_layout_t* layout, const dicm_batch_view_t* bv,
+                           const dicm_attn_params_t* attn, float* head_in, float* scores, float* stats,
+                           dicm_stream_t stream) {
   int rc = validate(layout, bv);
   if (rc) return rc;
   if (bv->batch == 0) return DICM_OK;
@@ -828,21 +840,47 @@ int dicm_sample_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
   a.scores = scores;
   a.stats = stats;
   const int grid = (bv->batch + FWD_WARPS - 1) / FWD_WARPS;
-  {
-    const int probe_slot = probe_begin(DICM_PROBE_SAMPLE_FWD, (cudaStream_t)stream);
-    // 2 blocks/SM at 128 registers; DICM_FWD_OCC=3 cuts the budget to 80
-    // registers (spills): 0.127 vs 0.086 ms at cfg2, A/B on one box (r2c)
-    static const int occ = [] {
-      const char* e = getenv("DICM_FWD_OCC");
-      return e && e[0] == '3' ? 3 : 2;
-    }();
-    if (occ == 2)
-      k_sample_fwd<2><<<grid, FWD_WARPS * 32, 0, (cudaStream_t)stream>>>(a);
-    else
-      k_sample_fwd<3><<<grid, FWD_WARPS * 32, 0, (cudaStream_t)stream>>>(a);
-    probe_end(probe_slot, (cudaStream_t)stream);
-  }
+  cudaStream_t st = (cudaStream_t)stream;
+  // 2 blocks/SM at 128 registers; DICM_FWD_OCC=3 cuts the budget to 80
+  // registers (spills in the whole-input variant: 0.127 vs 0.086 ms at cfg2, r2c)
+  static const int occ = [] {
+    const char* e = getenv("DICM_FWD_OCC");
+    return e && e[0] == '3' ? 3 : 2;
+  }();
+  static const int occ_attn = [] {
+    const char* e = getenv("DICM_FWD_OCC");
+    return e && e[0] == '2' ? 2 : 3;
+  }();
+  const int probe_slot = part == 1 ? -1 : probe_begin(DICM_PROBE_SAMPLE_FWD, st);
+  if (part == 1)
+    k_sample_fwd<3, 1><<<grid, FWD_WARPS * 32, 0, st>>>(a);
+  else if (part == 2 && layout->kind == 1 && occ_attn == 3)  // single-head attention alone: 80 registers, no spills
+    k_sample_fwd<3, 2, 1><<<grid, FWD_WARPS * 32, 0, st>>>(a);
+  else if (part == 2 && layout->kind == 1)
+    k_sample_fwd<2, 2, 1><<<grid, FWD_WARPS * 32, 0, st>>>(a);
+  else if (part == 2)
+    k_sample_fwd<2, 2><<<grid, FWD_WARPS * 32, 0, st>>>(a);
+  else if (occ == 3)
+    k_sample_fwd<3, 0><<<grid, FWD_WARPS * 32, 0, st>>>(a);
+  else
+    k_sample_fwd<2, 0><<<grid, FWD_WARPS * 32, 0, st>>>(a);
+  probe_end(probe_slot, st);
   return last_launch("dicm_sample_fwd");
+}
+
+int dicm_sample_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const dicm_attn_params_t* attn,
+                    float* head_in, float* scores, float* stats, dicm_stream_t stream) {
+  return sample_fwd_part(0, layout, bv, attn, head_in, scores, stats, stream);
+}
+
+int dicm_fields_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, float* head_in,
+                    dicm_stream_t stream) {
+  return sample_fwd_part(1, layout, bv, nullptr, head_in, nullptr, nullptr, stream);
+}
+
+int dicm_images_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const dicm_attn_params_t* attn,
+                    float* head_in, float* scores, float* stats, dicm_stream_t stream) {
+  return sample_fwd_part(2, layout, bv, attn, head_in, scores, stats, stream);
 }
 
 // the reference lists of the image rows and the ID rows (see RefSeg)

@@ -690,17 +690,20 @@ class StepEngine:
                 L.check(L.lib.dicm_csr_segments(self._dptr(o), pk.B, self.id_seg.data_ptr() + 4 * self.inv_id_off[f.name],
                                                 self.s))
 
-    def _local_step(self, emb, d_emb, denom, reduce=True, id_rows=True):
+    def _local_step(self, emb, d_emb, denom, reduce=True, id_rows=True, fwd=True):
         """a6-a12 forward and backward on the local batch: pooling, head, BCE.
         Reads image embeddings ``emb`` and compact ID rows ``self.id_rows``;
         writes ``d_emb`` / ``self.d_rows`` (``id_rows=False``: left to
-        ``_id_row_grads``) and the head/attention gradients."""
+        ``_id_row_grads``) and the head/attention gradients.  ``fwd=False``:
+        the head input was already built (``self._bv``, split forward)."""
         pk, s = self.pk, self.s
         B = pk.B
         st = self.status.data_ptr()
-        bv = self._bv = self._batch_view(emb)
-        L.check(L.lib.dicm_sample_fwd(C.byref(self.layout), C.byref(bv), self.attn, self.head_in.data_ptr(),
-                                      self.scores.data_ptr(), self.stats.data_ptr(), s))
+        if fwd:
+            bv = self._bv = self._batch_view(emb)
+            L.check(L.lib.dicm_sample_fwd(C.byref(self.layout), C.byref(bv), self.attn, self.head_in.data_ptr(),
+                                          self.scores.data_ptr(), self.stats.data_ptr(), s))
+        bv = self._bv
         self._head_fwd_bwd(B, denom)
         nhb = self._head_blocks(B)
         L.check(L.lib.dicm_loss_finalize(self.loss_part.data_ptr(), nhb, 1.0 / denom, self.loss.data_ptr(), st, s))
@@ -746,15 +749,21 @@ class StepEngine:
         denom = float(db.pk.B if denominator is None else denominator)
         side = self._side_stream()
         if side is not None:
-            # the ID chain (dedup over every field -> compact rows) shares no
-            # buffer with the image chain; it runs on a forked stream and joins
-            # before the per-sample kernels (a graph branch once captured)
+            # the ID chain (dedup over every field -> compact rows -> the ID
+            # columns of the head input -> its transpose) shares no buffer
+            # with the image chain; it runs on a forked stream (a graph branch
+            # once captured) and joins before the head
             main = self.s
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):
                 self.s = side.cuda_stream
                 self._dedup_ids()
                 self._gather_id_rows()
+                ids_ready = torch.cuda.Event()
+                ids_ready.record(side)
+                self._bv = self._batch_view(self.net.emb)
+                L.check(L.lib.dicm_fields_fwd(C.byref(self.layout), C.byref(self._bv), self.head_in.data_ptr(),
+                                              self.s))
                 self._transpose_ids()
             self.s = main
             self._dedup_images()
@@ -764,18 +773,23 @@ class StepEngine:
                 self.s = side.cuda_stream
                 self._transpose_images()
             self.s = main
+            if self.n_img_segs:
+                self._image_forward(self.net, self.uniq_img, self.counts.data_ptr())
+            if self.model.layout.multiquery:  # the ID query rows of the second channel
+                torch.cuda.current_stream().wait_event(ids_ready)
+            L.check(L.lib.dicm_images_fwd(C.byref(self.layout), C.byref(self._bv), self.attn, self.head_in.data_ptr(),
+                                          self.scores.data_ptr(), self.stats.data_ptr(), self.s))
+            torch.cuda.current_stream().wait_stream(side)
+            self._local_step(self.net.emb, self.net.d_emb, denom, reduce=False, id_rows=False, fwd=False)
         else:
             self._dedup_images()
             self._dedup_ids()
             self._transpose_images()
             self._transpose_ids()
-        if self.n_img_segs:
-            self._image_forward(self.net, self.uniq_img, self.counts.data_ptr())
-        if side is not None:
-            torch.cuda.current_stream().wait_stream(side)
-        else:
+            if self.n_img_segs:
+                self._image_forward(self.net, self.uniq_img, self.counts.data_ptr())
             self._gather_id_rows()
-        self._local_step(self.net.emb, self.net.d_emb, denom, reduce=side is None, id_rows=side is None)
+            self._local_step(self.net.emb, self.net.d_emb, denom)
         if side is not None:  # the ID-row gradients and the partial reduces overlap the image-MLP backward
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):
