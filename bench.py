@@ -12,9 +12,9 @@ Workload (BASELINE.json configs):
 A step = one full training iteration (dedup, image MLP fwd/bwd, pooling,
 head, BCE, backward, Adam on every dense parameter and every touched ID row)
 over one batch of synthetic data.  ``value`` times K steps with the inputs
-already in HBM; ``e2e`` times the public API (Cluster.train_stream on
-a host Batch: host packing, H2D of the packed batch + D2H of the loss inside
-the region; Cluster.train_stream overlaps the host side of step i+1 with step i).
+already in HBM; ``e2e`` times the public API (Cluster.train_batch_async on
+host Batches: host packing, H2D of the packed batch + D2H of the loss inside
+the region; the host side of step i+1 overlaps step i).
 """
 
 from __future__ import annotations
@@ -508,7 +508,10 @@ def main():
         s2, e2_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s2.record()
         t_cpu = time.perf_counter()
-        if os.environ.get("DICM_E2E_API", "stream") == "stream":
+        # default: one call per iteration (the host packs step i+1 while the
+        # device runs step i; measured 0.98 x value at cfg2); train_stream
+        # (worker-thread packing) contends for the GIL and measured 0.85 (r2e)
+        if os.environ.get("DICM_E2E_API", "batch") == "stream":
             for i, loss in enumerate(cluster.train_stream(host)):
                 pinned_loss[i:i + 1].copy_(loss, non_blocking=True)
         else:  # one call per iteration, host side of step i+1 after step i is enqueued
@@ -529,8 +532,10 @@ def main():
         ems = float(te.item())
         e2e = {"value": union * len(host) / (ems / 1000.0), "unit": "samples/s",
                "h2d_bytes_per_step": int(np.mean([eng.h2d_bytes(b) for b in host])), "d2h_bytes_per_step": 4,
-               "api": "Cluster.train_stream (host CSR union batch -> worker-thread slice + pack into pinned memory "
-                      "-> H2D on a copy stream -> step -> loss D2H into pinned memory)"}
+               "api": "Cluster.train_batch_async per iteration (host CSR batch -> multithreaded pack into pinned "
+                      "memory -> H2D on a copy stream, overlapping the previous step -> step -> loss D2H into "
+                      "pinned memory)" if os.environ.get("DICM_E2E_API", "batch") != "stream" else
+                      "Cluster.train_stream (worker-thread slice + pack, H2D on a copy stream, loss D2H)"}
 
     # roofline: per-kernel algorithmic bytes / flops over the
     # kernel times the library's own event probe measured on its stream

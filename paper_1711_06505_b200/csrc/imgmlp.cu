@@ -268,9 +268,12 @@ int check_aligned(const void* a, const void* b, const void* c, const void* d) {
 }
 
 int check_shapes(int d_raw, int64_t rows_max) {
-  if (d_raw % 64 != 0 || d_raw / 16 != H1)
+  // the hidden widths are compiled (256 -> 64 -> 12); the row width is any
+  // multiple of 64 (narrower image nets are zero-padded into these widths,
+  // schema.KernelGeometry; the tensor-core paths need a multiple of 256)
+  if (d_raw % 64 != 0 || d_raw < 64 || d_raw > (1 << 16))
     return fail(DICM_ERR_UNSUPPORTED,
-                "image MLP: kernels are built for d_raw=4096 (4096->256->64->12), got d_raw=%d", d_raw);
+                "image MLP: d_raw must be a multiple of 64 in [64, 65536] (256 -> 64 -> 12 hidden), got %d", d_raw);
   if (rows_max < 0 || rows_max > (int64_t)1 << 30) return fail(DICM_ERR_VALUE, "image MLP: rows_max out of range");
   return DICM_OK;
 }
