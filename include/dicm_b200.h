@@ -144,9 +144,10 @@ int dicm_imgmlp_bwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
  * Backward: the same graph reversed (segment_softmax bwd autograd.py:334-337,
  *   col_scale bwd 348-350); embedding and ID-row gradients are summed into
  *   the deduplicated row buffers (np.add.at, autograd.py:267-271) WITHOUT
- *   float atomics: every unique key sums its references in ascending
- *   reference order (the dedup inverse transposed by dicm_ref_transpose), so
- *   a step is bit-reproducible like the reference's (runtime.py:16-21);
+ *   float atomics: every unique key sums its references (grouped by
+ *   dicm_ref_transpose) exactly in 64-bit fixed point, which does not depend
+ *   on their order, so a step is bit-reproducible like the reference's
+ *   (runtime.py:16-21);
  *   attention-parameter gradients are written as per-block partial sums.
  * ---------------------------------------------------------------------- */
 typedef struct {
@@ -195,10 +196,12 @@ typedef struct {
 } dicm_batch_view_t;
 
 /* Transpose of a dedup inverse (inv[p] = key of reference p, keys < key_cap):
- * order[] = 0..n-1 stably sorted by key, start[k] = first slot of key k,
- * start[last key + 1] = n.  Stream-ordered; ws of dicm_ref_transpose_workspace
- * bytes.  Replaces nothing in the reference: it fixes the summation order of
- * np.add.at (autograd.py:267-271) on the device. */
+ * order[] = 0..n-1 grouped by key (any order inside a group), start[k] = first
+ * slot of key k, start[k] = n for every k past the last key.  A counting sort
+ * (integer atomics, exclusive scan, cursor fill); stream-ordered; ws of
+ * dicm_ref_transpose_workspace bytes.  With the order-independent exact group
+ * sums of dicm_sample_bwd it replaces np.add.at (autograd.py:267-271)
+ * deterministically. */
 size_t dicm_ref_transpose_workspace(int64_t n, int64_t key_cap);
 int dicm_ref_transpose(const int32_t* inv, int64_t n, int64_t key_cap, void* ws, size_t ws_bytes,
                        int32_t* order, int32_t* start /* [key_cap + 1] */, dicm_stream_t stream);

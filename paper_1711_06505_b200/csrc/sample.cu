@@ -91,7 +91,6 @@ struct Args {
   float* attn_part;
 };
 
-__device__ __forceinline__ int dq_of(const Args& a, int ch) { return ch == 0 ? DICM_D : DICM_D * a.L.n_query; }
 
 __device__ void load_attn(AttnSmem& s, const dicm_attn_params_t& p, int dq) {
   const int in = dq + DICM_D;
@@ -165,17 +164,6 @@ __device__ __forceinline__ float attn_score_rc(const AttnSmem& s, const float* P
   return sc;
 }
 
-__device__ __forceinline__ float attn_score(const AttnSmem& s, const float* P, const Row12& k) {
-  float sc = s.b1;
-#pragma unroll 8
-  for (int j = 0; j < DICM_ATT; ++j) {
-    float pre = P[j];  // shared-memory broadcast
-#pragma unroll
-    for (int c = 0; c < DICM_D; ++c) pre = fmaf(s.wk[j][c], k.v[c], pre);
-    sc = fmaf(s.w1[j], prelu(pre, s.a0[j]), sc);
-  }
-  return sc;
-}
 
 // per-column max over a sample's behaviors and its FIRST argmax (the reference
 // keeps the earliest row on ties); every lane ends with the warp result;
@@ -704,10 +692,69 @@ __device__ __forceinline__ void store_row12(float* p, const float (&v)[DICM_D]) 
   q[2] = make_float4(v[8], v[9], v[10], v[11]);
 }
 
-// out[u] = sum of the gradient rows of key u's references, in ascending
-// reference order (thread per key; keys with > HOT_REFS references are
-// listed for k_ref_reduce_hot)
-__global__ void __launch_bounds__(256) k_ref_reduce(const __grid_constant__ RefSrc S, const int32_t* __restrict__ order,
+// Exact, order-independent sums.  A key's references come in no particular
+// order (the counting-sort transpose fills groups through atomic cursors), so
+// each component is summed in 64-bit fixed point: scale 2^shift chosen from
+// the group's largest |value| (max is order-independent) and count so that
+// the integer sum cannot overflow; integer addition is associative, hence the
+// same bits whatever the order, and the sum is exact up to the per-term
+// rounding at 2^-shift (far below fp32's).  A non-finite component falls back
+// to the fp32 sum, whose inf/nan outcome is order-independent too.
+struct FixedAcc {
+  float mx[DICM_D];
+  unsigned nf;  // bit c: component c saw a non-finite value
+};
+
+__device__ __forceinline__ void fx_init(FixedAcc& f) {
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) f.mx[c] = 0.f;
+  f.nf = 0;
+}
+
+__device__ __forceinline__ void fx_see(FixedAcc& f, const float (&v)[DICM_D]) {
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) {
+    if (!isfinite(v[c])) f.nf |= 1u << c;
+    f.mx[c] = fmaxf(f.mx[c], fabsf(v[c]));
+  }
+}
+
+__device__ __forceinline__ int fx_shift(float mx, int n) {
+  int e;
+  frexpf(mx, &e);  // mx < 2^e
+  const int lg = n > 1 ? 32 - __clz(n - 1) : 0;  // ceil(log2 n)
+  return 62 - e - lg;
+}
+
+__device__ __forceinline__ long long fx_quant(float v, int shift) { return __double2ll_rn(ldexp((double)v, shift)); }
+
+__device__ __forceinline__ float fx_result(long long q, int shift, const FixedAcc& f, int c) {
+  if (f.mx[c] == 0.f) return 0.f;
+  return (float)ldexp((double)q, -shift);  // exact scaling of the (53-bit rounded) sum, then fp32 rounding
+}
+
+// a group with a non-finite component (rare): the plain fp32 sum of that
+// component -- inf / nan outcomes do not depend on the order
+__device__ void fx_nonfinite(const RefSrc& S, const int32_t* __restrict__ order, int32_t j0, int32_t j1,
+                             int32_t step, unsigned nf, float (&r)[DICM_D]) {
+  float fs[DICM_D];
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) fs[c] = 0.f;
+  for (int32_t j = j0; j < j1; j += step) {
+    float v[DICM_D];
+    ref_contrib(S, __ldg(order + j), v);
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) fs[c] += v[c];
+  }
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c)
+    if ((nf >> c) & 1u) r[c] = fs[c];
+}
+
+// out[u] = sum of the gradient rows of key u's references (thread per key;
+// keys with > HOT_REFS references are listed for k_ref_reduce_hot)
+template <int MINB>  // DICM_REDUCE_OCC: 2 (128 registers) or 3 blocks/SM (80 registers, the rare multi-reference path spills)
+__global__ void __launch_bounds__(256, MINB) k_ref_reduce(const __grid_constant__ RefSrc S, const int32_t* __restrict__ order,
                                                     const int32_t* __restrict__ start,
                                                     const int32_t* __restrict__ n_keys, int64_t cap,
                                                     float* __restrict__ out, int32_t* __restrict__ hot_count,
@@ -715,56 +762,116 @@ __global__ void __launch_bounds__(256) k_ref_reduce(const __grid_constant__ RefS
   const int64_t n = min((int64_t)*n_keys, cap);
   for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
     const int32_t s0 = __ldg(start + u), s1 = __ldg(start + u + 1);
-    if (s1 - s0 > HOT_REFS) {
+    const int cnt = s1 - s0;
+    if (cnt > HOT_REFS) {
       hot_list[atomicAdd(hot_count, 1)] = (int32_t)u;
       continue;
     }
-    float acc[DICM_D];
-    ref_contrib(S, __ldg(order + s0), acc);
-    for (int32_t j = s0 + 1; j < s1; ++j) {
-      float v[DICM_D];
-      ref_contrib(S, __ldg(order + j), v);
+    float r[DICM_D];
+    ref_contrib(S, __ldg(order + s0), r);
+    if (cnt > 1) {
+      FixedAcc f;
+      fx_init(f);
+      fx_see(f, r);
+      for (int32_t j = s0 + 1; j < s1; ++j) {
+        float v[DICM_D];
+        ref_contrib(S, __ldg(order + j), v);
+        fx_see(f, v);
+      }
+      int sh[DICM_D];
+      long long q[DICM_D];
 #pragma unroll
-      for (int c = 0; c < DICM_D; ++c) acc[c] += v[c];
+      for (int c = 0; c < DICM_D; ++c) {
+        sh[c] = fx_shift(f.mx[c], cnt);
+        q[c] = fx_quant(r[c], sh[c]);
+      }
+      for (int32_t j = s0 + 1; j < s1; ++j) {
+        float v[DICM_D];
+        ref_contrib(S, __ldg(order + j), v);
+#pragma unroll
+        for (int c = 0; c < DICM_D; ++c) q[c] += fx_quant(v[c], sh[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) r[c] = fx_result(q[c], sh[c], f, c);
+      if (f.nf) fx_nonfinite(S, order, s0, s1, 1, f.nf, r);
     }
-    store_row12(out + u * DICM_D, acc);
+    store_row12(out + u * DICM_D, r);
   }
 }
 
-// the listed keys, one block each: thread t sums references t, t + 256, ...
-// in order, then a fixed-shape tree over the threads -- the result does not
-// depend on which block takes the key
+// the listed keys, one block each: per-thread partial maxima / fixed-point
+// sums over references t, t + 256, ..., combined in shared memory (the
+// integer sums are associative, the maxima order-independent)
 __global__ void __launch_bounds__(256) k_ref_reduce_hot(const __grid_constant__ RefSrc S,
                                                         const int32_t* __restrict__ order,
                                                         const int32_t* __restrict__ start,
                                                         const int32_t* __restrict__ hot_count,
                                                         const int32_t* __restrict__ hot_list,
                                                         float* __restrict__ out) {
-  __shared__ float red[256][DICM_D + 1];
+  __shared__ union {
+    float mx[256][DICM_D + 1];
+    long long q[256][DICM_D + 1];
+  } red;
+  __shared__ unsigned snf[256];
+  __shared__ float smx[DICM_D];
   const int t = threadIdx.x;
   const int nh = *hot_count;
   for (int h = blockIdx.x; h < nh; h += gridDim.x) {
     const int32_t u = hot_list[h];
     const int32_t s0 = start[u], s1 = start[u + 1];
-    float acc[DICM_D];
+    FixedAcc f;
+    fx_init(f);
+    for (int32_t j = s0 + t; j < s1; j += 256) {
+      float v[DICM_D];
+      ref_contrib(S, __ldg(order + j), v);
+      fx_see(f, v);
+    }
 #pragma unroll
-    for (int c = 0; c < DICM_D; ++c) acc[c] = 0.f;
+    for (int c = 0; c < DICM_D; ++c) red.mx[t][c] = f.mx[c];
+    snf[t] = f.nf;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {  // fixed-shape tree
+      if (t < w) {
+#pragma unroll
+        for (int c = 0; c < DICM_D; ++c) red.mx[t][c] = fmaxf(red.mx[t][c], red.mx[t + w][c]);
+        snf[t] |= snf[t + w];
+      }
+      __syncthreads();
+    }
+    if (t < DICM_D) smx[t] = red.mx[0][t];
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) f.mx[c] = smx[c];
+    f.nf = snf[0];
+    int sh[DICM_D];
+    long long q[DICM_D];
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) {
+      sh[c] = fx_shift(f.mx[c], s1 - s0);
+      q[c] = 0;
+    }
     for (int32_t j = s0 + t; j < s1; j += 256) {
       float v[DICM_D];
       ref_contrib(S, __ldg(order + j), v);
 #pragma unroll
-      for (int c = 0; c < DICM_D; ++c) acc[c] += v[c];
+      for (int c = 0; c < DICM_D; ++c) q[c] += fx_quant(v[c], sh[c]);
     }
 #pragma unroll
-    for (int c = 0; c < DICM_D; ++c) red[t][c] = acc[c];
+    for (int c = 0; c < DICM_D; ++c) red.q[t][c] = q[c];
     __syncthreads();
     for (int w = 128; w > 0; w >>= 1) {
       if (t < w)
 #pragma unroll
-        for (int c = 0; c < DICM_D; ++c) red[t][c] += red[t + w][c];
+        for (int c = 0; c < DICM_D; ++c) red.q[t][c] += red.q[t + w][c];
       __syncthreads();
     }
-    if (t < DICM_D) out[(int64_t)u * DICM_D + t] = red[0][t];
+    if (t == 0) {
+      float r[DICM_D];
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) r[c] = fx_result(red.q[0][c], sh[c], f, c);
+      if (f.nf) fx_nonfinite(S, order, s0, s1, 1, f.nf, r);
+      store_row12(out + (int64_t)u * DICM_D, r);
+    }
     __syncthreads();
   }
 }
@@ -938,6 +1045,19 @@ static RefSrc id_src(const dicm_layout_t* L, const dicm_batch_view_t* V, const f
   return S;
 }
 
+static void ref_reduce(const RefSrc& S, const int32_t* order, const int32_t* start, const int32_t* n_keys, int64_t cap,
+                       float* out, int32_t* hot_count, int32_t* hot_list, cudaStream_t st) {
+  static const int occ = [] {
+    const char* e = getenv("DICM_REDUCE_OCC");
+    return e && e[0] == '2' ? 2 : 3;
+  }();
+  const int grid = dicm_grid(cap, 256, 148 * 16);
+  if (occ == 2)
+    k_ref_reduce<2><<<grid, 256, 0, st>>>(S, order, start, n_keys, cap, out, hot_count, hot_list);
+  else
+    k_ref_reduce<3><<<grid, 256, 0, st>>>(S, order, start, n_keys, cap, out, hot_count, hot_list);
+}
+
 // every unique ID row's gradient (the hot-key counter bv->hot[1] must be
 // zero; dicm_sample_bwd clears both counters before its kernels)
 static void launch_id_reduce(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const float* d_head_in,
@@ -945,8 +1065,7 @@ static void launch_id_reduce(const dicm_layout_t* layout, const dicm_batch_view_
   if (layout->n_fields <= 0) return;
   int32_t* hot_list_id = bv->hot + 2 + bv->img_cap;
   const RefSrc S = id_src(layout, bv, d_head_in);
-  k_ref_reduce<<<dicm_grid(bv->id_cap, 256, 148 * 16), 256, 0, st>>>(S, bv->id_order, bv->id_start, bv->n_id_keys,
-                                                                   bv->id_cap, d_rows, bv->hot + 1, hot_list_id);
+  ref_reduce(S, bv->id_order, bv->id_start, bv->n_id_keys, bv->id_cap, d_rows, bv->hot + 1, hot_list_id, st);
   k_ref_reduce_hot<<<148, 256, 0, st>>>(S, bv->id_order, bv->id_start, bv->hot + 1, hot_list_id, d_rows);
 }
 
@@ -1000,14 +1119,11 @@ int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
   }
   // every unique image row and ID row: its references summed in order
   int32_t* hot_list_img = bv->hot + 2;
-  int32_t* hot_list_id = bv->hot + 2 + bv->img_cap;
   if (layout->use_ad_image || layout->use_behavior_images) {
     const RefSrc S = image_src(layout, bv, d_head_in);
-    k_ref_reduce<<<dicm_grid(bv->img_cap, 256, 148 * 16), 256, 0, st>>>(S, bv->img_order, bv->img_start, bv->n_img_keys,
-                                                                      bv->img_cap, d_emb, bv->hot, hot_list_img);
+    ref_reduce(S, bv->img_order, bv->img_start, bv->n_img_keys, bv->img_cap, d_emb, bv->hot, hot_list_img, st);
     k_ref_reduce_hot<<<148, 256, 0, st>>>(S, bv->img_order, bv->img_start, bv->hot, hot_list_img, d_emb);
   }
-  (void)hot_list_id;
   if (d_rows) launch_id_reduce(layout, bv, d_head_in, d_rows, st);
   probe_end(probe_slot, st);
   return last_launch("dicm_sample_bwd");
