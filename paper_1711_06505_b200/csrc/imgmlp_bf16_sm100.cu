@@ -83,10 +83,12 @@ __device__ __forceinline__ uint4 prelu_chunk(uint4 v, const float (&al)[8], bool
 // ===========================================================================
 // k_l12f: forward layers 1-2
 // ===========================================================================
-constexpr uint32_t FT = 64 * 1024;  // a0 tile: 4 boxes x 128 rows x 128 B (bf16, SW128)
+constexpr uint32_t FBOX = 16 * 1024;  // one a0 box: 128 rows x 64 columns (bf16, SW128); a tile is 4 boxes
+constexpr int FNB = 10;               // boxes in the ring (2.5 tiles in flight; the ring advances box by box)
 constexpr uint32_t FW = 32 * 1024;  // W1 [64 x 256] bf16 K-major SW128: 4 atoms x 64 rows x 128 B
 constexpr int FPAR = 256 + 64 + 64 + 768 + 16;  // al0 | b1 | al1 | w2 | b2
-constexpr size_t F_SMEM = 1024 + 2 * FT + FW + 4 * FPAR + 128 + 4 * epi::SCRATCH_FLOATS * 4;
+constexpr size_t F_SMEM = 1024 + FNB * FBOX + FW + 4 * FPAR + 8 * (3 * FNB + 4) + 16 + 4 * epi::SCRATCH_FLOATS * 4;
+static_assert(F_SMEM <= 232448, "k_l12f shared memory");
 constexpr int F_THREADS = 320;  // w0 TMA | w1 MMA | w2-5 PReLU | w6-9 epilogue
 
 __global__ void __launch_bounds__(F_THREADS, 1)
@@ -99,22 +101,25 @@ __global__ void __launch_bounds__(F_THREADS, 1)
   if ((int)blockIdx.x >= ntiles) return;
   extern __shared__ uint8_t raw[];
   const uint32_t r0 = smem_u32(raw), base = (r0 + 1023u) & ~1023u;
-  const uint32_t W = base + 2 * FT;
+  const uint32_t W = base + FNB * FBOX;
   float* sal0 = at<float>(raw, r0, W + FW);
   float* sb1 = sal0 + 256;
   float* sal1 = sb1 + 64;
   float* sw2 = sal1 + 64;
   float* sb2 = sw2 + 768;
+  // per box: full (TMA), ready (PReLU done), empty (MMA done); per tile accumulator: accf, acce
   const uint32_t bars = W + FW + 4 * FPAR;
-  const uint32_t full = bars, ready = bars + 16, empty = bars + 32, accf = bars + 48, acce = bars + 64,
-                 slot = bars + 80;
-  float* scr_base = at<float>(raw, r0, bars + 128);
+  const uint32_t full = bars, ready = bars + 8 * FNB, empty = bars + 16 * FNB, accf = bars + 24 * FNB,
+                 acce = accf + 16, slot = acce + 16;
+  float* scr_base = at<float>(raw, r0, slot + 16);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   if (t == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < FNB; ++i) {
       mbar_init(full + 8 * i, 1);
       mbar_init(ready + 8 * i, 128);
       mbar_init(empty + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(accf + 8 * i, 1);
       mbar_init(acce + 8 * i, 128);
     }
@@ -149,60 +154,64 @@ __global__ void __launch_bounds__(F_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      // ---- TMA producer: box j of every tile into the next free ring slot
       prefetch_tmap(&tmA0);
-      uint32_t it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const uint32_t s = it & 1, ph = (it >> 1) & 1;
-        mbar_wait(empty + 8 * s, ph ^ 1);
-        mbar_arrive_expect_tx(full + 8 * s, FT);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) tma_load_2d(base + s * FT + j * 16384, &tmA0, full + 8 * s, j * 64, tile * 128);
-      }
+      uint32_t g = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+        for (int j = 0; j < 4; ++j, ++g) {
+          const uint32_t b = g % FNB, ph = (g / FNB) & 1;
+          mbar_wait(empty + 8 * b, ph ^ 1);
+          mbar_arrive_expect_tx(full + 8 * b, FBOX);
+          tma_load_2d(base + b * FBOX, &tmA0, full + 8 * b, j * 64, tile * 128);
+        }
     }
   } else if (warp == 1) {
     if (lane == 0) {
+      // ---- MMA: K = 64 per box (4 x K16), each box released as soon as its MMAs are done
       const uint32_t idesc = instr_desc(1, 128, 64, 0, 0);
-      uint32_t it = 0;
+      uint32_t it = 0, g = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const uint32_t s = it & 1, ph = (it >> 1) & 1;
         mbar_wait(acce + 8 * s, ph ^ 1);
-        mbar_wait(ready + 8 * s, ph);
-        tc_fence_after();
-        const uint32_t A = base + s * FT;
+        for (int j = 0; j < 4; ++j, ++g) {
+          const uint32_t b = g % FNB;
+          mbar_wait(ready + 8 * b, (g / FNB) & 1);
+          tc_fence_after();
+          const uint32_t A = base + b * FBOX;
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-          const int j = kk >> 2, k4 = kk & 3;
-          mma<1>(tmem + s * 64, smem_desc(A + j * 16384 + k4 * 32, 16, 1024), smem_desc(W + j * 8192 + k4 * 32, 16, 1024),
-                 idesc, kk > 0);
+          for (int k4 = 0; k4 < 4; ++k4)
+            mma<1>(tmem + s * 64, smem_desc(A + k4 * 32, 16, 1024), smem_desc(W + j * 8192 + k4 * 32, 16, 1024),
+                   idesc, (j | k4) != 0);
+          mma_commit(empty + 8 * b);
         }
-        mma_commit(empty + 8 * s);
         mma_commit(accf + 8 * s);
       }
     }
   } else if (warp < 6) {
-    // ---- PReLU in place: thread owns physical chunk c of rows (tid>>3) + 16 i
-    // of every box; its logical column chunk (c ^ (row & 7)) is fixed
+    // ---- PReLU in place, box by box: thread owns physical chunk c of rows
+    // (tid>>3) + 16 i; its logical column chunk (c ^ (row & 7)) is fixed
     const int tid = t - 64, c = tid & 7, rlo = tid >> 3, lc = c ^ (rlo & 7);
     float al[4][8];
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int e = 0; e < 8; ++e) al[j][e] = sal0[j * 64 + lc * 8 + e];
-    uint32_t it = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const uint32_t s = it & 1, ph = (it >> 1) & 1;
-      mbar_wait(full + 8 * s, ph);
-      const uint32_t A = base + s * FT;
+    uint32_t g = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < 4; ++j, ++g) {
+        const uint32_t b = g % FNB;
+        mbar_wait(full + 8 * b, (g / FNB) & 1);
+        const uint32_t A = base + b * FBOX;
 #pragma unroll 4
         for (int i = 0; i < 8; ++i) {
           const int r = rlo + 16 * i;
-          uint4* p = at<uint4>(raw, r0, A + j * 16384 + r * 128 + (c << 4));
+          uint4* p = at<uint4>(raw, r0, A + r * 128 + (c << 4));
           *p = prelu_chunk(*p, al[j], true);
         }
-      fence_proxy_async();
-      mbar_arrive(ready + 8 * s);
+        fence_proxy_async();
+        mbar_arrive(ready + 8 * b);
+      }
     }
   } else {
     // ---- epilogue: TMEM lane quarter q = warp % 4

@@ -461,11 +461,52 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
     __syncwarp();
     // lane j: hidden unit j across the chunk's references
     const int nr = (int)min((int64_t)32, i1 - c0);
-#pragma unroll 4
-    for (int r = 0; r < nr; ++r) {  // unrolled: independent pre-activation chains interleave
+    // per reference r (in order): the rest of hidden unit j's backward from its pre-activation
+    auto unit = [&](int r, float pre, const float4& k0, const float4& k1, const float4& k2) {
+      const float dsr = ws.ds[r];
+      const float dh = dsr * w1j;
+      const bool pos = pre > 0.f;
+      const float dpre = pos ? dh : a0j * dh;
+      acc.w1 = fmaf(dsr, pos ? pre : a0j * pre, acc.w1);
+      if (!pos) acc.a0 = fmaf(pre, dh, acc.a0);
+      acc.b0 += dpre;
+      dP += dpre;
+      // paired FMAs (FFMA2), same per-element fma.rn as before
+      ffma2(acc.wk[0], acc.wk[1], k0.x, k0.y, dpre);
+      ffma2(acc.wk[2], acc.wk[3], k0.z, k0.w, dpre);
+      ffma2(acc.wk[4], acc.wk[5], k1.x, k1.y, dpre);
+      ffma2(acc.wk[6], acc.wk[7], k1.z, k1.w, dpre);
+      ffma2(acc.wk[8], acc.wk[9], k2.x, k2.y, dpre);
+      ffma2(acc.wk[10], acc.wk[11], k2.z, k2.w, dpre);
+      ws.dp[r][lane] = dpre;
+    };
+    // two references at a time: their pre-activations as paired FMAs (each
+    // element the forward's chain pre = Pj, then fma(wk[c], k[c], pre) in c order)
+    int r = 0;
+#pragma unroll 2
+    for (; r + 1 < nr; r += 2) {
+      const float4* ka = reinterpret_cast<const float4*>(ws.ks[r]);
+      const float4* kb = reinterpret_cast<const float4*>(ws.ks[r + 1]);
+      const float4 a0 = ka[0], a1 = ka[1], a2 = ka[2], b0 = kb[0], b1 = kb[1], b2 = kb[2];
+      float pa = Pj, pb = Pj;
+      ffma2(pa, pb, a0.x, b0.x, wkj[0]);
+      ffma2(pa, pb, a0.y, b0.y, wkj[1]);
+      ffma2(pa, pb, a0.z, b0.z, wkj[2]);
+      ffma2(pa, pb, a0.w, b0.w, wkj[3]);
+      ffma2(pa, pb, a1.x, b1.x, wkj[4]);
+      ffma2(pa, pb, a1.y, b1.y, wkj[5]);
+      ffma2(pa, pb, a1.z, b1.z, wkj[6]);
+      ffma2(pa, pb, a1.w, b1.w, wkj[7]);
+      ffma2(pa, pb, a2.x, b2.x, wkj[8]);
+      ffma2(pa, pb, a2.y, b2.y, wkj[9]);
+      ffma2(pa, pb, a2.z, b2.z, wkj[10]);
+      ffma2(pa, pb, a2.w, b2.w, wkj[11]);
+      unit(r, pa, a0, a1, a2);
+      unit(r + 1, pb, b0, b1, b2);
+    }
+    if (r < nr) {
       const float4* kr = reinterpret_cast<const float4*>(ws.ks[r]);
       const float4 k0 = kr[0], k1 = kr[1], k2 = kr[2];
-      // the forward's pre-activation, same fma order (attn_score_rc)
       float pre = Pj;
       pre = fmaf(wkj[0], k0.x, pre);
       pre = fmaf(wkj[1], k0.y, pre);
@@ -479,23 +520,7 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
       pre = fmaf(wkj[9], k2.y, pre);
       pre = fmaf(wkj[10], k2.z, pre);
       pre = fmaf(wkj[11], k2.w, pre);
-      const float dsr = ws.ds[r];
-      const float dh = dsr * w1j;
-      const bool pos = pre > 0.f;
-      const float dpre = pos ? dh : a0j * dh;
-      acc.w1 = fmaf(dsr, pos ? pre : a0j * pre, acc.w1);
-      if (!pos) acc.a0 = fmaf(pre, dh, acc.a0);
-      acc.b0 += dpre;
-      dP += dpre;
-      {  // paired FMAs (FFMA2), same per-element fma.rn as before
-        ffma2(acc.wk[0], acc.wk[1], k0.x, k0.y, dpre);
-        ffma2(acc.wk[2], acc.wk[3], k0.z, k0.w, dpre);
-        ffma2(acc.wk[4], acc.wk[5], k1.x, k1.y, dpre);
-        ffma2(acc.wk[6], acc.wk[7], k1.z, k1.w, dpre);
-        ffma2(acc.wk[8], acc.wk[9], k2.x, k2.y, dpre);
-        ffma2(acc.wk[10], acc.wk[11], k2.z, k2.w, dpre);
-      }
-      ws.dp[r][lane] = dpre;
+      unit(r, pre, k0, k1, k2);
     }
     __syncwarp();
     if (valid) {
