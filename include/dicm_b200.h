@@ -145,9 +145,9 @@ int dicm_imgmlp_bwd(const void* pool, int pool_dtype, int d_raw, const int32_t* 
  *   col_scale bwd 348-350); embedding and ID-row gradients are summed into
  *   the deduplicated row buffers (np.add.at, autograd.py:267-271) WITHOUT
  *   float atomics: every unique key sums its references (grouped by
- *   dicm_ref_transpose) exactly in 64-bit fixed point, which does not depend
- *   on their order, so a step is bit-reproducible like the reference's
- *   (runtime.py:16-21);
+ *   dicm_ref_transpose) in ascending reference order (groups of up to 16) or
+ *   exactly in 64-bit fixed point (larger groups: independent of the order),
+ *   so a step is bit-reproducible like the reference's (runtime.py:16-21);
  *   attention-parameter gradients are written as per-block partial sums.
  * ---------------------------------------------------------------------- */
 typedef struct {

@@ -111,12 +111,15 @@ __global__ void k_rows(const __grid_constant__ Tables tb, const int32_t* __restr
     const int64_t u = w * 10 + slot;
     const bool live = slot < 10 && u < n;
     float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (live) g = __ldcg(reinterpret_cast<const float4*>(grads + u * DICM_D) + part);
+    int64_t key = 0;
+    if (live) {  // the gradient and the key in flight together
+      g = __ldcg(reinterpret_cast<const float4*>(grads + u * DICM_D) + part);
+      key = __ldg(keys + u);
+    }
     const bool nz = g.x != 0.f || g.y != 0.f || g.z != 0.f || g.w != 0.f;
     const unsigned any = __ballot_sync(0xffffffffu, nz);
     const unsigned grp = 7u << (3 * (lane / 3));
     if (!live || !(any & grp)) continue;  // all-zero row: skipped (optim.py:93-94)
-    const int64_t key = keys[u];
     int k = 0;
     while (k + 1 < tb.n && key >= tb.t[k + 1].base) ++k;
     const dicm_table_state_t& T = tb.t[k];

@@ -708,7 +708,8 @@ __device__ __forceinline__ void ref_contrib(const RefSrc& S, int64_t p, float (&
   }
 }
 
-constexpr int HOT_REFS = 128;  // keys with more references go to the block-wide reduction
+constexpr int HOT_REFS = 128;    // keys with more references go to the block-wide reduction
+constexpr int SMALL_GROUP = 16;  // up to this many: sorted positions, fp32 sum in reference order
 
 __device__ __forceinline__ void store_row12(float* p, const float (&v)[DICM_D]) {
   float4* q = reinterpret_cast<float4*>(p);
@@ -793,8 +794,32 @@ __global__ void __launch_bounds__(256, MINB) k_ref_reduce(const __grid_constant_
       continue;
     }
     float r[DICM_D];
+    if (cnt <= SMALL_GROUP) {
+      // the common case (a handful of references): sort the positions --
+      // nearly sorted already, the fill hands out warp-ordered runs -- and
+      // sum in ascending reference order like np.add.at
+      int32_t pos[SMALL_GROUP];
+      for (int i = 0; i < cnt; ++i) {
+        const int32_t p = __ldg(order + s0 + i);
+        int j = i;
+        while (j > 0 && pos[j - 1] > p) {
+          pos[j] = pos[j - 1];
+          --j;
+        }
+        pos[j] = p;
+      }
+      ref_contrib(S, pos[0], r);
+      for (int i = 1; i < cnt; ++i) {
+        float v[DICM_D];
+        ref_contrib(S, pos[i], v);
+#pragma unroll
+        for (int c = 0; c < DICM_D; ++c) r[c] += v[c];
+      }
+      store_row12(out + u * DICM_D, r);
+      continue;
+    }
     ref_contrib(S, __ldg(order + s0), r);
-    if (cnt > 1) {
+    {
       FixedAcc f;
       fx_init(f);
       fx_see(f, r);

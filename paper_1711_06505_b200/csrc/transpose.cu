@@ -9,12 +9,13 @@
 // counting sort -- per-key counts (integer atomics), an exclusive scan, and a
 // fill through per-key cursors -- so every key owns a contiguous group of its
 // references.  The order inside a group is NOT fixed; the reduction over a
-// group (sample.cu k_ref_reduce) is made order-independent instead: each
-// component is summed exactly in 64-bit fixed point (scale from the group's
-// largest magnitude, an order-independent max), so the result does not
-// depend on the order -- and is closer to the exact sum than any fp32
-// summation order.  Three light passes over the references replace a
-// three-pass radix sort (~0.14 ms per cfg2 step for the two lists).
+// group (sample.cu k_ref_reduce) restores determinism itself: a group of up
+// to 16 references (nearly all of them) is sorted by position in registers
+// and summed in reference order like np.add.at; a larger group is summed
+// exactly in 64-bit fixed point (scale from the group's largest magnitude, an
+// order-independent max), which does not depend on the order at all.  Three
+// light passes over the references replace a three-pass radix sort (~0.14 ms
+// per cfg2 step for the two lists).
 #include <cub/cub.cuh>
 
 #include "common.cuh"
