@@ -794,10 +794,30 @@ __global__ void __launch_bounds__(256, MINB) k_ref_reduce(const __grid_constant_
       continue;
     }
     float r[DICM_D];
+    if (cnt <= 3) {  // most groups: a register sort of the positions, sum in reference order
+      int32_t p0 = __ldg(order + s0), p1 = cnt > 1 ? __ldg(order + s0 + 1) : INT_MAX,
+              p2 = cnt > 2 ? __ldg(order + s0 + 2) : INT_MAX;
+      if (p1 < p0) { const int32_t x = p0; p0 = p1; p1 = x; }
+      if (p2 < p1) { const int32_t x = p1; p1 = p2; p2 = x; }
+      if (p1 < p0) { const int32_t x = p0; p0 = p1; p1 = x; }
+      ref_contrib(S, p0, r);
+      if (cnt > 1) {
+        float v[DICM_D];
+        ref_contrib(S, p1, v);
+#pragma unroll
+        for (int c = 0; c < DICM_D; ++c) r[c] += v[c];
+        if (cnt > 2) {
+          ref_contrib(S, p2, v);
+#pragma unroll
+          for (int c = 0; c < DICM_D; ++c) r[c] += v[c];
+        }
+      }
+      store_row12(out + u * DICM_D, r);
+      continue;
+    }
     if (cnt <= SMALL_GROUP) {
-      // the common case (a handful of references): sort the positions --
-      // nearly sorted already, the fill hands out warp-ordered runs -- and
-      // sum in ascending reference order like np.add.at
+      // a handful of references: sort the positions (insertion sort) and sum
+      // in ascending reference order like np.add.at
       int32_t pos[SMALL_GROUP];
       for (int i = 0; i < cnt; ++i) {
         const int32_t p = __ldg(order + s0 + i);
