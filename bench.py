@@ -146,28 +146,45 @@ def build_workload(name, rank, world, precision, seed=0, device="cuda"):
     return schema, model, pool
 
 
-def kernel_work(U, B, R, W, D, e):
-    """Algorithmic (bytes, flops) per launch of each probed kernel, counting
-    only what the math needs: U unique images, B samples, R
-    behaviors, W head-input width, D = d_raw, e = layer-0 operand bytes.  The
-    saved activations act0/act1 (and da1/da0) are stored in the operand dtype
-    in bf16 mode (e = 2) and in fp32 otherwise."""
+# FP32 CUDA-core peak for the per-sample kernels (no measured figure exists):
+# 148 SMs x 4 SMSPs x 32 lanes x 2 FMAs (paired FFMA2, one every 2 cycles,
+# B300_MICROARCH.md pipe rates) x 2 FLOP at 1.965 GHz
+FP32_PEAK_TFLOPS = 148 * 4 * 32 * 2 * 2 / 2 * 1.965e9 / 1e12
+
+
+def attn_flops_per_ref(kind):
+    """(forward, backward) FP32 FLOP per behavior reference of the attention
+    channels (the 12 -> 32 key projection, PReLU and score per
+    hidden unit, the softmax and weighted sum; backward: the projection again,
+    the PReLU / softmax backward, dWk, dk)."""
+    ch = {"attn": 1, "multiquery-attn": 2}.get(kind, 0)
+    return ch * (2 * 12 * 32 + 4 * 32 + 2 * 12 + 8), ch * (3 * 2 * 12 * 32 + 8 * 32 + 4 * 12 + 16)
+
+
+def kernel_work(U, B, R, W, D, e, kind="attn"):
+    """Algorithmic (bytes, tensor flops, CUDA-core flops) per launch of each
+    probed kernel, counting only what the math needs: U unique
+    images, B samples, R behaviors, W head-input width, D = d_raw, e = layer-0
+    operand bytes.  The saved activations act0/act1 (and da1/da0) are stored
+    in the operand dtype in bf16 mode (e = 2) and in fp32 otherwise."""
     Rimg = B + R
     a = e  # bytes per saved activation
+    af, ab = attn_flops_per_ref(kind)
     return {
         # X rows + W0 in, act0 out
-        "img_fwd_l0": (U * D * e + 256 * D * e + U * 256 * a, 2 * U * D * 256),
+        "img_fwd_l0": (U * D * e + 256 * D * e + U * 256 * a, 2 * U * D * 256, 0),
         # act0 in, act1 + emb out
-        "img_fwd_l12": (U * ((256 + 64) * a + 12 * 4), 2 * U * (256 * 64 + 64 * 12)),
+        "img_fwd_l12": (U * ((256 + 64) * a + 12 * 4), 2 * U * (256 * 64 + 64 * 12), 0),
         # dE, act1, act0 in; da1, da0 out (dh2, dW2, dh1)
-        "img_bwd_l12": (U * (12 * 4 + (64 + 256 + 64 + 256) * a), 2 * U * (2 * 12 * 64 + 64 * 256)),
+        "img_bwd_l12": (U * (12 * 4 + (64 + 256 + 64 + 256) * a), 2 * U * (2 * 12 * 64 + 64 * 256), 0),
         # act0 (-> h1), da1 in
-        "img_bwd_dw1": (U * (256 + 64) * a, 2 * U * 64 * 256),
+        "img_bwd_dw1": (U * (256 + 64) * a, 2 * U * 64 * 256, 0),
         # X rows + da0 in, dW0 out
-        "img_bwd_dw0": (U * D * e + U * 256 * e + 256 * D * 4, 2 * U * D * 256),
-        # inverse ids + embedding rows per reference, head input out
-        "sample_fwd": (Rimg * (4 + 48) + B * W * 4, 0),
-        "sample_bwd": (Rimg * (4 + 48) + U * 48 + B * W * 4, 0),
+        "img_bwd_dw0": (U * D * e + U * 256 * e + 256 * D * 4, 2 * U * D * 256, 0),
+        # image columns of the head input: inverse ids + embedding rows per reference, the attention math
+        "sample_fwd": (Rimg * (4 + 48) + B * W * 4, 0, R * af),
+        # attention backward + the ordered sums into dE: rows per reference in, dE out
+        "sample_bwd": (Rimg * (4 + 48) + U * 48 + B * W * 4, 0, R * ab),
     }
 
 
@@ -553,17 +570,22 @@ def main():
     tc_peak = peaks.get("bf16_tflops_sustained", 1362.2) if precision == "bf16" else \
         peaks.get("bf16_tflops_sustained", 1362.2) / 2.0
     elem = 2 if precision == "bf16" else 4
-    kern = kernel_work(U, B, R, width, schema.d_raw, elem)
+    kern = kernel_work(U, B, R, width, schema.d_raw, elem, kind)
     table = {}
-    for k, (nbytes, flops) in kern.items():
+    for k, (nbytes, flops, sflops) in kern.items():
         t = probes.get(k) or []
         if not t:
             continue
         ms_k = statistics.mean(t)
-        ideal = max(nbytes / (hbm_peak * 1e9), flops / (tc_peak * 1e12) if k.startswith("img") else 0.0)
+        ideal = max(nbytes / (hbm_peak * 1e9), flops / (tc_peak * 1e12), sflops / (FP32_PEAK_TFLOPS * 1e12))
         table[k] = {"ms": ms_k, "launches": len(t), "alg_bytes": nbytes, "GB_s": nbytes / (ms_k / 1e3) / 1e9,
                     "flops": flops, "TFLOP_s": flops / (ms_k / 1e3) / 1e12,
                     "roofline_frac": ideal / (ms_k / 1e3)}
+        if sflops:
+            table[k].update({"fp32_flops": sflops, "fp32_TFLOP_s": sflops / (ms_k / 1e3) / 1e12,
+                             "fp32_peak_TFLOP_s": FP32_PEAK_TFLOPS,
+                             "bound": "fp32" if sflops / FP32_PEAK_TFLOPS / 1e12 > nbytes / hbm_peak / 1e9
+                             else "hbm"})
     img = [k for k in table if k.startswith("img")]
     mlp_ms = sum(table[k]["ms"] for k in img)
     mlp_flops = sum(table[k]["flops"] for k in img)
@@ -597,15 +619,18 @@ def main():
         comp = {k: max(kern[k][0] / (hbm_peak * 1e9), kern[k][1] / (tc_peak * 1e12)) for k in kern
                 if k.startswith("img")}
         comp["dedup"] = (Rimg * 12 + U * 8 + n_id * 12 + K * 8) / (hbm_peak * 1e9)
-        comp["pooling"] = (kern["sample_fwd"][0] + kern["sample_bwd"][0]) / (hbm_peak * 1e9)
+        comp["pooling"] = sum(max(kern[k][0] / (hbm_peak * 1e9), kern[k][2] / (FP32_PEAK_TFLOPS * 1e12))
+                              for k in ("sample_fwd", "sample_bwd"))
         comp["id_rows"] = (2 * n_id * (4 + 48) + K * 48 + K * (6 * 48 + 16)) / (hbm_peak * 1e9)
         comp["head"] = 2 * B * width * 4 / (hbm_peak * 1e9)
         comp["dense_adam"] = int(model.dense.numel()) * 20 / (hbm_peak * 1e9)
         t_roof = sum(comp.values())
         roof["step"] = {"roofline_ms": 1e3 * t_roof, "measured_ms": ms_step, "frac": 1e3 * t_roof / ms_step,
                         "components_ms": {k: round(1e3 * v, 4) for k, v in comp.items()},
-                        "note": "per-GPU step; image MLP at max(bytes/HBM, flops/TC) per kernel, the rest "
-                                "HBM-bound (SURVEY.md 8d byte counts)"}
+                        "note": "per-GPU step; image MLP at max(bytes/HBM, flops/TC) per kernel, pooling at "
+                                "max(bytes/HBM, attention FP32 flops/CUDA-core peak), the rest HBM-bound "
+                                "(SURVEY.md 8d byte counts)",
+                        "fp32_peak_TFLOP_s": FP32_PEAK_TFLOPS}
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
