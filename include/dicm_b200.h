@@ -192,7 +192,7 @@ typedef struct {
   int64_t img_cap, id_cap;      /* capacities of d_emb / d_rows (>= U, K) */
   float* ref_grad;              /* attn / max / concat: [R, 12] scratch, gradient per behavior reference */
   float* q_grad;                /* attn: [B, 36] scratch, query gradients (ad image 12 | ID query fields 24) */
-  int32_t* hot;                 /* [2 + img_cap + id_cap] scratch: keys with > 128 references */
+  int32_t* hot;                 /* [4 + 2 (img_cap + id_cap)] scratch: work lists of keys with many references */
 } dicm_batch_view_t;
 
 /* Transpose of a dedup inverse (inv[p] = key of reference p, keys < key_cap):

@@ -83,196 +83,14 @@ __device__ __forceinline__ uint4 prelu_chunk(uint4 v, const float (&al)[8], bool
 // ===========================================================================
 // k_l12f: forward layers 1-2
 // ===========================================================================
-constexpr uint32_t FBOX = 16 * 1024;  // one a0 box: 128 rows x 64 columns (bf16, SW128); a tile is 4 boxes
-constexpr int FNB = 10;               // boxes in the ring (2.5 tiles in flight; the ring advances box by box)
+constexpr uint32_t FT = 64 * 1024;  // a0 tile: 4 boxes x 128 rows x 128 B (bf16, SW128)
 constexpr uint32_t FW = 32 * 1024;  // W1 [64 x 256] bf16 K-major SW128: 4 atoms x 64 rows x 128 B
 constexpr int FPAR = 256 + 64 + 64 + 768 + 16;  // al0 | b1 | al1 | w2 | b2
-constexpr size_t F_SMEM = 1024 + FNB * FBOX + FW + 4 * FPAR + 8 * (3 * FNB + 4) + 16 + 4 * epi::SCRATCH_FLOATS * 4;
-static_assert(F_SMEM <= 232448, "k_l12f shared memory");
 constexpr int F_THREADS = 320;  // w0 TMA | w1 MMA | w2-5 PReLU | w6-9 epilogue
+constexpr size_t F_SMEM = 1024 + 2 * FT + FW + 4 * FPAR + 128 + 4 * epi::SCRATCH_FLOATS * 4;
 
 __global__ void __launch_bounds__(F_THREADS, 1)
     k_l12f(const __grid_constant__ CUtensorMap tmA0, const float* __restrict__ al0, const float* __restrict__ w1,
-           const float* __restrict__ b1, const float* __restrict__ al1, const float* __restrict__ w2,
-           const float* __restrict__ b2, const int32_t* __restrict__ count, bf16* __restrict__ act1,
-           float* __restrict__ emb) {
-  const int U = *count;
-  const int ntiles = (U + 127) / 128;
-  if ((int)blockIdx.x >= ntiles) return;
-  extern __shared__ uint8_t raw[];
-  const uint32_t r0 = smem_u32(raw), base = (r0 + 1023u) & ~1023u;
-  const uint32_t W = base + FNB * FBOX;
-  float* sal0 = at<float>(raw, r0, W + FW);
-  float* sb1 = sal0 + 256;
-  float* sal1 = sb1 + 64;
-  float* sw2 = sal1 + 64;
-  float* sb2 = sw2 + 768;
-  // per box: full (TMA), ready (PReLU done), empty (MMA done); per tile accumulator: accf, acce
-  const uint32_t bars = W + FW + 4 * FPAR;
-  const uint32_t full = bars, ready = bars + 8 * FNB, empty = bars + 16 * FNB, accf = bars + 24 * FNB,
-                 acce = accf + 16, slot = acce + 16;
-  float* scr_base = at<float>(raw, r0, slot + 16);
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  if (t == 0) {
-    for (int i = 0; i < FNB; ++i) {
-      mbar_init(full + 8 * i, 1);
-      mbar_init(ready + 8 * i, 128);
-      mbar_init(empty + 8 * i, 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(accf + 8 * i, 1);
-      mbar_init(acce + 8 * i, 128);
-    }
-    fence_mbar_init();
-  }
-  // W1 [n=64][k=256] fp32 -> bf16 K-major SW128: atom k/64, row n, 16-B chunk (k%64)/8 ^ (n&7)
-  for (int i = t; i < 64 * 32; i += F_THREADS) {
-    const int n = i >> 5, q = i & 31, j = q >> 3, c = q & 7;
-    const float4 a = __ldg(reinterpret_cast<const float4*>(w1 + n * H1 + q * 8));
-    const float4 b = __ldg(reinterpret_cast<const float4*>(w1 + n * H1 + q * 8 + 4));
-    *at<uint4>(raw, r0, W + j * 8192 + n * 128 + ((c ^ (n & 7)) << 4)) =
-        make_uint4(f2_to_bf2(a.x, a.y), f2_to_bf2(a.z, a.w), f2_to_bf2(b.x, b.y), f2_to_bf2(b.z, b.w));
-  }
-  for (int i = t; i < 256; i += F_THREADS) sal0[i] = al0[i];
-  if (t < 64) {
-    sb1[t] = b1[t];
-    sal1[t] = al1[t];
-  }
-  // W2 [12][64] transposed to [64][12]: one hidden unit's 12 weights are
-  // three 16-B shared loads feeding six paired FMAs
-  for (int i = t; i < 768; i += F_THREADS) sw2[(i & 63) * 12 + (i >> 6)] = w2[i];
-  if (t < 12) sb2[t] = b2[t];
-  if (warp == 1) {
-    tmem_alloc(slot, 128);
-    tmem_relinquish();
-  }
-  fence_proxy_async();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *at<volatile uint32_t>(raw, r0, slot);
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // ---- TMA producer: box j of every tile into the next free ring slot
-      prefetch_tmap(&tmA0);
-      uint32_t g = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-        for (int j = 0; j < 4; ++j, ++g) {
-          const uint32_t b = g % FNB, ph = (g / FNB) & 1;
-          mbar_wait(empty + 8 * b, ph ^ 1);
-          mbar_arrive_expect_tx(full + 8 * b, FBOX);
-          tma_load_2d(base + b * FBOX, &tmA0, full + 8 * b, j * 64, tile * 128);
-        }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // ---- MMA: K = 64 per box (4 x K16), each box released as soon as its MMAs are done
-      const uint32_t idesc = instr_desc(1, 128, 64, 0, 0);
-      uint32_t it = 0, g = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const uint32_t s = it & 1, ph = (it >> 1) & 1;
-        mbar_wait(acce + 8 * s, ph ^ 1);
-        for (int j = 0; j < 4; ++j, ++g) {
-          const uint32_t b = g % FNB;
-          mbar_wait(ready + 8 * b, (g / FNB) & 1);
-          tc_fence_after();
-          const uint32_t A = base + b * FBOX;
-#pragma unroll
-          for (int k4 = 0; k4 < 4; ++k4)
-            mma<1>(tmem + s * 64, smem_desc(A + k4 * 32, 16, 1024), smem_desc(W + j * 8192 + k4 * 32, 16, 1024),
-                   idesc, (j | k4) != 0);
-          mma_commit(empty + 8 * b);
-        }
-        mma_commit(accf + 8 * s);
-      }
-    }
-  } else if (warp < 6) {
-    // ---- PReLU in place, box by box: thread owns physical chunk c of rows
-    // (tid>>3) + 16 i; its logical column chunk (c ^ (row & 7)) is fixed
-    const int tid = t - 64, c = tid & 7, rlo = tid >> 3, lc = c ^ (rlo & 7);
-    float al[4][8];
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 8; ++e) al[j][e] = sal0[j * 64 + lc * 8 + e];
-    uint32_t g = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j, ++g) {
-        const uint32_t b = g % FNB;
-        mbar_wait(full + 8 * b, (g / FNB) & 1);
-        const uint32_t A = base + b * FBOX;
-#pragma unroll 4
-        for (int i = 0; i < 8; ++i) {
-          const int r = rlo + 16 * i;
-          uint4* p = at<uint4>(raw, r0, A + r * 128 + (c << 4));
-          *p = prelu_chunk(*p, al[j], true);
-        }
-        fence_proxy_async();
-        mbar_arrive(ready + 8 * b);
-      }
-    }
-  } else {
-    // ---- epilogue: TMEM lane quarter q = warp % 4
-    const int q = warp & 3;
-    float* scr = scr_base + q * epi::SCRATCH_FLOATS;
-    uint32_t it = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const uint32_t s = it & 1, ph = (it >> 1) & 1;
-      const int m0 = tile * 128;
-      mbar_wait(accf + 8 * s, ph);
-      tc_fence_after();
-      const int row = m0 + q * 32 + lane;
-      float e[12];
-#pragma unroll
-      for (int c = 0; c < 12; ++c) e[c] = sb2[c];
-#pragma unroll 1
-      for (int hh = 0; hh < 2; ++hh) {
-        float a[32];
-        tmem_ld32(tmem + s * 64 + ((uint32_t)(q * 32) << 16) + 32 * hh, a);
-        if (hh == 1) {
-          tc_fence_before();
-          mbar_arrive(acce + 8 * s);
-        }
-#pragma unroll
-        for (int i = 0; i < 32; ++i) a[i] += sb1[32 * hh + i];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float h = prelu(a[i], sal1[32 * hh + i]);
-          const float4* wv = reinterpret_cast<const float4*>(sw2 + (32 * hh + i) * 12);
-          const float4 w0 = wv[0], w1 = wv[1], w2v = wv[2];
-          ffma2(e[0], e[1], w0.x, w0.y, h);
-          ffma2(e[2], e[3], w0.z, w0.w, h);
-          ffma2(e[4], e[5], w1.x, w1.y, h);
-          ffma2(e[6], e[7], w1.z, w1.w, h);
-          ffma2(e[8], e[9], w2v.x, w2v.y, h);
-          ffma2(e[10], e[11], w2v.z, w2v.w, h);
-        }
-        epi::store_bf16(a, scr, lane, m0 + q * 32, U, [&](int r) { return act1 + (int64_t)r * H2 + 32 * hh; });
-      }
-      if (row < U) {
-        float4* eo = reinterpret_cast<float4*>(emb + (int64_t)row * 12);
-        eo[0] = make_float4(e[0], e[1], e[2], e[3]);
-        eo[1] = make_float4(e[4], e[5], e[6], e[7]);
-        eo[2] = make_float4(e[8], e[9], e[10], e[11]);
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 128);
-}
-
-// ---------------------------------------------------------------------------
-// k_l12f_tile: the same forward with a 2-deep ring of whole 64-KB tiles
-// (DICM_L12F=tile; kept for A/B against the box ring)
-// ---------------------------------------------------------------------------
-constexpr uint32_t FT = 64 * 1024;  // a0 tile: 4 boxes x 128 rows x 128 B (bf16, SW128)
-constexpr size_t FT_SMEM = 1024 + 2 * FT + FW + 4 * FPAR + 128 + 4 * epi::SCRATCH_FLOATS * 4;
-
-__global__ void __launch_bounds__(F_THREADS, 1)
-    k_l12f_tile(const __grid_constant__ CUtensorMap tmA0, const float* __restrict__ al0, const float* __restrict__ w1,
            const float* __restrict__ b1, const float* __restrict__ al1, const float* __restrict__ w2,
            const float* __restrict__ b2, const int32_t* __restrict__ count, bf16* __restrict__ act1,
            float* __restrict__ emb) {
@@ -919,17 +737,13 @@ int grid_tiles(int64_t rows_max) {
 int fwd_layers12_bf16(const bf16* act0, const int32_t* count, int64_t rows_max, const float* al0, const float* w1,
                       const float* b1, const float* al1, const float* w2, const float* b2, bf16* act1, float* emb,
                       cudaStream_t st) {
-  static int once = smem_attr3(k_l12f, F_SMEM) | smem_attr3(k_l12f_tile, FT_SMEM);
+  static int once = smem_attr3(k_l12f, F_SMEM);
   if (once) return once;
   CUtensorMap ma;
   int rc = map2d(&ma, act0, true, rows_max, H1, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  static const bool tile_ring = getenv("DICM_L12F") && getenv("DICM_L12F")[0] == 't';
   const int probe_slot = probe_begin(DICM_PROBE_IMG_FWD_L12, st);
-  if (tile_ring)
-    k_l12f_tile<<<grid_tiles(rows_max), F_THREADS, FT_SMEM, st>>>(ma, al0, w1, b1, al1, w2, b2, count, act1, emb);
-  else
-    k_l12f<<<grid_tiles(rows_max), F_THREADS, F_SMEM, st>>>(ma, al0, w1, b1, al1, w2, b2, count, act1, emb);
+  k_l12f<<<grid_tiles(rows_max), F_THREADS, F_SMEM, st>>>(ma, al0, w1, b1, al1, w2, b2, count, act1, emb);
   probe_end(probe_slot, st);
   return last_launch("tcgen05 bf16 layers 1-2 forward");
 }

@@ -708,8 +708,7 @@ __device__ __forceinline__ void ref_contrib(const RefSrc& S, int64_t p, float (&
   }
 }
 
-constexpr int HOT_REFS = 128;    // keys with more references go to the block-wide reduction
-constexpr int SMALL_GROUP = 16;  // up to this many: sorted positions, fp32 sum in reference order
+constexpr int HOT_REFS = 32;  // more references: one block per key (k_ref_reduce_hot); 3..32: one warp (k_ref_reduce_mid)
 
 __device__ __forceinline__ void store_row12(float* p, const float (&v)[DICM_D]) {
   float4* q = reinterpret_cast<float4*>(p);
@@ -777,95 +776,79 @@ __device__ void fx_nonfinite(const RefSrc& S, const int32_t* __restrict__ order,
     if ((nf >> c) & 1u) r[c] = fs[c];
 }
 
-// out[u] = sum of the gradient rows of key u's references (thread per key;
-// keys with > HOT_REFS references are listed for k_ref_reduce_hot)
-template <int MINB>  // DICM_REDUCE_OCC: 2 (128 registers) or 3 blocks/SM (80 registers, the rare multi-reference path spills)
-__global__ void __launch_bounds__(256, MINB) k_ref_reduce(const __grid_constant__ RefSrc S, const int32_t* __restrict__ order,
-                                                    const int32_t* __restrict__ start,
-                                                    const int32_t* __restrict__ n_keys, int64_t cap,
-                                                    float* __restrict__ out, int32_t* __restrict__ hot_count,
-                                                    int32_t* __restrict__ hot_list) {
+// out[u] = sum of the gradient rows of key u's references in ascending
+// reference order (np.add.at's order).  Thread per key for up to two
+// references (nearly every image); keys with 3..32 references are listed for
+// k_ref_reduce_mid (a warp each), larger ones for k_ref_reduce_hot (a block).
+template <int MINB>  // DICM_REDUCE_OCC: 2 or 3 (default) resident blocks per SM
+__global__ void __launch_bounds__(256, MINB) k_ref_reduce(const __grid_constant__ RefSrc S,
+                                                          const int32_t* __restrict__ order,
+                                                          const int32_t* __restrict__ start,
+                                                          const int32_t* __restrict__ n_keys, int64_t cap,
+                                                          float* __restrict__ out, int32_t* __restrict__ counters,
+                                                          int32_t* __restrict__ hot_list,
+                                                          int32_t* __restrict__ mid_list) {
   const int64_t n = min((int64_t)*n_keys, cap);
   for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
     const int32_t s0 = __ldg(start + u), s1 = __ldg(start + u + 1);
     const int cnt = s1 - s0;
     if (cnt > HOT_REFS) {
-      hot_list[atomicAdd(hot_count, 1)] = (int32_t)u;
+      hot_list[atomicAdd(counters, 1)] = (int32_t)u;
       continue;
+    }
+    if (cnt > 2) {
+      mid_list[atomicAdd(counters + 1, 1)] = (int32_t)u;
+      continue;
+    }
+    int32_t p0 = __ldg(order + s0), p1 = cnt > 1 ? __ldg(order + s0 + 1) : INT_MAX;
+    if (p1 < p0) {
+      const int32_t x = p0;
+      p0 = p1;
+      p1 = x;
     }
     float r[DICM_D];
-    if (cnt <= 3) {  // most groups: a register sort of the positions, sum in reference order
-      int32_t p0 = __ldg(order + s0), p1 = cnt > 1 ? __ldg(order + s0 + 1) : INT_MAX,
-              p2 = cnt > 2 ? __ldg(order + s0 + 2) : INT_MAX;
-      if (p1 < p0) { const int32_t x = p0; p0 = p1; p1 = x; }
-      if (p2 < p1) { const int32_t x = p1; p1 = p2; p2 = x; }
-      if (p1 < p0) { const int32_t x = p0; p0 = p1; p1 = x; }
-      ref_contrib(S, p0, r);
-      if (cnt > 1) {
-        float v[DICM_D];
-        ref_contrib(S, p1, v);
+    ref_contrib(S, p0, r);
+    if (cnt > 1) {
+      float v[DICM_D];
+      ref_contrib(S, p1, v);
 #pragma unroll
-        for (int c = 0; c < DICM_D; ++c) r[c] += v[c];
-        if (cnt > 2) {
-          ref_contrib(S, p2, v);
-#pragma unroll
-          for (int c = 0; c < DICM_D; ++c) r[c] += v[c];
-        }
-      }
-      store_row12(out + u * DICM_D, r);
-      continue;
-    }
-    if (cnt <= SMALL_GROUP) {
-      // a handful of references: sort the positions (insertion sort) and sum
-      // in ascending reference order like np.add.at
-      int32_t pos[SMALL_GROUP];
-      for (int i = 0; i < cnt; ++i) {
-        const int32_t p = __ldg(order + s0 + i);
-        int j = i;
-        while (j > 0 && pos[j - 1] > p) {
-          pos[j] = pos[j - 1];
-          --j;
-        }
-        pos[j] = p;
-      }
-      ref_contrib(S, pos[0], r);
-      for (int i = 1; i < cnt; ++i) {
-        float v[DICM_D];
-        ref_contrib(S, pos[i], v);
-#pragma unroll
-        for (int c = 0; c < DICM_D; ++c) r[c] += v[c];
-      }
-      store_row12(out + u * DICM_D, r);
-      continue;
-    }
-    ref_contrib(S, __ldg(order + s0), r);
-    {
-      FixedAcc f;
-      fx_init(f);
-      fx_see(f, r);
-      for (int32_t j = s0 + 1; j < s1; ++j) {
-        float v[DICM_D];
-        ref_contrib(S, __ldg(order + j), v);
-        fx_see(f, v);
-      }
-      int sh[DICM_D];
-      long long q[DICM_D];
-#pragma unroll
-      for (int c = 0; c < DICM_D; ++c) {
-        sh[c] = fx_shift(f.mx[c], cnt);
-        q[c] = fx_quant(r[c], sh[c]);
-      }
-      for (int32_t j = s0 + 1; j < s1; ++j) {
-        float v[DICM_D];
-        ref_contrib(S, __ldg(order + j), v);
-#pragma unroll
-        for (int c = 0; c < DICM_D; ++c) q[c] += fx_quant(v[c], sh[c]);
-      }
-#pragma unroll
-      for (int c = 0; c < DICM_D; ++c) r[c] = fx_result(q[c], sh[c], f, c);
-      if (f.nf) fx_nonfinite(S, order, s0, s1, 1, f.nf, r);
+      for (int c = 0; c < DICM_D; ++c) r[c] += v[c];
     }
     store_row12(out + u * DICM_D, r);
+  }
+}
+
+// the keys with 3..32 references, a warp each: lane i takes reference i, its
+// rank by position (a 32-way compare), the rows land in rank order in shared
+// memory and lanes 0..11 sum their column in ascending reference order
+__global__ void __launch_bounds__(256) k_ref_reduce_mid(const __grid_constant__ RefSrc S,
+                                                        const int32_t* __restrict__ order,
+                                                        const int32_t* __restrict__ start,
+                                                        const int32_t* __restrict__ mid_count,
+                                                        const int32_t* __restrict__ mid_list,
+                                                        float* __restrict__ out) {
+  __shared__ float slots[8][32][DICM_D + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nm = *mid_count;
+  for (int w = blockIdx.x * 8 + warp; w < nm; w += gridDim.x * 8) {
+    const int32_t u = __ldg(mid_list + w);
+    const int32_t s0 = __ldg(start + u), cnt = __ldg(start + u + 1) - s0;
+    const int32_t p = lane < cnt ? __ldg(order + s0 + lane) : INT_MAX;
+    int rank = 0;
+    for (int j = 0; j < cnt; ++j) rank += __shfl_sync(FULL, p, j) < p;
+    if (lane < cnt) {
+      float v[DICM_D];
+      ref_contrib(S, p, v);
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) slots[warp][rank][c] = v[c];
+    }
+    __syncwarp();
+    if (lane < DICM_D) {
+      float acc = slots[warp][0][lane];
+      for (int i = 1; i < cnt; ++i) acc += slots[warp][i][lane];
+      out[(int64_t)u * DICM_D + lane] = acc;
+    }
+    __syncwarp();
   }
 }
 
@@ -1115,17 +1098,20 @@ static RefSrc id_src(const dicm_layout_t* L, const dicm_batch_view_t* V, const f
   return S;
 }
 
+// counters: [hot, mid] of this list; the lists have room for every key
 static void ref_reduce(const RefSrc& S, const int32_t* order, const int32_t* start, const int32_t* n_keys, int64_t cap,
-                       float* out, int32_t* hot_count, int32_t* hot_list, cudaStream_t st) {
+                       float* out, int32_t* counters, int32_t* hot_list, int32_t* mid_list, cudaStream_t st) {
   static const int occ = [] {
     const char* e = getenv("DICM_REDUCE_OCC");
     return e && e[0] == '2' ? 2 : 3;
   }();
   const int grid = dicm_grid(cap, 256, 148 * 16);
   if (occ == 2)
-    k_ref_reduce<2><<<grid, 256, 0, st>>>(S, order, start, n_keys, cap, out, hot_count, hot_list);
+    k_ref_reduce<2><<<grid, 256, 0, st>>>(S, order, start, n_keys, cap, out, counters, hot_list, mid_list);
   else
-    k_ref_reduce<3><<<grid, 256, 0, st>>>(S, order, start, n_keys, cap, out, hot_count, hot_list);
+    k_ref_reduce<3><<<grid, 256, 0, st>>>(S, order, start, n_keys, cap, out, counters, hot_list, mid_list);
+  k_ref_reduce_mid<<<148 * 4, 256, 0, st>>>(S, order, start, counters + 1, mid_list, out);
+  k_ref_reduce_hot<<<148, 256, 0, st>>>(S, order, start, counters, hot_list, out);
 }
 
 // every unique ID row's gradient (the hot-key counter bv->hot[1] must be
@@ -1133,10 +1119,10 @@ static void ref_reduce(const RefSrc& S, const int32_t* order, const int32_t* sta
 static void launch_id_reduce(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const float* d_head_in,
                              float* d_rows, cudaStream_t st) {
   if (layout->n_fields <= 0) return;
-  int32_t* hot_list_id = bv->hot + 2 + bv->img_cap;
+  int32_t* lists = bv->hot + 4;
   const RefSrc S = id_src(layout, bv, d_head_in);
-  ref_reduce(S, bv->id_order, bv->id_start, bv->n_id_keys, bv->id_cap, d_rows, bv->hot + 1, hot_list_id, st);
-  k_ref_reduce_hot<<<148, 256, 0, st>>>(S, bv->id_order, bv->id_start, bv->hot + 1, hot_list_id, d_rows);
+  ref_reduce(S, bv->id_order, bv->id_start, bv->n_id_keys, bv->id_cap, d_rows, bv->hot + 2,
+             lists + 2 * bv->img_cap, lists + 2 * bv->img_cap + bv->id_cap, st);
 }
 
 int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const dicm_attn_params_t* attn,
@@ -1171,7 +1157,8 @@ int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
   const int grid = bwd_grid(bv->batch);
   const int64_t stride = part_size(layout);
   const int probe_slot = probe_begin(DICM_PROBE_SAMPLE_BWD, st);
-  if (check_cuda(cudaMemsetAsync(bv->hot, 0, 2 * sizeof(int32_t), st), "sample_bwd hot counters")) return DICM_ERR_CUDA;
+  if (check_cuda(cudaMemsetAsync(bv->hot, 0, 4 * sizeof(int32_t), st), "sample_bwd list counters"))
+    return DICM_ERR_CUDA;
   if (attn_chan) {
     // partial row layout in sorted names: attn/id/* before attn/img/*; the
     // id channel writes each reference's dk row, the img channel adds to it
@@ -1188,11 +1175,10 @@ int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
     k_ref_rows<<<grid, BWD_WARPS * 32, 0, st>>>(a);
   }
   // every unique image row and ID row: its references summed in order
-  int32_t* hot_list_img = bv->hot + 2;
   if (layout->use_ad_image || layout->use_behavior_images) {
     const RefSrc S = image_src(layout, bv, d_head_in);
-    ref_reduce(S, bv->img_order, bv->img_start, bv->n_img_keys, bv->img_cap, d_emb, bv->hot, hot_list_img, st);
-    k_ref_reduce_hot<<<148, 256, 0, st>>>(S, bv->img_order, bv->img_start, bv->hot, hot_list_img, d_emb);
+    ref_reduce(S, bv->img_order, bv->img_start, bv->n_img_keys, bv->img_cap, d_emb, bv->hot, bv->hot + 4,
+               bv->hot + 4 + bv->img_cap, st);
   }
   if (d_rows) launch_id_reduce(layout, bv, d_head_in, d_rows, st);
   probe_end(probe_slot, st);

@@ -477,7 +477,7 @@ class StepEngine:
         own_rows = lay.use_behavior_images and lay.aggregator.kind != "sum"
         self.ref_grad = torch.empty((max(R, 1) if own_rows else 1, 12), **f32)
         self.q_grad = torch.empty((max(B, 1), 36), **f32)
-        self.hot = torch.empty(2 + max(self.cap_u, 1) + max(self.cap_k, 1), **i32)
+        self.hot = torch.empty(4 + 2 * (max(self.cap_u, 1) + max(self.cap_k, 1)), **i32)
         self.ws_tr_img = _u8(L.lib.dicm_ref_transpose_workspace(n_img, max(self.cap_u, 1)), dev)
         self.ws_tr_id = _u8(L.lib.dicm_ref_transpose_workspace(n_id, max(self.cap_k, 1)), dev)
         self._alloc_image_net(self.cap_u)
