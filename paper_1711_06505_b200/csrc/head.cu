@@ -25,7 +25,7 @@ __host__ __device__ inline int64_t part_size(int W) {
 }
 
 struct Smem {
-  float w0[H0 * MAXW];  // mlp/0/w [128][W]
+  float w0[H0 * (MAXW + 1)];  // mlp/0/w [128][W] at an odd row stride (conflict-free column reads)
   float w1[H1 * H0];    // mlp/1/w [64][128]
   float xs[MAXW][BT];   // x^T
   float a0[H0][BT];     // layer-0 pre-activation^T
@@ -78,8 +78,9 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
   const int t = threadIdx.x;
   const int b0 = blockIdx.x * BT;
   const int nb = min(BT, B - b0);
+  const int WS = W | 1;  // shared-memory row stride of w0: odd, so a warp reading one column hits 32 banks
   if (!WIDE) {
-    for (int i = t; i < H0 * W; i += THREADS) s.w0[i] = p.w0[i];
+    for (int i = t; i < H0 * W; i += THREADS) s.w0[(i / W) * WS + i % W] = p.w0[i];
     for (int i = t; i < BT * W; i += THREADS) {
       const int r = i / W, c = i % W;
       s.xs[c][r] = r < nb ? x[(int64_t)(b0 + r) * W + c] : 0.f;
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
 #pragma unroll
     for (int r = 0; r < HB; ++r) acc[r] = bj;
     for (int k = 0; k < W; ++k) {
-      const float w = s.w0[j * W + k];
+      const float w = s.w0[j * WS + k];
       float xv[HB];
       loadn<HB>(&s.xs[k][h * HB], xv);
 #pragma unroll
@@ -254,19 +255,23 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
     }
     return;
   }
-  // dW0[k][c] = sum_r da0[r][k] x[r][c]: thread = (k, half of the columns)
+  // dW0[k][c] = sum_r da0[r][k] x[r][c]: thread = (column c, half of the k
+  // range), so each k writes one coalesced partial row; da0[k] is a broadcast
   {
-    const int k = t & (H0 - 1), h = t >> 7;
-    const int c0 = h * ((W + 1) / 2), c1 = h ? W : (W + 1) / 2;
-    float d[BT];
-    load32(s.da0[k], d);
-    for (int c = c0; c < c1; ++c) {
+    const int per = (THREADS / 2 >= W) ? THREADS / 2 : THREADS;  // W <= 128: two k-halves
+    const int c = t % per, h = t / per;
+    if (c < W) {
       float xv[BT];
       load32(s.xs[c], xv);
-      float acc = 0.f;
+      const int k0 = per == THREADS ? 0 : h * (H0 / 2), k1 = per == THREADS ? H0 : k0 + H0 / 2;
+      for (int k = k0; k < k1; ++k) {
+        float d[BT];
+        load32(s.da0[k], d);
+        float acc = 0.f;
 #pragma unroll
-      for (int r = 0; r < BT; ++r) acc = fmaf(d[r], xv[r], acc);
-      out[o_w0 + (int64_t)k * W + c] = acc;
+        for (int r = 0; r < BT; ++r) acc = fmaf(d[r], xv[r], acc);
+        out[o_w0 + (int64_t)k * W + c] = acc;
+      }
     }
   }
   // dx[r][c] = sum_k da0[r][k] W0[k][c]: thread = (column c, half of the tile)
@@ -277,7 +282,7 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
 #pragma unroll
       for (int r = 0; r < HB; ++r) acc[r] = 0.f;
       for (int k = 0; k < H0; ++k) {
-        const float w = s.w0[k * W + c];
+        const float w = s.w0[k * WS + c];
         float d[HB];
         loadn<HB>(&s.da0[k][h * HB], d);
 #pragma unroll
