@@ -708,7 +708,53 @@ __device__ __forceinline__ void ref_contrib(const RefSrc& S, int64_t p, float (&
   }
 }
 
-constexpr int HOT_REFS = 32;  // more references: one block per key (k_ref_reduce_hot); 3..32: one warp (k_ref_reduce_mid)
+constexpr int HOT_REFS = 32;    // more references: one block per key (k_ref_reduce_hot)
+constexpr int THREAD_REFS = 16;  // up to this many: one thread (sorting network); 17..32: one warp (k_ref_reduce_mid)
+
+// ascending sort of N positions held in registers (bitonic network, every
+// index a compile-time constant after unrolling)
+template <int N>
+__device__ __forceinline__ void sort_net(int32_t (&a)[N]) {
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const int32_t x = a[i], y = a[l];
+          const bool sw = ((i & k) == 0) ? (x > y) : (x < y);
+          a[i] = sw ? y : x;
+          a[l] = sw ? x : y;
+        }
+      }
+}
+
+// a group of 3..N references by one thread: positions sorted in registers,
+// rows fetched two at a time and summed in ascending reference order
+template <int N>
+__device__ __forceinline__ void thread_group(const RefSrc& S, const int32_t* __restrict__ order, int32_t s0, int cnt,
+                                             float (&r)[DICM_D]) {
+  int32_t p[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) p[i] = i < cnt ? __ldg(order + s0 + i) : INT_MAX;
+  sort_net<N>(p);
+  ref_contrib(S, p[0], r);
+#pragma unroll
+  for (int i = 1; i < N; i += 2) {
+    if (i >= cnt) break;
+    float v0[DICM_D], v1[DICM_D];
+    ref_contrib(S, p[i], v0);
+    const bool two = i + 1 < cnt;
+    if (two) ref_contrib(S, p[i + 1], v1);
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) r[c] += v0[c];
+    if (two)
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) r[c] += v1[c];
+  }
+}
 
 __device__ __forceinline__ void store_row12(float* p, const float (&v)[DICM_D]) {
   float4* q = reinterpret_cast<float4*>(p);
@@ -777,9 +823,10 @@ __device__ void fx_nonfinite(const RefSrc& S, const int32_t* __restrict__ order,
 }
 
 // out[u] = sum of the gradient rows of key u's references in ascending
-// reference order (np.add.at's order).  Thread per key for up to two
-// references (nearly every image); keys with 3..32 references are listed for
-// k_ref_reduce_mid (a warp each), larger ones for k_ref_reduce_hot (a block).
+// reference order (np.add.at's order).  Thread per key for up to 16
+// references (positions sorted in registers); keys with 17..32 references
+// are listed for k_ref_reduce_mid (a warp each), larger ones for
+// k_ref_reduce_hot (a block, exact fixed point).
 template <int MINB>  // DICM_REDUCE_OCC: 2 or 3 (default) resident blocks per SM
 __global__ void __launch_bounds__(256, MINB) k_ref_reduce(const __grid_constant__ RefSrc S,
                                                           const int32_t* __restrict__ order,
@@ -796,8 +843,19 @@ __global__ void __launch_bounds__(256, MINB) k_ref_reduce(const __grid_constant_
       hot_list[atomicAdd(counters, 1)] = (int32_t)u;
       continue;
     }
-    if (cnt > 2) {
+    if (cnt > THREAD_REFS) {
       mid_list[atomicAdd(counters + 1, 1)] = (int32_t)u;
+      continue;
+    }
+    if (cnt > 2) {
+      float r[DICM_D];
+      if (cnt <= 4)
+        thread_group<4>(S, order, s0, cnt, r);
+      else if (cnt <= 8)
+        thread_group<8>(S, order, s0, cnt, r);
+      else
+        thread_group<16>(S, order, s0, cnt, r);
+      store_row12(out + u * DICM_D, r);
       continue;
     }
     int32_t p0 = __ldg(order + s0), p1 = cnt > 1 ? __ldg(order + s0 + 1) : INT_MAX;
@@ -818,7 +876,7 @@ __global__ void __launch_bounds__(256, MINB) k_ref_reduce(const __grid_constant_
   }
 }
 
-// the keys with 3..32 references, a warp each: lane i takes reference i, its
+// the keys with 17..32 references, a warp each: lane i takes reference i, its
 // rank by position (a 32-way compare), the rows land in rank order in shared
 // memory and lanes 0..11 sum their column in ascending reference order
 __global__ void __launch_bounds__(256) k_ref_reduce_mid(const __grid_constant__ RefSrc S,
