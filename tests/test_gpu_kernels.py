@@ -149,3 +149,27 @@ def test_counter_based_table_init_is_rank_invariant():
         assert torch.count_nonzero(t[len(mine):]) == 0
     x = full.double()
     assert abs(x.mean().item()) < 1e-3 and abs(x.std().item() - 0.05) < 1e-3
+
+
+@pytest.mark.parametrize("n,keys", [(1, 1), (1000, 7), (823_296, 561_000), (200_000, 50)])
+def test_ref_transpose_groups_every_reference_under_its_key(n, keys):
+    """dicm_ref_transpose (counting sort of a dedup inverse): start[] is the
+    exclusive prefix of the per-key counts, start[k] = n past the last key,
+    and each group holds exactly its key's positions (any order)."""
+    from paper_1711_06505_b200 import _lib as L
+    rng = np.random.default_rng(n)
+    inv = rng.integers(0, keys, n).astype(np.int32)
+    inv[:min(keys, n)] = np.arange(min(keys, n))  # every key present
+    cap = keys + 17
+    d_inv = torch.as_tensor(inv, device="cuda")
+    order = torch.full((n,), -1, dtype=torch.int32, device="cuda")
+    start = torch.full((cap + 1,), -1, dtype=torch.int32, device="cuda")
+    ws = torch.empty(L.lib.dicm_ref_transpose_workspace(n, cap), dtype=torch.uint8, device="cuda")
+    L.check(L.lib.dicm_ref_transpose(d_inv.data_ptr(), n, cap, ws.data_ptr(), ws.numel(), order.data_ptr(),
+                                     start.data_ptr(), L.stream_handle()))
+    o, st = order.cpu().numpy(), start.cpu().numpy()
+    counts = np.bincount(inv, minlength=cap)
+    assert np.array_equal(st[:cap], np.concatenate([[0], np.cumsum(counts)[:-1]]))
+    assert st[cap] == n
+    assert np.array_equal(np.sort(o), np.arange(n))
+    assert np.array_equal(inv[o], np.repeat(np.arange(cap), counts))
