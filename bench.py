@@ -496,6 +496,7 @@ def main():
     ms = start.elapsed_time(end) if not flush else sum(a.elapsed_time(b) for a, b in evs[:args.steps])
     eng.raise_status()
     if os.environ.get("DICM_PHASE_TIMING") == "1" and hasattr(eng, "phase_times"):
+        barrier()  # the ranks start the timed eager step together
         step(staged[-1], eager=True)
         pt = eng.phase_times()
         if rank == 0:

@@ -165,6 +165,7 @@ class PeerExchange:
             off += (int(nbytes) + 255) // 256 * 256
 
         take("flags", 64 * 4)
+        take("flags_side", 64 * 4)  # the barriers of the forked stream (their own epoch counter)
         take("cmat", world * world * 2 * 4)
         take("recv_img", self.cap_ri * 4)
         take("recv_id", self.cap_rk * 4)
@@ -220,6 +221,11 @@ class PeerExchange:
         its sum over every rank, in rank order (bit-identical replicas)."""
         L.check(L.lib.dicm_p2p_allreduce(C.byref(self.peers), buf.data_ptr(), self.dense_n, self.off["grad_stage"],
                                          self.off["grad_sum"], self.off["flags"], status, buf.data_ptr(), s))
+
+    def barrier_side(self, status, s):
+        """A barrier on the forked stream: its own flag slots and epoch
+        counter, so it may run concurrently with the main stream's barriers."""
+        L.check(L.lib.dicm_p2p_barrier(C.byref(self.peers), self.off["flags_side"], 0, status, s))
 
     def barrier(self, status, s):
         # epoch 0: the kernel advances a device-side counter (CUDA-graph safe)
@@ -568,22 +574,20 @@ class ClusterEngine(StepEngine):
         L.check(L.lib.dicm_permute_rows12(px.back_id.data_ptr(), self.perm_id.data_ptr(), cnt[1:].data_ptr(),
                                           self.cap_k, 0, self.id_rows.data_ptr(), s))
         self._mark("rows back")
-        # (4) local pooling + head (the partial reduces wait for step 6)
-        self._local_step(self.emb_l, self.d_emb_l, denom, reduce=False)
+        # (4) local pooling + head (the partial reduces and the ID-row sums wait)
+        self._local_step(self.emb_l, self.d_emb_l, denom, reduce=False, id_rows=False)
         self._mark("pooling+head")
-        # (5) gradients to the owners (C4, C5); owners reduce in ascending source order
-        L.check(L.lib.dicm_permute_rows12(self.d_emb_l.data_ptr(), self.perm_img.data_ptr(), cnt.data_ptr(),
-                                          self.cap_u, 1, self.rows_buf.data_ptr(), s))
-        L.check(L.lib.dicm_permute_rows12(self.d_rows.data_ptr(), self.perm_id.data_ptr(), cnt[1:].data_ptr(),
-                                          self.cap_k, 1, self.push_out_id.data_ptr(), s))
-        px.scatter(0, 0, self.rows_buf.data_ptr(), 48, "push_img", s)
-        px.scatter(1, 0, self.push_out_id.data_ptr(), 48, "push_id", s)
-        px.barrier(st, s)
-        self._mark("grads to owners")
 
-        # (6) on the branch: the owner's ID-row gradients and the head /
-        # attention partial reduces; on the main stream the image-MLP backward
-        def id_grads_and_partials(ss):
+        # (5b, 6b) on the branch: this rank's ID-row sums, their push to the
+        # owners (C5) and a barrier on the branch's own flags, then the owner's
+        # ID-row reduction in ascending source order (runtime.py:208-219), the
+        # finite check and the head / attention partial reduces
+        def id_chain_bwd(ss):
+            self._id_row_grads(ss)
+            L.check(L.lib.dicm_permute_rows12(self.d_rows.data_ptr(), self.perm_id.data_ptr(), cnt[1:].data_ptr(),
+                                              self.cap_k, 1, self.push_out_id.data_ptr(), ss))
+            px.scatter(1, 0, self.push_out_id.data_ptr(), 48, "push_id", ss)
+            px.barrier_side(st, ss)
             L.check(L.lib.dicm_dedup_devn(px.recv_id.data_ptr(), self.cnt_dev[1:].data_ptr(), px.cap_rk,
                                           self.local_id_space, self.ws_id_owner.data_ptr(), self.ws_id_owner.numel(),
                                           self.uniq_id_o.data_ptr(), self.inv_id_o.data_ptr(), cnt[3:].data_ptr(), 3,
@@ -595,10 +599,17 @@ class ClusterEngine(StepEngine):
                                             st, ss))
             self._reduce_partials(ss)
 
+        on_side(id_chain_bwd)
+        # (5a, 6a) main stream: image gradients to the owners (C4), barrier, the
+        # owner's reduction in ascending source order, the image-MLP backward
+        L.check(L.lib.dicm_permute_rows12(self.d_emb_l.data_ptr(), self.perm_img.data_ptr(), cnt.data_ptr(),
+                                          self.cap_u, 1, self.rows_buf.data_ptr(), s))
+        px.scatter(0, 0, self.rows_buf.data_ptr(), 48, "push_img", s)
+        px.barrier(st, s)
+        self._mark("grads to owners")
         L.check(L.lib.dicm_owner_reduce_rows12(px.push_img.data_ptr(), self.inv_o.data_ptr(),
                                                self.segs_img.data_ptr(), G, px.cap_ri, cnt[2:].data_ptr(),
                                                self.cap_o, self.idx_ws_img.data_ptr(), self.net.d_emb.data_ptr(), s))
-        on_side(id_grads_and_partials)
         self._image_backward(self.net, self.uniq_o, cnt[2:].data_ptr(), self.cap_o if self.n_img_segs else 0)
         join()
         self._rows_checked = True
