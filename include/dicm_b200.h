@@ -193,7 +193,13 @@ typedef struct {
   float* ref_grad;              /* attn / max / concat: [R, 12] scratch, gradient per behavior reference */
   float* q_grad;                /* attn: [B, 36] scratch, query gradients (ad image 12 | ID query fields 24) */
   int32_t* hot;                 /* [4 + 2 (img_cap + id_cap)] scratch: work lists of keys with many references */
+  void* hot_acc;                /* dicm_hot_acc_bytes() scratch, zeroed once at allocation (the kernels leave
+                                   it ready for the next step): per-key accumulators that spread a key with
+                                   thousands of references (Zipf keys) over every SM; NULL = one block per key */
 } dicm_batch_view_t;
+
+/* Bytes of the batch view's hot_acc scratch (both key lists). */
+size_t dicm_hot_acc_bytes(void);
 
 /* Transpose of a dedup inverse (inv[p] = key of reference p, keys < key_cap):
  * order[] = 0..n-1 grouped by key (any order inside a group), start[k] = first

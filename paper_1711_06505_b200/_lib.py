@@ -84,7 +84,8 @@ class BatchView(C.Structure):
                 ("field_inv", P * 8), ("ad_local", P), ("beh_local", P), ("beh_off", P), ("emb", P),
                 ("img_order", P), ("img_start", P), ("id_order", P), ("id_start", P), ("field_ref_begin", I64 * 8),
                 ("beh_seg", P), ("field_seg", P * 8), ("n_img_keys", P), ("n_id_keys", P), ("img_cap", I64),
-                ("id_cap", I64), ("ref_grad", P), ("q_grad", P), ("hot", P)]
+                ("id_cap", I64), ("ref_grad", P), ("q_grad", P), ("hot", P),
+                ("hot_acc", P)]
 
 
 class AttnParams(C.Structure):
@@ -146,6 +147,7 @@ _sig("dicm_imgmlp_bwd", C.c_int, P, C.c_int, C.c_int, P, P, I64, C.POINTER(ImgMl
      C.POINTER(ImgMlpGrads), C.c_int, P, S, ST)
 _sig("dicm_attn_partial_size", I64, C.POINTER(Layout))
 _sig("dicm_ref_transpose_workspace", S, I64, I64)
+_sig("dicm_hot_acc_bytes", S)
 _sig("dicm_ref_transpose", C.c_int, P, I64, I64, P, S, P, P, ST)
 _sig("dicm_csr_segments", C.c_int, P, C.c_int, P, ST)
 _sig("dicm_id_row_grads", C.c_int, C.POINTER(Layout), C.POINTER(BatchView), P, P, ST)
@@ -219,7 +221,7 @@ EXPORTED = [
     "dicm_owner_reduce_rows12", "dicm_probe_enable", "dicm_probe_read",
     "dicm_p2p_alloc", "dicm_p2p_free", "dicm_ipc_handle", "dicm_ipc_open", "dicm_ipc_close", "dicm_p2p_barrier",
     "dicm_p2p_counts", "dicm_p2p_plan", "dicm_p2p_scatter", "dicm_dedup_devn", "dicm_head_fwd",
-    "dicm_ref_transpose_workspace", "dicm_ref_transpose", "dicm_csr_segments", "dicm_table_init", "dicm_id_row_grads", "dicm_p2p_allreduce", "dicm_fields_fwd", "dicm_images_fwd", "dicm_jsonl_parse", "dicm_jsonl_list_total", "dicm_jsonl_export", "dicm_jsonl_free",
+    "dicm_ref_transpose_workspace", "dicm_hot_acc_bytes", "dicm_ref_transpose", "dicm_csr_segments", "dicm_table_init", "dicm_id_row_grads", "dicm_p2p_allreduce", "dicm_fields_fwd", "dicm_images_fwd", "dicm_jsonl_parse", "dicm_jsonl_list_total", "dicm_jsonl_export", "dicm_jsonl_free",
     "dicm_towers_blocks", "dicm_towers_fwd_bwd", "dicm_towers_fwd", "dicm_head_wide_workspace",
     "dicm_head_wide_fwd_bwd", "dicm_head_wide_fwd", "dicm_host_pack", "dicm_zero_async",
 ]

@@ -766,29 +766,23 @@ __device__ __forceinline__ void store_row12(float* p, const float (&v)[DICM_D]) 
 // Exact, order-independent sums.  A key's references come in no particular
 // order (the counting-sort transpose fills groups through atomic cursors), so
 // each component is summed in 64-bit fixed point: scale 2^shift chosen from
-// the group's largest |value| (max is order-independent) and count so that
-// the integer sum cannot overflow; integer addition is associative, hence the
-// same bits whatever the order, and the sum is exact up to the per-term
-// rounding at 2^-shift (far below fp32's).  A non-finite component falls back
-// to the fp32 sum, whose inf/nan outcome is order-independent too.
-struct FixedAcc {
-  float mx[DICM_D];
-  unsigned nf;  // bit c: component c saw a non-finite value
-};
+// the group's largest finite |value| (max is order-independent) and count so
+// that the integer sum cannot overflow; integer addition is associative, hence
+// the same bits whatever the order (or however the group is split over
+// threads and blocks), and the sum is exact up to the per-term rounding at
+// 2^-shift (far below fp32's).  Non-finite components are tracked as flags:
+// any nan, or both infinities -> nan, else the infinity's sign -- the outcome
+// of the fp32 sum in every order.
+constexpr int FL_POS = 16, FL_NEG = 32;  // flag bits: c nan, FL_POS + c +inf, FL_NEG + c -inf
 
-__device__ __forceinline__ void fx_init(FixedAcc& f) {
-#pragma unroll
-  for (int c = 0; c < DICM_D; ++c) f.mx[c] = 0.f;
-  f.nf = 0;
+__device__ __forceinline__ unsigned long long fx_flags(float v, int c) {
+  if (isnan(v)) return 1ull << c;
+  if (isinf(v)) return 1ull << ((v > 0.f ? FL_POS : FL_NEG) + c);
+  return 0ull;
 }
 
-__device__ __forceinline__ void fx_see(FixedAcc& f, const float (&v)[DICM_D]) {
-#pragma unroll
-  for (int c = 0; c < DICM_D; ++c) {
-    if (!isfinite(v[c])) f.nf |= 1u << c;
-    f.mx[c] = fmaxf(f.mx[c], fabsf(v[c]));
-  }
-}
+// max(|v|) over the finite values as float bits (non-negative floats order like their bits)
+__device__ __forceinline__ unsigned fx_bits(float v) { return isfinite(v) ? __float_as_uint(fabsf(v)) : 0u; }
 
 __device__ __forceinline__ int fx_shift(float mx, int n) {
   int e;
@@ -797,36 +791,44 @@ __device__ __forceinline__ int fx_shift(float mx, int n) {
   return 62 - e - lg;
 }
 
-__device__ __forceinline__ long long fx_quant(float v, int shift) { return __double2ll_rn(ldexp((double)v, shift)); }
+__device__ __forceinline__ long long fx_quant(float v, int shift) {
+  return isfinite(v) ? __double2ll_rn(ldexp((double)v, shift)) : 0ll;
+}
 
-__device__ __forceinline__ float fx_result(long long q, int shift, const FixedAcc& f, int c) {
-  if (f.mx[c] == 0.f) return 0.f;
+__device__ __forceinline__ float fx_result(long long q, int shift, float mx, unsigned long long fl, int c) {
+  const bool nan = (fl >> c) & 1ull, pos = (fl >> (FL_POS + c)) & 1ull, neg = (fl >> (FL_NEG + c)) & 1ull;
+  if (nan || (pos && neg)) return __int_as_float(0x7fffffff);
+  if (pos) return __int_as_float(0x7f800000);
+  if (neg) return __int_as_float(0xff800000);
+  if (mx == 0.f) return 0.f;
   return (float)ldexp((double)q, -shift);  // exact scaling of the (53-bit rounded) sum, then fp32 rounding
 }
 
-// a group with a non-finite component (rare): the plain fp32 sum of that
-// component -- inf / nan outcomes do not depend on the order
-__device__ void fx_nonfinite(const RefSrc& S, const int32_t* __restrict__ order, int32_t j0, int32_t j1,
-                             int32_t step, unsigned nf, float (&r)[DICM_D]) {
-  float fs[DICM_D];
-#pragma unroll
-  for (int c = 0; c < DICM_D; ++c) fs[c] = 0.f;
-  for (int32_t j = j0; j < j1; j += step) {
-    float v[DICM_D];
-    ref_contrib(S, __ldg(order + j), v);
-#pragma unroll
-    for (int c = 0; c < DICM_D; ++c) fs[c] += v[c];
-  }
-#pragma unroll
-  for (int c = 0; c < DICM_D; ++c)
-    if ((nf >> c) & 1u) r[c] = fs[c];
-}
+// Keys with more than HOT_REFS references.  The first HOT_SLOTS listed keys
+// get accumulators (dicm_batch_view_t.hot_acc) and are split into chunks of
+// HOT_CHUNK references spread over every block: k_ref_hot_max forms each
+// key's maxima and flags, k_ref_reduce_hot its fixed-point sums (integer
+// atomics: exact, so the split does not change a bit), and the last block to
+// finish writes the rows.  Keys past HOT_SLOTS (or every key without
+// accumulators) are summed one block each with the same arithmetic.
+constexpr int HOT_SLOTS = 4096;
+constexpr int HOT_CHUNK = 256;  // = block size: one reference per thread
+struct HotEnt {
+  int32_t u, s0, cnt, pad;
+};
+struct HotAcc {  // one key list's accumulators
+  unsigned done, pad[3];
+  HotEnt ent[HOT_SLOTS];
+  unsigned mx[HOT_SLOTS][DICM_D];
+  unsigned long long fl[HOT_SLOTS];
+  long long q[HOT_SLOTS][DICM_D];
+};
 
 // out[u] = sum of the gradient rows of key u's references in ascending
 // reference order (np.add.at's order).  Thread per key for up to 16
 // references (positions sorted in registers); keys with 17..32 references
-// are listed for k_ref_reduce_mid (a warp each), larger ones for
-// k_ref_reduce_hot (a block, exact fixed point).
+// are listed for k_ref_reduce_mid (a warp each), larger ones for the hot-key
+// passes (exact fixed point).
 template <int MINB>  // DICM_REDUCE_OCC: 2 or 3 (default) resident blocks per SM
 __global__ void __launch_bounds__(256, MINB) k_ref_reduce(const __grid_constant__ RefSrc S,
                                                           const int32_t* __restrict__ order,
@@ -834,13 +836,23 @@ __global__ void __launch_bounds__(256, MINB) k_ref_reduce(const __grid_constant_
                                                           const int32_t* __restrict__ n_keys, int64_t cap,
                                                           float* __restrict__ out, int32_t* __restrict__ counters,
                                                           int32_t* __restrict__ hot_list,
-                                                          int32_t* __restrict__ mid_list) {
+                                                          int32_t* __restrict__ mid_list, HotAcc* __restrict__ acc) {
   const int64_t n = min((int64_t)*n_keys, cap);
   for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
     const int32_t s0 = __ldg(start + u), s1 = __ldg(start + u + 1);
     const int cnt = s1 - s0;
     if (cnt > HOT_REFS) {
-      hot_list[atomicAdd(counters, 1)] = (int32_t)u;
+      const int h = atomicAdd(counters, 1);
+      hot_list[h] = (int32_t)u;
+      if (acc && h < HOT_SLOTS) {  // this key's accumulator slot, cleared for the chunk passes
+        acc->ent[h] = HotEnt{(int32_t)u, s0, cnt, 0};
+#pragma unroll
+        for (int c = 0; c < DICM_D; ++c) {
+          acc->mx[h][c] = 0u;
+          acc->q[h][c] = 0ll;
+        }
+        acc->fl[h] = 0ull;
+      }
       continue;
     }
     if (cnt > THREAD_REFS) {
@@ -910,81 +922,217 @@ __global__ void __launch_bounds__(256) k_ref_reduce_mid(const __grid_constant__ 
   }
 }
 
-// the listed keys, one block each: per-thread partial maxima / fixed-point
-// sums over references t, t + 256, ..., combined in shared memory (the
-// integer sums are associative, the maxima order-independent)
+// one hot key by one block (keys without an accumulator slot): per-thread
+// partial maxima / flags / fixed-point sums over references t, t + 256, ...,
+// combined in shared memory (integer sums associative, maxima and flags
+// order-independent)
+__device__ void hot_block(const RefSrc& S, const int32_t* __restrict__ order, int32_t u, int32_t s0, int32_t s1,
+                          float* __restrict__ out) {
+  __shared__ unsigned smx[8][DICM_D];
+  __shared__ unsigned long long sfl[8];
+  __shared__ long long sq[8][DICM_D];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  unsigned m[DICM_D];
+  unsigned long long fl = 0;
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) m[c] = 0u;
+  for (int32_t j = s0 + t; j < s1; j += 256) {
+    float v[DICM_D];
+    ref_contrib(S, __ldg(order + j), v);
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) {
+      m[c] = max(m[c], fx_bits(v[c]));
+      fl |= fx_flags(v[c], c);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) m[c] = __reduce_max_sync(FULL, m[c]);
+  fl = ((unsigned long long)__reduce_or_sync(FULL, (unsigned)(fl >> 32)) << 32) | __reduce_or_sync(FULL, (unsigned)fl);
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) smx[warp][c] = m[c];
+    sfl[warp] = fl;
+  }
+  __syncthreads();
+  int sh[DICM_D];
+  long long q[DICM_D];
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c) {
+    unsigned mm = 0u;
+    for (int w = 0; w < 8; ++w) mm = max(mm, smx[w][c]);
+    sh[c] = fx_shift(__uint_as_float(mm), s1 - s0);
+    q[c] = 0;
+  }
+  fl = 0;
+  for (int w = 0; w < 8; ++w) fl |= sfl[w];
+  for (int32_t j = s0 + t; j < s1; j += 256) {
+    float v[DICM_D];
+    ref_contrib(S, __ldg(order + j), v);
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) q[c] += fx_quant(v[c], sh[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < DICM_D; ++c)
+    for (int o = 16; o > 0; o >>= 1) q[c] += __shfl_down_sync(FULL, q[c], o);
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) sq[warp][c] = q[c];
+  __syncthreads();
+  if (t < DICM_D) {  // component t (register arrays stay compile-time indexed)
+    long long tot = 0;
+    unsigned mm = 0u;
+    for (int w = 0; w < 8; ++w) {
+      tot += sq[w][t];
+      mm = max(mm, smx[w][t]);
+    }
+    const float mx = __uint_as_float(mm);
+    out[(int64_t)u * DICM_D + t] = fx_result(tot, fx_shift(mx, s1 - s0), mx, fl, t);
+  }
+  __syncthreads();
+}
+
+// chunk offsets of the slotted hot keys (every block forms the same scan in
+// shared memory); returns the number of chunks
+__device__ int hot_chunks(const HotAcc* __restrict__ acc, int nh, int* off) {
+  constexpr int PER = HOT_SLOTS / 256;
+  __shared__ int part[256];
+  const int t = threadIdx.x;
+  int c[PER], sum = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int h = t * PER + k;
+    c[k] = h < nh ? (acc->ent[h].cnt + HOT_CHUNK - 1) / HOT_CHUNK : 0;
+    sum += c[k];
+  }
+  part[t] = sum;
+  __syncthreads();
+  for (int d = 1; d < 256; d <<= 1) {  // inclusive scan of the per-thread sums
+    const int x = t >= d ? part[t - d] : 0;
+    __syncthreads();
+    part[t] += x;
+    __syncthreads();
+  }
+  int run = part[t] - sum;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    off[t * PER + k] = run;
+    run += c[k];
+  }
+  if (t == 255) off[HOT_SLOTS] = part[255];
+  __syncthreads();
+  return off[HOT_SLOTS];
+}
+
+// the slot owning chunk g: the last h with off[h] <= g
+__device__ __forceinline__ int hot_slot_of(const int* off, int nh, int g) {
+  int lo = 0, hi = nh - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= g)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+// pass 1 over the chunks: each slot's maxima and non-finite flags
+__global__ void __launch_bounds__(256) k_ref_hot_max(const __grid_constant__ RefSrc S,
+                                                     const int32_t* __restrict__ order,
+                                                     const int32_t* __restrict__ hot_count, HotAcc* __restrict__ acc) {
+  __shared__ int off[HOT_SLOTS + 1];
+  const int nh = min(*hot_count, HOT_SLOTS);
+  if (nh == 0) return;
+  const int total = hot_chunks(acc, nh, off);
+  const int t = threadIdx.x, lane = t & 31;
+  for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    const int h = hot_slot_of(off, nh, g);
+    const HotEnt e = acc->ent[h];
+    const int32_t j = e.s0 + (g - off[h]) * HOT_CHUNK + t;
+    unsigned m[DICM_D];
+    unsigned long long fl = 0;
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) m[c] = 0u;
+    if (j < e.s0 + e.cnt) {
+      float v[DICM_D];
+      ref_contrib(S, __ldg(order + j), v);
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c) {
+        m[c] = fx_bits(v[c]);
+        fl |= fx_flags(v[c], c);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) m[c] = __reduce_max_sync(FULL, m[c]);
+    fl = ((unsigned long long)__reduce_or_sync(FULL, (unsigned)(fl >> 32)) << 32) |
+         __reduce_or_sync(FULL, (unsigned)fl);
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < DICM_D; ++c)
+        if (m[c]) atomicMax(&acc->mx[h][c], m[c]);
+      if (fl) atomicOr(&acc->fl[h], fl);
+    }
+  }
+}
+
+// pass 2: the keys without a slot one block each, then each slot's
+// fixed-point sums over the chunks; the last block to finish writes the rows
+// of the slotted keys and re-arms the done counter
 __global__ void __launch_bounds__(256) k_ref_reduce_hot(const __grid_constant__ RefSrc S,
                                                         const int32_t* __restrict__ order,
                                                         const int32_t* __restrict__ start,
                                                         const int32_t* __restrict__ hot_count,
-                                                        const int32_t* __restrict__ hot_list,
+                                                        const int32_t* __restrict__ hot_list, HotAcc* __restrict__ acc,
                                                         float* __restrict__ out) {
-  __shared__ union {
-    float mx[256][DICM_D + 1];
-    long long q[256][DICM_D + 1];
-  } red;
-  __shared__ unsigned snf[256];
-  __shared__ float smx[DICM_D];
-  const int t = threadIdx.x;
-  const int nh = *hot_count;
-  for (int h = blockIdx.x; h < nh; h += gridDim.x) {
+  __shared__ int off[HOT_SLOTS + 1];
+  __shared__ bool last;
+  const int n_hot = *hot_count;
+  const int first = acc ? min(n_hot, HOT_SLOTS) : 0;
+  for (int h = first + blockIdx.x; h < n_hot; h += gridDim.x) {
     const int32_t u = hot_list[h];
-    const int32_t s0 = start[u], s1 = start[u + 1];
-    FixedAcc f;
-    fx_init(f);
-    for (int32_t j = s0 + t; j < s1; j += 256) {
-      float v[DICM_D];
-      ref_contrib(S, __ldg(order + j), v);
-      fx_see(f, v);
-    }
-#pragma unroll
-    for (int c = 0; c < DICM_D; ++c) red.mx[t][c] = f.mx[c];
-    snf[t] = f.nf;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {  // fixed-shape tree
-      if (t < w) {
-#pragma unroll
-        for (int c = 0; c < DICM_D; ++c) red.mx[t][c] = fmaxf(red.mx[t][c], red.mx[t + w][c]);
-        snf[t] |= snf[t + w];
-      }
-      __syncthreads();
-    }
-    if (t < DICM_D) smx[t] = red.mx[0][t];
-    __syncthreads();
-#pragma unroll
-    for (int c = 0; c < DICM_D; ++c) f.mx[c] = smx[c];
-    f.nf = snf[0];
-    int sh[DICM_D];
+    hot_block(S, order, u, start[u], start[u + 1], out);
+  }
+  const int nh = first;
+  if (nh == 0) return;
+  const int total = hot_chunks(acc, nh, off);
+  const int t = threadIdx.x, lane = t & 31;
+  for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    const int h = hot_slot_of(off, nh, g);
+    const HotEnt e = acc->ent[h];
+    const int32_t j = e.s0 + (g - off[h]) * HOT_CHUNK + t;
     long long q[DICM_D];
 #pragma unroll
-    for (int c = 0; c < DICM_D; ++c) {
-      sh[c] = fx_shift(f.mx[c], s1 - s0);
-      q[c] = 0;
-    }
-    for (int32_t j = s0 + t; j < s1; j += 256) {
+    for (int c = 0; c < DICM_D; ++c) q[c] = 0;
+    if (j < e.s0 + e.cnt) {
       float v[DICM_D];
       ref_contrib(S, __ldg(order + j), v);
 #pragma unroll
-      for (int c = 0; c < DICM_D; ++c) q[c] += fx_quant(v[c], sh[c]);
+      for (int c = 0; c < DICM_D; ++c) q[c] = fx_quant(v[c], fx_shift(__uint_as_float(__ldcg(&acc->mx[h][c])), e.cnt));
     }
 #pragma unroll
-    for (int c = 0; c < DICM_D; ++c) red.q[t][c] = q[c];
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-      if (t < w)
+    for (int c = 0; c < DICM_D; ++c)
+      for (int o = 16; o > 0; o >>= 1) q[c] += __shfl_down_sync(FULL, q[c], o);
+    if (lane == 0)
 #pragma unroll
-        for (int c = 0; c < DICM_D; ++c) red.q[t][c] += red.q[t + w][c];
-      __syncthreads();
-    }
-    if (t == 0) {
-      float r[DICM_D];
-#pragma unroll
-      for (int c = 0; c < DICM_D; ++c) r[c] = fx_result(red.q[0][c], sh[c], f, c);
-      if (f.nf) fx_nonfinite(S, order, s0, s1, 1, f.nf, r);
-      store_row12(out + (int64_t)u * DICM_D, r);
-    }
-    __syncthreads();
+      for (int c = 0; c < DICM_D; ++c)
+        if (q[c]) atomicAdd(reinterpret_cast<unsigned long long*>(&acc->q[h][c]), (unsigned long long)q[c]);
   }
+  __syncthreads();
+  if (t == 0) {
+    __threadfence();
+    last = atomicAdd(&acc->done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int i = t; i < nh * DICM_D; i += 256) {
+    const int h = i / DICM_D, c = i % DICM_D;
+    const HotEnt e = acc->ent[h];
+    const float mx = __uint_as_float(__ldcg(&acc->mx[h][c]));
+    out[(int64_t)e.u * DICM_D + c] =
+        fx_result(__ldcg(&acc->q[h][c]), fx_shift(mx, e.cnt), mx, __ldcg(&acc->fl[h]), c);
+  }
+  if (t == 0) acc->done = 0;
 }
 
 int bwd_grid(int batch) {
@@ -1156,20 +1304,27 @@ static RefSrc id_src(const dicm_layout_t* L, const dicm_batch_view_t* V, const f
   return S;
 }
 
-// counters: [hot, mid] of this list; the lists have room for every key
+// counters: [hot, mid] of this list; the lists have room for every key;
+// acc: this list's accumulators (or NULL)
 static void ref_reduce(const RefSrc& S, const int32_t* order, const int32_t* start, const int32_t* n_keys, int64_t cap,
-                       float* out, int32_t* counters, int32_t* hot_list, int32_t* mid_list, cudaStream_t st) {
+                       float* out, int32_t* counters, int32_t* hot_list, int32_t* mid_list, HotAcc* acc,
+                       cudaStream_t st) {
   static const int occ = [] {
     const char* e = getenv("DICM_REDUCE_OCC");
     return e && e[0] == '2' ? 2 : 3;
   }();
   const int grid = dicm_grid(cap, 256, 148 * 16);
   if (occ == 2)
-    k_ref_reduce<2><<<grid, 256, 0, st>>>(S, order, start, n_keys, cap, out, counters, hot_list, mid_list);
+    k_ref_reduce<2><<<grid, 256, 0, st>>>(S, order, start, n_keys, cap, out, counters, hot_list, mid_list, acc);
   else
-    k_ref_reduce<3><<<grid, 256, 0, st>>>(S, order, start, n_keys, cap, out, counters, hot_list, mid_list);
+    k_ref_reduce<3><<<grid, 256, 0, st>>>(S, order, start, n_keys, cap, out, counters, hot_list, mid_list, acc);
   k_ref_reduce_mid<<<148 * 4, 256, 0, st>>>(S, order, start, counters + 1, mid_list, out);
-  k_ref_reduce_hot<<<148, 256, 0, st>>>(S, order, start, counters, hot_list, out);
+  if (acc) k_ref_hot_max<<<148 * 4, 256, 0, st>>>(S, order, counters, acc);
+  k_ref_reduce_hot<<<148 * 4, 256, 0, st>>>(S, order, start, counters, hot_list, acc, out);
+}
+
+static HotAcc* hot_acc(const dicm_batch_view_t* bv, int list) {
+  return bv->hot_acc ? reinterpret_cast<HotAcc*>(bv->hot_acc) + list : nullptr;
 }
 
 // every unique ID row's gradient (the hot-key counter bv->hot[1] must be
@@ -1180,8 +1335,10 @@ static void launch_id_reduce(const dicm_layout_t* layout, const dicm_batch_view_
   int32_t* lists = bv->hot + 4;
   const RefSrc S = id_src(layout, bv, d_head_in);
   ref_reduce(S, bv->id_order, bv->id_start, bv->n_id_keys, bv->id_cap, d_rows, bv->hot + 2,
-             lists + 2 * bv->img_cap, lists + 2 * bv->img_cap + bv->id_cap, st);
+             lists + 2 * bv->img_cap, lists + 2 * bv->img_cap + bv->id_cap, hot_acc(bv, 1), st);
 }
+
+size_t dicm_hot_acc_bytes(void) { return 2 * sizeof(HotAcc); }
 
 int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const dicm_attn_params_t* attn,
                     const float* head_in, const float* d_head_in, const float* scores, const float* stats,
@@ -1236,7 +1393,7 @@ int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
   if (layout->use_ad_image || layout->use_behavior_images) {
     const RefSrc S = image_src(layout, bv, d_head_in);
     ref_reduce(S, bv->img_order, bv->img_start, bv->n_img_keys, bv->img_cap, d_emb, bv->hot, bv->hot + 4,
-               bv->hot + 4 + bv->img_cap, st);
+               bv->hot + 4 + bv->img_cap, hot_acc(bv, 0), st);
   }
   if (d_rows) launch_id_reduce(layout, bv, d_head_in, d_rows, st);
   probe_end(probe_slot, st);

@@ -238,6 +238,7 @@ class StepEngine:
         self.prec_code = L.PRECISIONS[precision]
         self.lr0, self.lr_decay, self.lr_interval = lr0, lr_decay, lr_interval
         self.iteration = 0
+        self.hot_acc_on = True  # chunked hot-key passes (False: one block per hot key; same bits)
         dev = self.dev = model.device
         lay = model.layout
         self.fields = list(lay.schema.fields)  # the fields with tables (pre-rank: tower fields)
@@ -478,6 +479,7 @@ class StepEngine:
         self.ref_grad = torch.empty((max(R, 1) if own_rows else 1, 12), **f32)
         self.q_grad = torch.empty((max(B, 1), 36), **f32)
         self.hot = torch.empty(4 + 2 * (max(self.cap_u, 1) + max(self.cap_k, 1)), **i32)
+        self.hot_acc = torch.zeros(L.lib.dicm_hot_acc_bytes(), dtype=torch.uint8, device=dev)  # kept re-armed
         self.ws_tr_img = _u8(L.lib.dicm_ref_transpose_workspace(n_img, max(self.cap_u, 1)), dev)
         self.ws_tr_id = _u8(L.lib.dicm_ref_transpose_workspace(n_id, max(self.cap_k, 1)), dev)
         self._alloc_image_net(self.cap_u)
@@ -661,6 +663,7 @@ class StepEngine:
         bv.n_img_keys, bv.n_id_keys = self.counts.data_ptr(), self.counts[1:].data_ptr()
         bv.img_cap, bv.id_cap = max(self.cap_u, 1), max(self.cap_k, 1)
         bv.ref_grad, bv.q_grad, bv.hot = self.ref_grad.data_ptr(), self.q_grad.data_ptr(), self.hot.data_ptr()
+        bv.hot_acc = self.hot_acc.data_ptr() if self.hot_acc_on else 0  # 0: one block per hot key
         return bv
 
     def _transpose_images(self):

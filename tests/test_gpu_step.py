@@ -303,6 +303,35 @@ def test_hot_keys_match_oracle(kind):
         assert O.rel_err(rows_, out["tgrads"][f][1]) < FP32_TOL, f
 
 
+@pytest.mark.parametrize("kind", ["sum", "attn"])
+def test_hot_key_passes_match_block_path_and_oracle(kind):
+    """More than 4096 image keys with > 32 references each: the chunked
+    accumulator passes (every SM on one key) take the first 4096 listed keys,
+    the rest go one block per key; with the accumulators off every key takes
+    the block path.  The sums are exact fixed point, so the bits agree."""
+    from paper_1711_06505_b200.engine import StepEngine
+    model, pool, batch = _bench_like(kind, B=2048, L=100, P=5000)
+    counts = np.bincount(batch.beh_image_ids, minlength=5000)
+    assert (counts > 32).sum() > 4096
+    outs = []
+    for on in (True, False):
+        e = StepEngine(model, pool, "fp32")
+        e.hot_acc_on = on
+        loss = e.forward_backward(e.upload(batch))
+        torch.cuda.synchronize()
+        e.raise_status()
+        U = len(e.unique_images())
+        outs.append((loss.item(), e.d_emb[:U].cpu().numpy().copy(), H.table_grads(e)))
+    (l0, d0, t0), (l1, d1, t1) = outs
+    assert l0 == l1 and np.array_equal(d0, d1)
+    for f in t0:
+        assert np.array_equal(t0[f][1], t1[f][1]), f
+    out = O.forward_backward(H.host_params(model), H.oracle_cfg_of(model), H.oracle_batch(batch),
+                             pool.rows.double().cpu().numpy())
+    assert O.rel_err(l0, out["loss"]) < FP32_TOL
+    assert O.rel_err(d0, out["dE"]) < FP32_TOL
+
+
 @pytest.mark.parametrize("L", [2, 9])
 def test_concat_narrow_and_wide_heads_match_oracle(L):
     """concat (reference scatter_concat, autograd.py:370-385): b_max = 2 keeps
