@@ -61,6 +61,23 @@ __device__ __forceinline__ void load32(const float* p, float (&v)[BT]) {
   }
 }
 
+__device__ __forceinline__ bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// n4 float4s of src handed to put(i, v), eight loads in flight per thread
+template <typename F>
+__device__ __forceinline__ void stage4(const float* __restrict__ src, int n4, F put) {
+  const float4* g = reinterpret_cast<const float4*>(src);
+  for (int base = threadIdx.x; base < n4; base += THREADS * 8) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (base + u * THREADS < n4) v[u] = __ldg(g + base + u * THREADS);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (base + u * THREADS < n4) put(base + u * THREADS, v[u]);
+  }
+}
+
 // WIDE: the input is wider than the shared-memory-resident W0 allows (the
 // concat aggregator); layer 0 then runs as separate GEMMs (k_sgemm below):
 // ``x`` holds the layer-0 pre-activations [B][H0] on entry, and on exit
@@ -79,7 +96,20 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
   const int b0 = blockIdx.x * BT;
   const int nb = min(BT, B - b0);
   const int WS = W | 1;  // shared-memory row stride of w0: odd, so a warp reading one column hits 32 banks
-  if (!WIDE) {
+  const bool vec = (W & 3) == 0 && aligned16(p.w0) && aligned16(p.w1) && aligned16(x);
+  if (!WIDE && vec) {  // float4 loads, 8 in flight per thread
+    const int W4 = W >> 2;
+    stage4(p.w0, H0 * W4, [&](int i, float4 v) {
+      const int r = i / W4, c = (i - r * W4) * 4;
+      float* d = s.w0 + r * WS + c;
+      d[0] = v.x, d[1] = v.y, d[2] = v.z, d[3] = v.w;
+    });
+    stage4(x + (int64_t)b0 * W, nb * W4, [&](int i, float4 v) {
+      const int r = i / W4, c = (i - r * W4) * 4;
+      s.xs[c][r] = v.x, s.xs[c + 1][r] = v.y, s.xs[c + 2][r] = v.z, s.xs[c + 3][r] = v.w;
+    });
+    for (int i = t; i < (BT - nb) * W; i += THREADS) s.xs[i % W][nb + i / W] = 0.f;  // a short last tile
+  } else if (!WIDE) {
     for (int i = t; i < H0 * W; i += THREADS) s.w0[(i / W) * WS + i % W] = p.w0[i];
     for (int i = t; i < BT * W; i += THREADS) {
       const int r = i / W, c = i % W;
@@ -93,7 +123,10 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
       s.h0[j][r] = prelu(a, __ldg(p.a0 + j));
     }
   }
-  for (int i = t; i < H1 * H0; i += THREADS) s.w1[i] = p.w1[i];
+  if (vec)
+    stage4(p.w1, H1 * H0 / 4, [&](int i, float4 v) { reinterpret_cast<float4*>(s.w1)[i] = v; });
+  else
+    for (int i = t; i < H1 * H0; i += THREADS) s.w1[i] = p.w1[i];
   __syncthreads();
 
   // layer 0: thread = (unit j, half of the tile)

@@ -806,7 +806,7 @@ __device__ __forceinline__ float fx_result(long long q, int shift, float mx, uns
 
 // Keys with more than HOT_REFS references.  The first HOT_SLOTS listed keys
 // get accumulators (dicm_batch_view_t.hot_acc) and are split into chunks of
-// HOT_CHUNK references spread over every block: k_ref_hot_max forms each
+// HOT_CHUNK references spread over every block: k_ref_mid_hot forms each
 // key's maxima and flags, k_ref_reduce_hot its fixed-point sums (integer
 // atomics: exact, so the split does not change a bit), and the last block to
 // finish writes the rows.  Keys past HOT_SLOTS (or every key without
@@ -827,7 +827,7 @@ struct HotAcc {  // one key list's accumulators
 // out[u] = sum of the gradient rows of key u's references in ascending
 // reference order (np.add.at's order).  Thread per key for up to 16
 // references (positions sorted in registers); keys with 17..32 references
-// are listed for k_ref_reduce_mid (a warp each), larger ones for the hot-key
+// are listed for mid_pass (a warp each), larger ones for the hot-key
 // passes (exact fixed point).
 template <int MINB>  // DICM_REDUCE_OCC: 2 or 3 (default) resident blocks per SM
 __global__ void __launch_bounds__(256, MINB) k_ref_reduce(const __grid_constant__ RefSrc S,
@@ -891,12 +891,9 @@ __global__ void __launch_bounds__(256, MINB) k_ref_reduce(const __grid_constant_
 // the keys with 17..32 references, a warp each: lane i takes reference i, its
 // rank by position (a 32-way compare), the rows land in rank order in shared
 // memory and lanes 0..11 sum their column in ascending reference order
-__global__ void __launch_bounds__(256) k_ref_reduce_mid(const __grid_constant__ RefSrc S,
-                                                        const int32_t* __restrict__ order,
-                                                        const int32_t* __restrict__ start,
-                                                        const int32_t* __restrict__ mid_count,
-                                                        const int32_t* __restrict__ mid_list,
-                                                        float* __restrict__ out) {
+__device__ __forceinline__ void mid_pass(const RefSrc& S, const int32_t* __restrict__ order,
+                                         const int32_t* __restrict__ start, const int32_t* __restrict__ mid_count,
+                                         const int32_t* __restrict__ mid_list, float* __restrict__ out) {
   __shared__ float slots[8][32][DICM_D + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nm = *mid_count;
@@ -1036,12 +1033,17 @@ __device__ __forceinline__ int hot_slot_of(const int* off, int nh, int g) {
   return lo;
 }
 
-// pass 1 over the chunks: each slot's maxima and non-finite flags
-__global__ void __launch_bounds__(256) k_ref_hot_max(const __grid_constant__ RefSrc S,
+// the keys with 17..32 references (mid_pass), then pass 1 over the hot-key
+// chunks: each slot's maxima and non-finite flags.  counters: [hot, mid]
+__global__ void __launch_bounds__(256) k_ref_mid_hot(const __grid_constant__ RefSrc S,
                                                      const int32_t* __restrict__ order,
-                                                     const int32_t* __restrict__ hot_count, HotAcc* __restrict__ acc) {
+                                                     const int32_t* __restrict__ start,
+                                                     const int32_t* __restrict__ counters,
+                                                     const int32_t* __restrict__ mid_list, float* __restrict__ out,
+                                                     HotAcc* __restrict__ acc) {
   __shared__ int off[HOT_SLOTS + 1];
-  const int nh = min(*hot_count, HOT_SLOTS);
+  mid_pass(S, order, start, counters + 1, mid_list, out);
+  const int nh = acc ? min(counters[0], HOT_SLOTS) : 0;
   if (nh == 0) return;
   const int total = hot_chunks(acc, nh, off);
   const int t = threadIdx.x, lane = t & 31;
@@ -1318,8 +1320,7 @@ static void ref_reduce(const RefSrc& S, const int32_t* order, const int32_t* sta
     k_ref_reduce<2><<<grid, 256, 0, st>>>(S, order, start, n_keys, cap, out, counters, hot_list, mid_list, acc);
   else
     k_ref_reduce<3><<<grid, 256, 0, st>>>(S, order, start, n_keys, cap, out, counters, hot_list, mid_list, acc);
-  k_ref_reduce_mid<<<148 * 4, 256, 0, st>>>(S, order, start, counters + 1, mid_list, out);
-  if (acc) k_ref_hot_max<<<148 * 4, 256, 0, st>>>(S, order, counters, acc);
+  k_ref_mid_hot<<<148 * 4, 256, 0, st>>>(S, order, start, counters, mid_list, out, acc);
   k_ref_reduce_hot<<<148 * 4, 256, 0, st>>>(S, order, start, counters, hot_list, acc, out);
 }
 

@@ -1014,15 +1014,15 @@ class StepEngine:
 
     @property
     def launches_per_step(self):
-        """Estimated kernels per eager step, from the kernel sequence of each
-        C-ABI call (memsets excluded; some reductions depend on the shape).
-        Only a fallback: ``bench.py`` counts the kernel nodes of the captured
-        step graph (``kernel_nodes``) whenever steps run as graphs.  cfg2 bf16
-        attn: 35, as in the ncu launch list and the graph."""
+        """This library's kernels per step (CUB's scan kernels and memsets
+        excluded), from the kernel sequence of each C-ABI call; equals the
+        ``own`` count of ``kernel_nodes`` for a graphed step
+        (tests/test_gpu_step.py).  Only a fallback: ``bench.py`` counts the
+        kernel nodes of the captured step graph whenever steps run as graphs."""
         lay = self.model.layout
         n = 5 + 5  # two dedups: mark, tile sums, scan, emit, inverse
         if self.prec_code == L.PREC_BF16:
-            n += 3 + 6 + 2  # to_bf16, fwd2, l12f | l12b, dw1b, colsum_multi, l1_finish, dw0, sum_splits | 2 colsums
+            n += 3 + 6 + 2  # to_bf16, fwd4, l12f | l12b, dw1b, colsum_multi, l1_finish, dw0p, sum_splits | 2 colsums
         else:
             n += 4 + 9
         n += 1  # gather_keyed
@@ -1031,9 +1031,13 @@ class StepEngine:
             n += 1  # attention partial reduce
         elif lay.aggregator.kind in ("max", "concat"):
             n += 1  # per-reference rows
-        n += 2 * 7 + (1 if lay.aggregator.kind == "sum" else 0) + sum(1 for f in self.fields if f.multi)  # transposes (iota, CUB radix sort, starts), CSR segments
-        n += 4  # ordered row sums (images, IDs) and their hot-key passes
-        n += 1 + 1 + 1 + 1  # sample fwd, head, loss, head partial reduce
+        images = lay.use_ad_image or lay.use_behavior_images
+        lists = int(images) + int(bool(self.fields))
+        n += 2 * lists  # transposes: count, fill (the scan is CUB's)
+        n += int(lay.use_behavior_images and lay.aggregator.kind == "sum") + sum(1 for f in self.fields if f.multi)
+        n += 3 * lists  # ordered row sums: thread/ warp / hot-key passes per list
+        n += 1 if os.environ.get("DICM_FORK", "1") == "0" else 2  # sample forward (fields, images apart when forked)
+        n += 1 + 1 + 1  # head, loss, head partial reduce
         if self.wide_head:
             n += 3 + 2 - 1  # layer-0 GEMMs + two column reduces instead of the partial reduce
         n += 1 + 3 + 1  # check_finite, adam dense (flags, update, steps), adam rows

@@ -204,12 +204,14 @@ class DicmModel:
                            for n, _, _ in self.specs}
         real_shapes = {n: shp for n, shp, _ in self.specs}
         # fused dense buffer
-        # the image group starts on a 256-B boundary so the kernels can use
-        # 16-B vector loads on img/*/w; the gap is its own (always-zero) span
+        # the image and head groups start on 256-B boundaries so the kernels
+        # can use 16-B vector loads on their weights (mlp/0/w, mlp/1/w sit a
+        # multiple of 4 floats into the group); a gap is its own (always-zero) span
         self.dense_offsets, off = {}, 0
         self.dense_spans = []  # (offset, size, name or None) tiling the buffer
+        first_mlp = next((n for n in self.dense_names if n.startswith("mlp/")), None)
         for n in self.dense_names:
-            if n.startswith("img/") and off % 64:
+            if (n.startswith("img/") or n == first_mlp) and off % 64:
                 pad = 64 - off % 64
                 self.dense_spans.append((off, pad, None))
                 off += pad
