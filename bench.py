@@ -641,11 +641,15 @@ def main():
     # kernel launches inside the timed region: the captured step graph's kernel
     # nodes (this library's only; NCCL / torch nodes excluded) x steps, or the
     # engine's per-call kernel sequence for eager steps
-    kn = eng.kernel_nodes(detail=True) if graphs else None
-    launches = kn[0] * args.steps if kn else eng.launches_per_step * args.steps
-    launch_src = ({"own_kernels_per_step": kn[0], "cub_sort_kernels_per_step": kn[1],
-                   "kernel_nodes_per_step": kn[2], "source": "captured step graph"}
-                  if kn else {"source": "engine kernel sequence"})
+    kn, src = (eng.kernel_nodes(detail=True), "captured step graph") if graphs else (None, None)
+    if kn is None:  # eager steps: one representative step captured (never replayed) and counted
+        try:
+            kn, src = eng.count_step_kernels(staged[-1], union), "one eager step captured for counting"
+        except Exception as ex:  # e.g. the NCCL exchange (host syncs) cannot be captured
+            src = f"uncounted: {ex!r}"[:120]
+    launches = kn[0] * args.steps if kn else None
+    launch_src = ({"own_kernels_per_step": kn[0], "cub_scan_kernels_per_step": kn[1],
+                   "kernel_nodes_per_step": kn[2], "source": src} if kn else {"source": src})
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",

@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdicm_b200.so")
+# DICM_LIB_PATH: an alternate build of the same library (scripts/ab_lib.sh A/B runs)
+LIB_PATH = os.environ.get("DICM_LIB_PATH") or os.path.join(_HERE, "libdicm_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -164,6 +164,39 @@ __device__ __forceinline__ float attn_score_rc(const AttnSmem& s, const float* P
   return sc;
 }
 
+// the scores of two references at once (each bit-identical to
+// attn_score_rc's): every 16-B read of the transposed Wk feeds both, halving
+// the shared-memory traffic per reference (the forward's limiter)
+__device__ __forceinline__ void attn_score_rc2(const AttnSmem& s, const float* P, const Row12& ka, const Row12& kb,
+                                               float& sa, float& sb) {
+  sa = s.b1;
+  sb = s.b1;
+#pragma unroll
+  for (int g = 0; g < DICM_ATT / 8; ++g) {
+    const float4 p0 = reinterpret_cast<const float4*>(P)[2 * g], p1 = reinterpret_cast<const float4*>(P)[2 * g + 1];
+    float pa[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+    float pb[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+    for (int c = 0; c < DICM_D; ++c) {
+      const float4* w = reinterpret_cast<const float4*>(&s.wkT[c][8 * g]);
+      const float4 wa = w[0], wb = w[1];
+      ffma2(pa[0], pa[1], wa.x, wa.y, ka.v[c]);
+      ffma2(pa[2], pa[3], wa.z, wa.w, ka.v[c]);
+      ffma2(pa[4], pa[5], wb.x, wb.y, ka.v[c]);
+      ffma2(pa[6], pa[7], wb.z, wb.w, ka.v[c]);
+      ffma2(pb[0], pb[1], wa.x, wa.y, kb.v[c]);
+      ffma2(pb[2], pb[3], wa.z, wa.w, kb.v[c]);
+      ffma2(pb[4], pb[5], wb.x, wb.y, kb.v[c]);
+      ffma2(pb[6], pb[7], wb.z, wb.w, kb.v[c]);
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float w1 = s.w1[8 * g + e], al = s.a0[8 * g + e];
+      sa = fmaf(w1, prelu(pa[e], al), sa);
+      sb = fmaf(w1, prelu(pb[e], al), sb);
+    }
+  }
+}
 
 // per-column max over a sample's behaviors and its FIRST argmax (the reference
 // keeps the earliest row on ties); every lane ends with the warp result;
@@ -203,7 +236,7 @@ __device__ __forceinline__ void seg_max(const Args& a, int b, int lane, float (&
 // forward
 // ---------------------------------------------------------------------------
 
-template <int DQ>
+template <int DQ, bool PAIR>  // PAIR: two references per lane per pass (more registers, half the Wk reads)
 __device__ void attn_fwd(const Args& a, const AttnSmem& s, int ch, int b, int lane, float* P) {
   {
     float q[DQ];
@@ -218,21 +251,7 @@ __device__ void attn_fwd(const Args& a, const AttnSmem& s, int ch, int b, int la
 #pragma unroll
   for (int c = 0; c < DICM_D; ++c) acc[c] = 0.f;
   const bool norm = a.L.normalize != 0;
-  // the next reference's row (and the one after's index) are in flight
-  // while this one is scored
-  Row12 k_n;
-  int32_t u_nn = 0;
-  {
-    const int64_t i = i0 + lane;
-    if (i < i1) k_n = load_row12(a.V.emb + (int64_t)__ldg(a.V.beh_local + i) * DICM_D);
-    if (i + 32 < i1) u_nn = __ldg(a.V.beh_local + i + 32);
-  }
-  for (int64_t i = i0 + lane; i < i1; i += 32) {
-    const Row12 k = k_n;
-    if (i + 32 < i1) k_n = load_row12(a.V.emb + (int64_t)u_nn * DICM_D);
-    if (i + 64 < i1) u_nn = __ldg(a.V.beh_local + i + 64);
-    const float sc = attn_score_rc(s, P, k);
-    a.scores[(int64_t)ch * a.V.refs + i] = sc;
+  auto take = [&](float sc, const Row12& k) {  // online segment softmax (or the raw weighted sum)
     if (norm) {
       const float mn = fmaxf(m, sc);
       const float scale = expf(m - mn);  // exp(-inf) = 0 on the first element
@@ -245,6 +264,58 @@ __device__ void attn_fwd(const Args& a, const AttnSmem& s, int ch, int b, int la
 #pragma unroll
       for (int c = 0; c < DICM_D; ++c) acc[c] = fmaf(sc, k.v[c], acc[c]);
     }
+  };
+  auto row_of = [&](int64_t i) { return load_row12(a.V.emb + (int64_t)__ldg(a.V.beh_local + i) * DICM_D); };
+  // chunks of 64 references (lane: references c0 + lane and c0 + 32 + lane,
+  // scored together) while more than 32 remain, then one chunk of <= 32; the
+  // next chunk's rows are in flight while this one is scored
+  float* scores = a.scores + (int64_t)ch * a.V.refs;
+  if (!PAIR) {
+    // one reference per lane per pass; the next reference's row (and the one
+    // after's index) are in flight while this one is scored
+    Row12 k_n;
+    int32_t u_nn = 0;
+    {
+      const int64_t i = i0 + lane;
+      if (i < i1) k_n = load_row12(a.V.emb + (int64_t)__ldg(a.V.beh_local + i) * DICM_D);
+      if (i + 32 < i1) u_nn = __ldg(a.V.beh_local + i + 32);
+    }
+    for (int64_t i = i0 + lane; i < i1; i += 32) {
+      const Row12 k = k_n;
+      if (i + 32 < i1) k_n = load_row12(a.V.emb + (int64_t)u_nn * DICM_D);
+      if (i + 64 < i1) u_nn = __ldg(a.V.beh_local + i + 64);
+      const float sc = attn_score_rc(s, P, k);
+      scores[i] = sc;
+      take(sc, k);
+    }
+  } else {
+  Row12 ka, kb;
+  if (i0 + lane < i1) ka = row_of(i0 + lane);
+  if (i0 + 32 + lane < i1) kb = row_of(i0 + 32 + lane);
+  for (int64_t c0 = i0; c0 < i1;) {
+    const bool two = i1 - c0 > 32;  // warp-uniform
+    const int64_t ia = c0 + lane, ib = ia + 32, n0 = c0 + (two ? 64 : 32);
+    Row12 na, nb;
+    if (n0 + lane < i1) na = row_of(n0 + lane);
+    if (n0 + 32 + lane < i1) nb = row_of(n0 + 32 + lane);
+    if (two) {
+      float sa, sb;
+      attn_score_rc2(s, P, ka, kb, sa, sb);
+      scores[ia] = sa;
+      take(sa, ka);
+      if (ib < i1) {
+        scores[ib] = sb;
+        take(sb, kb);
+      }
+    } else if (ia < i1) {
+      const float sa = attn_score_rc(s, P, ka);
+      scores[ia] = sa;
+      take(sa, ka);
+    }
+    ka = na;
+    kb = nb;
+    c0 = n0;
+  }
   }
   float out[DICM_D];
   if (norm) {
@@ -345,12 +416,12 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, MINB) k_sample_fwd(const __gri
         if (lane == c) row[a.L.pool_col + c] = acc[c];
     } else {
       if constexpr (PART != 1) {
-        attn_fwd<DICM_D>(a, sa[0], 0, b, lane, Pw[warp]);
+        attn_fwd<DICM_D, KIND == 1>(a, sa[0], 0, b, lane, Pw[warp]);
         if (kind == 2) {
           if (a.L.n_query == 2)
-            attn_fwd<2 * DICM_D>(a, sa[1], 1, b, lane, Pw[warp]);
+            attn_fwd<2 * DICM_D, false>(a, sa[1], 1, b, lane, Pw[warp]);
           else
-            attn_fwd<DICM_D>(a, sa[1], 1, b, lane, Pw[warp]);
+            attn_fwd<DICM_D, false>(a, sa[1], 1, b, lane, Pw[warp]);
         }
       }
     }
@@ -1215,14 +1286,14 @@ static int sample_fwd_part(int part, const dicm_layout_t* layout, const dicm_bat
     const char* e = getenv("DICM_FWD_OCC");
     return e && e[0] == '3' ? 3 : 2;
   }();
-  static const int occ_attn = [] {
+  static const int occ_attn = [] {  // the single-head images kernel scores reference pairs: 128 registers
     const char* e = getenv("DICM_FWD_OCC");
-    return e && e[0] == '2' ? 2 : 3;
+    return e && e[0] == '3' ? 3 : 2;
   }();
   const int probe_slot = part == 1 ? -1 : probe_begin(DICM_PROBE_SAMPLE_FWD, st);
   if (part == 1)
     k_sample_fwd<3, 1><<<grid, FWD_WARPS * 32, 0, st>>>(a);
-  else if (part == 2 && layout->kind == 1 && occ_attn == 3)  // single-head attention alone: 80 registers, no spills
+  else if (part == 2 && layout->kind == 1 && occ_attn == 3)  // single-head attention alone at 80 registers
     k_sample_fwd<3, 2, 1><<<grid, FWD_WARPS * 32, 0, st>>>(a);
   else if (part == 2 && layout->kind == 1)
     k_sample_fwd<2, 2, 1><<<grid, FWD_WARPS * 32, 0, st>>>(a);

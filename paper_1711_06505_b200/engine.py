@@ -1012,36 +1012,22 @@ class StepEngine:
         if ev is not None:
             ev.record()
 
-    @property
-    def launches_per_step(self):
-        """This library's kernels per step (CUB's scan kernels and memsets
-        excluded), from the kernel sequence of each C-ABI call; equals the
-        ``own`` count of ``kernel_nodes`` for a graphed step
-        (tests/test_gpu_step.py).  Only a fallback: ``bench.py`` counts the
-        kernel nodes of the captured step graph whenever steps run as graphs."""
-        lay = self.model.layout
-        n = 5 + 5  # two dedups: mark, tile sums, scan, emit, inverse
-        if self.prec_code == L.PREC_BF16:
-            n += 3 + 6 + 2  # to_bf16, fwd4, l12f | l12b, dw1b, colsum_multi, l1_finish, dw0p, sum_splits | 2 colsums
-        else:
-            n += 4 + 9
-        n += 1  # gather_keyed
-        if lay.attentive:
-            n += 2 if lay.multiquery else 1  # attn_bwd per channel
-            n += 1  # attention partial reduce
-        elif lay.aggregator.kind in ("max", "concat"):
-            n += 1  # per-reference rows
-        images = lay.use_ad_image or lay.use_behavior_images
-        lists = int(images) + int(bool(self.fields))
-        n += 2 * lists  # transposes: count, fill (the scan is CUB's)
-        n += int(lay.use_behavior_images and lay.aggregator.kind == "sum") + sum(1 for f in self.fields if f.multi)
-        n += 3 * lists  # ordered row sums: thread/ warp / hot-key passes per list
-        n += 1 if os.environ.get("DICM_FORK", "1") == "0" else 2  # sample forward (fields, images apart when forked)
-        n += 1 + 1 + 1  # head, loss, head partial reduce
-        if self.wide_head:
-            n += 3 + 2 - 1  # layer-0 GEMMs + two column reduces instead of the partial reduce
-        n += 1 + 3 + 1  # check_finite, adam dense (flags, update, steps), adam rows
-        return n
+    def count_step_kernels(self, db, denominator=None):
+        """(own, cub, total) kernel nodes of one step (forward_backward +
+        optimizer_step) captured into a throwaway graph that is never
+        replayed: the launch count of an eager step, read from the same graph
+        API as ``kernel_nodes``.  Needs a warmed-up engine (kernel attributes
+        set) and no other thread issuing CUDA work during the capture."""
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph(keep_graph=True)
+        with torch.cuda.graph(g):
+            self.forward_backward(db, denominator)
+            self.optimizer_step(self.lr())
+        saved, self._last_graph = getattr(self, "_last_graph", None), g
+        try:
+            return self.kernel_nodes(detail=True)
+        finally:
+            self._last_graph = saved
 
     # -- inspection ---------------------------------------------------
     def unique_images(self):
