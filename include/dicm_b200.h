@@ -244,8 +244,9 @@ int dicm_images_fwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv,
 /* Stream-ordered on `stream`.  Writes every row d_emb[0..U) and
  * d_rows[0..K) (no zeroing needed); the scratch buffers of the batch view are
  * overwritten.  d_rows = NULL leaves the ID rows to dicm_id_row_grads, which
- * may then run on another stream (after this call) beside the image-MLP
- * backward. */
+ * reads only d_head_in and the ID half of the batch view's scratch, so it may
+ * run on another stream concurrently with this call (once the head has
+ * written d_head_in). */
 int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv,
                     const dicm_attn_params_t* attn, const float* head_in, const float* d_head_in,
                     const float* scores, const float* stats, float* d_emb /* [U,12] */,

@@ -1399,8 +1399,8 @@ static HotAcc* hot_acc(const dicm_batch_view_t* bv, int list) {
   return bv->hot_acc ? reinterpret_cast<HotAcc*>(bv->hot_acc) + list : nullptr;
 }
 
-// every unique ID row's gradient (the hot-key counter bv->hot[1] must be
-// zero; dicm_sample_bwd clears both counters before its kernels)
+// every unique ID row's gradient (the ID list's counters bv->hot[2..3] must be
+// zero: cleared by the calling entry point)
 static void launch_id_reduce(const dicm_layout_t* layout, const dicm_batch_view_t* bv, const float* d_head_in,
                              float* d_rows, cudaStream_t st) {
   if (layout->n_fields <= 0) return;
@@ -1444,7 +1444,9 @@ int dicm_sample_bwd(const dicm_layout_t* layout, const dicm_batch_view_t* bv, co
   const int grid = bwd_grid(bv->batch);
   const int64_t stride = part_size(layout);
   const int probe_slot = probe_begin(DICM_PROBE_SAMPLE_BWD, st);
-  if (check_cuda(cudaMemsetAsync(bv->hot, 0, 4 * sizeof(int32_t), st), "sample_bwd list counters"))
+  // this call's list counters: the image list's, and the ID list's when it
+  // sums the ID rows too (dicm_id_row_grads clears its own)
+  if (check_cuda(cudaMemsetAsync(bv->hot, 0, (d_rows ? 4 : 2) * sizeof(int32_t), st), "sample_bwd list counters"))
     return DICM_ERR_CUDA;
   if (attn_chan) {
     // partial row layout in sorted names: attn/id/* before attn/img/*; the
@@ -1478,6 +1480,8 @@ int dicm_id_row_grads(const dicm_layout_t* layout, const dicm_batch_view_t* bv, 
   if (rc) return rc;
   if (bv->batch == 0) return DICM_OK;
   if (!bv->hot || !bv->id_order) return fail(DICM_ERR_VALUE, "id_row_grads: the batch view lacks its buffers");
+  if (check_cuda(cudaMemsetAsync(bv->hot + 2, 0, 2 * sizeof(int32_t), (cudaStream_t)stream), "id_row_grads counters"))
+    return DICM_ERR_CUDA;
   launch_id_reduce(layout, bv, d_head_in, d_rows, (cudaStream_t)stream);
   return last_launch("dicm_id_row_grads");
 }

@@ -213,6 +213,13 @@ class ImageNetBuffers:
         self.ws = _u8(L.lib.dicm_imgmlp_workspace(self.cap, d_raw, prec_code), dev, zero=True)
 
 
+class _Joined:
+    """A forked stream whose backward work is already queued (forward_backward)."""
+
+    def __init__(self, stream):
+        self.stream = stream
+
+
 class StepEngine:
     """Owns the optimizer state and the step buffers of one model replica.
 
@@ -693,7 +700,7 @@ class StepEngine:
                 L.check(L.lib.dicm_csr_segments(self._dptr(o), pk.B, self.id_seg.data_ptr() + 4 * self.inv_id_off[f.name],
                                                 self.s))
 
-    def _local_step(self, emb, d_emb, denom, reduce=True, id_rows=True, fwd=True):
+    def _local_step(self, emb, d_emb, denom, reduce=True, id_rows=True, fwd=True, after_head=None):
         """a6-a12 forward and backward on the local batch: pooling, head, BCE.
         Reads image embeddings ``emb`` and compact ID rows ``self.id_rows``;
         writes ``d_emb`` / ``self.d_rows`` (``id_rows=False``: left to
@@ -710,6 +717,8 @@ class StepEngine:
         self._head_fwd_bwd(B, denom)
         nhb = self._head_blocks(B)
         L.check(L.lib.dicm_loss_finalize(self.loss_part.data_ptr(), nhb, 1.0 / denom, self.loss.data_ptr(), st, s))
+        if after_head is not None:  # work that needs only the head's gradients (forked by the caller)
+            after_head()
         L.check(L.lib.dicm_sample_bwd(C.byref(self.layout), C.byref(bv), self.attn, self.head_in.data_ptr(),
                                       self.d_head_in.data_ptr(), self.scores.data_ptr(), self.stats.data_ptr(),
                                       d_emb.data_ptr(), self.d_rows.data_ptr() if id_rows else None,
@@ -724,11 +733,18 @@ class StepEngine:
     def _reduce_partials(self, s):
         """Head and attention parameter gradients from their block partials
         (fixed-order reduces)."""
+        self._reduce_head_partials(s)
+        self._reduce_attn_partials(s)
+
+    def _reduce_head_partials(self, s):
         B = self.pk.B
         h0, h1 = self.head_range
         if not self.wide_head:
             L.check(L.lib.dicm_reduce_partials(self.head_part.data_ptr(), self._head_blocks(B), h1 - h0,
                                                self.grad.data_ptr() + 4 * h0, 0, s))
+
+    def _reduce_attn_partials(self, s):
+        B = self.pk.B
         if self.attn_range is not None:
             a0, a1 = self.attn_range
             L.check(L.lib.dicm_reduce_partials(self.attn_partial.data_ptr(), L.lib.dicm_sample_blocks(B), a1 - a0,
@@ -783,7 +799,29 @@ class StepEngine:
             L.check(L.lib.dicm_images_fwd(C.byref(self.layout), C.byref(self._bv), self.attn, self.head_in.data_ptr(),
                                           self.scores.data_ptr(), self.stats.data_ptr(), self.s))
             torch.cuda.current_stream().wait_stream(side)
-            self._local_step(self.net.emb, self.net.d_emb, denom, reduce=False, id_rows=False, fwd=False)
+            def id_grads_after_head():
+                # the ID-row ordered sums, the head partial reduce and the
+                # row-gradient finite check need only the head's gradients:
+                # forked here, they run beside the attention backward
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    self._id_row_grads(side.cuda_stream)
+                    self._reduce_head_partials(side.cuda_stream)
+                    L.check(L.lib.dicm_check_finite(self.d_rows.data_ptr(), self.cap_k * 12,
+                                                    self.counts[1:].data_ptr(), 12, 4, self.status.data_ptr(),
+                                                    side.cuda_stream))
+
+            # (multi-query attention: the ID query fields' rows also collect
+            # the attention backward's query gradients, so they wait for it)
+            early = os.environ.get("DICM_ID_FORK", "head") == "head" and not self.model.layout.multiquery
+            self._local_step(self.net.emb, self.net.d_emb, denom, reduce=False, id_rows=False, fwd=False,
+                             after_head=id_grads_after_head if early else None)
+            if early:  # the attention partial reduce waits for the attention backward
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    self._reduce_attn_partials(side.cuda_stream)
+                self._rows_checked = True
+                side = _Joined(side)
         else:
             self._dedup_images()
             self._dedup_ids()
@@ -793,8 +831,8 @@ class StepEngine:
                 self._image_forward(self.net, self.uniq_img, self.counts.data_ptr())
             self._gather_id_rows()
             self._local_step(self.net.emb, self.net.d_emb, denom)
-        if side is not None:  # the ID-row gradients and the partial reduces overlap the image-MLP backward
-            side.wait_stream(torch.cuda.current_stream())
+        if side is not None and not isinstance(side, _Joined):  # the ID-row gradients and the partial reduces
+            side.wait_stream(torch.cuda.current_stream())       # overlap the image-MLP backward
             with torch.cuda.stream(side):
                 self._id_row_grads(side.cuda_stream)
                 self._reduce_partials(side.cuda_stream)
@@ -804,7 +842,7 @@ class StepEngine:
             self._rows_checked = True
         self._image_backward(self.net, self.uniq_img, self.counts.data_ptr(), self.cap_u if self.n_img_segs else 0)
         if side is not None:
-            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.current_stream().wait_stream(side.stream if isinstance(side, _Joined) else side)
         return self.loss
 
     def optimizer_step(self, lr, row_keys=None, row_count=None, row_grads=None, row_cap=None, tabstate=None):
