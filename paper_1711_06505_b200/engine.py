@@ -813,7 +813,9 @@ class StepEngine:
 
             # (multi-query attention: the ID query fields' rows also collect
             # the attention backward's query gradients, so they wait for it)
-            early = os.environ.get("DICM_ID_FORK", "head") == "head" and not self.model.layout.multiquery
+            # DICM_ID_FORK=head: measured neutral (r2 idfork A/B: k_dw1b -43 us,
+            # the attention backward + image sums +46 us), so off by default
+            early = os.environ.get("DICM_ID_FORK", "bwd") == "head" and not self.model.layout.multiquery
             self._local_step(self.net.emb, self.net.d_emb, denom, reduce=False, id_rows=False, fwd=False,
                              after_head=id_grads_after_head if early else None)
             if early:  # the attention partial reduce waits for the attention backward
