@@ -538,6 +538,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F4, 1)
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + sub * 256 + cb * 32, v);
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] += __ldg(bias + cb * 32 + j);
+#ifdef DICM_FWD4_NOSTORE  // measurement build only: the drain without its act0 stores
+        if (v[0] == 12345.f) reinterpret_cast<float*>(act0_)[0] = v[lane];  // keeps the TMEM loads live
+        if (false)
+#endif
         if constexpr (SCR) {
           if constexpr (KIND == 1)
             epi::store_bf16(v, scr, lane, m0, U, [&](int r) {
