@@ -523,21 +523,14 @@ __global__ void __launch_bounds__(B_THREADS, 1)
 //   db0[f]     = sum_r da0 = sum_j W1[j,f] (db1[j] - (1 - alpha0[f]) Gm[f,j])
 // (dh1 = da1 W1, so every sum over rows of dh1 folds through W1).
 // ===========================================================================
-// Two rings: the TMA ring holds only what is loaded (a0 and da1 of 32 rows,
-// 20 KB a stage, 8 stages = 160 KB in flight per SM), the build ring the two
-// operands the transform warps make from a0 (p, m: 2 x 32 KB), so that the
-// loads are not held back while operands are built and consumed.
-constexpr int D_STAGES = 8;              // TMA ring
-constexpr int D_BUILD = 2;               // p | m ring
+constexpr int D_STAGES = 4;
 constexpr int DBK = 32;                  // rows per stage
 constexpr uint32_t DX = 4 * 4096;        // one operand: 4 boxes of 64 features x 32 rows (bf16 MN-major SW128)
 constexpr uint32_t DB = 4096;            // da1: 64 x 32 rows
-constexpr uint32_t DSTG = DX + DB;       // TMA stage: a0 (as loaded) | da1
-constexpr uint32_t DBLD = 2 * DX;        // build stage: p | m
-constexpr size_t D_SMEM = 1024 + D_STAGES * DSTG + D_BUILD * DBLD + 256;
+constexpr uint32_t DSTG = 3 * DX + DB;   // a0 (as loaded) | p | m | da1
+constexpr size_t D_SMEM = 1024 + D_STAGES * DSTG + 256;
 constexpr int D_THREADS = 192;  // w0-3 transform + epilogue, w4 MMA, w5 TMA
 constexpr int G_PART = 3 * 64 * 256;
-static_assert(D_SMEM <= 232448, "k_dw1b shared memory");
 
 __global__ void __launch_bounds__(D_THREADS, 1)
     k_dw1b(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmD,
@@ -554,17 +547,13 @@ __global__ void __launch_bounds__(D_THREADS, 1)
   }
   extern __shared__ uint8_t raw[];
   const uint32_t r0 = smem_u32(raw), base = (r0 + 1023u) & ~1023u;
-  const uint32_t bld = base + D_STAGES * DSTG;  // build ring
-  const uint32_t full = bld + D_BUILD * DBLD, empty = full + 8 * D_STAGES, ready = empty + 8 * D_STAGES,
-                 bfree = ready + 8 * D_BUILD, accb = bfree + 8 * D_BUILD, slot = accb + 8;
+  const uint32_t full = base + D_STAGES * DSTG, ready = full + 8 * D_STAGES, empty = ready + 8 * D_STAGES,
+                 accb = empty + 8 * D_STAGES, slot = accb + 8;
   if (t == 0) {
     for (int i = 0; i < D_STAGES; ++i) {
       mbar_init(full + 8 * i, 1);
-      mbar_init(empty + 8 * i, 1);
-    }
-    for (int i = 0; i < D_BUILD; ++i) {
       mbar_init(ready + 8 * i, 128);
-      mbar_init(bfree + 8 * i, 1);
+      mbar_init(empty + 8 * i, 1);
     }
     mbar_init(accb, 1);
     fence_mbar_init();
@@ -589,29 +578,26 @@ __global__ void __launch_bounds__(D_THREADS, 1)
         const int row = rb + kb * DBK;
 #pragma unroll
         for (int j = 0; j < 4; ++j) tma_load_2d(a + j * 4096, &tmH, full + 8 * s, j * 64, row);
-        tma_load_2d(a + DX, &tmD, full + 8 * s, 0, row);
+        tma_load_2d(a + 3 * DX, &tmD, full + 8 * s, 0, row);
       }
     }
   } else if (warp == 4) {
     if (lane == 0) {
       const uint32_t idesc = instr_desc(1, 128, 64, 1, 1);
       for (int kb = 0; kb < nk; ++kb) {
-        const uint32_t s = kb % D_STAGES, sb = kb % D_BUILD;
-        mbar_wait(ready + 8 * sb, (kb / D_BUILD) & 1);
+        const uint32_t s = kb % D_STAGES, itn = kb / D_STAGES;
+        mbar_wait(ready + 8 * s, itn & 1);
         tc_fence_after();
-        const uint32_t a = base + s * DSTG, b = a + DX, pm = bld + sb * DBLD;
-        // operand x: 0 = a0 (TMA stage), 1 = p, 2 = m (build stage)
+        const uint32_t a = base + s * DSTG, b = a + 3 * DX;
 #pragma unroll
         for (int x = 0; x < 3; ++x)
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int k = 0; k < DBK / 16; ++k)
-              mma<1>(tmem + x * 128 + h * 64,
-                     smem_desc((x == 0 ? a : pm + (x - 1) * DX) + h * 8192 + k * 2048, 4096, 1024, 2),
+              mma<1>(tmem + x * 128 + h * 64, smem_desc(a + x * DX + h * 8192 + k * 2048, 4096, 1024, 2),
                      smem_desc(b + k * 2048, 4096, 1024, 2), idesc, (kb | k) != 0);
         mma_commit(empty + 8 * s);
-        mma_commit(bfree + 8 * sb);
       }
       mma_commit(accb);
     }
@@ -620,11 +606,9 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     // t&7 of rows (t>>3) and (t>>3)+16 of every box
     const int c = t & 7, rlo = t >> 3;
     for (int kb = 0; kb < nk; ++kb) {
-      const uint32_t s = kb % D_STAGES, sb = kb % D_BUILD;
-      mbar_wait(full + 8 * s, (kb / D_STAGES) & 1);
-      mbar_wait(bfree + 8 * sb, ((kb / D_BUILD) & 1) ^ 1);
+      const uint32_t s = kb % D_STAGES, itn = kb / D_STAGES;
+      mbar_wait(full + 8 * s, itn & 1);
       uint8_t* a = raw + (base + s * DSTG - r0);
-      uint8_t* pm = raw + (bld + sb * DBLD - r0);
       const int row0 = rb + kb * DBK;
 #pragma unroll
       for (int j = 0; j < 4; ++j)
@@ -645,11 +629,11 @@ __global__ void __launch_bounds__(D_THREADS, 1)
           // a0 itself is the third operand (Ga = a0^T da1); rows outside this
           // CTA's range are zeroed so that no operand picks them up
           if (!valid) *reinterpret_cast<uint4*>(a + off) = make_uint4(0u, 0u, 0u, 0u);
-          *reinterpret_cast<uint4*>(pm + off) = make_uint4(pp[0], pp[1], pp[2], pp[3]);
-          *reinterpret_cast<uint4*>(pm + DX + off) = make_uint4(mm[0], mm[1], mm[2], mm[3]);
+          *reinterpret_cast<uint4*>(a + DX + off) = make_uint4(pp[0], pp[1], pp[2], pp[3]);
+          *reinterpret_cast<uint4*>(a + 2 * DX + off) = make_uint4(mm[0], mm[1], mm[2], mm[3]);
         }
       fence_proxy_async();
-      mbar_arrive(ready + 8 * sb);
+      mbar_arrive(ready + 8 * s);
     }
     mbar_wait(accb, 0);
     tc_fence_after();
