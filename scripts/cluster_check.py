@@ -47,6 +47,7 @@ def main():
     ap.add_argument("--full-model", action="store_true")
     ap.add_argument("--short-last", action="store_true")
     ap.add_argument("--ckpt", default="")
+    ap.add_argument("--zipf", type=float, default=0.0, help="Zipf image keys (hot keys: the chunked hot-key passes)")
     a = ap.parse_args()
     kind, precision = a.kind, a.precision
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -87,7 +88,7 @@ def main():
     sizes = [U] * iters
     if a.short_last:
         sizes[-1] = bpw // 2  # only worker 0 gets samples: every other GPU trains an empty slice
-    unions = [synthetic_batch(rng, schema, n, rng.integers(0, 31, n), P) for n in sizes]
+    unions = [synthetic_batch(rng, schema, n, rng.integers(0, 31, n), P, zipf=a.zipf or None) for n in sizes]
     out = []
     for i, u in enumerate(unions):
         out.append(cl.run_iteration(u, digests=True))

@@ -47,8 +47,9 @@ def test_cluster_matches_oracle_on_union(kind, precision, mode):
 
 
 @pytest.mark.parametrize("extra", [["--workers", "3", "--servers", "5"], ["--workers", "8", "--servers", "1"],
-                                   ["--full-model"], ["--short-last"], ["--workers", "1", "--servers", "3"]],
-                         ids=["m3n5", "m8n1", "full-model", "short-last", "m1n3"])
+                                   ["--full-model"], ["--short-last"], ["--workers", "1", "--servers", "3"],
+                                   ["--zipf", "1.1"]],
+                         ids=["m3n5", "m8n1", "full-model", "short-last", "m1n3", "zipf-hot-keys"])
 def test_cluster_topologies_match_oracle(extra):
     """Logical workers / servers mapped onto the GPUs (reference
     tests/test_runtime.py:46-59 runs M = 4, N = 2): results equal the
