@@ -20,7 +20,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROBE = {"k_fwd": "img_fwd_l0", "k_fwd2": "img_fwd_l0", "k_fwd4": "img_fwd_l0", "k_l12_fwd": "img_fwd_l12", "k_l12f": "img_fwd_l12",
          "k_l12_bwd": "img_bwd_l12", "k_l12b": "img_bwd_l12", "k_dw1": "img_bwd_dw1", "k_dw1b": "img_bwd_dw1",
-         "k_dw0": "img_bwd_dw0", "k_sample_fwd": "sample_fwd", "k_sample_bwd": "sample_bwd",
+         "k_dw0": "img_bwd_dw0", "k_dw0p": "img_bwd_dw0", "k_sample_fwd": "sample_fwd", "k_sample_bwd": "sample_bwd",
          "k_attn_bwd": "sample_bwd", "k_sample_scatter": "sample_bwd"}
 METRICS = [
     ("gpu__time_duration.sum", "time"),
