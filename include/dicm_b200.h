@@ -90,6 +90,12 @@ size_t dicm_dedup_workspace(int64_t key_space);
 int dicm_dedup(const dicm_keyseg_t* segs, int nseg, int64_t key_space, void* workspace,
                size_t workspace_bytes, int32_t* uniq_out, int32_t* inv_out, int32_t* count_dev,
                int32_t tag, int32_t* status, dicm_stream_t stream);
+/* inv_out = NULL above leaves the inverse to this call, which may run on
+ * another stream (after dicm_dedup, before the workspace is reused): the
+ * step launches the image-MLP forward on the unique keys while the inverse
+ * (needed only by the per-sample kernels) is formed beside it. */
+int dicm_dedup_inverse(const dicm_keyseg_t* segs, int nseg, int64_t key_space, const void* workspace,
+                       size_t workspace_bytes, int32_t* inv_out, dicm_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * a3: the image pool -- 4096-d feature rows resident in HBM.

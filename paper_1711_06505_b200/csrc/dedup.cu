@@ -211,16 +211,13 @@ size_t dicm_dedup_workspace(int64_t key_space) {
   return (size_t)(W * 4 * 2 + (W / kTile) * 4 + 256);
 }
 
-int dicm_dedup(const dicm_keyseg_t* segs, int nseg, int64_t key_space, void* workspace,
-               size_t workspace_bytes, int32_t* uniq_out, int32_t* inv_out, int32_t* count_dev,
-               int32_t tag, int32_t* status, dicm_stream_t stream) {
+static int make_segs(const dicm_keyseg_t* segs, int nseg, int64_t key_space, size_t workspace_bytes, Segs& s) {
   using namespace dicm;
-  cudaStream_t st = (cudaStream_t)stream;
   if (nseg < 1 || nseg > DICM_MAX_SEGS) return fail(DICM_ERR_VALUE, "dedup: nseg %d not in [1, %d]", nseg, DICM_MAX_SEGS);
   if (key_space < 1 || key_space > (int64_t)1 << 31)
     return fail(DICM_ERR_VALUE, "dedup: key space %lld outside [1, 2^31]", (long long)key_space);
   if (workspace_bytes < dicm_dedup_workspace(key_space)) return fail(DICM_ERR_VALUE, "dedup: workspace too small");
-  Segs s{};
+  s = Segs{};
   s.nseg = nseg;
   s.start[0] = 0;
   for (int i = 0; i < nseg; ++i) {
@@ -233,7 +230,29 @@ int dicm_dedup(const dicm_keyseg_t* segs, int nseg, int64_t key_space, void* wor
       return fail(DICM_ERR_VALUE, "dedup: segment %d [%lld, +%lld) exceeds key space %lld", i,
                   (long long)segs[i].base, (long long)segs[i].vocab, (long long)key_space);
   }
-  return run_dedup(s, key_space, workspace, uniq_out, inv_out, count_dev, tag, status, st);
+  return DICM_OK;
+}
+
+int dicm_dedup(const dicm_keyseg_t* segs, int nseg, int64_t key_space, void* workspace,
+               size_t workspace_bytes, int32_t* uniq_out, int32_t* inv_out, int32_t* count_dev,
+               int32_t tag, int32_t* status, dicm_stream_t stream) {
+  Segs s;
+  if (int rc = make_segs(segs, nseg, key_space, workspace_bytes, s)) return rc;
+  return run_dedup(s, key_space, workspace, uniq_out, inv_out, count_dev, tag, status, (cudaStream_t)stream);
+}
+
+int dicm_dedup_inverse(const dicm_keyseg_t* segs, int nseg, int64_t key_space, const void* workspace,
+                       size_t workspace_bytes, int32_t* inv_out, dicm_stream_t stream) {
+  using namespace dicm;
+  Segs s;
+  if (int rc = make_segs(segs, nseg, key_space, workspace_bytes, s)) return rc;
+  const int64_t total = s.start[nseg];
+  if (total <= 0) return DICM_OK;
+  const int64_t W = padded_words(key_space);
+  const uint32_t* bitmap = (const uint32_t*)workspace;
+  const int32_t* word_prefix = (const int32_t*)(bitmap + W);
+  k_inverse<<<dicm_grid(total, 256, 148 * 32), 256, 0, (cudaStream_t)stream>>>(s, bitmap, word_prefix, inv_out);
+  return last_launch("dicm_dedup_inverse");
 }
 
 int dicm_dedup_devn(const int32_t* keys, const int32_t* n_dev, int64_t n_max, int64_t vocab, void* workspace,
@@ -271,7 +290,7 @@ int run_dedup(const Segs& s, int64_t key_space, void* workspace, int32_t* uniq_o
   k_tile_sums<<<ntiles, kScanThreads, 0, st>>>(bitmap, tile_sums);
   k_scan_tiles<<<1, kScanThreads, 0, st>>>(tile_sums, ntiles, count_dev);
   k_emit<<<ntiles, kScanThreads, 0, st>>>(bitmap, tile_sums, word_prefix, uniq_out);
-  if (total > 0)
+  if (total > 0 && inv_out)
     k_inverse<<<dicm_grid(total, 256, 148 * 32), 256, 0, st>>>(s, bitmap, word_prefix, inv_out);
   return last_launch("dicm_dedup");
 }

@@ -13,10 +13,14 @@
 // thread parses its chunk into private columns, which are concatenated in
 // chunk order, so the result does not depend on the thread count.
 #include <algorithm>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -28,6 +32,62 @@ int fail(int code, const char* fmt, ...);
 }
 
 namespace {
+
+// A persistent worker pool for the per-step host copies: pool_run(n, fn)
+// calls fn(0..n-1), fn(0) on the caller, the rest on pool threads created
+// once (a step no longer pays thread creation).  One caller at a time.
+class Pool {
+ public:
+  void run(int n, const std::function<void(int)>& fn) {
+    std::unique_lock<std::mutex> call(call_m_);
+    {
+      std::unique_lock<std::mutex> lk(m_);
+      while ((int)th_.size() < n - 1) {
+        const int id = (int)th_.size() + 1;
+        th_.emplace_back([this, id] { loop(id); });
+        th_.back().detach();
+      }
+      fn_ = &fn;
+      n_ = n;
+      left_ = n - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0);
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [this] { return left_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void loop(int id) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* f;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (id >= n_) continue;
+        f = fn_;
+      }
+      (*f)(id);
+      std::unique_lock<std::mutex> lk(m_);
+      if (--left_ == 0) done_.notify_one();
+    }
+  }
+  std::mutex call_m_, m_;
+  std::condition_variable cv_, done_;
+  std::vector<std::thread> th_;
+  const std::function<void(int)>* fn_ = nullptr;
+  int n_ = 0, left_ = 0;
+  uint64_t gen_ = 0;
+};
+
+void pool_run(int n, const std::function<void(int)>& fn) {
+  static Pool* pool = new Pool();  // never destroyed: detached workers outlive static destructors
+  pool->run(n, fn);
+}
 
 struct Col {
   bool list = false;
@@ -301,7 +361,14 @@ int dicm_host_pack(void* dst, const void* const* srcs, const int64_t* bytes, con
                    int nthreads) {
   int64_t total = 0;
   for (int i = 0; i < n; ++i) total += bytes[i];
-  int nt = nthreads > 0 ? nthreads : (int)std::max(1u, std::thread::hardware_concurrency());
+  // a handful of threads saturate a host's memcpy bandwidth; more only add
+  // contention when every GPU's rank packs at once (DICM_HOST_THREADS overrides)
+  static const int def_threads = [] {
+    const char* e = getenv("DICM_HOST_THREADS");
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    return e && atoi(e) > 0 ? atoi(e) : std::min(hw, 4);
+  }();
+  int nt = nthreads > 0 ? nthreads : def_threads;
   nt = (int)std::max<int64_t>(1, std::min<int64_t>(nt, total / (256 << 10) + 1));
   auto work = [&](int64_t lo, int64_t hi) {  // byte range [lo, hi) of the concatenated segments
     int64_t pos = 0;
@@ -316,10 +383,7 @@ int dicm_host_pack(void* dst, const void* const* srcs, const int64_t* bytes, con
     work(0, total);
     return DICM_OK;
   }
-  std::vector<std::thread> th;
-  for (int t = 1; t < nt; ++t) th.emplace_back(work, total * t / nt, total * (t + 1) / nt);
-  work(0, total / nt);
-  for (auto& x : th) x.join();
+  pool_run(nt, [&](int t) { work(total * t / nt, total * (t + 1) / nt); });
   return DICM_OK;
 }
 

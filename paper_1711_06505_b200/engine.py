@@ -581,8 +581,9 @@ class StepEngine:
         self._dptr = lambda off: base_ptr + 4 * off
         self.s = L.stream_handle()
 
-    def _dedup_images(self):
-        """a2 over the image keys (model.py:182-187) -> uniq_img, inv_img, counts[0]."""
+    def _dedup_images(self, inverse=True):
+        """a2 over the image keys (model.py:182-187) -> uniq_img, inv_img, counts[0]
+        (``inverse=False``: inv_img is left to ``_inverse_images``)."""
         lay, pk = self.model.layout, self.pk
         segs, inv_off = [], 0
         space = self.pool.global_size if getattr(self, "world", 1) > 1 else self.image_key_space
@@ -593,10 +594,17 @@ class StepEngine:
             segs.append(L.KeySeg(self._dptr(pk.beh), pk.R, 0, space, inv_off))
         self.n_img_segs = len(segs)
         if segs:
-            arr = (L.KeySeg * len(segs))(*segs)
-            L.check(L.lib.dicm_dedup(arr, len(segs), space, self.ws_img.data_ptr(), self.ws_img.numel(),
-                                     self.uniq_img.data_ptr(), self.inv_img.data_ptr(), self.counts.data_ptr(), 0,
-                                     self.status.data_ptr(), self.s))
+            arr = self._img_segs = ((L.KeySeg * len(segs))(*segs), len(segs), space)
+            L.check(L.lib.dicm_dedup(arr[0], len(segs), space, self.ws_img.data_ptr(), self.ws_img.numel(),
+                                     self.uniq_img.data_ptr(), self.inv_img.data_ptr() if inverse else None,
+                                     self.counts.data_ptr(), 0, self.status.data_ptr(), self.s))
+
+    def _inverse_images(self):
+        """The image inverse of the last ``_dedup_images(inverse=False)``."""
+        if self.n_img_segs:
+            arr, n, space = self._img_segs
+            L.check(L.lib.dicm_dedup_inverse(arr, n, space, self.ws_img.data_ptr(), self.ws_img.numel(),
+                                             self.inv_img.data_ptr(), self.s))
 
     def _dedup_ids(self):
         """a2 over every ID field (Batch.unique_field_ids, model.py:152-155)."""
@@ -785,15 +793,20 @@ class StepEngine:
                                               self.s))
                 self._transpose_ids()
             self.s = main
-            self._dedup_images()
-            # the image transpose runs on the branch too, beside the image-MLP forward
+            self._dedup_images(inverse=False)
+            # the image inverse and its transpose run on the branch, beside the
+            # image-MLP forward (which needs only the unique keys)
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):
                 self.s = side.cuda_stream
+                self._inverse_images()
+                inv_ready = torch.cuda.Event()
+                inv_ready.record(side)
                 self._transpose_images()
             self.s = main
             if self.n_img_segs:
                 self._image_forward(self.net, self.uniq_img, self.counts.data_ptr())
+            torch.cuda.current_stream().wait_event(inv_ready)  # the per-sample kernels read inv_img
             if self.model.layout.multiquery:  # the ID query rows of the second channel
                 torch.cuda.current_stream().wait_event(ids_ready)
             L.check(L.lib.dicm_images_fwd(C.byref(self.layout), C.byref(self._bv), self.attn, self.head_in.data_ptr(),

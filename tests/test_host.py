@@ -158,7 +158,7 @@ def test_host_pack_matches_numpy_layout():
     for a, o in zip(arrs, offs):
         ref[o:o + len(a)] = a
     n = len(arrs)
-    for nt in (1, 3, 0):
+    for nt in (1, 3, 0, 8, 2, 0, 5):  # the persistent pool grows and is reused
         out = np.zeros(total, np.int32)
         L.check(L.lib.dicm_host_pack(out.ctypes.data, (ctypes.c_void_p * n)(*[a.ctypes.data for a in arrs]),
                                      (ctypes.c_int64 * n)(*[a.nbytes for a in arrs]),
