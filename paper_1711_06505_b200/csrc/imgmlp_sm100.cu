@@ -532,6 +532,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F4, 1)
       mbar_wait(accf, tl & 1);
       tc_fence_after();
       const int m0 = tile * 512 + sub * 256 + (int)rank * 128 + q * 32;
+#ifdef DICM_FWD4_NODRAIN  // measurement build only: no drain at all
+      if (false)
+#endif
 #pragma unroll 1
       for (int cb = 0; cb < 8; ++cb) {
         float v[32];
