@@ -532,15 +532,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F4, 1)
       mbar_wait(accf, tl & 1);
       tc_fence_after();
       const int m0 = tile * 512 + sub * 256 + (int)rank * 128 + q * 32;
-#ifdef DICM_FWD4_NODRAIN  // measurement build only: no drain at all
-      if (false)
-#endif
-#pragma unroll 1
-      for (int cb = 0; cb < 8; ++cb) {
+      // one 32-column block: bias, then bf16/fp32 rows of act0
+      auto emit = [&](int cb, uint32_t (&r)[32]) {
         float v[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + sub * 256 + cb * 32, v);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] += __ldg(bias + cb * 32 + j);
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + __ldg(bias + cb * 32 + j);
 #ifdef DICM_FWD4_NOSTORE  // measurement build only: the drain without its act0 stores
         if (v[0] == 12345.f) reinterpret_cast<float*>(act0_)[0] = v[lane];  // keeps the TMEM loads live
         if (false)
@@ -573,10 +569,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F4, 1)
             for (int q4 = 0; q4 < 8; ++q4) o[q4] = make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
           }
         }
+      };
+      // the TMEM loads are software-pipelined one block ahead of the
+      // processing, and the accumulator is released (acce) as soon as its last
+      // block is in registers, before that block is processed
+      const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + sub * 256;
+      uint32_t ra[32], rb[32];
+      tmem_ld32_issue(tb, ra);
+      tmem_ld_wait(ra);
+#pragma unroll 1
+      for (int cb = 0; cb < 8; cb += 2) {
+        tmem_ld32_issue(tb + (cb + 1) * 32, rb);
+        emit(cb, ra);
+        tmem_ld_wait(rb);
+        if (cb + 2 < 8) {
+          tmem_ld32_issue(tb + (cb + 2) * 32, ra);
+          emit(cb + 1, rb);
+          tmem_ld_wait(ra);
+        } else {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(lacce);
+          emit(cb + 1, rb);
+        }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(lacce);
     }
   }
   tc_fence_before();
@@ -1029,7 +1045,9 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
     // default: 512-row pair tiles (k_fwd4); DICM_FWD4=0 selects the 256-row
     // tiles with double-buffered accumulators (k_fwd2)
     static const bool four = !(getenv("DICM_FWD4") && getenv("DICM_FWD4")[0] == '0');
-    static int a44 = -1, t44 = -1;
+    // DICM_FWD4_SCR=0: each lane stores its own act0 row (no shared-memory transposes)
+    static const bool scr = !(getenv("DICM_FWD4_SCR") && getenv("DICM_FWD4_SCR")[0] == '0');
+    static int a44 = -1, t44 = -1, a44n = -1;
     auto launch4 = [&](auto kern, size_t bytes, int& attr) -> int {
       if (attr < 0)
         attr = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes),
@@ -1040,7 +1058,8 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
       return 0;
     };
     const int probe_slot = probe_begin(DICM_PROBE_IMG_FWD_L0, st);
-    const int lrc = four ? (bf16 ? launch4(k_fwd4<1, 4, 4, true>, smem4(4, 4, true), a44)
+    const int lrc = four ? (bf16 ? (scr ? launch4(k_fwd4<1, 4, 4, true>, smem4(4, 4, true), a44)
+                                        : launch4(k_fwd4<1, 4, 4, false>, smem4(4, 4, false), a44n))
                                  : launch4(k_fwd4<0, 4, 4, true>, smem4(4, 4, true), t44))
                          : (bf16 ? launch(k_fwd2<1, 6, 6>, smem2(6, 6), a66) : launch(k_fwd2<0, 6, 6>, smem2(6, 6), t66));
     probe_end(probe_slot, st);
