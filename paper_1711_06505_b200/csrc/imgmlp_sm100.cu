@@ -538,7 +538,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F4, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + __ldg(bias + cb * 32 + j);
 #ifdef DICM_FWD4_NOSTORE  // measurement build only: the drain without its act0 stores
-        if (v[0] == 12345.f) reinterpret_cast<float*>(act0_)[0] = v[lane];  // keeps the TMEM loads live
+        float keep = 0.f;  // keeps the TMEM loads and bias adds live (no dynamic index: no local memory)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) keep += v[j];
+        if (keep == 12345.f) reinterpret_cast<float*>(act0_)[0] = keep;
         if (false)
 #endif
         if constexpr (SCR) {
