@@ -392,17 +392,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F, 1)
 // gather ring keeps filling.
 // ---------------------------------------------------------------------------
 constexpr int THREADS_F4 = 448;  // w0-3 gather, w4 MMA / relay, w5 TMA, w6-13 epilogue
-__host__ __device__ constexpr size_t smem4(int sa, int sb, bool scr) {
-  return (size_t)sa * 2 * OPB2 + (size_t)sb * OPB2 + 1024 + 256 + (scr ? 8 * epi::SCRATCH_FLOATS * 4 : 0);
+constexpr uint32_t STG4 = 8 * 4096;  // EPI 2: one 32-row x 128-B TMA-store staging box per epilogue warp
+__host__ __device__ constexpr size_t smem4(int sa, int sb, int epi_mode) {
+  return (size_t)sa * 2 * OPB2 + (size_t)sb * OPB2 + 1024 + 256 +
+         (epi_mode == 1 ? 8 * epi::SCRATCH_FLOATS * 4 : epi_mode == 2 ? STG4 : 0);
 }
 
-// SCR: transpose each 32x32 block through shared memory for whole-line stores;
-// without it the ring gets the space and every lane stores its own row
-template <int KIND, int SA, int SB, bool SCR>
+// EPI: how the epilogue writes act0.  1: each 32x32 block transposed through
+// shared memory for whole-line stores; 0: every lane stores its own row;
+// 2 (bf16): two blocks (64 columns) converted into a swizzled staging box and
+// written by one TMA store (cp.async.bulk.tensor), so the drain issues no
+// global stores of its own
+template <int KIND, int SA, int SB, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F4, 1)
-    k_fwd4(const __grid_constant__ CUtensorMap tmW, const void* __restrict__ pool_, int d_raw,
-           const int32_t* __restrict__ rows, const int32_t* __restrict__ count, const float* __restrict__ bias,
-           void* __restrict__ act0_) {
+    k_fwd4(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmO,
+           const void* __restrict__ pool_, int d_raw, const int32_t* __restrict__ rows,
+           const int32_t* __restrict__ count, const float* __restrict__ bias, void* __restrict__ act0_) {
+  constexpr bool SCR = EPI == 1;
+  static_assert(EPI != 2 || KIND == 1, "the TMA-store epilogue writes bf16 act0");
   using T = Elem<KIND>;
   constexpr int EPB = 128 / sizeof(T);
   constexpr uint32_t ASTG = 2 * OPB2;  // two sub-tiles of 128 rows
@@ -414,7 +421,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F4, 1)
   extern __shared__ uint8_t smem_raw[];
   const uint32_t r0s = smem_u32(smem_raw);
   const uint32_t base = (r0s + 1023u) & ~1023u, bbase = base + SA * ASTG;
-  const uint32_t fullA = bbase + SB * OPB2, emptyA = fullA + 8 * SA, fullB = emptyA + 8 * SA,
+  const uint32_t stg = bbase + SB * OPB2;  // EPI 2 staging (1024-B aligned)
+  const uint32_t fullA = stg + (EPI == 2 ? STG4 : 0), emptyA = fullA + 8 * SA, fullB = emptyA + 8 * SA,
                  emptyB = fullB + 8 * SB, accf = emptyB + 8 * SB, acce = accf + 8, slot = acce + 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -573,10 +581,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F4, 1)
           }
         }
       };
+      const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + sub * 256;
+      if constexpr (EPI == 2) {
+        // per pair of blocks: both in registers, bias, bf16 into this warp's
+        // staging box (row = lane, 16-B chunk c at c ^ (lane & 7): SWIZZLE_128B),
+        // one TMA store of 32 rows x 64 columns; the accumulator is released
+        // once the last pair is in registers
+        const uint32_t box = stg + (uint32_t)(warp - 6) * 4096;
+        uint32_t ra[32], rb[32];
+#pragma unroll 1
+        for (int cb = 0; cb < 8; cb += 2) {
+          tmem_ld32_issue(tb + cb * 32, ra);
+          tmem_ld32_issue(tb + (cb + 1) * 32, rb);
+          tmem_ld_wait(ra);
+          tmem_ld_wait(rb);
+          if (cb == 6) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(lacce);
+          }
+          if (lane == 0) bulk_wait_read0();  // the previous store has read the box
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int j = (8 * c + 2 * e) & 31;  // column within its block
+              const float x0 = __uint_as_float(c < 4 ? ra[j] : rb[j]) + __ldg(bias + cb * 32 + 8 * c + 2 * e);
+              const float x1 = __uint_as_float(c < 4 ? ra[j + 1] : rb[j + 1]) + __ldg(bias + cb * 32 + 8 * c + 2 * e + 1);
+              __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+              w[e] = *reinterpret_cast<uint32_t*>(&h);
+            }
+            st_shared_v4(box + lane * 128 + ((c ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmO, box, cb * 32, m0);
+            bulk_commit();
+          }
+        }
+        continue;
+      }
       // the TMEM loads are software-pipelined one block ahead of the
       // processing, and the accumulator is released (acce) as soon as its last
       // block is in registers, before that block is processed
-      const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + sub * 256;
       uint32_t ra[32], rb[32];
       tmem_ld32_issue(tb, ra);
       tmem_ld_wait(ra);
@@ -597,6 +647,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F4, 1)
         }
       }
     }
+    if constexpr (EPI == 2)
+      if (lane == 0) bulk_wait0();  // every act0 store of this warp has completed
   }
   tc_fence_before();
   cluster_sync();
@@ -1048,22 +1100,28 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
     // default: 512-row pair tiles (k_fwd4); DICM_FWD4=0 selects the 256-row
     // tiles with double-buffered accumulators (k_fwd2)
     static const bool four = !(getenv("DICM_FWD4") && getenv("DICM_FWD4")[0] == '0');
-    // DICM_FWD4_SCR=0: each lane stores its own act0 row (no shared-memory transposes)
-    static const bool scr = !(getenv("DICM_FWD4_SCR") && getenv("DICM_FWD4_SCR")[0] == '0');
-    static int a44 = -1, t44 = -1, a44n = -1;
+    // DICM_FWD4_EPI: act0 epilogue mode (see k_fwd4): 1 (default), 0, 2 (TMA store)
+    static const int epi_mode = [] {
+      const char* e = getenv("DICM_FWD4_EPI");
+      return e && (e[0] == '0' || e[0] == '2') ? e[0] - '0' : 1;
+    }();
+    static int a44 = -1, t44 = -1, a44n = -1, a44t = -1;
+    CUtensorMap omap{};
+    if (bf16 && epi_mode == 2 && (rc = make_map(&omap, act0, true, (uint64_t)rows_max, 256, 32))) return rc;
     auto launch4 = [&](auto kern, size_t bytes, int& attr) -> int {
       if (attr < 0)
         attr = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes),
                           "k_fwd4 smem");
       if (attr) return attr;
       const int grid4 = 2 * (int)std::min<int64_t>(std::max<int64_t>(dicm_grid_cap() / 2, 1), (rows_max + 511) / 512);
-      kern<<<grid4, THREADS_F4, bytes, st>>>(map, pool, d_raw, rows, count, b0, act0);
+      kern<<<grid4, THREADS_F4, bytes, st>>>(map, omap, pool, d_raw, rows, count, b0, act0);
       return 0;
     };
     const int probe_slot = probe_begin(DICM_PROBE_IMG_FWD_L0, st);
-    const int lrc = four ? (bf16 ? (scr ? launch4(k_fwd4<1, 4, 4, true>, smem4(4, 4, true), a44)
-                                        : launch4(k_fwd4<1, 4, 4, false>, smem4(4, 4, false), a44n))
-                                 : launch4(k_fwd4<0, 4, 4, true>, smem4(4, 4, true), t44))
+    const int lrc = four ? (bf16 ? (epi_mode == 1   ? launch4(k_fwd4<1, 4, 4, 1>, smem4(4, 4, 1), a44)
+                                    : epi_mode == 2 ? launch4(k_fwd4<1, 4, 4, 2>, smem4(4, 4, 2), a44t)
+                                                    : launch4(k_fwd4<1, 4, 4, 0>, smem4(4, 4, 0), a44n))
+                                 : launch4(k_fwd4<0, 4, 4, 1>, smem4(4, 4, 1), t44))
                          : (bf16 ? launch(k_fwd2<1, 6, 6>, smem2(6, 6), a66) : launch(k_fwd2<0, 6, 6>, smem2(6, 6), t66));
     probe_end(probe_slot, st);
     if (lrc) return lrc;
