@@ -600,6 +600,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F4, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(lacce);
           }
+          // a box reaching past the count (the last tile) is stored row by row
+          // instead: rows >= U stay untouched
+          const bool whole = m0 + 32 <= U;
           if (lane == 0) bulk_wait_read0();  // the previous store has read the box
           __syncwarp();
 #pragma unroll
@@ -613,13 +616,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F4, 1)
               __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
               w[e] = *reinterpret_cast<uint32_t*>(&h);
             }
-            st_shared_v4(box + lane * 128 + ((c ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
+            if (whole)
+              st_shared_v4(box + lane * 128 + ((c ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
+            else if (m0 + lane < U)
+              reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(act0_) + (int64_t)(m0 + lane) * 256 +
+                                       cb * 32)[c] = make_uint4(w[0], w[1], w[2], w[3]);
           }
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&tmO, box, cb * 32, m0);
-            bulk_commit();
+          if (whole) {
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmO, box, cb * 32, m0);
+              bulk_commit();
+            }
           }
         }
         continue;
@@ -1100,10 +1109,10 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
     // default: 512-row pair tiles (k_fwd4); DICM_FWD4=0 selects the 256-row
     // tiles with double-buffered accumulators (k_fwd2)
     static const bool four = !(getenv("DICM_FWD4") && getenv("DICM_FWD4")[0] == '0');
-    // DICM_FWD4_EPI: act0 epilogue mode (see k_fwd4): 1 (default), 0, 2 (TMA store)
+    // DICM_FWD4_EPI: act0 epilogue mode (see k_fwd4): 2 (TMA store, default), 1, 0
     static const int epi_mode = [] {
       const char* e = getenv("DICM_FWD4_EPI");
-      return e && (e[0] == '0' || e[0] == '2') ? e[0] - '0' : 1;
+      return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : 2;
     }();
     static int a44 = -1, t44 = -1, a44n = -1, a44t = -1;
     CUtensorMap omap{};
