@@ -608,11 +608,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F4, 1)
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             uint32_t w[4];
+            // bias of the chunk's 8 columns: two 16-B uniform loads (b0 is 16-B aligned)
+            const float4 bl = __ldg(reinterpret_cast<const float4*>(bias + cb * 32 + 8 * c));
+            const float4 bh = __ldg(reinterpret_cast<const float4*>(bias + cb * 32 + 8 * c + 4));
+            const float bv[8] = {bl.x, bl.y, bl.z, bl.w, bh.x, bh.y, bh.z, bh.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int j = (8 * c + 2 * e) & 31;  // column within its block
-              const float x0 = __uint_as_float(c < 4 ? ra[j] : rb[j]) + __ldg(bias + cb * 32 + 8 * c + 2 * e);
-              const float x1 = __uint_as_float(c < 4 ? ra[j + 1] : rb[j + 1]) + __ldg(bias + cb * 32 + 8 * c + 2 * e + 1);
+              const float x0 = __uint_as_float(c < 4 ? ra[j] : rb[j]) + bv[2 * e];
+              const float x1 = __uint_as_float(c < 4 ? ra[j + 1] : rb[j + 1]) + bv[2 * e + 1];
               __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
               w[e] = *reinterpret_cast<uint32_t*>(&h);
             }
@@ -1115,8 +1119,10 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
       return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : 2;
     }();
     static int a44 = -1, t44 = -1, a44n = -1, a44t = -1;
+    // the TMA-store epilogue reads the bias as float4: an unaligned b0 takes mode 1
+    const int em = (epi_mode == 2 && ((uintptr_t)b0 & 15)) ? 1 : epi_mode;
     CUtensorMap omap{};
-    if (bf16 && epi_mode == 2 && (rc = make_map(&omap, act0, true, (uint64_t)rows_max, 256, 32))) return rc;
+    if (bf16 && em == 2 && (rc = make_map(&omap, act0, true, (uint64_t)rows_max, 256, 32))) return rc;
     auto launch4 = [&](auto kern, size_t bytes, int& attr) -> int {
       if (attr < 0)
         attr = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes),
@@ -1127,8 +1133,8 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
       return 0;
     };
     const int probe_slot = probe_begin(DICM_PROBE_IMG_FWD_L0, st);
-    const int lrc = four ? (bf16 ? (epi_mode == 1   ? launch4(k_fwd4<1, 4, 4, 1>, smem4(4, 4, 1), a44)
-                                    : epi_mode == 2 ? launch4(k_fwd4<1, 4, 4, 2>, smem4(4, 4, 2), a44t)
+    const int lrc = four ? (bf16 ? (em == 1   ? launch4(k_fwd4<1, 4, 4, 1>, smem4(4, 4, 1), a44)
+                                    : em == 2 ? launch4(k_fwd4<1, 4, 4, 2>, smem4(4, 4, 2), a44t)
                                                     : launch4(k_fwd4<1, 4, 4, 0>, smem4(4, 4, 0), a44n))
                                  : launch4(k_fwd4<0, 4, 4, 1>, smem4(4, 4, 1), t44))
                          : (bf16 ? launch(k_fwd2<1, 6, 6>, smem2(6, 6), a66) : launch(k_fwd2<0, 6, 6>, smem2(6, 6), t66));

@@ -1,0 +1,4 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/test_gpu_bench_shapes.py tests/test_gpu_tensorcore.py tests/test_gpu_step.py tests/test_gpu_kernels.py -x -q > gpurun_out/epi2_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/epi2_pytest.log
+bash scripts/abn.sh epi2 200 "DICM_FWD4_EPI=1" "DICM_X=0"
