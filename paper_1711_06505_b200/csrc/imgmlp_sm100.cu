@@ -409,7 +409,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F4, 1)
            const void* __restrict__ pool_, int d_raw, const int32_t* __restrict__ rows,
            const int32_t* __restrict__ count, const float* __restrict__ bias, void* __restrict__ act0_) {
   constexpr bool SCR = EPI == 1;
-  static_assert(EPI != 2 || KIND == 1, "the TMA-store epilogue writes bf16 act0");
   using T = Elem<KIND>;
   constexpr int EPB = 128 / sizeof(T);
   constexpr uint32_t ASTG = 2 * OPB2;  // two sub-tiles of 128 rows
@@ -585,8 +584,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F4, 1)
       if constexpr (EPI == 2) {
         // per pair of blocks: both in registers, bias, bf16 into this warp's
         // staging box (row = lane, 16-B chunk c at c ^ (lane & 7): SWIZZLE_128B),
-        // one TMA store of 32 rows x 64 columns; the accumulator is released
-        // once the last pair is in registers
+        // one TMA store of 32 rows x 64 columns (fp32: one box of 32 columns
+        // per block); the accumulator is released once the last pair is in
+        // registers
         const uint32_t box = stg + (uint32_t)(warp - 6) * 4096;
         uint32_t ra[32], rb[32];
 #pragma unroll 1
@@ -603,6 +603,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_F4, 1)
           // a box reaching past the count (the last tile) is stored row by row
           // instead: rows >= U stay untouched
           const bool whole = m0 + 32 <= U;
+          if constexpr (KIND == 0) {  // fp32 act0: one 32-column box per block
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (lane == 0) bulk_wait_read0();
+              __syncwarp();
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + (cb + h) * 32 + 4 * c));
+                const uint32_t(&r)[32] = h == 0 ? ra : rb;
+                const float4 o = make_float4(__uint_as_float(r[4 * c]) + b4.x, __uint_as_float(r[4 * c + 1]) + b4.y,
+                                             __uint_as_float(r[4 * c + 2]) + b4.z, __uint_as_float(r[4 * c + 3]) + b4.w);
+                if (whole)
+                  st_shared_v4(box + lane * 128 + ((c ^ (lane & 7)) << 4), __float_as_uint(o.x), __float_as_uint(o.y),
+                               __float_as_uint(o.z), __float_as_uint(o.w));
+                else if (m0 + lane < U)
+                  reinterpret_cast<float4*>(reinterpret_cast<float*>(act0_) + (int64_t)(m0 + lane) * 256 +
+                                            (cb + h) * 32)[c] = o;
+              }
+              if (whole) {
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                  tma_store_2d(&tmO, box, (cb + h) * 32, m0);
+                  bulk_commit();
+                }
+              }
+            }
+            continue;
+          }
           if (lane == 0) bulk_wait_read0();  // the previous store has read the box
           __syncwarp();
 #pragma unroll
@@ -1118,11 +1147,11 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
       const char* e = getenv("DICM_FWD4_EPI");
       return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : 2;
     }();
-    static int a44 = -1, t44 = -1, a44n = -1, a44t = -1;
+    static int a44 = -1, t44 = -1, a44n = -1, a44t = -1, t44t = -1;
     // the TMA-store epilogue reads the bias as float4: an unaligned b0 takes mode 1
     const int em = (epi_mode == 2 && ((uintptr_t)b0 & 15)) ? 1 : epi_mode;
     CUtensorMap omap{};
-    if (bf16 && em == 2 && (rc = make_map(&omap, act0, true, (uint64_t)rows_max, 256, 32))) return rc;
+    if (em == 2 && (rc = make_map(&omap, act0, bf16, (uint64_t)rows_max, 256, 32))) return rc;
     auto launch4 = [&](auto kern, size_t bytes, int& attr) -> int {
       if (attr < 0)
         attr = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes),
@@ -1136,7 +1165,8 @@ int fwd_layer0(const void* pool, int pool_dtype, int d_raw, const int32_t* rows,
     const int lrc = four ? (bf16 ? (em == 1   ? launch4(k_fwd4<1, 4, 4, 1>, smem4(4, 4, 1), a44)
                                     : em == 2 ? launch4(k_fwd4<1, 4, 4, 2>, smem4(4, 4, 2), a44t)
                                                     : launch4(k_fwd4<1, 4, 4, 0>, smem4(4, 4, 0), a44n))
-                                 : launch4(k_fwd4<0, 4, 4, 1>, smem4(4, 4, 1), t44))
+                                 : (em == 2 ? launch4(k_fwd4<0, 4, 4, 2>, smem4(4, 4, 2), t44t)
+                                            : launch4(k_fwd4<0, 4, 4, 1>, smem4(4, 4, 1), t44)))
                          : (bf16 ? launch(k_fwd2<1, 6, 6>, smem2(6, 6), a66) : launch(k_fwd2<0, 6, 6>, smem2(6, 6), t66));
     probe_end(probe_slot, st);
     if (lrc) return lrc;
