@@ -93,10 +93,12 @@ __global__ void __launch_bounds__(F_THREADS, 1)
     k_l12f(const __grid_constant__ CUtensorMap tmA0, const float* __restrict__ al0, const float* __restrict__ w1,
            const float* __restrict__ b1, const float* __restrict__ al1, const float* __restrict__ w2,
            const float* __restrict__ b2, const int32_t* __restrict__ count, bf16* __restrict__ act1,
-           float* __restrict__ emb) {
+           float* __restrict__ emb, int reverse) {
   const int U = *count;
   const int ntiles = (U + 127) / 128;
   if ((int)blockIdx.x >= ntiles) return;
+  // reverse: the tiles the layer-0 forward wrote last (still in L2) first
+  auto row_of = [&](int tile) { return (reverse ? ntiles - 1 - tile : tile) * 128; };
   extern __shared__ uint8_t raw[];
   const uint32_t r0 = smem_u32(raw), base = (r0 + 1023u) & ~1023u;
   const uint32_t W = base + 2 * FT;
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(F_THREADS, 1)
         mbar_wait(empty + 8 * s, ph ^ 1);
         mbar_arrive_expect_tx(full + 8 * s, FT);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) tma_load_2d(base + s * FT + j * 16384, &tmA0, full + 8 * s, j * 64, tile * 128);
+        for (int j = 0; j < 4; ++j) tma_load_2d(base + s * FT + j * 16384, &tmA0, full + 8 * s, j * 64, row_of(tile));
       }
     }
   } else if (warp == 1) {
@@ -211,7 +213,7 @@ __global__ void __launch_bounds__(F_THREADS, 1)
     uint32_t it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const uint32_t s = it & 1, ph = (it >> 1) & 1;
-      const int m0 = tile * 128;
+      const int m0 = row_of(tile);
       mbar_wait(accf + 8 * s, ph);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
@@ -743,7 +745,11 @@ int fwd_layers12_bf16(const bf16* act0, const int32_t* count, int64_t rows_max, 
   int rc = map2d(&ma, act0, true, rows_max, H1, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   const int probe_slot = probe_begin(DICM_PROBE_IMG_FWD_L12, st);
-  k_l12f<<<grid_tiles(rows_max), F_THREADS, F_SMEM, st>>>(ma, al0, w1, b1, al1, w2, b2, count, act1, emb);
+  static const int reverse = [] {  // DICM_L12F_ORDER=fwd: ascending tiles
+    const char* e = getenv("DICM_L12F_ORDER");
+    return e && e[0] == 'f' ? 0 : 1;
+  }();
+  k_l12f<<<grid_tiles(rows_max), F_THREADS, F_SMEM, st>>>(ma, al0, w1, b1, al1, w2, b2, count, act1, emb, reverse);
   probe_end(probe_slot, st);
   return last_launch("tcgen05 bf16 layers 1-2 forward");
 }
