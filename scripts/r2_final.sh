@@ -21,6 +21,6 @@ done
 timeout 600 python bench.py --config cfg1 > gpurun_out/${tag}_cfg1_n1.log 2>&1; echo "rc=$?" >> gpurun_out/${tag}_cfg1_n1.log
 timeout 900 python bench.py --config cfg1 --impl reference > gpurun_out/${tag}_cfg1_ref.log 2>&1; echo "rc=$?" >> gpurun_out/${tag}_cfg1_ref.log
 for c in cfg3 cfg4 cfg5; do
-  timeout 1200 python bench.py --config $c --gpus $n --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/${tag}_${c}_n${n}.log 2>&1
+  timeout 1200 python bench.py --config $c --gpus $n --steps 200 --warmup 5 --no-cpu-baseline > gpurun_out/${tag}_${c}_n${n}.log 2>&1
   echo "rc=$?" >> gpurun_out/${tag}_${c}_n${n}.log
 done
