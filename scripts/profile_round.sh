@@ -16,4 +16,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 ncu --set full --clock-control none --import-source on \
     -k regex:'k_fwd|k_dw0|k_l12|k_dw1|k_sample|k_attn_bwd|k_ref|k_head|k_rows|k_mark' --launch-skip 40 --launch-count 16 \
     -o "$OUT/full" -f $CMD > "$OUT/ncu_full.log" 2>&1
+# the layer-0 GEMMs (outside the window above): one launch each, after warm-up
+ncu --set full --clock-control none --import-source on -k regex:'k_fwd4|k_dw0p' --launch-skip 4 --launch-count 2 \
+    -o "$OUT/gemm" -f $CMD > "$OUT/ncu_gemm.log" 2>&1
 echo "done $OUT"
