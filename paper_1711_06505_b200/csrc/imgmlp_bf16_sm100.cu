@@ -85,18 +85,10 @@ __device__ __forceinline__ uint4 prelu_chunk(uint4 v, const float (&al)[8], bool
 // ===========================================================================
 constexpr uint32_t FT = 64 * 1024;  // a0 tile: 4 boxes x 128 rows x 128 B (bf16, SW128)
 constexpr uint32_t FW = 32 * 1024;  // W1 [64 x 256] bf16 K-major SW128: 4 atoms x 64 rows x 128 B
+constexpr int FPAR = 256 + 64 + 64 + 768 + 16;  // al0 | b1 | al1 | w2 | b2
 constexpr int F_THREADS = 320;  // w0 TMA | w1 MMA | w2-5 PReLU | w6-9 epilogue
-// NS = 2: al0 | b1 | al1 | w2^T | b2 and the epilogue's transpose scratch in
-// shared memory.  NS = 3: a third a0 stage (more bytes in flight) in place of
-// both: al0 in the PReLU warps' registers, W2 read through L1, each lane
-// stores its own act1 row
-constexpr int fpar(int ns) { return ns == 2 ? 256 + 64 + 64 + 768 + 16 : 64 + 64 + 16; }
-constexpr size_t f_smem(int ns) {
-  return 1024 + (size_t)ns * FT + FW + 4 * fpar(ns) + 128 + (ns == 2 ? 4 * epi::SCRATCH_FLOATS * 4 : 0);
-}
-static_assert(f_smem(3) <= 232448, "k_l12f<3> shared memory");
+constexpr size_t F_SMEM = 1024 + 2 * FT + FW + 4 * FPAR + 128 + 4 * epi::SCRATCH_FLOATS * 4;
 
-template <int NS>
 __global__ void __launch_bounds__(F_THREADS, 1)
     k_l12f(const __grid_constant__ CUtensorMap tmA0, const float* __restrict__ al0, const float* __restrict__ w1,
            const float* __restrict__ b1, const float* __restrict__ al1, const float* __restrict__ w2,
@@ -109,25 +101,22 @@ __global__ void __launch_bounds__(F_THREADS, 1)
   auto row_of = [&](int tile) { return (reverse ? ntiles - 1 - tile : tile) * 128; };
   extern __shared__ uint8_t raw[];
   const uint32_t r0 = smem_u32(raw), base = (r0 + 1023u) & ~1023u;
-  const uint32_t W = base + NS * FT;
-  float* sal0 = at<float>(raw, r0, W + FW);  // NS = 2 only
-  float* sb1 = NS == 2 ? sal0 + 256 : sal0;
+  const uint32_t W = base + 2 * FT;
+  float* sal0 = at<float>(raw, r0, W + FW);
+  float* sb1 = sal0 + 256;
   float* sal1 = sb1 + 64;
-  float* sw2 = sal1 + 64;  // NS = 2 only
-  float* sb2 = NS == 2 ? sw2 + 768 : sw2;
-  const uint32_t bars = W + FW + 4 * fpar(NS);
-  // barriers: full / ready / empty per a0 stage, accf / acce per accumulator
-  const uint32_t full = bars, ready = full + 8 * NS, empty = ready + 8 * NS, accf = empty + 8 * NS,
-                 acce = accf + 16, slot = acce + 16;
+  float* sw2 = sal1 + 64;
+  float* sb2 = sw2 + 768;
+  const uint32_t bars = W + FW + 4 * FPAR;
+  const uint32_t full = bars, ready = bars + 16, empty = bars + 32, accf = bars + 48, acce = bars + 64,
+                 slot = bars + 80;
   float* scr_base = at<float>(raw, r0, bars + 128);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   if (t == 0) {
-    for (int i = 0; i < NS; ++i) {
+    for (int i = 0; i < 2; ++i) {
       mbar_init(full + 8 * i, 1);
       mbar_init(ready + 8 * i, 128);
       mbar_init(empty + 8 * i, 1);
-    }
-    for (int i = 0; i < 2; ++i) {
       mbar_init(accf + 8 * i, 1);
       mbar_init(acce + 8 * i, 128);
     }
@@ -141,16 +130,14 @@ __global__ void __launch_bounds__(F_THREADS, 1)
     *at<uint4>(raw, r0, W + j * 8192 + n * 128 + ((c ^ (n & 7)) << 4)) =
         make_uint4(f2_to_bf2(a.x, a.y), f2_to_bf2(a.z, a.w), f2_to_bf2(b.x, b.y), f2_to_bf2(b.z, b.w));
   }
-  if constexpr (NS == 2) {
-    for (int i = t; i < 256; i += F_THREADS) sal0[i] = al0[i];
-    // W2 [12][64] transposed to [64][12]: one hidden unit's 12 weights are
-    // three 16-B shared loads feeding six paired FMAs
-    for (int i = t; i < 768; i += F_THREADS) sw2[(i & 63) * 12 + (i >> 6)] = w2[i];
-  }
+  for (int i = t; i < 256; i += F_THREADS) sal0[i] = al0[i];
   if (t < 64) {
     sb1[t] = b1[t];
     sal1[t] = al1[t];
   }
+  // W2 [12][64] transposed to [64][12]: one hidden unit's 12 weights are
+  // three 16-B shared loads feeding six paired FMAs
+  for (int i = t; i < 768; i += F_THREADS) sw2[(i & 63) * 12 + (i >> 6)] = w2[i];
   if (t < 12) sb2[t] = b2[t];
   if (warp == 1) {
     tmem_alloc(slot, 128);
@@ -167,7 +154,7 @@ __global__ void __launch_bounds__(F_THREADS, 1)
       prefetch_tmap(&tmA0);
       uint32_t it = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const uint32_t s = it % NS, ph = (it / NS) & 1;
+        const uint32_t s = it & 1, ph = (it >> 1) & 1;
         mbar_wait(empty + 8 * s, ph ^ 1);
         mbar_arrive_expect_tx(full + 8 * s, FT);
 #pragma unroll
@@ -179,19 +166,19 @@ __global__ void __launch_bounds__(F_THREADS, 1)
       const uint32_t idesc = instr_desc(1, 128, 64, 0, 0);
       uint32_t it = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const uint32_t s = it % NS, ph = (it / NS) & 1, ab = it & 1, aph = (it >> 1) & 1;
-        mbar_wait(acce + 8 * ab, aph ^ 1);
+        const uint32_t s = it & 1, ph = (it >> 1) & 1;
+        mbar_wait(acce + 8 * s, ph ^ 1);
         mbar_wait(ready + 8 * s, ph);
         tc_fence_after();
         const uint32_t A = base + s * FT;
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk) {
           const int j = kk >> 2, k4 = kk & 3;
-          mma<1>(tmem + ab * 64, smem_desc(A + j * 16384 + k4 * 32, 16, 1024), smem_desc(W + j * 8192 + k4 * 32, 16, 1024),
+          mma<1>(tmem + s * 64, smem_desc(A + j * 16384 + k4 * 32, 16, 1024), smem_desc(W + j * 8192 + k4 * 32, 16, 1024),
                  idesc, kk > 0);
         }
         mma_commit(empty + 8 * s);
-        mma_commit(accf + 8 * ab);
+        mma_commit(accf + 8 * s);
       }
     }
   } else if (warp < 6) {
@@ -202,10 +189,10 @@ __global__ void __launch_bounds__(F_THREADS, 1)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) al[j][e] = NS == 2 ? sal0[j * 64 + lc * 8 + e] : __ldg(al0 + j * 64 + lc * 8 + e);
+      for (int e = 0; e < 8; ++e) al[j][e] = sal0[j * 64 + lc * 8 + e];
     uint32_t it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const uint32_t s = it % NS, ph = (it / NS) & 1;
+      const uint32_t s = it & 1, ph = (it >> 1) & 1;
       mbar_wait(full + 8 * s, ph);
       const uint32_t A = base + s * FT;
 #pragma unroll
@@ -223,12 +210,11 @@ __global__ void __launch_bounds__(F_THREADS, 1)
     // ---- epilogue: TMEM lane quarter q = warp % 4
     const int q = warp & 3;
     float* scr = scr_base + q * epi::SCRATCH_FLOATS;
-    (void)scr;
     uint32_t it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const uint32_t ab = it & 1, aph = (it >> 1) & 1;
+      const uint32_t s = it & 1, ph = (it >> 1) & 1;
       const int m0 = row_of(tile);
-      mbar_wait(accf + 8 * ab, aph);
+      mbar_wait(accf + 8 * s, ph);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
       float e[12];
@@ -237,38 +223,26 @@ __global__ void __launch_bounds__(F_THREADS, 1)
 #pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {
         float a[32];
-        tmem_ld32(tmem + ab * 64 + ((uint32_t)(q * 32) << 16) + 32 * hh, a);
+        tmem_ld32(tmem + s * 64 + ((uint32_t)(q * 32) << 16) + 32 * hh, a);
         if (hh == 1) {
           tc_fence_before();
-          mbar_arrive(acce + 8 * ab);
+          mbar_arrive(acce + 8 * s);
         }
 #pragma unroll
         for (int i = 0; i < 32; ++i) a[i] += sb1[32 * hh + i];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const float h = prelu(a[i], sal1[32 * hh + i]);
-          float w[12];
-          if constexpr (NS == 2) {
-            const float4* wv = reinterpret_cast<const float4*>(sw2 + (32 * hh + i) * 12);
-            const float4 w0 = wv[0], w1v = wv[1], w2v = wv[2];
-            w[0] = w0.x, w[1] = w0.y, w[2] = w0.z, w[3] = w0.w, w[4] = w1v.x, w[5] = w1v.y;
-            w[6] = w1v.z, w[7] = w1v.w, w[8] = w2v.x, w[9] = w2v.y, w[10] = w2v.z, w[11] = w2v.w;
-          } else {
-#pragma unroll
-            for (int c = 0; c < 12; ++c) w[c] = __ldg(w2 + c * 64 + 32 * hh + i);
-          }
-#pragma unroll
-          for (int c = 0; c < 12; c += 2) ffma2(e[c], e[c + 1], w[c], w[c + 1], h);
+          const float4* wv = reinterpret_cast<const float4*>(sw2 + (32 * hh + i) * 12);
+          const float4 w0 = wv[0], w1 = wv[1], w2v = wv[2];
+          ffma2(e[0], e[1], w0.x, w0.y, h);
+          ffma2(e[2], e[3], w0.z, w0.w, h);
+          ffma2(e[4], e[5], w1.x, w1.y, h);
+          ffma2(e[6], e[7], w1.z, w1.w, h);
+          ffma2(e[8], e[9], w2v.x, w2v.y, h);
+          ffma2(e[10], e[11], w2v.z, w2v.w, h);
         }
-        if constexpr (NS == 2) {
-          epi::store_bf16(a, scr, lane, m0 + q * 32, U, [&](int r) { return act1 + (int64_t)r * H2 + 32 * hh; });
-        } else if (row < U) {  // the lane's own 64 B of its act1 row
-          uint4* o = reinterpret_cast<uint4*>(act1 + (int64_t)row * H2 + 32 * hh);
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4)
-            o[q4] = make_uint4(f2_to_bf2(a[8 * q4], a[8 * q4 + 1]), f2_to_bf2(a[8 * q4 + 2], a[8 * q4 + 3]),
-                               f2_to_bf2(a[8 * q4 + 4], a[8 * q4 + 5]), f2_to_bf2(a[8 * q4 + 6], a[8 * q4 + 7]));
-        }
+        epi::store_bf16(a, scr, lane, m0 + q * 32, U, [&](int r) { return act1 + (int64_t)r * H2 + 32 * hh; });
       }
       if (row < U) {
         float4* eo = reinterpret_cast<float4*>(emb + (int64_t)row * 12);
@@ -765,7 +739,7 @@ int grid_tiles(int64_t rows_max) {
 int fwd_layers12_bf16(const bf16* act0, const int32_t* count, int64_t rows_max, const float* al0, const float* w1,
                       const float* b1, const float* al1, const float* w2, const float* b2, bf16* act1, float* emb,
                       cudaStream_t st) {
-  static int once = smem_attr3(k_l12f<2>, f_smem(2)) | smem_attr3(k_l12f<3>, f_smem(3));
+  static int once = smem_attr3(k_l12f, F_SMEM);
   if (once) return once;
   CUtensorMap ma;
   int rc = map2d(&ma, act0, true, rows_max, H1, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -775,14 +749,7 @@ int fwd_layers12_bf16(const bf16* act0, const int32_t* count, int64_t rows_max, 
     const char* e = getenv("DICM_L12F_ORDER");
     return e && e[0] == 'f' ? 0 : 1;
   }();
-  static const int ns = [] {  // DICM_L12F_STAGES=2: two a0 stages with the shared-memory epilogue
-    const char* e = getenv("DICM_L12F_STAGES");
-    return e && e[0] == '2' ? 2 : 3;
-  }();
-  if (ns == 3)
-    k_l12f<3><<<grid_tiles(rows_max), F_THREADS, f_smem(3), st>>>(ma, al0, w1, b1, al1, w2, b2, count, act1, emb, reverse);
-  else
-    k_l12f<2><<<grid_tiles(rows_max), F_THREADS, f_smem(2), st>>>(ma, al0, w1, b1, al1, w2, b2, count, act1, emb, reverse);
+  k_l12f<<<grid_tiles(rows_max), F_THREADS, F_SMEM, st>>>(ma, al0, w1, b1, al1, w2, b2, count, act1, emb, reverse);
   probe_end(probe_slot, st);
   return last_launch("tcgen05 bf16 layers 1-2 forward");
 }
