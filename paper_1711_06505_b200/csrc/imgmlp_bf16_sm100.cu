@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(F_THREADS, 1)
     k_l12f(const __grid_constant__ CUtensorMap tmA0, const float* __restrict__ al0, const float* __restrict__ w1,
            const float* __restrict__ b1, const float* __restrict__ al1, const float* __restrict__ w2,
            const float* __restrict__ b2, const int32_t* __restrict__ count, bf16* __restrict__ act1,
-           float* __restrict__ emb, int reverse, int pf) {
+           float* __restrict__ emb, int reverse) {
   const int U = *count;
   const int ntiles = (U + 127) / 128;
   if ((int)blockIdx.x >= ntiles) return;
@@ -159,11 +159,6 @@ __global__ void __launch_bounds__(F_THREADS, 1)
         mbar_arrive_expect_tx(full + 8 * s, FT);
 #pragma unroll
         for (int j = 0; j < 4; ++j) tma_load_2d(base + s * FT + j * 16384, &tmA0, full + 8 * s, j * 64, row_of(tile));
-        // the tile after the next one into L2: more bytes in flight than the two stages hold
-        const int ahead = tile + pf * (int)gridDim.x;
-        if (pf && ahead < ntiles)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) tma_prefetch_2d(&tmA0, j * 64, row_of(ahead));
       }
     }
   } else if (warp == 1) {
@@ -541,7 +536,7 @@ constexpr int G_PART = 3 * 64 * 256;
 
 __global__ void __launch_bounds__(D_THREADS, 1)
     k_dw1b(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmD,
-           const int32_t* __restrict__ count, float* __restrict__ part, int pf) {
+           const int32_t* __restrict__ count, float* __restrict__ part) {
   const int U = *count;
   const int per = (((U + gridDim.x - 1) / gridDim.x) + DBK - 1) / DBK * DBK;
   const int rb = blockIdx.x * per, re = min(U, rb + per);
@@ -586,12 +581,6 @@ __global__ void __launch_bounds__(D_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 4; ++j) tma_load_2d(a + j * 4096, &tmH, full + 8 * s, j * 64, row);
         tma_load_2d(a + 3 * DX, &tmD, full + 8 * s, 0, row);
-        if (pf && kb + pf < nk) {  // rows pf stages ahead into L2
-          const int prow = rb + (kb + pf) * DBK;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) tma_prefetch_2d(&tmH, j * 64, prow);
-          tma_prefetch_2d(&tmD, 0, prow);
-        }
       }
     }
   } else if (warp == 4) {
@@ -760,12 +749,7 @@ int fwd_layers12_bf16(const bf16* act0, const int32_t* count, int64_t rows_max, 
     const char* e = getenv("DICM_L12F_ORDER");
     return e && e[0] == 'f' ? 0 : 1;
   }();
-  static const int pf = [] {  // DICM_L12F_PF=k: L2 prefetch k tiles ahead (0: off)
-    const char* e = getenv("DICM_L12F_PF");
-    return e ? atoi(e) : 2;
-  }();
-  k_l12f<<<grid_tiles(rows_max), F_THREADS, F_SMEM, st>>>(ma, al0, w1, b1, al1, w2, b2, count, act1, emb, reverse,
-                                                          pf);
+  k_l12f<<<grid_tiles(rows_max), F_THREADS, F_SMEM, st>>>(ma, al0, w1, b1, al1, w2, b2, count, act1, emb, reverse);
   probe_end(probe_slot, st);
   return last_launch("tcgen05 bf16 layers 1-2 forward");
 }
@@ -797,11 +781,7 @@ int bwd_layers12_bf16(const float* demb, const bf16* act1, const bf16* act0, con
   if (rc) return rc;
   {
     const int probe_slot = probe_begin(DICM_PROBE_IMG_BWD_DW1, st);
-    static const int pf = [] {  // DICM_DW1_PF=k: L2 prefetch k stages ahead (0: off)
-      const char* e = getenv("DICM_DW1_PF");
-      return e ? atoi(e) : 8;
-    }();
-    k_dw1b<<<small_dw1_blocks(rows_max), D_THREADS, D_SMEM, st>>>(mh, md, count, part_dw1, pf);
+    k_dw1b<<<small_dw1_blocks(rows_max), D_THREADS, D_SMEM, st>>>(mh, md, count, part_dw1);
     probe_end(probe_slot, st);
   }
   return last_launch("tcgen05 bf16 layer-1 row GEMMs");
