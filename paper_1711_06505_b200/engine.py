@@ -1002,7 +1002,7 @@ class StepEngine:
     def kernel_nodes(self, detail=False):
         """(own, total) kernel nodes of the last captured step graph: every
         kernel the step launches, and those written in this library
-        (csrc/*.cu).  The CUB radix-sort kernels instantiated inside the
+        (csrc/*.cu).  The CUB scan kernels instantiated inside the
         library by dicm_ref_transpose (CUDA toolkit templates) are counted
         apart (``detail=True`` -> (own, cub, total)); NCCL or torch kernels
         in the graph are counted in total only."""
