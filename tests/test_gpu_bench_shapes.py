@@ -166,6 +166,20 @@ def test_persistent_loops_wrap_at_small_sizes():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("epi", ["0", "1"])
+def test_layer0_epilogue_variants_match_oracle(epi):
+    """The non-default act0 epilogues of k_fwd4 (DICM_FWD4_EPI, read once per
+    process: 1 = shared-memory transposes, also taken for an unaligned bias;
+    0 = per-lane row stores) at U = 20k, bf16 and tf32, against the oracle."""
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, DICM_FWD4_EPI=epi)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        os.path.join(here, "test_gpu_bench_shapes.py"), "-k",
+                        "test_image_mlp_at_bench_sizes_matches_oracle and 20000"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 def _cfg_model(kind, P, vocab, b_max, pool_dtype):
     from paper_1711_06505_b200.model import DicmModel
     from paper_1711_06505_b200.schema import AggregatorSpec, default_schema
