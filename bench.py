@@ -367,6 +367,13 @@ def run_reference_arm(args):
         return
     world = max(world, args.gpus)
     name = args.config
+    # torchrun sets OMP_NUM_THREADS=1 for every rank; rank 0 runs alone here,
+    # so the reference's numpy/BLAS gets every host thread back
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=os.cpu_count() or 1)
+    except Exception:  # reported through the thread count in cpu_baseline
+        pass
     cols = gen_columns(name, 1, seed=1000)[0]
     # ~10 ms of host work per sample at L = 200: size the slice so W + K steps take ~2.5 min
     per_sample = 0.01 * max(CONFIGS[name]["L"], 40) / 200.0
