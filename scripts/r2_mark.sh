@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_step.py -x -q > gpurun_out/mark_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/mark_pytest.log
+bash scripts/launches_only.sh cfg4 mnew DICM_X=0
+bash scripts/launches_only.sh cfg4 mold DICM_LIB_PATH=build/ab/libdicm_b200_HEAD~1.so
+bash scripts/launches_only.sh cfg2 mnew DICM_X=0
+bash scripts/launches_only.sh cfg2 mold DICM_LIB_PATH=build/ab/libdicm_b200_HEAD~1.so
