@@ -38,24 +38,12 @@ __device__ __forceinline__ int find_seg(const Segs& s, int64_t i) {
   return k;
 }
 
-// Keys that share a bitmap word are combined before they reach global
-// memory: within a warp (one RED.OR per distinct word and warp), then within
-// the block through a small shared-memory table (word -> bits, open
-// addressing) flushed once at the end: small-vocabulary fields (scenario,
-// ad_category: a handful of ids over the whole batch) and Zipf-hot keys
-// (cfg4: ~9% of all references on one key) would otherwise queue thousands
-// of reductions on one word.  A full table falls back to the global RED.
-constexpr int kMarkSlots = 512;
-constexpr uint32_t kMarkEmpty = 0xffffffffu;
-
-__global__ void __launch_bounds__(256) k_mark(const __grid_constant__ Segs segs, uint32_t* __restrict__ bitmap,
-                                              int tag, int32_t* __restrict__ status) {
-  __shared__ uint32_t hk[kMarkSlots], hv[kMarkSlots];
-  for (int j = threadIdx.x; j < kMarkSlots; j += blockDim.x) {
-    hk[j] = kMarkEmpty;
-    hv[j] = 0u;
-  }
-  __syncthreads();
+// Keys that share a bitmap word within a warp are combined first (one
+// fire-and-forget RED.OR per distinct word and warp): small-vocabulary fields
+// (scenario, ad_category: a handful of ids over the whole batch) and Zipf-hot
+// keys would otherwise queue thousands of reductions on one word.
+__global__ void k_mark(const __grid_constant__ Segs segs, uint32_t* __restrict__ bitmap, int tag,
+                       int32_t* __restrict__ status) {
   const int64_t total = seg_total(segs);
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -83,24 +71,8 @@ __global__ void __launch_bounds__(256) k_mark(const __grid_constant__ Segs segs,
       const uint32_t b = __shfl_sync(0xffffffffu, bit, src);
       if ((peers >> src) & 1u) bits |= b;
     }
-    if (w != 0xffffffffu && lane == __ffs(peers) - 1) {
-      const uint32_t h = (w * 0x9E3779B1u) >> 23;  // 9 bits: kMarkSlots
-      bool done = false;
-#pragma unroll 1
-      for (int p = 0; p < 8 && !done; ++p) {
-        const uint32_t slot = (h + p) & (kMarkSlots - 1);
-        const uint32_t prev = atomicCAS(&hk[slot], kMarkEmpty, w);
-        if (prev == kMarkEmpty || prev == w) {
-          atomicOr(&hv[slot], bits);
-          done = true;
-        }
-      }
-      if (!done) atomicOr(bitmap + w, bits);  // result unused: RED.OR
-    }
+    if (w != 0xffffffffu && lane == __ffs(peers) - 1) atomicOr(bitmap + w, bits);  // result unused: RED.OR
   }
-  __syncthreads();
-  for (int j = threadIdx.x; j < kMarkSlots; j += blockDim.x)
-    if (hk[j] != kMarkEmpty) atomicOr(bitmap + hk[j], hv[j]);
 }
 
 __device__ __forceinline__ int block_excl_scan(int v, int* total) {
