@@ -432,12 +432,9 @@ __global__ void __launch_bounds__(FWD_WARPS * 32, MINB) k_sample_fwd(const __gri
 // backward
 // ---------------------------------------------------------------------------
 
-constexpr int KP_STRIDE = 28;  // floats per reference pair in WarpScratch::kp (16-B rows, 2-way stores)
 struct __align__(16) WarpScratch {
   float ds[32];
   float ks[32][DICM_D];
-  float kp[16][KP_STRIDE];  // the same rows pair-interleaved: kp[r/2][2c + r%2] = k_r[c] (the pre-activation
-                            // recompute's FFMA2 operands land in register pairs without moves)
   float dp[32][DICM_ATT + 4];  // the chunk's key projections, overwritten by dpre (row = reference);
                                // stride 36: 16-B rows for cp.async, conflict-free column reads
   float wq[32][MAXQ + 1];      // lane j's dWq accumulators (kept out of registers)
@@ -531,8 +528,6 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
     ws.ds[lane] = ds;
 #pragma unroll
     for (int c = 0; c < DICM_D; ++c) ws.ks[lane][c] = k.v[c];
-#pragma unroll
-    for (int c = 0; c < DICM_D; ++c) ws.kp[lane >> 1][2 * c + (lane & 1)] = k.v[c];
     acc.b1 += ds;
     __syncwarp();
     // lane j: hidden unit j across the chunk's references
@@ -561,18 +556,22 @@ __device__ void attn_bwd(const Args& a, const AttnSmem& s, WarpScratch& ws, int 
     int r = 0;
 #pragma unroll 2
     for (; r + 1 < nr; r += 2) {
-      // (k_r[c], k_r+1[c]) pairs straight from the interleaved rows
-      const float4* kq = reinterpret_cast<const float4*>(ws.kp[r >> 1]);
-      float pa = Pj, pb = Pj;
-#pragma unroll
-      for (int q = 0; q < DICM_D / 2; ++q) {
-        const float4 v = kq[q];
-        ffma2(pa, pb, v.x, v.y, wkj[2 * q]);
-        ffma2(pa, pb, v.z, v.w, wkj[2 * q + 1]);
-      }
       const float4* ka = reinterpret_cast<const float4*>(ws.ks[r]);
       const float4* kb = reinterpret_cast<const float4*>(ws.ks[r + 1]);
       const float4 a0 = ka[0], a1 = ka[1], a2 = ka[2], b0 = kb[0], b1 = kb[1], b2 = kb[2];
+      float pa = Pj, pb = Pj;
+      ffma2(pa, pb, a0.x, b0.x, wkj[0]);
+      ffma2(pa, pb, a0.y, b0.y, wkj[1]);
+      ffma2(pa, pb, a0.z, b0.z, wkj[2]);
+      ffma2(pa, pb, a0.w, b0.w, wkj[3]);
+      ffma2(pa, pb, a1.x, b1.x, wkj[4]);
+      ffma2(pa, pb, a1.y, b1.y, wkj[5]);
+      ffma2(pa, pb, a1.z, b1.z, wkj[6]);
+      ffma2(pa, pb, a1.w, b1.w, wkj[7]);
+      ffma2(pa, pb, a2.x, b2.x, wkj[8]);
+      ffma2(pa, pb, a2.y, b2.y, wkj[9]);
+      ffma2(pa, pb, a2.z, b2.z, wkj[10]);
+      ffma2(pa, pb, a2.w, b2.w, wkj[11]);
       unit(r, pa, a0, a1, a2);
       unit(r + 1, pb, b0, b1, b2);
     }
