@@ -457,6 +457,12 @@ int dicm_p2p_plan(const dicm_peers_t* peers, int64_t cmat_off, int64_t* seg_img,
                   int32_t* cnt_dev, int64_t* plan, dicm_stream_t stream);
 int dicm_p2p_scatter(const dicm_peers_t* peers, const int64_t* plan, int kind /* 0 img, 1 id */,
                      int dir, const void* src, int row_bytes, int64_t dst_off, dicm_stream_t stream);
+/* dicm_permute_rows12(rows, idx) fused into dicm_p2p_scatter for 12-float
+ * rows: row j of each peer's segment is rows[idx[s0 + j]], gathered locally
+ * and stored into the peer's buffer over NVLink in one pass (the owner's
+ * embeddings back to the requesters, reference runtime.py:387-422). */
+int dicm_p2p_gather_scatter12(const dicm_peers_t* peers, const int64_t* plan, int kind, int dir, const float* rows,
+                              const int32_t* idx, int64_t dst_off, dicm_stream_t stream);
 /* Sum of src[0..n) over every rank, into dst on every rank, over peer
  * memory: stage into this rank's region (stage_off, float4-padded), barrier,
  * each rank reduces 1/world of the elements in rank order and writes the sums

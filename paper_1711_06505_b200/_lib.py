@@ -185,6 +185,7 @@ _sig("dicm_p2p_barrier", C.c_int, C.POINTER(Peers), I64, C.c_uint32, P, ST)
 _sig("dicm_p2p_counts", C.c_int, C.POINTER(Peers), P, I64, ST)
 _sig("dicm_p2p_plan", C.c_int, C.POINTER(Peers), I64, P, P, P, P, ST)
 _sig("dicm_p2p_scatter", C.c_int, C.POINTER(Peers), P, C.c_int, C.c_int, P, C.c_int, I64, ST)
+_sig("dicm_p2p_gather_scatter12", C.c_int, C.POINTER(Peers), P, C.c_int, C.c_int, P, P, I64, ST)
 _sig("dicm_dedup_devn", C.c_int, P, P, I64, I64, P, S, P, P, P, C.c_int, P, ST)
 _sig("dicm_jsonl_parse", P, C.c_char_p, I64, C.POINTER(JsonlSpec), C.c_int, C.POINTER(I64), C.POINTER(I64))
 _sig("dicm_jsonl_list_total", I64, P, C.c_int)
@@ -222,7 +223,7 @@ EXPORTED = [
     "dicm_bucket_workspace", "dicm_bucket_by_owner", "dicm_permute_rows12", "dicm_gather_rows_by_key",
     "dicm_owner_reduce_rows12", "dicm_probe_enable", "dicm_probe_read",
     "dicm_p2p_alloc", "dicm_p2p_free", "dicm_ipc_handle", "dicm_ipc_open", "dicm_ipc_close", "dicm_p2p_barrier",
-    "dicm_p2p_counts", "dicm_p2p_plan", "dicm_p2p_scatter", "dicm_dedup_devn", "dicm_head_fwd",
+    "dicm_p2p_counts", "dicm_p2p_plan", "dicm_p2p_scatter", "dicm_p2p_gather_scatter12", "dicm_dedup_devn", "dicm_head_fwd",
     "dicm_ref_transpose_workspace", "dicm_hot_acc_bytes", "dicm_dedup_inverse", "dicm_ref_transpose", "dicm_csr_segments", "dicm_table_init", "dicm_id_row_grads", "dicm_p2p_allreduce", "dicm_fields_fwd", "dicm_images_fwd", "dicm_jsonl_parse", "dicm_jsonl_list_total", "dicm_jsonl_export", "dicm_jsonl_free",
     "dicm_towers_blocks", "dicm_towers_fwd_bwd", "dicm_towers_fwd", "dicm_head_wide_workspace",
     "dicm_head_wide_fwd_bwd", "dicm_head_wide_fwd", "dicm_host_pack", "dicm_zero_async",

@@ -139,6 +139,29 @@ __global__ void __launch_bounds__(256) k_scatter(const __grid_constant__ Peers P
   }
 }
 
+// k_scatter with the row gather fused in (12-float rows): row j of the
+// segment is rows[idx[s0 + j]] -- the owner's embedding of the j-th key a
+// requester sent -- read locally and stored straight into the peer's buffer
+// over NVLink (no staged copy in between)
+__global__ void __launch_bounds__(256) k_gather_scatter12(const __grid_constant__ Peers P,
+                                                          const int64_t* __restrict__ plan, int kind, int dir,
+                                                          const float* __restrict__ rows,
+                                                          const int32_t* __restrict__ idx, int64_t dst_off) {
+  const int p = blockIdx.y;
+  const int64_t* pl = plan + (int64_t)kind * 4 * (DICM_MAX_PEERS + 1);
+  constexpr int S = DICM_MAX_PEERS + 1;
+  const int64_t s0 = dir == 0 ? pl[p] : pl[2 * S + p];
+  const int64_t n = dir == 0 ? pl[p + 1] - pl[p] : pl[2 * S + p + 1] - pl[2 * S + p];
+  const int64_t d0 = dir == 0 ? pl[S + p] : pl[3 * S + p];
+  int4* d4 = reinterpret_cast<int4*>(P.region[p] + dst_off) + d0 * 3;
+  const int4* r4 = reinterpret_cast<const int4*>(rows);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * 3; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = i / 3;
+    const int q = (int)(i - j * 3);
+    d4[i] = __ldg(r4 + (int64_t)__ldg(idx + s0 + j) * 3 + q);
+  }
+}
+
 int check_peers(const dicm_peers_t* p) {
   if (!p || p->world < 1 || p->world > DICM_MAX_PEERS || p->rank < 0 || p->rank >= p->world)
     return fail(DICM_ERR_VALUE, "p2p: bad peer table");
@@ -264,6 +287,19 @@ int dicm_p2p_scatter(const dicm_peers_t* peers, const int64_t* plan, int kind, i
   k_scatter<<<dim3(per, peers->world), 256, 0, (cudaStream_t)stream>>>(to_dev(peers), plan, kind, dir,
                                                                       (const uint8_t*)src, row_bytes, dst_off);
   return last_launch("dicm_p2p_scatter");
+}
+
+int dicm_p2p_gather_scatter12(const dicm_peers_t* peers, const int64_t* plan, int kind, int dir, const float* rows,
+                              const int32_t* idx, int64_t dst_off, dicm_stream_t stream) {
+  using namespace dicm;
+  int rc = check_peers(peers);
+  if (rc) return rc;
+  if ((kind != 0 && kind != 1) || (dir != 0 && dir != 1))
+    return fail(DICM_ERR_VALUE, "p2p_gather_scatter12: kind %d dir %d", kind, dir);
+  const int per = std::max(1, 148 * 4 / peers->world);
+  k_gather_scatter12<<<dim3(per, peers->world), 256, 0, (cudaStream_t)stream>>>(to_dev(peers), plan, kind, dir, rows,
+                                                                               idx, dst_off);
+  return last_launch("dicm_p2p_gather_scatter12");
 }
 
 }  // extern "C"

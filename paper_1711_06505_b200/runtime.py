@@ -242,6 +242,11 @@ class PeerExchange:
         L.check(L.lib.dicm_p2p_scatter(C.byref(self.peers), self.plan.data_ptr(), kind, direction, src, row_bytes,
                                        self.off[dst], s))
 
+    def gather_scatter12(self, kind, direction, rows, idx, dst, s):
+        """scatter() of rows[idx[i]] (12-float rows) without a staged copy."""
+        L.check(L.lib.dicm_p2p_gather_scatter12(C.byref(self.peers), self.plan.data_ptr(), kind, direction, rows,
+                                                idx, self.off[dst], s))
+
     def close(self):
         for p in self._opened:
             L.lib.dicm_ipc_close(p)
@@ -564,9 +569,8 @@ class ClusterEngine(StepEngine):
         if self.n_img_segs:
             self._image_forward(self.net, self.uniq_o, cnt[2:].data_ptr())
         self._mark("image MLP fwd")
-        L.check(L.lib.dicm_permute_rows12(self.net.emb.data_ptr(), self.inv_o.data_ptr(), self.cnt_dev.data_ptr(),
-                                          px.cap_ri, 0, self.resp.data_ptr(), s))
-        px.scatter(0, 1, self.resp.data_ptr(), 48, "back_img", s)
+        # the owner's embeddings gathered by key and stored into the requesters' buffers in one pass
+        px.gather_scatter12(0, 1, self.net.emb.data_ptr(), self.inv_o.data_ptr(), "back_img", s)
         join()
         px.barrier(st, s)
         L.check(L.lib.dicm_permute_rows12(px.back_img.data_ptr(), self.perm_img.data_ptr(), cnt.data_ptr(),
