@@ -384,12 +384,14 @@ int dicm_adam_rows(const dicm_table_state_t* tabs, int ntab, const int32_t* uniq
  * Cluster.run_iteration runtime.py:370-470, shard_of runtime.py:60-68).
  * Keys are owned by rank = key % world; the owner's local row is key / world.
  * bucket: stable partition of sorted keys[0..*count_dev) by owner ->
- *   send_keys (owner-local ids), send_counts[world], perm[i] = slot of key i.
+ *   send_keys (owner-local ids), send_counts[world], perm[i] = slot of key i,
+ *   perm_inv[slot] = i (optional, NULL to skip: the gather form of perm, used
+ *   to push per-key rows to the owners with dicm_p2p_gather_scatter12).
  * permute rows: out[perm[i]] = in[i] (scatter) or out[i] = in[perm[i]] (gather)
  *   for 12-float rows.
  * ---------------------------------------------------------------------- */
 int dicm_bucket_by_owner(const int32_t* keys, const int32_t* count_dev, int64_t n_max, int world,
-                         int32_t* send_keys, int32_t* send_counts, int32_t* perm,
+                         int32_t* send_keys, int32_t* send_counts, int32_t* perm, int32_t* perm_inv,
                          void* workspace, size_t workspace_bytes, dicm_stream_t stream);
 size_t dicm_bucket_workspace(int64_t n_max, int world);
 int dicm_permute_rows12(const float* in, const int32_t* perm, const int32_t* count_dev,

@@ -172,7 +172,7 @@ _sig("dicm_adam_dense_workspace", S, C.c_int)
 _sig("dicm_adam_dense", C.c_int, P, P, P, P, P, C.POINTER(Span), C.c_int, F, F, F, F, P, S, P, ST)
 _sig("dicm_adam_rows", C.c_int, C.POINTER(TableState), C.c_int, P, P, I64, P, F, F, F, F, P, ST)
 _sig("dicm_bucket_workspace", S, I64, C.c_int)
-_sig("dicm_bucket_by_owner", C.c_int, P, P, I64, C.c_int, P, P, P, P, S, ST)
+_sig("dicm_bucket_by_owner", C.c_int, P, P, I64, C.c_int, P, P, P, P, P, S, ST)
 _sig("dicm_permute_rows12", C.c_int, P, P, P, I64, C.c_int, P, ST)
 _sig("dicm_gather_rows_by_key", C.c_int, C.POINTER(TableState), C.c_int, P, P, I64, P, ST)
 _sig("dicm_owner_reduce_rows12", C.c_int, P, P, P, C.c_int, I64, P, I64, P, P, ST)

@@ -56,7 +56,8 @@ __global__ void __launch_bounds__(256) k_scan_counts(int32_t* __restrict__ blkcn
 
 __global__ void k_place(const int32_t* __restrict__ keys, const int32_t* __restrict__ count, int64_t n_max, int world,
                         const int32_t* __restrict__ base, const int32_t* __restrict__ send_counts,
-                        int32_t* __restrict__ send_keys, int32_t* __restrict__ perm) {
+                        int32_t* __restrict__ send_keys, int32_t* __restrict__ perm,
+                        int32_t* __restrict__ perm_inv) {
   __shared__ int warp_cnt[BLK / 32][MAXW];
   __shared__ int owner_base[MAXW];
   if (threadIdx.x == 0) {
@@ -85,6 +86,7 @@ __global__ void k_place(const int32_t* __restrict__ keys, const int32_t* __restr
     const int pos = owner_base[own] + base[(int64_t)blockIdx.x * world + own] + before + rank;
     send_keys[pos] = key / world;
     perm[i] = pos;
+    if (perm_inv) perm_inv[pos] = (int32_t)i;
   }
 }
 
@@ -112,8 +114,8 @@ size_t dicm_bucket_workspace(int64_t n_max, int world) {
 }
 
 int dicm_bucket_by_owner(const int32_t* keys, const int32_t* count_dev, int64_t n_max, int world, int32_t* send_keys,
-                         int32_t* send_counts, int32_t* perm, void* workspace, size_t workspace_bytes,
-                         dicm_stream_t stream) {
+                         int32_t* send_counts, int32_t* perm, int32_t* perm_inv, void* workspace,
+                         size_t workspace_bytes, dicm_stream_t stream) {
   using namespace dicm;
   if (world < 1 || world > MAXW) return fail(DICM_ERR_VALUE, "bucket: world %d not in [1, %d]", world, MAXW);
   if (workspace_bytes < dicm_bucket_workspace(n_max, world)) return fail(DICM_ERR_VALUE, "bucket: workspace");
@@ -126,7 +128,7 @@ int dicm_bucket_by_owner(const int32_t* keys, const int32_t* count_dev, int64_t 
   int32_t* blkcnt = (int32_t*)workspace;
   k_block_counts<<<nblk, BLK, 0, st>>>(keys, count_dev, n_max, world, blkcnt);
   k_scan_counts<<<world, 256, 0, st>>>(blkcnt, nblk, world, send_counts);
-  k_place<<<nblk, BLK, 0, st>>>(keys, count_dev, n_max, world, blkcnt, send_counts, send_keys, perm);
+  k_place<<<nblk, BLK, 0, st>>>(keys, count_dev, n_max, world, blkcnt, send_counts, send_keys, perm, perm_inv);
   return last_launch("dicm_bucket_by_owner");
 }
 

@@ -325,8 +325,10 @@ class ClusterEngine(StepEngine):
         self.d_emb_l = torch.empty((cu, 12), **f32)
         self.send_img = torch.empty(cu, **i32)
         self.perm_img = torch.empty(cu, **i32)
+        self.perm_inv_img = torch.empty(cu, **i32)  # gather form of perm_img (the gradient push)
         self.send_id = torch.empty(ck, **i32)
         self.perm_id = torch.empty(ck, **i32)
+        self.perm_inv_id = torch.empty(ck, **i32)
         self.ws_bucket = _u8(L.lib.dicm_bucket_workspace(max(cu, ck), G), dev)
         self.ws_bucket_id = _u8(L.lib.dicm_bucket_workspace(max(cu, ck), G), dev)
         self.rows_buf = torch.empty((max(cu, ck), 12), **f32)  # responses in / pushes out
@@ -402,10 +404,10 @@ class ClusterEngine(StepEngine):
         cnt = self.counts
         # (2) requests: bucket by owner, exchange counts, then keys
         L.check(L.lib.dicm_bucket_by_owner(self.uniq_img.data_ptr(), cnt.data_ptr(), self.cap_u, G,
-                                           self.send_img.data_ptr(), self._col(0), self.perm_img.data_ptr(),
+                                           self.send_img.data_ptr(), self._col(0), self.perm_img.data_ptr(), None,
                                            self.ws_bucket.data_ptr(), self.ws_bucket.numel(), s))
         L.check(L.lib.dicm_bucket_by_owner(self.uniq_id.data_ptr(), cnt[1:].data_ptr(), self.cap_k, G,
-                                           self.send_id.data_ptr(), self._col(1), self.perm_id.data_ptr(),
+                                           self.send_id.data_ptr(), self._col(1), self.perm_id.data_ptr(), None,
                                            self.ws_bucket.data_ptr(), self.ws_bucket.numel(), s))
         self._mark("dedup+bucket")
         pair = self._cnt_both.t().contiguous()
@@ -493,7 +495,6 @@ class ClusterEngine(StepEngine):
                                    self.local_id_space, self.group, dense_n=self.grad_ext.numel())
             self._alloc_owner(self.px.cap_ri, self.px.cap_rk)  # every owner buffer at the agreed capacity
             self.resp_id = torch.empty((max(self.px.cap_rk, 1), 12), dtype=torch.float32, device=self.dev)
-            self.push_out_id = torch.empty((max(self.cap_k, 1), 12), dtype=torch.float32, device=self.dev)
         px = self.px
         side = self._side_stream()
         main_stream = torch.cuda.current_stream()
@@ -527,7 +528,8 @@ class ClusterEngine(StepEngine):
             self._dedup_ids()
             L.check(L.lib.dicm_bucket_by_owner(self.uniq_id.data_ptr(), cnt[1:].data_ptr(), self.cap_k, G,
                                                self.send_id.data_ptr(), self._col(1), self.perm_id.data_ptr(),
-                                               self.ws_bucket_id.data_ptr(), self.ws_bucket_id.numel(), ss))
+                                               self.perm_inv_id.data_ptr(), self.ws_bucket_id.data_ptr(),
+                                               self.ws_bucket_id.numel(), ss))
 
         # the ID chain beside the image chain; the counts wait for both buckets
         on_side(swap(id_chain))
@@ -538,7 +540,8 @@ class ClusterEngine(StepEngine):
         self._dedup_images()
         L.check(L.lib.dicm_bucket_by_owner(self.uniq_img.data_ptr(), cnt.data_ptr(), self.cap_u, G,
                                            self.send_img.data_ptr(), self._col(0), self.perm_img.data_ptr(),
-                                           self.ws_bucket.data_ptr(), self.ws_bucket.numel(), s))
+                                           self.perm_inv_img.data_ptr(), self.ws_bucket.data_ptr(),
+                                           self.ws_bucket.numel(), s))
         # the backward's summation order, needed only at the local step (joined before it)
         on_side(swap(lambda ss: (self._transpose_ids(), self._transpose_images())))
         if id_bucketed is not None:
@@ -588,9 +591,7 @@ class ClusterEngine(StepEngine):
         # finite check and the head / attention partial reduces
         def id_chain_bwd(ss):
             self._id_row_grads(ss)
-            L.check(L.lib.dicm_permute_rows12(self.d_rows.data_ptr(), self.perm_id.data_ptr(), cnt[1:].data_ptr(),
-                                              self.cap_k, 1, self.push_out_id.data_ptr(), ss))
-            px.scatter(1, 0, self.push_out_id.data_ptr(), 48, "push_id", ss)
+            px.gather_scatter12(1, 0, self.d_rows.data_ptr(), self.perm_inv_id.data_ptr(), "push_id", ss)
             px.barrier_side(st, ss)
             L.check(L.lib.dicm_dedup_devn(px.recv_id.data_ptr(), self.cnt_dev[1:].data_ptr(), px.cap_rk,
                                           self.local_id_space, self.ws_id_owner.data_ptr(), self.ws_id_owner.numel(),
@@ -606,9 +607,8 @@ class ClusterEngine(StepEngine):
         on_side(id_chain_bwd)
         # (5a, 6a) main stream: image gradients to the owners (C4), barrier, the
         # owner's reduction in ascending source order, the image-MLP backward
-        L.check(L.lib.dicm_permute_rows12(self.d_emb_l.data_ptr(), self.perm_img.data_ptr(), cnt.data_ptr(),
-                                          self.cap_u, 1, self.rows_buf.data_ptr(), s))
-        px.scatter(0, 0, self.rows_buf.data_ptr(), 48, "push_img", s)
+        # this rank's image gradients, in owner order, straight into the owners' buffers
+        px.gather_scatter12(0, 0, self.d_emb_l.data_ptr(), self.perm_inv_img.data_ptr(), "push_img", s)
         px.barrier(st, s)
         self._mark("grads to owners")
         L.check(L.lib.dicm_owner_reduce_rows12(px.push_img.data_ptr(), self.inv_o.data_ptr(),

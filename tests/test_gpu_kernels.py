@@ -117,9 +117,11 @@ def test_bucket_by_owner_stable_partition(L):
         send = torch.empty(n, dtype=torch.int32, device=dev)
         counts = torch.empty(world, dtype=torch.int32, device=dev)
         perm = torch.empty(n, dtype=torch.int32, device=dev)
+        perm_inv = torch.empty(n, dtype=torch.int32, device=dev)
         ws = torch.empty(L.lib.dicm_bucket_workspace(n, world), dtype=torch.uint8, device=dev)
         L.check(L.lib.dicm_bucket_by_owner(t.data_ptr(), cnt.data_ptr(), n, world, send.data_ptr(), counts.data_ptr(),
-                                           perm.data_ptr(), ws.data_ptr(), ws.numel(), L.stream_handle()))
+                                           perm.data_ptr(), perm_inv.data_ptr(), ws.data_ptr(), ws.numel(),
+                                           L.stream_handle()))
         torch.cuda.synchronize()
         owner = keys % world
         exp_counts = np.bincount(owner, minlength=world)
@@ -129,6 +131,7 @@ def test_bucket_by_owner_stable_partition(L):
         p = perm.cpu().numpy()
         assert np.array_equal(np.sort(p), np.arange(n))
         assert np.array_equal(p[order], np.arange(n))
+        assert np.array_equal(perm_inv.cpu().numpy()[p], np.arange(n))  # the gather form of perm
 
 
 def test_counter_based_table_init_is_rank_invariant():
