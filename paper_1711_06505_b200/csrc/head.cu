@@ -136,7 +136,6 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
     const float bj = p.b0[j];
 #pragma unroll
     for (int r = 0; r < HB; ++r) acc[r] = bj;
-    #pragma unroll 4
     for (int k = 0; k < W; ++k) {
       const float w = s.w0[j * WS + k];
       float xv[HB];
@@ -159,7 +158,6 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
     const float bj = p.b1[j];
 #pragma unroll
     for (int r = 0; r < QB; ++r) acc[r] = bj;
-    #pragma unroll 4
     for (int k = 0; k < H0; ++k) {
       const float w = s.w1[j * H0 + k];
       float hv[QB];
@@ -242,7 +240,6 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
     {
       float hv[BT];
       load32(s.h0[k], hv);
-      #pragma unroll 4
       for (int j = h * (H1 / 2); j < (h + 1) * (H1 / 2); ++j) {
         float d[BT];
         load32(s.da1[j], d);
@@ -255,7 +252,6 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
     float dh[HB];
 #pragma unroll
     for (int r = 0; r < HB; ++r) dh[r] = 0.f;
-    #pragma unroll 4
     for (int j = 0; j < H1; ++j) {
       const float w = s.w1[j * H0 + k];
       float d[HB];
@@ -301,7 +297,6 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
       float xv[BT];
       load32(s.xs[c], xv);
       const int k0 = per == THREADS ? 0 : h * (H0 / 2), k1 = per == THREADS ? H0 : k0 + H0 / 2;
-      #pragma unroll 4
       for (int k = k0; k < k1; ++k) {
         float d[BT];
         load32(s.da0[k], d);
@@ -319,7 +314,6 @@ __global__ void __launch_bounds__(THREADS) k_head(const float* __restrict__ x, i
       float acc[HB];
 #pragma unroll
       for (int r = 0; r < HB; ++r) acc[r] = 0.f;
-      #pragma unroll 4
       for (int k = 0; k < H0; ++k) {
         const float w = s.w0[k * WS + c];
         float d[HB];
